@@ -1,0 +1,269 @@
+"""TEST INFRASTRUCTURE ONLY -- the CPU checker for the B200 GF(p) RREF path.
+
+Only ``tests/``, ``__graft_entry__.smoke()`` and ``bench.py``'s
+``cpu_baseline`` / ``--impl reference`` legs may import this package.  The
+product (``paper_1806_04211_b200``) never imports it; its compute path is the
+CUDA library and fails loudly when that is missing.
+
+Contents
+--------
+``lib``      ctypes handle on ``oracle/liboracle.so`` -- the plain-C restatement
+             (``gfq_oracle.c``) of the reference's generators, block
+             multiply-accumulate and sequential RREF oracle.
+``ref``      ctypes handle on ``oracle/_ref/libgfrref_ref.so`` -- the reference
+             library itself, compiled from /root/reference by ``oracle/Makefile``
+             (None when that build is absent).
+``restate``  numpy restatement of the reference's jobs, tasks and Chief plan
+             (``restate.py``), used as the task-level checker.
+
+Parity pin: ``tests/test_oracle.py`` checks all three against the golden
+vectors in ``tests/golden/`` (values from the reference's own test suite) and
+against each other.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import subprocess
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+_LIB_PATH = os.path.join(HERE, "liboracle.so")
+_REF_PATH = os.path.join(HERE, "_ref", "libgfrref_ref.so")
+
+_u8p = ctypes.POINTER(ctypes.c_uint8)
+_u32p = ctypes.POINTER(ctypes.c_uint32)
+_sz = ctypes.c_size_t
+
+
+def _build_if_missing():
+    if not os.path.exists(_LIB_PATH):
+        subprocess.run(["make", "-s", "-C", HERE, "oracle"], check=True)
+
+
+def _load():
+    _build_if_missing()
+    lib = ctypes.CDLL(_LIB_PATH)
+    lib.gfo_random_matrix.argtypes = [ctypes.c_uint32, _sz, _sz, ctypes.c_uint64, _u8p, _sz]
+    lib.gfo_random_product_matrix.argtypes = [ctypes.c_uint32, _sz, _sz, _sz, ctypes.c_uint64, _u8p, _sz]
+    lib.gfo_mad.argtypes = [ctypes.c_uint32, _sz, _sz, _sz, _u8p, _sz, _u8p, _sz, _u8p, _sz, _u8p, _sz]
+    lib.gfo_oracle_rref.argtypes = [ctypes.c_uint32, _sz, _sz, _u8p, _sz, _u32p, _u32p, _u8p, _u8p, _u8p]
+    lib.gfo_oracle_rref.restype = ctypes.c_int64
+    lib.gfo_inv.argtypes = [ctypes.c_uint32, ctypes.c_uint32]
+    lib.gfo_inv.restype = ctypes.c_uint32
+    return lib
+
+
+def _load_ref():
+    if not os.path.exists(_REF_PATH):
+        return None
+    r = ctypes.CDLL(_REF_PATH)
+    r.ref_last_error.restype = ctypes.c_char_p
+    r.ref_hardware_concurrency.restype = ctypes.c_int
+    r.ref_random_matrix.argtypes = [ctypes.c_uint32, _sz, _sz, ctypes.c_uint64, _u8p, _sz]
+    r.ref_random_product_matrix.argtypes = [ctypes.c_uint32, _sz, _sz, _sz, ctypes.c_uint64, _u8p, _sz]
+    r.ref_mad.argtypes = [ctypes.c_uint32, _sz, _sz, _sz, _u8p, _sz, _u8p, _sz, _u8p, _sz, _u8p, _sz]
+    r.ref_mad.restype = ctypes.c_int
+    for fn in (r.ref_ech, r.ref_oracle_rref):
+        fn.restype = ctypes.c_int64
+    r.ref_ech.argtypes = [ctypes.c_uint32, _sz, _sz, _u8p, _sz, _sz, _u32p, _u32p, _u8p, _u8p, _u8p]
+    r.ref_oracle_rref.argtypes = [ctypes.c_uint32, _sz, _sz, _u8p, _sz, _u32p, _u32p, _u8p, _u8p, _u8p]
+    r.ref_echelonize.restype = ctypes.c_void_p
+    r.ref_echelonize.argtypes = [ctypes.c_uint32, _sz, _sz, _u8p, _sz, _sz, ctypes.c_int, ctypes.c_int, _sz,
+                                 ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_double)]
+    r.ref_out_free.argtypes = [ctypes.c_void_p]
+    for fn in (r.ref_out_rank, r.ref_out_a, r.ref_out_b):
+        fn.restype = ctypes.c_int64
+        fn.argtypes = [ctypes.c_void_p]
+    r.ref_out_select.restype = ctypes.c_int64
+    r.ref_out_select.argtypes = [ctypes.c_void_p, ctypes.c_int, _sz, _u32p]
+    r.ref_out_block.restype = ctypes.c_int
+    r.ref_out_block.argtypes = [ctypes.c_void_p, ctypes.c_int, _sz, _sz, ctypes.POINTER(ctypes.c_int64),
+                                ctypes.POINTER(ctypes.c_int64), _u8p]
+    r.ref_out_materialize.argtypes = [ctypes.c_void_p, _u8p]
+    r.ref_out_assembled_R.argtypes = [ctypes.c_void_p, _u8p]
+    r.ref_verify.argtypes = [ctypes.c_void_p, ctypes.c_uint32, _sz, _sz, _u8p, _sz]
+    return r
+
+
+lib = _load()
+ref = _load_ref()
+
+
+def u8ptr(a: np.ndarray):
+    if a is None:
+        return None
+    assert a.dtype == np.uint8 and a.flags["C_CONTIGUOUS"]
+    return a.ctypes.data_as(_u8p)
+
+
+def u32ptr(a: np.ndarray):
+    assert a.dtype == np.uint32 and a.flags["C_CONTIGUOUS"]
+    return a.ctypes.data_as(_u32p)
+
+
+def random_matrix(p: int, rows: int, cols: int, seed: int) -> np.ndarray:
+    """C restatement of reference ``random_matrix`` (src/generate.cpp:16-24)."""
+    out = np.zeros((rows, cols), np.uint8)
+    lib.gfo_random_matrix(p, rows, cols, seed, u8ptr(out), max(cols, 1))
+    return out
+
+
+def random_product_matrix(p: int, rows: int, cols: int, inner: int, seed: int) -> np.ndarray:
+    """C restatement of reference ``random_product_matrix`` (src/generate.cpp:26-38)."""
+    out = np.zeros((rows, cols), np.uint8)
+    lib.gfo_random_product_matrix(p, rows, cols, inner, seed, u8ptr(out), max(cols, 1))
+    return out
+
+
+def mad(p: int, a: np.ndarray, b: np.ndarray, c: np.ndarray | None = None) -> np.ndarray:
+    """C restatement of reference ``mul_add_kernel`` (src/matrix.cpp:81-133)."""
+    a = np.ascontiguousarray(a, np.uint8)
+    b = np.ascontiguousarray(b, np.uint8)
+    m, k = a.shape
+    k2, n = b.shape
+    if k != k2:
+        raise ValueError("mul: inner dimensions disagree")
+    if c is not None:
+        c = np.ascontiguousarray(c, np.uint8)
+        if c.shape != (m, n):
+            raise ValueError("mad: addend shape mismatch")
+    out = np.zeros((m, n), np.uint8)
+    if m and n:
+        lib.gfo_mad(p, m, k, n, u8ptr(a) if a.size else u8ptr(np.zeros(1, np.uint8)), max(k, 1),
+                    u8ptr(b) if b.size else u8ptr(np.zeros(1, np.uint8)), max(n, 1),
+                    u8ptr(c) if c is not None else None, n, u8ptr(out), n)
+    return out
+
+
+def oracle_rref(p: int, C: np.ndarray):
+    """C restatement of reference ``oracle_rref`` (src/chief.cpp:427-487).
+
+    Returns dict(rank, rho, gamma, M, K, R) with the reference's conventions.
+    """
+    C = np.ascontiguousarray(C, np.uint8)
+    m, n = C.shape
+    rho = np.zeros(max(m, 1), np.uint32)
+    gamma = np.zeros(max(n, 1), np.uint32)
+    M = np.zeros(max(m * m, 1), np.uint8)
+    K = np.zeros(max(m * m, 1), np.uint8)
+    R = np.zeros(max(m * n, 1), np.uint8)
+    src = C if C.size else np.zeros((1, 1), np.uint8)
+    r = lib.gfo_oracle_rref(p, m, n, u8ptr(src), max(n, 1), u32ptr(rho), u32ptr(gamma),
+                            u8ptr(M), u8ptr(K), u8ptr(R))
+    if r < 0:
+        raise MemoryError("oracle_rref: allocation failed")
+    return dict(rank=int(r), rho=rho[:r].copy(), gamma=gamma[:r].copy(),
+                M=M[: r * r].reshape(r, r).copy(), K=K[: (m - r) * r].reshape(m - r, r).copy(),
+                R=R[: r * (n - r)].reshape(r, n - r).copy())
+
+
+# ---------------------------------------------------------------- reference shim
+class RefOutput:
+    """Handle on a ``gfrref::EchelonOutput`` produced by the reference library."""
+
+    def __init__(self, handle, m, n, wall_s, run_s):
+        self.h = handle
+        self.m, self.n = m, n
+        self.wall_s, self.run_s = wall_s, run_s
+
+    def __del__(self):
+        if getattr(self, "h", None) and ref is not None:
+            ref.ref_out_free(self.h)
+            self.h = None
+
+    @property
+    def rank(self):
+        return int(ref.ref_out_rank(self.h))
+
+    @property
+    def a(self):
+        return int(ref.ref_out_a(self.h))
+
+    @property
+    def b(self):
+        return int(ref.ref_out_b(self.h))
+
+    def select(self, which: int, x: int) -> np.ndarray:
+        cnt = ref.ref_out_select(self.h, which, x, None)
+        buf = np.zeros(max(cnt, 1), np.uint32)
+        ref.ref_out_select(self.h, which, x, u32ptr(buf))
+        return buf[:cnt].copy()
+
+    def upsilon(self, j):
+        return self.select(0, j)
+
+    def varrho(self, i):
+        return self.select(1, i)
+
+    def block(self, kind: int, x: int, y: int) -> np.ndarray:
+        rows, cols = ctypes.c_int64(), ctypes.c_int64()
+        if ref.ref_out_block(self.h, kind, x, y, ctypes.byref(rows), ctypes.byref(cols), None):
+            raise IndexError(ref.ref_last_error().decode())
+        buf = np.zeros((rows.value, cols.value), np.uint8)
+        if buf.size:
+            ref.ref_out_block(self.h, kind, x, y, ctypes.byref(rows), ctypes.byref(cols), u8ptr(buf))
+        return buf
+
+    def materialize_transform(self) -> np.ndarray:
+        t = np.zeros((self.m, self.m), np.uint8)
+        if t.size and ref.ref_out_materialize(self.h, u8ptr(t)):
+            raise RuntimeError(ref.ref_last_error().decode())
+        return t
+
+    def assembled_R(self) -> np.ndarray:
+        r = self.rank
+        out = np.zeros((r, self.n - r), np.uint8)
+        if out.size:
+            ref.ref_out_assembled_R(self.h, u8ptr(out))
+        return out
+
+
+def ref_echelonize(p: int, C: np.ndarray, block: int, threads: int = 1, with_transform: bool = True,
+                   threshold: int = 256) -> RefOutput:
+    """Run the reference's own ``gfrref::echelonize`` (src/chief.cpp:322-386)."""
+    if ref is None:
+        raise RuntimeError("reference library oracle/_ref/libgfrref_ref.so not built")
+    C = np.ascontiguousarray(C, np.uint8)
+    m, n = C.shape
+    wall, run = ctypes.c_double(), ctypes.c_double()
+    src = C if C.size else np.zeros((1, 1), np.uint8)
+    h = ref.ref_echelonize(p, m, n, u8ptr(src), max(n, 1), block, threads, int(with_transform), threshold,
+                           ctypes.byref(wall), ctypes.byref(run))
+    if not h:
+        raise RuntimeError(ref.ref_last_error().decode())
+    return RefOutput(h, m, n, wall.value, run.value)
+
+
+def ref_ech(p: int, H: np.ndarray, threshold: int = 256):
+    """The reference's own single-block ``ech`` (src/jobs.cpp:202-225)."""
+    H = np.ascontiguousarray(H, np.uint8)
+    m, n = H.shape
+    rho = np.zeros(max(m, 1), np.uint32)
+    gamma = np.zeros(max(n, 1), np.uint32)
+    M = np.zeros(max(m * m, 1), np.uint8)
+    K = np.zeros(max(m * m, 1), np.uint8)
+    R = np.zeros(max(m * n, 1), np.uint8)
+    src = H if H.size else np.zeros((1, 1), np.uint8)
+    r = ref.ref_ech(p, m, n, u8ptr(src), max(n, 1), threshold, u32ptr(rho), u32ptr(gamma), u8ptr(M),
+                    u8ptr(K), u8ptr(R))
+    if r < 0:
+        raise RuntimeError(ref.ref_last_error().decode())
+    return dict(rank=int(r), rho=rho[:r].copy(), gamma=gamma[:r].copy(),
+                M=M[: r * r].reshape(r, r).copy(), K=K[: (m - r) * r].reshape(m - r, r).copy(),
+                R=R[: r * (n - r)].reshape(r, n - r).copy())
+
+
+def ref_random_matrix(p: int, rows: int, cols: int, seed: int) -> np.ndarray:
+    out = np.zeros((rows, cols), np.uint8)
+    if out.size:
+        ref.ref_random_matrix(p, rows, cols, seed, u8ptr(out), cols)
+    return out
+
+
+def ref_random_product_matrix(p: int, rows: int, cols: int, inner: int, seed: int) -> np.ndarray:
+    out = np.zeros((rows, cols), np.uint8)
+    if out.size:
+        ref.ref_random_product_matrix(p, rows, cols, inner, seed, u8ptr(out), cols)
+    return out

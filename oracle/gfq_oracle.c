@@ -1,0 +1,178 @@
+/*
+ * gfq_oracle.c -- TEST INFRASTRUCTURE ONLY (see gfq_oracle.h).
+ *
+ * Plain-C restatement of the reference's GF(p) arithmetic, generators,
+ * block multiply-accumulate and sequential RREF oracle.  Each function cites
+ * the reference file:line it restates.  Not linked into the product.
+ */
+#include "gfq_oracle.h"
+
+#include <stdlib.h>
+#include <string.h>
+
+/* reference include/gfrref/generate.hpp:16-21 */
+uint64_t gfo_splitmix_next(uint64_t* state) {
+  uint64_t z = (*state += 0x9e3779b97f4a7c15ULL);
+  z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ULL;
+  z = (z ^ (z >> 27)) * 0x94d049bb133111ebULL;
+  return z ^ (z >> 31);
+}
+
+/* reference src/generate.cpp:5-14 */
+uint64_t gfo_below(uint64_t* state, uint64_t bound) {
+  if (bound <= 1) return 0;
+  const uint64_t limit = UINT64_MAX - UINT64_MAX % bound;
+  uint64_t v;
+  do {
+    v = gfo_splitmix_next(state);
+  } while (v >= limit);
+  return v % bound;
+}
+
+/* reference src/generate.cpp:16-24 */
+void gfo_random_matrix(uint32_t p, size_t rows, size_t cols, uint64_t seed,
+                       uint8_t* out, size_t ld) {
+  uint64_t st = seed;
+  for (size_t r = 0; r < rows; ++r)
+    for (size_t c = 0; c < cols; ++c)
+      out[r * ld + c] = (uint8_t)gfo_below(&st, p);
+}
+
+/* reference src/generate.cpp:26-38 */
+void gfo_random_product_matrix(uint32_t p, size_t rows, size_t cols,
+                               size_t inner, uint64_t seed, uint8_t* out,
+                               size_t ld) {
+  uint64_t st = seed;
+  uint8_t* P = (uint8_t*)malloc(rows * inner + 1);
+  uint8_t* Q = (uint8_t*)malloc(inner * cols + 1);
+  for (size_t r = 0; r < rows; ++r)
+    for (size_t c = 0; c < inner; ++c) P[r * inner + c] = (uint8_t)gfo_below(&st, p);
+  for (size_t r = 0; r < inner; ++r)
+    for (size_t c = 0; c < cols; ++c) Q[r * cols + c] = (uint8_t)gfo_below(&st, p);
+  gfo_mad(p, rows, inner, cols, P, inner, Q, cols, NULL, 0, out, ld);
+  free(P);
+  free(Q);
+}
+
+/* reference src/matrix.cpp:81-133 (prime path :91-114): per output row a
+ * 64-bit accumulator over `inner`, zero multipliers skipped, one % p at the
+ * end. */
+void gfo_mad(uint32_t p, size_t m, size_t k, size_t n, const uint8_t* A,
+             size_t lda, const uint8_t* B, size_t ldb, const uint8_t* Cin,
+             size_t ldc, uint8_t* D, size_t ldd) {
+  if (m == 0 || n == 0) return;
+  uint64_t* acc = (uint64_t*)malloc(n * sizeof(uint64_t));
+  for (size_t i = 0; i < m; ++i) {
+    if (Cin)
+      for (size_t j = 0; j < n; ++j) acc[j] = Cin[i * ldc + j];
+    else
+      memset(acc, 0, n * sizeof(uint64_t));
+    for (size_t t = 0; t < k; ++t) {
+      const uint64_t v = A[i * lda + t];
+      if (v == 0) continue;
+      const uint8_t* brow = B + t * ldb;
+      for (size_t j = 0; j < n; ++j) acc[j] += v * brow[j];
+    }
+    for (size_t j = 0; j < n; ++j) D[i * ldd + j] = (uint8_t)(acc[j] % p);
+  }
+  free(acc);
+}
+
+/* reference src/field.cpp:220-237 (Fermat inverse a^(p-2)) */
+uint32_t gfo_inv(uint32_t p, uint32_t a) {
+  uint64_t r = 1, b = a % p;
+  uint32_t e = p - 2;
+  while (e) {
+    if (e & 1) r = r * b % p;
+    b = b * b % p;
+    e >>= 1;
+  }
+  return (uint32_t)r;
+}
+
+/* reference src/chief.cpp:427-487 (`oracle_rref`). */
+int64_t gfo_oracle_rref(uint32_t p, size_t m, size_t n, const uint8_t* C,
+                        size_t ldc, uint32_t* rho, uint32_t* gamma,
+                        uint8_t* M, uint8_t* K, uint8_t* R) {
+  uint8_t* w = (uint8_t*)malloc(m * n + 1);
+  uint8_t* t = (uint8_t*)calloc(m * m + 1, 1);
+  uint8_t* is_piv = (uint8_t*)calloc(m + 1, 1);
+  uint32_t* prow = (uint32_t*)malloc((m + 1) * sizeof(uint32_t));
+  uint32_t* pcol = (uint32_t*)malloc((n + 1) * sizeof(uint32_t));
+  /* mul[a*p+b] = a*b mod p */
+  uint8_t* mul = (uint8_t*)malloc((size_t)p * p);
+  if (!w || !t || !is_piv || !prow || !pcol || !mul) return -1;
+  for (uint32_t a = 0; a < p; ++a)
+    for (uint32_t b = 0; b < p; ++b) mul[a * p + b] = (uint8_t)((a * b) % p);
+  for (size_t i = 0; i < m; ++i) memcpy(w + i * n, C + i * ldc, n);
+  for (size_t i = 0; i < m; ++i) t[i * m + i] = 1;
+
+  size_t r = 0;
+  for (size_t col = 0; col < n; ++col) {
+    size_t sel = m;
+    for (size_t row = 0; row < m; ++row)
+      if (!is_piv[row] && w[row * n + col] != 0) {
+        sel = row;
+        break;
+      }
+    if (sel == m) continue;
+    /* scale = -(inv(pivot)) so the pivot entry becomes -1 */
+    const uint32_t iv = gfo_inv(p, w[sel * n + col]);
+    const uint32_t scale = iv == 0 ? 0 : p - iv;
+    const uint8_t* ms = mul + (size_t)scale * p;
+    uint8_t* ws = w + sel * n;
+    uint8_t* ts = t + sel * m;
+    for (size_t c = 0; c < n; ++c) ws[c] = ms[ws[c]];
+    for (size_t c = 0; c < m; ++c) ts[c] = ms[ts[c]];
+    for (size_t row = 0; row < m; ++row) {
+      if (row == sel) continue;
+      const uint32_t v = w[row * n + col];
+      if (v == 0) continue;
+      const uint8_t* mv = mul + (size_t)v * p;
+      uint8_t* wr = w + row * n;
+      uint8_t* tr = t + row * m;
+      for (size_t c = 0; c < n; ++c) {
+        uint32_t s = (uint32_t)wr[c] + mv[ws[c]];
+        wr[c] = (uint8_t)(s >= p ? s - p : s);
+      }
+      for (size_t c = 0; c < m; ++c) {
+        uint32_t s = (uint32_t)tr[c] + mv[ts[c]];
+        tr[c] = (uint8_t)(s >= p ? s - p : s);
+      }
+    }
+    is_piv[sel] = 1;
+    prow[r] = (uint32_t)sel;
+    pcol[r] = (uint32_t)col;
+    ++r;
+  }
+
+  /* rho sorted ascending */
+  size_t nr = 0;
+  for (size_t row = 0; row < m; ++row)
+    if (is_piv[row]) rho[nr++] = (uint32_t)row;
+  for (size_t q = 0; q < r; ++q) gamma[q] = pcol[q];
+  /* non-pivot columns ascending */
+  uint8_t* is_pc = (uint8_t*)calloc(n + 1, 1);
+  for (size_t q = 0; q < r; ++q) is_pc[pcol[q]] = 1;
+  for (size_t q = 0; q < r; ++q) {
+    const size_t row = prow[q];
+    for (size_t s = 0; s < r; ++s) M[q * r + s] = t[row * m + rho[s]];
+    size_t c2 = 0;
+    for (size_t c = 0; c < n; ++c)
+      if (!is_pc[c]) R[q * (n - r) + c2++] = w[row * n + c];
+  }
+  size_t u = 0;
+  for (size_t row = 0; row < m; ++row) {
+    if (is_piv[row]) continue;
+    for (size_t s = 0; s < r; ++s) K[u * r + s] = t[row * m + rho[s]];
+    ++u;
+  }
+  free(is_pc);
+  free(w);
+  free(t);
+  free(is_piv);
+  free(prow);
+  free(pcol);
+  free(mul);
+  return (int64_t)r;
+}
