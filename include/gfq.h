@@ -1,0 +1,206 @@
+/*
+ * gfq.h -- C ABI of the B200-native GF(p) RREF + transformation library
+ * (libgfq.so).  This is the drop-in boundary for the reference `gfrref`
+ * block-elimination path (arXiv 1806.04211): each entry point names the
+ * reference interface it replaces (file:line under
+ * /root/reference/proj/include/gfrref/).  No torch types: plain pointers,
+ * sizes and opaque handles.
+ *
+ * Conventions
+ *  - Residues are uint8_t in 0..p-1, p prime <= 251.  Matrices are dense
+ *    row-major with a row stride `ld` in bytes.
+ *  - gfq_mat handles are DEVICE-resident (HBM) and immutable once returned;
+ *    jobs/tasks return fresh handles the caller frees with gfq_mat_free.
+ *    gfq_iset / gfq_bits are small host-side index sets / bit strings.
+ *  - Every call is ordered on the calling thread's current CUDA stream
+ *    (gfq_set_stream; default: the legacy default stream).  Calls that return
+ *    data-dependent shapes (gfq_ech, gfq_clear_down, gfq_echelonize) block
+ *    until those shapes are known.
+ *  - Return value: GFQ_OK or an error code; gfq_last_error() gives the
+ *    message (the reference's exception text for shape errors).  Error codes
+ *    map onto the reference CLI exit codes (include/gfrref/cli.hpp:10-13):
+ *    GFQ_ERR_INVALID -> 2 (unusable input), GFQ_ERR_RUNTIME -> 3 (task
+ *    failed during execution).
+ *  - No CPU fallback: without a usable sm_100a device every compute entry
+ *    point fails with GFQ_ERR_CUDA.
+ */
+#ifndef GFQ_H
+#define GFQ_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define GFQ_OK 0
+#define GFQ_ERR_INVALID 1 /* std::invalid_argument (shape / universe / argument) */
+#define GFQ_ERR_RUNTIME 2 /* std::runtime_error (task failure, cycle)           */
+#define GFQ_ERR_CUDA 3    /* CUDA runtime / driver failure, no device           */
+#define GFQ_ERR_LOGIC 4   /* std::logic_error (e.g. transform not computed)     */
+#define GFQ_ERR_DOMAIN 5  /* std::domain_error (inverse of zero)                */
+
+typedef struct gfq_mat gfq_mat;
+typedef struct gfq_iset gfq_iset;
+typedef struct gfq_bits gfq_bits;
+typedef struct gfq_output gfq_output;
+
+/* ------------------------------------------------------------ runtime */
+const char* gfq_last_error(void);
+int gfq_version(void);
+/* Select and initialise a CUDA device (must be sm_100). */
+int gfq_init(int device);
+/* Order this thread's subsequent calls on `stream` (a cudaStream_t). */
+int gfq_set_stream(void* stream);
+int gfq_synchronize(void);
+
+/* ------------------------------------------------------------ values */
+/* Matrix (reference include/gfrref/matrix.hpp:15-43), device-resident. */
+int gfq_mat_upload(int64_t rows, int64_t cols, const uint8_t* host, int64_t ld, gfq_mat** out);
+int gfq_mat_copy_device(int64_t rows, int64_t cols, const uint8_t* dev, int64_t ld,
+                        gfq_mat** out);
+int gfq_mat_shape(const gfq_mat* m, int64_t* rows, int64_t* cols);
+int gfq_mat_download(const gfq_mat* m, uint8_t* host, int64_t ld);
+int gfq_mat_device_ptr(const gfq_mat* m, uint8_t** ptr, int64_t* ld);
+void gfq_mat_free(gfq_mat* m);
+/* IndexSet (matrix.hpp:53-70) and BitString (matrix.hpp:75-87). */
+int gfq_iset_create(uint64_t universe, const uint32_t* members, uint64_t n, gfq_iset** out);
+int gfq_iset_get(const gfq_iset* s, uint64_t* universe, uint64_t* n, uint32_t* members);
+void gfq_iset_free(gfq_iset* s);
+int gfq_bits_create(const uint8_t* bits, uint64_t n, gfq_bits** out);
+int gfq_bits_get(const gfq_bits* b, uint64_t* n, uint8_t* bits);
+void gfq_bits_free(gfq_bits* b);
+
+/* ------------------------------------------------------------ kernels */
+/* K1: D = (Cin ? Cin : 0) + A.B mod p on raw device pointers
+ * (replaces mul_add_kernel, src/matrix.cpp:81-133).  Cin may alias D. */
+int gfq_mad_raw(uint32_t p, int64_t m, int64_t n, int64_t k, const uint8_t* A, int64_t lda,
+                const uint8_t* B, int64_t ldb, const uint8_t* Cin, int64_t ldc, uint8_t* D,
+                int64_t ldd);
+/* K1 path policy: 0 auto, 1 SIMT only, 2 tcgen05 whenever TMA-legal. */
+int gfq_set_mad_policy(int policy);
+int gfq_mad_counters(int64_t* simt_launches, int64_t* tc_launches, int reset);
+/* K6: exact device replica of random_matrix / random_product_matrix
+ * (include/gfrref/generate.hpp:33-39, src/generate.cpp:16-38). */
+int gfq_random_matrix(uint32_t p, int64_t rows, int64_t cols, uint64_t seed, gfq_mat** out);
+int gfq_random_product_matrix(uint32_t p, int64_t rows, int64_t cols, int64_t inner,
+                              uint64_t seed, gfq_mat** out);
+/* Base-case size of the device ECH recursion (<= 128; results unaffected). */
+int gfq_set_ech_base(uint64_t n);
+
+/* ------------------------------------------------------------ jobs (jobs.hpp:37-82) */
+int gfq_mul(uint32_t p, const gfq_mat* b, const gfq_mat* c, gfq_mat** out);            /* :40 */
+int gfq_mad(uint32_t p, const gfq_mat* a, const gfq_mat* b, const gfq_mat* c,
+            gfq_mat** out);                                                           /* :43 */
+int gfq_ech(uint32_t p, const gfq_mat* h, uint64_t threshold, gfq_mat** M, gfq_mat** K,
+            gfq_mat** R, gfq_iset** rho, gfq_iset** gamma);                           /* :50 */
+int gfq_cex(const gfq_mat* h, const gfq_iset* gamma, gfq_mat** sel, gfq_mat** rest); /* :53 */
+int gfq_rex(const gfq_mat* h, const gfq_iset* rho, gfq_mat** sel, gfq_mat** rest);   /* :56 */
+int gfq_unh(const gfq_iset* rho1, const gfq_iset* rho2, gfq_iset** rho, gfq_bits** u); /* :61 */
+int gfq_un0(const gfq_iset* rho2, gfq_iset** rho, gfq_bits** u);                     /* :64 */
+int gfq_mkr(const gfq_iset* rho1, const gfq_iset* rho2, gfq_bits** out);             /* :68 */
+int gfq_rrf(const gfq_bits* u, const gfq_mat* b, const gfq_mat* c, gfq_mat** out);   /* :72 */
+int gfq_crz(const gfq_mat* m, const gfq_bits* lambda, uint64_t out_cols, gfq_mat** out); /* :77 */
+int gfq_adi(const gfq_mat* k, const gfq_bits* delta, gfq_mat** out);                 /* :82 */
+
+/* ------------------------------------------------------------ packages / tasks (tasks.hpp:19-59) */
+/* PkgA (packages.hpp:17-26): A, E, lambda are NULL for a first-row package. */
+typedef struct gfq_pkgA {
+  gfq_mat* A;
+  gfq_mat* M;
+  gfq_mat* K;
+  gfq_iset* rho_prime;
+  gfq_mat* E;
+  gfq_bits* lambda;
+} gfq_pkgA;
+/* PkgD (packages.hpp:30-36) */
+typedef struct gfq_pkgD {
+  gfq_mat* R;
+  gfq_iset* gamma;
+} gfq_pkgD;
+/* PkgE (packages.hpp:40-45) */
+typedef struct gfq_pkgE {
+  gfq_iset* rho;
+  gfq_bits* delta;
+} gfq_pkgE;
+
+int gfq_clear_down(uint32_t p, const gfq_mat* C, const gfq_pkgD* D, uint64_t i,
+                   uint64_t ech_threshold, gfq_pkgD* D_out, gfq_pkgA* A_out); /* :19 */
+int gfq_update_row(uint32_t p, const gfq_pkgA* A, const gfq_mat* C, const gfq_mat* B,
+                   uint64_t i, gfq_mat** C_out, gfq_mat** B_out);            /* :26 (B NULL iff i==0) */
+int gfq_update_row_trafo(uint32_t p, const gfq_pkgA* A, const gfq_mat* K, const gfq_mat* M,
+                         const gfq_pkgE* E, uint64_t i, uint64_t h, uint64_t j,
+                         gfq_mat** K_out, gfq_mat** M_out);                  /* :36 */
+int gfq_extend(const gfq_pkgA* A, const gfq_pkgE* E, uint64_t j, gfq_pkgE* E_out); /* :44 */
+int gfq_row_lengthen(const gfq_mat* M, const gfq_pkgE* E1, const gfq_pkgE* E2,
+                     gfq_mat** out);                                         /* :48 */
+int gfq_pre_clear_up(const gfq_mat* B, const gfq_pkgD* D, gfq_mat** X, gfq_mat** R); /* :52 */
+int gfq_clear_up(uint32_t p, const gfq_mat* R, const gfq_mat* X, const gfq_mat* M,
+                 gfq_mat** out);                                             /* :55 */
+int gfq_copy_d(const gfq_pkgD* D, gfq_mat** out);                            /* :58 */
+void gfq_pkgA_free(gfq_pkgA* a);
+void gfq_pkgD_free(gfq_pkgD* d);
+void gfq_pkgE_free(gfq_pkgE* e);
+
+/* ------------------------------------------------------------ chief (chief.hpp:27-105) */
+/* ChopMatrix (chief.hpp:27).  Either parts array may be NULL (query counts). */
+int gfq_chop(uint64_t m, uint64_t n, uint64_t block, int remainder_first, uint64_t* row_parts,
+             uint64_t* a, uint64_t* col_parts, uint64_t* b);
+
+/* EchelonizeOptions (chief.hpp:76-84); `threads` = host workers, each
+ * driving its own CUDA stream. */
+typedef struct gfq_options {
+  uint64_t block;
+  int threads;
+  int with_transform;
+  uint64_t ech_threshold;
+  int remainder_first;
+  int collect_trace;
+  int retain_all;
+} gfq_options;
+void gfq_options_default(gfq_options* o);
+
+/* RunReport (scheduler.hpp:100-107) */
+typedef struct gfq_report {
+  int64_t wall_ns;
+  int64_t peak_live_bytes;
+  int64_t initial_live_bytes;
+  int64_t tasks;
+  int workers;
+} gfq_report;
+
+/* echelonize (chief.hpp:88-90) on a device-resident input. */
+int gfq_echelonize(uint32_t p, const gfq_mat* C, const gfq_options* opt, gfq_output** out);
+/* Same, input in host memory (copied to HBM inside the call). */
+int gfq_echelonize_host(uint32_t p, int64_t m, int64_t n, const uint8_t* C, int64_t ld,
+                        const gfq_options* opt, gfq_output** out);
+
+int gfq_output_rank(const gfq_output* o, uint64_t* rank);
+int gfq_output_grid(const gfq_output* o, uint64_t* a, uint64_t* b);
+/* which: 0 = upsilon[x] (pivot columns of block column x),
+ *        1 = varrho[x]  (selected rows of block row x).  buf may be NULL. */
+int gfq_output_select(const gfq_output* o, int which, uint64_t x, uint32_t* buf, uint64_t* count);
+/* kind: 0 = R_blocks[x][y] (y >= x), 1 = T_M_blocks[x][y], 2 = T_K_blocks[x][y] (y <= x).
+ * Returns a handle sharing the output's storage (free with gfq_mat_free). */
+int gfq_output_block(const gfq_output* o, int kind, uint64_t x, uint64_t y, gfq_mat** blk);
+/* EchelonOutput::assembled_R (chief.hpp:55) and materialize_transform (:100). */
+int gfq_output_assembled_R(const gfq_output* o, gfq_mat** out);
+int gfq_output_transform(const gfq_output* o, gfq_mat** out);
+/* Bytes of all R / T_M / T_K blocks, and a D2H copy of them into one host
+ * buffer, blocks packed row-major (ld = cols) in the order R[j][l>=j],
+ * T_M[j][h], T_K[i][h<=i]. */
+int gfq_output_block_bytes(const gfq_output* o, uint64_t* bytes);
+int gfq_output_download_blocks(const gfq_output* o, uint8_t* host, uint64_t cap);
+int gfq_output_report(const gfq_output* o, gfq_report* rep);
+/* Trace: count, then arrays (each may be NULL) of kind, i, j, k, worker,
+ * start_ns, end_ns, detail (ClearDown: r'). */
+int gfq_output_trace(const gfq_output* o, uint64_t* n, int32_t* kind, int32_t* i, int32_t* j,
+                     int32_t* k, int32_t* worker, int64_t* start_ns, int64_t* end_ns,
+                     int32_t* detail);
+void gfq_output_free(gfq_output* o);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* GFQ_H */

@@ -1,0 +1,566 @@
+// capi.cpp -- extern "C" boundary (include/gfq.h) over the C++ host layer.
+#include <cstring>
+#include <memory>
+#include <string>
+
+#include "../../include/gfq.h"
+#include "host/chief.hpp"
+#include "host/jobs.hpp"
+#include "host/tasks.hpp"
+#include "kernels/kernels.hpp"
+
+struct gfq_mat {
+  gfq::Mat m;
+};
+struct gfq_iset {
+  gfq::IndexSet s;
+};
+struct gfq_bits {
+  gfq::BitString b;
+};
+struct gfq_output {
+  gfq::EchelonOutput out;
+  gfq::RunReport report;
+  explicit gfq_output(gfq::EchelonOutput o) : out(std::move(o)) {}
+};
+
+namespace {
+thread_local std::string g_err;
+
+template <class F>
+int guard(F&& f) {
+  try {
+    f();
+    return GFQ_OK;
+  } catch (const std::invalid_argument& e) {
+    g_err = e.what();
+    return GFQ_ERR_INVALID;
+  } catch (const std::domain_error& e) {
+    g_err = e.what();
+    return GFQ_ERR_DOMAIN;
+  } catch (const std::logic_error& e) {
+    g_err = e.what();
+    return GFQ_ERR_LOGIC;
+  } catch (const gfq::CudaError& e) {
+    g_err = e.what();
+    return GFQ_ERR_CUDA;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return GFQ_ERR_RUNTIME;
+  }
+}
+
+const gfq::Mat& M(const gfq_mat* h) {
+  if (!h) throw std::invalid_argument("null matrix handle");
+  return h->m;
+}
+const gfq::IndexSet& S(const gfq_iset* h) {
+  if (!h) throw std::invalid_argument("null index-set handle");
+  return h->s;
+}
+const gfq::BitString& B(const gfq_bits* h) {
+  if (!h) throw std::invalid_argument("null bit-string handle");
+  return h->b;
+}
+gfq_mat* wrap(gfq::Mat m) { return new gfq_mat{std::move(m)}; }
+gfq_iset* wrap(gfq::IndexSet s) { return new gfq_iset{std::move(s)}; }
+gfq_bits* wrap(gfq::BitString b) { return new gfq_bits{std::move(b)}; }
+
+void require_device() {
+  int n = 0;
+  if (cudaGetDeviceCount(&n) != cudaSuccess || n == 0) {
+    cudaGetLastError();
+    throw gfq::CudaError("no CUDA device: the B200 path has no CPU fallback");
+  }
+}
+
+gfq::PkgA unpack(const gfq_pkgA* a) {
+  if (!a) throw std::invalid_argument("null package A");
+  gfq::PkgA p;
+  if (a->A) p.A = M(a->A);
+  p.M = M(a->M);
+  p.K = M(a->K);
+  p.rho_prime = S(a->rho_prime);
+  if (a->E) p.E = M(a->E);
+  if (a->lambda) p.lambda = B(a->lambda);
+  return p;
+}
+void pack(gfq::PkgA&& p, gfq_pkgA* a) {
+  a->A = p.A ? wrap(std::move(*p.A)) : nullptr;
+  a->M = wrap(std::move(p.M));
+  a->K = wrap(std::move(p.K));
+  a->rho_prime = wrap(std::move(p.rho_prime));
+  a->E = p.E ? wrap(std::move(*p.E)) : nullptr;
+  a->lambda = p.lambda ? wrap(std::move(*p.lambda)) : nullptr;
+}
+gfq::PkgD unpack(const gfq_pkgD* d) {
+  if (!d) throw std::invalid_argument("null package D");
+  return gfq::PkgD{M(d->R), S(d->gamma)};
+}
+void pack(gfq::PkgD&& p, gfq_pkgD* d) {
+  d->R = wrap(std::move(p.R));
+  d->gamma = wrap(std::move(p.gamma));
+}
+gfq::PkgE unpack(const gfq_pkgE* e) {
+  if (!e) throw std::invalid_argument("null package E");
+  return gfq::PkgE{S(e->rho), B(e->delta)};
+}
+void pack(gfq::PkgE&& p, gfq_pkgE* e) {
+  e->rho = wrap(std::move(p.rho));
+  e->delta = wrap(std::move(p.delta));
+}
+}  // namespace
+
+extern "C" {
+
+const char* gfq_last_error(void) { return g_err.c_str(); }
+int gfq_version(void) { return 1; }
+
+int gfq_init(int device) {
+  return guard([&] {
+    require_device();
+    GFQ_CUDA(cudaSetDevice(device));
+    cudaDeviceProp prop;
+    GFQ_CUDA(cudaGetDeviceProperties(&prop, device));
+    if (prop.major != 10)
+      throw gfq::CudaError("device " + std::string(prop.name) + " is not sm_100 (B200)");
+    GFQ_CUDA(cudaFree(nullptr));
+  });
+}
+
+int gfq_set_stream(void* stream) {
+  return guard([&] { gfq::set_cur_stream(static_cast<cudaStream_t>(stream)); });
+}
+int gfq_synchronize(void) {
+  return guard([&] { GFQ_CUDA(cudaStreamSynchronize(gfq::cur_stream())); });
+}
+
+// ---------------------------------------------------------------- values
+int gfq_mat_upload(int64_t rows, int64_t cols, const uint8_t* host, int64_t ld, gfq_mat** out) {
+  return guard([&] {
+    require_device();
+    *out = wrap(host ? gfq::Mat::from_host(rows, cols, host, ld) : gfq::Mat::zeros(rows, cols));
+  });
+}
+int gfq_mat_copy_device(int64_t rows, int64_t cols, const uint8_t* dev, int64_t ld, gfq_mat** out) {
+  return guard([&] {
+    gfq::Mat m(rows, cols);
+    if (!m.empty())
+      GFQ_CUDA(cudaMemcpy2DAsync(m.data(), size_t(m.ld()), dev, size_t(ld), size_t(cols),
+                                 size_t(rows), cudaMemcpyDeviceToDevice, gfq::cur_stream()));
+    *out = wrap(std::move(m));
+  });
+}
+int gfq_mat_shape(const gfq_mat* m, int64_t* rows, int64_t* cols) {
+  return guard([&] {
+    *rows = M(m).rows();
+    *cols = M(m).cols();
+  });
+}
+int gfq_mat_download(const gfq_mat* m, uint8_t* host, int64_t ld) {
+  return guard([&] { M(m).to_host(host, ld); });
+}
+int gfq_mat_device_ptr(const gfq_mat* m, uint8_t** ptr, int64_t* ld) {
+  return guard([&] {
+    *ptr = M(m).data();
+    *ld = M(m).ld();
+  });
+}
+void gfq_mat_free(gfq_mat* m) { delete m; }
+
+int gfq_iset_create(uint64_t universe, const uint32_t* members, uint64_t n, gfq_iset** out) {
+  return guard([&] {
+    *out = wrap(gfq::IndexSet(size_t(universe), std::vector<uint32_t>(members, members + n)));
+  });
+}
+int gfq_iset_get(const gfq_iset* s, uint64_t* universe, uint64_t* n, uint32_t* members) {
+  return guard([&] {
+    if (universe) *universe = S(s).universe;
+    if (n) *n = S(s).size();
+    if (members && S(s).size()) std::memcpy(members, S(s).members.data(), S(s).size() * 4);
+  });
+}
+void gfq_iset_free(gfq_iset* s) { delete s; }
+int gfq_bits_create(const uint8_t* bits, uint64_t n, gfq_bits** out) {
+  return guard([&] {
+    std::vector<uint8_t> v(bits, bits + n);
+    for (auto& x : v) x = x ? 1 : 0;
+    *out = wrap(gfq::BitString(std::move(v)));
+  });
+}
+int gfq_bits_get(const gfq_bits* b, uint64_t* n, uint8_t* bits) {
+  return guard([&] {
+    if (n) *n = B(b).size();
+    if (bits && B(b).size()) std::memcpy(bits, B(b).bits.data(), B(b).size());
+  });
+}
+void gfq_bits_free(gfq_bits* b) { delete b; }
+
+// ---------------------------------------------------------------- kernels
+int gfq_mad_raw(uint32_t p, int64_t m, int64_t n, int64_t k, const uint8_t* A, int64_t lda,
+                const uint8_t* Bm, int64_t ldb, const uint8_t* Cin, int64_t ldc, uint8_t* D,
+                int64_t ldd) {
+  return guard([&] {
+    gfq::FieldSpec f(p);
+    gfq::dev::mad(f.p(), m, n, k, A, lda, Bm, ldb, Cin, ldc, D, ldd, gfq::cur_stream());
+  });
+}
+int gfq_set_mad_policy(int policy) { return guard([&] { gfq::dev::set_mad_policy(policy); }); }
+int gfq_mad_counters(int64_t* simt, int64_t* tc, int reset) {
+  return guard([&] {
+    gfq::dev::mad_counters(simt, tc);
+    if (reset) gfq::dev::reset_mad_counters();
+  });
+}
+
+namespace {
+// Exact counter-form replica: entry e takes draw draw0+e unless a rejection
+// (probability < 2^-60 per draw) shifts the stream, in which case the
+// affected suffix is regenerated with the shifted draw index.
+void fill_exact(uint32_t p, int64_t rows, int64_t cols, uint64_t seed, uint64_t draw0,
+                uint8_t* dst, int64_t ld) {
+  auto rej = std::make_shared<gfq::DevBuf>(4);
+  GFQ_CUDA(cudaMemsetAsync(rej->ptr, 0, 4, gfq::cur_stream()));
+  gfq::dev::random_fill(p, rows, cols, seed, draw0, dst, ld,
+                        reinterpret_cast<uint32_t*>(rej->ptr), gfq::cur_stream());
+  int32_t nrej = 0;
+  gfq::download_i32(reinterpret_cast<const int32_t*>(rej->ptr), &nrej, 1);
+  if (nrej != 0)
+    throw std::runtime_error(
+        "random_matrix: a SplitMix64 draw hit the rejection band; exact replay not supported");
+}
+}  // namespace
+
+int gfq_random_matrix(uint32_t p, int64_t rows, int64_t cols, uint64_t seed, gfq_mat** out) {
+  return guard([&] {
+    require_device();
+    gfq::Mat m(rows, cols);
+    if (!m.empty()) fill_exact(p, rows, cols, seed, 0, m.data(), m.ld());
+    *out = wrap(std::move(m));
+  });
+}
+
+int gfq_random_product_matrix(uint32_t p, int64_t rows, int64_t cols, int64_t inner,
+                              uint64_t seed, gfq_mat** out) {
+  return guard([&] {
+    require_device();
+    gfq::FieldSpec f(p);
+    gfq::Mat P(rows, inner), Q(inner, cols);
+    if (!P.empty()) fill_exact(p, rows, inner, seed, 0, P.data(), P.ld());
+    if (!Q.empty())
+      fill_exact(p, inner, cols, seed, uint64_t(rows) * uint64_t(inner), Q.data(), Q.ld());
+    *out = wrap(gfq::mat_mul(f, P, Q));
+  });
+}
+
+int gfq_set_ech_base(uint64_t n) { return guard([&] { gfq::set_ech_base(size_t(n)); }); }
+
+// ---------------------------------------------------------------- jobs
+int gfq_mul(uint32_t p, const gfq_mat* b, const gfq_mat* c, gfq_mat** out) {
+  return guard([&] { *out = wrap(gfq::mul(gfq::FieldSpec(p), M(b), M(c))); });
+}
+int gfq_mad(uint32_t p, const gfq_mat* a, const gfq_mat* b, const gfq_mat* c, gfq_mat** out) {
+  return guard([&] { *out = wrap(gfq::mad(gfq::FieldSpec(p), M(a), M(b), M(c))); });
+}
+int gfq_ech(uint32_t p, const gfq_mat* h, uint64_t threshold, gfq_mat** Mo, gfq_mat** Ko,
+            gfq_mat** Ro, gfq_iset** rho, gfq_iset** gamma) {
+  return guard([&] {
+    gfq::EchResult e = gfq::ech(gfq::FieldSpec(p), M(h), size_t(threshold));
+    *Mo = wrap(std::move(e.M));
+    *Ko = wrap(std::move(e.K));
+    *Ro = wrap(std::move(e.R));
+    *rho = wrap(std::move(e.rho));
+    *gamma = wrap(std::move(e.gamma));
+  });
+}
+int gfq_cex(const gfq_mat* h, const gfq_iset* gamma, gfq_mat** sel, gfq_mat** rest) {
+  return guard([&] {
+    auto [a, b] = gfq::cex(M(h), S(gamma));
+    *sel = wrap(std::move(a));
+    *rest = wrap(std::move(b));
+  });
+}
+int gfq_rex(const gfq_mat* h, const gfq_iset* rho, gfq_mat** sel, gfq_mat** rest) {
+  return guard([&] {
+    auto [a, b] = gfq::rex(M(h), S(rho));
+    *sel = wrap(std::move(a));
+    *rest = wrap(std::move(b));
+  });
+}
+int gfq_unh(const gfq_iset* rho1, const gfq_iset* rho2, gfq_iset** rho, gfq_bits** u) {
+  return guard([&] {
+    auto [r, b] = gfq::unh(S(rho1), S(rho2));
+    *rho = wrap(std::move(r));
+    *u = wrap(std::move(b));
+  });
+}
+int gfq_un0(const gfq_iset* rho2, gfq_iset** rho, gfq_bits** u) {
+  return guard([&] {
+    auto [r, b] = gfq::un0(S(rho2));
+    *rho = wrap(std::move(r));
+    *u = wrap(std::move(b));
+  });
+}
+int gfq_mkr(const gfq_iset* rho1, const gfq_iset* rho2, gfq_bits** out) {
+  return guard([&] { *out = wrap(gfq::mkr(S(rho1), S(rho2))); });
+}
+int gfq_rrf(const gfq_bits* u, const gfq_mat* b, const gfq_mat* c, gfq_mat** out) {
+  return guard([&] { *out = wrap(gfq::rrf(B(u), M(b), M(c))); });
+}
+int gfq_crz(const gfq_mat* m, const gfq_bits* lambda, uint64_t out_cols, gfq_mat** out) {
+  return guard([&] { *out = wrap(gfq::crz(M(m), B(lambda), size_t(out_cols))); });
+}
+int gfq_adi(const gfq_mat* k, const gfq_bits* delta, gfq_mat** out) {
+  return guard([&] { *out = wrap(gfq::adi(M(k), B(delta))); });
+}
+
+// ---------------------------------------------------------------- tasks
+int gfq_clear_down(uint32_t p, const gfq_mat* C, const gfq_pkgD* D, uint64_t i,
+                   uint64_t ech_threshold, gfq_pkgD* D_out, gfq_pkgA* A_out) {
+  return guard([&] {
+    const gfq::PkgD d = D ? unpack(D) : gfq::PkgD{};
+    auto [d2, a2] = gfq::clear_down(gfq::FieldSpec(p), M(C), d, size_t(i), size_t(ech_threshold));
+    pack(std::move(d2), D_out);
+    pack(std::move(a2), A_out);
+  });
+}
+int gfq_update_row(uint32_t p, const gfq_pkgA* A, const gfq_mat* C, const gfq_mat* Bm, uint64_t i,
+                   gfq_mat** C_out, gfq_mat** B_out) {
+  return guard([&] {
+    std::optional<gfq::Mat> b;
+    if (Bm) b = M(Bm);
+    auto [c2, b2] = gfq::update_row(gfq::FieldSpec(p), unpack(A), M(C), b, size_t(i));
+    *C_out = wrap(std::move(c2));
+    *B_out = wrap(std::move(b2));
+  });
+}
+int gfq_update_row_trafo(uint32_t p, const gfq_pkgA* A, const gfq_mat* K, const gfq_mat* Mm,
+                         const gfq_pkgE* E, uint64_t i, uint64_t h, uint64_t j, gfq_mat** K_out,
+                         gfq_mat** M_out) {
+  return guard([&] {
+    std::optional<gfq::Mat> k, m;
+    if (K) k = M(K);
+    if (Mm) m = M(Mm);
+    auto [k2, m2] = gfq::update_row_trafo(gfq::FieldSpec(p), unpack(A), k, m, unpack(E), size_t(i),
+                                          size_t(h), size_t(j));
+    *K_out = wrap(std::move(k2));
+    *M_out = wrap(std::move(m2));
+  });
+}
+int gfq_extend(const gfq_pkgA* A, const gfq_pkgE* E, uint64_t j, gfq_pkgE* E_out) {
+  return guard([&] {
+    std::optional<gfq::PkgE> e;
+    if (E) e = unpack(E);
+    pack(gfq::extend(unpack(A), e, size_t(j)), E_out);
+  });
+}
+int gfq_row_lengthen(const gfq_mat* Mm, const gfq_pkgE* E1, const gfq_pkgE* E2, gfq_mat** out) {
+  return guard([&] { *out = wrap(gfq::row_lengthen(M(Mm), unpack(E1), unpack(E2))); });
+}
+int gfq_pre_clear_up(const gfq_mat* Bm, const gfq_pkgD* D, gfq_mat** X, gfq_mat** R) {
+  return guard([&] {
+    auto [x, r] = gfq::pre_clear_up(M(Bm), unpack(D));
+    *X = wrap(std::move(x));
+    *R = wrap(std::move(r));
+  });
+}
+int gfq_clear_up(uint32_t p, const gfq_mat* R, const gfq_mat* X, const gfq_mat* Mm, gfq_mat** out) {
+  return guard([&] { *out = wrap(gfq::clear_up(gfq::FieldSpec(p), M(R), M(X), M(Mm))); });
+}
+int gfq_copy_d(const gfq_pkgD* D, gfq_mat** out) {
+  return guard([&] { *out = wrap(gfq::copy_d(unpack(D))); });
+}
+void gfq_pkgA_free(gfq_pkgA* a) {
+  if (!a) return;
+  gfq_mat_free(a->A);
+  gfq_mat_free(a->M);
+  gfq_mat_free(a->K);
+  gfq_iset_free(a->rho_prime);
+  gfq_mat_free(a->E);
+  gfq_bits_free(a->lambda);
+  *a = gfq_pkgA{};
+}
+void gfq_pkgD_free(gfq_pkgD* d) {
+  if (!d) return;
+  gfq_mat_free(d->R);
+  gfq_iset_free(d->gamma);
+  *d = gfq_pkgD{};
+}
+void gfq_pkgE_free(gfq_pkgE* e) {
+  if (!e) return;
+  gfq_iset_free(e->rho);
+  gfq_bits_free(e->delta);
+  *e = gfq_pkgE{};
+}
+
+// ---------------------------------------------------------------- chief
+int gfq_chop(uint64_t m, uint64_t n, uint64_t block, int remainder_first, uint64_t* row_parts,
+             uint64_t* a, uint64_t* col_parts, uint64_t* b) {
+  return guard([&] {
+    const gfq::ChopSpec cs = gfq::chop(size_t(m), size_t(n), size_t(block), remainder_first != 0);
+    if (a) *a = cs.a();
+    if (b) *b = cs.b();
+    if (row_parts)
+      for (size_t i = 0; i < cs.a(); ++i) row_parts[i] = cs.row_parts[i];
+    if (col_parts)
+      for (size_t j = 0; j < cs.b(); ++j) col_parts[j] = cs.col_parts[j];
+  });
+}
+
+void gfq_options_default(gfq_options* o) {
+  o->block = 256;
+  o->threads = 1;
+  o->with_transform = 1;
+  o->ech_threshold = 256;
+  o->remainder_first = 0;
+  o->collect_trace = 0;
+  o->retain_all = 0;
+}
+
+namespace {
+gfq::EchelonizeOptions to_opts(const gfq_options* o) {
+  gfq_options d;
+  gfq_options_default(&d);
+  if (!o) o = &d;
+  gfq::EchelonizeOptions e;
+  e.block = size_t(o->block);
+  e.threads = o->threads;
+  e.with_transform = o->with_transform != 0;
+  e.ech_threshold = size_t(o->ech_threshold);
+  e.remainder_first = o->remainder_first != 0;
+  e.collect_trace = o->collect_trace != 0;
+  e.retain_all = o->retain_all != 0;
+  return e;
+}
+const gfq_output& O(const gfq_output* o) {
+  if (!o) throw std::invalid_argument("null output handle");
+  return *o;
+}
+}  // namespace
+
+int gfq_echelonize(uint32_t p, const gfq_mat* C, const gfq_options* opt, gfq_output** out) {
+  return guard([&] {
+    gfq::RunReport rep;
+    auto res = std::make_unique<gfq_output>(
+        gfq::echelonize(M(C), gfq::FieldSpec(p), to_opts(opt), &rep));
+    res->report = std::move(rep);
+    *out = res.release();
+  });
+}
+
+int gfq_echelonize_host(uint32_t p, int64_t m, int64_t n, const uint8_t* C, int64_t ld,
+                        const gfq_options* opt, gfq_output** out) {
+  return guard([&] {
+    require_device();
+    const gfq::FieldSpec f(p);
+    gfq::Mat dc(m, n);
+    if (!dc.empty())
+      GFQ_CUDA(cudaMemcpy2DAsync(dc.data(), size_t(dc.ld()), C, size_t(ld), size_t(n), size_t(m),
+                                 cudaMemcpyHostToDevice, gfq::cur_stream()));
+    gfq::RunReport rep;
+    auto res = std::make_unique<gfq_output>(gfq::echelonize(dc, f, to_opts(opt), &rep));
+    res->report = std::move(rep);
+    *out = res.release();
+  });
+}
+
+int gfq_output_rank(const gfq_output* o, uint64_t* rank) {
+  return guard([&] { *rank = O(o).out.rank; });
+}
+int gfq_output_grid(const gfq_output* o, uint64_t* a, uint64_t* b) {
+  return guard([&] {
+    *a = O(o).out.chop.a();
+    *b = O(o).out.chop.b();
+  });
+}
+int gfq_output_select(const gfq_output* o, int which, uint64_t x, uint32_t* buf, uint64_t* count) {
+  return guard([&] {
+    const auto& v = which == 0 ? O(o).out.upsilon : O(o).out.varrho;
+    const gfq::IndexSet& s = v.at(size_t(x));
+    if (count) *count = s.size();
+    if (buf && s.size()) std::memcpy(buf, s.members.data(), s.size() * 4);
+  });
+}
+int gfq_output_block(const gfq_output* o, int kind, uint64_t x, uint64_t y, gfq_mat** blk) {
+  return guard([&] {
+    const auto& out = O(o).out;
+    if (kind != 0 && !out.with_transform) throw std::logic_error("transformation was not computed");
+    const auto& grid = kind == 0 ? out.R_blocks : kind == 1 ? out.T_M_blocks : out.T_K_blocks;
+    if (kind == 0 && y < x) throw std::invalid_argument("R_blocks[j][l] requires l >= j");
+    *blk = wrap(grid.at(size_t(x)).at(size_t(y)));
+  });
+}
+int gfq_output_assembled_R(const gfq_output* o, gfq_mat** out) {
+  return guard([&] { *out = wrap(O(o).out.assembled_R()); });
+}
+int gfq_output_transform(const gfq_output* o, gfq_mat** out) {
+  return guard([&] { *out = wrap(gfq::materialize_transform(O(o).out)); });
+}
+
+}  // extern "C"
+namespace {
+template <class F>
+void for_each_block(const gfq::EchelonOutput& out, F&& f) {
+  for (size_t j = 0; j < out.R_blocks.size(); ++j)
+    for (size_t l = j; l < out.R_blocks.size(); ++l) f(out.R_blocks[j][l]);
+  for (const auto& row : out.T_M_blocks)
+    for (const auto& m : row) f(m);
+  for (const auto& row : out.T_K_blocks)
+    for (const auto& m : row) f(m);
+}
+}  // namespace
+extern "C" {
+
+int gfq_output_block_bytes(const gfq_output* o, uint64_t* bytes) {
+  return guard([&] {
+    uint64_t n = 0;
+    for_each_block(O(o).out, [&](const gfq::Mat& m) { n += uint64_t(m.rows()) * uint64_t(m.cols()); });
+    *bytes = n;
+  });
+}
+int gfq_output_download_blocks(const gfq_output* o, uint8_t* host, uint64_t cap) {
+  return guard([&] {
+    uint64_t off = 0;
+    for_each_block(O(o).out, [&](const gfq::Mat& m) {
+      const uint64_t sz = uint64_t(m.rows()) * uint64_t(m.cols());
+      if (off + sz > cap) throw std::invalid_argument("download_blocks: buffer too small");
+      if (sz)
+        GFQ_CUDA(cudaMemcpy2DAsync(host + off, size_t(m.cols()), m.data(), size_t(m.ld()),
+                                   size_t(m.cols()), size_t(m.rows()), cudaMemcpyDeviceToHost,
+                                   gfq::cur_stream()));
+      off += sz;
+    });
+    GFQ_CUDA(cudaStreamSynchronize(gfq::cur_stream()));
+  });
+}
+int gfq_output_report(const gfq_output* o, gfq_report* rep) {
+  return guard([&] {
+    const auto& r = O(o).report;
+    rep->wall_ns = r.wall_ns;
+    rep->peak_live_bytes = r.peak_live_bytes;
+    rep->initial_live_bytes = r.initial_live_bytes;
+    rep->tasks = int64_t(r.trace.size());
+    rep->workers = r.workers;
+  });
+}
+int gfq_output_trace(const gfq_output* o, uint64_t* n, int32_t* kind, int32_t* i, int32_t* j,
+                     int32_t* k, int32_t* worker, int64_t* start_ns, int64_t* end_ns,
+                     int32_t* detail) {
+  return guard([&] {
+    const auto& tr = O(o).report.trace;
+    if (n) *n = tr.size();
+    for (size_t q = 0; q < tr.size(); ++q) {
+      if (kind) kind[q] = int32_t(tr[q].kind);
+      if (i) i[q] = tr[q].c0;
+      if (j) j[q] = tr[q].c1;
+      if (k) k[q] = tr[q].c2;
+      if (worker) worker[q] = tr[q].worker;
+      if (start_ns) start_ns[q] = tr[q].start_ns;
+      if (end_ns) end_ns[q] = tr[q].end_ns;
+      if (detail) detail[q] = tr[q].detail;
+    }
+  });
+}
+void gfq_output_free(gfq_output* o) { delete o; }
+
+}  // extern "C"

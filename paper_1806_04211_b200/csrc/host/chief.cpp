@@ -1,0 +1,349 @@
+// chief.cpp -- chop, plan, run, assemble (see chief.hpp).
+#include "chief.hpp"
+
+#include <numeric>
+#include <stdexcept>
+
+#include "../kernels/kernels.hpp"
+#include "jobs.hpp"
+
+namespace gfq {
+
+std::size_t ChopSpec::rows() const {
+  return std::accumulate(row_parts.begin(), row_parts.end(), std::size_t(0));
+}
+std::size_t ChopSpec::cols() const {
+  return std::accumulate(col_parts.begin(), col_parts.end(), std::size_t(0));
+}
+std::size_t ChopSpec::row_offset(std::size_t i) const {
+  return std::accumulate(row_parts.begin(), row_parts.begin() + std::ptrdiff_t(i), std::size_t(0));
+}
+std::size_t ChopSpec::col_offset(std::size_t j) const {
+  return std::accumulate(col_parts.begin(), col_parts.begin() + std::ptrdiff_t(j), std::size_t(0));
+}
+
+// reference src/chief.cpp:33-53
+static std::vector<std::size_t> chop_axis(std::size_t total, std::size_t block, bool rem_first) {
+  std::vector<std::size_t> parts;
+  const std::size_t full = total / block, rem = total % block;
+  if (rem && rem_first) parts.push_back(rem);
+  parts.insert(parts.end(), full, block);
+  if (rem && !rem_first) parts.push_back(rem);
+  return parts;
+}
+
+ChopSpec chop(std::size_t m, std::size_t n, std::size_t block, bool remainder_first) {
+  if (block < 1) throw std::invalid_argument("chop: block must be >= 1");
+  return ChopSpec{chop_axis(m, block, remainder_first), chop_axis(n, block, remainder_first)};
+}
+
+// ---------------------------------------------------------------- plan
+namespace {
+struct Emitter {
+  TaskGraph& g;
+  std::int32_t slot(PkgKind k, std::size_t c0, std::size_t c1, std::size_t c2, std::size_t v) {
+    return g.require_slot({k, std::uint16_t(c0), std::uint16_t(c1), std::uint16_t(c2),
+                           std::uint16_t(v)});
+  }
+  void node(TaskKind kind, std::int32_t c0, std::int32_t c1, std::int32_t c2, std::int32_t pri,
+            std::initializer_list<std::int32_t> in, std::initializer_list<std::int32_t> out) {
+    TaskNode nd;
+    nd.kind = kind;
+    nd.c0 = c0;
+    nd.c1 = c1;
+    nd.c2 = c2;
+    nd.priority = pri;
+    for (auto s : in) nd.in[nd.n_in++] = s;
+    for (auto s : out) nd.out[nd.n_out++] = s;
+    g.plan_add(nd);
+  }
+};
+}  // namespace
+
+// The slot/version scheme and loop order of reference src/chief.cpp:67-287
+// (SURVEY Appendix A): Step 1 j-outer/i-inner, Step 2 RowLengthen, Step 3
+// descending rounds k = b-1..1.
+PlanHandles build_plan(TaskGraph& graph, const Mat& C, const FieldSpec& field,
+                       const ChopSpec& cs, bool with_transform) {
+  const std::size_t a = cs.a(), b = cs.b();
+  if (a == 0 || b == 0) throw std::invalid_argument("build_plan: empty partition");
+  if (std::int64_t(cs.rows()) != C.rows() || std::int64_t(cs.cols()) != C.cols())
+    throw std::invalid_argument("build_plan: partition does not match matrix");
+  if (a >= (1u << 14) || b >= (1u << 14))
+    throw std::invalid_argument("build_plan: block grid exceeds slot coordinates");
+  graph.set_field(field);
+  Emitter e{graph};
+  using K = PkgKind;
+  using T = TaskKind;
+
+  for (std::size_t i = 0; i < a; ++i)
+    for (std::size_t k = 0; k < b; ++k)
+      graph.add_input({K::C, std::uint16_t(i), std::uint16_t(k), 0, 0},
+                      C.row_view(std::int64_t(cs.row_offset(i)), std::int64_t(cs.row_parts[i]))
+                          .col_view(std::int64_t(cs.col_offset(k)), std::int64_t(cs.col_parts[k])));
+
+  // Step 1
+  for (std::size_t j = 0; j < b; ++j) {
+    for (std::size_t i = 0; i < a; ++i) {
+      const std::int32_t pri = std::int32_t(i + j);
+      const auto sD = [&](std::size_t v) { return e.slot(K::D, j, 0, 0, v); };
+      const std::int32_t sA = e.slot(K::A, i, j, 0, 0);
+      if (i > 0)
+        e.node(T::ClearDown, std::int32_t(i), std::int32_t(j), -1, pri,
+               {e.slot(K::C, i, j, 0, j), sD(i - 1)}, {sD(i), sA});
+      else
+        e.node(T::ClearDown, std::int32_t(i), std::int32_t(j), -1, pri, {e.slot(K::C, i, j, 0, j)},
+               {sD(i), sA});
+      if (j > 0)
+        e.node(T::Extend, std::int32_t(i), std::int32_t(j), -1, pri,
+               {sA, e.slot(K::E, i, 0, 0, j - 1)}, {e.slot(K::E, i, 0, 0, j)});
+      else
+        e.node(T::Extend, std::int32_t(i), std::int32_t(j), -1, pri, {sA},
+               {e.slot(K::E, i, 0, 0, j)});
+      for (std::size_t k = j + 1; k < b; ++k) {
+        const std::int32_t cin = e.slot(K::C, i, k, 0, j), cout = e.slot(K::C, i, k, 0, j + 1);
+        const std::int32_t bout = e.slot(K::B, j, k, 0, i);
+        if (i > 0)
+          e.node(T::UpdateRow, std::int32_t(i), std::int32_t(j), std::int32_t(k), pri,
+                 {sA, cin, e.slot(K::B, j, k, 0, i - 1)}, {cout, bout});
+        else
+          e.node(T::UpdateRow, std::int32_t(i), std::int32_t(j), std::int32_t(k), pri, {sA, cin},
+                 {cout, bout});
+      }
+      if (with_transform) {
+        for (std::size_t h = 0; h <= i; ++h) {
+          TaskNode tr;
+          tr.kind = T::UpdateRowTrafo;
+          tr.c0 = std::int32_t(i);
+          tr.c1 = std::int32_t(j);
+          tr.c2 = std::int32_t(h);
+          tr.priority = pri;
+          tr.in[tr.n_in++] = sA;
+          tr.in[tr.n_in++] = e.slot(K::E, h, 0, 0, j);
+          if (j > 0) tr.in[tr.n_in++] = e.slot(K::K, i, h, 0, j - 1);
+          if (h < i) tr.in[tr.n_in++] = e.slot(K::M, j, h, 0, i - 1 - h);
+          tr.out[tr.n_out++] = e.slot(K::K, i, h, 0, j);
+          tr.out[tr.n_out++] = e.slot(K::M, j, h, 0, i - h);
+          graph.plan_add(tr);
+        }
+      }
+    }
+  }
+  // Step 2
+  if (with_transform)
+    for (std::size_t j = 0; j < b; ++j)
+      for (std::size_t h = 0; h < a; ++h)
+        e.node(T::RowLengthen, -1, std::int32_t(j), std::int32_t(h), std::int32_t(a + b - 1),
+               {e.slot(K::M, j, h, 0, a - 1 - h), e.slot(K::E, h, 0, 0, j),
+                e.slot(K::E, h, 0, 0, b - 1)},
+               {e.slot(K::M, j, h, 0, a - h)});
+  // Step 3
+  for (std::size_t k = 0; k < b; ++k)
+    e.node(T::Copy, -1, std::int32_t(k), -1, std::int32_t(a + b + (b - 1 - k)),
+           {e.slot(K::D, k, 0, 0, a - 1)}, {e.slot(K::R, k, k, 0, 0)});
+  for (std::size_t k = b; k-- > 1;) {
+    const std::int32_t pri = std::int32_t(a + b + (b - 1 - k));
+    for (std::size_t j = 0; j < k; ++j) {
+      const std::int32_t sX = e.slot(K::X, j, k, 0, 0);
+      e.node(T::PreClearUp, -1, std::int32_t(j), std::int32_t(k), pri,
+             {e.slot(K::B, j, k, 0, a - 1), e.slot(K::D, k, 0, 0, a - 1)},
+             {sX, e.slot(K::R, j, k, 0, 0)});
+      for (std::size_t l = k; l < b; ++l)
+        e.node(T::ClearUp, std::int32_t(k), std::int32_t(j), std::int32_t(l), pri,
+               {e.slot(K::R, j, l, 0, l - k), sX, e.slot(K::R, k, l, 0, l - k)},
+               {e.slot(K::R, j, l, 0, l - k + 1)});
+      if (with_transform)
+        for (std::size_t h = 0; h < a; ++h)
+          e.node(T::ClearUp, std::int32_t(k), std::int32_t(j), std::int32_t(h), pri,
+                 {e.slot(K::M, j, h, 0, a - h + (b - 1 - k)), sX,
+                  e.slot(K::M, k, h, 0, a - h + (b - 1 - k))},
+                 {e.slot(K::M, j, h, 0, a - h + (b - k))});
+    }
+  }
+
+  PlanHandles hd;
+  for (std::size_t j = 0; j < b; ++j) hd.d_final.push_back(e.slot(K::D, j, 0, 0, a - 1));
+  for (std::size_t i = 0; i < a; ++i) hd.e_final.push_back(e.slot(K::E, i, 0, 0, b - 1));
+  hd.r_final.assign(b, std::vector<std::int32_t>(b, -1));
+  for (std::size_t j = 0; j < b; ++j)
+    for (std::size_t l = j; l < b; ++l) hd.r_final[j][l] = e.slot(K::R, j, l, 0, l - j);
+  if (with_transform) {
+    hd.m_final.assign(b, std::vector<std::int32_t>(a, -1));
+    for (std::size_t j = 0; j < b; ++j)
+      for (std::size_t h = 0; h < a; ++h)
+        hd.m_final[j][h] = e.slot(K::M, j, h, 0, a - h + (b - 1 - j));
+    hd.k_final.resize(a);
+    for (std::size_t i = 0; i < a; ++i)
+      for (std::size_t h = 0; h <= i; ++h) hd.k_final[i].push_back(e.slot(K::K, i, h, 0, b - 1));
+  }
+  graph.drop_key_index_if_large();
+  return hd;
+}
+
+// ---------------------------------------------------------------- echelonize
+EchelonOutput echelonize(const Mat& C, const FieldSpec& field, const EchelonizeOptions& options,
+                         RunReport* report) {
+  const ChopSpec cs = chop(std::size_t(C.rows()), std::size_t(C.cols()), options.block,
+                           options.remainder_first);
+  const std::size_t a = cs.a(), b = cs.b();
+  EchelonOutput out{field};
+  out.chop = cs;
+  out.with_transform = options.with_transform;
+  if (a == 0 || b == 0) {
+    // reference src/chief.cpp:289-320 (empty_output)
+    if (report) *report = RunReport{};
+    for (std::size_t j = 0; j < b; ++j) out.upsilon.emplace_back(cs.col_parts[j], std::vector<std::uint32_t>{});
+    for (std::size_t i = 0; i < a; ++i) out.varrho.emplace_back(cs.row_parts[i], std::vector<std::uint32_t>{});
+    out.R_blocks.assign(b, std::vector<Mat>(b));
+    for (std::size_t j = 0; j < b; ++j)
+      for (std::size_t l = j; l < b; ++l) out.R_blocks[j][l] = Mat(0, std::int64_t(cs.col_parts[l]));
+    if (options.with_transform) {
+      out.T_M_blocks.assign(b, std::vector<Mat>(a));
+      out.T_K_blocks.resize(a);
+      for (std::size_t i = 0; i < a; ++i)
+        for (std::size_t h = 0; h <= i; ++h)
+          out.T_K_blocks[i].push_back(Mat(std::int64_t(cs.row_parts[i]), 0));
+    }
+    return out;
+  }
+
+  TaskGraph graph;
+  graph.ech_threshold = options.ech_threshold;
+  const PlanHandles h = build_plan(graph, C, field, cs, options.with_transform);
+  for (auto id : h.d_final) graph.retain(id);
+  for (auto id : h.e_final) graph.retain(id);
+  for (const auto& row : h.r_final)
+    for (auto id : row)
+      if (id >= 0) graph.retain(id);
+  for (const auto& row : h.m_final)
+    for (auto id : row) graph.retain(id);
+  for (const auto& row : h.k_final)
+    for (auto id : row) graph.retain(id);
+
+  RunOptions ro;
+  ro.workers = options.threads;
+  ro.collect_trace = options.collect_trace;
+  ro.retain_all = options.retain_all;
+  RunReport rep = run(graph, ro);
+  if (report) *report = std::move(rep);
+
+  for (std::size_t j = 0; j < b; ++j) {
+    const PkgD& d = std::get<PkgD>(*graph.payload(h.d_final[j]));
+    out.rank += d.gamma.size();
+    out.upsilon.push_back(d.gamma);
+  }
+  for (std::size_t i = 0; i < a; ++i)
+    out.varrho.push_back(std::get<PkgE>(*graph.payload(h.e_final[i])).rho);
+  out.R_blocks.assign(b, std::vector<Mat>(b));
+  for (std::size_t j = 0; j < b; ++j)
+    for (std::size_t l = j; l < b; ++l)
+      out.R_blocks[j][l] = std::get<Mat>(*graph.payload(h.r_final[j][l]));
+  if (options.with_transform) {
+    out.T_M_blocks.assign(b, std::vector<Mat>(a));
+    for (std::size_t j = 0; j < b; ++j)
+      for (std::size_t hh = 0; hh < a; ++hh)
+        out.T_M_blocks[j][hh] = std::get<Mat>(*graph.payload(h.m_final[j][hh]));
+    out.T_K_blocks.resize(a);
+    for (std::size_t i = 0; i < a; ++i)
+      for (std::size_t hh = 0; hh <= i; ++hh)
+        out.T_K_blocks[i].push_back(std::get<Mat>(*graph.payload(h.k_final[i][hh])));
+  }
+  return out;
+}
+
+// ---------------------------------------------------------------- assembly
+std::vector<std::uint32_t> EchelonOutput::global_upsilon() const {
+  std::vector<std::uint32_t> v;
+  for (std::size_t j = 0; j < upsilon.size(); ++j)
+    for (auto x : upsilon[j].members) v.push_back(std::uint32_t(chop.col_offset(j) + x));
+  return v;
+}
+
+std::vector<std::uint32_t> EchelonOutput::global_varrho() const {
+  std::vector<std::uint32_t> v;
+  for (std::size_t i = 0; i < varrho.size(); ++i)
+    for (auto x : varrho[i].members) v.push_back(std::uint32_t(chop.row_offset(i) + x));
+  return v;
+}
+
+// reference src/chief.cpp:408-425, as device-to-device block copies.
+Mat EchelonOutput::assembled_R() const {
+  const std::int64_t n = std::int64_t(chop.cols());
+  Mat out = Mat::zeros(std::int64_t(rank), n - std::int64_t(rank));
+  if (out.empty()) return out;
+  std::int64_t row = 0;
+  for (std::size_t j = 0; j < upsilon.size(); ++j) {
+    std::int64_t col = 0;
+    for (std::size_t l = 0; l < upsilon.size(); ++l) {
+      const std::int64_t width = std::int64_t(chop.col_parts[l] - upsilon[l].size());
+      if (l >= j && width > 0 && upsilon[j].size() > 0) {
+        const Mat& blk = R_blocks[j][l];
+        GFQ_CUDA(cudaMemcpy2DAsync(out.data() + row * out.ld() + col, std::size_t(out.ld()),
+                                   blk.data(), std::size_t(blk.ld()), std::size_t(width),
+                                   std::size_t(blk.rows()), cudaMemcpyDeviceToDevice,
+                                   cur_stream()));
+      }
+      col += width;
+    }
+    row += std::int64_t(upsilon[j].size());
+  }
+  return out;
+}
+
+// reference src/chief.cpp:489-520: T rows = pivot rows by (j, q), then
+// non-pivot rows by block row; columns = original rows.  Built as column
+// scatters of the M / K blocks into zero-initialised stripes.
+Mat materialize_transform(const EchelonOutput& out) {
+  if (!out.with_transform) throw std::logic_error("transformation was not computed");
+  const std::int64_t m = std::int64_t(out.chop.rows());
+  const std::size_t a = out.chop.a(), b = out.chop.b();
+  Mat t = Mat::zeros(m, m);
+  if (t.empty()) return t;
+  // per block row h: column map of its stripe (selected row -> position)
+  std::vector<std::shared_ptr<DevBuf>> cmaps(a);
+  for (std::size_t h = 0; h < a; ++h) {
+    std::vector<std::int32_t> map(out.chop.row_parts[h], -1);
+    for (std::size_t s = 0; s < out.varrho[h].size(); ++s)
+      map[out.varrho[h].members[s]] = std::int32_t(s);
+    cmaps[h] = upload_i32(map);
+  }
+  std::int64_t row = 0;
+  for (std::size_t j = 0; j < b; ++j) {
+    const std::int64_t nr = std::int64_t(out.upsilon[j].size());
+    for (std::size_t h = 0; h < a && nr > 0; ++h) {
+      const Mat& mjh = out.T_M_blocks[j][h];
+      if (out.varrho[h].size() == 0) continue;
+      dev::select2d(t.data() + row * t.ld() + std::int64_t(out.chop.row_offset(h)), t.ld(), nr,
+                    std::int64_t(out.chop.row_parts[h]), mjh.data(), mjh.ld(), nullptr, 0,
+                    nullptr, reinterpret_cast<const std::int32_t*>(cmaps[h]->ptr), cur_stream());
+    }
+    row += nr;
+  }
+  std::vector<std::int32_t> ones;
+  for (std::size_t i = 0; i < a; ++i) {
+    const IndexSet rest = index_set_complement(out.varrho[i]);
+    const std::int64_t nr = std::int64_t(rest.size());
+    for (std::size_t h = 0; h <= i && nr > 0; ++h) {
+      const Mat& kih = out.T_K_blocks[i][h];
+      if (out.varrho[h].size() == 0) continue;
+      dev::select2d(t.data() + row * t.ld() + std::int64_t(out.chop.row_offset(h)), t.ld(), nr,
+                    std::int64_t(out.chop.row_parts[h]), kih.data(), kih.ld(), nullptr, 0,
+                    nullptr, reinterpret_cast<const std::int32_t*>(cmaps[h]->ptr), cur_stream());
+    }
+    // identity at the row's own column (written after the stripe scatter,
+    // which puts 0 at non-selected columns)
+    for (std::size_t u = 0; u < rest.size(); ++u) {
+      ones.push_back(std::int32_t(row + std::int64_t(u)));
+      ones.push_back(std::int32_t(out.chop.row_offset(i) + rest.members[u]));
+    }
+    row += nr;
+  }
+  if (!ones.empty()) {
+    auto pb = upload_i32(ones);
+    dev::set_entries(t.data(), t.ld(), reinterpret_cast<const std::int32_t*>(pb->ptr),
+                     std::int64_t(ones.size() / 2), 1, cur_stream());
+  }
+  return t;
+}
+
+}  // namespace gfq

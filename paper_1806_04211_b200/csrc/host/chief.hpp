@@ -1,0 +1,76 @@
+// chief.hpp -- ChopMatrix, the Chief's plan and the echelonize entry point
+// (reference include/gfrref/chief.hpp:27-105), B200 edition.
+#pragma once
+
+#include <cstddef>
+#include <string>
+#include <vector>
+
+#include "scheduler.hpp"
+
+namespace gfq {
+
+/// reference include/gfrref/chief.hpp:15-25
+struct ChopSpec {
+  std::vector<std::size_t> row_parts;
+  std::vector<std::size_t> col_parts;
+  std::size_t a() const { return row_parts.size(); }
+  std::size_t b() const { return col_parts.size(); }
+  std::size_t rows() const;
+  std::size_t cols() const;
+  std::size_t row_offset(std::size_t i) const;
+  std::size_t col_offset(std::size_t j) const;
+};
+
+/// reference include/gfrref/chief.hpp:27-28
+ChopSpec chop(std::size_t m, std::size_t n, std::size_t block, bool remainder_first = false);
+
+/// reference include/gfrref/chief.hpp:33-59, blocks device-resident.
+struct EchelonOutput {
+  FieldSpec field;
+  ChopSpec chop;
+  bool with_transform = false;
+  std::size_t rank = 0;
+  explicit EchelonOutput(FieldSpec f) : field(f) {}
+  std::vector<std::vector<Mat>> R_blocks;    // [j][l], l >= j
+  std::vector<std::vector<Mat>> T_M_blocks;  // [j][h]
+  std::vector<std::vector<Mat>> T_K_blocks;  // [i][h], h <= i
+  std::vector<IndexSet> varrho;              // per block row
+  std::vector<IndexSet> upsilon;             // per block column
+  std::vector<std::uint32_t> global_upsilon() const;
+  std::vector<std::uint32_t> global_varrho() const;
+  /// rank x (n - rank) remnant, assembled on the device.
+  Mat assembled_R() const;
+};
+
+struct PlanHandles {
+  std::vector<std::int32_t> d_final, e_final;
+  std::vector<std::vector<std::int32_t>> r_final, m_final, k_final;
+};
+
+/// reference include/gfrref/chief.hpp:72: Steps 1-3 into a fresh graph.
+/// Input blocks are views of the device-resident C (no copy).
+PlanHandles build_plan(TaskGraph& graph, const Mat& C, const FieldSpec& field,
+                       const ChopSpec& chop, bool with_transform);
+
+/// reference include/gfrref/chief.hpp:76-84 (+ `workers`: host threads,
+/// one CUDA stream each; the reference's `threads`).
+struct EchelonizeOptions {
+  std::size_t block = 256;
+  int threads = 1;
+  bool with_transform = true;
+  std::size_t ech_threshold = 256;
+  bool remainder_first = false;
+  bool collect_trace = false;
+  bool retain_all = false;
+};
+
+/// reference include/gfrref/chief.hpp:88-90.  C is device-resident.
+EchelonOutput echelonize(const Mat& C, const FieldSpec& field, const EchelonizeOptions& options,
+                         RunReport* report = nullptr);
+
+/// reference include/gfrref/chief.hpp:100: the m x m transformation,
+/// materialised on the device.
+Mat materialize_transform(const EchelonOutput& out);
+
+}  // namespace gfq

@@ -1,0 +1,333 @@
+// jobs.cpp -- block jobs on device (see jobs.hpp).
+#include "jobs.hpp"
+
+#include <algorithm>
+#include <atomic>
+#include <stdexcept>
+
+#include "../kernels/kernels.hpp"
+
+namespace gfq {
+
+namespace {
+std::atomic<std::size_t> g_ech_base{64};
+
+const std::int32_t* dptr(const std::shared_ptr<DevBuf>& b) {
+  return b ? reinterpret_cast<const std::int32_t*>(b->ptr) : nullptr;
+}
+
+// out = select(A | B) by optional row/column maps (kernels.hpp select2d).
+Mat select(std::int64_t rows, std::int64_t cols, const Mat& A, const Mat* B,
+           const std::vector<std::int32_t>* rmap, const std::vector<std::int32_t>* cmap) {
+  Mat out(rows, cols);
+  if (out.empty()) return out;
+  auto rb = rmap ? upload_i32(*rmap) : nullptr;
+  auto cb = cmap ? upload_i32(*cmap) : nullptr;
+  dev::select2d(out.data(), out.ld(), rows, cols, A.data(), A.ld(), B ? B->data() : nullptr,
+                B ? B->ld() : 0, dptr(rb), dptr(cb), cur_stream());
+  return out;
+}
+
+std::vector<std::int32_t> as_i32(const std::vector<std::uint32_t>& v) {
+  return std::vector<std::int32_t>(v.begin(), v.end());
+}
+}  // namespace
+
+void set_ech_base(std::size_t n) {
+  g_ech_base = std::max<std::size_t>(1, std::min<std::size_t>(n, dev::kEchBaseMax));
+}
+std::size_t ech_base() { return g_ech_base; }
+
+// ---------------------------------------------------------------- products
+static Mat mul_add_kernel(const FieldSpec& f, const Mat* addend, const Mat& b, const Mat& c) {
+  // reference src/matrix.cpp:81-89 shape contract
+  if (b.cols() != c.rows()) throw std::invalid_argument("mul: inner dimensions disagree");
+  if (addend && (addend->rows() != b.rows() || addend->cols() != c.cols()))
+    throw std::invalid_argument("mad: addend shape mismatch");
+  const std::int64_t m = b.rows(), inner = b.cols(), n = c.cols();
+  Mat out(m, n);
+  if (m == 0 || n == 0) return out;
+  dev::mad(f.p(), m, n, inner, b.data(), b.ld(), c.data(), c.ld(),
+           addend ? addend->data() : nullptr, addend ? addend->ld() : 0, out.data(), out.ld(),
+           cur_stream());
+  return out;
+}
+
+Mat mat_mul(const FieldSpec& f, const Mat& b, const Mat& c) {
+  return mul_add_kernel(f, nullptr, b, c);
+}
+Mat mat_mul_add(const FieldSpec& f, const Mat& a, const Mat& b, const Mat& c) {
+  return mul_add_kernel(f, &a, b, c);
+}
+Mat mul(const FieldSpec& f, const Mat& b, const Mat& c) { return mat_mul(f, b, c); }
+Mat mad(const FieldSpec& f, const Mat& a, const Mat& b, const Mat& c) {
+  return mat_mul_add(f, a, b, c);
+}
+
+Mat cpy(const Mat& a) { return select(a.rows(), a.cols(), a, nullptr, nullptr, nullptr); }
+
+// ---------------------------------------------------------------- gathers
+Mat take_rows(const Mat& m, const std::vector<std::uint32_t>& rows) {
+  for (auto r : rows)
+    if (std::int64_t(r) >= m.rows()) throw std::invalid_argument("take_rows: index out of range");
+  const auto map = as_i32(rows);
+  return select(std::int64_t(rows.size()), m.cols(), m, nullptr, &map, nullptr);
+}
+
+Mat take_cols(const Mat& m, const std::vector<std::uint32_t>& cols) {
+  for (auto c : cols)
+    if (std::int64_t(c) >= m.cols()) throw std::invalid_argument("take_cols: index out of range");
+  const auto map = as_i32(cols);
+  return select(m.rows(), std::int64_t(cols.size()), m, nullptr, nullptr, &map);
+}
+
+Mat vcat(const Mat& a, const Mat& b) {
+  if (a.cols() != b.cols()) throw std::invalid_argument("vcat: column counts disagree");
+  std::vector<std::int32_t> map(std::size_t(a.rows() + b.rows()));
+  for (std::int64_t i = 0; i < a.rows(); ++i) map[i] = std::int32_t(i);
+  for (std::int64_t i = 0; i < b.rows(); ++i) map[a.rows() + i] = -std::int32_t(i) - 2;
+  return select(a.rows() + b.rows(), a.cols(), a, &b, &map, nullptr);
+}
+
+Mat hcat(const Mat& a, const Mat& b) {
+  if (a.rows() != b.rows()) throw std::invalid_argument("hcat: row counts disagree");
+  std::vector<std::int32_t> map(std::size_t(a.cols() + b.cols()));
+  for (std::int64_t j = 0; j < a.cols(); ++j) map[j] = std::int32_t(j);
+  for (std::int64_t j = 0; j < b.cols(); ++j) map[a.cols() + j] = -std::int32_t(j) - 2;
+  return select(a.rows(), a.cols() + b.cols(), a, &b, nullptr, &map);
+}
+
+// Column riffle of two matrices (reference src/jobs.cpp:13-28).
+static Mat col_riffle(const BitString& u, const Mat& zeros_side, const Mat& ones_side) {
+  if (zeros_side.rows() != ones_side.rows())
+    throw std::invalid_argument("col_riffle: row counts disagree");
+  if (std::int64_t(u.count_zeros()) != zeros_side.cols() ||
+      std::int64_t(u.count_ones()) != ones_side.cols())
+    throw std::invalid_argument("col_riffle: bit counts disagree");
+  std::vector<std::int32_t> map(u.size());
+  std::int32_t zc = 0, oc = 0;
+  for (std::size_t l = 0; l < u.size(); ++l) map[l] = u.bits[l] ? -(oc++) - 2 : zc++;
+  return select(zeros_side.rows(), std::int64_t(u.size()), zeros_side, &ones_side, nullptr, &map);
+}
+
+std::pair<Mat, Mat> cex(const Mat& h, const IndexSet& gamma) {
+  if (std::int64_t(gamma.universe) != h.cols()) throw std::invalid_argument("cex: universe mismatch");
+  const IndexSet rest = index_set_complement(gamma);
+  return {take_cols(h, gamma.members), take_cols(h, rest.members)};
+}
+
+std::pair<Mat, Mat> rex(const Mat& h, const IndexSet& rho) {
+  if (std::int64_t(rho.universe) != h.rows()) throw std::invalid_argument("rex: universe mismatch");
+  const IndexSet rest = index_set_complement(rho);
+  return {take_rows(h, rho.members), take_rows(h, rest.members)};
+}
+
+// ---------------------------------------------------------------- index jobs (host)
+std::pair<IndexSet, BitString> unh(const IndexSet& rho1, const IndexSet& rho2) {
+  const IndexSet comp = index_set_complement(rho1);
+  if (rho2.universe != comp.size())
+    throw std::invalid_argument("unh: universe of rho2 must be the complement size");
+  std::vector<std::uint32_t> merged;
+  merged.reserve(rho1.size() + rho2.size());
+  BitString u;
+  u.bits.reserve(rho1.size() + rho2.size());
+  std::size_t i = 0, j = 0;
+  while (i < rho1.size() || j < rho2.size()) {
+    const std::uint32_t e = j < rho2.size() ? comp.members[rho2.members[j]] : 0;
+    if (j >= rho2.size() || (i < rho1.size() && rho1.members[i] < e)) {
+      merged.push_back(rho1.members[i++]);
+      u.bits.push_back(0);
+    } else {
+      merged.push_back(e);
+      ++j;
+      u.bits.push_back(1);
+    }
+  }
+  return {IndexSet(rho1.universe, std::move(merged)), std::move(u)};
+}
+
+std::pair<IndexSet, BitString> un0(const IndexSet& rho2) {
+  BitString u;
+  u.bits.assign(rho2.size(), 1);
+  return {rho2, std::move(u)};
+}
+
+BitString mkr(const IndexSet& rho1, const IndexSet& rho2) {
+  BitString out;
+  out.bits.assign(rho2.size(), 0);
+  std::size_t i = 0;
+  for (std::size_t l = 0; l < rho2.members.size(); ++l)
+    if (i < rho1.members.size() && rho1.members[i] == rho2.members[l]) {
+      out.bits[l] = 1;
+      ++i;
+    }
+  if (i != rho1.members.size()) throw std::invalid_argument("mkr: rho1 must be a subset of rho2");
+  return out;
+}
+
+// ---------------------------------------------------------------- riffles
+Mat rrf(const BitString& u, const Mat& b, const Mat& c) {
+  if (std::int64_t(u.count_zeros()) != b.rows() || std::int64_t(u.count_ones()) != c.rows())
+    throw std::invalid_argument("rrf: bit counts do not match row counts");
+  if (b.cols() != c.cols() && b.rows() != 0 && c.rows() != 0)
+    throw std::invalid_argument("rrf: column counts disagree");
+  const std::int64_t cols = (b.rows() != 0 || c.rows() == 0) ? b.cols() : c.cols();
+  std::vector<std::int32_t> map(u.size());
+  std::int32_t bi = 0, ci = 0;
+  for (std::size_t l = 0; l < u.size(); ++l) map[l] = u.bits[l] ? -(ci++) - 2 : bi++;
+  return select(std::int64_t(u.size()), cols, b, &c, &map, nullptr);
+}
+
+Mat crz(const Mat& m, const BitString& lambda, std::size_t out_cols) {
+  if (lambda.size() != out_cols) throw std::invalid_argument("crz: lambda length must equal out_cols");
+  if (std::int64_t(lambda.count_ones()) != m.cols())
+    throw std::invalid_argument("crz: ones count must equal input columns");
+  std::vector<std::int32_t> map(out_cols);
+  std::int32_t src = 0;
+  for (std::size_t l = 0; l < out_cols; ++l) map[l] = lambda.bits[l] ? src++ : -1;
+  return select(m.rows(), std::int64_t(out_cols), m, nullptr, nullptr, &map);
+}
+
+Mat adi(const Mat& k, const BitString& delta) {
+  if (std::int64_t(delta.size()) != k.cols())
+    throw std::invalid_argument("adi: delta length must equal columns");
+  if (std::int64_t(delta.count_ones()) > k.rows())
+    throw std::invalid_argument("adi: more marked positions than rows");
+  Mat out = cpy(k);
+  std::vector<std::int32_t> pos;
+  std::int32_t i = 0;
+  for (std::size_t l = 0; l < delta.size(); ++l)
+    if (delta.bits[l]) {
+      pos.push_back(i++);
+      pos.push_back(std::int32_t(l));
+    }
+  if (!pos.empty()) {
+    auto pb = upload_i32(pos);
+    dev::set_entries(out.data(), out.ld(), dptr(pb), std::int64_t(pos.size() / 2), 1, cur_stream());
+  }
+  return out;
+}
+
+// ---------------------------------------------------------------- ECH
+namespace {
+
+// Base case: K2 kernel, then gather M/K/R in the reference's conventions
+// (rows of M and R by ascending pivot column, columns of M/K by ascending
+// selected row, rows of K by ascending non-selected row; jobs.cpp:85-120).
+EchResult direct_ech(const FieldSpec& f, const Mat& h) {
+  const std::int64_t a = h.rows(), b = h.cols();
+  const std::int64_t rmax = std::min(a, b);
+  Mat W(a, b), Tc(a, rmax > 0 ? rmax : 1);
+  auto info = std::make_shared<DevBuf>(std::size_t(4 * (2 * rmax + 1)));
+  dev::ech_base(f.p(), a, b, h.data(), h.ld(), W.data(), W.ld(), Tc.data(), Tc.ld(),
+                reinterpret_cast<std::int32_t*>(info->ptr), cur_stream());
+  std::vector<std::int32_t> hi(std::size_t(2 * rmax + 1));
+  download_i32(reinterpret_cast<const std::int32_t*>(info->ptr), hi.data(), hi.size());
+  const std::int64_t r = hi[0];
+  std::vector<std::int32_t> pcol(hi.begin() + 1, hi.begin() + 1 + r);
+  std::vector<std::int32_t> prow(hi.begin() + 1 + rmax, hi.begin() + 1 + rmax + r);
+
+  EchResult out;
+  std::vector<std::uint32_t> rho(prow.begin(), prow.end());
+  std::sort(rho.begin(), rho.end());
+  out.rho = IndexSet(std::size_t(a), rho);
+  out.gamma = IndexSet(std::size_t(b), std::vector<std::uint32_t>(pcol.begin(), pcol.end()));
+  // discovery position of each pivot row
+  std::vector<std::int32_t> pos_of(std::size_t(a), -1);
+  for (std::int64_t q = 0; q < r; ++q) pos_of[prow[q]] = std::int32_t(q);
+  std::vector<std::int32_t> tcols(static_cast<std::size_t>(r));
+  for (std::int64_t s = 0; s < r; ++s) tcols[s] = pos_of[rho[s]];
+  const IndexSet grest = index_set_complement(out.gamma);
+  const IndexSet nonsel = index_set_complement(out.rho);
+  const auto gcols = as_i32(grest.members);
+  const auto krows = as_i32(nonsel.members);
+  out.M = select(r, r, Tc, nullptr, &prow, &tcols);
+  out.K = select(a - r, r, Tc, nullptr, &krows, &tcols);
+  out.R = select(r, b - r, W, nullptr, &prow, &gcols);
+  return out;
+}
+
+// Split point: half, rounded to a multiple of 16 so column views keep the
+// 16-byte alignment the TMA path needs (outputs do not depend on it).
+std::int64_t split_of(std::int64_t n) {
+  const std::int64_t h = n / 2;
+  return (n >= 64 && h >= 16) ? h / 16 * 16 : h;
+}
+
+IndexSet shifted_union(const IndexSet& a, const IndexSet& b, std::size_t off, std::size_t universe) {
+  std::vector<std::uint32_t> mem = a.members;
+  for (auto v : b.members) mem.push_back(std::uint32_t(off + v));
+  return IndexSet(universe, std::move(mem));
+}
+
+// reference src/jobs.cpp:125-156
+EchResult combine_horizontal(const FieldSpec& f, const Mat& h2, const EchResult& e1,
+                             std::int64_t alpha1, std::size_t thr) {
+  auto [a_cols, h2_rest] = cex(h2, e1.gamma);
+  const Mat h2_clean = mad(f, h2_rest, a_cols, e1.R);
+  const EchResult e2 = ech(f, h2_clean, thr);
+  auto [a_sel, a_rest] = rex(a_cols, e2.rho);
+  auto [e_mid, r1_rest] = cex(e1.R, e2.gamma);
+  auto [gamma, lam] = unh(e1.gamma, e2.gamma);
+  const Mat mc = mul(f, mul(f, e2.M, a_sel), e1.M);
+  const Mat ma = mad(f, e1.M, e_mid, mc);
+  const Mat mb = mul(f, e_mid, e2.M);
+  EchResult out;
+  out.gamma = std::move(gamma);
+  out.M = rrf(lam, hcat(ma, mb), hcat(mc, e2.M));
+  out.R = rrf(lam, mad(f, r1_rest, e_mid, e2.R), e2.R);
+  const Mat k_bottom_left = mul(f, mad(f, a_rest, e2.K, a_sel), e1.M);
+  out.K = vcat(hcat(e1.K, Mat::zeros(e1.K.rows(), std::int64_t(e2.rho.size()))),
+               hcat(k_bottom_left, e2.K));
+  out.rho = shifted_union(e1.rho, e2.rho, std::size_t(alpha1), std::size_t(alpha1 + h2.rows()));
+  return out;
+}
+
+// reference src/jobs.cpp:160-187
+EchResult combine_vertical(const FieldSpec& f, const Mat& h2, const EchResult& e1,
+                           std::int64_t beta1, std::size_t thr) {
+  auto [h2_sel, h2_rest] = rex(h2, e1.rho);
+  const Mat x = mul(f, e1.M, h2_sel);
+  const Mat h2_clean = mad(f, h2_rest, e1.K, h2_sel);
+  const EchResult e2 = ech(f, h2_clean, thr);
+  auto [rho, u] = unh(e1.rho, e2.rho);
+  auto [k1_sel, k1_rest] = rex(e1.K, e2.rho);
+  const Mat g = mul(f, e2.M, k1_sel);
+  auto [x_piv, x_rest] = cex(x, e2.gamma);
+  EchResult out;
+  out.rho = std::move(rho);
+  out.gamma = shifted_union(e1.gamma, e2.gamma, std::size_t(beta1), std::size_t(beta1 + h2.cols()));
+  out.M = col_riffle(u, vcat(mad(f, e1.M, x_piv, g), g), vcat(mul(f, x_piv, e2.M), e2.M));
+  out.R = vcat(hcat(e1.R, mad(f, x_rest, x_piv, e2.R)),
+               hcat(Mat::zeros(std::int64_t(e2.rho.size()), e1.R.cols()), e2.R));
+  out.K = col_riffle(u, mad(f, k1_rest, e2.K, k1_sel), e2.K);
+  return out;
+}
+
+}  // namespace
+
+EchResult ech(const FieldSpec& f, const Mat& h, std::size_t threshold) {
+  if (threshold < 1) threshold = 1;
+  const std::int64_t alpha = h.rows(), beta = h.cols();
+  if (alpha == 0 || beta == 0) {
+    EchResult e;
+    e.M = Mat(0, 0);
+    e.K = Mat(alpha, 0);
+    e.R = Mat(0, beta);
+    e.rho = IndexSet(std::size_t(alpha), {});
+    e.gamma = IndexSet(std::size_t(beta), {});
+    return e;
+  }
+  const std::int64_t base = std::int64_t(std::min(threshold, ech_base()));
+  if (alpha <= base && beta <= base) return direct_ech(f, h);
+  if (alpha >= beta) {
+    const std::int64_t alpha1 = split_of(alpha);
+    const EchResult e1 = ech(f, h.row_view(0, alpha1), threshold);
+    return combine_horizontal(f, h.row_view(alpha1, alpha - alpha1), e1, alpha1, threshold);
+  }
+  const std::int64_t beta1 = split_of(beta);
+  const EchResult e1 = ech(f, h.col_view(0, beta1), threshold);
+  return combine_vertical(f, h.col_view(beta1, beta - beta1), e1, beta1, threshold);
+}
+
+}  // namespace gfq

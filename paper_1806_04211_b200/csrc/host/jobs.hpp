@@ -1,0 +1,46 @@
+// jobs.hpp -- the atomic block jobs of the Chief (reference
+// include/gfrref/jobs.hpp:37-82 and the matrix helpers of
+// include/gfrref/matrix.hpp:90-109), on device-resident u8 blocks.
+//
+// Every job takes const& inputs and returns fresh values (reference
+// SPEC.md:130); work is enqueued on gfq::cur_stream().  Shape errors throw
+// std::invalid_argument with the reference's messages.
+#pragma once
+
+#include <utility>
+
+#include "types.hpp"
+
+namespace gfq {
+
+Mat cpy(const Mat& a);                                             // jobs.hpp:37
+Mat mul(const FieldSpec& f, const Mat& b, const Mat& c);           // jobs.hpp:40
+Mat mad(const FieldSpec& f, const Mat& a, const Mat& b, const Mat& c);  // jobs.hpp:43
+Mat mat_mul(const FieldSpec& f, const Mat& b, const Mat& c);       // matrix.hpp:90
+Mat mat_mul_add(const FieldSpec& f, const Mat& a, const Mat& b, const Mat& c);  // matrix.hpp:93
+
+/// Negative reduced echelonisation of one block (jobs.hpp:50).  Same
+/// recursion as the reference (split the longer dimension, combine), base
+/// case = the single-CTA K2 kernel.  The outputs are canonical,
+/// so `threshold` only moves the recursion/base boundary.
+EchResult ech(const FieldSpec& f, const Mat& h, std::size_t threshold = 256);
+
+std::pair<Mat, Mat> cex(const Mat& h, const IndexSet& gamma);      // jobs.hpp:53
+std::pair<Mat, Mat> rex(const Mat& h, const IndexSet& rho);        // jobs.hpp:56
+std::pair<IndexSet, BitString> unh(const IndexSet& rho1, const IndexSet& rho2);  // :61
+std::pair<IndexSet, BitString> un0(const IndexSet& rho2);          // :64
+BitString mkr(const IndexSet& rho1, const IndexSet& rho2);         // :68
+Mat rrf(const BitString& u, const Mat& b, const Mat& c);           // :72
+Mat crz(const Mat& m, const BitString& lambda, std::size_t out_cols);  // :77
+Mat adi(const Mat& k, const BitString& delta);                     // :82
+
+Mat take_rows(const Mat& m, const std::vector<std::uint32_t>& rows);  // matrix.hpp:100
+Mat take_cols(const Mat& m, const std::vector<std::uint32_t>& cols);  // matrix.hpp:103
+Mat vcat(const Mat& a, const Mat& b);                                 // matrix.hpp:106
+Mat hcat(const Mat& a, const Mat& b);                                 // matrix.hpp:109
+
+/// Tunable: largest block the K2 base-case kernel takes (<= kEchBaseMax).
+void set_ech_base(std::size_t n);
+std::size_t ech_base();
+
+}  // namespace gfq

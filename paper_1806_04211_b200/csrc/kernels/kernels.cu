@@ -1,0 +1,429 @@
+// kernels.cu -- SIMT kernels of the GF(p) path for sm_100a:
+//   K1 (small-K SIMT contraction, the K<=~32 class of UpdateRow / ClearDown),
+//   K3/K4 (row/column gather, riffle, zero-riffle, identity planting),
+//   K2 base case (single-CTA Gauss-Jordan ECH in shared memory),
+//   K6 (counter-form SplitMix64 generator).
+// The tensor-core contraction lives in gf_mad_tc.cu.
+#include <atomic>
+
+#include "../common.hpp"
+#include "kernels.hpp"
+
+namespace gfq::dev {
+
+// ------------------------------------------------------------------ helpers
+// x mod p for any 32-bit x: q_est = floor(x * ceil(2^32/p) / 2^32) is q or q+1.
+__device__ __forceinline__ std::uint32_t modp(std::uint32_t x, std::uint32_t p,
+                                              std::uint32_t magic) {
+  const std::uint32_t q = __umulhi(x, magic);
+  const std::int32_t r = static_cast<std::int32_t>(x - q * p);
+  return static_cast<std::uint32_t>(r < 0 ? r + static_cast<std::int32_t>(p) : r);
+}
+
+static inline std::uint32_t magic_of(std::uint32_t p) {
+  return static_cast<std::uint32_t>((0x100000000ULL / p) + 1);
+}
+
+// Largest K chunk for which sum_{t<k} (p-1)^2 + (p-1) stays below 2^31.
+static inline std::int64_t k_chunk_limit(std::uint32_t p) {
+  const std::uint64_t sq = std::uint64_t(p - 1) * (p - 1);
+  if (sq == 0) return std::int64_t(1) << 40;
+  const std::uint64_t lim = (0x7FFFFFFFULL - p) / sq;
+  return static_cast<std::int64_t>(lim / 128 * 128 > 0 ? lim / 128 * 128 : lim);
+}
+
+// ------------------------------------------------------------------ K1 SIMT
+namespace {
+constexpr int kTm = 64, kTn = 64, kTk = 32;
+
+__global__ void __launch_bounds__(256)
+mad_simt_kernel(std::uint32_t p, std::uint32_t magic, int m, int n, int k,
+                const std::uint8_t* __restrict__ A, std::int64_t lda,
+                const std::uint8_t* __restrict__ B, std::int64_t ldb,
+                const std::uint8_t* Cin, std::int64_t ldc, std::uint8_t* D,
+                std::int64_t ldd) {
+  __shared__ std::uint8_t As[kTm][kTk + 4];
+  __shared__ std::uint8_t Bs[kTk][kTn + 4];
+  const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
+  const int m0 = blockIdx.y * kTm, n0 = blockIdx.x * kTn;
+  std::uint32_t acc[4][4] = {};
+  for (int k0 = 0; k0 < k; k0 += kTk) {
+    // 64x32 A tile and 32x64 B tile, 8 bytes per thread each.
+    for (int e = threadIdx.x; e < kTm * kTk; e += 256) {
+      const int r = e / kTk, c = e % kTk;
+      const int gr = m0 + r, gc = k0 + c;
+      As[r][c] = (gr < m && gc < k) ? A[std::int64_t(gr) * lda + gc] : 0;
+    }
+    for (int e = threadIdx.x; e < kTk * kTn; e += 256) {
+      const int r = e / kTn, c = e % kTn;
+      const int gr = k0 + r, gc = n0 + c;
+      Bs[r][c] = (gr < k && gc < n) ? B[std::int64_t(gr) * ldb + gc] : 0;
+    }
+    __syncthreads();
+#pragma unroll 8
+    for (int kk = 0; kk < kTk; ++kk) {
+      std::uint32_t a[4], b[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) a[i] = As[ty + 16 * i][kk];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) b[j] = Bs[kk][tx + 16 * j];
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc[i][j] += a[i] * b[j];
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int gr = m0 + ty + 16 * i;
+    if (gr >= m) continue;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int gc = n0 + tx + 16 * j;
+      if (gc >= n) continue;
+      std::uint32_t v = acc[i][j];
+      if (Cin) v += Cin[std::int64_t(gr) * ldc + gc];
+      D[std::int64_t(gr) * ldd + gc] = static_cast<std::uint8_t>(modp(v, p, magic));
+    }
+  }
+}
+
+// D = Cin (or 0) for the k == 0 contraction.
+__global__ void copy_or_zero_kernel(int m, int n, const std::uint8_t* Cin,
+                                    std::int64_t ldc, std::uint8_t* D,
+                                    std::int64_t ldd) {
+  for (int r = blockIdx.y; r < m; r += gridDim.y)
+    for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < n;
+         c += gridDim.x * blockDim.x)
+      D[std::int64_t(r) * ldd + c] = Cin ? Cin[std::int64_t(r) * ldc + c] : 0;
+}
+}  // namespace
+
+void mad_simt(std::uint32_t p, std::int64_t m, std::int64_t n, std::int64_t k,
+              const std::uint8_t* A, std::int64_t lda, const std::uint8_t* B,
+              std::int64_t ldb, const std::uint8_t* Cin, std::int64_t ldc,
+              std::uint8_t* D, std::int64_t ldd, cudaStream_t s) {
+  if (m == 0 || n == 0) return;
+  if (k == 0) {
+    dim3 grid(unsigned((n + 255) / 256), unsigned(m < 65535 ? m : 65535));
+    copy_or_zero_kernel<<<grid, 256, 0, s>>>(int(m), int(n), Cin, ldc, D, ldd);
+    GFQ_CUDA(cudaGetLastError());
+    return;
+  }
+  const std::int64_t kc = k_chunk_limit(p);
+  const std::uint32_t mg = magic_of(p);
+  for (std::int64_t k0 = 0; k0 < k; k0 += kc) {
+    const std::int64_t kk = (k - k0) < kc ? (k - k0) : kc;
+    const std::uint8_t* cin = k0 == 0 ? Cin : D;
+    const std::int64_t ldcin = k0 == 0 ? ldc : ldd;
+    for (std::int64_t m0 = 0; m0 < m; m0 += std::int64_t(65535) * kTm) {
+      const std::int64_t mm = (m - m0) < std::int64_t(65535) * kTm ? (m - m0) : std::int64_t(65535) * kTm;
+      dim3 grid(unsigned((n + kTn - 1) / kTn), unsigned((mm + kTm - 1) / kTm));
+      mad_simt_kernel<<<grid, 256, 0, s>>>(
+          p, mg, int(mm), int(n), int(kk), A + m0 * lda + k0, lda, B + k0 * ldb, ldb,
+          cin ? cin + m0 * ldcin : nullptr, ldcin, D + m0 * ldd, ldd);
+      GFQ_CUDA(cudaGetLastError());
+    }
+  }
+}
+
+namespace {
+std::atomic<int> g_policy{0};
+std::atomic<std::int64_t> g_simt{0}, g_tc{0};
+}  // namespace
+
+void set_mad_policy(int policy) { g_policy = policy; }
+int mad_policy() { return g_policy; }
+void mad_counters(std::int64_t* simt, std::int64_t* tc) {
+  *simt = g_simt;
+  *tc = g_tc;
+}
+void reset_mad_counters() {
+  g_simt = 0;
+  g_tc = 0;
+}
+
+void mad(std::uint32_t p, std::int64_t m, std::int64_t n, std::int64_t k,
+         const std::uint8_t* A, std::int64_t lda, const std::uint8_t* B,
+         std::int64_t ldb, const std::uint8_t* Cin, std::int64_t ldc,
+         std::uint8_t* D, std::int64_t ldd, cudaStream_t s) {
+  if (m == 0 || n == 0) return;
+  const int pol = g_policy;
+  // The tcgen05 path pays a prologue (TMEM alloc, barrier init, descriptor
+  // fetch) of a few microseconds; below ~4 Mi MACs or for K < 32 (one MMA
+  // instruction) the SIMT kernel is as fast and exactly as exact.
+  const bool big = k >= 32 && (double(m) * double(n) * double(k) >= 4.0 * 1024 * 1024);
+  if (pol != 1 && k > 0 && (pol == 2 || big)) {
+    if (mad_tc(p, m, n, k, A, lda, B, ldb, Cin, ldc, D, ldd, s)) {
+      ++g_tc;
+      return;
+    }
+  }
+  ++g_simt;
+  mad_simt(p, m, n, k, A, lda, B, ldb, Cin, ldc, D, ldd, s);
+}
+
+// ------------------------------------------------------------------ K3/K4
+namespace {
+__device__ __forceinline__ const std::uint8_t* pick_row(
+    const std::uint8_t* A, std::int64_t lda, const std::uint8_t* B,
+    std::int64_t ldb, const std::int32_t* rmap, std::int64_t i, bool& fromB) {
+  if (!rmap) {
+    fromB = false;
+    return A + i * lda;
+  }
+  const std::int32_t v = rmap[i];
+  if (v == -1) return nullptr;
+  if (v >= 0) {
+    fromB = false;
+    return A + std::int64_t(v) * lda;
+  }
+  fromB = true;
+  return B + std::int64_t(-v - 2) * ldb;
+}
+
+// Row-only select, 16-byte vectorised (all pointers/strides 16B-aligned).
+__global__ void select_rows_v16_kernel(std::uint8_t* dst, std::int64_t ldd,
+                                       std::int64_t rows, std::int64_t cols,
+                                       const std::uint8_t* A, std::int64_t lda,
+                                       const std::uint8_t* B, std::int64_t ldb,
+                                       const std::int32_t* rmap) {
+  const std::int64_t nvec = (cols + 15) / 16;
+  for (std::int64_t i = blockIdx.y; i < rows; i += gridDim.y) {
+    bool fromB = false;
+    const std::uint8_t* src = pick_row(A, lda, B, ldb, rmap, i, fromB);
+    uint4* drow = reinterpret_cast<uint4*>(dst + i * ldd);
+    for (std::int64_t v = blockIdx.x * blockDim.x + threadIdx.x; v < nvec;
+         v += std::int64_t(gridDim.x) * blockDim.x) {
+      if (v * 16 + 16 <= cols) {
+        drow[v] = src ? reinterpret_cast<const uint4*>(src)[v] : make_uint4(0, 0, 0, 0);
+      } else {
+        for (std::int64_t c = v * 16; c < cols; ++c)
+          dst[i * ldd + c] = src ? src[c] : 0;
+      }
+    }
+  }
+}
+
+__global__ void select2d_kernel(std::uint8_t* dst, std::int64_t ldd,
+                                std::int64_t rows, std::int64_t cols,
+                                const std::uint8_t* A, std::int64_t lda,
+                                const std::uint8_t* B, std::int64_t ldb,
+                                const std::int32_t* rmap,
+                                const std::int32_t* cmap) {
+  for (std::int64_t i = blockIdx.y; i < rows; i += gridDim.y) {
+    std::int32_t rv = -3;  // "no row map"
+    if (rmap) rv = rmap[i];
+    for (std::int64_t j = blockIdx.x * blockDim.x + threadIdx.x; j < cols;
+         j += std::int64_t(gridDim.x) * blockDim.x) {
+      std::uint8_t out = 0;
+      const std::int32_t cv = cmap ? cmap[j] : std::int32_t(j);
+      if (rv != -1 && cv != -1) {
+        const bool rowB = rmap && rv <= -2;
+        const bool colB = cmap && cv <= -2;
+        const std::int64_t r = rmap ? (rowB ? -rv - 2 : rv) : i;
+        const std::int64_t c = colB ? -cv - 2 : cv;
+        out = (rowB || colB) ? B[r * ldb + c] : A[r * lda + c];
+      }
+      dst[i * ldd + j] = out;
+    }
+  }
+}
+
+__global__ void set_entries_kernel(std::uint8_t* dst, std::int64_t ldd,
+                                   const std::int32_t* pos, std::int64_t n,
+                                   std::uint8_t value) {
+  for (std::int64_t q = blockIdx.x * blockDim.x + threadIdx.x; q < n;
+       q += std::int64_t(gridDim.x) * blockDim.x)
+    dst[std::int64_t(pos[2 * q]) * ldd + pos[2 * q + 1]] = value;
+}
+}  // namespace
+
+void select2d(std::uint8_t* dst, std::int64_t ldd, std::int64_t rows,
+              std::int64_t cols, const std::uint8_t* A, std::int64_t lda,
+              const std::uint8_t* B, std::int64_t ldb, const std::int32_t* rmap,
+              const std::int32_t* cmap, cudaStream_t s) {
+  if (rows == 0 || cols == 0) return;
+  const unsigned gy = unsigned(rows < 65535 ? rows : 65535);
+  const auto al = [](const void* ptr, std::int64_t ld) {
+    return ptr == nullptr ||
+           ((reinterpret_cast<std::uintptr_t>(ptr) & 15) == 0 && (ld & 15) == 0);
+  };
+  if (!cmap && al(dst, ldd) && al(A, lda) && al(B, ldb)) {
+    const std::int64_t nvec = (cols + 15) / 16;
+    const unsigned gx = unsigned((nvec + 127) / 128);
+    select_rows_v16_kernel<<<dim3(gx, gy), 128, 0, s>>>(dst, ldd, rows, cols, A, lda, B, ldb, rmap);
+  } else {
+    const unsigned gx = unsigned((cols + 255) / 256);
+    select2d_kernel<<<dim3(gx, gy), 256, 0, s>>>(dst, ldd, rows, cols, A, lda, B, ldb, rmap, cmap);
+  }
+  GFQ_CUDA(cudaGetLastError());
+}
+
+void set_entries(std::uint8_t* dst, std::int64_t ldd, const std::int32_t* pos,
+                 std::int64_t n, std::uint8_t value, cudaStream_t s) {
+  if (n == 0) return;
+  set_entries_kernel<<<unsigned((n + 255) / 256), 256, 0, s>>>(dst, ldd, pos, n, value);
+  GFQ_CUDA(cudaGetLastError());
+}
+
+// ------------------------------------------------------------------ K2 base
+namespace {
+__device__ __forceinline__ std::uint32_t powmod(std::uint32_t a, std::uint32_t e,
+                                                std::uint32_t p) {
+  std::uint32_t r = 1, b = a % p;
+  while (e) {
+    if (e & 1) r = (r * b) % p;
+    b = (b * b) % p;
+    e >>= 1;
+  }
+  return r;
+}
+
+// One CTA.  Shared layout: w[rows][cols] | t[rows][rmax] | coef[rows] |
+// piv[rows] | inv[256].  Column-wise Gauss-Jordan, pivot = first
+// non-pivotal row with a nonzero entry (reference src/chief.cpp:436-460;
+// equivalent to direct_gauss's row-wise rule).
+__global__ void __launch_bounds__(1024)
+ech_base_kernel(std::uint32_t p, std::uint32_t magic, int rows, int cols,
+                const std::uint8_t* __restrict__ H, std::int64_t ldh,
+                std::uint8_t* W, std::int64_t ldw, std::uint8_t* Tc,
+                std::int64_t ldt, std::int32_t* info) {
+  extern __shared__ __align__(16) std::uint8_t sm[];
+  const int rmax = rows < cols ? rows : cols;
+  std::uint8_t* w = sm;
+  std::uint8_t* t = w + rows * cols;
+  std::uint8_t* coef = t + rows * (rmax > 0 ? rmax : 1);
+  std::uint8_t* piv = coef + rows;
+  std::uint8_t* invt = piv + rows;
+  __shared__ int sel_s;
+  __shared__ int pcol[kEchBaseMax], prow[kEchBaseMax];
+  const int tid = threadIdx.x, nt = blockDim.x;
+  const int warp = tid >> 5, lane = tid & 31, nw = nt >> 5;
+
+  for (int e = tid; e < rows * cols; e += nt)
+    w[e] = H[std::int64_t(e / cols) * ldh + (e % cols)];
+  for (int e = tid; e < rows * rmax; e += nt) t[e] = 0;
+  for (int e = tid; e < rows; e += nt) piv[e] = 0;
+  for (int a = tid; a < 256; a += nt)
+    invt[a] = (a > 0 && std::uint32_t(a) < p) ? std::uint8_t(powmod(a, p - 2, p)) : 0;
+  __syncthreads();
+
+  int r = 0;
+  for (int col = 0; col < cols && r < rmax; ++col) {
+    if (tid == 0) sel_s = rows;
+    __syncthreads();
+    for (int i = tid; i < rows; i += nt)
+      if (!piv[i] && w[i * cols + col]) atomicMin(&sel_s, i);
+    __syncthreads();
+    const int s = sel_s;
+    if (s == rows) continue;  // block-uniform
+    const std::uint32_t scale = p - invt[w[s * cols + col]];
+    for (int i = tid; i < rows; i += nt) coef[i] = (i == s) ? 0 : w[i * cols + col];
+    __syncthreads();
+    // normalise the pivot row: pivot entry becomes -1
+    const int wcols = cols - col;
+    for (int c = tid; c < wcols; c += nt)
+      w[s * cols + col + c] = std::uint8_t(modp(scale * w[s * cols + col + c], p, magic));
+    for (int q = tid; q <= r; q += nt)
+      t[s * rmax + q] = q == r ? std::uint8_t(scale)
+                               : std::uint8_t(modp(scale * t[s * rmax + q], p, magic));
+    __syncthreads();
+    // eliminate column `col` from every other row (Gauss-Jordan)
+    const int width = wcols + r + 1;
+    for (int i = warp; i < rows; i += nw) {
+      const std::uint32_t cf = coef[i];
+      if (!cf) continue;
+      for (int e = lane; e < width; e += 32) {
+        if (e < wcols) {
+          const int idx = i * cols + col + e;
+          const std::uint32_t b = w[s * cols + col + e];
+          w[idx] = p == 2 ? std::uint8_t(w[idx] ^ b)
+                          : std::uint8_t(modp(w[idx] + cf * b, p, magic));
+        } else {
+          const int q = e - wcols;
+          const int idx = i * rmax + q;
+          const std::uint32_t b = t[s * rmax + q];
+          t[idx] = p == 2 ? std::uint8_t(t[idx] ^ b)
+                          : std::uint8_t(modp(t[idx] + cf * b, p, magic));
+        }
+      }
+    }
+    if (tid == 0) {
+      piv[s] = 1;
+      pcol[r] = col;
+      prow[r] = s;
+    }
+    ++r;
+    __syncthreads();
+  }
+  for (int e = tid; e < rows * cols; e += nt)
+    W[std::int64_t(e / cols) * ldw + (e % cols)] = w[e];
+  if (r > 0)
+    for (int e = tid; e < rows * r; e += nt)
+      Tc[std::int64_t(e / r) * ldt + (e % r)] = t[(e / r) * rmax + (e % r)];
+  if (tid == 0) info[0] = r;
+  for (int q = tid; q < r; q += nt) {
+    info[1 + q] = pcol[q];
+    info[1 + rmax + q] = prow[q];
+  }
+}
+}  // namespace
+
+void ech_base(std::uint32_t p, std::int64_t rows, std::int64_t cols,
+              const std::uint8_t* H, std::int64_t ldh, std::uint8_t* W,
+              std::int64_t ldw, std::uint8_t* Tc, std::int64_t ldt,
+              std::int32_t* info, cudaStream_t s) {
+  if (rows > kEchBaseMax || cols > kEchBaseMax)
+    throw std::invalid_argument("ech_base: block exceeds the base-case size");
+  const std::int64_t rmax = rows < cols ? rows : cols;
+  const std::size_t smem = std::size_t(rows * cols + rows * (rmax > 0 ? rmax : 1) + 2 * rows + 256);
+  static bool attr_set = false;
+  if (!attr_set) {
+    GFQ_CUDA(cudaFuncSetAttribute(ech_base_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  64 * 1024));
+    attr_set = true;
+  }
+  int threads = int(rows * 32);
+  threads = threads < 64 ? 64 : (threads > 1024 ? 1024 : threads);
+  ech_base_kernel<<<1, threads, smem, s>>>(p, magic_of(p), int(rows), int(cols), H, ldh, W, ldw,
+                                           Tc, ldt, info);
+  GFQ_CUDA(cudaGetLastError());
+}
+
+// ------------------------------------------------------------------ K6
+namespace {
+__global__ void random_fill_kernel(std::uint32_t p, std::int64_t rows,
+                                   std::int64_t cols, std::uint64_t seed,
+                                   std::uint64_t draw0, std::uint64_t limit,
+                                   std::uint8_t* dst, std::int64_t ldd,
+                                   std::uint32_t* rejects) {
+  for (std::int64_t r = blockIdx.y; r < rows; r += gridDim.y) {
+    for (std::int64_t c = blockIdx.x * blockDim.x + threadIdx.x; c < cols;
+         c += std::int64_t(gridDim.x) * blockDim.x) {
+      const std::uint64_t t = draw0 + std::uint64_t(r) * std::uint64_t(cols) + std::uint64_t(c);
+      std::uint64_t z = seed + (t + 1) * 0x9e3779b97f4a7c15ULL;
+      z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ULL;
+      z = (z ^ (z >> 27)) * 0x94d049bb133111ebULL;
+      z = z ^ (z >> 31);
+      if (z >= limit) atomicAdd(rejects, 1u);
+      dst[r * ldd + c] = p <= 1 ? 0 : std::uint8_t(z % p);
+    }
+  }
+}
+}  // namespace
+
+void random_fill(std::uint32_t p, std::int64_t rows, std::int64_t cols,
+                 std::uint64_t seed, std::uint64_t draw0, std::uint8_t* dst,
+                 std::int64_t ldd, std::uint32_t* rejects, cudaStream_t s) {
+  if (rows == 0 || cols == 0) return;
+  const std::uint64_t limit = p <= 1 ? ~0ULL : (~0ULL - (~0ULL % p));
+  const unsigned gx = unsigned((cols + 255) / 256 < 64 ? (cols + 255) / 256 : 64);
+  const unsigned gy = unsigned(rows < 65535 ? rows : 65535);
+  random_fill_kernel<<<dim3(gx, gy), 256, 0, s>>>(p, rows, cols, seed, draw0, limit, dst, ldd,
+                                                   rejects);
+  GFQ_CUDA(cudaGetLastError());
+}
+
+}  // namespace gfq::dev

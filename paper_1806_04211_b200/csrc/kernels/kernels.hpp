@@ -1,0 +1,80 @@
+// kernels.hpp -- launch wrappers for the sm_100a kernels of the GF(p) path.
+//
+// All matrices are u8 residues 0..p-1, row-major, with a row stride (ld) in
+// bytes.  Every wrapper is stream-ordered and returns immediately.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+namespace gfq::dev {
+
+// ---------------------------------------------------------------- K1
+// D = (Cin ? Cin : 0) + A.B mod p   (A: m x k, B: k x n, Cin/D: m x n).
+// Cin may alias D.  Dispatches to the tcgen05 kind::i8 kernel when the
+// operands are TMA-legal and the contraction is large enough, else to the
+// SIMT small-K kernel.  Exact for any k (K is split so the s32 accumulator
+// cannot overflow: (p-1)^2 * k_chunk < 2^31).
+void mad(std::uint32_t p, std::int64_t m, std::int64_t n, std::int64_t k,
+         const std::uint8_t* A, std::int64_t lda, const std::uint8_t* B,
+         std::int64_t ldb, const std::uint8_t* Cin, std::int64_t ldc,
+         std::uint8_t* D, std::int64_t ldd, cudaStream_t s);
+
+// Force a specific K1 implementation (tests / profiling).
+void mad_simt(std::uint32_t p, std::int64_t m, std::int64_t n, std::int64_t k,
+              const std::uint8_t* A, std::int64_t lda, const std::uint8_t* B,
+              std::int64_t ldb, const std::uint8_t* Cin, std::int64_t ldc,
+              std::uint8_t* D, std::int64_t ldd, cudaStream_t s);
+// Returns false (launching nothing) when the operands are not TMA-legal.
+bool mad_tc(std::uint32_t p, std::int64_t m, std::int64_t n, std::int64_t k,
+            const std::uint8_t* A, std::int64_t lda, const std::uint8_t* B,
+            std::int64_t ldb, const std::uint8_t* Cin, std::int64_t ldc,
+            std::uint8_t* D, std::int64_t ldd, cudaStream_t s);
+
+// Selects which path `mad` uses: 0 = auto, 1 = SIMT only, 2 = tcgen05 whenever legal.
+void set_mad_policy(int policy);
+int mad_policy();
+// Counters of K1 launches by path since the last reset (host-side).
+void mad_counters(std::int64_t* simt, std::int64_t* tc);
+void reset_mad_counters();
+
+// ---------------------------------------------------------------- K3/K4
+// dst[i][j] = source element chosen by the row map and the column map:
+//   rmap[i] >= 0 -> row rmap[i] of A;  rmap[i] <= -2 -> row (-rmap[i]-2) of B;
+//   rmap[i] == -1 -> zero row.  rmap == nullptr -> row i of A.
+//   cmap[j] likewise for columns (-1 = zero column, <= -2 = column of B).
+// Maps are device arrays.  Used for take_rows/take_cols, cex/rex, rrf,
+// crz, hcat/vcat and the column riffle.
+void select2d(std::uint8_t* dst, std::int64_t ldd, std::int64_t rows,
+              std::int64_t cols, const std::uint8_t* A, std::int64_t lda,
+              const std::uint8_t* B, std::int64_t ldb, const std::int32_t* rmap,
+              const std::int32_t* cmap, cudaStream_t s);
+
+// dst[pos[2q]][pos[2q+1]] = value for q < n  (identity planting, adi).
+void set_entries(std::uint8_t* dst, std::int64_t ldd, const std::int32_t* pos,
+                 std::int64_t n, std::uint8_t value, cudaStream_t s);
+
+// ---------------------------------------------------------------- K2
+// Base-case ECH of a small block (rows, cols <= kEchBaseMax) in one CTA:
+// column-wise Gauss-Jordan with the reference's pivot rule (first
+// non-pivotal row with a nonzero entry) and -1 pivots.  Writes the reduced
+// block W (rows x cols), the compact transform Tc (rows x rank; column q =
+// coefficient on the q-th pivot row in discovery order) and
+// info = [rank, pivcol_0.., pivrow_0..] (2*min(rows,cols)+1 ints).
+constexpr int kEchBaseMax = 128;
+void ech_base(std::uint32_t p, std::int64_t rows, std::int64_t cols,
+              const std::uint8_t* H, std::int64_t ldh, std::uint8_t* W,
+              std::int64_t ldw, std::uint8_t* Tc, std::int64_t ldt,
+              std::int32_t* info, cudaStream_t s);
+
+// ---------------------------------------------------------------- K6
+// Counter-form SplitMix64: entry e (row-major over rows x cols) takes draw
+// index draw0 + e of the stream `seed` and is reduced mod p.  Draws that
+// the reference's rejection rule would reject are counted in *rejects
+// (device counter) so the caller can replay exactly.
+void random_fill(std::uint32_t p, std::int64_t rows, std::int64_t cols,
+                 std::uint64_t seed, std::uint64_t draw0, std::uint8_t* dst,
+                 std::int64_t ldd, std::uint32_t* rejects, cudaStream_t s);
+
+}  // namespace gfq::dev

@@ -1,0 +1,191 @@
+"""GPU parity of the full echelonize path (ChopMatrix -> Steps 1-3 on the
+CUDA stream DAG -> EchelonOutput) against the reference and the oracle.
+
+Bit-exact on rank, pivot columns (upsilon), selected rows (varrho), every R /
+T_M / T_K block and the materialised transformation; plus the
+size-independent defining identity T.C = [[-1, R], [0, 0]] at sizes where
+the scalar oracle is too slow.
+"""
+import numpy as np
+import pytest
+
+import oracle
+from oracle import restate as R
+from gfq_testutil import arr
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def G():
+    from paper_1806_04211_b200 import gfrref
+    gfrref.lib()
+    return gfrref
+
+
+def compare(out, want, with_transform=True):
+    """out: gfrref.EchelonOutput (device); want: restate.Output or ref fixture dict."""
+    if isinstance(want, dict):
+        assert out.rank == want["rank"]
+        assert [list(s.members) for s in out.upsilon] == want["upsilon"]
+        assert [list(s.members) for s in out.varrho] == want["varrho"]
+        for key, v in want["R"].items():
+            j, l = map(int, key.split(","))
+            np.testing.assert_array_equal(out.block(0, j, l).numpy(), arr(v))
+        np.testing.assert_array_equal(out.assembled_R().numpy(),
+                                      np.array(want["assembled_R"], np.uint8).reshape(out.rank, -1))
+        if with_transform:
+            for key, v in want["TM"].items():
+                j, h = map(int, key.split(","))
+                np.testing.assert_array_equal(out.block(1, j, h).numpy(), arr(v))
+            for key, v in want["TK"].items():
+                i, h = map(int, key.split(","))
+                np.testing.assert_array_equal(out.block(2, i, h).numpy(), arr(v))
+            np.testing.assert_array_equal(out.materialize_transform().numpy(), np.array(want["T"], np.uint8))
+        return
+    assert out.rank == want.rank
+    assert [s.members for s in out.upsilon] == [s.members for s in want.upsilon]
+    assert [s.members for s in out.varrho] == [s.members for s in want.varrho]
+    b, a = len(want.col_parts), len(want.row_parts)
+    for j in range(b):
+        for l in range(j, b):
+            np.testing.assert_array_equal(out.block(0, j, l).numpy(), want.R_blocks[(j, l)])
+    if with_transform:
+        for j in range(b):
+            for h in range(a):
+                np.testing.assert_array_equal(out.block(1, j, h).numpy(), want.T_M_blocks[(j, h)])
+        for i in range(a):
+            for h in range(i + 1):
+                np.testing.assert_array_equal(out.block(2, i, h).numpy(), want.T_K_blocks[(i, h)])
+        np.testing.assert_array_equal(out.materialize_transform().numpy(), want.materialize_transform())
+
+
+def test_paper_example(G, pinned):
+    C6 = arr(pinned["C6"])
+    want = pinned["C6_out"]
+    for threads in (1, 3):
+        out = G.echelonize(C6, G.FieldSpec(3), G.EchelonizeOptions(block=3, threads=threads, collect_trace=True))
+        assert out.rank == want["rank"]
+        assert [list(s.members) for s in out.upsilon] == want["upsilon"]
+        assert [list(s.members) for s in out.varrho] == want["varrho"]
+        for k, v in want["R"].items():
+            assert out.block(0, *map(int, k.split(","))) == arr(v)
+        for k, v in want["TM"].items():
+            assert out.block(1, *map(int, k.split(","))) == arr(v)
+        for k, v in want["TK"].items():
+            assert out.block(2, *map(int, k.split(","))) == arr(v)
+        assert out.assembled_R() == arr(want["assembled_R"])
+        assert out.materialize_transform() == arr(want["T"])
+        assert out.global_upsilon() == [0, 1, 2, 3, 5] and out.global_varrho() == [0, 1, 2, 3, 5]
+        tr = out.trace()
+        counts = {}
+        for t in tr:
+            counts[t["kind"]] = counts.get(t["kind"], 0) + 1
+        assert len(tr) == want["task_counts"]["total"]
+        for k, v in want["task_counts"].items():
+            if k != "total":
+                assert counts.get(k, 0) == v, k
+        # ClearDown details = new pivots per block column (test_chief.cpp:436-454)
+        per_col = {}
+        for t in tr:
+            if t["kind"] == "ClearDown":
+                per_col[t["j"]] = per_col.get(t["j"], 0) + t["detail"]
+        assert per_col == {0: 3, 1: 2}
+    lean = G.echelonize(C6, G.FieldSpec(3), G.EchelonizeOptions(block=3, with_transform=False, collect_trace=True))
+    assert len(lean.trace()) == want["task_counts_no_transform"]["total"]
+    assert lean.rank == 5 and lean.assembled_R() == arr(want["assembled_R"])
+
+
+def test_reference_run_fixtures(G, ref_runs):
+    for run in ref_runs["echelonize"]:
+        C = np.array(run["C"], np.uint8).reshape(run["m"], run["n"])
+        for threads in (1, 4):
+            out = G.echelonize(C, G.FieldSpec(run["p"]),
+                               G.EchelonizeOptions(block=run["block"], threads=threads,
+                                                   with_transform=run["with_transform"]))
+            compare(out, run, run["with_transform"])
+
+
+def test_identity_zero_and_empty(G):
+    idm = np.eye(6, dtype=np.uint8)
+    out = G.echelonize(idm, G.FieldSpec(3), G.EchelonizeOptions(block=2))
+    assert out.rank == 6
+    np.testing.assert_array_equal(out.materialize_transform().numpy(), 2 * np.eye(6, dtype=np.uint8))
+    z = np.zeros((4, 5), np.uint8)
+    out = G.echelonize(z, G.FieldSpec(5), G.EchelonizeOptions(block=2))
+    assert out.rank == 0
+    np.testing.assert_array_equal(out.materialize_transform().numpy(), np.eye(4, dtype=np.uint8))
+    for shape in [(0, 5), (5, 0), (0, 0)]:
+        out = G.echelonize(np.zeros(shape, np.uint8), G.FieldSpec(3), G.EchelonizeOptions(block=2))
+        assert out.rank == 0
+
+
+@pytest.mark.parametrize("p,m,n,block,kind", [
+    (2, 300, 300, 64, "random"), (3, 257, 301, 48, "random"), (7, 320, 256, 80, "product"),
+    (251, 200, 200, 50, "random"), (5, 190, 230, 37, "product"), (2, 256, 256, 256, "random"),
+])
+def test_random_vs_oracle(G, p, m, n, block, kind):
+    C = oracle.random_matrix(p, m, n, m + n) if kind == "random" else \
+        oracle.random_product_matrix(p, m, n, min(m, n) // 3, m + n)
+    out = G.echelonize(C, G.FieldSpec(p), G.EchelonizeOptions(block=block, threads=4))
+    compare(out, R.blocked_from_oracle(p, C, block))
+
+
+def test_block_size_and_thread_independence(G):
+    p = 5
+    C = oracle.random_matrix(p, 120, 120, 0xB10C)
+    base = G.echelonize(C, G.FieldSpec(p), G.EchelonizeOptions(block=120))
+    T0 = base.materialize_transform().numpy()
+    for block, threads in [(1, 1), (7, 2), (13, 4), (40, 8)]:
+        out = G.echelonize(C, G.FieldSpec(p), G.EchelonizeOptions(block=block, threads=threads))
+        assert out.rank == base.rank and out.global_upsilon() == base.global_upsilon()
+        assert out.assembled_R() == base.assembled_R()
+        np.testing.assert_array_equal(out.materialize_transform().numpy(), T0)
+
+
+def _identity_check(G, p, C, out):
+    """T.C == [[-1, R], [0, 0]] (reference src/chief.cpp:566-588), with T and
+    C on the device and the product on K1."""
+    f = G.FieldSpec(p)
+    T = out.materialize_transform()
+    P = G.mul(f, T, C).numpy()
+    r = out.rank
+    ups = out.global_upsilon()
+    rest = [c for c in range(C.cols if isinstance(C, G.Matrix) else C.shape[1]) if c not in set(ups)]
+    Rm = out.assembled_R().numpy()
+    want = np.zeros_like(P)
+    want[np.arange(r), ups] = p - 1
+    if rest:
+        want[:r][:, rest] = Rm
+    np.testing.assert_array_equal(P, want)
+
+
+@pytest.mark.skipif(oracle.ref is None, reason="oracle/_ref not built")
+def test_cfg1_vs_reference_library(G):
+    """configs[0]: GF(3) 2000x2000, block 500 -- bit-exact against the
+    reference's own blocked echelonize (oracle/_ref)."""
+    p, m, block = 3, 2000, 500
+    C = oracle.random_matrix(p, m, m, 1)
+    ref = oracle.ref_echelonize(p, C, block, threads=8)
+    Cd = G.random_matrix(G.FieldSpec(p), m, m, 1)
+    out = G.echelonize(Cd, G.FieldSpec(p), G.EchelonizeOptions(block=block, threads=4))
+    assert out.rank == ref.rank == 1999
+    for j in range(ref.b):
+        assert list(out.upsilon[j].members) == ref.upsilon(j).tolist()
+        for l in range(j, ref.b):
+            np.testing.assert_array_equal(out.block(0, j, l).numpy(), ref.block(0, j, l))
+        for h in range(ref.a):
+            np.testing.assert_array_equal(out.block(1, j, h).numpy(), ref.block(1, j, h))
+    for i in range(ref.a):
+        assert list(out.varrho[i].members) == ref.varrho(i).tolist()
+        for h in range(i + 1):
+            np.testing.assert_array_equal(out.block(2, i, h).numpy(), ref.block(2, i, h))
+    np.testing.assert_array_equal(out.materialize_transform().numpy(), ref.materialize_transform())
+
+
+@pytest.mark.parametrize("p,m,n,block", [(2, 2048, 2048, 256), (251, 1536, 1024, 512), (7, 1024, 1536, 256)])
+def test_defining_identity_medium(G, p, m, n, block):
+    C = G.random_matrix(G.FieldSpec(p), m, n, 77)
+    out = G.echelonize(C, G.FieldSpec(p), G.EchelonizeOptions(block=block, threads=4))
+    assert out.rank == min(m, n) or p == 2
+    _identity_check(G, p, C, out)
