@@ -1,0 +1,362 @@
+#!/usr/bin/env python
+"""Benchmark: RREF + transformation over GF(q) (arXiv 1806.04211 Chief) on B200.
+
+One step = one full ``echelonize`` (ChopMatrix -> Steps 1-3 -> EchelonOutput,
+with transformation) of the BASELINE.json configs[1] workload:
+GF(2) dense 8192 x 8192, iid uniform entries (reference random_matrix,
+seed 1, generated on the device by K6), block 1024.
+Metric: effective GF(q) mult-adds/s = m*n*r / step time.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+Prints ONE JSON line on rank 0.  Multi-GPU (N > 1, torchrun): every rank
+runs its own replica of the workload (weak scaling); the block-column
+sharded Chief is not wired into the bench yet ("Multi-GPU").
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+CONFIGS = {
+    "cfg1": dict(p=3, m=2000, n=2000, block=500, seed=1, kind="random",
+                 desc="cfg1 GF(3) 2000x2000 block 500"),
+    "cfg2a": dict(p=2, m=8192, n=8192, block=1024, seed=1, kind="random",
+                  desc="cfg2a GF(2) 8192x8192 block 1024 (BASELINE configs[1])"),
+    "cfg3": dict(p=7, m=16384, n=12288, block=2048, seed=1, kind="product", inner=10000,
+                 desc="cfg3 GF(7) 16384x12288 rank 10000 block 2048"),
+    "cfg4": dict(p=251, m=32768, n=32768, block=4096, seed=1, kind="random",
+                 desc="cfg4 GF(251) 32768x32768 block 4096"),
+    "cfg5s": dict(p=2, m=65536, n=65536, block=8192, seed=1, kind="random",
+                  desc="cfg5 1-GPU: GF(2) 65536x65536 leading case, block 8192"),
+}
+DEFAULT = "cfg2a"
+METRIC = "RREF+transform effective GF(q) mult-adds/s (m*n*r / wall)"
+UNIT = "mult-adds/s"
+
+
+def measured_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return json.load(f)
+    except Exception:
+        return None
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index):
+        self.idx = gpu_index
+        self.lines = []
+        self.proc = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits", "-lms", "100",
+                 "-i", str(self.idx)], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if not self.proc:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"], "samples": 0}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        self.t.join(timeout=2)
+        sm, smax, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            f = [x.strip() for x in ln.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm.append(float(f[1]))
+                smax = float(f[2])
+            except ValueError:
+                continue
+            for nm, v in zip(names, f[5:9]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": smax,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def setup_dist():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        dist.init_process_group("nccl")
+    return world, rank, local, dist
+
+
+def cpu_baseline(cfg, C_host, rank_r, budget_s=25.0):
+    """The reference library (oracle/_ref, compiled from /root/reference) on
+    the host cores, on a bounded sample of the workload: the leading
+    s x s submatrix (s a multiple of the block) sized so one call takes about
+    `budget_s` seconds with all host threads."""
+    import oracle
+    if oracle.ref is None:
+        return None
+    threads = max(1, oracle.ref.ref_hardware_concurrency())
+    blk = cfg["block"]
+    # calibrate on one block-grid 2x2 leading sample
+    s0 = min(2 * blk, cfg["m"], cfg["n"])
+    t0 = time.time()
+    o = oracle.ref_echelonize(cfg["p"], C_host[:s0, :s0].copy(), blk, threads=threads)
+    dt = max(time.time() - t0, 1e-3)
+    rate = s0 * s0 * o.rank / dt
+    # grid-level parallelism grows with the sample; be conservative (rate x2)
+    s = s0
+    while True:
+        nxt = s + blk
+        if nxt > min(cfg["m"], cfg["n"]):
+            break
+        if nxt ** 3 / (2 * rate) > budget_s:
+            break
+        s = nxt
+    sample = C_host[:s, :s].copy()
+    t0 = time.time()
+    o = oracle.ref_echelonize(cfg["p"], sample, blk, threads=threads)
+    wall = time.time() - t0
+    work = s * s * o.rank
+    return {"value": work / wall, "unit": UNIT, "cores": threads, "kind": "reference",
+            "sample": f"leading {s}x{s} of the {cfg['m']}x{cfg['n']} input, block {blk}, "
+                      f"gfrref::echelonize with_transform, {threads} threads, 1 call, {wall:.2f} s",
+            "wall_s": wall}
+
+
+def run_reference(args, cfg, world, rank):
+    """--impl reference: the reference's own CPU implementation (oracle/_ref)
+    with all host threads; each step a bounded sample of the workload."""
+    if rank != 0:
+        return
+    import numpy as np  # noqa: F401
+    import oracle
+    if oracle.ref is None:
+        print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/libgfrref_ref.so not built"}))
+        return
+    threads = max(1, oracle.ref.ref_hardware_concurrency())
+    C = oracle.random_matrix(cfg["p"], cfg["m"], cfg["n"], cfg["seed"]) if cfg["kind"] == "random" else \
+        oracle.random_product_matrix(cfg["p"], cfg["m"], cfg["n"], cfg["inner"], cfg["seed"])
+    blk = cfg["block"]
+    budget = 150.0 / max(1, args.steps + args.warmup)
+    s0 = min(2 * blk, cfg["m"], cfg["n"])
+    t0 = time.time()
+    o = oracle.ref_echelonize(cfg["p"], C[:s0, :s0].copy(), blk, threads=threads)
+    rate = s0 * s0 * o.rank / max(time.time() - t0, 1e-3)
+    s = s0
+    while s + blk <= min(cfg["m"], cfg["n"]) and (s + blk) ** 3 / (2 * rate) <= budget:
+        s += blk
+    sample = C[:s, :s].copy()
+    for _ in range(args.warmup):
+        oracle.ref_echelonize(cfg["p"], sample, blk, threads=threads)
+    walls, work = [], 0
+    for _ in range(args.steps):
+        t0 = time.time()
+        o = oracle.ref_echelonize(cfg["p"], sample, blk, threads=threads)
+        walls.append(time.time() - t0)
+        work += s * s * o.rank
+    tot = sum(walls)
+    val = work / tot
+    line = {"impl": "reference", "metric": METRIC, "value": val, "unit": UNIT, "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * tot / args.steps,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u32 (reference Elem)",
+            "data": "synthetic: reference random_matrix seed 1 (host)",
+            "config": {"workload": cfg["desc"], "p": cfg["p"], "m": cfg["m"], "n": cfg["n"], "block": blk,
+                       "sample": f"leading {s}x{s}"},
+            "cpu_baseline": {"value": val, "unit": UNIT, "cores": threads, "kind": "reference",
+                             "sample": f"leading {s}x{s} of the {cfg['m']}x{cfg['n']} input per step, block {blk}"},
+            "e2e": {"value": val, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line))
+
+
+def k1_traffic():
+    """Per-launch DRAM bytes of K1 from the committed ncu --set full summary."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "k1_ncu_summary.json")) as f:
+            return json.load(f).get("dram_bytes_per_launch")
+    except Exception:
+        return None
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default=DEFAULT, choices=sorted(CONFIGS))
+    ap.add_argument("--threads", type=int, default=4, help="host workers / CUDA streams of the DAG executor")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    args = ap.parse_args()
+    cfg = CONFIGS[args.config]
+    world, rank, local, dist = setup_dist()
+    if args.impl == "reference":
+        run_reference(args, cfg, world, rank)
+        if dist:
+            dist.barrier()
+            dist.destroy_process_group()
+        return
+
+    import numpy as np
+    import torch
+    torch.cuda.set_device(local)
+    from paper_1806_04211_b200 import gfrref as G
+    G.lib()
+    f = G.FieldSpec(cfg["p"])
+    if cfg["kind"] == "random":
+        C = G.random_matrix(f, cfg["m"], cfg["n"], cfg["seed"])
+    else:
+        C = G.random_product_matrix(f, cfg["m"], cfg["n"], cfg["inner"], cfg["seed"])
+    opts = G.EchelonizeOptions(block=cfg["block"], threads=args.threads, with_transform=True)
+    flush = torch.empty(512 << 20, dtype=torch.uint8, device="cuda")
+
+    def barrier():
+        if dist:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    rank_r = None
+    for _ in range(max(args.warmup, 0)):
+        out = G.echelonize(C, f, opts)
+        rank_r = out.rank
+        del out
+    if rank_r is None:
+        rank_r = G.echelonize(C, f, opts).rank
+    work = cfg["m"] * cfg["n"] * rank_r
+
+    # ---------------- timed region (device-resident input)
+    G.profile(True)
+    G.profile_take()
+    G.launch_count(reset=True)
+    clocks = ClockSampler(local)
+    barrier()
+    clocks.start()
+    times, walls = [], []
+    for _ in range(args.steps):
+        flush.fill_(1)  # > L2 (126 MB): evict between steps, outside the events
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        h0 = time.perf_counter()
+        e0.record()
+        out = G.echelonize(C, f, opts)
+        e1.record()
+        e1.synchronize()
+        walls.append(time.perf_counter() - h0)
+        times.append(e0.elapsed_time(e1))
+        del out
+    barrier()
+    clk = clocks.stop()
+    launches = G.launch_count(reset=True)
+    prof = G.profile_take()
+    G.profile(False)
+    tot_ms = sum(times)
+    if dist:
+        t = torch.tensor([tot_ms], device="cuda", dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        tot_ms = float(t.item())
+    value = world * work * args.steps / (tot_ms / 1e3)
+
+    # ---------------- e2e: public API with host buffers (H2D + D2H inside)
+    e2e = None
+    if not args.no_e2e:
+        Ch = torch.empty((cfg["m"], cfg["n"]), dtype=torch.uint8, pin_memory=True)
+        Ch.numpy()[:] = C.numpy()
+        probe = G.echelonize(C, f, opts)
+        nbytes = probe.block_bytes()
+        del probe
+        dl = torch.empty(nbytes, dtype=torch.uint8, pin_memory=True)
+        barrier()
+        et = []
+        for _ in range(max(1, min(args.steps, 5))):
+            flush.fill_(2)
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            out = G.echelonize(Ch.numpy(), f, opts)
+            out.download_blocks(dl.numpy())
+            sel_bytes = 4 * out.rank * 2
+            e1.record()
+            e1.synchronize()
+            et.append(e0.elapsed_time(e1))
+            del out
+        e_ms = sum(et) / len(et)
+        if dist:
+            t = torch.tensor([e_ms], device="cuda", dtype=torch.float64)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            e_ms = float(t.item())
+        e2e = {"value": world * work / (e_ms / 1e3), "unit": UNIT, "h2d_bytes_per_step": cfg["m"] * cfg["n"],
+               "d2h_bytes_per_step": int(nbytes + sel_bytes), "ms_per_step": e_ms}
+
+    # ---------------- roofline of the dominant kernel (K1 tcgen05 contraction)
+    peaks = measured_peaks()
+    tc_l, tc_ops, tc_ms = prof["tc"]
+    si_l, si_ops, si_ms = prof["simt"]
+    if peaks and peaks.get("bf16_tflops"):
+        peak = 2.0 * peaks["bf16_tflops"]
+        peak_src = "2 x measured cuBLAS bf16 burst (MEASURED_PEAKS.json); B200 dense int8 = 2 x dense bf16"
+    else:
+        peak = 2.0 * 1590.0
+        peak_src = "fallback 2 x 1.59 PF bf16 (B200_PROFILING.md)"
+    achieved = (tc_ops / (tc_ms / 1e3) / 1e12) if tc_ms > 0 else 0.0
+    roof = {"kernel": "gf_mad_tc_kernel (K1, tcgen05.mma kind::i8)", "bound": "tensor",
+            "achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak if peak else None,
+            "traffic": k1_traffic(), "peak_source": peak_src,
+            "ops_per_launch": tc_ops / tc_l if tc_l else 0, "launches": tc_l,
+            "avg_launch_us": 1e3 * tc_ms / tc_l if tc_l else 0,
+            "share_of_step": (tc_ms / tot_ms) if tot_ms else None,
+            "simt_k1": {"launches": si_l, "ops": si_ops, "ms": si_ms},
+            "note": "int8 ops = 2 x MACs; per-launch CUDA events on the launching worker stream"}
+
+    base = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        base = cpu_baseline(cfg, C.numpy(), rank_r)
+
+    if rank == 0:
+        line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+                "warmup": args.warmup, "ms_per_step": tot_ms / args.steps, "higher_is_better": True,
+                "scaling": "weak", "vs_baseline": None, "dtype": "u8",
+                "data": f"synthetic: reference random_matrix(GF({cfg['p']}), seed {cfg['seed']}) generated on "
+                        f"device by K6 (bit-identical to the reference generator)",
+                "config": {"workload": cfg["desc"], "p": cfg["p"], "m": cfg["m"], "n": cfg["n"],
+                           "block": cfg["block"], "rank": rank_r, "with_transform": True,
+                           "executor_streams": args.threads,
+                           "l2": "flushed (512 MiB device write) before every timed step",
+                           "parallelism": f"replicas x{world}" if world > 1 else "1 GPU"},
+                "wall_ms_per_step": 1e3 * sum(walls) / len(walls),
+                "roofline": roof, "cpu_baseline": base, "e2e": e2e, "clocks": clk,
+                "gpu_launches": launches}
+        print(json.dumps(line))
+    if dist:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -88,6 +88,13 @@ int gfq_random_product_matrix(uint32_t p, int64_t rows, int64_t cols, int64_t in
                               uint64_t seed, gfq_mat** out);
 /* Base-case size of the device ECH recursion (<= 128; results unaffected). */
 int gfq_set_ech_base(uint64_t n);
+/* Accounting: kernel launches issued by this library (optionally reset),
+ * and K1 per-launch device timing (CUDA events on the launch stream).
+ * gfq_profile_take returns, for [0] = tcgen05 path and [1] = SIMT path,
+ * launches, algorithmic int8 ops (2*m*n*k) and summed device ms. */
+int gfq_launch_count(int reset, int64_t* launches);
+int gfq_profile(int on);
+int gfq_profile_take(int64_t* launches2, double* ops2, double* ms2);
 
 /* ------------------------------------------------------------ jobs (jobs.hpp:37-82) */
 int gfq_mul(uint32_t p, const gfq_mat* b, const gfq_mat* c, gfq_mat** out);            /* :40 */

@@ -72,6 +72,9 @@ PROTOS = {
     "gfq_random_matrix": (I, [U32, I64, I64, U64, vpp]),
     "gfq_random_product_matrix": (I, [U32, I64, I64, I64, U64, vpp]),
     "gfq_set_ech_base": (I, [U64]),
+    "gfq_launch_count": (I, [I, c_i64p]),
+    "gfq_profile": (I, [I]),
+    "gfq_profile_take": (I, [c_i64p, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_double)]),
     "gfq_mul": (I, [U32, vp, vp, vpp]),
     "gfq_mad": (I, [U32, vp, vp, vp, vpp]),
     "gfq_ech": (I, [U32, vp, U64, vpp, vpp, vpp, vpp, vpp]),

@@ -254,6 +254,13 @@ int gfq_random_product_matrix(uint32_t p, int64_t rows, int64_t cols, int64_t in
 }
 
 int gfq_set_ech_base(uint64_t n) { return guard([&] { gfq::set_ech_base(size_t(n)); }); }
+int gfq_launch_count(int reset, int64_t* launches) {
+  return guard([&] { *launches = gfq::dev::launch_count(reset != 0); });
+}
+int gfq_profile(int on) { return guard([&] { gfq::dev::set_profile(on != 0); }); }
+int gfq_profile_take(int64_t* launches2, double* ops2, double* ms2) {
+  return guard([&] { gfq::dev::profile_take(launches2, ops2, ms2); });
+}
 
 // ---------------------------------------------------------------- jobs
 int gfq_mul(uint32_t p, const gfq_mat* b, const gfq_mat* c, gfq_mat** out) {

@@ -371,6 +371,7 @@ bool mad_tc(std::uint32_t p, std::int64_t m, std::int64_t n, std::int64_t k,
     gf_mad_tc_kernel<<<grid, NUM_THREADS, SMEM_BYTES, s>>>(mA, mB, int(m), int(n), int(kk), p,
                                                            magic, cin, ldcin, D, ldd);
     GFQ_CUDA(cudaGetLastError());
+    count_launch();
   }
   return true;
 }

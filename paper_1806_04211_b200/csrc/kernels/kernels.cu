@@ -5,6 +5,8 @@
 //   K6 (counter-form SplitMix64 generator).
 // The tensor-core contraction lives in gf_mad_tc.cu.
 #include <atomic>
+#include <mutex>
+#include <vector>
 
 #include "../common.hpp"
 #include "kernels.hpp"
@@ -109,6 +111,7 @@ void mad_simt(std::uint32_t p, std::int64_t m, std::int64_t n, std::int64_t k,
     dim3 grid(unsigned((n + 255) / 256), unsigned(m < 65535 ? m : 65535));
     copy_or_zero_kernel<<<grid, 256, 0, s>>>(int(m), int(n), Cin, ldc, D, ldd);
     GFQ_CUDA(cudaGetLastError());
+    count_launch();
     return;
   }
   const std::int64_t kc = k_chunk_limit(p);
@@ -124,6 +127,7 @@ void mad_simt(std::uint32_t p, std::int64_t m, std::int64_t n, std::int64_t k,
           p, mg, int(mm), int(n), int(kk), A + m0 * lda + k0, lda, B + k0 * ldb, ldb,
           cin ? cin + m0 * ldcin : nullptr, ldcin, D + m0 * ldd, ldd);
       GFQ_CUDA(cudaGetLastError());
+    count_launch();
     }
   }
 }
@@ -131,7 +135,44 @@ void mad_simt(std::uint32_t p, std::int64_t m, std::int64_t n, std::int64_t k,
 namespace {
 std::atomic<int> g_policy{0};
 std::atomic<std::int64_t> g_simt{0}, g_tc{0};
+std::atomic<std::int64_t> g_launches{0};
+std::atomic<bool> g_profile{false};
+struct ProfRec {
+  cudaEvent_t e0, e1;
+  double ops;
+  int path;
+};
+std::mutex g_prof_mtx;
+std::vector<ProfRec> g_prof;
 }  // namespace
+
+void count_launch(std::int64_t n) { g_launches += n; }
+std::int64_t launch_count(bool reset) {
+  return reset ? g_launches.exchange(0) : g_launches.load();
+}
+void set_profile(bool on) { g_profile = on; }
+void profile_take(std::int64_t launches[2], double ops[2], double ms[2]) {
+  std::vector<ProfRec> recs;
+  {
+    std::lock_guard<std::mutex> lk(g_prof_mtx);
+    recs.swap(g_prof);
+  }
+  for (int q = 0; q < 2; ++q) {
+    launches[q] = 0;
+    ops[q] = 0;
+    ms[q] = 0;
+  }
+  for (auto& r : recs) {
+    float t = 0;
+    GFQ_CUDA(cudaEventSynchronize(r.e1));
+    GFQ_CUDA(cudaEventElapsedTime(&t, r.e0, r.e1));
+    launches[r.path] += 1;
+    ops[r.path] += r.ops;
+    ms[r.path] += t;
+    cudaEventDestroy(r.e0);
+    cudaEventDestroy(r.e1);
+  }
+}
 
 void set_mad_policy(int policy) { g_policy = policy; }
 int mad_policy() { return g_policy; }
@@ -154,14 +195,30 @@ void mad(std::uint32_t p, std::int64_t m, std::int64_t n, std::int64_t k,
   // fetch) of a few microseconds; below ~4 Mi MACs or for K < 32 (one MMA
   // instruction) the SIMT kernel is as fast and exactly as exact.
   const bool big = k >= 32 && (double(m) * double(n) * double(k) >= 4.0 * 1024 * 1024);
+  const bool prof = g_profile;
+  ProfRec rec{nullptr, nullptr, 2.0 * double(m) * double(n) * double(k), 0};
+  if (prof) {
+    GFQ_CUDA(cudaEventCreate(&rec.e0));
+    GFQ_CUDA(cudaEventCreate(&rec.e1));
+    GFQ_CUDA(cudaEventRecord(rec.e0, s));
+  }
+  bool done = false;
   if (pol != 1 && k > 0 && (pol == 2 || big)) {
     if (mad_tc(p, m, n, k, A, lda, B, ldb, Cin, ldc, D, ldd, s)) {
       ++g_tc;
-      return;
+      done = true;
     }
   }
-  ++g_simt;
-  mad_simt(p, m, n, k, A, lda, B, ldb, Cin, ldc, D, ldd, s);
+  if (!done) {
+    ++g_simt;
+    rec.path = 1;
+    mad_simt(p, m, n, k, A, lda, B, ldb, Cin, ldc, D, ldd, s);
+  }
+  if (prof) {
+    GFQ_CUDA(cudaEventRecord(rec.e1, s));
+    std::lock_guard<std::mutex> lk(g_prof_mtx);
+    g_prof.push_back(rec);
+  }
 }
 
 // ------------------------------------------------------------------ K3/K4
@@ -259,6 +316,7 @@ void select2d(std::uint8_t* dst, std::int64_t ldd, std::int64_t rows,
     select2d_kernel<<<dim3(gx, gy), 256, 0, s>>>(dst, ldd, rows, cols, A, lda, B, ldb, rmap, cmap);
   }
   GFQ_CUDA(cudaGetLastError());
+    count_launch();
 }
 
 void set_entries(std::uint8_t* dst, std::int64_t ldd, const std::int32_t* pos,
@@ -266,6 +324,7 @@ void set_entries(std::uint8_t* dst, std::int64_t ldd, const std::int32_t* pos,
   if (n == 0) return;
   set_entries_kernel<<<unsigned((n + 255) / 256), 256, 0, s>>>(dst, ldd, pos, n, value);
   GFQ_CUDA(cudaGetLastError());
+    count_launch();
 }
 
 // ------------------------------------------------------------------ K2 base
@@ -390,6 +449,7 @@ void ech_base(std::uint32_t p, std::int64_t rows, std::int64_t cols,
   ech_base_kernel<<<1, threads, smem, s>>>(p, magic_of(p), int(rows), int(cols), H, ldh, W, ldw,
                                            Tc, ldt, info);
   GFQ_CUDA(cudaGetLastError());
+    count_launch();
 }
 
 // ------------------------------------------------------------------ K6
@@ -424,6 +484,7 @@ void random_fill(std::uint32_t p, std::int64_t rows, std::int64_t cols,
   random_fill_kernel<<<dim3(gx, gy), 256, 0, s>>>(p, rows, cols, seed, draw0, limit, dst, ldd,
                                                    rejects);
   GFQ_CUDA(cudaGetLastError());
+    count_launch();
 }
 
 }  // namespace gfq::dev

@@ -32,6 +32,17 @@ bool mad_tc(std::uint32_t p, std::int64_t m, std::int64_t n, std::int64_t k,
             std::int64_t ldb, const std::uint8_t* Cin, std::int64_t ldc,
             std::uint8_t* D, std::int64_t ldd, cudaStream_t s);
 
+// ---------------------------------------------------------------- accounting
+// Every kernel launch of this library bumps a counter (bench.py's
+// gpu_launches).  With profiling on, each K1 launch is bracketed by CUDA
+// events on its own stream; profile_take() syncs them and returns, per path
+// (0 = tcgen05, 1 = SIMT), launches, algorithmic int8 ops (2*m*n*k) and
+// summed device milliseconds.
+void count_launch(std::int64_t n = 1);
+std::int64_t launch_count(bool reset);
+void set_profile(bool on);
+void profile_take(std::int64_t launches[2], double ops[2], double ms[2]);
+
 // Selects which path `mad` uses: 0 = auto, 1 = SIMT only, 2 = tcgen05 whenever legal.
 void set_mad_policy(int policy);
 int mad_policy();

@@ -759,6 +759,26 @@ def set_ech_base(n: int):
     _check(lib().gfq_set_ech_base(n))
 
 
+def launch_count(reset: bool = False) -> int:
+    v = ctypes.c_int64()
+    _check(lib().gfq_launch_count(int(reset), ctypes.byref(v)))
+    return v.value
+
+
+def profile(on: bool):
+    _check(lib().gfq_profile(int(on)))
+
+
+def profile_take():
+    """K1 per-launch device timing since the last take:
+    {"tc": (launches, ops, ms), "simt": (launches, ops, ms)}."""
+    l = (ctypes.c_int64 * 2)()
+    o = (ctypes.c_double * 2)()
+    t = (ctypes.c_double * 2)()
+    _check(lib().gfq_profile_take(l, o, t))
+    return {"tc": (l[0], o[0], t[0]), "simt": (l[1], o[1], t[1])}
+
+
 def set_stream(stream_ptr: int):
     _check(lib().gfq_set_stream(stream_ptr or None))
 

@@ -33,7 +33,8 @@ def compare(out, want, with_transform=True):
             j, l = map(int, key.split(","))
             np.testing.assert_array_equal(out.block(0, j, l).numpy(), arr(v))
         np.testing.assert_array_equal(out.assembled_R().numpy(),
-                                      np.array(want["assembled_R"], np.uint8).reshape(out.rank, -1))
+                                      np.array(want["assembled_R"], np.uint8).reshape(out.rank,
+                                                                                      want["n"] - out.rank))
         if with_transform:
             for key, v in want["TM"].items():
                 j, h = map(int, key.split(","))

@@ -154,6 +154,11 @@ def test_random_task_chains_vs_restatement(G, p):
         gk2, gm2 = G.update_row_trafo(f, ga1, None, None, ge1, 1, 1, 0)
         rk2, rm2 = R.update_row_trafo(p, ra1, None, None, re1, 1, 1, 0)
         assert gk2 == rk2 and gm2 == rm2
-        x, rr = G.pre_clear_up(gb1, gd1)
-        wx, wr = R.pre_clear_up(rb1, rd1)
+        # PreClearUp / ClearUp on the pivotal-row store of the right column
+        side = oracle.random_matrix(p, 6, beta + 3, 70 + seed)
+        gdr, _ = G.clear_down(f, side, None, 0)
+        rdr, _ = R.clear_down(p, side, R.PkgD(), 0)
+        x, rr = G.pre_clear_up(gb1, gdr)
+        wx, wr = R.pre_clear_up(rb1, rdr)
         assert x == wx and rr == wr
+        assert G.clear_up(f, rr, x, gdr.R) == R.clear_up(p, wr, wx, rdr.R)
