@@ -88,6 +88,9 @@ int gfq_random_product_matrix(uint32_t p, int64_t rows, int64_t cols, int64_t in
                               uint64_t seed, gfq_mat** out);
 /* Base-case size of the device ECH recursion (<= 128; results unaffected). */
 int gfq_set_ech_base(uint64_t n);
+/* ECH algorithm: 0 = panel Gauss-Jordan on [W | T] (default), 1 = the
+ * reference's split/combine recursion (jobs.cpp:202-225).  Same outputs. */
+int gfq_set_ech_mode(int mode);
 /* Accounting: kernel launches issued by this library (optionally reset),
  * and K1 per-launch device timing (CUDA events on the launch stream).
  * gfq_profile_take returns, for [0] = tcgen05 path and [1] = SIMT path,

@@ -33,6 +33,12 @@ std::vector<std::int32_t> as_i32(const std::vector<std::uint32_t>& v) {
 }
 }  // namespace
 
+namespace {
+std::atomic<int> g_ech_mode{0};
+}
+void set_ech_mode(int mode) { g_ech_mode = mode; }
+int ech_mode() { return g_ech_mode; }
+
 void set_ech_base(std::size_t n) {
   g_ech_base = std::max<std::size_t>(1, std::min<std::size_t>(n, dev::kEchBaseMax));
 }
@@ -247,6 +253,61 @@ EchResult direct_ech(const FieldSpec& f, const Mat& h) {
   return out;
 }
 
+// Device ECH: right-looking panel Gauss-Jordan on Aug = [W | T] (T = I), one
+// K2 panel launch + a row gather + two K1 launches per 32-column panel, no
+// host round trip until the pivots are read back at the end.  Outputs in the
+// reference's conventions (same extraction as direct_ech, T uncompacted).
+EchResult panel_ech(const FieldSpec& f, const Mat& h) {
+  const std::int64_t a = h.rows(), b = h.cols(), w = 32;
+  const std::int64_t cap = std::min(a, b);
+  const cudaStream_t s = cur_stream();
+  Mat aug = Mat::zeros(a, b + a);
+  dev::select2d(aug.data(), aug.ld(), a, b, h.data(), h.ld(), nullptr, 0, nullptr, nullptr, s);
+  {
+    std::vector<std::int32_t> diag(std::size_t(2 * a));
+    for (std::int64_t i = 0; i < a; ++i) {
+      diag[2 * i] = std::int32_t(i);
+      diag[2 * i + 1] = std::int32_t(b + i);
+    }
+    auto db = upload_i32(diag);
+    dev::set_entries(aug.data(), aug.ld(), dptr(db), a, 1, s);
+  }
+  DevBuf flags{static_cast<std::size_t>(a)};
+  DevBuf info{static_cast<std::size_t>(4 * (1 + 2 * cap))};
+  DevBuf rho2{static_cast<std::size_t>(4 * w)};
+  GFQ_CUDA(cudaMemsetAsync(flags.ptr, 0, flags.bytes, s));
+  GFQ_CUDA(cudaMemsetAsync(info.ptr, 0, info.bytes, s));
+  Mat G(a, w), Bp(w, b + a);
+  auto* inf = reinterpret_cast<std::int32_t*>(info.ptr);
+  auto* r2 = reinterpret_cast<std::int32_t*>(rho2.ptr);
+  for (std::int64_t c0 = 0; c0 < b; c0 += w) {
+    const std::int64_t wc = std::min(w, b - c0), n = b + a - c0;
+    dev::ech_panel(f.p(), a, c0, wc, w, aug.data(), aug.ld(), flags.ptr, inf, cap, G.data(),
+                   G.ld(), r2, s);
+    dev::select2d(Bp.data(), Bp.ld(), w, n, aug.data() + c0, aug.ld(), nullptr, 0, r2, nullptr, s);
+    dev::mad(f.p(), a, n, w, G.data(), G.ld(), Bp.data(), Bp.ld(), aug.data() + c0, aug.ld(),
+             aug.data() + c0, aug.ld(), s);
+  }
+  std::vector<std::int32_t> hi(std::size_t(1 + 2 * cap));
+  download_i32(inf, hi.data(), hi.size());
+  const std::int64_t r = hi[0];
+  std::vector<std::int32_t> pcol(hi.begin() + 1, hi.begin() + 1 + r);
+  std::vector<std::int32_t> prow(hi.begin() + 1 + cap, hi.begin() + 1 + cap + r);
+  EchResult out;
+  std::vector<std::uint32_t> rho(prow.begin(), prow.end());
+  std::sort(rho.begin(), rho.end());
+  out.rho = IndexSet(std::size_t(a), rho);
+  out.gamma = IndexSet(std::size_t(b), std::vector<std::uint32_t>(pcol.begin(), pcol.end()));
+  const auto tcols = as_i32(rho);
+  const auto krows = as_i32(index_set_complement(out.rho).members);
+  const auto gcols = as_i32(index_set_complement(out.gamma).members);
+  const Mat W = aug.col_view(0, b), T = aug.col_view(b, a);
+  out.M = select(r, r, T, nullptr, &prow, &tcols);
+  out.K = select(a - r, r, T, nullptr, &krows, &tcols);
+  out.R = select(r, b - r, W, nullptr, &prow, &gcols);
+  return out;
+}
+
 // Split point: half, rounded to a multiple of 16 so column views keep the
 // 16-byte alignment the TMA path needs (outputs do not depend on it).
 std::int64_t split_of(std::int64_t n) {
@@ -317,6 +378,14 @@ EchResult ech(const FieldSpec& f, const Mat& h, std::size_t threshold) {
     e.rho = IndexSet(std::size_t(alpha), {});
     e.gamma = IndexSet(std::size_t(beta), {});
     return e;
+  }
+  if (ech_mode() == 0) {
+    // panel ECH whenever the panel fits one CTA's shared memory; taller
+    // blocks split their rows (reference combine_horizontal) first
+    if (alpha * 33 <= dev::kPanelSmem) return panel_ech(f, h);
+    const std::int64_t alpha1 = split_of(alpha);
+    const EchResult e1 = ech(f, h.row_view(0, alpha1), threshold);
+    return combine_horizontal(f, h.row_view(alpha1, alpha - alpha1), e1, alpha1, threshold);
   }
   const std::int64_t base = std::int64_t(std::min(threshold, ech_base()));
   if (alpha <= base && beta <= base) return direct_ech(f, h);

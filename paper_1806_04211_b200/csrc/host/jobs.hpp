@@ -42,5 +42,10 @@ Mat hcat(const Mat& a, const Mat& b);                                 // matrix.
 /// Tunable: largest block the K2 base-case kernel takes (<= kEchBaseMax).
 void set_ech_base(std::size_t n);
 std::size_t ech_base();
+/// ECH algorithm: 0 = device panel Gauss-Jordan (default), 1 = the
+/// reference's split/combine recursion down to the K2 base case.  Both give
+/// the same (canonical) outputs.
+void set_ech_mode(int mode);
+int ech_mode();
 
 }  // namespace gfq

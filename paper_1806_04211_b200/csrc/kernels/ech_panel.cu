@@ -1,0 +1,275 @@
+// ech_panel.cu -- K2: the panel step of the device ECH.
+//
+// The block H (rows x cols) is eliminated in place inside the augmented
+// matrix Aug = [W | T] (T = I at the start) by right-looking Gauss-Jordan
+// over panels of w <= 32 columns.  This kernel is the latency-critical part
+// of a panel: one CTA holds the panel columns of every row in shared memory
+// and runs the reference's column-wise pivot rule on the rows that are not
+// yet pivotal (first non-pivotal row with a nonzero entry, reference
+// src/chief.cpp:436-460; the same canonical rho/gamma as direct_gauss,
+// SURVEY 8c): warp min-reduction + one shared atomic per warp for the pivot
+// search, the pivot row broadcast through shared memory, a packed rank-1
+// elimination of the panel (XOR words for p = 2).  It then inverts the
+// r2 x r2 pivot block with the whole CTA and emits the panel multipliers
+//   G = Ap.N2, Ap = Aug[:, c0 + gamma2] (+ I on the new pivot rows),
+//   N2 = -inv(Aug[rho2, c0 + gamma2]),
+// so that Aug[:, c0:] += G.Aug[rho2, c0:] finishes the panel (K1).  Nothing
+// returns to the host until the last panel: the ECH is a fixed launch
+// sequence.
+#include "../common.hpp"
+#include "kernels.hpp"
+
+namespace gfq::dev {
+namespace {
+
+__device__ __forceinline__ std::uint32_t modp(std::uint32_t x, std::uint32_t p,
+                                              std::uint32_t magic) {
+  const std::uint32_t q = __umulhi(x, magic);
+  const std::int32_t r = static_cast<std::int32_t>(x - q * p);
+  return static_cast<std::uint32_t>(r < 0 ? r + static_cast<std::int32_t>(p) : r);
+}
+
+__device__ __forceinline__ std::uint32_t powmod(std::uint32_t a, std::uint32_t e,
+                                                std::uint32_t p) {
+  std::uint32_t r = 1, b = a % p;
+  while (e) {
+    if (e & 1) r = (r * b) % p;
+    b = (b * b) % p;
+    e >>= 1;
+  }
+  return r;
+}
+
+constexpr int kW = 32;  // max panel width (bytes per panel row in smem)
+
+// Load the 32-byte panel segment of row i (bytes >= wc zeroed).
+__device__ __forceinline__ void load_seg(const std::uint8_t* src, int wc, uint4& a, uint4& b) {
+  if (wc == kW && (reinterpret_cast<std::uintptr_t>(src) & 15) == 0) {
+    a = reinterpret_cast<const uint4*>(src)[0];
+    b = reinterpret_cast<const uint4*>(src)[1];
+    return;
+  }
+  std::uint32_t w[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  for (int c = 0; c < wc; ++c) w[c >> 2] |= std::uint32_t(src[c]) << (8 * (c & 3));
+  a = make_uint4(w[0], w[1], w[2], w[3]);
+  b = make_uint4(w[4], w[5], w[6], w[7]);
+}
+
+__global__ void __launch_bounds__(1024)
+ech_panel_kernel(std::uint32_t p, std::uint32_t magic, int rows, int c0, int wc, int w,
+                 const std::uint8_t* __restrict__ Aug, std::int64_t ld, std::uint8_t* flags,
+                 std::int32_t* info, int cap, std::uint8_t* G, std::int64_t ldg,
+                 std::int32_t* rho2) {
+  extern __shared__ __align__(16) std::uint8_t sm[];
+  std::uint8_t* P = sm;                   // rows x kW
+  std::uint8_t* fl = sm + rows * kW;      // rows (pivot flags)
+  __shared__ std::uint8_t invt[256];
+  __shared__ __align__(16) std::uint8_t prow[kW];
+  __shared__ unsigned sel_s;
+  __shared__ int pc[kW], pr[kW];
+  __shared__ std::uint8_t X[kW][2 * kW];  // [pivot block | I] -> [I | inverse]
+  __shared__ std::uint32_t N2[kW][kW];    // -inverse, zero padded
+  __shared__ int r_old, piv_s;
+  const int tid = threadIdx.x, nt = blockDim.x, lane = tid & 31;
+
+  for (int a = tid; a < 256; a += nt)
+    invt[a] = (a > 0 && std::uint32_t(a) < p) ? std::uint8_t(powmod(a, p - 2, p)) : 0;
+  for (int i = tid; i < rows; i += nt) {
+    const std::uint8_t f = flags[i];
+    fl[i] = f;
+    if (!f) {
+      uint4 a, b;
+      load_seg(Aug + std::int64_t(i) * ld + c0, wc, a, b);
+      reinterpret_cast<uint4*>(P + i * kW)[0] = a;
+      reinterpret_cast<uint4*>(P + i * kW)[1] = b;
+    }
+  }
+  if (tid == 0) r_old = info[0];
+  __syncthreads();
+
+  // ---- column-wise Gauss-Jordan on the non-pivotal rows of the panel
+  int r2 = 0;
+  for (int c = 0; c < wc; ++c) {
+    if (tid == 0) sel_s = 0xFFFFFFFFu;
+    __syncthreads();
+    unsigned cand = 0xFFFFFFFFu;
+    for (int i = tid; i < rows; i += nt)
+      if (!fl[i] && P[i * kW + c] && unsigned(i) < cand) cand = unsigned(i);
+    cand = __reduce_min_sync(0xffffffffu, cand);
+    if (lane == 0 && cand != 0xFFFFFFFFu) atomicMin(&sel_s, cand);
+    __syncthreads();
+    const unsigned s = sel_s;
+    if (s != 0xFFFFFFFFu) {
+      const std::uint32_t scale = p - invt[P[s * kW + c]];
+      if (tid < kW)
+        prow[tid] = tid < c ? 0 : std::uint8_t(modp(scale * P[s * kW + tid], p, magic));
+      if (tid == 0) {
+        fl[s] = 1;
+        pc[r2] = c;
+        pr[r2] = int(s);
+      }
+      __syncthreads();
+      const std::uint32_t* pw = reinterpret_cast<const std::uint32_t*>(prow);
+      const int w0 = c >> 2;
+      for (int i = tid; i < rows; i += nt) {
+        if (fl[i]) continue;
+        const std::uint32_t cf = P[i * kW + c];
+        if (!cf) continue;
+        std::uint32_t* rw = reinterpret_cast<std::uint32_t*>(P + i * kW);
+        if (p == 2) {
+#pragma unroll
+          for (int q = 0; q < kW / 4; ++q)
+            if (q >= w0) rw[q] ^= pw[q];
+        } else {
+#pragma unroll
+          for (int q = 0; q < kW / 4; ++q) {
+            if (q < w0) continue;
+            const std::uint32_t a = rw[q], b = pw[q];
+            // two 16-bit lanes per multiply: (p-1)^2 + (p-1) < 2^16
+            const std::uint32_t lo = (a & 0x00FF00FFu) + cf * (b & 0x00FF00FFu);
+            const std::uint32_t hi = ((a >> 8) & 0x00FF00FFu) + cf * ((b >> 8) & 0x00FF00FFu);
+            rw[q] = modp(lo & 0xFFFF, p, magic) | (modp(hi & 0xFFFF, p, magic) << 8) |
+                    (modp(lo >> 16, p, magic) << 16) | (modp(hi >> 16, p, magic) << 24);
+          }
+        }
+      }
+      ++r2;
+    }
+    __syncthreads();
+  }
+
+  // ---- N2 = -inv(Aug[rho2, c0 + gamma2]) with the whole CTA
+  for (int e = tid; e < kW * 2 * kW; e += nt) {
+    const int q = e / (2 * kW), t = e % (2 * kW);
+    std::uint8_t v = 0;
+    if (q < r2 && t < r2) v = Aug[std::int64_t(pr[q]) * ld + c0 + pc[t]];
+    else if (q < r2 && t >= kW && t - kW == q) v = 1;
+    X[q][t] = v;
+  }
+  __syncthreads();
+  for (int q = 0; q < r2; ++q) {
+    if (tid < 32) {
+      const unsigned bal = __ballot_sync(0xffffffffu, tid >= q && tid < r2 && X[tid][q] != 0);
+      if (tid == 0) piv_s = __ffs(bal) - 1;
+    }
+    __syncthreads();
+    const int pv = piv_s;
+    if (pv != q && tid < 2 * kW) {
+      const std::uint8_t t0 = X[q][tid];
+      X[q][tid] = X[pv][tid];
+      X[pv][tid] = t0;
+    }
+    __syncthreads();
+    const std::uint32_t iv = invt[X[q][q]];
+    __syncthreads();
+    if (tid < 2 * kW) X[q][tid] = std::uint8_t(modp(iv * X[q][tid], p, magic));
+    __syncthreads();
+    // eliminate column q from the other rows: element (row, col) per thread
+    for (int e = tid; e < kW * 2 * kW; e += nt) {
+      const int row = e / (2 * kW), col = e % (2 * kW);
+      if (row >= r2 || row == q) continue;
+      const std::uint32_t f = X[row][q];
+      if (!f || col == q) continue;
+      X[row][col] = std::uint8_t(modp(X[row][col] + (p - f) * X[q][col], p, magic));
+    }
+    __syncthreads();
+    if (tid < kW && tid < r2 && tid != q) X[tid][q] = 0;
+    __syncthreads();
+  }
+  for (int e = tid; e < kW * kW; e += nt) {
+    const int q = e / kW, t = e % kW;
+    std::uint32_t v = 0;
+    if (q < r2 && t < r2) {
+      const std::uint32_t x = X[q][kW + t];
+      v = x ? p - x : 0;
+    }
+    N2[q][t] = v;
+  }
+  if (tid < kW) rho2[tid] = tid < r2 ? pr[tid] : -1;
+  if (tid < r2) {
+    info[1 + r_old + tid] = c0 + pc[tid];
+    info[1 + cap + r_old + tid] = pr[tid];
+    flags[pr[tid]] = 1;
+  }
+  if (tid == 0) info[0] = r_old + r2;
+  __syncthreads();
+
+  // ---- G[i] = Ap[i].N2, Ap[i][q] = Aug[i][c0 + pc[q]] (+1 on pivot row of q)
+  for (int i = tid; i < rows; i += nt) {
+    uint4 a, b;
+    load_seg(Aug + std::int64_t(i) * ld + c0, wc, a, b);
+    const std::uint32_t seg[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
+    std::uint32_t acc[kW];
+#pragma unroll
+    for (int t = 0; t < kW; ++t) acc[t] = 0;
+    for (int q = 0; q < r2; ++q) {
+      const int cq = pc[q];
+      std::uint32_t v = (seg[cq >> 2] >> (8 * (cq & 3))) & 0xFF;
+      if (pr[q] == i) v += 1;
+      if (!v) continue;
+#pragma unroll
+      for (int t = 0; t < kW; ++t) acc[t] += v * N2[q][t];
+    }
+    std::uint32_t outw[kW / 4];
+#pragma unroll
+    for (int t4 = 0; t4 < kW / 4; ++t4) {
+      std::uint32_t word = 0;
+#pragma unroll
+      for (int by = 0; by < 4; ++by) word |= modp(acc[4 * t4 + by], p, magic) << (8 * by);
+      outw[t4] = word;
+    }
+    uint4* dst = reinterpret_cast<uint4*>(G + std::int64_t(i) * ldg);
+    dst[0] = make_uint4(outw[0], outw[1], outw[2], outw[3]);
+    dst[1] = make_uint4(outw[4], outw[5], outw[6], outw[7]);
+  }
+}
+
+__global__ void scatter_rows_kernel(std::uint8_t* dst, std::int64_t ldd, std::int64_t rows,
+                                    std::int64_t cols, const std::uint8_t* src,
+                                    std::int64_t lds, const std::int32_t* rmap) {
+  for (std::int64_t i = blockIdx.y; i < rows; i += gridDim.y) {
+    const std::int32_t t = rmap[i];
+    if (t < 0) continue;
+    for (std::int64_t j = blockIdx.x * blockDim.x + threadIdx.x; j < cols;
+         j += std::int64_t(gridDim.x) * blockDim.x)
+      dst[std::int64_t(t) * ldd + j] = src[i * lds + j];
+  }
+}
+
+}  // namespace
+
+void ech_panel(std::uint32_t p, std::int64_t rows, std::int64_t c0, std::int64_t wc,
+               std::int64_t w, const std::uint8_t* Aug, std::int64_t ld, std::uint8_t* flags,
+               std::int32_t* info, std::int64_t cap, std::uint8_t* G, std::int64_t ldg,
+               std::int32_t* rho2, cudaStream_t s) {
+  if (w != kW || wc > w) throw std::invalid_argument("ech_panel: panel width must be 32");
+  if ((ldg & 15) || (reinterpret_cast<std::uintptr_t>(G) & 15))
+    throw std::invalid_argument("ech_panel: G must be 16-byte aligned");
+  const std::size_t smem = std::size_t(rows) * (kW + 1);
+  if (smem > std::size_t(kPanelSmem)) throw std::invalid_argument("ech_panel: block too tall");
+  static bool attr = false;
+  if (!attr) {
+    GFQ_CUDA(cudaFuncSetAttribute(ech_panel_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  kPanelSmem));
+    attr = true;
+  }
+  const std::int64_t r32 = (rows + 31) / 32 * 32;
+  const int threads = r32 >= 1024 ? 1024 : int(r32 < 64 ? 64 : r32);
+  const std::uint32_t magic = static_cast<std::uint32_t>((0x100000000ULL / p) + 1);
+  ech_panel_kernel<<<1, threads, smem, s>>>(p, magic, int(rows), int(c0), int(wc), int(w), Aug, ld,
+                                            flags, info, int(cap), G, ldg, rho2);
+  GFQ_CUDA(cudaGetLastError());
+  count_launch();
+}
+
+void scatter_rows(std::uint8_t* dst, std::int64_t ldd, std::int64_t rows, std::int64_t cols,
+                  const std::uint8_t* src, std::int64_t lds, const std::int32_t* rmap,
+                  cudaStream_t s) {
+  if (rows == 0 || cols == 0) return;
+  const unsigned gx = unsigned((cols + 255) / 256), gy = unsigned(rows < 65535 ? rows : 65535);
+  scatter_rows_kernel<<<dim3(gx, gy), 256, 0, s>>>(dst, ldd, rows, cols, src, lds, rmap);
+  GFQ_CUDA(cudaGetLastError());
+  count_launch();
+}
+
+}  // namespace gfq::dev

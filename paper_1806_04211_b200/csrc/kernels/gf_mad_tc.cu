@@ -245,13 +245,23 @@ gf_mad_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
       const int mb = tile % num_m, nb = tile / num_m;
       const int acc = it & 1;
       const std::uint32_t acc_phase = (it >> 1) & 1;
-      mbar_wait(&tfull[acc], acc_phase);
-      fence_after();
       const int row = mb * BM + row_in_tile;
       const bool row_ok = row < m;
       const std::uint8_t* crow = (Cin && row_ok) ? Cin + std::int64_t(row) * ldc : nullptr;
       std::uint8_t* drow = row_ok ? D + std::int64_t(row) * ldd : nullptr;
-#pragma unroll 1
+      // Prefetch this row's addend segment before waiting on the MMAs, so
+      // its HBM latency hides behind the mainloop.
+      const bool pre = crow && nb * BN + BN <= n &&
+                       (reinterpret_cast<std::uintptr_t>(crow + nb * BN) & 15) == 0;
+      uint4 cpre[BN / 16];
+      if (pre) {
+#pragma unroll
+        for (int q = 0; q < BN / 16; ++q)
+          cpre[q] = reinterpret_cast<const uint4*>(crow + nb * BN)[q];
+      }
+      mbar_wait(&tfull[acc], acc_phase);
+      fence_after();
+#pragma unroll
       for (int ch = 0; ch < BN / 32; ++ch) {
         std::uint32_t v[32];
         const std::uint32_t taddr = tmem_base + (std::uint32_t(quarter * 32) << 16) +
@@ -265,7 +275,10 @@ gf_mad_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
                          (!crow || (reinterpret_cast<std::uintptr_t>(crow + col0) & 15) == 0);
         if (vec) {
           uint4 cv[2] = {make_uint4(0, 0, 0, 0), make_uint4(0, 0, 0, 0)};
-          if (crow) {
+          if (pre) {
+            cv[0] = cpre[2 * ch];
+            cv[1] = cpre[2 * ch + 1];
+          } else if (crow) {
             cv[0] = reinterpret_cast<const uint4*>(crow + col0)[0];
             cv[1] = reinterpret_cast<const uint4*>(crow + col0)[1];
           }

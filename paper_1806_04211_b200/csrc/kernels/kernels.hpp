@@ -79,6 +79,28 @@ void ech_base(std::uint32_t p, std::int64_t rows, std::int64_t cols,
               std::int64_t ldw, std::uint8_t* Tc, std::int64_t ldt,
               std::int32_t* info, cudaStream_t s);
 
+// Panel step of the device ECH (right-looking Gauss-Jordan on the augmented
+// block Aug = [W | T], rows x (cols + rows), T starting at I).  One CTA:
+// finds, among the rows not yet pivotal (flags[i] == 0), the pivots of
+// panel columns [c0, c0+wc) with the column-wise rule, and writes
+//   G (rows x 32): the panel multipliers, G = Ap.N2 with
+//                  Ap = Aug[:, c0 + gamma2] (+ I on the new pivot rows) and
+//                  N2 = -inv(Aug[rho2, c0 + gamma2]) (zero padded),
+//   rho2 (32):     new pivot rows in discovery order (-1 padded),
+// and appends (c0 + gamma2, rho2) to info = [rank, cols[cap], rows[cap]].
+// The caller then applies Aug[:, c0:] += G.Aug[rho2, c0:].
+// Requires w == 32 and rows * 33 <= kPanelSmem bytes.
+constexpr int kPanelSmem = 200 * 1024;
+void ech_panel(std::uint32_t p, std::int64_t rows, std::int64_t c0, std::int64_t wc,
+               std::int64_t w, const std::uint8_t* Aug, std::int64_t ld, std::uint8_t* flags,
+               std::int32_t* info, std::int64_t cap, std::uint8_t* G, std::int64_t ldg,
+               std::int32_t* rho2, cudaStream_t s);
+
+// dst[rmap[i]] = src[i] for rmap[i] >= 0 (row scatter).
+void scatter_rows(std::uint8_t* dst, std::int64_t ldd, std::int64_t rows, std::int64_t cols,
+                  const std::uint8_t* src, std::int64_t lds, const std::int32_t* rmap,
+                  cudaStream_t s);
+
 // ---------------------------------------------------------------- K6
 // Counter-form SplitMix64: entry e (row-major over rows x cols) takes draw
 // index draw0 + e of the stream `seed` and is reduced mod p.  Draws that

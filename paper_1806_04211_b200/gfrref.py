@@ -759,6 +759,11 @@ def set_ech_base(n: int):
     _check(lib().gfq_set_ech_base(n))
 
 
+def set_ech_mode(mode: int):
+    """0 = device panel Gauss-Jordan (default), 1 = reference split/combine recursion."""
+    _check(lib().gfq_set_ech_mode(mode))
+
+
 def launch_count(reset: bool = False) -> int:
     v = ctypes.c_int64()
     _check(lib().gfq_launch_count(int(reset), ctypes.byref(v)))

@@ -163,6 +163,13 @@ def test_index_jobs_pinned(G, pinned):
 
 
 # ------------------------------------------------------------------ K2 + recursion (ech)
+@pytest.fixture(params=[0, 1], ids=["panel", "recursive"])
+def mode(G, request):
+    G.set_ech_mode(request.param)
+    yield request.param
+    G.set_ech_mode(0)
+
+
 def check_ech(G, p, H, e, thr=None):
     o = oracle.oracle_rref(p, H)
     assert e.rank() == o["rank"]
@@ -174,7 +181,7 @@ def check_ech(G, p, H, e, thr=None):
         np.testing.assert_array_equal(got.numpy(), o[key])
 
 
-def test_ech_pinned(G, pinned):
+def test_ech_pinned(G, mode, pinned):
     f = G.FieldSpec(3)
     for c in pinned["ech"]:
         h = arr(c["h"])
@@ -186,7 +193,7 @@ def test_ech_pinned(G, pinned):
         assert e.R == arr(c["R"]).reshape(r, h.shape[1] - r)
 
 
-def test_ech_empty_and_zero(G):
+def test_ech_empty_and_zero(G, mode):
     f = G.FieldSpec(3)
     for shape in [(0, 3), (3, 0), (0, 0)]:
         e = G.ech(f, np.zeros(shape, np.uint8))
@@ -196,7 +203,7 @@ def test_ech_empty_and_zero(G):
 
 
 @pytest.mark.parametrize("p", PRIMES)
-def test_ech_random_shapes_and_thresholds(G, p):
+def test_ech_random_shapes_and_thresholds(G, mode, p):
     f = G.FieldSpec(p)
     cases = [(1, 1), (4, 4), (5, 3), (3, 5), (16, 16), (33, 17), (100, 100), (200, 130), (130, 300)]
     for t, (m, n) in enumerate(cases):
@@ -209,7 +216,7 @@ def test_ech_random_shapes_and_thresholds(G, p):
     check_ech(G, p, low, G.ech(f, low, 32))
 
 
-def test_ech_reference_fixtures(G, ref_runs):
+def test_ech_reference_fixtures(G, mode, ref_runs):
     for c in ref_runs["ech"]:
         H = np.array(c["H"], np.uint8).reshape(c["m"], c["n"])
         e = G.ech(G.FieldSpec(c["p"]), H, c["threshold"])
@@ -229,7 +236,7 @@ def test_ech_base_size_does_not_change_results(G, base):
         G.set_ech_base(64)
 
 
-def test_ech_large_block(G):
+def test_ech_large_block(G, mode):
     p = 2
     H = rnd(p, 1024, 1024, 3)
     e = G.ech(G.FieldSpec(p), H)

@@ -1,0 +1,17 @@
+"""Run single device jobs once (for ncu launch lists): python tools/one_ech.py [n] [p] [mode]"""
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+from paper_1806_04211_b200 import gfrref as G  # noqa: E402
+
+n = int(sys.argv[1]) if len(sys.argv) > 1 else 1024
+p = int(sys.argv[2]) if len(sys.argv) > 2 else 2
+mode = int(sys.argv[3]) if len(sys.argv) > 3 else 0
+G.lib()
+G.set_ech_mode(mode)
+f = G.FieldSpec(p)
+H = G.random_matrix(f, n, n, 7)
+e = G.ech(f, H)
+G.synchronize()
+print("rank", e.rank())

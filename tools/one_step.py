@@ -1,0 +1,32 @@
+"""One echelonize step of a bench config (for ncu launch lists / traces).
+
+python tools/one_step.py [cfg2a] [threads] [--trace out.csv]
+"""
+import os
+import sys
+import time
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+from bench import CONFIGS  # noqa: E402
+from paper_1806_04211_b200 import gfrref as G  # noqa: E402
+
+name = sys.argv[1] if len(sys.argv) > 1 else "cfg2a"
+threads = int(sys.argv[2]) if len(sys.argv) > 2 else 4
+cfg = CONFIGS[name]
+G.lib()
+f = G.FieldSpec(cfg["p"])
+C = G.random_matrix(f, cfg["m"], cfg["n"], cfg["seed"]) if cfg["kind"] == "random" else \
+    G.random_product_matrix(f, cfg["m"], cfg["n"], cfg["inner"], cfg["seed"])
+G.synchronize()
+t0 = time.time()
+out = G.echelonize(C, f, G.EchelonizeOptions(block=cfg["block"], threads=threads,
+                                             collect_trace="--trace" in sys.argv))
+G.synchronize()
+print("rank", out.rank, "wall_ms", 1e3 * (time.time() - t0))
+if "--trace" in sys.argv:
+    import csv
+    with open(sys.argv[sys.argv.index("--trace") + 1], "w") as fh:
+        w = csv.writer(fh)
+        w.writerow(["task_kind", "i", "j", "k", "worker", "start_ns", "end_ns", "detail"])
+        for t in out.trace():
+            w.writerow([t["kind"], t["i"], t["j"], t["k"], t["worker"], t["start_ns"], t["end_ns"], t["detail"]])
