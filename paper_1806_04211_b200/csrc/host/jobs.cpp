@@ -382,7 +382,7 @@ EchResult ech(const FieldSpec& f, const Mat& h, std::size_t threshold) {
   if (ech_mode() == 0) {
     // panel ECH whenever the panel fits one CTA's shared memory; taller
     // blocks split their rows (reference combine_horizontal) first
-    if (alpha * 33 <= dev::kPanelSmem) return panel_ech(f, h);
+    if (alpha * (f.p() == 2 ? 5 : 33) <= dev::kPanelSmem) return panel_ech(f, h);
     const std::int64_t alpha1 = split_of(alpha);
     const EchResult e1 = ech(f, h.row_view(0, alpha1), threshold);
     return combine_horizontal(f, h.row_view(alpha1, alpha - alpha1), e1, alpha1, threshold);

@@ -198,24 +198,28 @@ std::size_t PkgA::byte_size() const {
 
 // ---------------------------------------------------------------- staging
 namespace {
+// One process-wide pinned staging ring for small index uploads (pinning is
+// expensive: it is done once, not per executor thread or per call).
 struct Staging {
+  std::mutex mtx;
   std::uint8_t* host = nullptr;
   std::size_t cap = 0, off = 0;
-  ~Staging() {
-    if (host) cudaFreeHost(host);
-  }
 };
-thread_local Staging t_stage;
+Staging& staging() {
+  static Staging* st = new Staging();  // intentionally leaked (process lifetime)
+  return *st;
+}
 }  // namespace
 
 std::shared_ptr<DevBuf> upload_i32(const std::vector<std::int32_t>& v) {
   const std::size_t bytes = v.size() * sizeof(std::int32_t);
   auto buf = std::make_shared<DevBuf>(bytes > 0 ? bytes : 4);
   if (bytes == 0) return buf;
-  Staging& st = t_stage;
+  Staging& st = staging();
   const std::size_t need = (bytes + 255) / 256 * 256;
+  std::lock_guard<std::mutex> lk(st.mtx);
   if (!st.host) {
-    st.cap = std::size_t(32) << 20;
+    st.cap = std::size_t(64) << 20;
     GFQ_CUDA(cudaMallocHost(reinterpret_cast<void**>(&st.host), st.cap));
   }
   if (need > st.cap) {
@@ -225,7 +229,7 @@ std::shared_ptr<DevBuf> upload_i32(const std::vector<std::int32_t>& v) {
     return buf;
   }
   if (st.off + need > st.cap) {
-    // wrap: earlier copies out of the ring must have landed
+    // wrap: earlier copies out of the ring (on any stream) must have landed
     GFQ_CUDA(cudaDeviceSynchronize());
     st.off = 0;
   }

@@ -224,6 +224,131 @@ ech_panel_kernel(std::uint32_t p, std::uint32_t magic, int rows, int c0, int wc,
   }
 }
 
+// GF(2): the 32 panel columns of a row are one 32-bit word, a row
+// operation is one XOR, the pivot block inversion is a 32 x 32 bit-matrix
+// Gauss-Jordan in one warp's registers and G = Ap.N2 is a masked XOR of
+// N2's row words.  Same outputs as ech_panel_kernel for p = 2.
+__global__ void __launch_bounds__(1024)
+ech_panel_gf2_kernel(int rows, int c0, int wc, const std::uint8_t* __restrict__ Aug, std::int64_t ld,
+                     std::uint8_t* flags, std::int32_t* info, int cap, std::uint8_t* G,
+                     std::int64_t ldg, std::int32_t* rho2) {
+  extern __shared__ __align__(16) std::uint8_t sm[];
+  std::uint32_t* bits = reinterpret_cast<std::uint32_t*>(sm);  // rows words
+  std::uint8_t* fl = sm + 4 * rows;                             // rows flags
+  __shared__ unsigned sel_s[2];
+  __shared__ int pc[kW], pr[kW];
+  __shared__ std::uint32_t n2[kW];  // N2 rows as bit words (column t = bit t)
+  __shared__ int r_old;
+  const int tid = threadIdx.x, nt = blockDim.x, lane = tid & 31;
+
+  for (int i = tid; i < rows; i += nt) {
+    const std::uint8_t f = flags[i];
+    fl[i] = f;
+    std::uint32_t word = 0;
+    if (!f) {
+      uint4 a, b;
+      load_seg(Aug + std::int64_t(i) * ld + c0, wc, a, b);
+      const std::uint32_t wds[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        const std::uint32_t v = wds[q] & 0x01010101u;  // one bit per byte
+        word |= ((v & 1u) | ((v >> 7) & 2u) | ((v >> 14) & 4u) | ((v >> 21) & 8u)) << (4 * q);
+      }
+    }
+    bits[i] = word;
+  }
+  if (tid == 0) {
+    r_old = info[0];
+    sel_s[0] = 0xFFFFFFFFu;
+  }
+  __syncthreads();
+
+  int r2 = 0;
+  for (int c = 0; c < wc; ++c) {
+    unsigned cand = 0xFFFFFFFFu;
+    for (int i = tid; i < rows; i += nt)
+      if (!fl[i] && ((bits[i] >> c) & 1u) && unsigned(i) < cand) cand = unsigned(i);
+    cand = __reduce_min_sync(0xffffffffu, cand);
+    if (lane == 0 && cand != 0xFFFFFFFFu) atomicMin(&sel_s[c & 1], cand);
+    __syncthreads();
+    const unsigned s = sel_s[c & 1];
+    if (tid == 0) sel_s[(c + 1) & 1] = 0xFFFFFFFFu;
+    if (s != 0xFFFFFFFFu) {
+      const std::uint32_t ps = bits[s];
+      for (int i = tid; i < rows; i += nt)
+        if (i != int(s) && !fl[i] && ((bits[i] >> c) & 1u)) bits[i] ^= ps;
+      if (tid == 0) {
+        fl[s] = 1;
+        pc[r2] = c;
+        pr[r2] = int(s);
+      }
+      ++r2;
+    }
+    __syncthreads();
+  }
+
+  // N2 = inv(X) (= -inv over GF(2)), X[q][t] = Aug[pr[q]][c0 + pc[t]]
+  if (tid < 32) {
+    std::uint32_t x = 0, inv = 0;  // row `lane` of [X | I] as two bit words
+    if (lane < r2) {
+      const std::uint8_t* src = Aug + std::int64_t(pr[lane]) * ld + c0;
+      for (int t = 0; t < r2; ++t) x |= std::uint32_t(src[pc[t]] & 1u) << t;
+      inv = 1u << lane;
+    }
+    for (int q = 0; q < r2; ++q) {
+      const unsigned bal = __ballot_sync(0xffffffffu, lane >= q && lane < r2 && ((x >> q) & 1u));
+      const int pv = __ffs(bal) - 1;
+      // swap rows q and pv
+      const std::uint32_t xq = __shfl_sync(0xffffffffu, x, q), iq = __shfl_sync(0xffffffffu, inv, q);
+      const std::uint32_t xp = __shfl_sync(0xffffffffu, x, pv), ip = __shfl_sync(0xffffffffu, inv, pv);
+      if (lane == q) {
+        x = xp;
+        inv = ip;
+      } else if (lane == pv) {
+        x = xq;
+        inv = iq;
+      }
+      const std::uint32_t px = __shfl_sync(0xffffffffu, x, q), pi = __shfl_sync(0xffffffffu, inv, q);
+      if (lane != q && ((x >> q) & 1u)) {
+        x ^= px;
+        inv ^= pi;
+      }
+    }
+    n2[lane] = lane < r2 ? inv : 0u;
+    if (lane < kW) rho2[lane] = lane < r2 ? pr[lane] : -1;
+    if (lane < r2) {
+      info[1 + r_old + lane] = c0 + pc[lane];
+      info[1 + cap + r_old + lane] = pr[lane];
+      flags[pr[lane]] = 1;
+    }
+    if (lane == 0) info[0] = r_old + r2;
+  }
+  __syncthreads();
+
+  // G[i] = (Aug[i, c0 + gamma2] + e_{pivot of i}) . N2 over GF(2)
+  for (int i = tid; i < rows; i += nt) {
+    uint4 a, b;
+    load_seg(Aug + std::int64_t(i) * ld + c0, wc, a, b);
+    const std::uint32_t seg[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
+    std::uint32_t g = 0;
+    for (int q = 0; q < r2; ++q) {
+      const int cq = pc[q];
+      std::uint32_t v = (seg[cq >> 2] >> (8 * (cq & 3))) & 1u;
+      if (pr[q] == i) v ^= 1u;
+      if (v) g ^= n2[q];
+    }
+    std::uint32_t outw[8];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      const std::uint32_t nib = (g >> (4 * q)) & 0xFu;
+      outw[q] = (nib & 1u) | ((nib & 2u) << 7) | ((nib & 4u) << 14) | ((nib & 8u) << 21);
+    }
+    uint4* dst = reinterpret_cast<uint4*>(G + std::int64_t(i) * ldg);
+    dst[0] = make_uint4(outw[0], outw[1], outw[2], outw[3]);
+    dst[1] = make_uint4(outw[4], outw[5], outw[6], outw[7]);
+  }
+}
+
 __global__ void scatter_rows_kernel(std::uint8_t* dst, std::int64_t ldd, std::int64_t rows,
                                     std::int64_t cols, const std::uint8_t* src,
                                     std::int64_t lds, const std::int32_t* rmap) {
@@ -245,16 +370,27 @@ void ech_panel(std::uint32_t p, std::int64_t rows, std::int64_t c0, std::int64_t
   if (w != kW || wc > w) throw std::invalid_argument("ech_panel: panel width must be 32");
   if ((ldg & 15) || (reinterpret_cast<std::uintptr_t>(G) & 15))
     throw std::invalid_argument("ech_panel: G must be 16-byte aligned");
-  const std::size_t smem = std::size_t(rows) * (kW + 1);
-  if (smem > std::size_t(kPanelSmem)) throw std::invalid_argument("ech_panel: block too tall");
   static bool attr = false;
   if (!attr) {
     GFQ_CUDA(cudaFuncSetAttribute(ech_panel_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   kPanelSmem));
+    GFQ_CUDA(cudaFuncSetAttribute(ech_panel_gf2_kernel,
+                                  cudaFuncAttributeMaxDynamicSharedMemorySize, kPanelSmem));
     attr = true;
   }
   const std::int64_t r32 = (rows + 31) / 32 * 32;
   const int threads = r32 >= 1024 ? 1024 : int(r32 < 64 ? 64 : r32);
+  if (p == 2) {
+    const std::size_t smem2 = std::size_t(rows) * 5;
+    if (smem2 > std::size_t(kPanelSmem)) throw std::invalid_argument("ech_panel: block too tall");
+    ech_panel_gf2_kernel<<<1, threads, smem2, s>>>(int(rows), int(c0), int(wc), Aug, ld, flags,
+                                                   info, int(cap), G, ldg, rho2);
+    GFQ_CUDA(cudaGetLastError());
+    count_launch();
+    return;
+  }
+  const std::size_t smem = std::size_t(rows) * (kW + 1);
+  if (smem > std::size_t(kPanelSmem)) throw std::invalid_argument("ech_panel: block too tall");
   const std::uint32_t magic = static_cast<std::uint32_t>((0x100000000ULL / p) + 1);
   ech_panel_kernel<<<1, threads, smem, s>>>(p, magic, int(rows), int(c0), int(wc), int(w), Aug, ld,
                                             flags, info, int(cap), G, ldg, rho2);

@@ -4,6 +4,7 @@
 //   K2 base case (single-CTA Gauss-Jordan ECH in shared memory),
 //   K6 (counter-form SplitMix64 generator).
 // The tensor-core contraction lives in gf_mad_tc.cu.
+#include <algorithm>
 #include <atomic>
 #include <mutex>
 #include <vector>
@@ -87,6 +88,96 @@ mad_simt_kernel(std::uint32_t p, std::uint32_t magic, int m, int n, int k,
       std::uint32_t v = acc[i][j];
       if (Cin) v += Cin[std::int64_t(gr) * ldc + gc];
       D[std::int64_t(gr) * ldd + gc] = static_cast<std::uint8_t>(modp(v, p, magic));
+    }
+  }
+}
+
+// Small-K contraction (K <= 32): the rank-r' updates of UpdateRow /
+// ClearDown when a block row contributes few new pivots (the
+// K in 1..7 class).  HBM-bound: each thread owns 16 consecutive outputs of
+// one row (one uint4 of D and of Cin), the K coefficients of its A row and
+// the K x 16-byte slab of B (both L1/L2 resident across threads).
+constexpr int kSmallK = 32;
+__global__ void __launch_bounds__(256)
+mad_smallk_kernel(std::uint32_t p, std::uint32_t magic, int m, int n, int k,
+                  const std::uint8_t* __restrict__ A, std::int64_t lda,
+                  const std::uint8_t* __restrict__ B, std::int64_t ldb,
+                  const std::uint8_t* Cin, std::int64_t ldc, std::uint8_t* D, std::int64_t ldd) {
+  const int nvec = (n + 15) >> 4;
+  const std::int64_t tid = std::int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  const std::int64_t total = std::int64_t(m) * nvec;
+  for (std::int64_t e = tid; e < total; e += std::int64_t(gridDim.x) * blockDim.x) {
+    const int i = int(e / nvec), v = int(e % nvec);
+    const int j0 = v << 4;
+    const bool full = j0 + 16 <= n;
+    const std::uint8_t* arow = A + std::int64_t(i) * lda;
+    std::uint32_t acc[16];
+    if (p == 2) {
+      uint4 x = make_uint4(0, 0, 0, 0);
+      for (int t = 0; t < k; ++t) {
+        if (!arow[t]) continue;
+        const std::uint8_t* brow = B + std::int64_t(t) * ldb + j0;
+        uint4 b;
+        if (full) {
+          b = *reinterpret_cast<const uint4*>(brow);
+        } else {
+          std::uint32_t w[4] = {0, 0, 0, 0};
+          for (int c = 0; c < n - j0; ++c) w[c >> 2] |= std::uint32_t(brow[c]) << (8 * (c & 3));
+          b = make_uint4(w[0], w[1], w[2], w[3]);
+        }
+        x.x ^= b.x;
+        x.y ^= b.y;
+        x.z ^= b.z;
+        x.w ^= b.w;
+      }
+      const std::uint32_t xw[4] = {x.x, x.y, x.z, x.w};
+#pragma unroll
+      for (int c = 0; c < 16; ++c) acc[c] = (xw[c >> 2] >> (8 * (c & 3))) & 1;
+    } else {
+#pragma unroll
+      for (int c = 0; c < 16; ++c) acc[c] = 0;
+      for (int t = 0; t < k; ++t) {
+        const std::uint32_t a = arow[t];
+        if (!a) continue;
+        const std::uint8_t* brow = B + std::int64_t(t) * ldb + j0;
+        if (full) {
+          const uint4 b = *reinterpret_cast<const uint4*>(brow);
+          const std::uint32_t bw[4] = {b.x, b.y, b.z, b.w};
+#pragma unroll
+          for (int c = 0; c < 16; ++c) acc[c] += a * ((bw[c >> 2] >> (8 * (c & 3))) & 0xFF);
+        } else {
+          for (int c = 0; c < n - j0; ++c) acc[c] += a * brow[c];
+        }
+      }
+    }
+    const std::uint8_t* crow = Cin ? Cin + std::int64_t(i) * ldc + j0 : nullptr;
+    std::uint8_t* drow = D + std::int64_t(i) * ldd + j0;
+    if (full) {
+      std::uint32_t cw[4] = {0, 0, 0, 0};
+      if (crow) {
+        const uint4 cv = *reinterpret_cast<const uint4*>(crow);
+        cw[0] = cv.x;
+        cw[1] = cv.y;
+        cw[2] = cv.z;
+        cw[3] = cv.w;
+      }
+      std::uint32_t ow[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        std::uint32_t word = 0;
+#pragma unroll
+        for (int by = 0; by < 4; ++by) {
+          const std::uint32_t x = acc[4 * q + by] + ((cw[q] >> (8 * by)) & 0xFF);
+          word |= (p == 2 ? (x & 1) : modp(x, p, magic)) << (8 * by);
+        }
+        ow[q] = word;
+      }
+      *reinterpret_cast<uint4*>(drow) = make_uint4(ow[0], ow[1], ow[2], ow[3]);
+    } else {
+      for (int c = 0; c < n - j0; ++c) {
+        const std::uint32_t x = acc[c] + (crow ? crow[c] : 0);
+        drow[c] = std::uint8_t(modp(x, p, magic));
+      }
     }
   }
 }
@@ -203,7 +294,22 @@ void mad(std::uint32_t p, std::int64_t m, std::int64_t n, std::int64_t k,
     GFQ_CUDA(cudaEventRecord(rec.e0, s));
   }
   bool done = false;
-  if (pol != 1 && k > 0 && (pol == 2 || big)) {
+  const auto al = [](const void* q, std::int64_t ld) {
+    return q == nullptr || ((reinterpret_cast<std::uintptr_t>(q) & 15) == 0 && (ld & 15) == 0);
+  };
+  if (pol != 2 && k >= 1 && k <= kSmallK && al(B, ldb) && al(Cin, ldc) && al(D, ldd)) {
+    ++g_simt;
+    rec.path = 1;
+    const std::int64_t total = m * ((n + 15) / 16);
+    const std::int64_t cap = std::int64_t(sm_count()) * 8;
+    const unsigned grid = unsigned(std::min<std::int64_t>((total + 255) / 256, cap));
+    mad_smallk_kernel<<<grid, 256, 0, s>>>(p, magic_of(p), int(m), int(n), int(k), A, lda, B, ldb,
+                                           Cin, ldc, D, ldd);
+    GFQ_CUDA(cudaGetLastError());
+    count_launch();
+    done = true;
+  }
+  if (!done && pol != 1 && k > 0 && (pol == 2 || big)) {
     if (mad_tc(p, m, n, k, A, lda, B, ldb, Cin, ldc, D, ldd, s)) {
       ++g_tc;
       done = true;
