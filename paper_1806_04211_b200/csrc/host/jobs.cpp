@@ -253,6 +253,31 @@ EchResult direct_ech(const FieldSpec& f, const Mat& h) {
   return out;
 }
 
+// Read back the pivots (the one host round trip of a device ECH) and gather
+// M, K, R from the reduced Aug = [W | T] (T uncompacted: column t = original
+// row t) in the reference's conventions.
+EchResult extract_ech(std::int64_t a, std::int64_t b, const Mat& aug, const std::int32_t* inf,
+                      std::int64_t cap) {
+  std::vector<std::int32_t> hi(std::size_t(1 + 2 * cap));
+  download_i32(inf, hi.data(), hi.size());
+  const std::int64_t r = hi[0];
+  std::vector<std::int32_t> pcol(hi.begin() + 1, hi.begin() + 1 + r);
+  std::vector<std::int32_t> prow(hi.begin() + 1 + cap, hi.begin() + 1 + cap + r);
+  EchResult out;
+  std::vector<std::uint32_t> rho(prow.begin(), prow.end());
+  std::sort(rho.begin(), rho.end());
+  out.rho = IndexSet(std::size_t(a), rho);
+  out.gamma = IndexSet(std::size_t(b), std::vector<std::uint32_t>(pcol.begin(), pcol.end()));
+  const auto tcols = as_i32(rho);
+  const auto krows = as_i32(index_set_complement(out.rho).members);
+  const auto gcols = as_i32(index_set_complement(out.gamma).members);
+  const Mat W = aug.col_view(0, b), T = aug.col_view(b, a);
+  out.M = select(r, r, T, nullptr, &prow, &tcols);
+  out.K = select(a - r, r, T, nullptr, &krows, &tcols);
+  out.R = select(r, b - r, W, nullptr, &prow, &gcols);
+  return out;
+}
+
 // Device ECH: right-looking panel Gauss-Jordan on Aug = [W | T] (T = I), one
 // K2 panel launch + a row gather + two K1 launches per 32-column panel, no
 // host round trip until the pivots are read back at the end.  Outputs in the
@@ -261,6 +286,15 @@ EchResult panel_ech(const FieldSpec& f, const Mat& h) {
   const std::int64_t a = h.rows(), b = h.cols(), w = 32;
   const std::int64_t cap = std::min(a, b);
   const cudaStream_t s = cur_stream();
+  if (f.p() == 2 && a <= 1024 && (a + b + 31) / 32 <= 256) {
+    // GF(2): the whole ECH in one bit-packed single-CTA launch
+    Mat aug(a, b + a);
+    DevBuf scratch{static_cast<std::size_t>(4 * dev::ech_gf2_scratch_words(a, b))};
+    DevBuf info{static_cast<std::size_t>(4 * (1 + 2 * cap))};
+    dev::ech_gf2_block(a, b, h.data(), h.ld(), reinterpret_cast<std::uint32_t*>(scratch.ptr),
+                       aug.data(), aug.ld(), reinterpret_cast<std::int32_t*>(info.ptr), cap, s);
+    return extract_ech(a, b, aug, reinterpret_cast<const std::int32_t*>(info.ptr), cap);
+  }
   Mat aug = Mat::zeros(a, b + a);
   dev::select2d(aug.data(), aug.ld(), a, b, h.data(), h.ld(), nullptr, 0, nullptr, nullptr, s);
   {
@@ -288,24 +322,7 @@ EchResult panel_ech(const FieldSpec& f, const Mat& h) {
     dev::mad(f.p(), a, n, w, G.data(), G.ld(), Bp.data(), Bp.ld(), aug.data() + c0, aug.ld(),
              aug.data() + c0, aug.ld(), s);
   }
-  std::vector<std::int32_t> hi(std::size_t(1 + 2 * cap));
-  download_i32(inf, hi.data(), hi.size());
-  const std::int64_t r = hi[0];
-  std::vector<std::int32_t> pcol(hi.begin() + 1, hi.begin() + 1 + r);
-  std::vector<std::int32_t> prow(hi.begin() + 1 + cap, hi.begin() + 1 + cap + r);
-  EchResult out;
-  std::vector<std::uint32_t> rho(prow.begin(), prow.end());
-  std::sort(rho.begin(), rho.end());
-  out.rho = IndexSet(std::size_t(a), rho);
-  out.gamma = IndexSet(std::size_t(b), std::vector<std::uint32_t>(pcol.begin(), pcol.end()));
-  const auto tcols = as_i32(rho);
-  const auto krows = as_i32(index_set_complement(out.rho).members);
-  const auto gcols = as_i32(index_set_complement(out.gamma).members);
-  const Mat W = aug.col_view(0, b), T = aug.col_view(b, a);
-  out.M = select(r, r, T, nullptr, &prow, &tcols);
-  out.K = select(a - r, r, T, nullptr, &krows, &tcols);
-  out.R = select(r, b - r, W, nullptr, &prow, &gcols);
-  return out;
+  return extract_ech(a, b, aug, inf, cap);
 }
 
 // Split point: half, rounded to a multiple of 16 so column views keep the

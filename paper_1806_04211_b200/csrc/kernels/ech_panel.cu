@@ -16,6 +16,8 @@
 // so that Aug[:, c0:] += G.Aug[rho2, c0:] finishes the panel (K1).  Nothing
 // returns to the host until the last panel: the ECH is a fixed launch
 // sequence.
+#include <cstdlib>
+
 #include "../common.hpp"
 #include "kernels.hpp"
 
@@ -349,6 +351,133 @@ ech_panel_gf2_kernel(int rows, int c0, int wc, const std::uint8_t* __restrict__ 
   }
 }
 
+// GF(2), rows <= 1024: the pivot chain of the panel runs in ONE warp with
+// no block barriers.  Lane l owns rows 32r + l (r < 32) as 32-bit panel
+// words in registers; per column: a ballot-style mask of candidate rows,
+// a warp min-reduction (first non-pivotal row with the bit set), the pivot
+// word broadcast by shuffle and a masked XOR of the lane's rows.  The rest
+// of the CTA then writes G in parallel.
+__global__ void __launch_bounds__(1024)
+ech_panel_gf2w_kernel(int rows, int c0, int wc, const std::uint8_t* __restrict__ Aug,
+                      std::int64_t ld, std::uint8_t* flags, std::int32_t* info, int cap,
+                      std::uint8_t* G, std::int64_t ldg, std::int32_t* rho2) {
+  __shared__ std::uint32_t orig[1024];
+  __shared__ int pc[kW], pr[kW];
+  __shared__ std::uint32_t n2[kW];
+  __shared__ int r2_s;
+  const int tid = threadIdx.x, nt = blockDim.x, lane = tid & 31;
+
+  for (int i = tid; i < 1024; i += nt) {
+    std::uint32_t word = 0;
+    if (i < rows) {  // every row: G needs the panel bits of old pivot rows too
+      uint4 a, b;
+      load_seg(Aug + std::int64_t(i) * ld + c0, wc, a, b);
+      const std::uint32_t wds[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        const std::uint32_t v = wds[q] & 0x01010101u;
+        word |= ((v & 1u) | ((v >> 7) & 2u) | ((v >> 14) & 4u) | ((v >> 21) & 8u)) << (4 * q);
+      }
+    }
+    orig[i] = word;
+  }
+  __syncthreads();
+
+  if (tid < 32) {
+    std::uint32_t row[32];
+    std::uint32_t fm = 0;  // bit r: row 32r + lane is pivotal (or absent)
+#pragma unroll
+    for (int r = 0; r < 32; ++r) {
+      const int i = 32 * r + lane;
+      row[r] = orig[i];
+      if (i >= rows || flags[i]) fm |= 1u << r;
+    }
+    int r2 = 0;
+    for (int c = 0; c < wc; ++c) {
+      std::uint32_t cm = 0;
+#pragma unroll
+      for (int r = 0; r < 32; ++r) cm |= ((row[r] >> c) & 1u) << r;
+      cm &= ~fm;
+      unsigned cand = cm ? unsigned(32 * (__ffs(cm) - 1) + lane) : 0xFFFFFFFFu;
+      cand = __reduce_min_sync(0xffffffffu, cand);
+      if (cand == 0xFFFFFFFFu) continue;
+      const int sl = int(cand & 31), sr = int(cand >> 5);
+      std::uint32_t mine = 0;
+#pragma unroll
+      for (int r = 0; r < 32; ++r) mine = (r == sr) ? row[r] : mine;
+      const std::uint32_t ps = __shfl_sync(0xffffffffu, mine, sl);
+      if (lane == sl) {
+        cm &= ~(1u << sr);
+        fm |= 1u << sr;
+      }
+#pragma unroll
+      for (int r = 0; r < 32; ++r) row[r] ^= ps & (0u - ((cm >> r) & 1u));
+      if (lane == 0) {
+        pc[r2] = c;
+        pr[r2] = int(cand);
+      }
+      ++r2;
+    }
+    __syncwarp();
+    // N2 = inv(X), X[q][t] = bit pc[t] of the original word of row pr[q]
+    std::uint32_t x = 0, inv = 0;
+    if (lane < r2) {
+      const std::uint32_t ow = orig[pr[lane]];
+      for (int t = 0; t < r2; ++t) x |= ((ow >> pc[t]) & 1u) << t;
+      inv = 1u << lane;
+    }
+    for (int q = 0; q < r2; ++q) {
+      const unsigned bal = __ballot_sync(0xffffffffu, lane >= q && lane < r2 && ((x >> q) & 1u));
+      const int pv = __ffs(bal) - 1;
+      const std::uint32_t xq = __shfl_sync(0xffffffffu, x, q), iq = __shfl_sync(0xffffffffu, inv, q);
+      const std::uint32_t xp = __shfl_sync(0xffffffffu, x, pv), ip = __shfl_sync(0xffffffffu, inv, pv);
+      if (lane == q) {
+        x = xp;
+        inv = ip;
+      } else if (lane == pv) {
+        x = xq;
+        inv = iq;
+      }
+      const std::uint32_t px = __shfl_sync(0xffffffffu, x, q), pi = __shfl_sync(0xffffffffu, inv, q);
+      if (lane != q && ((x >> q) & 1u)) {
+        x ^= px;
+        inv ^= pi;
+      }
+    }
+    n2[lane] = lane < r2 ? inv : 0u;
+    rho2[lane] = lane < r2 ? pr[lane] : -1;
+    const int r_old = info[0];
+    if (lane < r2) {
+      info[1 + r_old + lane] = c0 + pc[lane];
+      info[1 + cap + r_old + lane] = pr[lane];
+      flags[pr[lane]] = 1;
+    }
+    __syncwarp();
+    if (lane == 0) {
+      info[0] = r_old + r2;
+      r2_s = r2;
+    }
+  }
+  __syncthreads();
+  // G[i] = (orig bits of row i at gamma2, + e on its own pivot) . N2
+  const int r2 = r2_s;
+  for (int i = tid; i < rows; i += nt) {
+    const std::uint32_t ow = orig[i];
+    std::uint32_t g = 0;
+    for (int q = 0; q < r2; ++q)
+      if (((ow >> pc[q]) & 1u) ^ (pr[q] == i ? 1u : 0u)) g ^= n2[q];
+    std::uint32_t outw[8];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      const std::uint32_t nib = (g >> (4 * q)) & 0xFu;
+      outw[q] = (nib & 1u) | ((nib & 2u) << 7) | ((nib & 4u) << 14) | ((nib & 8u) << 21);
+    }
+    uint4* dst = reinterpret_cast<uint4*>(G + std::int64_t(i) * ldg);
+    dst[0] = make_uint4(outw[0], outw[1], outw[2], outw[3]);
+    dst[1] = make_uint4(outw[4], outw[5], outw[6], outw[7]);
+  }
+}
+
 __global__ void scatter_rows_kernel(std::uint8_t* dst, std::int64_t ldd, std::int64_t rows,
                                     std::int64_t cols, const std::uint8_t* src,
                                     std::int64_t lds, const std::int32_t* rmap) {
@@ -378,8 +507,22 @@ void ech_panel(std::uint32_t p, std::int64_t rows, std::int64_t c0, std::int64_t
                                   cudaFuncAttributeMaxDynamicSharedMemorySize, kPanelSmem));
     attr = true;
   }
+  // Threads per panel CTA: each thread owns rows/threads rows; fewer warps
+  // make the per-column barriers cheaper (GFQ_PANEL_THREADS overrides).
+  static const int max_threads = [] {
+    const char* e = std::getenv("GFQ_PANEL_THREADS");
+    const int v = e ? std::atoi(e) : 0;
+    return v >= 64 && v <= 1024 ? v : 1024;
+  }();
   const std::int64_t r32 = (rows + 31) / 32 * 32;
-  const int threads = r32 >= 1024 ? 1024 : int(r32 < 64 ? 64 : r32);
+  const int threads = r32 >= max_threads ? max_threads : int(r32 < 64 ? 64 : r32);
+  if (p == 2 && rows <= 1024) {
+    ech_panel_gf2w_kernel<<<1, 1024, 0, s>>>(int(rows), int(c0), int(wc), Aug, ld, flags, info,
+                                             int(cap), G, ldg, rho2);
+    GFQ_CUDA(cudaGetLastError());
+    count_launch();
+    return;
+  }
   if (p == 2) {
     const std::size_t smem2 = std::size_t(rows) * 5;
     if (smem2 > std::size_t(kPanelSmem)) throw std::invalid_argument("ech_panel: block too tall");

@@ -285,7 +285,10 @@ void mad(std::uint32_t p, std::int64_t m, std::int64_t n, std::int64_t k,
   // The tcgen05 path pays a prologue (TMEM alloc, barrier init, descriptor
   // fetch) of a few microseconds; below ~4 Mi MACs or for K < 32 (one MMA
   // instruction) the SIMT kernel is as fast and exactly as exact.
-  const bool big = k >= 32 && (double(m) * double(n) * double(k) >= 4.0 * 1024 * 1024);
+  // Deep-K skinny products (e.g. n = 1 when a block column has one
+  // remaining non-pivot column) also belong on K1: the SIMT tile kernel
+  // would stream K through 64-wide tiles with a tiny grid.
+  const bool big = k >= 32 && (double(m) * double(n) * double(k) >= 4.0 * 1024 * 1024 || k >= 128);
   const bool prof = g_profile;
   ProfRec rec{nullptr, nullptr, 2.0 * double(m) * double(n) * double(k), 0};
   if (prof) {

@@ -96,6 +96,16 @@ void ech_panel(std::uint32_t p, std::int64_t rows, std::int64_t c0, std::int64_t
                std::int32_t* info, std::int64_t cap, std::uint8_t* G, std::int64_t ldg,
                std::int32_t* rho2, cudaStream_t s);
 
+// GF(2) block ECH in one launch (rows <= 1024, cols + rows <= 8192): the
+// reduced [W | T] is written to Out (rows x (cols + rows) u8) and the pivots
+// to info = [rank, cols[cap], rows[cap]].  scratch holds
+// ech_gf2_scratch_words() 32-bit words.  Returns false (nothing launched)
+// when the block is outside those limits.
+bool ech_gf2_block(std::int64_t rows, std::int64_t cols, const std::uint8_t* H, std::int64_t ldh,
+                   std::uint32_t* scratch, std::uint8_t* Out, std::int64_t ldo, std::int32_t* info,
+                   std::int64_t cap, cudaStream_t s);
+std::int64_t ech_gf2_scratch_words(std::int64_t rows, std::int64_t cols);
+
 // dst[rmap[i]] = src[i] for rmap[i] >= 0 (row scatter).
 void scatter_rows(std::uint8_t* dst, std::int64_t ldd, std::int64_t rows, std::int64_t cols,
                   const std::uint8_t* src, std::int64_t lds, const std::int32_t* rmap,

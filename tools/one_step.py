@@ -18,6 +18,9 @@ f = G.FieldSpec(cfg["p"])
 C = G.random_matrix(f, cfg["m"], cfg["n"], cfg["seed"]) if cfg["kind"] == "random" else \
     G.random_product_matrix(f, cfg["m"], cfg["n"], cfg["inner"], cfg["seed"])
 G.synchronize()
+if "--warm" in sys.argv:
+    G.echelonize(C, f, G.EchelonizeOptions(block=cfg["block"], threads=threads))
+    G.synchronize()
 t0 = time.time()
 out = G.echelonize(C, f, G.EchelonizeOptions(block=cfg["block"], threads=threads,
                                              collect_trace="--trace" in sys.argv))
