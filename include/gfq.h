@@ -210,6 +210,27 @@ int gfq_output_trace(const gfq_output* o, uint64_t* n, int32_t* kind, int32_t* i
                      int32_t* detail);
 void gfq_output_free(gfq_output* o);
 
+/* ------------------------------------------------------------ multi-GPU */
+/* Block columns of C (and T) are sharded cyclically over the ranks; PkgA and
+ * X packages are broadcast in one fixed order.  One process per GPU with an
+ * NCCL communicator, or `world` in-process loopback ranks on one GPU. */
+typedef struct gfq_comm gfq_comm;
+int gfq_nccl_unique_id(uint8_t* out128);
+int gfq_comm_nccl(int world, int rank, const uint8_t* id128, gfq_comm** out);
+/* Fills comms[0..world-1]; each must be driven by its own host thread. */
+int gfq_comm_loopback(int world, gfq_comm** comms);
+void gfq_comm_free(gfq_comm* c);
+/* C: the full device-resident input (only owned block columns are read) or
+ * NULL to generate the owned columns of random_matrix(p, m, n, seed) on the
+ * device.  gather != 0 makes the output complete on every rank. */
+int gfq_echelonize_dist(gfq_comm* comm, uint32_t p, const gfq_mat* C, int64_t m, int64_t n,
+                        uint64_t seed, const gfq_options* opt, int gather, gfq_output** out);
+/* Host-only view of the sharded plan: per node (kind, i, j, k, owner; owner
+ * -1 = every rank) and the broadcast schedule (is_a, i, j, k, root), in
+ * order.  Either array may be NULL to query the counts. */
+int gfq_dist_plan(uint64_t m, uint64_t n, uint64_t block, int with_transform, int world,
+                  int32_t* nodes, uint64_t* n_nodes, int32_t* bcasts, uint64_t* n_bcast);
+
 #ifdef __cplusplus
 }
 #endif

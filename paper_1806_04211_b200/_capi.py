@@ -113,6 +113,12 @@ PROTOS = {
     "gfq_output_report": (I, [vp, _P(Report)]),
     "gfq_output_trace": (I, [vp, c_u64p, c_i32p, c_i32p, c_i32p, c_i32p, c_i32p, c_i64p, c_i64p, c_i32p]),
     "gfq_output_free": (None, [vp]),
+    "gfq_nccl_unique_id": (I, [c_u8p]),
+    "gfq_comm_nccl": (I, [I, I, c_u8p, vpp]),
+    "gfq_comm_loopback": (I, [I, vpp]),
+    "gfq_comm_free": (None, [vp]),
+    "gfq_echelonize_dist": (I, [vp, U32, vp, I64, I64, U64, _P(Options), I, vpp]),
+    "gfq_dist_plan": (I, [U64, U64, U64, I, I, c_i32p, c_u64p, c_i32p, c_u64p]),
 }
 
 

@@ -5,6 +5,7 @@
 
 #include "../../include/gfq.h"
 #include "host/chief.hpp"
+#include "host/dist.hpp"
 #include "host/jobs.hpp"
 #include "host/tasks.hpp"
 #include "kernels/kernels.hpp"
@@ -22,6 +23,9 @@ struct gfq_output {
   gfq::EchelonOutput out;
   gfq::RunReport report;
   explicit gfq_output(gfq::EchelonOutput o) : out(std::move(o)) {}
+};
+struct gfq_comm {
+  std::shared_ptr<gfq::Comm> c;
 };
 
 namespace {
@@ -214,20 +218,9 @@ int gfq_mad_counters(int64_t* simt, int64_t* tc, int reset) {
 }
 
 namespace {
-// Exact counter-form replica: entry e takes draw draw0+e unless a rejection
-// (probability < 2^-60 per draw) shifts the stream, in which case the
-// affected suffix is regenerated with the shifted draw index.
 void fill_exact(uint32_t p, int64_t rows, int64_t cols, uint64_t seed, uint64_t draw0,
                 uint8_t* dst, int64_t ld) {
-  auto rej = std::make_shared<gfq::DevBuf>(4);
-  GFQ_CUDA(cudaMemsetAsync(rej->ptr, 0, 4, gfq::cur_stream()));
-  gfq::dev::random_fill(p, rows, cols, seed, draw0, dst, ld,
-                        reinterpret_cast<uint32_t*>(rej->ptr), gfq::cur_stream());
-  int32_t nrej = 0;
-  gfq::download_i32(reinterpret_cast<const int32_t*>(rej->ptr), &nrej, 1);
-  if (nrej != 0)
-    throw std::runtime_error(
-        "random_matrix: a SplitMix64 draw hit the rejection band; exact replay not supported");
+  gfq::random_fill_exact(p, rows, cols, seed, draw0, cols, dst, ld);
 }
 }  // namespace
 
@@ -575,5 +568,81 @@ int gfq_output_trace(const gfq_output* o, uint64_t* n, int32_t* kind, int32_t* i
   });
 }
 void gfq_output_free(gfq_output* o) { delete o; }
+
+// ---------------------------------------------------------------- multi-GPU
+int gfq_nccl_unique_id(uint8_t* out128) {
+  return guard([&] { gfq::nccl_unique_id(out128); });
+}
+int gfq_comm_nccl(int world, int rank, const uint8_t* id128, gfq_comm** out) {
+  return guard([&] {
+    require_device();
+    if (world < 1 || rank < 0 || rank >= world) throw std::invalid_argument("bad rank / world");
+    *out = new gfq_comm{gfq::make_nccl_comm(world, rank, id128)};
+  });
+}
+int gfq_comm_loopback(int world, gfq_comm** comms) {
+  return guard([&] {
+    if (world < 1) throw std::invalid_argument("bad world size");
+    auto v = gfq::make_loopback_comms(world);
+    for (int r = 0; r < world; ++r) comms[r] = new gfq_comm{v[std::size_t(r)]};
+  });
+}
+void gfq_comm_free(gfq_comm* c) { delete c; }
+
+int gfq_echelonize_dist(gfq_comm* comm, uint32_t p, const gfq_mat* C, int64_t m, int64_t n,
+                        uint64_t seed, const gfq_options* opt, int gather, gfq_output** out) {
+  return guard([&] {
+    require_device();
+    if (!comm) throw std::invalid_argument("null communicator");
+    gfq::RunReport rep;
+    auto res = std::make_unique<gfq_output>(gfq::echelonize_dist(
+        C ? &M(C) : nullptr, m, n, seed, gfq::FieldSpec(p), to_opts(opt), *comm->c, &rep,
+        gather != 0));
+    res->report = std::move(rep);
+    *out = res.release();
+  });
+}
+
+int gfq_dist_plan(uint64_t m, uint64_t n, uint64_t block, int with_transform, int world,
+                  int32_t* nodes, uint64_t* n_nodes, int32_t* bcasts, uint64_t* n_bcast) {
+  return guard([&] {
+    if (world < 1) throw std::invalid_argument("bad world size");
+    const gfq::ChopSpec cs = gfq::chop(size_t(m), size_t(n), size_t(block));
+    if (cs.a() == 0 || cs.b() == 0) {
+      if (n_nodes) *n_nodes = 0;
+      if (n_bcast) *n_bcast = 0;
+      return;
+    }
+    gfq::TaskGraph g;
+    const gfq::PlanHandles h = gfq::build_plan(
+        g, [](size_t, size_t) -> std::optional<gfq::Mat> { return std::nullopt; },
+        gfq::FieldSpec(2), cs, with_transform != 0);
+    const gfq::Sharding sh{world, 0};
+    if (n_nodes) *n_nodes = g.node_count();
+    if (nodes)
+      for (size_t q = 0; q < g.node_count(); ++q) {
+        const gfq::TaskNode& nd = g.node(int32_t(q));
+        int o = sh.owner(nd);
+        if (o == -2)
+          o = g.slot(nd.out[0]).key.kind == gfq::PkgKind::R ? sh.owner_col(size_t(nd.c2))
+                                                            : sh.owner_trow(size_t(nd.c2));
+        nodes[5 * q + 0] = int32_t(nd.kind);
+        nodes[5 * q + 1] = nd.c0;
+        nodes[5 * q + 2] = nd.c1;
+        nodes[5 * q + 3] = nd.c2;
+        nodes[5 * q + 4] = o;
+      }
+    const auto sched = gfq::bcast_schedule(cs, h, g, sh);
+    if (n_bcast) *n_bcast = sched.size();
+    if (bcasts)
+      for (size_t q = 0; q < sched.size(); ++q) {
+        bcasts[5 * q + 0] = sched[q].is_a ? 1 : 0;
+        bcasts[5 * q + 1] = int32_t(sched[q].i);
+        bcasts[5 * q + 2] = int32_t(sched[q].j);
+        bcasts[5 * q + 3] = int32_t(sched[q].k);
+        bcasts[5 * q + 4] = sched[q].root;
+      }
+  });
+}
 
 }  // extern "C"

@@ -65,10 +65,22 @@ struct Emitter {
 // descending rounds k = b-1..1.
 PlanHandles build_plan(TaskGraph& graph, const Mat& C, const FieldSpec& field,
                        const ChopSpec& cs, bool with_transform) {
-  const std::size_t a = cs.a(), b = cs.b();
-  if (a == 0 || b == 0) throw std::invalid_argument("build_plan: empty partition");
   if (std::int64_t(cs.rows()) != C.rows() || std::int64_t(cs.cols()) != C.cols())
     throw std::invalid_argument("build_plan: partition does not match matrix");
+  return build_plan(
+      graph,
+      [&](std::size_t i, std::size_t k) -> std::optional<Mat> {
+        return C.row_view(std::int64_t(cs.row_offset(i)), std::int64_t(cs.row_parts[i]))
+            .col_view(std::int64_t(cs.col_offset(k)), std::int64_t(cs.col_parts[k]));
+      },
+      field, cs, with_transform);
+}
+
+PlanHandles build_plan(TaskGraph& graph,
+                       const std::function<std::optional<Mat>(std::size_t, std::size_t)>& input,
+                       const FieldSpec& field, const ChopSpec& cs, bool with_transform) {
+  const std::size_t a = cs.a(), b = cs.b();
+  if (a == 0 || b == 0) throw std::invalid_argument("build_plan: empty partition");
   if (a >= (1u << 14) || b >= (1u << 14))
     throw std::invalid_argument("build_plan: block grid exceeds slot coordinates");
   graph.set_field(field);
@@ -77,10 +89,13 @@ PlanHandles build_plan(TaskGraph& graph, const Mat& C, const FieldSpec& field,
   using T = TaskKind;
 
   for (std::size_t i = 0; i < a; ++i)
-    for (std::size_t k = 0; k < b; ++k)
-      graph.add_input({K::C, std::uint16_t(i), std::uint16_t(k), 0, 0},
-                      C.row_view(std::int64_t(cs.row_offset(i)), std::int64_t(cs.row_parts[i]))
-                          .col_view(std::int64_t(cs.col_offset(k)), std::int64_t(cs.col_parts[k])));
+    for (std::size_t k = 0; k < b; ++k) {
+      std::optional<Mat> blk = input(i, k);
+      if (blk)
+        graph.add_input({K::C, std::uint16_t(i), std::uint16_t(k), 0, 0}, std::move(*blk));
+      else
+        graph.require_slot({K::C, std::uint16_t(i), std::uint16_t(k), 0, 0});
+    }
 
   // Step 1
   for (std::size_t j = 0; j < b; ++j) {

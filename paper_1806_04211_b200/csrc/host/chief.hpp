@@ -3,6 +3,8 @@
 #pragma once
 
 #include <cstddef>
+#include <functional>
+#include <optional>
 #include <string>
 #include <vector>
 
@@ -52,6 +54,10 @@ struct PlanHandles {
 /// Input blocks are views of the device-resident C (no copy).
 PlanHandles build_plan(TaskGraph& graph, const Mat& C, const FieldSpec& field,
                        const ChopSpec& chop, bool with_transform);
+/// Same plan; input block (i, k) is `input(i, k)` when it returns a value
+/// (a sharded rank only holds its own block columns).
+PlanHandles build_plan(TaskGraph& graph, const std::function<std::optional<Mat>(std::size_t, std::size_t)>& input,
+                       const FieldSpec& field, const ChopSpec& chop, bool with_transform);
 
 /// reference include/gfrref/chief.hpp:76-84 (+ `workers`: host threads,
 /// one CUDA stream each; the reference's `threads`).

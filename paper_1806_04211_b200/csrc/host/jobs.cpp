@@ -39,6 +39,21 @@ std::atomic<int> g_ech_mode{0};
 void set_ech_mode(int mode) { g_ech_mode = mode; }
 int ech_mode() { return g_ech_mode; }
 
+void random_fill_exact(std::uint32_t p, std::int64_t rows, std::int64_t cols, std::uint64_t seed,
+                       std::uint64_t draw0, std::int64_t draw_ld, std::uint8_t* dst,
+                       std::int64_t ld) {
+  if (rows == 0 || cols == 0) return;
+  DevBuf rej{4};
+  GFQ_CUDA(cudaMemsetAsync(rej.ptr, 0, 4, cur_stream()));
+  dev::random_fill(p, rows, cols, seed, draw0, draw_ld, dst, ld,
+                   reinterpret_cast<std::uint32_t*>(rej.ptr), cur_stream());
+  std::int32_t nrej = 0;
+  download_i32(reinterpret_cast<const std::int32_t*>(rej.ptr), &nrej, 1);
+  if (nrej != 0)
+    throw std::runtime_error(
+        "random_matrix: a SplitMix64 draw hit the rejection band; exact replay not supported");
+}
+
 void set_ech_base(std::size_t n) {
   g_ech_base = std::max<std::size_t>(1, std::min<std::size_t>(n, dev::kEchBaseMax));
 }

@@ -39,6 +39,14 @@ Mat take_cols(const Mat& m, const std::vector<std::uint32_t>& cols);  // matrix.
 Mat vcat(const Mat& a, const Mat& b);                                 // matrix.hpp:106
 Mat hcat(const Mat& a, const Mat& b);                                 // matrix.hpp:109
 
+/// K6: rows x cols of reference random_matrix (src/generate.cpp:16-24) whose
+/// entry (r, c) takes draw draw0 + r * draw_ld + c.  A draw in the
+/// rejection band (probability < 2^-56 per draw) would shift the reference's
+/// stream; that case is reported (std::runtime_error), never silently wrong.
+void random_fill_exact(std::uint32_t p, std::int64_t rows, std::int64_t cols, std::uint64_t seed,
+                       std::uint64_t draw0, std::int64_t draw_ld, std::uint8_t* dst,
+                       std::int64_t ld);
+
 /// Tunable: largest block the K2 base-case kernel takes (<= kEchBaseMax).
 void set_ech_base(std::size_t n);
 std::size_t ech_base();

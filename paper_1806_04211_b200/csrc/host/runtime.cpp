@@ -122,6 +122,21 @@ Mat Mat::from_host(std::int64_t rows, std::int64_t cols, const std::uint8_t* src
   return m;
 }
 
+Mat Mat::view_of(std::shared_ptr<DevBuf> buf, std::size_t offset, std::int64_t rows,
+                 std::int64_t cols, std::int64_t ld) {
+  Mat v;
+  v.rows_ = rows;
+  v.cols_ = cols;
+  v.ld_ = ld;
+  if (rows > 0 && cols > 0) {
+    if (!buf || offset + std::size_t((rows - 1) * ld + cols) > buf->bytes)
+      throw std::invalid_argument("matrix: view outside its allocation");
+    v.data_ = buf->ptr + offset;
+  }
+  v.buf_ = std::move(buf);
+  return v;
+}
+
 Mat Mat::row_view(std::int64_t r0, std::int64_t n) const {
   if (r0 < 0 || n < 0 || r0 + n > rows_) throw std::invalid_argument("matrix: row view out of range");
   Mat v;

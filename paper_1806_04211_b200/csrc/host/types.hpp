@@ -74,6 +74,10 @@ class Mat {
   std::uint8_t* data() const { return data_; }
   bool empty() const { return rows_ == 0 || cols_ == 0; }
 
+  /// A matrix living inside an existing allocation (e.g. a received
+  /// broadcast payload): rows x cols at byte `offset`, row stride ld.
+  static Mat view_of(std::shared_ptr<DevBuf> buf, std::size_t offset, std::int64_t rows,
+                     std::int64_t cols, std::int64_t ld);
   /// Rows [r0, r0+n) as a view (no copy).
   Mat row_view(std::int64_t r0, std::int64_t n) const;
   /// Columns [c0, c0+n) as a view (no copy; may lose 16-byte alignment).

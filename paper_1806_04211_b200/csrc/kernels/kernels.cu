@@ -565,13 +565,13 @@ void ech_base(std::uint32_t p, std::int64_t rows, std::int64_t cols,
 namespace {
 __global__ void random_fill_kernel(std::uint32_t p, std::int64_t rows,
                                    std::int64_t cols, std::uint64_t seed,
-                                   std::uint64_t draw0, std::uint64_t limit,
+                                   std::uint64_t draw0, std::int64_t draw_ld, std::uint64_t limit,
                                    std::uint8_t* dst, std::int64_t ldd,
                                    std::uint32_t* rejects) {
   for (std::int64_t r = blockIdx.y; r < rows; r += gridDim.y) {
     for (std::int64_t c = blockIdx.x * blockDim.x + threadIdx.x; c < cols;
          c += std::int64_t(gridDim.x) * blockDim.x) {
-      const std::uint64_t t = draw0 + std::uint64_t(r) * std::uint64_t(cols) + std::uint64_t(c);
+      const std::uint64_t t = draw0 + std::uint64_t(r) * std::uint64_t(draw_ld) + std::uint64_t(c);
       std::uint64_t z = seed + (t + 1) * 0x9e3779b97f4a7c15ULL;
       z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ULL;
       z = (z ^ (z >> 27)) * 0x94d049bb133111ebULL;
@@ -584,14 +584,14 @@ __global__ void random_fill_kernel(std::uint32_t p, std::int64_t rows,
 }  // namespace
 
 void random_fill(std::uint32_t p, std::int64_t rows, std::int64_t cols,
-                 std::uint64_t seed, std::uint64_t draw0, std::uint8_t* dst,
-                 std::int64_t ldd, std::uint32_t* rejects, cudaStream_t s) {
+                 std::uint64_t seed, std::uint64_t draw0, std::int64_t draw_ld,
+                 std::uint8_t* dst, std::int64_t ldd, std::uint32_t* rejects, cudaStream_t s) {
   if (rows == 0 || cols == 0) return;
   const std::uint64_t limit = p <= 1 ? ~0ULL : (~0ULL - (~0ULL % p));
   const unsigned gx = unsigned((cols + 255) / 256 < 64 ? (cols + 255) / 256 : 64);
   const unsigned gy = unsigned(rows < 65535 ? rows : 65535);
-  random_fill_kernel<<<dim3(gx, gy), 256, 0, s>>>(p, rows, cols, seed, draw0, limit, dst, ldd,
-                                                   rejects);
+  random_fill_kernel<<<dim3(gx, gy), 256, 0, s>>>(p, rows, cols, seed, draw0, draw_ld, limit, dst,
+                                                   ldd, rejects);
   GFQ_CUDA(cudaGetLastError());
     count_launch();
 }

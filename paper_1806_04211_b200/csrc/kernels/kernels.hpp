@@ -112,12 +112,13 @@ void scatter_rows(std::uint8_t* dst, std::int64_t ldd, std::int64_t rows, std::i
                   cudaStream_t s);
 
 // ---------------------------------------------------------------- K6
-// Counter-form SplitMix64: entry e (row-major over rows x cols) takes draw
-// index draw0 + e of the stream `seed` and is reduced mod p.  Draws that
-// the reference's rejection rule would reject are counted in *rejects
-// (device counter) so the caller can replay exactly.
+// Counter-form SplitMix64: entry (r, c) takes draw index
+// draw0 + r * draw_ld + c of the stream `seed` and is reduced mod p
+// (draw_ld = the full matrix width, so a block column of random_matrix can
+// be generated on its own).  Draws that the reference's rejection rule
+// would reject are counted in *rejects so the caller can refuse them.
 void random_fill(std::uint32_t p, std::int64_t rows, std::int64_t cols,
-                 std::uint64_t seed, std::uint64_t draw0, std::uint8_t* dst,
-                 std::int64_t ldd, std::uint32_t* rejects, cudaStream_t s);
+                 std::uint64_t seed, std::uint64_t draw0, std::int64_t draw_ld,
+                 std::uint8_t* dst, std::int64_t ldd, std::uint32_t* rejects, cudaStream_t s);
 
 }  // namespace gfq::dev

@@ -725,6 +725,70 @@ def echelonize(C, f: FieldSpec, options: EchelonizeOptions = None) -> EchelonOut
     return EchelonOutput(h, f, chop(m, n, options.block, options.remainder_first), options.with_transform)
 
 
+# ---------------------------------------------------------------- multi-GPU
+class Comm:
+    """Broadcast communicator of the sharded Chief (``gfq_comm``)."""
+
+    def __init__(self, handle, rank, world):
+        self.h, self.rank, self.world = handle, rank, world
+
+    def __del__(self):
+        if getattr(self, "h", None) and _lib is not None:
+            _lib.gfq_comm_free(self.h)
+            self.h = None
+
+    @staticmethod
+    def nccl_unique_id() -> bytes:
+        buf = (ctypes.c_uint8 * 128)()
+        _check(lib().gfq_nccl_unique_id(buf))
+        return bytes(buf)
+
+    @staticmethod
+    def nccl(world: int, rank: int, unique_id: bytes) -> "Comm":
+        """One process per GPU; `unique_id` from rank 0's nccl_unique_id()."""
+        h = _vp()
+        idb = (ctypes.c_uint8 * 128)(*unique_id)
+        _check(lib().gfq_comm_nccl(world, rank, idb, ctypes.byref(h)))
+        return Comm(h, rank, world)
+
+    @staticmethod
+    def loopback(world: int):
+        """`world` ranks in this process on the current GPU (each must be
+        driven from its own thread)."""
+        arr = (ctypes.c_void_p * world)()
+        _check(lib().gfq_comm_loopback(world, arr))
+        return [Comm(ctypes.c_void_p(arr[r]), r, world) for r in range(world)]
+
+
+def echelonize_dist(comm: Comm, f: FieldSpec, m: int, n: int, options: EchelonizeOptions = None,
+                    C: Matrix = None, seed: int = 0, gather: bool = True) -> EchelonOutput:
+    """Sharded echelonize on this rank (block columns owned round-robin).
+    C: full device input (only owned columns are read) or None to generate
+    random_matrix(p, m, n, seed) columns on the device."""
+    options = options or EchelonizeOptions()
+    o = options._struct()
+    h = _vp()
+    _check(lib().gfq_echelonize_dist(comm.h, f.p, C.h if C is not None else None, m, n, seed,
+                                     ctypes.byref(o), int(gather), ctypes.byref(h)))
+    return EchelonOutput(h, f, chop(m, n, options.block, options.remainder_first), options.with_transform)
+
+
+def dist_plan(m: int, n: int, block: int, with_transform: bool, world: int):
+    """Host-only view of the sharded plan: ([(kind, i, j, k, owner)], [(is_a, i, j, k, root)])."""
+    nn, nb = ctypes.c_uint64(), ctypes.c_uint64()
+    L = raw_lib()
+    _check(L.gfq_dist_plan(m, n, block, int(with_transform), world, None, ctypes.byref(nn), None,
+                           ctypes.byref(nb)))
+    nodes = np.zeros(5 * max(nn.value, 1), np.int32)
+    bc = np.zeros(5 * max(nb.value, 1), np.int32)
+    _check(L.gfq_dist_plan(m, n, block, int(with_transform), world, nodes.ctypes.data_as(_capi.c_i32p), None,
+                           bc.ctypes.data_as(_capi.c_i32p), None))
+    nodes = [(TASK_KINDS[r[0]], int(r[1]), int(r[2]), int(r[3]), int(r[4]))
+             for r in nodes[: 5 * nn.value].reshape(-1, 5)]
+    bcasts = [(bool(r[0]), int(r[1]), int(r[2]), int(r[3]), int(r[4])) for r in bc[: 5 * nb.value].reshape(-1, 5)]
+    return nodes, bcasts
+
+
 def random_matrix(f: FieldSpec, rows: int, cols: int, seed: int) -> Matrix:
     """reference generate.hpp:33-35, generated on the device (K6)."""
     h = _vp()
