@@ -28,18 +28,8 @@ import time
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
-CONFIGS = {
-    "cfg1": dict(p=3, m=2000, n=2000, block=500, seed=1, kind="random",
-                 desc="cfg1 GF(3) 2000x2000 block 500"),
-    "cfg2a": dict(p=2, m=8192, n=8192, block=1024, seed=1, kind="random",
-                  desc="cfg2a GF(2) 8192x8192 block 1024 (BASELINE configs[1])"),
-    "cfg3": dict(p=7, m=16384, n=12288, block=2048, seed=1, kind="product", inner=10000,
-                 desc="cfg3 GF(7) 16384x12288 rank 10000 block 2048"),
-    "cfg4": dict(p=251, m=32768, n=32768, block=4096, seed=1, kind="random",
-                 desc="cfg4 GF(251) 32768x32768 block 4096"),
-    "cfg5s": dict(p=2, m=65536, n=65536, block=8192, seed=1, kind="random",
-                  desc="cfg5 1-GPU: GF(2) 65536x65536 leading case, block 8192"),
-}
+from paper_1806_04211_b200.workloads import CONFIGS  # noqa: E402
+
 DEFAULT = "cfg2a"
 METRIC = "RREF+transform effective GF(q) mult-adds/s (m*n*r / wall)"
 UNIT = "mult-adds/s"
@@ -164,8 +154,10 @@ def run_reference(args, cfg, world, rank):
         print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/libgfrref_ref.so not built"}))
         return
     threads = max(1, oracle.ref.ref_hardware_concurrency())
-    C = oracle.random_matrix(cfg["p"], cfg["m"], cfg["n"], cfg["seed"]) if cfg["kind"] == "random" else \
-        oracle.random_product_matrix(cfg["p"], cfg["m"], cfg["n"], cfg["inner"], cfg["seed"])
+    if cfg["kind"] != "random":
+        print(json.dumps({"impl": "reference", "unavailable": "reference arm wired for the random workloads only"}))
+        return
+    C = oracle.random_matrix(cfg["p"], cfg["m"], cfg["n"], cfg["seed"])
     blk = cfg["block"]
     budget = 150.0 / max(1, args.steps + args.warmup)
     s0 = min(2 * blk, cfg["m"], cfg["n"])
@@ -233,10 +225,8 @@ def main():
     from paper_1806_04211_b200 import gfrref as G
     G.lib()
     f = G.FieldSpec(cfg["p"])
-    if cfg["kind"] == "random":
-        C = G.random_matrix(f, cfg["m"], cfg["n"], cfg["seed"])
-    else:
-        C = G.random_product_matrix(f, cfg["m"], cfg["n"], cfg["inner"], cfg["seed"])
+    from paper_1806_04211_b200 import workloads
+    C = workloads.build(G, args.config)
     opts = G.EchelonizeOptions(block=cfg["block"], threads=args.threads, with_transform=True)
     flush = torch.empty(512 << 20, dtype=torch.uint8, device="cuda")
 
@@ -378,8 +368,8 @@ def main():
         line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": tot_ms / args.steps, "higher_is_better": True,
                 "scaling": "strong", "vs_baseline": None, "dtype": "u8",
-                "data": f"synthetic: reference random_matrix(GF({cfg['p']}), seed {cfg['seed']}) generated on "
-                        f"device by K6 (bit-identical to the reference generator)",
+                "data": f"synthetic: {cfg['kind']} GF({cfg['p']}) input, seed {cfg['seed']}, generated on the "
+                        f"device by K6/K1 (bit-identical to the reference generators; workloads.py)",
                 "config": {"workload": cfg["desc"], "p": cfg["p"], "m": cfg["m"], "n": cfg["n"],
                            "block": cfg["block"], "rank": rank_r, "with_transform": True,
                            "executor_streams": args.threads,

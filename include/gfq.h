@@ -210,6 +210,21 @@ int gfq_output_trace(const gfq_output* o, uint64_t* n, int32_t* kind, int32_t* i
                      int32_t* detail);
 void gfq_output_free(gfq_output* o);
 
+/* gfrref::verify (src/chief.cpp:531-590) on the device, without the oracle
+ * argument.  C is the device-resident input the output was computed from
+ * (a sharded output must have been gathered).  method: 0 = auto (exact when
+ * T, C and T.C fit in half the free HBM, else Freivalds), 1 = exact (T
+ * materialised, T.C compared entry by entry), 2 = Freivalds (T.(C.X) vs
+ * E.X for a seeded random n x 64 X, from T's blocks; false-accept
+ * probability <= p^-64).  Without the transform the row-space containment
+ * C[:,rest] + C[:,pivots].R == 0 is checked instead.  Always checks the
+ * select sets against the rank and the echelon shape of R.  *ok = 1 when
+ * every check passed; else diag (may be NULL) receives the first failure,
+ * NUL-terminated and truncated to diag_len.  checked (may be NULL)
+ * receives the check actually run ("exact" / "freivalds" / "row-space"). */
+int gfq_verify(const gfq_output* o, const gfq_mat* C, int method, uint64_t seed, int* ok,
+               char* diag, size_t diag_len, char* checked, size_t checked_len);
+
 /* ------------------------------------------------------------ multi-GPU */
 /* Block columns of C (and T) are sharded cyclically over the ranks; PkgA and
  * X packages are broadcast in one fixed order.  One process per GPU with an

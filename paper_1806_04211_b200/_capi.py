@@ -113,6 +113,8 @@ PROTOS = {
     "gfq_output_report": (I, [vp, _P(Report)]),
     "gfq_output_trace": (I, [vp, c_u64p, c_i32p, c_i32p, c_i32p, c_i32p, c_i32p, c_i64p, c_i64p, c_i32p]),
     "gfq_output_free": (None, [vp]),
+    "gfq_verify": (I, [vp, vp, I, U64, c_i32p, ctypes.c_char_p, ctypes.c_size_t, ctypes.c_char_p,
+                       ctypes.c_size_t]),
     "gfq_nccl_unique_id": (I, [c_u8p]),
     "gfq_comm_nccl": (I, [I, I, c_u8p, vpp]),
     "gfq_comm_loopback": (I, [I, vpp]),

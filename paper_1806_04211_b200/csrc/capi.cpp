@@ -8,6 +8,7 @@
 #include "host/dist.hpp"
 #include "host/jobs.hpp"
 #include "host/tasks.hpp"
+#include "host/verify.hpp"
 #include "kernels/kernels.hpp"
 
 struct gfq_mat {
@@ -568,6 +569,25 @@ int gfq_output_trace(const gfq_output* o, uint64_t* n, int32_t* kind, int32_t* i
   });
 }
 void gfq_output_free(gfq_output* o) { delete o; }
+
+int gfq_verify(const gfq_output* o, const gfq_mat* C, int method, uint64_t seed, int* ok,
+               char* diag, size_t diag_len, char* checked, size_t checked_len) {
+  return guard([&] {
+    if (!o || !C || !ok) throw std::invalid_argument("gfq_verify: null argument");
+    if (method < 0 || method > 2) throw std::invalid_argument("gfq_verify: method must be 0, 1 or 2");
+    const gfq::VerifyResult r =
+        gfq::verify(M(C), O(o).out, static_cast<gfq::VerifyMethod>(method), seed);
+    *ok = r.ok ? 1 : 0;
+    auto put = [](char* dst, size_t len, const std::string& v) {
+      if (!dst || len == 0) return;
+      const size_t k = v.size() < len - 1 ? v.size() : len - 1;
+      std::memcpy(dst, v.data(), k);
+      dst[k] = 0;
+    };
+    put(diag, diag_len, r.diag);
+    put(checked, checked_len, r.method);
+  });
+}
 
 // ---------------------------------------------------------------- multi-GPU
 int gfq_nccl_unique_id(uint8_t* out128) {

@@ -576,7 +576,7 @@ __global__ void random_fill_kernel(std::uint32_t p, std::int64_t rows,
       z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ULL;
       z = (z ^ (z >> 27)) * 0x94d049bb133111ebULL;
       z = z ^ (z >> 31);
-      if (z >= limit) atomicAdd(rejects, 1u);
+      if (z >= limit && rejects) atomicAdd(rejects, 1u);
       dst[r * ldd + c] = p <= 1 ? 0 : std::uint8_t(z % p);
     }
   }

@@ -121,4 +121,17 @@ void random_fill(std::uint32_t p, std::int64_t rows, std::int64_t cols,
                  std::uint64_t seed, std::uint64_t draw0, std::int64_t draw_ld,
                  std::uint8_t* dst, std::int64_t ldd, std::uint32_t* rejects, cudaStream_t s);
 
+// ---------------------------------------------------------------- verify
+// count_first[0] += #mismatches, count_first[1] = min(first mismatch as
+// row * cols + col) (caller initialises [0, ~0]).  mode 0: A == B;
+// mode 1: A == 0; mode 2: A == value * I.
+void compare(std::int64_t rows, std::int64_t cols, const std::uint8_t* A, std::int64_t lda,
+             const std::uint8_t* B, std::int64_t ldb, int mode, std::uint8_t value,
+             unsigned long long* count_first, cudaStream_t s);
+// Echelon shape of the remnant R (rows x cols): R[r][c] must be 0 whenever
+// restcol[c] < pivcol[r] (global column indices).
+void echelon_check(std::int64_t rows, std::int64_t cols, const std::uint8_t* R, std::int64_t ldr,
+                   const std::int32_t* pivcol, const std::int32_t* restcol,
+                   unsigned long long* count_first, cudaStream_t s);
+
 }  // namespace gfq::dev

@@ -773,6 +773,22 @@ def echelonize_dist(comm: Comm, f: FieldSpec, m: int, n: int, options: Echeloniz
     return EchelonOutput(h, f, chop(m, n, options.block, options.remainder_first), options.with_transform)
 
 
+VERIFY_METHODS = {"auto": 0, "exact": 1, "freivalds": 2}
+
+
+def verify(C, out: EchelonOutput, method: str = "auto", seed: int = 1):
+    """reference gfrref::verify (src/chief.cpp:531-590), on the device and
+    without the oracle argument (gfq_verify).  Returns (ok, diag, checked):
+    `checked` is "exact" (T materialised, T.C compared), "freivalds"
+    (T.(C.X) vs E.X, X random n x 64) or "row-space" (no transform)."""
+    C = _as_matrix(C)
+    ok = ctypes.c_int32()
+    diag = ctypes.create_string_buffer(512)
+    chk = ctypes.create_string_buffer(32)
+    _check(lib().gfq_verify(out.h, C.h, VERIFY_METHODS[method], seed, ctypes.byref(ok), diag, 512, chk, 32))
+    return bool(ok.value), diag.value.decode(), chk.value.decode()
+
+
 def dist_plan(m: int, n: int, block: int, with_transform: bool, world: int):
     """Host-only view of the sharded plan: ([(kind, i, j, k, owner)], [(is_a, i, j, k, root)])."""
     nn, nb = ctypes.c_uint64(), ctypes.c_uint64()

@@ -1,0 +1,47 @@
+"""The BASELINE.json workloads (configs[0..4]) as seeded device-generated
+inputs.  Generation follows the reference generators
+(src/generate.cpp:16-38: random_matrix, random_product_matrix), run on the
+device by K6 / K1 and bit-identical to them; cfg2b is the second variant
+of configs[1], defined here (the reference has no generator for it):
+
+  top    = random_matrix(GF(2), 4096, 8192, seed) with columns 0..1023 zeroed
+  bottom = random_matrix(GF(2), 4096, 4096, seed + 1) . top
+  C      = [top; bottom]          (8192 x 8192, rank <= 4096)
+"""
+from __future__ import annotations
+
+import numpy as np
+
+CONFIGS = {
+    "cfg1": dict(p=3, m=2000, n=2000, block=500, seed=1, kind="random",
+                 desc="cfg1 GF(3) 2000x2000 block 500"),
+    "cfg2a": dict(p=2, m=8192, n=8192, block=1024, seed=1, kind="random",
+                  desc="cfg2a GF(2) 8192x8192 block 1024 (BASELINE configs[1])"),
+    "cfg2b": dict(p=2, m=8192, n=8192, block=1024, seed=1, kind="cfg2b",
+                  desc="cfg2b GF(2) 8192x8192 block 1024, zero first block column, rows 4096.. dependent"),
+    "cfg3": dict(p=7, m=16384, n=12288, block=2048, seed=1, kind="product", inner=10000,
+                 desc="cfg3 GF(7) 16384x12288 rank 10000 block 2048"),
+    "cfg4": dict(p=251, m=32768, n=32768, block=4096, seed=1, kind="random",
+                 desc="cfg4 GF(251) 32768x32768 block 4096"),
+    "cfg5s": dict(p=2, m=65536, n=65536, block=8192, seed=1, kind="random",
+                  desc="cfg5 1-GPU: GF(2) 65536x65536 leading case, block 8192"),
+}
+
+
+def build(G, name: str):
+    """Device Matrix of workload `name` (G = paper_1806_04211_b200.gfrref)."""
+    cfg = CONFIGS[name]
+    f = G.FieldSpec(cfg["p"])
+    if cfg["kind"] == "random":
+        return G.random_matrix(f, cfg["m"], cfg["n"], cfg["seed"])
+    if cfg["kind"] == "product":
+        return G.random_product_matrix(f, cfg["m"], cfg["n"], cfg["inner"], cfg["seed"])
+    if cfg["kind"] == "cfg2b":
+        half = cfg["m"] // 2
+        top = G.random_matrix(f, half, cfg["n"], cfg["seed"]).numpy()
+        top[:, : cfg["block"]] = 0
+        top_d = G.Matrix.from_numpy(top)
+        comb = G.random_matrix(f, half, half, cfg["seed"] + 1)
+        bottom = G.mul(f, comb, top_d).numpy()
+        return G.Matrix.from_numpy(np.vstack([top, bottom]))
+    raise ValueError(f"unknown workload kind {cfg['kind']}")

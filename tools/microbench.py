@@ -65,9 +65,22 @@ def bench_mad():
         G.set_mad_policy(0)
 
 
+def bench_mad_shape(p, m, k, n, reps):
+    """One K1 shape on the tcgen05 path (for ncu captures of a single launch)."""
+    f = G.FieldSpec(p)
+    A, B, Cc = G.random_matrix(f, m, k, 1), G.random_matrix(f, k, n, 2), G.random_matrix(f, m, n, 3)
+    G.set_mad_policy(2)
+    ms = timed(lambda: G.mad(f, Cc, A, B), reps=reps)
+    print(json.dumps({"job": "mad", "p": p, "m": m, "k": k, "n": n, "path": "tc", "ms": ms,
+                      "TOPS": 2 * m * n * k / (ms / 1e3) / 1e12}))
+
+
 if __name__ == "__main__":
     G.lib()
     what = sys.argv[1] if len(sys.argv) > 1 else "all"
+    if what == "madshape":
+        bench_mad_shape(*(int(x) for x in sys.argv[2:7]))
+        sys.exit(0)
     if what in ("mad", "all"):
         bench_mad()
     if what in ("ech", "all"):

@@ -7,7 +7,8 @@ import sys
 import time
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
-from bench import CONFIGS  # noqa: E402
+from paper_1806_04211_b200 import workloads  # noqa: E402
+from paper_1806_04211_b200.workloads import CONFIGS  # noqa: E402
 from paper_1806_04211_b200 import gfrref as G  # noqa: E402
 
 name = sys.argv[1] if len(sys.argv) > 1 else "cfg2a"
@@ -15,8 +16,7 @@ threads = int(sys.argv[2]) if len(sys.argv) > 2 else 4
 cfg = CONFIGS[name]
 G.lib()
 f = G.FieldSpec(cfg["p"])
-C = G.random_matrix(f, cfg["m"], cfg["n"], cfg["seed"]) if cfg["kind"] == "random" else \
-    G.random_product_matrix(f, cfg["m"], cfg["n"], cfg["inner"], cfg["seed"])
+C = workloads.build(G, name)
 G.synchronize()
 if "--warm" in sys.argv:
     G.echelonize(C, f, G.EchelonizeOptions(block=cfg["block"], threads=threads))
