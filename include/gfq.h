@@ -98,6 +98,11 @@ int gfq_set_ech_mode(int mode);
 int gfq_launch_count(int reset, int64_t* launches);
 int gfq_profile(int on);
 int gfq_profile_take(int64_t* launches2, double* ops2, double* ms2);
+/* Developer timing of the last K1 tcgen05 launch when the process runs with
+ * GFQ_TC_DEBUG set: 148 x 8 globaltimer stamps per CTA (0 start, 1 setup,
+ * 2 first stage landed, 3 MMAs issued, 4 accumulator ready, 5 epilogue
+ * done, 6 exit); zeros otherwise. */
+int gfq_tc_debug_take(uint64_t* stamps);
 
 /* ------------------------------------------------------------ jobs (jobs.hpp:37-82) */
 int gfq_mul(uint32_t p, const gfq_mat* b, const gfq_mat* c, gfq_mat** out);            /* :40 */
@@ -208,6 +213,11 @@ int gfq_output_report(const gfq_output* o, gfq_report* rep);
 int gfq_output_trace(const gfq_output* o, uint64_t* n, int32_t* kind, int32_t* i, int32_t* j,
                      int32_t* k, int32_t* worker, int64_t* start_ns, int64_t* end_ns,
                      int32_t* detail);
+/* Device window of each trace record (same order as gfq_output_trace): ns
+ * from the run's start on the device to the task's stream reaching its
+ * first kernel, and to its last kernel completing; -1 when unavailable. */
+int gfq_output_trace_device(const gfq_output* o, uint64_t* n, int64_t* dev_start_ns,
+                            int64_t* dev_end_ns);
 void gfq_output_free(gfq_output* o);
 
 /* gfrref::verify (src/chief.cpp:531-590) on the device, without the oracle

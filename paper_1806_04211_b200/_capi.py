@@ -112,7 +112,9 @@ PROTOS = {
     "gfq_output_download_blocks": (I, [vp, c_u8p, U64]),
     "gfq_output_report": (I, [vp, _P(Report)]),
     "gfq_output_trace": (I, [vp, c_u64p, c_i32p, c_i32p, c_i32p, c_i32p, c_i32p, c_i64p, c_i64p, c_i32p]),
+    "gfq_output_trace_device": (I, [vp, c_u64p, c_i64p, c_i64p]),
     "gfq_output_free": (None, [vp]),
+    "gfq_tc_debug_take": (I, [c_u64p]),
     "gfq_verify": (I, [vp, vp, I, U64, c_i32p, ctypes.c_char_p, ctypes.c_size_t, ctypes.c_char_p,
                        ctypes.c_size_t]),
     "gfq_nccl_unique_id": (I, [c_u8p]),

@@ -130,6 +130,7 @@ int gfq_init(int device) {
     if (prop.major != 10)
       throw gfq::CudaError("device " + std::string(prop.name) + " is not sm_100 (B200)");
     GFQ_CUDA(cudaFree(nullptr));
+    gfq::warm_runtime();
   });
 }
 
@@ -260,6 +261,12 @@ int gfq_launch_count(int reset, int64_t* launches) {
 int gfq_profile(int on) { return guard([&] { gfq::dev::set_profile(on != 0); }); }
 int gfq_profile_take(int64_t* launches2, double* ops2, double* ms2) {
   return guard([&] { gfq::dev::profile_take(launches2, ops2, ms2); });
+}
+int gfq_tc_debug_take(uint64_t* stamps) {
+  return guard([&] {
+    if (!stamps) throw std::invalid_argument("gfq_tc_debug_take: null buffer");
+    gfq::dev::tc_debug_take(reinterpret_cast<unsigned long long*>(stamps));
+  });
 }
 
 // ---------------------------------------------------------------- jobs
@@ -565,6 +572,17 @@ int gfq_output_trace(const gfq_output* o, uint64_t* n, int32_t* kind, int32_t* i
       if (start_ns) start_ns[q] = tr[q].start_ns;
       if (end_ns) end_ns[q] = tr[q].end_ns;
       if (detail) detail[q] = tr[q].detail;
+    }
+  });
+}
+int gfq_output_trace_device(const gfq_output* o, uint64_t* n, int64_t* dev_start_ns,
+                            int64_t* dev_end_ns) {
+  return guard([&] {
+    const auto& tr = O(o).report.trace;
+    if (n) *n = tr.size();
+    for (size_t q = 0; q < tr.size(); ++q) {
+      if (dev_start_ns) dev_start_ns[q] = tr[q].dev_start_ns;
+      if (dev_end_ns) dev_end_ns[q] = tr[q].dev_end_ns;
     }
   });
 }

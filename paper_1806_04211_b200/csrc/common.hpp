@@ -25,11 +25,41 @@ struct CudaError : std::runtime_error {
 
 /// The stream every device job of the calling host thread is ordered on.
 /// Set by the executor (one stream per worker) or by gfq_set_stream().
+/// The first call after set_pending_waits() enqueues those event waits on
+/// the stream first (so a task that never touches the device issues no
+/// waits), and every call marks the thread's stream as touched.
 cudaStream_t cur_stream();
 void set_cur_stream(cudaStream_t s);
+/// The stream without flushing waits or marking it touched (allocator).
+cudaStream_t cur_stream_raw();
+/// Executor hooks: events the next device operation on this thread's
+/// stream must wait for (the caller keeps them alive until
+/// end_pending_waits()), whether the device was touched since, and the
+/// end of the task (unflushed waits are dropped: nothing needed them).
+void set_pending_waits(const cudaEvent_t* evs, int n);
+bool stream_touched();
+void end_pending_waits();
 
 /// Number of SMs of the current device (cached).
 int sm_count();
+
+/// Developer host-cost profile (env GFQ_HOSTPROF): wall ns spent in the
+/// CUDA API / host work of each category, summed over threads, printed to
+/// stderr at exit.
+namespace hprof {
+enum Slot { kMalloc, kFree, kUpload, kMad, kSelect, kEvent, kMemset, kMiss, kTask, kSlots };
+extern const bool on;
+void add(Slot s, std::int64_t ns, std::int64_t count = 1);
+std::int64_t now();
+struct Scope {
+  Slot slot;
+  std::int64_t t0;
+  explicit Scope(Slot s) : slot(s), t0(on ? now() : 0) {}
+  ~Scope() {
+    if (on) add(slot, now() - t0);
+  }
+};
+}  // namespace hprof
 
 inline std::int64_t round_up(std::int64_t v, std::int64_t m) {
   return (v + m - 1) / m * m;

@@ -1,8 +1,13 @@
 // runtime.cpp -- device memory, streams, staging and the value types.
 #include <algorithm>
 #include <atomic>
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
+#include <unordered_map>
+#include <vector>
 #include <stdexcept>
 
 #include "types.hpp"
@@ -32,8 +37,37 @@ void init_pool() {
 }
 }  // namespace
 
-cudaStream_t cur_stream() { return t_stream; }
+namespace {
+thread_local cudaEvent_t t_waits[8];
+thread_local int t_n_waits = 0;
+thread_local bool t_touched = false;
+}  // namespace
+
+cudaStream_t cur_stream() {
+  if (t_n_waits) {
+    const int n = t_n_waits;
+    t_n_waits = 0;
+    hprof::Scope hp(hprof::kEvent);
+    for (int q = 0; q < n; ++q) GFQ_CUDA(cudaStreamWaitEvent(t_stream, t_waits[q], 0));
+  }
+  t_touched = true;
+  return t_stream;
+}
+cudaStream_t cur_stream_raw() { return t_stream; }
 void set_cur_stream(cudaStream_t s) { t_stream = s; }
+void set_pending_waits(const cudaEvent_t* evs, int n) {
+  if (n > 8) throw std::logic_error("set_pending_waits: too many events");
+  for (int q = 0; q < n; ++q) t_waits[q] = evs[q];
+  t_n_waits = n;
+  t_touched = false;
+  static const bool eager = std::getenv("GFQ_NO_LAZY_WAITS") != nullptr;
+  if (eager) cur_stream();
+}
+bool stream_touched() { return t_touched; }
+void end_pending_waits() {
+  t_n_waits = 0;
+  t_touched = false;
+}
 
 int sm_count() {
   static int n = 0;
@@ -67,12 +101,119 @@ Elem FieldSpec::inv(Elem a) const {
   return Elem(r);
 }
 
+// ---------------------------------------------------------------- host profile
+namespace hprof {
+const bool on = std::getenv("GFQ_HOSTPROF") != nullptr;
+namespace {
+std::atomic<std::int64_t> g_ns[kSlots];
+std::atomic<std::int64_t> g_cnt[kSlots];
+struct Printer {
+  ~Printer() {
+    if (!on) return;
+    static const char* names[kSlots] = {"malloc", "free", "upload", "mad", "select",
+                                        "event", "memset", "alloc_miss", "task"};
+    for (int q = 0; q < kSlots; ++q)
+      std::fprintf(stderr, "hostprof %-12s %10.3f ms %8lld calls %8.2f us/call\n", names[q],
+                   double(g_ns[q]) / 1e6, static_cast<long long>(g_cnt[q].load()),
+                   g_cnt[q] ? double(g_ns[q]) / 1e3 / double(g_cnt[q]) : 0.0);
+  }
+} g_printer;
+}  // namespace
+void add(Slot s, std::int64_t ns, std::int64_t count) {
+  g_ns[s] += ns;
+  g_cnt[s] += count;
+}
+std::int64_t now() {
+  return std::chrono::duration_cast<std::chrono::nanoseconds>(
+             std::chrono::steady_clock::now().time_since_epoch())
+      .count();
+}
+}  // namespace hprof
+
 // ---------------------------------------------------------------- DevBuf / Mat
+// Caching block allocator over the stream-ordered pool.  A block freed
+// while the current stream is s goes back to s's free list and is reused
+// by the next allocation on s at once (stream order makes that safe, the
+// same contract as cudaFreeAsync); release_stream(s) -- called once s has
+// drained -- moves s's blocks to the idle list any stream may take.  Hits
+// cost a mutex instead of a CUDA API call; sizes are rounded to classes of
+// 1/8 of a power of two (<= 12.5% slack).
+namespace {
+struct BlockCache {
+  std::mutex mtx;
+  std::unordered_map<cudaStream_t, std::unordered_map<std::size_t, std::vector<void*>>> by_stream;
+  std::unordered_map<std::size_t, std::vector<void*>> idle;
+  std::unordered_map<void*, std::size_t> cls_of;
+};
+BlockCache& cache() {
+  static BlockCache* c = new BlockCache();  // process lifetime
+  return *c;
+}
+std::size_t size_class(std::size_t n) {
+  if (n <= 4096) return (n + 511) / 512 * 512;
+  std::size_t p2 = std::size_t(1) << (63 - __builtin_clzll(n));
+  const std::size_t step = p2 / 8;
+  return (n + step - 1) / step * step;
+}
+void* take(std::unordered_map<std::size_t, std::vector<void*>>& lists, std::size_t cls) {
+  auto it = lists.find(cls);
+  if (it == lists.end() || it->second.empty()) return nullptr;
+  void* p = it->second.back();
+  it->second.pop_back();
+  return p;
+}
+}  // namespace
+
+void release_stream(cudaStream_t s) {
+  BlockCache& c = cache();
+  std::lock_guard<std::mutex> lk(c.mtx);
+  auto it = c.by_stream.find(s);
+  if (it == c.by_stream.end()) return;
+  for (auto& [cls, v] : it->second) {
+    auto& dst = c.idle[cls];
+    dst.insert(dst.end(), v.begin(), v.end());
+  }
+  c.by_stream.erase(it);
+}
+
 DevBuf::DevBuf(std::size_t n) : bytes(n) {
   if (n == 0) return;
   init_pool();
+  hprof::Scope hp(hprof::kMalloc);
+  const cudaStream_t s = cur_stream_raw();
+  const std::size_t cls = size_class(n);
+  BlockCache& c = cache();
   void* p = nullptr;
-  GFQ_CUDA(cudaMallocAsync(&p, n, cur_stream()));
+  static const bool nocache = std::getenv("GFQ_NO_BLOCK_CACHE") != nullptr;
+  if (!nocache) {
+    std::lock_guard<std::mutex> lk(c.mtx);
+    auto it = c.by_stream.find(s);
+    if (it != c.by_stream.end()) p = take(it->second, cls);
+    if (!p) p = take(c.idle, cls);
+  }
+  if (!p) {
+    hprof::Scope hm(hprof::kMiss);
+    cudaError_t e = cudaMallocAsync(&p, cls, s);
+    if (e == cudaErrorMemoryAllocation) {
+      // return every idle cached block to the pool and retry once
+      cudaGetLastError();
+      std::vector<void*> drop;
+      {
+        std::lock_guard<std::mutex> lk(c.mtx);
+        for (auto& [k, v] : c.idle)
+          for (void* q : v) {
+            drop.push_back(q);
+            c.cls_of.erase(q);
+          }
+        c.idle.clear();
+      }
+      for (void* q : drop) cudaFreeAsync(q, s);
+      e = cudaMallocAsync(&p, cls, s);
+    }
+    GFQ_CUDA(e);
+    std::lock_guard<std::mutex> lk(c.mtx);
+    c.cls_of[p] = cls;
+  }
   ptr = static_cast<std::uint8_t*>(p);
   const std::int64_t now = (g_live += std::int64_t(n));
   std::int64_t prev = g_peak.load();
@@ -82,9 +223,18 @@ DevBuf::DevBuf(std::size_t n) : bytes(n) {
 
 DevBuf::~DevBuf() {
   if (ptr) {
-    // Stream-ordered free: every job on this value was issued on the
+    // Stream-ordered release: every job on this value was issued on the
     // current stream (or joined into it by the executor) before release.
-    cudaFreeAsync(ptr, cur_stream());
+    hprof::Scope hp(hprof::kFree);
+    BlockCache& c = cache();
+    std::lock_guard<std::mutex> lk(c.mtx);
+    auto it = c.cls_of.find(ptr);
+    static const bool nocache = std::getenv("GFQ_NO_BLOCK_CACHE") != nullptr;
+    if (it != c.cls_of.end() && !nocache) c.by_stream[cur_stream_raw()][it->second].push_back(ptr);
+    else {
+      if (it != c.cls_of.end()) c.cls_of.erase(it);
+      cudaFreeAsync(ptr, cur_stream_raw());
+    }
     g_live -= std::int64_t(bytes);
   }
 }
@@ -104,8 +254,10 @@ Mat::Mat(std::int64_t rows, std::int64_t cols) : rows_(rows), cols_(cols) {
 
 Mat Mat::zeros(std::int64_t rows, std::int64_t cols) {
   Mat m(rows, cols);
-  if (!m.empty())
+  if (!m.empty()) {
+    hprof::Scope hp(hprof::kMemset);
     GFQ_CUDA(cudaMemsetAsync(m.data_, 0, std::size_t(rows) * std::size_t(m.ld_), cur_stream()));
+  }
   return m;
 }
 
@@ -226,7 +378,18 @@ Staging& staging() {
 }
 }  // namespace
 
+void warm_runtime() {
+  init_pool();
+  Staging& st = staging();
+  std::lock_guard<std::mutex> lk(st.mtx);
+  if (!st.host) {
+    st.cap = std::size_t(64) << 20;
+    GFQ_CUDA(cudaMallocHost(reinterpret_cast<void**>(&st.host), st.cap));
+  }
+}
+
 std::shared_ptr<DevBuf> upload_i32(const std::vector<std::int32_t>& v) {
+  hprof::Scope hp(hprof::kUpload);
   const std::size_t bytes = v.size() * sizeof(std::int32_t);
   auto buf = std::make_shared<DevBuf>(bytes > 0 ? bytes : 4);
   if (bytes == 0) return buf;

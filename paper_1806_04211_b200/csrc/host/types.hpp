@@ -52,6 +52,12 @@ struct DevBuf {
   DevBuf& operator=(const DevBuf&) = delete;
 };
 
+/// The stream `s` has drained (synchronised): blocks released on it become
+/// reusable from any stream.
+void release_stream(cudaStream_t s);
+/// One-time runtime setup (memory pool attributes, pinned staging ring).
+void warm_runtime();
+
 /// Live device bytes held by DevBufs (for RunReport accounting).
 std::int64_t live_device_bytes();
 std::int64_t peak_device_bytes();

@@ -281,6 +281,7 @@ void mad(std::uint32_t p, std::int64_t m, std::int64_t n, std::int64_t k,
          std::int64_t ldb, const std::uint8_t* Cin, std::int64_t ldc,
          std::uint8_t* D, std::int64_t ldd, cudaStream_t s) {
   if (m == 0 || n == 0) return;
+  hprof::Scope hp(hprof::kMad);
   const int pol = g_policy;
   // The tcgen05 path pays a prologue (TMEM alloc, barrier init, descriptor
   // fetch) of a few microseconds; below ~4 Mi MACs or for K < 32 (one MMA
@@ -411,6 +412,7 @@ void select2d(std::uint8_t* dst, std::int64_t ldd, std::int64_t rows,
               const std::uint8_t* B, std::int64_t ldb, const std::int32_t* rmap,
               const std::int32_t* cmap, cudaStream_t s) {
   if (rows == 0 || cols == 0) return;
+  hprof::Scope hp(hprof::kSelect);
   const unsigned gy = unsigned(rows < 65535 ? rows : 65535);
   const auto al = [](const void* ptr, std::int64_t ld) {
     return ptr == nullptr ||

@@ -43,6 +43,11 @@ std::int64_t launch_count(bool reset);
 void set_profile(bool on);
 void profile_take(std::int64_t launches[2], double ops[2], double ms[2]);
 
+// Developer timing of K1 (env GFQ_TC_DEBUG): per-CTA globaltimer stamps of
+// the last launch, 148 x 8 u64 (0 start, 1 setup done, 2 first stage
+// landed, 3 MMAs issued, 4 first accumulator ready, 5 epilogue done, 6 exit).
+void tc_debug_take(unsigned long long* host);
+
 // Selects which path `mad` uses: 0 = auto, 1 = SIMT only, 2 = tcgen05 whenever legal.
 void set_mad_policy(int policy);
 int mad_policy();

@@ -190,3 +190,32 @@ def test_defining_identity_medium(G, p, m, n, block):
     out = G.echelonize(C, G.FieldSpec(p), G.EchelonizeOptions(block=block, threads=4))
     assert out.rank == min(m, n) or p == 2
     _identity_check(G, p, C, out)
+
+
+def test_dependency_race_regression(G):
+    """A rank-deficient input whose ClearDowns often have no new pivots (no
+    device work of their own): their packages must still be ordered after
+    their inputs.  Slow SIMT contractions and 8 workers widen the window;
+    every repetition must give the same output (a lost wait showed up as
+    spurious pivots in ~20% of runs)."""
+    import hashlib
+    p, half, n, block = 2, 512, 1024, 128
+    f = G.FieldSpec(p)
+    top = G.random_matrix(f, half, n, 5).numpy()
+    top[:, :block] = 0
+    comb = G.random_matrix(f, half, half, 6)
+    bottom = G.mul(f, comb, G.Matrix.from_numpy(top)).numpy()
+    C = G.Matrix.from_numpy(np.vstack([top, bottom]))
+    want = None
+    G.set_mad_policy(1)
+    try:
+        for _ in range(12):
+            out = G.echelonize(C, f, G.EchelonizeOptions(block=block, threads=8))
+            buf = np.zeros(out.block_bytes(), np.uint8)
+            out.download_blocks(buf)
+            got = (out.rank, hashlib.sha1(buf.tobytes()).hexdigest())
+            want = want or got
+            assert got == want
+    finally:
+        G.set_mad_policy(0)
+    assert want[0] <= half

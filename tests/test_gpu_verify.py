@@ -97,7 +97,9 @@ def test_echelon_shape_violation(G):
     any product is formed."""
     p = 5
     f = G.FieldSpec(p)
-    C = G.random_product_matrix(f, 64, 96, 20, 9)
+    Cn = G.random_product_matrix(f, 64, 96, 20, 9).numpy()
+    Cn[:, 5] = 0  # a non-pivot column left of later pivots
+    C = G.Matrix.from_numpy(Cn)
     out = G.echelonize(C, f, G.EchelonizeOptions(block=32))
     ups = out.global_upsilon()
     rest = [c for c in range(96) if c not in set(ups)]

@@ -21,15 +21,21 @@ G.synchronize()
 if "--warm" in sys.argv:
     G.echelonize(C, f, G.EchelonizeOptions(block=cfg["block"], threads=threads))
     G.synchronize()
-t0 = time.time()
-out = G.echelonize(C, f, G.EchelonizeOptions(block=cfg["block"], threads=threads,
-                                             collect_trace="--trace" in sys.argv))
-G.synchronize()
-print("rank", out.rank, "wall_ms", 1e3 * (time.time() - t0))
+reps = int(sys.argv[sys.argv.index("--reps") + 1]) if "--reps" in sys.argv else 1
+walls = []
+for _ in range(reps):
+    t0 = time.time()
+    out = G.echelonize(C, f, G.EchelonizeOptions(block=cfg["block"], threads=threads,
+                                                 collect_trace="--trace" in sys.argv))
+    G.synchronize()
+    walls.append(1e3 * (time.time() - t0))
+print("rank", out.rank, "wall_ms", " ".join(f"{w:.2f}" for w in walls), "min", f"{min(walls):.2f}")
 if "--trace" in sys.argv:
     import csv
     with open(sys.argv[sys.argv.index("--trace") + 1], "w") as fh:
         w = csv.writer(fh)
-        w.writerow(["task_kind", "i", "j", "k", "worker", "start_ns", "end_ns", "detail"])
+        w.writerow(["task_kind", "i", "j", "k", "worker", "start_ns", "end_ns", "detail", "dev_start_ns",
+                    "dev_end_ns"])
         for t in out.trace():
-            w.writerow([t["kind"], t["i"], t["j"], t["k"], t["worker"], t["start_ns"], t["end_ns"], t["detail"]])
+            w.writerow([t["kind"], t["i"], t["j"], t["k"], t["worker"], t["start_ns"], t["end_ns"], t["detail"],
+                        t["dev_start_ns"], t["dev_end_ns"]])
