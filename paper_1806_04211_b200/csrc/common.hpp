@@ -47,7 +47,8 @@ int sm_count();
 /// CUDA API / host work of each category, summed over threads, printed to
 /// stderr at exit.
 namespace hprof {
-enum Slot { kMalloc, kFree, kUpload, kMad, kSelect, kEvent, kMemset, kMiss, kTask, kSlots };
+enum Slot { kMalloc, kFree, kUpload, kMad, kSelect, kEvent, kMemset, kMiss, kSync, kOtherLaunch, kTask,
+            kTaskKind0, kSlots = kTaskKind0 + 8 };
 extern const bool on;
 void add(Slot s, std::int64_t ns, std::int64_t count = 1);
 std::int64_t now();

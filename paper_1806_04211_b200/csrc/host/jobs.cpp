@@ -304,11 +304,14 @@ EchResult panel_ech(const FieldSpec& f, const Mat& h) {
   if (f.p() == 2 && a <= 1024 && (a + b + 31) / 32 <= 256) {
     // GF(2): the whole ECH in one bit-packed single-CTA launch
     Mat aug(a, b + a);
-    DevBuf scratch{static_cast<std::size_t>(4 * dev::ech_gf2_scratch_words(a, b))};
     DevBuf info{static_cast<std::size_t>(4 * (1 + 2 * cap))};
-    dev::ech_gf2_block(a, b, h.data(), h.ld(), reinterpret_cast<std::uint32_t*>(scratch.ptr),
-                       aug.data(), aug.ld(), reinterpret_cast<std::int32_t*>(info.ptr), cap, s);
-    return extract_ech(a, b, aug, reinterpret_cast<const std::int32_t*>(info.ptr), cap);
+    auto* inf = reinterpret_cast<std::int32_t*>(info.ptr);
+    if (!dev::ech_gf2_cluster(a, b, h.data(), h.ld(), aug.data(), aug.ld(), inf, cap, s)) {
+      DevBuf scratch{static_cast<std::size_t>(4 * dev::ech_gf2_scratch_words(a, b))};
+      dev::ech_gf2_block(a, b, h.data(), h.ld(), reinterpret_cast<std::uint32_t*>(scratch.ptr),
+                         aug.data(), aug.ld(), inf, cap, s);
+    }
+    return extract_ech(a, b, aug, inf, cap);
   }
   Mat aug = Mat::zeros(a, b + a);
   dev::select2d(aug.data(), aug.ld(), a, b, h.data(), h.ld(), nullptr, 0, nullptr, nullptr, s);

@@ -110,8 +110,10 @@ std::atomic<std::int64_t> g_cnt[kSlots];
 struct Printer {
   ~Printer() {
     if (!on) return;
-    static const char* names[kSlots] = {"malloc", "free", "upload", "mad", "select",
-                                        "event", "memset", "alloc_miss", "task"};
+    static const char* names[kSlots] = {
+        "malloc", "free",  "upload", "mad", "select", "event", "memset", "alloc_miss", "sync",
+        "other_launch", "task", "ClearDown", "UpdateRow", "UpdateRowTrafo", "Extend", "RowLengthen",
+        "PreClearUp", "ClearUp", "Copy"};
     for (int q = 0; q < kSlots; ++q)
       std::fprintf(stderr, "hostprof %-12s %10.3f ms %8lld calls %8.2f us/call\n", names[q],
                    double(g_ns[q]) / 1e6, static_cast<long long>(g_cnt[q].load()),
@@ -420,6 +422,7 @@ std::shared_ptr<DevBuf> upload_i32(const std::vector<std::int32_t>& v) {
 
 void download_i32(const std::int32_t* dev, std::int32_t* host, std::size_t n) {
   if (n == 0) return;
+  hprof::Scope hp(hprof::kSync);
   GFQ_CUDA(cudaMemcpyAsync(host, dev, n * sizeof(std::int32_t), cudaMemcpyDeviceToHost,
                            cur_stream()));
   GFQ_CUDA(cudaStreamSynchronize(cur_stream()));

@@ -110,6 +110,12 @@ bool ech_gf2_block(std::int64_t rows, std::int64_t cols, const std::uint8_t* H, 
                    std::uint32_t* scratch, std::uint8_t* Out, std::int64_t ldo, std::int32_t* info,
                    std::int64_t cap, cudaStream_t s);
 std::int64_t ech_gf2_scratch_words(std::int64_t rows, std::int64_t cols);
+// Same contract, cluster-resident (one 8-CTA cluster, distributed shared
+// memory): rows <= 1024 and cols + rows <= 8192, no scratch.  Returns false
+// (nothing launched) outside those limits or with GFQ_NO_GF2_CLUSTER set.
+bool ech_gf2_cluster(std::int64_t rows, std::int64_t cols, const std::uint8_t* H, std::int64_t ldh,
+                     std::uint8_t* Out, std::int64_t ldo, std::int32_t* info, std::int64_t cap,
+                     cudaStream_t s);
 
 // dst[rmap[i]] = src[i] for rmap[i] >= 0 (row scatter).
 void scatter_rows(std::uint8_t* dst, std::int64_t ldd, std::int64_t rows, std::int64_t cols,

@@ -12,6 +12,8 @@ G.lib()
 G.set_ech_mode(mode)
 f = G.FieldSpec(p)
 H = G.random_matrix(f, n, n, 7)
-e = G.ech(f, H)
+reps = int(sys.argv[sys.argv.index("--reps") + 1]) if "--reps" in sys.argv else 1
+for _ in range(reps):
+    e = G.ech(f, H)
 G.synchronize()
 print("rank", e.rank())
