@@ -173,6 +173,8 @@ typedef struct gfq_options {
   int remainder_first;
   int collect_trace;
   int retain_all;
+  int fuse;  /* 1 (default): wide UpdateRow / ClearUp jobs per panel (single GPU);
+                0: the reference's per-block task grid */
 } gfq_options;
 void gfq_options_default(gfq_options* o);
 

@@ -37,7 +37,7 @@ class PkgE(ctypes.Structure):
 class Options(ctypes.Structure):
     _fields_ = [("block", ctypes.c_uint64), ("threads", ctypes.c_int), ("with_transform", ctypes.c_int),
                 ("ech_threshold", ctypes.c_uint64), ("remainder_first", ctypes.c_int),
-                ("collect_trace", ctypes.c_int), ("retain_all", ctypes.c_int)]
+                ("collect_trace", ctypes.c_int), ("retain_all", ctypes.c_int), ("fuse", ctypes.c_int)]
 
 
 class Report(ctypes.Structure):

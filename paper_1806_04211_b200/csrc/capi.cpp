@@ -429,6 +429,7 @@ void gfq_options_default(gfq_options* o) {
   o->remainder_first = 0;
   o->collect_trace = 0;
   o->retain_all = 0;
+  o->fuse = 1;
 }
 
 namespace {
@@ -444,6 +445,7 @@ gfq::EchelonizeOptions to_opts(const gfq_options* o) {
   e.remainder_first = o->remainder_first != 0;
   e.collect_trace = o->collect_trace != 0;
   e.retain_all = o->retain_all != 0;
+  e.fuse = o->fuse != 0;
   return e;
 }
 const gfq_output& O(const gfq_output* o) {

@@ -57,6 +57,18 @@ struct Emitter {
     for (auto s : out) nd.out[nd.n_out++] = s;
     g.plan_add(nd);
   }
+  void node(TaskKind kind, std::int32_t c0, std::int32_t c1, std::int32_t c2, std::int32_t pri,
+            const std::vector<std::int32_t>& in, std::initializer_list<std::int32_t> out) {
+    TaskNode nd;
+    nd.kind = kind;
+    nd.c0 = c0;
+    nd.c1 = c1;
+    nd.c2 = c2;
+    nd.priority = pri;
+    for (auto s : in) nd.in[nd.n_in++] = s;
+    for (auto s : out) nd.out[nd.n_out++] = s;
+    g.plan_add(nd);
+  }
 };
 }  // namespace
 
@@ -195,6 +207,183 @@ PlanHandles build_plan(TaskGraph& graph,
   return hd;
 }
 
+// Fused single-GPU plan: the same Steps 1-3 and slot versions, but the jobs
+// that apply one package to every block of a panel run as ONE wide job:
+//   UpdateRow(i, j, k): k = j+1 (on the Step-1 critical path) alone, k > j+1
+//     together on the row panel (UpdateRowW); C and B row panels stay one
+//     matrix (MatParts) from the input view onwards;
+//   ClearUp(k, j, l) for all l (ClearUpRW) and ClearUp(k, j, h) for all h
+//     (ClearUpMW), on padded panels.
+// Every value is the one the reference plan computes (the jobs are
+// column-separable); only the task granularity changes.
+PlanHandles build_plan_fused(TaskGraph& graph, const Mat& C, const FieldSpec& field,
+                             const ChopSpec& cs, bool with_transform) {
+  const std::size_t a = cs.a(), b = cs.b();
+  if (a == 0 || b == 0) throw std::invalid_argument("build_plan: empty partition");
+  if (2 * a + 1 > std::size_t(TaskNode::kMaxIn))
+    throw std::invalid_argument("build_plan_fused: block grid too tall for the fused plan");
+  if (std::int64_t(cs.rows()) != C.rows() || std::int64_t(cs.cols()) != C.cols())
+    throw std::invalid_argument("build_plan: partition does not match matrix");
+  graph.set_field(field);
+  Emitter e{graph};
+  using K = PkgKind;
+  using T = TaskKind;
+  const auto blk = [&](std::size_t i, std::size_t k) {
+    return C.row_view(std::int64_t(cs.row_offset(i)), std::int64_t(cs.row_parts[i]))
+        .col_view(std::int64_t(cs.col_offset(k)), std::int64_t(cs.col_parts[k]));
+  };
+  for (std::size_t i = 0; i < a; ++i) {
+    graph.add_input({K::C, std::uint16_t(i), 0, 0, 0}, blk(i, 0));
+    if (b > 1) {
+      MatParts panel;
+      const std::int64_t o1 = std::int64_t(cs.col_offset(1));
+      panel.m = C.row_view(std::int64_t(cs.row_offset(i)), std::int64_t(cs.row_parts[i]))
+                    .col_view(o1, C.cols() - o1);
+      for (std::size_t k = 1; k < b; ++k) {
+        panel.off.push_back(std::int64_t(cs.col_offset(k)) - o1);
+        panel.w.push_back(std::int64_t(cs.col_parts[k]));
+      }
+      graph.add_input({K::CW, std::uint16_t(i), 1, 0, 0}, std::move(panel));
+    }
+  }
+
+  // Step 1
+  for (std::size_t j = 0; j < b; ++j) {
+    for (std::size_t i = 0; i < a; ++i) {
+      const std::int32_t pri = std::int32_t(i + j);
+      const auto sD = [&](std::size_t v) { return e.slot(K::D, j, 0, 0, v); };
+      const std::int32_t sA = e.slot(K::A, i, j, 0, 0);
+      const std::int32_t sC = e.slot(K::C, i, j, 0, j);
+      if (i > 0)
+        e.node(T::ClearDown, std::int32_t(i), std::int32_t(j), -1, pri, {sC, sD(i - 1)}, {sD(i), sA});
+      else
+        e.node(T::ClearDown, std::int32_t(i), std::int32_t(j), -1, pri, {sC}, {sD(i), sA});
+      if (j > 0)
+        e.node(T::Extend, std::int32_t(i), std::int32_t(j), -1, pri,
+               {sA, e.slot(K::E, i, 0, 0, j - 1)}, {e.slot(K::E, i, 0, 0, j)});
+      else
+        e.node(T::Extend, std::int32_t(i), std::int32_t(j), -1, pri, {sA},
+               {e.slot(K::E, i, 0, 0, j)});
+      if (j + 1 < b) {
+        const std::int32_t panel = e.slot(K::CW, i, j + 1, 0, j);
+        const std::int32_t cout = e.slot(K::C, i, j + 1, 0, j + 1);
+        const std::int32_t bout = e.slot(K::B, j, j + 1, 0, i);
+        if (i > 0)
+          e.node(T::UpdateRow, std::int32_t(i), std::int32_t(j), std::int32_t(j + 1), pri,
+                 {sA, panel, e.slot(K::B, j, j + 1, 0, i - 1)}, {cout, bout});
+        else
+          e.node(T::UpdateRow, std::int32_t(i), std::int32_t(j), std::int32_t(j + 1), pri,
+                 {sA, panel}, {cout, bout});
+        if (j + 2 < b) {
+          const std::int32_t pout = e.slot(K::CW, i, j + 2, 0, j + 1);
+          const std::int32_t bwout = e.slot(K::BW, j, j + 2, 0, i);
+          if (i > 0)
+            e.node(T::UpdateRowW, std::int32_t(i), std::int32_t(j), std::int32_t(j + 2), pri,
+                   {sA, panel, e.slot(K::BW, j, j + 2, 0, i - 1)}, {pout, bwout});
+          else
+            e.node(T::UpdateRowW, std::int32_t(i), std::int32_t(j), std::int32_t(j + 2), pri,
+                   {sA, panel}, {pout, bwout});
+        }
+      }
+      if (with_transform) {
+        for (std::size_t h = 0; h <= i; ++h) {
+          TaskNode tr;
+          tr.kind = T::UpdateRowTrafo;
+          tr.c0 = std::int32_t(i);
+          tr.c1 = std::int32_t(j);
+          tr.c2 = std::int32_t(h);
+          tr.priority = pri;
+          tr.in[tr.n_in++] = sA;
+          tr.in[tr.n_in++] = e.slot(K::E, h, 0, 0, j);
+          if (j > 0) tr.in[tr.n_in++] = e.slot(K::K, i, h, 0, j - 1);
+          if (h < i) tr.in[tr.n_in++] = e.slot(K::M, j, h, 0, i - 1 - h);
+          tr.out[tr.n_out++] = e.slot(K::K, i, h, 0, j);
+          tr.out[tr.n_out++] = e.slot(K::M, j, h, 0, i - h);
+          graph.plan_add(tr);
+        }
+      }
+    }
+  }
+  // Step 2
+  if (with_transform)
+    for (std::size_t j = 0; j < b; ++j)
+      for (std::size_t h = 0; h < a; ++h)
+        e.node(T::RowLengthen, -1, std::int32_t(j), std::int32_t(h), std::int32_t(a + b - 1),
+               {e.slot(K::M, j, h, 0, a - 1 - h), e.slot(K::E, h, 0, 0, j),
+                e.slot(K::E, h, 0, 0, b - 1)},
+               {e.slot(K::M, j, h, 0, a - h)});
+  // Step 3
+  for (std::size_t k = 0; k < b; ++k)
+    e.node(T::Copy, -1, std::int32_t(k), -1, std::int32_t(a + b + (b - 1 - k)),
+           {e.slot(K::D, k, 0, 0, a - 1)}, {e.slot(K::R, k, k, 0, 0)});
+  for (std::size_t k = b; k-- > 1;) {
+    const std::int32_t pri = std::int32_t(a + b + (b - 1 - k));
+    for (std::size_t j = 0; j < k; ++j) {
+      const std::int32_t sX = e.slot(K::X, j, k, 0, 0);
+      if (k == j + 1)
+        e.node(T::PreClearUp, -1, std::int32_t(j), std::int32_t(k), pri,
+               {e.slot(K::B, j, k, 0, a - 1), e.slot(K::D, k, 0, 0, a - 1)},
+               {sX, e.slot(K::R, j, k, 0, 0)});
+      else
+        e.node(T::PreClearUp, std::int32_t(k - (j + 2)), std::int32_t(j), std::int32_t(k), pri,
+               {e.slot(K::BW, j, j + 2, 0, a - 1), e.slot(K::D, k, 0, 0, a - 1)},
+               {sX, e.slot(K::R, j, k, 0, 0)});
+      std::vector<std::int32_t> rin{sX, e.slot(K::R, j, k, 0, 0), e.slot(K::R, k, k, 0, 0)};
+      if (k + 1 < b) {
+        rin.push_back(e.slot(K::RW, j, k + 1, 0, 0));
+        rin.push_back(e.slot(K::RW, k, k + 1, 0, 0));
+      }
+      e.node(T::ClearUpRW, std::int32_t(k), std::int32_t(j), -1, pri, rin,
+             {e.slot(K::RW, j, k, 0, 0)});
+      if (with_transform) {
+        std::vector<std::int32_t> min{sX};
+        if (k + 1 == b) {
+          for (std::size_t h = 0; h < a; ++h) min.push_back(e.slot(K::M, j, h, 0, a - h));
+          for (std::size_t h = 0; h < a; ++h) min.push_back(e.slot(K::M, k, h, 0, a - h));
+        } else {
+          min.push_back(e.slot(K::MW, j, k + 1, 0, 0));
+          min.push_back(e.slot(K::MW, k, k + 1, 0, 0));
+        }
+        e.node(T::ClearUpMW, std::int32_t(k), std::int32_t(j), -1, pri, min,
+               {e.slot(K::MW, j, k, 0, 0)});
+      }
+    }
+  }
+
+  PlanHandles hd;
+  for (std::size_t j = 0; j < b; ++j) hd.d_final.push_back(e.slot(K::D, j, 0, 0, a - 1));
+  for (std::size_t i = 0; i < a; ++i) hd.e_final.push_back(e.slot(K::E, i, 0, 0, b - 1));
+  hd.r_final.assign(b, std::vector<std::int32_t>(b, -1));
+  hd.r_part.assign(b, std::vector<std::int32_t>(b, -1));
+  for (std::size_t j = 0; j < b; ++j)
+    for (std::size_t l = j; l < b; ++l) {
+      if (l == j) {
+        hd.r_final[j][l] = e.slot(K::R, j, j, 0, 0);
+      } else {
+        hd.r_final[j][l] = e.slot(K::RW, j, j + 1, 0, 0);
+        hd.r_part[j][l] = std::int32_t(l - (j + 1));
+      }
+    }
+  if (with_transform) {
+    hd.m_final.assign(b, std::vector<std::int32_t>(a, -1));
+    hd.m_part.assign(b, std::vector<std::int32_t>(a, -1));
+    for (std::size_t j = 0; j < b; ++j)
+      for (std::size_t h = 0; h < a; ++h) {
+        if (j + 1 == b) {
+          hd.m_final[j][h] = e.slot(K::M, j, h, 0, a - h);
+        } else {
+          hd.m_final[j][h] = e.slot(K::MW, j, j + 1, 0, 0);
+          hd.m_part[j][h] = std::int32_t(h);
+        }
+      }
+    hd.k_final.resize(a);
+    for (std::size_t i = 0; i < a; ++i)
+      for (std::size_t h = 0; h <= i; ++h) hd.k_final[i].push_back(e.slot(K::K, i, h, 0, b - 1));
+  }
+  graph.drop_key_index_if_large();
+  return hd;
+}
+
 // ---------------------------------------------------------------- echelonize
 EchelonOutput echelonize(const Mat& C, const FieldSpec& field, const EchelonizeOptions& options,
                          RunReport* report) {
@@ -224,7 +413,9 @@ EchelonOutput echelonize(const Mat& C, const FieldSpec& field, const EchelonizeO
 
   TaskGraph graph;
   graph.ech_threshold = options.ech_threshold;
-  const PlanHandles h = build_plan(graph, C, field, cs, options.with_transform);
+  const bool fused = options.fuse && 2 * a + 1 <= std::size_t(TaskNode::kMaxIn);
+  const PlanHandles h = fused ? build_plan_fused(graph, C, field, cs, options.with_transform)
+                              : build_plan(graph, C, field, cs, options.with_transform);
   for (auto id : h.d_final) graph.retain(id);
   for (auto id : h.e_final) graph.retain(id);
   for (const auto& row : h.r_final)
@@ -250,14 +441,18 @@ EchelonOutput echelonize(const Mat& C, const FieldSpec& field, const EchelonizeO
   for (std::size_t i = 0; i < a; ++i)
     out.varrho.push_back(std::get<PkgE>(*graph.payload(h.e_final[i])).rho);
   out.R_blocks.assign(b, std::vector<Mat>(b));
+  const auto value_of = [&](std::int32_t slot, std::int32_t part) {
+    const PackageValue& v = *graph.payload(slot);
+    return part < 0 ? std::get<Mat>(v) : std::get<MatParts>(v).part(std::size_t(part));
+  };
   for (std::size_t j = 0; j < b; ++j)
     for (std::size_t l = j; l < b; ++l)
-      out.R_blocks[j][l] = std::get<Mat>(*graph.payload(h.r_final[j][l]));
+      out.R_blocks[j][l] = value_of(h.r_final[j][l], h.r_part.empty() ? -1 : h.r_part[j][l]);
   if (options.with_transform) {
     out.T_M_blocks.assign(b, std::vector<Mat>(a));
     for (std::size_t j = 0; j < b; ++j)
       for (std::size_t hh = 0; hh < a; ++hh)
-        out.T_M_blocks[j][hh] = std::get<Mat>(*graph.payload(h.m_final[j][hh]));
+        out.T_M_blocks[j][hh] = value_of(h.m_final[j][hh], h.m_part.empty() ? -1 : h.m_part[j][hh]);
     out.T_K_blocks.resize(a);
     for (std::size_t i = 0; i < a; ++i)
       for (std::size_t hh = 0; hh <= i; ++hh)

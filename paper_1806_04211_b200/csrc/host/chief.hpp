@@ -48,6 +48,8 @@ struct EchelonOutput {
 struct PlanHandles {
   std::vector<std::int32_t> d_final, e_final;
   std::vector<std::vector<std::int32_t>> r_final, m_final, k_final;
+  // fused plan: the block is part r_part / m_part of a MatParts slot (-1: plain)
+  std::vector<std::vector<std::int32_t>> r_part, m_part;
 };
 
 /// reference include/gfrref/chief.hpp:72: Steps 1-3 into a fresh graph.
@@ -69,7 +71,12 @@ struct EchelonizeOptions {
   bool remainder_first = false;
   bool collect_trace = false;
   bool retain_all = false;
+  bool fuse = true;  // wide UpdateRow / ClearUp jobs (single GPU); false = the reference's task grid
 };
+
+/// The fused single-GPU plan (same values, wide jobs per panel).
+PlanHandles build_plan_fused(TaskGraph& graph, const Mat& C, const FieldSpec& field,
+                             const ChopSpec& chop, bool with_transform);
 
 /// reference include/gfrref/chief.hpp:88-90.  C is device-resident.
 EchelonOutput echelonize(const Mat& C, const FieldSpec& field, const EchelonizeOptions& options,

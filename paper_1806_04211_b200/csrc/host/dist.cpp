@@ -33,6 +33,10 @@ int Sharding::owner(const TaskNode& nd) const {
       return owner_col(std::size_t(nd.c2));
     case TaskKind::ClearUp:
       return -2;  // resolved by the output kind (R vs M), see owner_of()
+    case TaskKind::UpdateRowW:
+    case TaskKind::ClearUpRW:
+    case TaskKind::ClearUpMW:
+      throw std::logic_error("fused (single-GPU) tasks cannot be sharded");
   }
   return -1;
 }

@@ -77,6 +77,18 @@ static Mat mul_add_kernel(const FieldSpec& f, const Mat* addend, const Mat& b, c
 Mat mat_mul(const FieldSpec& f, const Mat& b, const Mat& c) {
   return mul_add_kernel(f, nullptr, b, c);
 }
+
+void mad_into(const FieldSpec& f, const Mat& d, const Mat* addend, const Mat& b, const Mat& c) {
+  if (b.cols() != c.rows()) throw std::invalid_argument("mul: inner dimensions disagree");
+  if (d.rows() != b.rows() || d.cols() != c.cols())
+    throw std::invalid_argument("mad_into: destination shape mismatch");
+  if (addend && (addend->rows() != b.rows() || addend->cols() != c.cols()))
+    throw std::invalid_argument("mad: addend shape mismatch");
+  if (d.empty()) return;
+  dev::mad(f.p(), d.rows(), d.cols(), b.cols(), b.data(), b.ld(), c.data(), c.ld(),
+           addend ? addend->data() : nullptr, addend ? addend->ld() : 0, d.data(), d.ld(),
+           cur_stream());
+}
 Mat mat_mul_add(const FieldSpec& f, const Mat& a, const Mat& b, const Mat& c) {
   return mul_add_kernel(f, &a, b, c);
 }

@@ -18,6 +18,9 @@ Mat mul(const FieldSpec& f, const Mat& b, const Mat& c);           // jobs.hpp:4
 Mat mad(const FieldSpec& f, const Mat& a, const Mat& b, const Mat& c);  // jobs.hpp:43
 Mat mat_mul(const FieldSpec& f, const Mat& b, const Mat& c);       // matrix.hpp:90
 Mat mat_mul_add(const FieldSpec& f, const Mat& a, const Mat& b, const Mat& c);  // matrix.hpp:93
+/// d = (addend ? addend : 0) + b.c written into an existing matrix or view
+/// (the fused plan's wide outputs); addend may alias d.
+void mad_into(const FieldSpec& f, const Mat& d, const Mat* addend, const Mat& b, const Mat& c);
 
 /// Negative reduced echelonisation of one block (jobs.hpp:50).  Same
 /// recursion as the reference (split the longer dimension, combine), base

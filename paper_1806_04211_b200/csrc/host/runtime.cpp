@@ -38,7 +38,7 @@ void init_pool() {
 }  // namespace
 
 namespace {
-thread_local cudaEvent_t t_waits[8];
+thread_local cudaEvent_t t_waits[80];
 thread_local int t_n_waits = 0;
 thread_local bool t_touched = false;
 }  // namespace
@@ -56,7 +56,7 @@ cudaStream_t cur_stream() {
 cudaStream_t cur_stream_raw() { return t_stream; }
 void set_cur_stream(cudaStream_t s) { t_stream = s; }
 void set_pending_waits(const cudaEvent_t* evs, int n) {
-  if (n > 8) throw std::logic_error("set_pending_waits: too many events");
+  if (n > 80) throw std::logic_error("set_pending_waits: too many events");
   for (int q = 0; q < n; ++q) t_waits[q] = evs[q];
   t_n_waits = n;
   t_touched = false;
@@ -113,7 +113,7 @@ struct Printer {
     static const char* names[kSlots] = {
         "malloc", "free",  "upload", "mad", "select", "event", "memset", "alloc_miss", "sync",
         "other_launch", "task", "ClearDown", "UpdateRow", "UpdateRowTrafo", "Extend", "RowLengthen",
-        "PreClearUp", "ClearUp", "Copy"};
+        "PreClearUp", "ClearUp", "Copy", "UpdateRowW", "ClearUpRW", "ClearUpMW"};
     for (int q = 0; q < kSlots; ++q)
       std::fprintf(stderr, "hostprof %-12s %10.3f ms %8lld calls %8.2f us/call\n", names[q],
                    double(g_ns[q]) / 1e6, static_cast<long long>(g_cnt[q].load()),

@@ -597,13 +597,16 @@ class EchelonizeOptions:
     remainder_first: bool = False
     collect_trace: bool = False
     retain_all: bool = False
+    fuse: bool = True  # wide UpdateRow / ClearUp jobs per panel (single GPU); False = reference task grid
 
     def _struct(self):
         return _capi.Options(self.block, self.threads, int(self.with_transform), self.ech_threshold,
-                             int(self.remainder_first), int(self.collect_trace), int(self.retain_all))
+                             int(self.remainder_first), int(self.collect_trace), int(self.retain_all),
+                             int(self.fuse))
 
 
-TASK_KINDS = ["ClearDown", "UpdateRow", "UpdateRowTrafo", "Extend", "RowLengthen", "PreClearUp", "ClearUp", "Copy"]
+TASK_KINDS = ["ClearDown", "UpdateRow", "UpdateRowTrafo", "Extend", "RowLengthen", "PreClearUp", "ClearUp", "Copy",
+              "UpdateRowW", "ClearUpRW", "ClearUpMW"]
 
 
 class EchelonOutput:

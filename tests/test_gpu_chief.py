@@ -65,7 +65,8 @@ def test_paper_example(G, pinned):
     C6 = arr(pinned["C6"])
     want = pinned["C6_out"]
     for threads in (1, 3):
-        out = G.echelonize(C6, G.FieldSpec(3), G.EchelonizeOptions(block=3, threads=threads, collect_trace=True))
+        out = G.echelonize(C6, G.FieldSpec(3), G.EchelonizeOptions(block=3, threads=threads, collect_trace=True,
+                                                                   fuse=False))
         assert out.rank == want["rank"]
         assert [list(s.members) for s in out.upsilon] == want["upsilon"]
         assert [list(s.members) for s in out.varrho] == want["varrho"]
@@ -92,7 +93,8 @@ def test_paper_example(G, pinned):
             if t["kind"] == "ClearDown":
                 per_col[t["j"]] = per_col.get(t["j"], 0) + t["detail"]
         assert per_col == {0: 3, 1: 2}
-    lean = G.echelonize(C6, G.FieldSpec(3), G.EchelonizeOptions(block=3, with_transform=False, collect_trace=True))
+    lean = G.echelonize(C6, G.FieldSpec(3), G.EchelonizeOptions(block=3, with_transform=False, collect_trace=True,
+                                                                 fuse=False))
     assert len(lean.trace()) == want["task_counts_no_transform"]["total"]
     assert lean.rank == 5 and lean.assembled_R() == arr(want["assembled_R"])
 
@@ -219,3 +221,35 @@ def test_dependency_race_regression(G):
     finally:
         G.set_mad_policy(0)
     assert want[0] <= half
+
+
+@pytest.mark.parametrize("p,m,n,block,kind,wt", [
+    (2, 300, 300, 64, "random", True), (3, 257, 301, 48, "random", True), (7, 320, 256, 80, "product", True),
+    (251, 200, 230, 50, "random", True), (5, 190, 230, 37, "product", True), (2, 512, 384, 64, "product", False),
+    (3, 96, 400, 32, "random", True), (2, 64, 64, 64, "random", True),
+])
+def test_fused_plan_matches_reference_grid(G, p, m, n, block, kind, wt):
+    """The fused single-GPU plan (wide UpdateRow / ClearUp jobs on panels)
+    computes exactly the reference task grid's values."""
+    f = G.FieldSpec(p)
+    C = G.random_matrix(f, m, n, 21) if kind == "random" else G.random_product_matrix(f, m, n, min(m, n) // 3, 21)
+    ref = G.echelonize(C, f, G.EchelonizeOptions(block=block, threads=3, with_transform=wt, fuse=False))
+    fus = G.echelonize(C, f, G.EchelonizeOptions(block=block, threads=3, with_transform=wt, fuse=True))
+    assert fus.rank == ref.rank
+    assert [s.members for s in fus.upsilon] == [s.members for s in ref.upsilon]
+    assert [s.members for s in fus.varrho] == [s.members for s in ref.varrho]
+    a, b = len(ref.chop.row_parts), len(ref.chop.col_parts)
+    for j in range(b):
+        for l in range(j, b):
+            np.testing.assert_array_equal(fus.block(0, j, l).numpy(), ref.block(0, j, l).numpy())
+        if wt:
+            for h in range(a):
+                np.testing.assert_array_equal(fus.block(1, j, h).numpy(), ref.block(1, j, h).numpy())
+    if wt:
+        for i in range(a):
+            for h in range(i + 1):
+                np.testing.assert_array_equal(fus.block(2, i, h).numpy(), ref.block(2, i, h).numpy())
+    kinds = {t["kind"] for t in G.echelonize(C, f, G.EchelonizeOptions(block=block, with_transform=wt,
+                                                                       collect_trace=True)).trace()}
+    if b > 2:
+        assert "UpdateRowW" in kinds and "ClearUpRW" in kinds
