@@ -48,7 +48,7 @@ int sm_count();
 /// stderr at exit.
 namespace hprof {
 enum Slot { kMalloc, kFree, kUpload, kMad, kSelect, kEvent, kMemset, kMiss, kSync, kOtherLaunch, kTask,
-            kTaskKind0, kSlots = kTaskKind0 + 11 };
+            kTaskKind0, kSlots = kTaskKind0 + 12 };
 extern const bool on;
 void add(Slot s, std::int64_t ns, std::int64_t count = 1);
 std::int64_t now();

@@ -286,32 +286,45 @@ PlanHandles build_plan_fused(TaskGraph& graph, const Mat& C, const FieldSpec& fi
         }
       }
       if (with_transform) {
-        for (std::size_t h = 0; h <= i; ++h) {
+        // h = i: the reference task (K(i,i,.) and M(j,i,0) stay blocks)
+        {
           TaskNode tr;
           tr.kind = T::UpdateRowTrafo;
           tr.c0 = std::int32_t(i);
           tr.c1 = std::int32_t(j);
-          tr.c2 = std::int32_t(h);
+          tr.c2 = std::int32_t(i);
           tr.priority = pri;
           tr.in[tr.n_in++] = sA;
-          tr.in[tr.n_in++] = e.slot(K::E, h, 0, 0, j);
-          if (j > 0) tr.in[tr.n_in++] = e.slot(K::K, i, h, 0, j - 1);
-          if (h < i) tr.in[tr.n_in++] = e.slot(K::M, j, h, 0, i - 1 - h);
-          tr.out[tr.n_out++] = e.slot(K::K, i, h, 0, j);
-          tr.out[tr.n_out++] = e.slot(K::M, j, h, 0, i - h);
+          tr.in[tr.n_in++] = e.slot(K::E, i, 0, 0, j);
+          if (j > 0) tr.in[tr.n_in++] = e.slot(K::K, i, i, 0, j - 1);
+          tr.out[tr.n_out++] = e.slot(K::K, i, i, 0, j);
+          tr.out[tr.n_out++] = e.slot(K::M, j, i, 0, 0);
           graph.plan_add(tr);
+        }
+        // h < i: one wide task on the K(i, ., .) and T_M(j, ., .) panels
+        if (i > 0) {
+          std::vector<std::int32_t> in{sA};
+          for (std::size_t h = 0; h < i; ++h) in.push_back(e.slot(K::E, h, 0, 0, j));
+          if (j > 0) in.push_back(e.slot(K::KW, i, 0, 0, j - 1));
+          if (i >= 2) in.push_back(e.slot(K::MT, j, 0, 0, i - 1));
+          in.push_back(e.slot(K::M, j, i - 1, 0, 0));
+          e.node(T::UpdateRowTrafoW, std::int32_t(i), std::int32_t(j), -1, pri, in,
+                 {e.slot(K::KW, i, 0, 0, j), e.slot(K::MT, j, 0, 0, i)});
         }
       }
     }
   }
-  // Step 2
+  // Step 2 (M(j, h, a-1-h): part h of the row-(a-1) T_M panel, or the h = a-1 block)
   if (with_transform)
     for (std::size_t j = 0; j < b; ++j)
-      for (std::size_t h = 0; h < a; ++h)
-        e.node(T::RowLengthen, -1, std::int32_t(j), std::int32_t(h), std::int32_t(a + b - 1),
-               {e.slot(K::M, j, h, 0, a - 1 - h), e.slot(K::E, h, 0, 0, j),
-                e.slot(K::E, h, 0, 0, b - 1)},
+      for (std::size_t h = 0; h < a; ++h) {
+        const bool part = h + 1 < a;
+        e.node(T::RowLengthen, part ? std::int32_t(h) : -1, std::int32_t(j), std::int32_t(h),
+               std::int32_t(a + b - 1),
+               {part ? e.slot(K::MT, j, 0, 0, a - 1) : e.slot(K::M, j, a - 1, 0, 0),
+                e.slot(K::E, h, 0, 0, j), e.slot(K::E, h, 0, 0, b - 1)},
                {e.slot(K::M, j, h, 0, a - h)});
+      }
   // Step 3
   for (std::size_t k = 0; k < b; ++k)
     e.node(T::Copy, -1, std::int32_t(k), -1, std::int32_t(a + b + (b - 1 - k)),
@@ -377,8 +390,12 @@ PlanHandles build_plan_fused(TaskGraph& graph, const Mat& C, const FieldSpec& fi
         }
       }
     hd.k_final.resize(a);
+    hd.k_part.resize(a);
     for (std::size_t i = 0; i < a; ++i)
-      for (std::size_t h = 0; h <= i; ++h) hd.k_final[i].push_back(e.slot(K::K, i, h, 0, b - 1));
+      for (std::size_t h = 0; h <= i; ++h) {
+        hd.k_final[i].push_back(h == i ? e.slot(K::K, i, i, 0, b - 1) : e.slot(K::KW, i, 0, 0, b - 1));
+        hd.k_part[i].push_back(h == i ? -1 : std::int32_t(h));
+      }
   }
   graph.drop_key_index_if_large();
   return hd;
@@ -456,7 +473,7 @@ EchelonOutput echelonize(const Mat& C, const FieldSpec& field, const EchelonizeO
     out.T_K_blocks.resize(a);
     for (std::size_t i = 0; i < a; ++i)
       for (std::size_t hh = 0; hh <= i; ++hh)
-        out.T_K_blocks[i].push_back(std::get<Mat>(*graph.payload(h.k_final[i][hh])));
+        out.T_K_blocks[i].push_back(value_of(h.k_final[i][hh], h.k_part.empty() ? -1 : h.k_part[i][hh]));
   }
   return out;
 }

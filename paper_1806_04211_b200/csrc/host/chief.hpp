@@ -49,7 +49,7 @@ struct PlanHandles {
   std::vector<std::int32_t> d_final, e_final;
   std::vector<std::vector<std::int32_t>> r_final, m_final, k_final;
   // fused plan: the block is part r_part / m_part of a MatParts slot (-1: plain)
-  std::vector<std::vector<std::int32_t>> r_part, m_part;
+  std::vector<std::vector<std::int32_t>> r_part, m_part, k_part;
 };
 
 /// reference include/gfrref/chief.hpp:72: Steps 1-3 into a fresh graph.

@@ -36,6 +36,7 @@ int Sharding::owner(const TaskNode& nd) const {
     case TaskKind::UpdateRowW:
     case TaskKind::ClearUpRW:
     case TaskKind::ClearUpMW:
+    case TaskKind::UpdateRowTrafoW:
       throw std::logic_error("fused (single-GPU) tasks cannot be sharded");
   }
   return -1;

@@ -2,6 +2,7 @@
 #include "jobs.hpp"
 
 #include <algorithm>
+#include <string>
 #include <atomic>
 #include <stdexcept>
 
@@ -78,12 +79,18 @@ Mat mat_mul(const FieldSpec& f, const Mat& b, const Mat& c) {
   return mul_add_kernel(f, nullptr, b, c);
 }
 
+Mat col_gather(const Mat& m, std::int64_t out_cols, const std::vector<std::int32_t>& cmap) {
+  return select(m.rows(), out_cols, m, nullptr, nullptr, &cmap);
+}
+
 void mad_into(const FieldSpec& f, const Mat& d, const Mat* addend, const Mat& b, const Mat& c) {
   if (b.cols() != c.rows()) throw std::invalid_argument("mul: inner dimensions disagree");
   if (d.rows() != b.rows() || d.cols() != c.cols())
     throw std::invalid_argument("mad_into: destination shape mismatch");
   if (addend && (addend->rows() != b.rows() || addend->cols() != c.cols()))
-    throw std::invalid_argument("mad: addend shape mismatch");
+    throw std::invalid_argument("mad_into: addend shape mismatch (" + std::to_string(addend->rows()) +
+                                "x" + std::to_string(addend->cols()) + " vs " +
+                                std::to_string(b.rows()) + "x" + std::to_string(c.cols()) + ")");
   if (d.empty()) return;
   dev::mad(f.p(), d.rows(), d.cols(), b.cols(), b.data(), b.ld(), c.data(), c.ld(),
            addend ? addend->data() : nullptr, addend ? addend->ld() : 0, d.data(), d.ld(),

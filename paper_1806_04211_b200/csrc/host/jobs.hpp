@@ -21,6 +21,8 @@ Mat mat_mul_add(const FieldSpec& f, const Mat& a, const Mat& b, const Mat& c);  
 /// d = (addend ? addend : 0) + b.c written into an existing matrix or view
 /// (the fused plan's wide outputs); addend may alias d.
 void mad_into(const FieldSpec& f, const Mat& d, const Mat* addend, const Mat& b, const Mat& c);
+/// out[:, c] = m[:, cmap[c]] (cmap[c] = -1: zero column), one K3 launch.
+Mat col_gather(const Mat& m, std::int64_t out_cols, const std::vector<std::int32_t>& cmap);
 
 /// Negative reduced echelonisation of one block (jobs.hpp:50).  Same
 /// recursion as the reference (split the longer dimension, combine), base

@@ -113,7 +113,7 @@ struct Printer {
     static const char* names[kSlots] = {
         "malloc", "free",  "upload", "mad", "select", "event", "memset", "alloc_miss", "sync",
         "other_launch", "task", "ClearDown", "UpdateRow", "UpdateRowTrafo", "Extend", "RowLengthen",
-        "PreClearUp", "ClearUp", "Copy", "UpdateRowW", "ClearUpRW", "ClearUpMW"};
+        "PreClearUp", "ClearUp", "Copy", "UpdateRowW", "ClearUpRW", "ClearUpMW", "UpdateRowTrafoW"};
     for (int q = 0; q < kSlots; ++q)
       std::fprintf(stderr, "hostprof %-12s %10.3f ms %8lld calls %8.2f us/call\n", names[q],
                    double(g_ns[q]) / 1e6, static_cast<long long>(g_cnt[q].load()),

@@ -15,6 +15,17 @@ std::pair<PkgD, PkgA> clear_down(const FieldSpec& f, const Mat& C, const PkgD& D
                                  std::size_t i, std::size_t ech_threshold = 256);
 std::pair<Mat, Mat> update_row(const FieldSpec& f, const PkgA& A, const Mat& C,
                                const std::optional<Mat>& B, std::size_t i);
+/// UpdateRowTrafo(i, j, h) for every h < i at once (fused plan).  Kw: the
+/// K(i, h, j-1) panel (j > 0); Mw: M(j, h, i-1-h) for h < i-1 as a panel
+/// (i >= 2), Md: M(j, i-1, 0); deltas[h] = E(h, j).delta.  Returns the
+/// K(i, h, j) and M(j, h, i-h) panels in the padded layout of the widths
+/// |delta_h|.
+std::pair<MatParts, MatParts> update_row_trafo_off(const FieldSpec& f, const PkgA& A,
+                                                   const MatParts* Kw, const MatParts* Mw,
+                                                   const Mat& Md,
+                                                   const std::vector<const BitString*>& deltas,
+                                                   std::size_t i, std::size_t j);
+
 std::pair<Mat, Mat> update_row_trafo(const FieldSpec& f, const PkgA& A,
                                      const std::optional<Mat>& K,
                                      const std::optional<Mat>& M, const PkgE& E,

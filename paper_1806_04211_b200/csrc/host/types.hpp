@@ -160,6 +160,25 @@ struct PkgE {
   std::size_t byte_size() const { return rho.byte_size() + delta.byte_size(); }
 };
 
+/// A block-row (or block-column-set) panel stored as ONE device matrix: part
+/// p is columns [off[p], off[p] + w[p]) of m.  Part starts are 16-column
+/// aligned (TMA-legal views); padding columns hold don't-care residues.  The
+/// fused single-GPU plan uses it to run one wide job instead of one per block.
+struct MatParts {
+  Mat m;
+  std::vector<std::int64_t> off, w;
+  std::size_t parts() const { return w.size(); }
+  Mat part(std::size_t p) const { return m.col_view(off[p], w[p]); }
+  /// parts [p, end) as one view (their padded span)
+  Mat tail(std::size_t p) const {
+    return p == 0 ? m : m.col_view(off[p], m.cols() - off[p]);
+  }
+  MatParts tail_parts(std::size_t p) const;
+  std::size_t byte_size() const { return m.byte_size(); }
+};
+/// Padded layout for part widths: starts rounded up to 16 columns.
+MatParts layout_parts(std::int64_t rows, const std::vector<std::int64_t>& widths);
+
 // ---------------------------------------------------------------- staging
 /// Upload a small host int32 array to a fresh device buffer on the current
 /// stream (through a pinned staging ring).

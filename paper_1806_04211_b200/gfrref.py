@@ -606,7 +606,7 @@ class EchelonizeOptions:
 
 
 TASK_KINDS = ["ClearDown", "UpdateRow", "UpdateRowTrafo", "Extend", "RowLengthen", "PreClearUp", "ClearUp", "Copy",
-              "UpdateRowW", "ClearUpRW", "ClearUpMW"]
+              "UpdateRowW", "ClearUpRW", "ClearUpMW", "UpdateRowTrafoW"]
 
 
 class EchelonOutput:

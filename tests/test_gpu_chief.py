@@ -253,3 +253,5 @@ def test_fused_plan_matches_reference_grid(G, p, m, n, block, kind, wt):
                                                                        collect_trace=True)).trace()}
     if b > 2:
         assert "UpdateRowW" in kinds and "ClearUpRW" in kinds
+    if wt and a > 1:
+        assert "UpdateRowTrafoW" in kinds
