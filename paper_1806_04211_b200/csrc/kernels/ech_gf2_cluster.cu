@@ -3,20 +3,29 @@
 // shared memory of ONE 8-CTA thread-block cluster (each CTA holds a stripe of
 // <= 128 rows), and every exchange between CTAs goes through distributed
 // shared memory with cluster barriers instead of global memory and grid
-// barriers.  Per 32-column panel (right-looking Gauss-Jordan with the
-// reference's column-wise pivot rule, src/chief.cpp:436-460):
-//   a. every CTA pushes word `wi` of its rows into the leader's `orig`;
-//   b. the leader finds the panel's pivots and each row's multiplier word
-//      G[i] (which pivot rows' ORIGINAL values to add): warp 0 runs the chain
-//      on a 64-row window starting at the first non-pivotal row, tracking per
-//      row the set of pivots added (Gauss-Jordan, so pivot rows are reduced
-//      too); rows outside the window get G from nibble tables of the pivots'
-//      coefficient sets.  A column without a window candidate sends the panel
-//      to a CTA-wide chain over all rows.  G and the pivot list are pushed to
-//      the owning CTAs;
-//   c. every CTA pulls the panel's pivot rows from their owners (DSMEM loads);
-//   d. every CTA updates its stripe: row ^= XOR_{q in G} pivot_q, through
-//      per-panel nibble tables of pivot-row combinations (8 lookups a word).
+// barriers.  Right-looking Gauss-Jordan over 32-column panels with the
+// reference's column-wise pivot rule (src/chief.cpp:436-460).
+//
+// The leader (CTA 0) finds a panel's pivots from the rows' panel words: warp
+// 0 runs the chain on a 64-row window from the first non-pivotal row (the
+// chosen row is the FIRST non-pivotal one with the bit, so a full-rank
+// panel's pivots are all there), in column layout (lane q holds column q as
+// a 64-bit row mask: a pivot step is one broadcast and one masked XOR per
+// lane), tracking for every window row the set of pivots added to it.
+// Gauss-Jordan, so a pivot row's set is its multiplier word G; any other
+// row's G is the XOR, over the pivot columns set in its panel word, of that
+// pivot's (own + set) -- evaluated by every CTA for its own rows from nibble
+// tables.  A column without a window candidate sends the panel to a
+// CTA-wide chain over all rows.
+//
+// Per panel k (one-panel look-ahead):
+//   1. every CTA: G for its rows; pull the panel's pivot rows (DSMEM loads)
+//      and build nibble tables of pivot-row combinations;  -- barrier Y
+//   2. every CTA updates word k+1 of its rows and pushes it to the leader;
+//      arrive Z; the leader's warp 0 waits on Z and factorizes panel k+1
+//      while all other warps update the rest of their stripes (8 table
+//      lookups a word); wait Z;
+//   3. the leader publishes panel k+1's pivots to every CTA;  -- barrier X.
 // The reduced block is unpacked to u8 at the end; pivots go to
 // info = [rank, cols[cap], rows[cap]] like the other ECH paths.
 #include <cooperative_groups.h>
@@ -56,24 +65,29 @@ __device__ __forceinline__ unsigned long long gtime() {
   return t;
 }
 
+__device__ __forceinline__ void cl_arrive() {
+  asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void cl_wait() {
+  asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+
 __global__ void __launch_bounds__(kThreads, 1) ech_gf2_cluster_kernel(ClArgs g) {
   extern __shared__ __align__(16) std::uint32_t sm[];
   const int Wd = g.Wd, rows = g.rows, cols = g.cols;
-  std::uint32_t* A = sm;                       // kStripe x Wd   (my rows)
-  std::uint32_t* bp = A + kStripe * Wd;        // 32 x Wd        (pivot rows of the panel)
-  std::uint32_t* orig = bp + 32 * Wd;          // 1024           (leader: panel word per row)
-  std::uint32_t* gl = orig + 1024;             // kStripe        (multiplier word per my row)
-  std::uint8_t* fl = reinterpret_cast<std::uint8_t*>(gl + kStripe);  // 1024 (leader)
-  std::uint32_t* gall = reinterpret_cast<std::uint32_t*>(fl + 1024);  // 1024 (leader: G per row)
-  std::uint32_t* tab = gall + 1024;  // 128 x Wd nibble tables (when Wd <= kTabWd)
+  std::uint32_t* A = sm;                        // kStripe x Wd   (my rows)
+  std::uint32_t* bp = A + kStripe * Wd;         // 32 x Wd        (pivot rows of the panel)
+  std::uint32_t* orig = bp + 32 * Wd;           // 1024           (leader: panel word per row)
+  std::uint32_t* gl = orig + 1024;              // kStripe        (multiplier word per my row)
+  std::uint8_t* fl = reinterpret_cast<std::uint8_t*>(gl + kStripe);   // 1024 (leader: pivotal)
+  std::uint32_t* gall = reinterpret_cast<std::uint32_t*>(fl + 1024);  // 1024 (leader fallback)
+  std::uint32_t* tab = gall + 1024;             // 128 x Wd nibble tables (when Wd <= kTabWd)
   const bool use_tab = Wd <= kTabWd;
-  __shared__ int pc[32], pr[32];
-  __shared__ int r2_sh;
+  // the current panel's pivots (the leader's copy is authoritative)
+  __shared__ int pc[32], pr[32], r2_sh, ok_sh, lo_sh;
+  __shared__ std::uint32_t pcoef[32], ntab[128];
   __shared__ std::uint32_t nomw[2][32], nomc[2][32];
   __shared__ unsigned best[3];
-  __shared__ int lo_sh, win_ok;
-  __shared__ std::uint32_t pcoef[32], ntab[128];
-  __shared__ std::uint8_t thisp[1024];
 
   cg::cluster_group cluster = cg::this_cluster();
   const int cr = int(cluster.block_rank());
@@ -81,6 +95,14 @@ __global__ void __launch_bounds__(kThreads, 1) ech_gf2_cluster_kernel(ClArgs g) 
   const int row0 = cr * kStripe;
   const int nloc = rows - row0 < 0 ? 0 : (rows - row0 < kStripe ? rows - row0 : kStripe);
   std::uint32_t* lead_orig = cluster.map_shared_rank(orig, 0);
+  const int npan = (cols + 31) / 32;
+  auto pmask = [&](int k) {
+    const int wc = cols - 32 * k < 32 ? cols - 32 * k : 32;
+    return wc == 32 ? 0xFFFFFFFFu : ((1u << wc) - 1u);
+  };
+  auto stamp = [&](int k, int ph) {
+    if (g.dbg && cr == 0 && tid == 0 && k < 8) g.dbg[k * 16 + ph] = gtime();
+  };
 
   // ---- pack my stripe of [H | I] (warp per row, lane per word)
   for (int li = warp; li < nloc; li += kThreads / 32) {
@@ -114,248 +136,213 @@ __global__ void __launch_bounds__(kThreads, 1) ech_gf2_cluster_kernel(ClArgs g) 
       orig[i] = 0u;
     }
     if (tid == 0) lo_sh = 0;
-    for (int i = tid; i < 1024; i += kThreads) thisp[i] = 0;
   }
   cluster.sync();
 
-  const int npan = (cols + 31) / 32;
+  // ---- leader: pivots of panel k from `orig` (window chain in warp 0; the
+  // caller falls back to full_chain when ok_sh == 0)
+  auto window_chain = [&](int k) {
+    const int wc = cols - 32 * k < 32 ? cols - 32 * k : 32;
+    int lo = lo_sh;
+    for (;;) {
+      const int idx = lo + lane;
+      const unsigned b = __ballot_sync(0xffffffffu, idx < rows && fl[idx] == 0);
+      if (b || lo >= rows) {
+        if (b) lo += __ffs(b) - 1;
+        break;
+      }
+      lo += 32;
+    }
+    if (lo > rows) lo = rows;
+    const int i0 = lo + lane, i1 = lo + 32 + lane;
+    const std::uint32_t w0 = i0 < 1024 ? orig[i0] : 0u, w1 = i1 < 1024 ? orig[i1] : 0u;
+    const bool p0 = i0 >= rows || fl[i0] != 0, p1 = i1 >= rows || fl[i1] != 0;
+    std::uint64_t cmask = 0, kmask = 0;
+#pragma unroll
+    for (int q = 0; q < 32; ++q) {
+      const unsigned lo32 = __ballot_sync(0xffffffffu, (w0 >> q) & 1u);
+      const unsigned hi32 = __ballot_sync(0xffffffffu, (w1 >> q) & 1u);
+      if (lane == q) cmask = std::uint64_t(lo32) | (std::uint64_t(hi32) << 32);
+    }
+    std::uint64_t piv = std::uint64_t(__ballot_sync(0xffffffffu, p0)) |
+                        (std::uint64_t(__ballot_sync(0xffffffffu, p1)) << 32);
+    int r2 = 0, ok = 1;
+    for (int c = 0; c < wc; ++c) {
+      const std::uint64_t col = __shfl_sync(0xffffffffu, cmask, c);
+      const std::uint64_t cand = col & ~piv;
+      if (!cand) {  // uniform
+        ok = 0;
+        break;
+      }
+      const int pw = __ffsll(static_cast<long long>(cand)) - 1;
+      const std::uint64_t sset = col & ~(std::uint64_t(1) << pw);
+      if ((cmask >> pw) & 1u) cmask ^= sset;
+      if (lane < r2 && ((kmask >> pw) & 1u)) kmask ^= sset;
+      if (lane == r2) kmask = sset;
+      piv |= std::uint64_t(1) << pw;
+      if (lane == 0) {
+        pc[r2] = c;
+        pr[r2] = lo + pw;
+      }
+      ++r2;
+    }
+    __syncwarp();
+    if (ok)
+      for (int t = 0; t < r2; ++t) {
+        const unsigned cf = __ballot_sync(0xffffffffu, (kmask >> (pr[t] - lo)) & 1u);
+        if (lane == t) pcoef[t] = cf ^ (1u << t);
+      }
+    if (lane == 0) {
+      ok_sh = ok;
+      r2_sh = r2;
+      lo_sh = lo;
+    }
+  };
+  // CTA-wide chain over all rows (warps 0..7, 4 rows per lane); leader CTA,
+  // every thread calls it
+  auto full_chain = [&](int k) {
+    const int wc = cols - 32 * k < 32 ? cols - 32 * k : 32;
+    constexpr int kChainWarps = 8, kRowsPerLane = 1024 / (32 * kChainWarps);
+    if (warp < kChainWarps) {
+      std::uint32_t word[kRowsPerLane], coef[kRowsPerLane];
+      std::uint32_t pivm = 0;  // bit s: row 256*s + tid is pivotal
+#pragma unroll
+      for (int s2 = 0; s2 < kRowsPerLane; ++s2) {
+        word[s2] = orig[256 * s2 + tid];
+        coef[s2] = 0u;
+        pivm |= std::uint32_t(fl[256 * s2 + tid] != 0) << s2;
+      }
+      int r2 = 0;
+      if (tid < 3) best[tid] = 0xFFFFFFFFu;
+      asm volatile("bar.sync 1, 256;" ::: "memory");
+#pragma unroll 1
+      for (int c = 0; c < wc; ++c) {
+        const int par = c & 1, b3 = c % 3;
+        int ws = -1, wl = 0;
+#pragma unroll
+        for (int s2 = 0; s2 < kRowsPerLane; ++s2) {
+          const unsigned b =
+              __ballot_sync(0xffffffffu, ((word[s2] >> c) & 1u) && !((pivm >> s2) & 1u));
+          if (ws < 0 && b) {
+            ws = s2;
+            wl = __ffs(b) - 1;
+          }
+        }
+        if (ws >= 0 && lane == wl) {
+          std::uint32_t wv = 0, cv = 0;
+#pragma unroll
+          for (int t = 0; t < kRowsPerLane; ++t)
+            if (t == ws) {
+              wv = word[t];
+              cv = coef[t];
+            }
+          nomw[par][warp] = wv;
+          nomc[par][warp] = cv;
+          atomicMin(&best[b3], unsigned(256 * ws + 32 * warp + wl));
+        }
+        asm volatile("bar.sync 1, 256;" ::: "memory");
+        const unsigned m = best[b3];
+        // column c-1's buffer: its readers all passed this barrier, and
+        // column c+2's nominations come after the next one
+        if (tid == 0) best[(c + 2) % 3] = 0xFFFFFFFFu;
+        if (m == 0xFFFFFFFFu) continue;  // uniform: no pivot in column c
+        const unsigned owner = (m & 255u) >> 5;
+        const std::uint32_t pw = nomw[par][owner], pcf = nomc[par][owner] ^ (1u << r2);
+#pragma unroll
+        for (int s2 = 0; s2 < kRowsPerLane; ++s2) {
+          const unsigned row = unsigned(256 * s2 + tid);
+          if (row == m) {
+            pivm |= 1u << s2;
+          } else if ((word[s2] >> c) & 1u) {
+            word[s2] ^= pw;
+            coef[s2] ^= pcf;
+          }
+        }
+        if (tid == 0) {
+          pc[r2] = c;
+          pr[r2] = int(m);
+        }
+        ++r2;
+      }
+#pragma unroll
+      for (int s2 = 0; s2 < kRowsPerLane; ++s2) gall[256 * s2 + tid] = coef[s2];
+      if (tid == 0) r2_sh = r2;
+    }
+    __syncthreads();
+    if (tid < r2_sh) pcoef[tid] = gall[pr[tid]] ^ (1u << tid);
+    __syncthreads();
+  };
+  // leader, every thread: record panel k's pivots and send them to CTAs 1..7
+  auto publish = [&](int k, int rtot) {
+    const int r2 = r2_sh;
+    if (tid < r2) {
+      g.info[1 + rtot + tid] = 32 * k + pc[tid];
+      g.info[1 + g.cap + rtot + tid] = pr[tid];
+      fl[pr[tid]] = 1;
+    }
+    if (tid >= 32 && tid < kCl * 32) {
+      const unsigned dst = unsigned(tid >> 5);
+      const int q = tid & 31;
+      if (q < r2) {
+        *cluster.map_shared_rank(&pr[q], dst) = pr[q];
+        *cluster.map_shared_rank(&pc[q], dst) = pc[q];
+        *cluster.map_shared_rank(&pcoef[q], dst) = pcoef[q];
+      }
+      if (q == 0) *cluster.map_shared_rank(&r2_sh, dst) = r2;
+    }
+  };
+
+  // ---- panel 0 pivots (no look-ahead yet)
+  {
+    const std::uint32_t pm = pmask(0);
+    for (int li = tid; li < nloc; li += kThreads) lead_orig[row0 + li] = A[li * Wd] & pm;
+  }
+  cluster.sync();
+  if (cr == 0) {
+    if (warp == 0) window_chain(0);
+    __syncthreads();
+    if (!ok_sh) full_chain(0);
+    __syncthreads();
+    publish(0, 0);
+  }
+  cluster.sync();
+
   int rtot = 0;
   for (int k = 0; k < npan; ++k) {
-    const int wi = k, c0 = 32 * k;
-    const int wc = cols - c0 < 32 ? cols - c0 : 32;
-    const std::uint32_t pm = wc == 32 ? 0xFFFFFFFFu : ((1u << wc) - 1u);
-    auto stamp = [&](int ph) {
-      if (g.dbg && cr == 0 && tid == 0 && k < 8) {
-        g.dbg[k * 16 + ph] = gtime();
-        if (ph == 0) g.dbg[k * 16 + 15] = clock64();
-        if (ph == 7) g.dbg[k * 16 + 14] = clock64();
-      }
-    };
-    stamp(0);
-    // a. panel word of my rows -> leader
-    for (int li = tid; li < nloc; li += kThreads) lead_orig[row0 + li] = A[li * Wd + wi] & pm;
-    cluster.sync();
-    stamp(1);
-
-    // b. leader: the pivot chain, CTA-wide.  Thread t owns row t: its
-    // current panel word and `coef`, the set of this panel's pivot rows (by
-    // pivot index) whose ORIGINAL rows have been added to it.  Per column,
-    // every warp nominates its first non-pivotal row with the bit set (word
-    // and coef), one barrier, every warp min-reduces the nominations, and
-    // EVERY other row with the bit set (pivotal ones too: Gauss-Jordan) adds
-    // the pivot row.  Selection only looks at non-pivotal rows, so the pivots
-    // are the reference's; at the end row t = orig_t + sum_{q in coef_t}
-    // orig(pivot q) is reduced on all pivot columns, i.e. coef_t is its
-    // multiplier word G[t].
-    if (cr == 0) {
-      // Fast path: the first 64 rows from the first non-pivotal one hold
-      // every pivot of a full-rank panel (the chosen row is the FIRST
-      // non-pivotal one with the bit), so warp 0 runs the chain on that
-      // window alone (2 rows per lane, no barriers).  If some column has no
-      // candidate inside the window the whole panel goes to the CTA-wide
-      // chain instead (free columns, rank-deficient blocks).
-      if (warp == 0) {
-        int lo = lo_sh;
-        for (;;) {
-          const int idx = lo + lane;
-          const unsigned b = __ballot_sync(0xffffffffu, idx < rows && fl[idx] == 0);
-          if (b || lo >= rows) {
-            if (b) lo += __ffs(b) - 1;
-            break;
-          }
-          lo += 32;
-        }
-        if (lo > rows) lo = rows;
-        const int i0 = lo + lane, i1 = lo + 32 + lane;
-        std::uint32_t w0 = i0 < 1024 ? orig[i0] : 0u, w1 = i1 < 1024 ? orig[i1] : 0u;
-        bool p0 = i0 >= rows || fl[i0] != 0, p1 = i1 >= rows || fl[i1] != 0;
-        std::uint32_t cf0 = 0, cf1 = 0;
-        int r2 = 0, ok = 1;
-        for (int c = 0; c < wc; ++c) {
-          const unsigned b0 = __ballot_sync(0xffffffffu, ((w0 >> c) & 1u) && !p0);
-          const unsigned b1 = __ballot_sync(0xffffffffu, ((w1 >> c) & 1u) && !p1);
-          if (!(b0 | b1)) {
-            ok = 0;
-            break;
-          }
-          const int hi = b0 ? 0 : 1;
-          const int sl = __ffs(hi ? b1 : b0) - 1;
-          const std::uint32_t pw = __shfl_sync(0xffffffffu, hi ? w1 : w0, sl);
-          const std::uint32_t pcf = __shfl_sync(0xffffffffu, hi ? cf1 : cf0, sl) ^ (1u << r2);
-          const bool me0 = !hi && lane == sl, me1 = hi && lane == sl;
-          if (me0) p0 = true;
-          else if ((w0 >> c) & 1u) {
-            w0 ^= pw;
-            cf0 ^= pcf;
-          }
-          if (me1) p1 = true;
-          else if ((w1 >> c) & 1u) {
-            w1 ^= pw;
-            cf1 ^= pcf;
-          }
-          if (lane == 0) {
-            pc[r2] = c;
-            pr[r2] = lo + 32 * hi + sl;
-          }
-          ++r2;
-        }
-        if (lane == 0) {
-          win_ok = ok;
-          r2_sh = r2;
-          lo_sh = lo;
-        }
-        if (ok) {
-          // the pivots' own multipliers (others are recomputed below)
-          if (i0 < rows) gall[i0] = cf0;
-          if (i1 < rows) gall[i1] = cf1;
-          __syncwarp();
-          if (lane < r2) pcoef[lane] = gall[pr[lane]] ^ (1u << lane);
-        }
-      }
-      __syncthreads();
-      if (win_ok) {
-        // G[i] = XOR over the pivot columns set in orig_i of (own original +
-        // coef) of that column's pivot, via 8 nibble tables
-        // ntab[k][m] = XOR_{b in m} pcoef(pivot of column 4k+b).  This
-        // panel's pivot rows keep their chain coef.
-        const int r2 = r2_sh;
-        if (tid < 128) {
-          const int kq = tid >> 4, m = tid & 15;
-          std::uint32_t v = 0;
-          for (int q = 0; q < r2; ++q) {
-            const int cq = pc[q];
-            if ((cq >> 2) == kq && ((m >> (cq & 3)) & 1)) v ^= pcoef[q];
-          }
-          ntab[tid] = v;
-        }
-        if (tid < r2) thisp[pr[tid]] = 1;
-        __syncthreads();
-        for (int i = tid; i < rows; i += kThreads) {
-          if (thisp[i]) continue;
-          const std::uint32_t ow = orig[i];
-          std::uint32_t gv = 0;
-#pragma unroll
-          for (int kq = 0; kq < 8; ++kq) gv ^= ntab[16 * kq + ((ow >> (4 * kq)) & 15u)];
-          gall[i] = gv;
-        }
-        __syncthreads();
-        if (tid < r2) {
-          fl[pr[tid]] = 1;
-          thisp[pr[tid]] = 0;
-        }
-      } else {
-      constexpr int kChainWarps = 8, kRowsPerLane = 1024 / (32 * kChainWarps);
-        if (warp < kChainWarps) {
-          std::uint32_t word[kRowsPerLane], coef[kRowsPerLane];
-          std::uint32_t pivm = 0;  // bit s: row 256*s + tid is pivotal
-#pragma unroll
-          for (int s2 = 0; s2 < kRowsPerLane; ++s2) {
-            word[s2] = orig[256 * s2 + tid];
-            coef[s2] = 0u;
-            pivm |= std::uint32_t(fl[256 * s2 + tid] != 0) << s2;
-          }
-          int r2 = 0;
-          if (tid < 3) best[tid] = 0xFFFFFFFFu;
-          asm volatile("bar.sync 1, 256;" ::: "memory");
-#pragma unroll 1
-          for (int c = 0; c < wc; ++c) {
-            const int par = c & 1, b3 = c % 3;
-            // this warp's first non-pivotal row with bit c: rows 256*s + tid,
-            // so the smallest s with any candidate lane, then the lowest lane
-            int ws = -1, wl = 0;
-#pragma unroll
-            for (int s2 = 0; s2 < kRowsPerLane; ++s2) {
-              const unsigned b =
-                  __ballot_sync(0xffffffffu, ((word[s2] >> c) & 1u) && !((pivm >> s2) & 1u));
-              if (ws < 0 && b) {
-                ws = s2;
-                wl = __ffs(b) - 1;
-              }
-            }
-            if (ws >= 0 && lane == wl) {
-              std::uint32_t wv = 0, cv = 0;
-#pragma unroll
-              for (int t = 0; t < kRowsPerLane; ++t)
-                if (t == ws) {
-                  wv = word[t];
-                  cv = coef[t];
-                }
-              nomw[par][warp] = wv;
-              nomc[par][warp] = cv;
-              atomicMin(&best[b3], unsigned(256 * ws + 32 * warp + wl));
-            }
-            asm volatile("bar.sync 1, 256;" ::: "memory");
-            const unsigned m = best[b3];
-            // column c-1's buffer: its readers all passed this barrier, and
-            // column c+2's nominations come after the next one
-            if (tid == 0) best[(c + 2) % 3] = 0xFFFFFFFFu;
-            if (m == 0xFFFFFFFFu) continue;  // uniform: no pivot in column c
-            const unsigned owner = (m & 255u) >> 5;
-            const std::uint32_t pw = nomw[par][owner], pcf = nomc[par][owner] ^ (1u << r2);
-#pragma unroll
-            for (int s2 = 0; s2 < kRowsPerLane; ++s2) {
-              const unsigned row = unsigned(256 * s2 + tid);
-              if (row == m) {
-                pivm |= 1u << s2;
-              } else if ((word[s2] >> c) & 1u) {
-                word[s2] ^= pw;
-                coef[s2] ^= pcf;
-              }
-            }
-            if (tid == 0) {
-              pc[r2] = c;
-              pr[r2] = int(m);
-            }
-            ++r2;
-            }
-  #pragma unroll
-          for (int s2 = 0; s2 < kRowsPerLane; ++s2) {
-            const int i = 256 * s2 + tid;
-            gall[i] = coef[s2];
-            if ((pivm >> s2) & 1u) fl[i] = 1;
-          }
-          if (tid == 0) r2_sh = r2;
-        }
-      }
-      __syncthreads();  // gall, pc / pr / r2 complete
-      const int r2 = r2_sh;
-      for (int i = tid; i < rows; i += kThreads)
-        *cluster.map_shared_rank(&gl[i % kStripe], unsigned(i / kStripe)) = gall[i];
-      if (tid < r2) {
-        g.info[1 + rtot + tid] = c0 + pc[tid];
-        g.info[1 + g.cap + rtot + tid] = pr[tid];
-      }
-      // pivot list -> every CTA
-      if (tid < kCl * 32) {
-        const unsigned dst = unsigned(tid >> 5);
-        const int q = tid & 31;
-        if (q < r2) *cluster.map_shared_rank(&pr[q], dst) = pr[q];
-        if (q == 0) *cluster.map_shared_rank(&r2_sh, dst) = r2;
-      }
-      stamp(2);
-    }
-    stamp(3);
-    cluster.sync();
-    stamp(4);
-
+    const int wi = k;
     const int r2 = r2_sh;
+    const std::uint32_t pm = pmask(k);
+    const bool has_next = k + 1 < npan;
+    const int nw = Wd - wi;
+    stamp(k, 0);
+    // 1. G for my rows, pivot rows, tables
     if (r2 > 0) {
-      // c. pull the pivot rows (words >= wi) from their owners' stripes
-      const int nw = Wd - wi;
+      if (tid < 128) {
+        const int kq = tid >> 4, m = tid & 15;
+        std::uint32_t v = 0;
+        for (int q = 0; q < r2; ++q) {
+          const int cq = pc[q];
+          if ((cq >> 2) == kq && ((m >> (cq & 3)) & 1)) v ^= pcoef[q];
+        }
+        ntab[tid] = v;
+      }
       for (int e = tid; e < r2 * nw; e += kThreads) {
         const int q = e / nw, w = wi + e % nw;
         const int row = pr[q];
-        const std::uint32_t* src =
-            cluster.map_shared_rank(&A[(row % kStripe) * Wd + w], unsigned(row / kStripe));
-        bp[q * Wd + w] = *src;
+        bp[q * Wd + w] =
+            *cluster.map_shared_rank(&A[(row % kStripe) * Wd + w], unsigned(row / kStripe));
       }
-      stamp(5);
-      cluster.sync();  // every pull done before any owner rewrites a pivot row
-      stamp(6);
-      // d. update my stripe.  With the nibble tables (Wd <= kTabWd):
-      // tab[k][m][w] = XOR_{b in m} pivot_{4k+b}[w], so a row's update is 8
-      // lookups per word instead of one XOR per set multiplier bit.
-      if (use_tab) {
+      __syncthreads();
+      for (int li = tid; li < nloc; li += kThreads) {
+        const std::uint32_t ow = A[li * Wd + wi] & pm;
+        std::uint32_t gv = 0;
+#pragma unroll
+        for (int kq = 0; kq < 8; ++kq) gv ^= ntab[16 * kq + ((ow >> (4 * kq)) & 15u)];
+        for (int q = 0; q < r2; ++q)
+          if (pr[q] == row0 + li) gv = pcoef[q] ^ (1u << q);
+        gl[li] = gv;
+      }
+      if (use_tab)
         for (int e = tid; e < 128 * nw; e += kThreads) {
           const int km = e / nw, w = wi + e % nw;
           const int kq = km >> 4, m = km & 15;
@@ -365,38 +352,69 @@ __global__ void __launch_bounds__(kThreads, 1) ech_gf2_cluster_kernel(ClArgs g) 
             if (((m >> b2) & 1) && 4 * kq + b2 < r2) v ^= bp[(4 * kq + b2) * Wd + w];
           tab[km * Wd + w] = v;
         }
-        __syncthreads();
-        for (int li = warp; li < nloc; li += kThreads / 32) {
-          const std::uint32_t gv = gl[li];
-          if (!gv) continue;
-          std::uint32_t* arow = A + li * Wd;
-          for (int w = wi + lane; w < Wd; w += 32) {
-            std::uint32_t x = arow[w];
+      __syncthreads();
+    }
+    stamp(k, 1);
+    cluster.sync();  // Y: every pull done before any stripe changes
+    stamp(k, 2);
+
+    // word w of my row li after this panel
+    auto upd = [&](int li, int w) {
+      const std::uint32_t gv = gl[li];
+      std::uint32_t x = A[li * Wd + w];
+      if (use_tab) {
 #pragma unroll
-            for (int kq = 0; kq < 8; ++kq) x ^= tab[(16 * kq + ((gv >> (4 * kq)) & 15u)) * Wd + w];
-            arow[w] = x;
-          }
-        }
+        for (int kq = 0; kq < 8; ++kq) x ^= tab[(16 * kq + ((gv >> (4 * kq)) & 15u)) * Wd + w];
       } else {
-        for (int li = warp; li < nloc; li += kThreads / 32) {
-          const std::uint32_t gv = gl[li];
-          if (!gv) continue;
-          std::uint32_t* arow = A + li * Wd;
-          for (int w = wi + lane; w < Wd; w += 32) {
-            std::uint32_t x = arow[w];
-            std::uint32_t gg = gv;
-            while (gg) {
-              const int q = __ffs(gg) - 1;
-              gg &= gg - 1;
-              x ^= bp[q * Wd + w];
-            }
-            arow[w] = x;
-          }
+        std::uint32_t gg = gv;
+        while (gg) {
+          const int q = __ffs(gg) - 1;
+          gg &= gg - 1;
+          x ^= bp[q * Wd + w];
         }
       }
-      __syncthreads();
-      stamp(7);
+      return x;
+    };
+    // 2. word k+1 first (the next panel's chain input), pushed to the leader
+    if (has_next) {
+      const std::uint32_t pmn = pmask(k + 1);
+      for (int li = tid; li < nloc; li += kThreads) {
+        const std::uint32_t x = r2 > 0 ? upd(li, wi + 1) : A[li * Wd + wi + 1];
+        A[li * Wd + wi + 1] = x;
+        lead_orig[row0 + li] = x & pmn;
+      }
     }
+    __syncthreads();
+    cl_arrive();  // Z: my panel-(k+1) words are with the leader
+    stamp(k, 3);
+    const bool chain_warp = has_next && cr == 0 && warp == 0;
+    if (chain_warp) {
+      cl_wait();
+      window_chain(k + 1);
+      stamp(k, 4);
+    }
+    // the rest of panel k's update: word wi and words wi+2.. (the leader's
+    // warp 0 is busy with the chain, so its rows go to warps 1..31)
+    if (r2 > 0) {
+      const int w_first = cr == 0 && has_next ? 1 : 0;
+      const int nwarps = 32 - w_first;
+      if (warp >= w_first)
+        for (int li = warp - w_first; li < nloc; li += nwarps)
+          for (int t = lane; t < nw; t += 32) {
+            const int w = wi + t;
+            if (has_next && w == wi + 1) continue;
+            A[li * Wd + w] = upd(li, w);
+          }
+    }
+    if (!chain_warp) cl_wait();
+    stamp(k, 5);
+    if (cr == 0 && has_next) {
+      __syncthreads();
+      if (!ok_sh) full_chain(k + 1);
+      publish(k + 1, rtot + r2);
+    }
+    cluster.sync();  // X: panel k done everywhere, panel k+1's pivots published
+    stamp(k, 6);
     rtot += r2;
   }
 
@@ -471,10 +489,9 @@ bool ech_gf2_cluster(std::int64_t rows, std::int64_t cols, const std::uint8_t* H
     const unsigned long long* dbg = hd;
     for (int k = 0; k < 4; ++k) {
       std::fprintf(stderr, "gf2cl panel %d:", k);
-      for (int ph = 1; ph < 8; ++ph)
+      for (int ph = 1; ph < 7; ++ph)
         std::fprintf(stderr, " %lld", static_cast<long long>(dbg[k * 16 + ph] - dbg[k * 16 + ph - 1]));
-      std::fprintf(stderr, " | clk %.0f MHz", double(dbg[k * 16 + 14] - dbg[k * 16 + 15]) * 1e3 /
-                                              double(dbg[k * 16 + 7] - dbg[k * 16]));
+
       std::fprintf(stderr, " | total %lld ns\n",
                    static_cast<long long>(dbg[(k + 1) * 16] - dbg[k * 16]));
     }
