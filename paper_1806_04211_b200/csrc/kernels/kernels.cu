@@ -183,14 +183,6 @@ mad_smallk_kernel(std::uint32_t p, std::uint32_t magic, int m, int n, int k,
 }
 
 // D = Cin (or 0) for the k == 0 contraction.
-__global__ void copy_or_zero_kernel(int m, int n, const std::uint8_t* Cin,
-                                    std::int64_t ldc, std::uint8_t* D,
-                                    std::int64_t ldd) {
-  for (int r = blockIdx.y; r < m; r += gridDim.y)
-    for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < n;
-         c += gridDim.x * blockDim.x)
-      D[std::int64_t(r) * ldd + c] = Cin ? Cin[std::int64_t(r) * ldc + c] : 0;
-}
 }  // namespace
 
 void mad_simt(std::uint32_t p, std::int64_t m, std::int64_t n, std::int64_t k,
@@ -199,10 +191,13 @@ void mad_simt(std::uint32_t p, std::int64_t m, std::int64_t n, std::int64_t k,
               std::uint8_t* D, std::int64_t ldd, cudaStream_t s) {
   if (m == 0 || n == 0) return;
   if (k == 0) {
-    dim3 grid(unsigned((n + 255) / 256), unsigned(m < 65535 ? m : 65535));
-    copy_or_zero_kernel<<<grid, 256, 0, s>>>(int(m), int(n), Cin, ldc, D, ldd);
-    GFQ_CUDA(cudaGetLastError());
-    count_launch();
+    // D = Cin or 0: a strided copy / memset (no kernel of ours)
+    if (Cin == D && ldc == ldd) return;
+    if (Cin)
+      GFQ_CUDA(cudaMemcpy2DAsync(D, std::size_t(ldd), Cin, std::size_t(ldc), std::size_t(n),
+                                 std::size_t(m), cudaMemcpyDeviceToDevice, s));
+    else
+      GFQ_CUDA(cudaMemset2DAsync(D, std::size_t(ldd), 0, std::size_t(n), std::size_t(m), s));
     return;
   }
   const std::int64_t kc = k_chunk_limit(p);
@@ -398,6 +393,64 @@ __global__ void select2d_kernel(std::uint8_t* dst, std::int64_t ldd,
   }
 }
 
+// General select (column map present), 16 output columns per thread: the
+// column map is read as int4 vectors and the 16 gathered bytes leave as one
+// 16-byte store (dst 16B-aligned rows).
+__global__ void select2d_v16_kernel(std::uint8_t* dst, std::int64_t ldd,
+                                    std::int64_t rows, std::int64_t cols,
+                                    const std::uint8_t* A, std::int64_t lda,
+                                    const std::uint8_t* B, std::int64_t ldb,
+                                    const std::int32_t* rmap,
+                                    const std::int32_t* cmap) {
+  const std::int64_t nvec = (cols + 15) / 16;
+  for (std::int64_t i = blockIdx.y; i < rows; i += gridDim.y) {
+    std::int32_t rv = -3;  // "no row map"
+    if (rmap) rv = rmap[i];
+    const bool rowB = rmap && rv <= -2;
+    const std::int64_t r = rmap ? (rowB ? -rv - 2 : rv) : i;
+    const std::uint8_t* arow = (rv == -1 || rowB) ? nullptr : A + r * lda;
+    const std::uint8_t* brow = B ? B + (rowB ? r : (rmap ? r : i)) * ldb : nullptr;
+    for (std::int64_t v = blockIdx.x * blockDim.x + threadIdx.x; v < nvec;
+         v += std::int64_t(gridDim.x) * blockDim.x) {
+      const std::int64_t j0 = v * 16;
+      std::uint32_t w[4] = {0, 0, 0, 0};
+      if (rv != -1) {
+        std::int32_t cm[16];
+        if (j0 + 16 <= cols && (reinterpret_cast<std::uintptr_t>(cmap + j0) & 15) == 0) {
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            const int4 c4 = reinterpret_cast<const int4*>(cmap + j0)[q];
+            cm[4 * q] = c4.x;
+            cm[4 * q + 1] = c4.y;
+            cm[4 * q + 2] = c4.z;
+            cm[4 * q + 3] = c4.w;
+          }
+        } else {
+#pragma unroll
+          for (int q = 0; q < 16; ++q) cm[q] = j0 + q < cols ? cmap[j0 + q] : -1;
+        }
+#pragma unroll
+        for (int q = 0; q < 16; ++q) {
+          const std::int32_t cv = cm[q];
+          std::uint32_t x = 0;
+          if (cv >= 0) {
+            x = rowB ? brow[cv] : arow[cv];
+          } else if (cv <= -2) {
+            x = brow[-cv - 2];
+          }
+          w[q >> 2] |= x << (8 * (q & 3));
+        }
+      }
+      if (j0 + 16 <= cols) {
+        *reinterpret_cast<uint4*>(dst + i * ldd + j0) = make_uint4(w[0], w[1], w[2], w[3]);
+      } else {
+        for (std::int64_t c = j0; c < cols; ++c)
+          dst[i * ldd + c] = std::uint8_t((w[(c - j0) >> 2] >> (8 * ((c - j0) & 3))) & 0xFF);
+      }
+    }
+  }
+}
+
 __global__ void set_entries_kernel(std::uint8_t* dst, std::int64_t ldd,
                                    const std::int32_t* pos, std::int64_t n,
                                    std::uint8_t value) {
@@ -422,6 +475,10 @@ void select2d(std::uint8_t* dst, std::int64_t ldd, std::int64_t rows,
     const std::int64_t nvec = (cols + 15) / 16;
     const unsigned gx = unsigned((nvec + 127) / 128);
     select_rows_v16_kernel<<<dim3(gx, gy), 128, 0, s>>>(dst, ldd, rows, cols, A, lda, B, ldb, rmap);
+  } else if (cmap && al(dst, ldd)) {
+    const std::int64_t nvec = (cols + 15) / 16;
+    const unsigned gx = unsigned((nvec + 127) / 128);
+    select2d_v16_kernel<<<dim3(gx, gy), 128, 0, s>>>(dst, ldd, rows, cols, A, lda, B, ldb, rmap, cmap);
   } else {
     const unsigned gx = unsigned((cols + 255) / 256);
     select2d_kernel<<<dim3(gx, gy), 256, 0, s>>>(dst, ldd, rows, cols, A, lda, B, ldb, rmap, cmap);
