@@ -469,12 +469,10 @@ int gfq_echelonize_host(uint32_t p, int64_t m, int64_t n, const uint8_t* C, int6
   return guard([&] {
     require_device();
     const gfq::FieldSpec f(p);
-    gfq::Mat dc(m, n);
-    if (!dc.empty())
-      GFQ_CUDA(cudaMemcpy2DAsync(dc.data(), size_t(dc.ld()), C, size_t(ld), size_t(n), size_t(m),
-                                 cudaMemcpyHostToDevice, gfq::cur_stream()));
+    if (m < 0 || n < 0 || (m > 0 && n > 0 && (!C || ld < n)))
+      throw std::invalid_argument("echelonize_host: bad matrix arguments");
     gfq::RunReport rep;
-    auto res = std::make_unique<gfq_output>(gfq::echelonize(dc, f, to_opts(opt), &rep));
+    auto res = std::make_unique<gfq_output>(gfq::echelonize_host(C, m, n, ld, f, to_opts(opt), &rep));
     res->report = std::move(rep);
     *out = res.release();
   });

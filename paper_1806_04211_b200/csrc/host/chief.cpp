@@ -217,7 +217,8 @@ PlanHandles build_plan(TaskGraph& graph,
 // Every value is the one the reference plan computes (the jobs are
 // column-separable); only the task granularity changes.
 PlanHandles build_plan_fused(TaskGraph& graph, const Mat& C, const FieldSpec& field,
-                             const ChopSpec& cs, bool with_transform) {
+                             const ChopSpec& cs, bool with_transform,
+                             const std::vector<std::shared_ptr<EventBox>>* row_ready) {
   const std::size_t a = cs.a(), b = cs.b();
   if (a == 0 || b == 0) throw std::invalid_argument("build_plan: empty partition");
   if (2 * a + 1 > std::size_t(TaskNode::kMaxIn))
@@ -232,8 +233,11 @@ PlanHandles build_plan_fused(TaskGraph& graph, const Mat& C, const FieldSpec& fi
     return C.row_view(std::int64_t(cs.row_offset(i)), std::int64_t(cs.row_parts[i]))
         .col_view(std::int64_t(cs.col_offset(k)), std::int64_t(cs.col_parts[k]));
   };
+  const auto ready = [&](std::size_t i) {
+    return row_ready ? (*row_ready)[i] : std::shared_ptr<EventBox>();
+  };
   for (std::size_t i = 0; i < a; ++i) {
-    graph.add_input({K::C, std::uint16_t(i), 0, 0, 0}, blk(i, 0));
+    graph.add_input({K::C, std::uint16_t(i), 0, 0, 0}, blk(i, 0), ready(i));
     if (b > 1) {
       MatParts panel;
       const std::int64_t o1 = std::int64_t(cs.col_offset(1));
@@ -243,7 +247,7 @@ PlanHandles build_plan_fused(TaskGraph& graph, const Mat& C, const FieldSpec& fi
         panel.off.push_back(std::int64_t(cs.col_offset(k)) - o1);
         panel.w.push_back(std::int64_t(cs.col_parts[k]));
       }
-      graph.add_input({K::CW, std::uint16_t(i), 1, 0, 0}, std::move(panel));
+      graph.add_input({K::CW, std::uint16_t(i), 1, 0, 0}, std::move(panel), ready(i));
     }
   }
 
@@ -402,8 +406,63 @@ PlanHandles build_plan_fused(TaskGraph& graph, const Mat& C, const FieldSpec& fi
 }
 
 // ---------------------------------------------------------------- echelonize
+namespace {
+EchelonOutput echelonize_impl(const Mat& C, const FieldSpec& field, const EchelonizeOptions& options,
+                              RunReport* report,
+                              const std::vector<std::shared_ptr<EventBox>>* row_ready);
+}  // namespace
+
 EchelonOutput echelonize(const Mat& C, const FieldSpec& field, const EchelonizeOptions& options,
                          RunReport* report) {
+  return echelonize_impl(C, field, options, report, nullptr);
+}
+
+EchelonOutput echelonize_host(const std::uint8_t* host, std::int64_t m, std::int64_t n,
+                              std::int64_t ld, const FieldSpec& field,
+                              const EchelonizeOptions& options, RunReport* report) {
+  Mat C(m, n);
+  const ChopSpec cs = chop(std::size_t(m), std::size_t(n), options.block, options.remainder_first);
+  const bool streamed = options.fuse && !C.empty() && cs.a() > 0 && cs.b() > 0 &&
+                        2 * cs.a() + 1 <= std::size_t(TaskNode::kMaxIn);
+  if (!streamed) {
+    if (!C.empty()) {
+      GFQ_CUDA(cudaMemcpy2DAsync(C.data(), std::size_t(C.ld()), host, std::size_t(ld), std::size_t(n),
+                                 std::size_t(m), cudaMemcpyHostToDevice, cur_stream()));
+    }
+    return echelonize_impl(C, field, options, report, nullptr);
+  }
+  // copy stream ordered after the allocation, one event per block row
+  cudaStream_t cs_stream;
+  GFQ_CUDA(cudaStreamCreateWithFlags(&cs_stream, cudaStreamNonBlocking));
+  std::vector<std::shared_ptr<EventBox>> row_ready;
+  try {
+    auto alloc_done = std::make_shared<EventBox>();
+    GFQ_CUDA(cudaEventRecord(alloc_done->ev, cur_stream()));
+    GFQ_CUDA(cudaStreamWaitEvent(cs_stream, alloc_done->ev, 0));
+    for (std::size_t i = 0; i < cs.a(); ++i) {
+      const std::int64_t r0 = std::int64_t(cs.row_offset(i)), nr = std::int64_t(cs.row_parts[i]);
+      GFQ_CUDA(cudaMemcpy2DAsync(C.data() + r0 * C.ld(), std::size_t(C.ld()), host + r0 * ld,
+                                 std::size_t(ld), std::size_t(n), std::size_t(nr),
+                                 cudaMemcpyHostToDevice, cs_stream));
+      auto ev = std::make_shared<EventBox>();
+      GFQ_CUDA(cudaEventRecord(ev->ev, cs_stream));
+      row_ready.push_back(std::move(ev));
+    }
+    EchelonOutput out = echelonize_impl(C, field, options, report, &row_ready);
+    GFQ_CUDA(cudaStreamSynchronize(cs_stream));  // the host buffer may be reused on return
+    cudaStreamDestroy(cs_stream);
+    return out;
+  } catch (...) {
+    cudaStreamSynchronize(cs_stream);
+    cudaStreamDestroy(cs_stream);
+    throw;
+  }
+}
+
+namespace {
+EchelonOutput echelonize_impl(const Mat& C, const FieldSpec& field, const EchelonizeOptions& options,
+                              RunReport* report,
+                              const std::vector<std::shared_ptr<EventBox>>* row_ready) {
   const ChopSpec cs = chop(std::size_t(C.rows()), std::size_t(C.cols()), options.block,
                            options.remainder_first);
   const std::size_t a = cs.a(), b = cs.b();
@@ -431,7 +490,7 @@ EchelonOutput echelonize(const Mat& C, const FieldSpec& field, const EchelonizeO
   TaskGraph graph;
   graph.ech_threshold = options.ech_threshold;
   const bool fused = options.fuse && 2 * a + 1 <= std::size_t(TaskNode::kMaxIn);
-  const PlanHandles h = fused ? build_plan_fused(graph, C, field, cs, options.with_transform)
+  const PlanHandles h = fused ? build_plan_fused(graph, C, field, cs, options.with_transform, row_ready)
                               : build_plan(graph, C, field, cs, options.with_transform);
   for (auto id : h.d_final) graph.retain(id);
   for (auto id : h.e_final) graph.retain(id);
@@ -477,6 +536,8 @@ EchelonOutput echelonize(const Mat& C, const FieldSpec& field, const EchelonizeO
   }
   return out;
 }
+
+}  // namespace
 
 // ---------------------------------------------------------------- assembly
 std::vector<std::uint32_t> EchelonOutput::global_upsilon() const {

@@ -74,9 +74,18 @@ struct EchelonizeOptions {
   bool fuse = true;  // wide UpdateRow / ClearUp jobs (single GPU); false = the reference's task grid
 };
 
-/// The fused single-GPU plan (same values, wide jobs per panel).
+/// The fused single-GPU plan (same values, wide jobs per panel).  With
+/// row_ready, block row i of C is valid once row_ready[i] fires.
 PlanHandles build_plan_fused(TaskGraph& graph, const Mat& C, const FieldSpec& field,
-                             const ChopSpec& chop, bool with_transform);
+                             const ChopSpec& chop, bool with_transform,
+                             const std::vector<std::shared_ptr<EventBox>>* row_ready = nullptr);
+
+/// echelonize from host memory: block rows are copied to HBM on a copy
+/// stream in the order Step 1 needs them, and each block row's tasks start
+/// as soon as its copy lands (the fused plan; otherwise one upload first).
+EchelonOutput echelonize_host(const std::uint8_t* host, std::int64_t m, std::int64_t n,
+                              std::int64_t ld, const FieldSpec& field,
+                              const EchelonizeOptions& options, RunReport* report = nullptr);
 
 /// reference include/gfrref/chief.hpp:88-90.  C is device-resident.
 EchelonOutput echelonize(const Mat& C, const FieldSpec& field, const EchelonizeOptions& options,
