@@ -1,4 +1,5 @@
 // capi.cpp -- extern "C" boundary (include/gfq.h) over the C++ host layer.
+#include <atomic>
 #include <cstring>
 #include <memory>
 #include <string>
@@ -31,10 +32,19 @@ struct gfq_comm {
 
 namespace {
 thread_local std::string g_err;
+// the device gfq_init chose; every host thread entering the ABI adopts it
+// once (the CUDA runtime's current device is per thread)
+std::atomic<int> g_device{-1};
+thread_local int t_device = -1;
 
 template <class F>
 int guard(F&& f) {
   try {
+    const int d = g_device.load(std::memory_order_relaxed);
+    if (d >= 0 && t_device != d) {
+      GFQ_CUDA(cudaSetDevice(d));
+      t_device = d;
+    }
     f();
     return GFQ_OK;
   } catch (const std::invalid_argument& e) {
@@ -125,6 +135,8 @@ int gfq_init(int device) {
   return guard([&] {
     require_device();
     GFQ_CUDA(cudaSetDevice(device));
+    g_device = device;
+    t_device = device;
     cudaDeviceProp prop;
     GFQ_CUDA(cudaGetDeviceProperties(&prop, device));
     if (prop.major != 10)

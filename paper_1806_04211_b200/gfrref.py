@@ -17,6 +17,7 @@ is no CPU fallback.
 from __future__ import annotations
 
 import ctypes
+import os
 from dataclasses import dataclass, field
 from typing import Optional, Sequence
 
@@ -43,12 +44,21 @@ class LogicError(GfqError):
     code = 4
 
 
+def default_device() -> int:
+    """GFQ_DEVICE, else the launcher's LOCAL_RANK (one process per GPU), else 0."""
+    for var in ("GFQ_DEVICE", "LOCAL_RANK"):
+        if os.environ.get(var, "").strip().isdigit():
+            return int(os.environ[var])
+    return 0
+
+
 def lib():
-    """The loaded libgfq.so (initialised on device 0)."""
+    """The loaded libgfq.so, initialised on default_device() (the library's
+    CUDA runtime is its own: its current device is set here, not by torch)."""
     global _lib
     if _lib is None:
         l = _capi.load()
-        rc = l.gfq_init(0)
+        rc = l.gfq_init(default_device())
         if rc != 0:
             raise CudaError(l.gfq_last_error().decode())
         _lib = l
