@@ -222,6 +222,15 @@ int gfq_output_trace_device(const gfq_output* o, uint64_t* n, int64_t* dev_start
                             int64_t* dev_end_ns);
 void gfq_output_free(gfq_output* o);
 
+/* ------------------------------------------------------------ text I/O */
+/* The reference's GFMAT v1 / SELECTS v1 / TRANSFORM v1 files, byte-identical
+ * (include/gfrref/io.hpp:17-45; src/io.cpp:199-286), prime fields only.
+ * Malformed input -> GFQ_ERR_INVALID with "file:line: message". */
+int gfq_read_gfmat_file(const char* path, uint32_t* p, gfq_mat** out);
+int gfq_write_gfmat_file(const char* path, uint32_t p, const gfq_mat* m);
+int gfq_output_write_selects_file(const gfq_output* o, const char* path);
+int gfq_output_write_transform_file(const gfq_output* o, const char* path);
+
 /* gfrref::verify (src/chief.cpp:531-590) on the device, without the oracle
  * argument.  C is the device-resident input the output was computed from
  * (a sharded output must have been gathered).  method: 0 = auto (exact when

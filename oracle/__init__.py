@@ -137,6 +137,28 @@ def mad(p: int, a: np.ndarray, b: np.ndarray, c: np.ndarray | None = None) -> np
     return out
 
 
+REF_ECH = os.path.join(HERE, "_ref", "ref_ech")
+
+
+def ref_cli(*args):
+    """Run the reference-library driver oracle/_ref/ref_ech (reference
+    read_gfmat / echelonize / write_* in its own process; see
+    ref_ech_main.cpp).  Returns (exit code, stdout)."""
+    r = subprocess.run([REF_ECH, *map(str, args)], capture_output=True, text=True)
+    return r.returncode, r.stdout
+
+
+def ref_write_gfmat(p: int, C: np.ndarray, path: str):
+    """The reference's write_gfmat_file (src/io.cpp:228) on a host matrix."""
+    C = np.ascontiguousarray(C, np.uint8)
+    raw = path + ".raw"
+    C.tofile(raw)
+    rc, _ = ref_cli("gfmat", p, C.shape[0], C.shape[1], raw, path)
+    os.remove(raw)
+    if rc:
+        raise RuntimeError("ref_ech gfmat failed")
+
+
 def oracle_rref(p: int, C: np.ndarray):
     """C restatement of reference ``oracle_rref`` (src/chief.cpp:427-487).
 
@@ -162,6 +184,7 @@ def oracle_rref(p: int, C: np.ndarray):
 # ---------------------------------------------------------------- reference shim
 class RefOutput:
     """Handle on a ``gfrref::EchelonOutput`` produced by the reference library."""
+
 
     def __init__(self, handle, m, n, wall_s, run_s):
         self.h = handle

@@ -115,6 +115,10 @@ PROTOS = {
     "gfq_output_trace_device": (I, [vp, c_u64p, c_i64p, c_i64p]),
     "gfq_output_free": (None, [vp]),
     "gfq_tc_debug_take": (I, [c_u64p]),
+    "gfq_read_gfmat_file": (I, [ctypes.c_char_p, _P(U32), vpp]),
+    "gfq_write_gfmat_file": (I, [ctypes.c_char_p, U32, vp]),
+    "gfq_output_write_selects_file": (I, [vp, ctypes.c_char_p]),
+    "gfq_output_write_transform_file": (I, [vp, ctypes.c_char_p]),
     "gfq_verify": (I, [vp, vp, I, U64, c_i32p, ctypes.c_char_p, ctypes.c_size_t, ctypes.c_char_p,
                        ctypes.c_size_t]),
     "gfq_nccl_unique_id": (I, [c_u8p]),

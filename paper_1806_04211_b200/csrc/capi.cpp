@@ -7,6 +7,7 @@
 #include "../../include/gfq.h"
 #include "host/chief.hpp"
 #include "host/dist.hpp"
+#include "host/io.hpp"
 #include "host/jobs.hpp"
 #include "host/tasks.hpp"
 #include "host/verify.hpp"
@@ -599,6 +600,33 @@ int gfq_output_trace_device(const gfq_output* o, uint64_t* n, int64_t* dev_start
   });
 }
 void gfq_output_free(gfq_output* o) { delete o; }
+
+int gfq_read_gfmat_file(const char* path, uint32_t* p, gfq_mat** out) {
+  return guard([&] {
+    if (!path || !p || !out) throw std::invalid_argument("gfq_read_gfmat_file: null argument");
+    const gfq::GfMatHost h = gfq::read_gfmat_file(path);
+    *p = h.p;
+    *out = wrap(gfq::Mat::from_host(h.rows, h.cols, h.data.data(), h.cols > 0 ? h.cols : 1));
+  });
+}
+int gfq_write_gfmat_file(const char* path, uint32_t p, const gfq_mat* m) {
+  return guard([&] {
+    if (!path) throw std::invalid_argument("gfq_write_gfmat_file: null path");
+    gfq::write_gfmat_file(path, p, M(m));
+  });
+}
+int gfq_output_write_selects_file(const gfq_output* o, const char* path) {
+  return guard([&] {
+    if (!o || !path) throw std::invalid_argument("gfq_output_write_selects_file: null argument");
+    gfq::write_selects_file(path, O(o).out);
+  });
+}
+int gfq_output_write_transform_file(const gfq_output* o, const char* path) {
+  return guard([&] {
+    if (!o || !path) throw std::invalid_argument("gfq_output_write_transform_file: null argument");
+    gfq::write_transform_file(path, O(o).out);
+  });
+}
 
 int gfq_verify(const gfq_output* o, const gfq_mat* C, int method, uint64_t seed, int* ok,
                char* diag, size_t diag_len, char* checked, size_t checked_len) {

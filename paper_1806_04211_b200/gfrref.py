@@ -700,6 +700,14 @@ class EchelonOutput:
         _check(lib().gfq_output_download_blocks(self.h, buf.ctypes.data_as(_capi.c_u8p), buf.nbytes))
         return n
 
+    def write_selects_file(self, path: str):
+        """reference write_selects_file (src/io.cpp:261), byte-identical."""
+        _check(lib().gfq_output_write_selects_file(self.h, os.fsencode(path)))
+
+    def write_transform_file(self, path: str):
+        """reference write_transform_file (src/io.cpp:288), byte-identical."""
+        _check(lib().gfq_output_write_transform_file(self.h, os.fsencode(path)))
+
     def report(self) -> dict:
         r = _capi.Report()
         _check(lib().gfq_output_report(self.h, ctypes.byref(r)))
@@ -788,6 +796,20 @@ def echelonize_dist(comm: Comm, f: FieldSpec, m: int, n: int, options: Echeloniz
     _check(lib().gfq_echelonize_dist(comm.h, f.p, C.h if C is not None else None, m, n, seed,
                                      ctypes.byref(o), int(gather), ctypes.byref(h)))
     return EchelonOutput(h, f, chop(m, n, options.block, options.remainder_first), options.with_transform)
+
+
+def read_gfmat_file(path: str):
+    """reference read_gfmat_file (src/io.cpp:215): (FieldSpec, device Matrix)."""
+    p = ctypes.c_uint32()
+    h = _vp()
+    _check(lib().gfq_read_gfmat_file(os.fsencode(path), ctypes.byref(p), ctypes.byref(h)))
+    return FieldSpec(p.value), _mat(h)
+
+
+def write_gfmat_file(path: str, f: FieldSpec, m) -> None:
+    """reference write_gfmat_file (src/io.cpp:228), byte-identical."""
+    m = _as_matrix(m)
+    _check(lib().gfq_write_gfmat_file(os.fsencode(path), f.p, m.h))
 
 
 VERIFY_METHODS = {"auto": 0, "exact": 1, "freivalds": 2}
