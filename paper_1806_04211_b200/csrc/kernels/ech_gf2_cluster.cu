@@ -166,25 +166,51 @@ __global__ void __launch_bounds__(kThreads, 1) ech_gf2_cluster_kernel(ClArgs g) 
     }
     std::uint64_t piv = std::uint64_t(__ballot_sync(0xffffffffu, p0)) |
                         (std::uint64_t(__ballot_sync(0xffffffffu, p1)) << 32);
+    // Four columns per round: their current masks are broadcast together,
+    // every lane derives the four pivots from them in registers (each
+    // pivot's elimination applied to the later columns of the round), then
+    // applies the four eliminations to its own column and coefficient mask.
     int r2 = 0, ok = 1;
-    for (int c = 0; c < wc; ++c) {
-      const std::uint64_t col = __shfl_sync(0xffffffffu, cmask, c);
-      const std::uint64_t cand = col & ~piv;
-      if (!cand) {  // uniform
-        ok = 0;
-        break;
+    for (int c0 = 0; c0 < wc && ok; c0 += 4) {
+      const int nt = wc - c0 < 4 ? wc - c0 : 4;
+      std::uint64_t bc[4], ss[4];
+      int pv[4];
+#pragma unroll
+      for (int t = 0; t < 4; ++t) bc[t] = __shfl_sync(0xffffffffu, cmask, (c0 + t) & 31);
+      int np = 0;
+#pragma unroll
+      for (int t = 0; t < 4; ++t) {
+        pv[t] = -1;
+        ss[t] = 0;
+        if (t < nt && ok) {
+          const std::uint64_t cand = bc[t] & ~piv;
+          if (!cand) {
+            ok = 0;  // a column without a window candidate: uniform
+          } else {
+            const int p = __ffsll(static_cast<long long>(cand)) - 1;
+            pv[t] = p;
+            ss[t] = bc[t] & ~(std::uint64_t(1) << p);
+            piv |= std::uint64_t(1) << p;
+#pragma unroll
+            for (int u = t + 1; u < 4; ++u)
+              if ((bc[u] >> p) & 1u) bc[u] ^= ss[t];
+            ++np;
+          }
+        }
       }
-      const int pw = __ffsll(static_cast<long long>(cand)) - 1;
-      const std::uint64_t sset = col & ~(std::uint64_t(1) << pw);
-      if ((cmask >> pw) & 1u) cmask ^= sset;
-      if (lane < r2 && ((kmask >> pw) & 1u)) kmask ^= sset;
-      if (lane == r2) kmask = sset;
-      piv |= std::uint64_t(1) << pw;
-      if (lane == 0) {
-        pc[r2] = c;
-        pr[r2] = lo + pw;
+#pragma unroll
+      for (int t = 0; t < 4; ++t) {
+        if (pv[t] < 0) continue;
+        const int p = pv[t], q = r2 + t;
+        if ((cmask >> p) & 1u) cmask ^= ss[t];
+        if (lane < q && ((kmask >> p) & 1u)) kmask ^= ss[t];
+        if (lane == q) kmask = ss[t];
+        if (lane == 0) {
+          pc[q] = c0 + t;
+          pr[q] = lo + p;
+        }
       }
-      ++r2;
+      r2 += np;
     }
     __syncwarp();
     if (ok)
@@ -390,6 +416,7 @@ __global__ void __launch_bounds__(kThreads, 1) ech_gf2_cluster_kernel(ClArgs g) 
     const bool chain_warp = has_next && cr == 0 && warp == 0;
     if (chain_warp) {
       cl_wait();
+      stamp(k, 8);
       window_chain(k + 1);
       stamp(k, 4);
     }
@@ -492,6 +519,8 @@ bool ech_gf2_cluster(std::int64_t rows, std::int64_t cols, const std::uint8_t* H
       for (int ph = 1; ph < 7; ++ph)
         std::fprintf(stderr, " %lld", static_cast<long long>(dbg[k * 16 + ph] - dbg[k * 16 + ph - 1]));
 
+      std::fprintf(stderr, " | zwait %lld chain %lld", static_cast<long long>(dbg[k * 16 + 8] - dbg[k * 16 + 3]),
+                   static_cast<long long>(dbg[k * 16 + 4] - dbg[k * 16 + 8]));
       std::fprintf(stderr, " | total %lld ns\n",
                    static_cast<long long>(dbg[(k + 1) * 16] - dbg[k * 16]));
     }
