@@ -321,11 +321,36 @@ EchResult panel_ech(const FieldSpec& f, const Mat& h) {
   const std::int64_t cap = std::min(a, b);
   const cudaStream_t s = cur_stream();
   if (f.p() == 2 && a <= 1024 && (a + b + 31) / 32 <= 256) {
-    // GF(2): the whole ECH in one bit-packed single-CTA launch
-    Mat aug(a, b + a);
     DevBuf info{static_cast<std::size_t>(4 * (1 + 2 * cap))};
     auto* inf = reinterpret_cast<std::int32_t*>(info.ptr);
-    if (!dev::ech_gf2_cluster(a, b, h.data(), h.ld(), aug.data(), aug.ld(), inf, cap, s)) {
+    {
+      // GF(2), one 8-CTA cluster: the kernel writes M / K / R itself (no
+      // unpacked [W | T] and no gathers on the host's critical path)
+      Mat mb(cap, cap), kb(a, cap), rb(cap, b);
+      const std::int64_t wd = (a + b + 31) / 32;
+      DevBuf scratch{static_cast<std::size_t>(4 * a * wd + 2 * (2 * a + b) + 64)};
+      auto* pk = reinterpret_cast<std::uint32_t*>(scratch.ptr);
+      auto* maps = reinterpret_cast<std::int16_t*>(pk + a * wd);
+      const dev::EchExtract ex{mb.data(), kb.data(), rb.data(), mb.ld(), kb.ld(), rb.ld(),
+                               pk, maps, maps + a, maps + 2 * a};
+      if (dev::ech_gf2_small(a, b, h.data(), h.ld(), inf, cap, s, ex) ||
+          dev::ech_gf2_cluster(a, b, h.data(), h.ld(), nullptr, 0, inf, cap, s, &ex)) {
+        std::vector<std::int32_t> hi(std::size_t(1 + 2 * cap));
+        download_i32(inf, hi.data(), hi.size());
+        const std::int64_t r = hi[0];
+        EchResult out;
+        std::vector<std::uint32_t> rho(hi.begin() + 1 + cap, hi.begin() + 1 + cap + r);
+        std::sort(rho.begin(), rho.end());
+        out.rho = IndexSet(std::size_t(a), std::move(rho));
+        out.gamma = IndexSet(std::size_t(b), std::vector<std::uint32_t>(hi.begin() + 1, hi.begin() + 1 + r));
+        out.M = mb.row_view(0, r).col_view(0, r);
+        out.K = kb.row_view(0, a - r).col_view(0, r);
+        out.R = rb.row_view(0, r).col_view(0, b - r);
+        return out;
+      }
+    }
+    Mat aug(a, b + a);
+    {
       DevBuf scratch{static_cast<std::size_t>(4 * dev::ech_gf2_scratch_words(a, b))};
       dev::ech_gf2_block(a, b, h.data(), h.ld(), reinterpret_cast<std::uint32_t*>(scratch.ptr),
                          aug.data(), aug.ld(), inf, cap, s);

@@ -57,7 +57,16 @@ struct ClArgs {
   std::int64_t ldo;
   std::int32_t* info;
   unsigned long long* dbg;  // developer phase stamps (GFQ_GF2_DEBUG)
+  // extraction mode (Out == nullptr): the reduced rows stay bit-packed
+  // (P, Wd words a row) and the leader writes the index maps the extraction
+  // kernel needs: sorted pivot rows (RS), row -> pivot index q or -(u+1)
+  // for the u-th non-pivot row (QK), non-pivot columns (GC)
+  std::uint32_t* P;
+  std::int16_t *RS, *QK, *GC;
 };
+
+// leader scratch of the extraction epilogue (pivot-column flags, bytes)
+constexpr int kExBytes = 8192;
 
 __device__ __forceinline__ unsigned long long gtime() {
   unsigned long long t;
@@ -83,8 +92,10 @@ __global__ void __launch_bounds__(kThreads, 1) ech_gf2_cluster_kernel(ClArgs g) 
   std::uint32_t* gall = reinterpret_cast<std::uint32_t*>(fl + 1024);  // 1024 (leader fallback)
   std::uint32_t* tab = gall + 1024;             // 128 x Wd nibble tables (when Wd <= kTabWd)
   const bool use_tab = Wd <= kTabWd;
+  std::uint8_t* ex = reinterpret_cast<std::uint8_t*>(tab + (use_tab ? 128 * Wd : 0));
+  std::uint8_t* ex_cf = ex;  // pivot-column flags (leader, extraction mode)
   // the current panel's pivots (the leader's copy is authoritative)
-  __shared__ int pc[32], pr[32], r2_sh, ok_sh, lo_sh;
+  __shared__ int pc[32], pr[32], r2_sh, ok_sh, lo_sh, npiv_sh;
   __shared__ std::uint32_t pcoef[32], ntab[128];
   __shared__ std::uint32_t nomw[2][32], nomc[2][32];
   __shared__ unsigned best[3];
@@ -135,7 +146,10 @@ __global__ void __launch_bounds__(kThreads, 1) ech_gf2_cluster_kernel(ClArgs g) 
       fl[i] = i < rows ? 0 : 1;
       orig[i] = 0u;
     }
-    if (tid == 0) lo_sh = 0;
+    if (tid == 0) {
+      lo_sh = 0;
+      npiv_sh = 0;
+    }
   }
   cluster.sync();
 
@@ -166,6 +180,9 @@ __global__ void __launch_bounds__(kThreads, 1) ech_gf2_cluster_kernel(ClArgs g) 
     }
     std::uint64_t piv = std::uint64_t(__ballot_sync(0xffffffffu, p0)) |
                         (std::uint64_t(__ballot_sync(0xffffffffu, p1)) << 32);
+    // the window holds every non-pivotal row: a column without a candidate
+    // is then a free column, not a reason to fall back
+    const bool covers_all = 64 - __popcll(piv) == rows - npiv_sh;
     // Four columns per round: their current masks are broadcast together,
     // every lane derives the four pivots from them in registers (each
     // pivot's elimination applied to the later columns of the round), then
@@ -185,7 +202,7 @@ __global__ void __launch_bounds__(kThreads, 1) ech_gf2_cluster_kernel(ClArgs g) 
         if (t < nt && ok) {
           const std::uint64_t cand = bc[t] & ~piv;
           if (!cand) {
-            ok = 0;  // a column without a window candidate: uniform
+            if (!covers_all) ok = 0;  // a column without a window candidate: uniform
           } else {
             const int p = __ffsll(static_cast<long long>(cand)) - 1;
             pv[t] = p;
@@ -198,10 +215,11 @@ __global__ void __launch_bounds__(kThreads, 1) ech_gf2_cluster_kernel(ClArgs g) 
           }
         }
       }
+      int qn = r2;
 #pragma unroll
       for (int t = 0; t < 4; ++t) {
         if (pv[t] < 0) continue;
-        const int p = pv[t], q = r2 + t;
+        const int p = pv[t], q = qn++;
         if ((cmask >> p) & 1u) cmask ^= ss[t];
         if (lane < q && ((kmask >> p) & 1u)) kmask ^= ss[t];
         if (lane == q) kmask = ss[t];
@@ -301,6 +319,8 @@ __global__ void __launch_bounds__(kThreads, 1) ech_gf2_cluster_kernel(ClArgs g) 
   // leader, every thread: record panel k's pivots and send them to CTAs 1..7
   auto publish = [&](int k, int rtot) {
     const int r2 = r2_sh;
+    __syncthreads();
+    if (tid == 0) npiv_sh = rtot + r2;
     if (tid < r2) {
       g.info[1 + rtot + tid] = 32 * k + pc[tid];
       g.info[1 + g.cap + rtot + tid] = pr[tid];
@@ -445,56 +465,154 @@ __global__ void __launch_bounds__(kThreads, 1) ech_gf2_cluster_kernel(ClArgs g) 
     rtot += r2;
   }
 
-  // ---- unpack my stripe of the reduced [W | T] to u8 (warp per row)
-  const int tot = cols + rows;
-  for (int li = warp; li < nloc; li += kThreads / 32) {
-    const std::uint32_t* arow = A + li * Wd;
-    std::uint8_t* orow = g.Out + std::int64_t(row0 + li) * g.ldo;
-    for (int w = lane; w < Wd; w += 32) {
-      const std::uint32_t word = arow[w];
-      const int j0 = 32 * w;
-      if (j0 + 32 <= tot && (reinterpret_cast<std::uintptr_t>(orow + j0) & 15) == 0) {
-        std::uint32_t outw[8];
+  if (g.dbg && cr == 0 && tid == 0) g.dbg[8 * 16 + 0] = gtime();
+  if (g.Out) {
+    // ---- unpack my stripe of the reduced [W | T] to u8 (warp per row)
+    const int tot = cols + rows;
+    for (int li = warp; li < nloc; li += kThreads / 32) {
+      const std::uint32_t* arow = A + li * Wd;
+      std::uint8_t* orow = g.Out + std::int64_t(row0 + li) * g.ldo;
+      for (int w = lane; w < Wd; w += 32) {
+        const std::uint32_t word = arow[w];
+        const int j0 = 32 * w;
+        if (j0 + 32 <= tot && (reinterpret_cast<std::uintptr_t>(orow + j0) & 15) == 0) {
+          std::uint32_t outw[8];
 #pragma unroll
-        for (int q = 0; q < 8; ++q) {
-          const std::uint32_t nib = (word >> (4 * q)) & 0xFu;
-          outw[q] = (nib & 1u) | ((nib & 2u) << 7) | ((nib & 4u) << 14) | ((nib & 8u) << 21);
+          for (int q = 0; q < 8; ++q) {
+            const std::uint32_t nib = (word >> (4 * q)) & 0xFu;
+            outw[q] = (nib & 1u) | ((nib & 2u) << 7) | ((nib & 4u) << 14) | ((nib & 8u) << 21);
+          }
+          reinterpret_cast<uint4*>(orow + j0)[0] = make_uint4(outw[0], outw[1], outw[2], outw[3]);
+          reinterpret_cast<uint4*>(orow + j0)[1] = make_uint4(outw[4], outw[5], outw[6], outw[7]);
+        } else {
+          for (int b = 0; b < 32 && j0 + b < tot; ++b) orow[j0 + b] = (word >> b) & 1u;
         }
-        reinterpret_cast<uint4*>(orow + j0)[0] = make_uint4(outw[0], outw[1], outw[2], outw[3]);
-        reinterpret_cast<uint4*>(orow + j0)[1] = make_uint4(outw[4], outw[5], outw[6], outw[7]);
-      } else {
-        for (int b = 0; b < 32 && j0 + b < tot; ++b) orow[j0 + b] = (word >> b) & 1u;
+      }
+    }
+  } else {
+    // ---- extraction, part 1 (reference src/jobs.cpp:104-121 conventions):
+    // packed rows to global, and the leader's index maps
+    for (int e = tid; e < nloc * Wd; e += kThreads)
+      g.P[std::int64_t(row0 + e / Wd) * Wd + e % Wd] = A[e];
+    const int r = rtot;
+    if (cr == 0) {
+      for (int c = tid; c < cols; c += kThreads) ex_cf[c] = 0;
+      __syncthreads();
+      for (int q = tid; q < r; q += kThreads) {
+        ex_cf[g.info[1 + q]] = 1;
+        g.QK[g.info[1 + g.cap + q]] = std::int16_t(q);
+      }
+      // rows: one per thread, block prefix of the pivot flags
+      const int i = tid;
+      const bool pv = i < rows && fl[i] != 0;
+      const unsigned bal = __ballot_sync(0xffffffffu, pv);
+      if (lane == 0) nomw[0][warp] = __popc(bal);
+      __syncthreads();
+      if (warp == 0) {
+        std::uint32_t v = nomw[0][lane], x = v;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const std::uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+          if (lane >= o) x += y;
+        }
+        nomc[0][lane] = x - v;  // exclusive prefix per warp
+      }
+      __syncthreads();
+      const int before = int(nomc[0][warp]) + __popc(bal & ((1u << lane) - 1u));
+      if (i < rows) {
+        if (pv) g.RS[before] = std::int16_t(i);
+        else g.QK[i] = std::int16_t(-(i - before) - 1);
+      }
+      // non-pivot columns: 8 per thread, block prefix of the counts
+      int cnt = 0;
+      for (int t = 0; t < 8; ++t) {
+        const int c = 8 * tid + t;
+        cnt += (c < cols && !ex_cf[c]) ? 1 : 0;
+      }
+      std::uint32_t x = std::uint32_t(cnt);
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const std::uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= o) x += y;
+      }
+      if (lane == 31) nomw[1][warp] = x;
+      __syncthreads();
+      if (warp == 0) {
+        std::uint32_t v = nomw[1][lane], y2 = v;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const std::uint32_t z = __shfl_up_sync(0xffffffffu, y2, o);
+          if (lane >= o) y2 += z;
+        }
+        nomc[1][lane] = y2 - v;
+      }
+      __syncthreads();
+      int pos = int(nomc[1][warp] + x) - cnt;
+      for (int t = 0; t < 8; ++t) {
+        const int c = 8 * tid + t;
+        if (c < cols && !ex_cf[c]) g.GC[pos++] = std::int16_t(c);
       }
     }
   }
+  if (g.dbg && cr == 0 && tid == 0) g.dbg[8 * 16 + 1] = gtime();
   if (cr == 0 && tid == 0) g.info[0] = rtot;
   cluster.sync();  // no CTA may exit while others still address its shared memory
+}
+
+// Extraction, part 2: one block per row of the reduced packed [W | T].
+// Row i with pivot index q writes M row q (T bits at the sorted pivot rows)
+// and R row q (W bits at the non-pivot columns); the u-th non-pivot row
+// writes K row u.
+__global__ void __launch_bounds__(128) gf2_extract_kernel(int rows, int cols, int Wd,
+                                                          const std::uint32_t* P,
+                                                          const std::int32_t* info, int cap,
+                                                          const std::int16_t* RS,
+                                                          const std::int16_t* QK,
+                                                          const std::int16_t* GC, EchExtract ex) {
+  (void)cap;
+  const int i = blockIdx.x;
+  const int r = info[0];
+  const std::uint32_t* prow = P + std::int64_t(i) * Wd;
+  auto bit = [&](int pos) { return std::uint8_t((prow[pos >> 5] >> (pos & 31)) & 1u); };
+  const int qk = QK[i];
+  if (qk >= 0) {
+    std::uint8_t* m = ex.M + std::int64_t(qk) * ex.ldm;
+    for (int t = threadIdx.x; t < r; t += blockDim.x) m[t] = bit(cols + RS[t]);
+    std::uint8_t* rr = ex.R + std::int64_t(qk) * ex.ldr;
+    for (int t = threadIdx.x; t < cols - r; t += blockDim.x) rr[t] = bit(GC[t]);
+  } else {
+    std::uint8_t* k = ex.K + std::int64_t(-qk - 1) * ex.ldk;
+    for (int t = threadIdx.x; t < r; t += blockDim.x) k[t] = bit(cols + RS[t]);
+  }
 }
 
 }  // namespace
 
 bool ech_gf2_cluster(std::int64_t rows, std::int64_t cols, const std::uint8_t* H, std::int64_t ldh,
                      std::uint8_t* Out, std::int64_t ldo, std::int32_t* info, std::int64_t cap,
-                     cudaStream_t s) {
+                     cudaStream_t s, const EchExtract* ex) {
   static const bool off = std::getenv("GFQ_NO_GF2_CLUSTER") != nullptr;
   const std::int64_t Wd = (cols + rows + 31) / 32;
   if (off || rows > kCl * kStripe || Wd > kMaxWd || rows <= 0 || cols <= 0) return false;
   const std::size_t smem =
       std::size_t(kStripe * Wd + 32 * Wd + 1024 + kStripe) * 4 + 1024 + 4096 +
-      (Wd <= kTabWd ? std::size_t(128 * Wd) * 4 : 0);
+      (Wd <= kTabWd ? std::size_t(128 * Wd) * 4 : 0) + kExBytes;
   static bool attr = false;
   if (!attr) {
     GFQ_CUDA(cudaFuncSetAttribute(ech_gf2_cluster_kernel,
                                   cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   int(std::max(std::size_t(kStripe * kMaxWd + 32 * kMaxWd + 1024 + kStripe) * 4 + 1024 + 4096,
                                                std::size_t(kStripe * kTabWd + 32 * kTabWd + 1024 + kStripe) * 4 +
-                                                   1024 + 4096 + std::size_t(128 * kTabWd) * 4))));
+                                                   1024 + 4096 + std::size_t(128 * kTabWd) * 4) +
+                                      kExBytes)));
     attr = true;
   }
   static const bool debug = std::getenv("GFQ_GF2_DEBUG") != nullptr;
   static unsigned long long* dbg = nullptr;
-  if (debug && !dbg) GFQ_CUDA(cudaMalloc(&dbg, 8 * 16 * sizeof(unsigned long long)));
-  ClArgs g{int(rows), int(cols), int(Wd), int(cap), H, ldh, Out, ldo, info, debug ? dbg : nullptr};
+  if (debug && !dbg) GFQ_CUDA(cudaMalloc(&dbg, 9 * 16 * sizeof(unsigned long long)));
+  ClArgs g{int(rows), int(cols), int(Wd), int(cap), H, ldh, Out, ldo, info, debug ? dbg : nullptr,
+            ex ? ex->P : nullptr, ex ? ex->RS : nullptr, ex ? ex->QK : nullptr,
+            ex ? ex->GC : nullptr};
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(kCl);
   cfg.blockDim = dim3(kThreads);
@@ -509,12 +627,21 @@ bool ech_gf2_cluster(std::int64_t rows, std::int64_t cols, const std::uint8_t* H
   cfg.numAttrs = 1;
   GFQ_CUDA(cudaLaunchKernelEx(&cfg, ech_gf2_cluster_kernel, g));
   count_launch();
+  if (ex) {
+    gf2_extract_kernel<<<unsigned(rows), 128, 0, s>>>(int(rows), int(cols), int(Wd), ex->P, info,
+                                                       int(cap), ex->RS, ex->QK, ex->GC, *ex);
+    GFQ_CUDA(cudaGetLastError());
+    count_launch();
+  }
   if (debug) {
     GFQ_CUDA(cudaStreamSynchronize(s));
-    unsigned long long hd[8 * 16];
+    unsigned long long hd[9 * 16];
     GFQ_CUDA(cudaMemcpy(hd, dbg, sizeof hd, cudaMemcpyDeviceToHost));
     const unsigned long long* dbg = hd;
-    for (int k = 0; k < 4; ++k) {
+    std::fprintf(stderr, "gf2cl rows %lld cols %lld Wd %lld epilogue %lld ns\n", static_cast<long long>(rows),
+                 static_cast<long long>(cols), static_cast<long long>(Wd),
+                 static_cast<long long>(hd[8 * 16 + 1] - hd[8 * 16]));
+    for (int k = 0; k < 4 && k < (cols + 31) / 32; ++k) {
       std::fprintf(stderr, "gf2cl panel %d:", k);
       for (int ph = 1; ph < 7; ++ph)
         std::fprintf(stderr, " %lld", static_cast<long long>(dbg[k * 16 + ph] - dbg[k * 16 + ph - 1]));
@@ -525,6 +652,113 @@ bool ech_gf2_cluster(std::int64_t rows, std::int64_t cols, const std::uint8_t* H
                    static_cast<long long>(dbg[(k + 1) * 16] - dbg[k * 16]));
     }
   }
+  return true;
+}
+
+}  // namespace gfq::dev
+
+// ---------------------------------------------------------------- few rows
+// GF(2) ECH of a block with at most 32 rows (the ClearDowns of a block row
+// that has all but a few of its pivots already): one warp, one row per lane,
+// the bit-packed [W | T] rows in shared memory; column by column, the first
+// non-pivotal row with the bit is the pivot and every other row with the bit
+// adds it (Gauss-Jordan); the loop stops once every row is pivotal.  Writes
+// info and the EchResult blocks like the extraction mode above.
+namespace gfq::dev {
+namespace {
+
+__global__ void __launch_bounds__(32) ech_gf2_small_kernel(int rows, int cols, const std::uint8_t* H,
+                                                           std::int64_t ldh, std::int32_t* info,
+                                                           int cap, EchExtract ex) {
+  extern __shared__ std::uint32_t sw[];
+  const int lane = threadIdx.x;
+  const int Wd = (cols + rows + 31) / 32, st = Wd + 1;  // padded row stride: no bank conflicts
+  std::uint32_t* row = sw + lane * st;
+  std::uint8_t* colpiv = reinterpret_cast<std::uint8_t*>(sw + 32 * st);  // cols bytes
+  __shared__ int pc[32], pr[32];
+  if (lane < rows) {
+    const std::uint8_t* h = H + std::int64_t(lane) * ldh;
+    for (int w = 0; w < Wd; ++w) {
+      std::uint32_t word = 0;
+      for (int b = 0; b < 32; ++b) {
+        const int j = 32 * w + b;
+        if (j < cols) word |= std::uint32_t(h[j] & 1u) << b;
+      }
+      if (32 * w <= cols + lane && cols + lane < 32 * w + 32) word |= 1u << (cols + lane - 32 * w);
+      row[w] = word;
+    }
+  }
+  for (int c = lane; c < cols; c += 32) colpiv[c] = 0;
+  __syncwarp();
+  bool piv = lane >= rows;
+  int r = 0;
+  for (int c = 0; c < cols; ++c) {
+    const unsigned open = __ballot_sync(0xffffffffu, !piv);
+    if (!open) break;
+    const bool has = lane < rows && ((row[c >> 5] >> (c & 31)) & 1u);
+    const unsigned cand = __ballot_sync(0xffffffffu, has && !piv);
+    if (!cand) continue;
+    const int p = __ffs(cand) - 1;
+    const std::uint32_t* prow = sw + p * st;
+    if (has && lane != p)
+      for (int w = c >> 5; w < Wd; ++w) row[w] ^= prow[w];
+    __syncwarp();
+    if (lane == p) piv = true;
+    if (lane == 0) {
+      pc[r] = c;
+      pr[r] = p;
+      colpiv[c] = 1;
+    }
+    ++r;
+  }
+  __syncwarp();
+  if (lane < r) {
+    info[1 + lane] = pc[lane];
+    info[1 + cap + lane] = pr[lane];
+  }
+  if (lane == 0) info[0] = r;
+  // sorted pivot rows (= pivotal lanes in order) and each row's output index
+  const unsigned pivmask = __ballot_sync(0xffffffffu, lane < rows && piv);
+  int q = -1;
+  for (int t = 0; t < r; ++t)
+    if (pr[t] == lane) q = t;
+  const int below = __popc(pivmask & ((1u << lane) - 1u));  // pivot rows before me
+  // M / K rows: the T columns at the sorted pivot rows
+  if (lane < rows) {
+    std::uint8_t* out = q >= 0 ? ex.M + std::int64_t(q) * ex.ldm : ex.K + std::int64_t(lane - below) * ex.ldk;
+    unsigned m = pivmask;
+    for (int s = 0; s < r; ++s) {
+      const int pos = cols + (__ffs(m) - 1);
+      m &= m - 1;
+      out[s] = std::uint8_t((row[pos >> 5] >> (pos & 31)) & 1u);
+    }
+    // R rows: the non-pivot columns of pivot rows
+    if (q >= 0) {
+      std::uint8_t* rr = ex.R + std::int64_t(q) * ex.ldr;
+      int t = 0;
+      for (int c = 0; c < cols; ++c)
+        if (!colpiv[c]) rr[t++] = std::uint8_t((row[c >> 5] >> (c & 31)) & 1u);
+    }
+  }
+}
+
+}  // namespace
+
+bool ech_gf2_small(std::int64_t rows, std::int64_t cols, const std::uint8_t* H, std::int64_t ldh,
+                   std::int32_t* info, std::int64_t cap, cudaStream_t s, const EchExtract& ex) {
+  if (rows < 1 || rows > 32 || cols < 1) return false;
+  const std::int64_t Wd = (cols + rows + 31) / 32;
+  const std::size_t smem = std::size_t(32 * (Wd + 1)) * 4 + std::size_t(cols) + 16;
+  if (smem > 200 * 1024) return false;
+  static bool attr = false;
+  if (!attr) {
+    GFQ_CUDA(cudaFuncSetAttribute(ech_gf2_small_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  200 * 1024));
+    attr = true;
+  }
+  ech_gf2_small_kernel<<<1, 32, smem, s>>>(int(rows), int(cols), H, ldh, info, int(cap), ex);
+  GFQ_CUDA(cudaGetLastError());
+  count_launch();
   return true;
 }
 

@@ -113,9 +113,25 @@ std::int64_t ech_gf2_scratch_words(std::int64_t rows, std::int64_t cols);
 // Same contract, cluster-resident (one 8-CTA cluster, distributed shared
 // memory): rows <= 1024 and cols + rows <= 8192, no scratch.  Returns false
 // (nothing launched) outside those limits or with GFQ_NO_GF2_CLUSTER set.
+// With ex (Out == nullptr) the kernel writes the reference's EchResult
+// blocks directly: M (cap x cap: rows by pivot order, columns by sorted pivot
+// row), K (rows x cap: non-pivot rows in order), R (cap x cols: non-pivot
+// columns in order); the caller views the leading r x r / (rows-r) x r /
+// r x (cols-r) corners once it has read the rank.
+struct EchExtract {
+  std::uint8_t *M, *K, *R;
+  std::int64_t ldm, ldk, ldr;
+  // scratch of the cluster path: packed rows (rows x Wd words) and index maps
+  std::uint32_t* P;
+  std::int16_t *RS, *QK, *GC;  // rows, rows, cols entries
+};
 bool ech_gf2_cluster(std::int64_t rows, std::int64_t cols, const std::uint8_t* H, std::int64_t ldh,
                      std::uint8_t* Out, std::int64_t ldo, std::int32_t* info, std::int64_t cap,
-                     cudaStream_t s);
+                     cudaStream_t s, const EchExtract* ex = nullptr);
+// GF(2) ECH of a block with <= 32 rows (any width): one warp, extraction
+// outputs as above.  Returns false (nothing launched) outside its limits.
+bool ech_gf2_small(std::int64_t rows, std::int64_t cols, const std::uint8_t* H, std::int64_t ldh,
+                   std::int32_t* info, std::int64_t cap, cudaStream_t s, const EchExtract& ex);
 
 // dst[rmap[i]] = src[i] for rmap[i] >= 0 (row scatter).
 void scatter_rows(std::uint8_t* dst, std::int64_t ldd, std::int64_t rows, std::int64_t cols,
