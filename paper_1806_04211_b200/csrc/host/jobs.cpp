@@ -368,7 +368,7 @@ EchResult panel_ech(const FieldSpec& f, const Mat& h) {
     auto db = upload_i32(diag);
     dev::set_entries(aug.data(), aug.ld(), dptr(db), a, 1, s);
   }
-  DevBuf flags{static_cast<std::size_t>(a)};
+  DevBuf flags{static_cast<std::size_t>(dev::ech_panel_flag_bytes(a))};
   DevBuf info{static_cast<std::size_t>(4 * (1 + 2 * cap))};
   DevBuf rho2{static_cast<std::size_t>(4 * w)};
   GFQ_CUDA(cudaMemsetAsync(flags.ptr, 0, flags.bytes, s));

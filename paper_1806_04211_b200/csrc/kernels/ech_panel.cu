@@ -52,16 +52,34 @@ __device__ __forceinline__ void load_seg(const std::uint8_t* src, int wc, uint4&
     return;
   }
   std::uint32_t w[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-  for (int c = 0; c < wc; ++c) w[c >> 2] |= std::uint32_t(src[c]) << (8 * (c & 3));
+#pragma unroll
+  for (int c = 0; c < kW; ++c)
+    if (c < wc) w[c >> 2] |= std::uint32_t(src[c]) << (8 * (c & 3));
   a = make_uint4(w[0], w[1], w[2], w[3]);
   b = make_uint4(w[4], w[5], w[6], w[7]);
 }
 
-__global__ void __launch_bounds__(1024)
-ech_panel_kernel(std::uint32_t p, std::uint32_t magic, int rows, int c0, int wc, int w,
-                 const std::uint8_t* __restrict__ Aug, std::int64_t ld, std::uint8_t* flags,
-                 std::int32_t* info, int cap, std::uint8_t* G, std::int64_t ldg,
-                 std::int32_t* rho2) {
+// byte k (0..31) of a row held as 8 packed words
+// (a select tree in PTX: a plain select chain is turned back into a
+// dynamically indexed local-memory array by the compiler)
+__device__ __forceinline__ std::uint32_t sel(bool c, std::uint32_t a, std::uint32_t b) {
+  std::uint32_t r;
+  asm("{ .reg .pred q; setp.ne.u32 q, %1, 0; selp.b32 %0, %2, %3, q; }"
+      : "=r"(r) : "r"(std::uint32_t(c)), "r"(a), "r"(b));
+  return r;
+}
+__device__ __forceinline__ std::uint32_t byte_of(const std::uint32_t (&w)[8], int k) {
+  const bool b2 = k & 4, b3 = k & 8, b4 = k & 16;
+  const std::uint32_t x01 = sel(b2, w[1], w[0]), x23 = sel(b2, w[3], w[2]);
+  const std::uint32_t x45 = sel(b2, w[5], w[4]), x67 = sel(b2, w[7], w[6]);
+  const std::uint32_t x = sel(b4, sel(b3, x67, x45), sel(b3, x23, x01));
+  return (x >> (8 * (k & 3))) & 0xFFu;
+}
+__device__ __forceinline__ void panel_full(std::uint32_t p, std::uint32_t magic, int rows, int c0,
+                                           int wc, const std::uint8_t* __restrict__ Aug,
+                                           std::int64_t ld, std::uint8_t* flags, std::int32_t* info,
+                                           int cap, std::uint8_t* G, std::int64_t ldg,
+                                           std::int32_t* rho2) {
   extern __shared__ __align__(16) std::uint8_t sm[];
   std::uint8_t* P = sm;                   // rows x kW
   std::uint8_t* fl = sm + rows * kW;      // rows (pivot flags)
@@ -206,7 +224,7 @@ ech_panel_kernel(std::uint32_t p, std::uint32_t magic, int rows, int c0, int wc,
     for (int t = 0; t < kW; ++t) acc[t] = 0;
     for (int q = 0; q < r2; ++q) {
       const int cq = pc[q];
-      std::uint32_t v = (seg[cq >> 2] >> (8 * (cq & 3))) & 0xFF;
+      std::uint32_t v = byte_of(seg, cq);
       if (pr[q] == i) v += 1;
       if (!v) continue;
 #pragma unroll
@@ -224,6 +242,237 @@ ech_panel_kernel(std::uint32_t p, std::uint32_t magic, int rows, int c0, int wc,
     dst[0] = make_uint4(outw[0], outw[1], outw[2], outw[3]);
     dst[1] = make_uint4(outw[4], outw[5], outw[6], outw[7]);
   }
+}
+
+__global__ void __launch_bounds__(1024)
+ech_panel_kernel(std::uint32_t p, std::uint32_t magic, int rows, int c0, int wc, int w,
+                 const std::uint8_t* __restrict__ Aug, std::int64_t ld, std::uint8_t* flags,
+                 std::int32_t* info, int cap, std::uint8_t* G, std::int64_t ldg,
+                 std::int32_t* rho2) {
+  (void)w;
+  panel_full(p, magic, rows, c0, wc, Aug, ld, flags, info, cap, G, ldg, rho2);
+}
+
+// a + v * b, bytewise mod p (two 16-bit lanes per product)
+__device__ __forceinline__ std::uint32_t axpy4(std::uint32_t a, std::uint32_t v, std::uint32_t b,
+                                               std::uint32_t p, std::uint32_t magic) {
+  const std::uint32_t lo = (a & 0x00FF00FFu) + v * (b & 0x00FF00FFu);
+  const std::uint32_t hi = ((a >> 8) & 0x00FF00FFu) + v * ((b >> 8) & 0x00FF00FFu);
+  return modp(lo & 0xFFFF, p, magic) | (modp(hi & 0xFFFF, p, magic) << 8) |
+         (modp(lo >> 16, p, magic) << 16) | (modp(hi >> 16, p, magic) << 24);
+}
+
+// General p, windowed: the panel's pivots all lie in the 64 rows from the
+// first non-pivotal one when the panel has full rank (the chosen row is the
+// FIRST non-pivotal row with a nonzero), so warp 0 runs the chain on that
+// window alone (2 rows per lane, no barriers), tracking for each row the
+// coefficients of the pivot rows' ORIGINAL values added to it (Gauss-Jordan,
+// so pivot rows are reduced too; a pivot row is scaled by -1/pivot).  Then
+//   G[pivot row q] = its coefficients ĉ_q,
+//   G[other row i] = a_i . (I + Ĉ), a_i = orig_i at the pivot columns,
+// the same multipliers ech_panel_kernel produces through -inv(pivot block).
+// A column without a window candidate while rows outside the window are
+// still open sends the panel to the full CTA algorithm.
+__global__ void __launch_bounds__(1024)
+ech_panel_win_kernel(std::uint32_t p, std::uint32_t magic, int rows, int c0, int wc,
+                     const std::uint8_t* __restrict__ Aug, std::int64_t ld, std::uint8_t* flags,
+                     std::int32_t* info, int cap, std::uint8_t* G, std::int64_t ldg,
+                     std::int32_t* rho2, std::int32_t* lo_state) {
+  __shared__ std::uint8_t invw[256];
+  __shared__ int wpc[kW], wpr[kW], wr2, wok, wrold;
+  __shared__ __align__(16) std::uint32_t chat[kW][kW / 4];  // pivot q's coefficients (packed)
+  __shared__ std::uint32_t Nm[kW][kW];                       // I + Ĉ
+  __shared__ std::uint32_t sP[8], sCP[8];                    // current pivot row / coefficients
+  const int tid = threadIdx.x, nt = blockDim.x, lane = tid & 31;
+  for (int a = tid; a < 256; a += nt)
+    invw[a] = (a > 0 && std::uint32_t(a) < p) ? std::uint8_t(powmod(a, p - 2, p)) : 0;
+  if (tid == 0) wrold = info[0];
+  __syncthreads();
+  if (tid < 32) {
+    const int r_old = wrold;
+    int lo = *lo_state;
+    for (;;) {
+      const int idx = lo + lane;
+      const unsigned b = __ballot_sync(0xffffffffu, idx < rows && flags[idx] == 0);
+      if (b || lo >= rows) {
+        if (b) lo += __ffs(b) - 1;
+        break;
+      }
+      lo += 32;
+    }
+    if (lo > rows) lo = rows;
+    const int i0 = lo + lane, i1 = lo + 32 + lane;
+    std::uint32_t w0[8], w1[8], k0[8], k1[8];
+    {
+      uint4 a, b;
+      if (i0 < rows) load_seg(Aug + std::int64_t(i0) * ld + c0, wc, a, b);
+      else a = b = make_uint4(0, 0, 0, 0);
+      w0[0] = a.x; w0[1] = a.y; w0[2] = a.z; w0[3] = a.w; w0[4] = b.x; w0[5] = b.y; w0[6] = b.z; w0[7] = b.w;
+      if (i1 < rows) load_seg(Aug + std::int64_t(i1) * ld + c0, wc, a, b);
+      else a = b = make_uint4(0, 0, 0, 0);
+      w1[0] = a.x; w1[1] = a.y; w1[2] = a.z; w1[3] = a.w; w1[4] = b.x; w1[5] = b.y; w1[6] = b.z; w1[7] = b.w;
+    }
+#pragma unroll
+    for (int q = 0; q < 8; ++q) k0[q] = k1[q] = 0;
+    bool p0 = i0 >= rows || flags[i0] != 0, p1 = i1 >= rows || flags[i1] != 0;
+    const int open_in = __popc(__ballot_sync(0xffffffffu, !p0)) + __popc(__ballot_sync(0xffffffffu, !p1));
+    const bool covers_all = open_in == rows - r_old;
+    int q0 = -1, q1 = -1;  // pivot index of my rows, if any
+    int r2 = 0, ok = 1;
+#pragma unroll
+    for (int cw = 0; cw < kW / 4; ++cw)
+    for (int cb = 0; cb < 4; ++cb) {
+      const int c = 4 * cw + cb;
+      if (c >= wc) break;
+      const std::uint32_t v0 = (w0[cw] >> (8 * cb)) & 0xFFu, v1 = (w1[cw] >> (8 * cb)) & 0xFFu;
+      const unsigned b0 = __ballot_sync(0xffffffffu, v0 != 0 && !p0);
+      const unsigned b1 = __ballot_sync(0xffffffffu, v1 != 0 && !p1);
+      if (!(b0 | b1)) {
+        if (covers_all) continue;  // a free column
+        ok = 0;
+        goto chain_done;
+      }
+      const int hi = b0 ? 0 : 1;
+      const int sl = __ffs(hi ? b1 : b0) - 1;
+      // the pivot lane scales its row by s = -1/v and forms the coefficients
+      if (lane == sl) {
+        std::uint32_t P[8], CP[8];
+        const std::uint32_t v = hi ? v1 : v0;
+        const std::uint32_t sc = p - invw[v];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+          P[q] = axpy4(0, sc, hi ? w1[q] : w0[q], p, magic);
+          CP[q] = axpy4(0, sc, hi ? k1[q] : k0[q], p, magic);
+        }
+        // + (s - 1) on its own pivot index r2
+        const int wq = r2 >> 2, sh = 8 * (r2 & 3);
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+          const std::uint32_t m = sel(q == wq, 0xFFu << sh, 0u);
+          const std::uint32_t nv = modp(((CP[q] >> sh) & 0xFFu) + sc + p - 1, p, magic);
+          CP[q] = (CP[q] & ~m) | ((nv << sh) & m);
+        }
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+          sP[q] = P[q];
+          sCP[q] = CP[q];
+        }
+      }
+      __syncwarp();
+      const std::uint32_t* P = sP;
+      const std::uint32_t* CP = sCP;
+      const bool me0 = !hi && lane == sl, me1 = hi && lane == sl;
+      // the pivot's own index bit: coefficient v on pivot r2 (the "+e_q")
+      const int wq = r2 >> 2, sh = 8 * (r2 & 3);
+      if (me0) {
+#pragma unroll
+        for (int q = 0; q < 8; ++q) { w0[q] = P[q]; k0[q] = CP[q]; }
+        p0 = true;
+        q0 = r2;
+      } else if (v0) {
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+          if (q >= cw) w0[q] = axpy4(w0[q], v0, P[q], p, magic);
+          const std::uint32_t e = sel(q == wq, 1u << sh, 0u);
+          k0[q] = axpy4(k0[q], v0, CP[q] + e, p, magic);
+        }
+      }
+      if (me1) {
+#pragma unroll
+        for (int q = 0; q < 8; ++q) { w1[q] = P[q]; k1[q] = CP[q]; }
+        p1 = true;
+        q1 = r2;
+      } else if (v1) {
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+          if (q >= cw) w1[q] = axpy4(w1[q], v1, P[q], p, magic);
+          const std::uint32_t e = sel(q == wq, 1u << sh, 0u);
+          k1[q] = axpy4(k1[q], v1, CP[q] + e, p, magic);
+        }
+      }
+      __syncwarp();  // sP/sCP are rewritten by the next pivot
+      if (lane == 0) {
+        wpc[r2] = c;
+        wpr[r2] = lo + 32 * hi + sl;
+      }
+      ++r2;
+    }
+  chain_done:
+    if (ok) {
+      if (q0 >= 0) {
+#pragma unroll
+        for (int q = 0; q < 8; ++q) chat[q0][q] = k0[q];
+      }
+      if (q1 >= 0) {
+#pragma unroll
+        for (int q = 0; q < 8; ++q) chat[q1][q] = k1[q];
+      }
+    }
+    if (lane == 0) {
+      wok = ok;
+      wr2 = r2;
+      *lo_state = lo;
+    }
+  }
+  __syncthreads();
+  if (!wok) {
+    panel_full(p, magic, rows, c0, wc, Aug, ld, flags, info, cap, G, ldg, rho2);
+    return;
+  }
+  const int r2 = wr2, r_old = wrold;
+  // N = I + Ĉ (u32 entries < p)
+  for (int e = tid; e < kW * kW; e += nt) {
+    const int q = e / kW, t = e % kW;
+    std::uint32_t v = 0;
+    if (q < r2 && t < r2) {
+      v = (chat[q][t >> 2] >> (8 * (t & 3))) & 0xFFu;
+      if (t == q) v = v + 1 == p ? 0 : v + 1;
+    }
+    Nm[q][t] = v;
+  }
+  if (tid < kW) rho2[tid] = tid < r2 ? wpr[tid] : -1;
+  if (tid < r2) {
+    info[1 + r_old + tid] = c0 + wpc[tid];
+    info[1 + cap + r_old + tid] = wpr[tid];
+  }
+  __syncthreads();
+  for (int i = tid; i < rows; i += nt) {
+    int qi = -1;
+    for (int q = 0; q < r2; ++q)
+      if (wpr[q] == i) qi = q;
+    std::uint32_t outw[kW / 4];
+    if (qi >= 0) {
+#pragma unroll
+      for (int t4 = 0; t4 < kW / 4; ++t4) outw[t4] = chat[qi][t4];
+    } else {
+      uint4 a, b;
+      load_seg(Aug + std::int64_t(i) * ld + c0, wc, a, b);
+      const std::uint32_t seg[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
+      std::uint32_t acc[kW];
+#pragma unroll
+      for (int t = 0; t < kW; ++t) acc[t] = 0;
+      for (int q = 0; q < r2; ++q) {
+        const int cq = wpc[q];
+        const std::uint32_t v = byte_of(seg, cq);
+        if (!v) continue;
+#pragma unroll
+        for (int t = 0; t < kW; ++t) acc[t] += v * Nm[q][t];
+      }
+#pragma unroll
+      for (int t4 = 0; t4 < kW / 4; ++t4) {
+        std::uint32_t word = 0;
+#pragma unroll
+        for (int by = 0; by < 4; ++by) word |= modp(acc[4 * t4 + by], p, magic) << (8 * by);
+        outw[t4] = word;
+      }
+    }
+    uint4* dst = reinterpret_cast<uint4*>(G + std::int64_t(i) * ldg);
+    dst[0] = make_uint4(outw[0], outw[1], outw[2], outw[3]);
+    dst[1] = make_uint4(outw[4], outw[5], outw[6], outw[7]);
+  }
+  __syncthreads();
+  if (tid < r2) flags[wpr[tid]] = 1;
+  if (tid == 0) info[0] = r_old + r2;
 }
 
 // GF(2): the 32 panel columns of a row are one 32-bit word, a row
@@ -535,8 +784,17 @@ void ech_panel(std::uint32_t p, std::int64_t rows, std::int64_t c0, std::int64_t
   const std::size_t smem = std::size_t(rows) * (kW + 1);
   if (smem > std::size_t(kPanelSmem)) throw std::invalid_argument("ech_panel: block too tall");
   const std::uint32_t magic = static_cast<std::uint32_t>((0x100000000ULL / p) + 1);
-  ech_panel_kernel<<<1, threads, smem, s>>>(p, magic, int(rows), int(c0), int(wc), int(w), Aug, ld,
-                                            flags, info, int(cap), G, ldg, rho2);
+  static bool attr_w = false;
+  if (!attr_w) {
+    GFQ_CUDA(cudaFuncSetAttribute(ech_panel_win_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  kPanelSmem));
+    attr_w = true;
+  }
+  // the window start persists after the flags (the caller allocates
+  // ech_panel_flag_bytes(rows) and zeroes them before the first panel)
+  auto* lo_state = reinterpret_cast<std::int32_t*>(flags + ((rows + 15) / 16) * 16);
+  ech_panel_win_kernel<<<1, threads, smem, s>>>(p, magic, int(rows), int(c0), int(wc), Aug, ld, flags,
+                                                info, int(cap), G, ldg, rho2, lo_state);
   GFQ_CUDA(cudaGetLastError());
   count_launch();
 }

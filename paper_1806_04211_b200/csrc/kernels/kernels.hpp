@@ -96,6 +96,9 @@ void ech_base(std::uint32_t p, std::int64_t rows, std::int64_t cols,
 // The caller then applies Aug[:, c0:] += G.Aug[rho2, c0:].
 // Requires w == 32 and rows * 33 <= kPanelSmem bytes.
 constexpr int kPanelSmem = 200 * 1024;
+// Bytes the caller allocates (and zeroes) for ech_panel's `flags`: one per
+// row plus the persistent window state of the general-p panel kernel.
+inline std::int64_t ech_panel_flag_bytes(std::int64_t rows) { return (rows + 15) / 16 * 16 + 16; }
 void ech_panel(std::uint32_t p, std::int64_t rows, std::int64_t c0, std::int64_t wc,
                std::int64_t w, const std::uint8_t* Aug, std::int64_t ld, std::uint8_t* flags,
                std::int32_t* info, std::int64_t cap, std::uint8_t* G, std::int64_t ldg,

@@ -216,6 +216,33 @@ def test_ech_random_shapes_and_thresholds(G, mode, p):
     check_ech(G, p, low, G.ech(f, low, 32))
 
 
+@pytest.mark.parametrize("p", [3, 7, 251])
+def test_ech_panel_window_fallbacks(G, p):
+    """Panel shapes that defeat the general-p 64-row window (pivots more than
+    64 rows below the first open row, free columns, pivotal rows inside the
+    window) must give the same result as the full CTA algorithm."""
+    G.set_ech_mode(0)
+    f = G.FieldSpec(p)
+    rng = np.random.default_rng(p)
+    H = rnd(p, 300, 200, 1)
+    H[:100] = 0                       # window of panel 0 sees zero rows only
+    check_ech(G, p, H, G.ech(f, H))
+    H = rnd(p, 300, 200, 2)
+    H[:100, :64] = 0                  # panels 0-1 fall back, later panels use the window
+    check_ech(G, p, H, G.ech(f, H))
+    H = rnd(p, 90, 200, 3)
+    H[:, rng.choice(200, 50, replace=False)] = 0   # free columns
+    check_ech(G, p, H, G.ech(f, H))
+    H = rnd(p, 400, 120, 4)
+    H[rng.choice(400, 300, replace=False)] = 0     # sparse rows: windows skip zeros
+    check_ech(G, p, H, G.ech(f, H))
+    H = rnd(p, 2000, 96, 5)
+    H[::3] = 0
+    check_ech(G, p, H, G.ech(f, H))
+    low = oracle.random_product_matrix(p, 500, 300, 70, 6)   # rank 70 < 300 columns
+    check_ech(G, p, low, G.ech(f, low))
+
+
 def test_ech_reference_fixtures(G, mode, ref_runs):
     for c in ref_runs["ech"]:
         H = np.array(c["H"], np.uint8).reshape(c["m"], c["n"])
