@@ -91,6 +91,10 @@ int gfq_set_ech_base(uint64_t n);
 /* ECH algorithm: 0 = panel Gauss-Jordan on [W | T] (default), 1 = the
  * reference's split/combine recursion (jobs.cpp:202-225).  Same outputs. */
 int gfq_set_ech_mode(int mode);
+/* Outer panel width of the two-level device ECH: -1 = automatic (default),
+ * 0 = one level (32-wide steps over all of [W | T]), else 32..256 (rounded
+ * down to a multiple of 32).  Same outputs. */
+int gfq_set_ech_outer(int width);
 /* Accounting: kernel launches issued by this library (optionally reset),
  * and K1 per-launch device timing (CUDA events on the launch stream).
  * gfq_profile_take returns, for [0] = tcgen05 path and [1] = SIMT path,

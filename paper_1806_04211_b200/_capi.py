@@ -72,6 +72,7 @@ PROTOS = {
     "gfq_random_matrix": (I, [U32, I64, I64, U64, vpp]),
     "gfq_random_product_matrix": (I, [U32, I64, I64, I64, U64, vpp]),
     "gfq_set_ech_base": (I, [U64]),
+    "gfq_set_ech_outer": (I, [ctypes.c_int]),
     "gfq_set_ech_mode": (I, [I]),
     "gfq_launch_count": (I, [I, c_i64p]),
     "gfq_profile": (I, [I]),

@@ -2,6 +2,7 @@
 #include "jobs.hpp"
 
 #include <algorithm>
+#include <cstdlib>
 #include <string>
 #include <atomic>
 #include <stdexcept>
@@ -291,7 +292,7 @@ EchResult direct_ech(const FieldSpec& f, const Mat& h) {
 // M, K, R from the reduced Aug = [W | T] (T uncompacted: column t = original
 // row t) in the reference's conventions.
 EchResult extract_ech(std::int64_t a, std::int64_t b, const Mat& aug, const std::int32_t* inf,
-                      std::int64_t cap) {
+                      std::int64_t cap, std::int64_t toff) {
   std::vector<std::int32_t> hi(std::size_t(1 + 2 * cap));
   download_i32(inf, hi.data(), hi.size());
   const std::int64_t r = hi[0];
@@ -305,11 +306,27 @@ EchResult extract_ech(std::int64_t a, std::int64_t b, const Mat& aug, const std:
   const auto tcols = as_i32(rho);
   const auto krows = as_i32(index_set_complement(out.rho).members);
   const auto gcols = as_i32(index_set_complement(out.gamma).members);
-  const Mat W = aug.col_view(0, b), T = aug.col_view(b, a);
+  const Mat W = aug.col_view(0, b), T = aug.col_view(toff, a);
   out.M = select(r, r, T, nullptr, &prow, &tcols);
   out.K = select(a - r, r, T, nullptr, &krows, &tcols);
   out.R = select(r, b - r, W, nullptr, &prow, &gcols);
   return out;
+}
+
+// Outer panel width of the two-level device ECH (0 = one level).  Blocks
+// whose trailing updates are big enough for K1's tensor path take 256-wide
+// outer panels: the 32-wide steps then only sweep an L2-resident a x 512
+// scratch, and the rest of [W | T] sees one K = 256 contraction per outer
+// panel instead of eight K = 32 ones.  GFQ_ECH_OUTER overrides (0 disables).
+constexpr std::int64_t kEchOuterMax = 256;
+std::atomic<int> g_ech_outer{[] {
+  const char* e = std::getenv("GFQ_ECH_OUTER");
+  return e ? std::atoi(e) : -1;
+}()};
+std::int64_t ech_outer_width(std::int64_t a, std::int64_t b) {
+  const std::int64_t forced = g_ech_outer;
+  if (forced >= 0) return forced == 0 ? 0 : std::min<std::int64_t>(kEchOuterMax, std::max<std::int64_t>(32, forced / 32 * 32));
+  return (b > 64 && a * (a + b) >= std::int64_t(1) << 20) ? kEchOuterMax : 0;
 }
 
 // Device ECH: right-looking panel Gauss-Jordan on Aug = [W | T] (T = I), one
@@ -355,36 +372,87 @@ EchResult panel_ech(const FieldSpec& f, const Mat& h) {
       dev::ech_gf2_block(a, b, h.data(), h.ld(), reinterpret_cast<std::uint32_t*>(scratch.ptr),
                          aug.data(), aug.ld(), inf, cap, s);
     }
-    return extract_ech(a, b, aug, inf, cap);
+    return extract_ech(a, b, aug, inf, cap, b);
   }
-  Mat aug = Mat::zeros(a, b + a);
+  // Aug = [W | 0 | T]: T starts at the 16-aligned column tb so every
+  // trailing update below is a TMA-legal view
+  const std::int64_t tb = (b + 15) / 16 * 16;
+  Mat aug = Mat::zeros(a, tb + a);
   dev::select2d(aug.data(), aug.ld(), a, b, h.data(), h.ld(), nullptr, 0, nullptr, nullptr, s);
   {
     std::vector<std::int32_t> diag(std::size_t(2 * a));
     for (std::int64_t i = 0; i < a; ++i) {
       diag[2 * i] = std::int32_t(i);
-      diag[2 * i + 1] = std::int32_t(b + i);
+      diag[2 * i + 1] = std::int32_t(tb + i);
     }
     auto db = upload_i32(diag);
     dev::set_entries(aug.data(), aug.ld(), dptr(db), a, 1, s);
   }
   DevBuf flags{static_cast<std::size_t>(dev::ech_panel_flag_bytes(a))};
-  DevBuf info{static_cast<std::size_t>(4 * (1 + 2 * cap))};
+  DevBuf info{static_cast<std::size_t>(4 * (1 + 2 * cap) + 4 * (2 + kEchOuterMax))};
   DevBuf rho2{static_cast<std::size_t>(4 * w)};
   GFQ_CUDA(cudaMemsetAsync(flags.ptr, 0, flags.bytes, s));
   GFQ_CUDA(cudaMemsetAsync(info.ptr, 0, info.bytes, s));
-  Mat G(a, w), Bp(w, b + a);
   auto* inf = reinterpret_cast<std::int32_t*>(info.ptr);
   auto* r2 = reinterpret_cast<std::int32_t*>(rho2.ptr);
-  for (std::int64_t c0 = 0; c0 < b; c0 += w) {
-    const std::int64_t wc = std::min(w, b - c0), n = b + a - c0;
-    dev::ech_panel(f.p(), a, c0, wc, w, aug.data(), aug.ld(), flags.ptr, inf, cap, G.data(),
-                   G.ld(), r2, s);
-    dev::select2d(Bp.data(), Bp.ld(), w, n, aug.data() + c0, aug.ld(), nullptr, 0, r2, nullptr, s);
-    dev::mad(f.p(), a, n, w, G.data(), G.ld(), Bp.data(), Bp.ld(), aug.data() + c0, aug.ld(),
-             aug.data() + c0, aug.ld(), s);
+  const std::int64_t ow = ech_outer_width(a, b);
+  if (ow == 0) {
+    Mat G(a, w), Bp(w, tb + a);
+    for (std::int64_t c0 = 0; c0 < b; c0 += w) {
+      const std::int64_t wc = std::min(w, b - c0), n = tb + a - c0;
+      dev::ech_panel(f.p(), a, c0, wc, w, aug.data(), aug.ld(), flags.ptr, inf, cap, G.data(),
+                     G.ld(), r2, s);
+      dev::select2d(Bp.data(), Bp.ld(), w, n, aug.data() + c0, aug.ld(), nullptr, 0, r2, nullptr, s);
+      dev::mad(f.p(), a, n, w, G.data(), G.ld(), Bp.data(), Bp.ld(), aug.data() + c0, aug.ld(),
+               aug.data() + c0, aug.ld(), s);
+    }
+    return extract_ech(a, b, aug, inf, cap, tb);
   }
-  return extract_ech(a, b, aug, inf, cap);
+  // Two-level: each outer panel of `ow` columns is eliminated in Z = [X | Y]
+  // by 32-wide steps (their updates stay inside Z, L2-resident), then ONE
+  // deep-K contraction Aug[:, right] += Gout.Aug[P, right] applies the
+  // panel's row operator to everything right of it (W and T) on K1.
+  auto* base = inf + 1 + 2 * cap;  // rank at the start of the outer panel
+  auto* rmap = base + 1;           // the outer panel's pivot rows (ow slots)
+  Mat Z(a, 2 * ow), Bt(ow, tb + a);
+  DevBuf step{static_cast<std::size_t>(dev::ech_step_scratch_bytes())};
+  const bool fused = a * 33 <= dev::kPanelSmem;
+  Mat G(fused ? 0 : a, w), Bp(fused ? 0 : w, 2 * ow);
+  for (std::int64_t C0 = 0; C0 < b; C0 += ow) {
+    const std::int64_t wd = std::min(ow, b - C0), kc = std::min(wd, a);
+    // Z[:, 0:wd] = Aug[:, C0:C0+wd], Z[:, ow:] = 0
+    GFQ_CUDA(cudaMemcpy2DAsync(Z.data(), std::size_t(Z.ld()), aug.data() + C0, std::size_t(aug.ld()),
+                               std::size_t(wd), std::size_t(a), cudaMemcpyDeviceToDevice, s));
+    GFQ_CUDA(cudaMemset2DAsync(Z.data() + wd, std::size_t(Z.ld()), 0, std::size_t(2 * ow - wd),
+                               std::size_t(a), s));
+    std::uint8_t* Y = Z.data() + ow;
+    for (std::int64_t c0 = 0; c0 < wd; c0 += w) {
+      const std::int64_t wc = std::min(w, wd - c0);
+      // the step updates Z columns from c0 through Y's used slots
+      const std::int64_t n = (ow + std::min(kc, c0 + w) - c0 + 15) / 16 * 16;
+      if (fused) {
+        dev::ech_step(f.p(), a, c0, wc, n, Z.data(), Z.ld(), flags.ptr, inf, cap, r2, step.ptr, Y,
+                      base, s);
+        continue;
+      }
+      // GF(2) blocks too tall for the fused step's fallback: the panel
+      // kernel's G for every row, then the gather and the K1 update
+      dev::ech_panel(f.p(), a, c0, wc, w, Z.data(), Z.ld(), flags.ptr, inf, cap, G.data(), G.ld(),
+                     r2, s);
+      dev::ech_panel_plant(Y, Z.ld(), r2, inf, base, s);
+      dev::select2d(Bp.data(), Bp.ld(), w, n, Z.data() + c0, Z.ld(), nullptr, 0, r2, nullptr, s);
+      dev::mad(f.p(), a, n, w, G.data(), G.ld(), Bp.data(), Bp.ld(), Z.data() + c0, Z.ld(),
+               Z.data() + c0, Z.ld(), s);
+    }
+    dev::ech_outer_finish(f.p(), Y, Z.ld(), kc, inf, cap, base, rmap, C0, s);
+    GFQ_CUDA(cudaMemcpy2DAsync(aug.data() + C0, std::size_t(aug.ld()), Z.data(), std::size_t(Z.ld()),
+                               std::size_t(wd), std::size_t(a), cudaMemcpyDeviceToDevice, s));
+    const std::int64_t r0 = C0 + wd, n = tb + a - r0;
+    dev::select2d(Bt.data(), Bt.ld(), kc, n, aug.data() + r0, aug.ld(), nullptr, 0, rmap, nullptr, s);
+    dev::mad(f.p(), a, n, kc, Y, Z.ld(), Bt.data(), Bt.ld(), aug.data() + r0, aug.ld(),
+             aug.data() + r0, aug.ld(), s);
+  }
+  return extract_ech(a, b, aug, inf, cap, tb);
 }
 
 // Split point: half, rounded to a multiple of 16 so column views keep the
@@ -445,6 +513,11 @@ EchResult combine_vertical(const FieldSpec& f, const Mat& h2, const EchResult& e
 }
 
 }  // namespace
+
+void set_ech_outer(int width) {
+  if (width < -1 || width > kEchOuterMax) throw std::invalid_argument("ech outer width must be -1..256");
+  g_ech_outer = width;
+}
 
 EchResult ech(const FieldSpec& f, const Mat& h, std::size_t threshold) {
   if (threshold < 1) threshold = 1;

@@ -59,6 +59,9 @@ std::size_t ech_base();
 /// reference's split/combine recursion down to the K2 base case.  Both give
 /// the same (canonical) outputs.
 void set_ech_mode(int mode);
+/// Outer panel width of the two-level device ECH: -1 = automatic, 0 = one
+/// level, else 32..256 (multiple of 32).  Outputs do not depend on it.
+void set_ech_outer(int width);
 int ech_mode();
 
 }  // namespace gfq

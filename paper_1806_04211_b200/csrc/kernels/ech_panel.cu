@@ -16,6 +16,7 @@
 // so that Aug[:, c0:] += G.Aug[rho2, c0:] finishes the panel (K1).  Nothing
 // returns to the host until the last panel: the ECH is a fixed launch
 // sequence.
+#include <algorithm>
 #include <cstdlib>
 
 #include "../common.hpp"
@@ -75,11 +76,21 @@ __device__ __forceinline__ std::uint32_t byte_of(const std::uint32_t (&w)[8], in
   const std::uint32_t x = sel(b4, sel(b3, x67, x45), sel(b3, x23, x01));
   return (x >> (8 * (k & 3))) & 0xFFu;
 }
+// Step outputs of the two-level ECH (ech_step_chain_kernel): instead of G
+// for every row, the 32 x 32 map NT (NT[t][c] = multiplier of panel column
+// c's ORIGINAL value in G[i][t], zero for non-pivot columns, so G[i] =
+// seg_i . NT^T for every row that is not a new pivot) and Gpiv (G rows of
+// the r2 new pivot rows, in pivot order); ech_step_update_kernel applies them.
+struct StepOut {
+  std::uint8_t* NT;
+  std::uint8_t* Gpiv;
+};
+
 __device__ __forceinline__ void panel_full(std::uint32_t p, std::uint32_t magic, int rows, int c0,
                                            int wc, const std::uint8_t* __restrict__ Aug,
                                            std::int64_t ld, std::uint8_t* flags, std::int32_t* info,
                                            int cap, std::uint8_t* G, std::int64_t ldg,
-                                           std::int32_t* rho2) {
+                                           std::int32_t* rho2, StepOut so = StepOut{nullptr, nullptr}) {
   extern __shared__ __align__(16) std::uint8_t sm[];
   std::uint8_t* P = sm;                   // rows x kW
   std::uint8_t* fl = sm + rows * kW;      // rows (pivot flags)
@@ -214,6 +225,28 @@ __device__ __forceinline__ void panel_full(std::uint32_t p, std::uint32_t magic,
   if (tid == 0) info[0] = r_old + r2;
   __syncthreads();
 
+  if (so.NT) {
+    // NT[t][pc[q]] = N2[q][t]; Gpiv[q] = Ap[pr[q]].N2 (Ap row with its +1)
+    for (int e = tid; e < kW * kW; e += nt) {
+      const int t = e / kW, c = e % kW;
+      std::uint32_t v = 0;
+      for (int q = 0; q < r2; ++q)
+        if (pc[q] == c) v = N2[q][t];
+      so.NT[e] = std::uint8_t(v);
+    }
+    for (int e = tid; e < kW * kW; e += nt) {
+      const int q = e / kW, t = e % kW;
+      std::uint32_t acc = 0;
+      if (q < r2) {
+        const std::uint8_t* src = Aug + std::int64_t(pr[q]) * ld + c0;
+        acc = N2[q][t];
+        for (int u = 0; u < r2; ++u) acc += std::uint32_t(src[pc[u]]) * N2[u][t];
+      }
+      so.Gpiv[e] = std::uint8_t(modp(acc, p, magic));
+    }
+    return;
+  }
+
   // ---- G[i] = Ap[i].N2, Ap[i][q] = Aug[i][c0 + pc[q]] (+1 on pivot row of q)
   for (int i = tid; i < rows; i += nt) {
     uint4 a, b;
@@ -273,11 +306,11 @@ __device__ __forceinline__ std::uint32_t axpy4(std::uint32_t a, std::uint32_t v,
 // the same multipliers ech_panel_kernel produces through -inv(pivot block).
 // A column without a window candidate while rows outside the window are
 // still open sends the panel to the full CTA algorithm.
-__global__ void __launch_bounds__(1024)
-ech_panel_win_kernel(std::uint32_t p, std::uint32_t magic, int rows, int c0, int wc,
-                     const std::uint8_t* __restrict__ Aug, std::int64_t ld, std::uint8_t* flags,
-                     std::int32_t* info, int cap, std::uint8_t* G, std::int64_t ldg,
-                     std::int32_t* rho2, std::int32_t* lo_state) {
+__device__ __forceinline__ void win_body(std::uint32_t p, std::uint32_t magic, int rows, int c0, int wc,
+                                         const std::uint8_t* __restrict__ Aug, std::int64_t ld,
+                                         std::uint8_t* flags, std::int32_t* info, int cap,
+                                         std::uint8_t* G, std::int64_t ldg, std::int32_t* rho2,
+                                         std::int32_t* lo_state, StepOut so) {
   __shared__ std::uint8_t invw[256];
   __shared__ int wpc[kW], wpr[kW], wr2, wok, wrold;
   __shared__ __align__(16) std::uint32_t chat[kW][kW / 4];  // pivot q's coefficients (packed)
@@ -319,12 +352,12 @@ ech_panel_win_kernel(std::uint32_t p, std::uint32_t magic, int rows, int c0, int
     const bool covers_all = open_in == rows - r_old;
     int q0 = -1, q1 = -1;  // pivot index of my rows, if any
     int r2 = 0, ok = 1;
-#pragma unroll
-    for (int cw = 0; cw < kW / 4; ++cw)
-    for (int cb = 0; cb < 4; ++cb) {
-      const int c = 4 * cw + cb;
-      if (c >= wc) break;
-      const std::uint32_t v0 = (w0[cw] >> (8 * cb)) & 0xFFu, v1 = (w1[cw] >> (8 * cb)) & 0xFFu;
+    // one column per iteration, NOT unrolled: the unrolled 32-column chain
+    // is ~300 KB of SASS run once by one warp, i.e. instruction-fetch bound
+#pragma unroll 1
+    for (int c = 0; c < wc; ++c) {
+      const int cw = c >> 2;
+      const std::uint32_t v0 = byte_of(w0, c), v1 = byte_of(w1, c);
       const unsigned b0 = __ballot_sync(0xffffffffu, v0 != 0 && !p0);
       const unsigned b1 = __ballot_sync(0xffffffffu, v1 != 0 && !p1);
       if (!(b0 | b1)) {
@@ -416,7 +449,7 @@ ech_panel_win_kernel(std::uint32_t p, std::uint32_t magic, int rows, int c0, int
   }
   __syncthreads();
   if (!wok) {
-    panel_full(p, magic, rows, c0, wc, Aug, ld, flags, info, cap, G, ldg, rho2);
+    panel_full(p, magic, rows, c0, wc, Aug, ld, flags, info, cap, G, ldg, rho2, so);
     return;
   }
   const int r2 = wr2, r_old = wrold;
@@ -436,6 +469,21 @@ ech_panel_win_kernel(std::uint32_t p, std::uint32_t magic, int rows, int c0, int
     info[1 + cap + r_old + tid] = wpr[tid];
   }
   __syncthreads();
+  if (so.NT) {
+    // NT[t][wpc[q]] = Nm[q][t]; Gpiv[q] = ĉ_q
+    for (int e = tid; e < kW * kW; e += nt) {
+      const int t = e / kW, c = e % kW;
+      std::uint32_t v = 0;
+      for (int q = 0; q < r2; ++q)
+        if (wpc[q] == c) v = Nm[q][t];
+      so.NT[e] = std::uint8_t(v);
+      const int q = e / kW, tt = e % kW;
+      so.Gpiv[e] = q < r2 ? std::uint8_t((chat[q][tt >> 2] >> (8 * (tt & 3))) & 0xFFu) : 0;
+    }
+    if (tid < r2) flags[wpr[tid]] = 1;
+    if (tid == 0) info[0] = r_old + r2;
+    return;
+  }
   for (int i = tid; i < rows; i += nt) {
     int qi = -1;
     for (int q = 0; q < r2; ++q)
@@ -473,6 +521,291 @@ ech_panel_win_kernel(std::uint32_t p, std::uint32_t magic, int rows, int c0, int
   __syncthreads();
   if (tid < r2) flags[wpr[tid]] = 1;
   if (tid == 0) info[0] = r_old + r2;
+}
+
+__global__ void __launch_bounds__(1024)
+ech_panel_win_kernel(std::uint32_t p, std::uint32_t magic, int rows, int c0, int wc,
+                     const std::uint8_t* __restrict__ Aug, std::int64_t ld, std::uint8_t* flags,
+                     std::int32_t* info, int cap, std::uint8_t* G, std::int64_t ldg,
+                     std::int32_t* rho2, std::int32_t* lo_state) {
+  win_body(p, magic, rows, c0, wc, Aug, ld, flags, info, cap, G, ldg, rho2, lo_state,
+           StepOut{nullptr, nullptr});
+}
+
+// word i (0..3) of a 4-word register group, dynamic index (select tree)
+__device__ __forceinline__ std::uint32_t word4(const std::uint32_t (&w)[4], int i) {
+  return sel(i & 2, sel(i & 1, w[3], w[2]), sel(i & 1, w[1], w[0]));
+}
+
+// Two-level ECH, step part 1 (one CTA of kStepThreads = 8 warps): the
+// pivot chain of the 32-wide step at scratch column c0 on the 64-row window
+// from the first open row (the pivots all lie there when the step's panel
+// has full rank -- the chosen row is the FIRST open row with a nonzero).
+// Thread (row = tid / 4, quarter = tid % 4) holds 4 of the row's 16 state
+// words in registers: quarters 0-1 the 32 panel bytes, quarters 2-3 the
+// coefficients of the pivot rows' ORIGINAL values added to the row
+// (Gauss-Jordan with coefficient tracking; a pivot row is scaled by
+// -1/pivot).  Per column: the factor by a 4-lane shuffle, candidates by
+// ballot, two CTA barriers (candidate masks, normalised pivot row), then
+// every row's axpy.  A column with no window candidate while open rows lie
+// outside the window sends the step to the full CTA algorithm (panel_full).
+// Then
+//   * NT / Gpiv (StepOut) instead of G: G[new pivot q] = ĉ_q, G[other i] =
+//     seg_i[pc] . (I + Ĉ)  (the multipliers of ech_panel_kernel),
+//   * Y[rho2[q], r_old + q - *base] = 1 (the outer panel's tracking units),
+//   * BpT[j][q] = Z[rho2[q]][c0 + j] for j < n (q >= r2: 0), the step's
+//     pivot rows transposed so ech_step_update_kernel contracts over q with
+//     dp4a (n x 32 bytes).
+constexpr int kStepThreads = 256;
+__global__ void __launch_bounds__(kStepThreads)
+ech_step_chain_kernel(std::uint32_t p, std::uint32_t magic, int rows, int c0, int wc, int n,
+                      std::uint8_t* __restrict__ Z, std::int64_t ld, std::uint8_t* flags,
+                      std::int32_t* info, int cap, std::int32_t* rho2, std::int32_t* lo_state,
+                      std::uint8_t* NT, std::uint8_t* Gpiv, std::uint8_t* Y, const std::int32_t* base,
+                      std::uint8_t* BpT) {
+  extern __shared__ __align__(16) std::uint8_t dsm[];
+  __shared__ std::uint8_t invw[256];
+  __shared__ int s_lo, s_rold, s_open;
+  __shared__ unsigned cmask[2][8];
+  __shared__ std::uint32_t Pbuf[16];
+  __shared__ int wpc[kW], wpr[kW], s_pr[kW];
+  __shared__ __align__(16) std::uint32_t chat[kW][8];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  for (int a = tid; a < 256; a += kStepThreads)
+    invw[a] = (a > 0 && std::uint32_t(a) < p) ? std::uint8_t(powmod(a, p - 2, p)) : 0;
+  if (warp == 0) {
+    int lo = *lo_state;
+    for (;;) {
+      const int idx = lo + lane;
+      const unsigned b = __ballot_sync(0xffffffffu, idx < rows && flags[idx] == 0);
+      if (b || lo >= rows) {
+        if (b) lo += __ffs(b) - 1;
+        break;
+      }
+      lo += 32;
+    }
+    if (lo > rows) lo = rows;
+    if (lane == 0) {
+      s_lo = lo;
+      s_rold = info[0];
+      s_open = 0;
+      *lo_state = lo;
+    }
+  }
+  __syncthreads();
+  const int lo = s_lo, r_old = s_rold;
+  const int row = tid >> 2, qd = tid & 3, gi = lo + row;
+  std::uint32_t w[4] = {0, 0, 0, 0};
+  bool open = gi < rows && flags[gi] == 0;
+  if (qd < 2 && gi < rows) {
+    const std::uint8_t* src = Z + std::int64_t(gi) * ld + c0 + 16 * qd;
+    if (wc == kW) {
+      const uint4 a = *reinterpret_cast<const uint4*>(src);
+      w[0] = a.x; w[1] = a.y; w[2] = a.z; w[3] = a.w;
+    } else {
+#pragma unroll
+      for (int c = 0; c < 16; ++c)
+        if (16 * qd + c < wc) w[c >> 2] |= std::uint32_t(src[c]) << (8 * (c & 3));
+    }
+  }
+  {
+    const unsigned b = __ballot_sync(0xffffffffu, open && qd == 0);
+    if (lane == 0 && b) atomicAdd(&s_open, __popc(b));
+  }
+  __syncthreads();
+  const bool covers_all = s_open == rows - r_old;
+  int r2 = 0, ok = 1, myq = -1;
+#pragma unroll 1
+  for (int c = 0; c < wc; ++c) {
+    const std::uint32_t mine = (word4(w, (c >> 2) & 3) >> (8 * (c & 3))) & 0xFFu;
+    const std::uint32_t v = __shfl_sync(0xffffffffu, mine, (lane & ~3) | (c >> 4));
+    const unsigned b = __ballot_sync(0xffffffffu, qd == 0 && open && v != 0);
+    if (lane == 0) cmask[c & 1][warp] = b;
+    __syncthreads();
+    int s = -1;
+#pragma unroll
+    for (int ww = 7; ww >= 0; --ww) {
+      const unsigned m = cmask[c & 1][ww];
+      if (m) s = 8 * ww + ((__ffs(m) - 1) >> 2);
+    }
+    if (s < 0) {
+      if (covers_all) continue;  // a free column (uniform)
+      ok = 0;
+      break;
+    }
+    // K byte of the new pivot's own index r2: quarter 2 + r2 / 16, word (r2 / 4) % 4
+    const int kq = 2 + (r2 >> 4), kwd = (r2 >> 2) & 3, ksh = 8 * (r2 & 3);
+    if (row == s) {
+      const std::uint32_t sc = p - invw[v];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        std::uint32_t x = axpy4(0, sc, w[j], p, magic);
+        if (qd == kq && j == kwd) {
+          // + (s - 1) on its own pivot index
+          const std::uint32_t nv = modp(((x >> ksh) & 0xFFu) + sc + p - 1, p, magic);
+          x = (x & ~(0xFFu << ksh)) | (nv << ksh);
+        }
+        Pbuf[4 * qd + j] = x;
+      }
+    }
+    __syncthreads();
+    if (row == s) {
+#pragma unroll
+      for (int j = 0; j < 4; ++j) w[j] = Pbuf[4 * qd + j];
+      open = false;
+      myq = r2;
+    } else if (v) {
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        // the pivot's own index bit: coefficient v on pivot r2 (the "+e_q")
+        const std::uint32_t e = (qd == kq && j == kwd) ? (1u << ksh) : 0u;
+        w[j] = axpy4(w[j], v, Pbuf[4 * qd + j] + e, p, magic);
+      }
+    }
+    if (tid == 0) {
+      wpc[r2] = c;
+      wpr[r2] = lo + s;
+    }
+    ++r2;
+  }
+  __syncthreads();
+  if (!ok) {
+    panel_full(p, magic, rows, c0, wc, Z, ld, flags, info, cap, nullptr, 0, rho2,
+               StepOut{NT, Gpiv});
+  } else {
+    if (myq >= 0 && qd >= 2) {
+#pragma unroll
+      for (int j = 0; j < 4; ++j) chat[myq][4 * (qd - 2) + j] = w[j];
+    }
+    __syncthreads();
+    // NT[t][wpc[q]] = (I + Ĉ)[q][t]; Gpiv[q] = ĉ_q
+    for (int e = tid; e < kW * kW; e += kStepThreads) {
+      const int t = e / kW, c = e % kW;
+      std::uint32_t v = 0;
+      for (int q = 0; q < r2; ++q)
+        if (wpc[q] == c) {
+          v = (chat[q][t >> 2] >> (8 * (t & 3))) & 0xFFu;
+          if (t == q) v = v + 1 == p ? 0 : v + 1;
+        }
+      NT[e] = std::uint8_t(v);
+      const int q = e / kW, tt = e % kW;
+      Gpiv[e] = q < r2 ? std::uint8_t((chat[q][tt >> 2] >> (8 * (tt & 3))) & 0xFFu) : 0;
+    }
+    if (tid < kW) rho2[tid] = tid < r2 ? wpr[tid] : -1;
+    if (tid < r2) {
+      info[1 + r_old + tid] = c0 + wpc[tid];
+      info[1 + cap + r_old + tid] = wpr[tid];
+      flags[wpr[tid]] = 1;
+    }
+    if (tid == 0) info[0] = r_old + r2;
+  }
+  __syncthreads();
+  if (tid < kW) {
+    const int r = rho2[tid];
+    s_pr[tid] = r;
+    if (r >= 0) Y[std::int64_t(r) * ld + (r_old + tid - *base)] = 1;
+  }
+  __syncthreads();
+  // stage the pivot rows (32 x n, 16-byte loads) in shared memory, then
+  // write them transposed
+  std::uint8_t* Bs = dsm;  // 32 x n
+  for (int e = tid; e < kW * (n / 16); e += kStepThreads) {
+    const int q = e / (n / 16), ch = e % (n / 16);
+    const int r = s_pr[q];
+    uint4 v = make_uint4(0, 0, 0, 0);
+    if (r >= 0) v = *reinterpret_cast<const uint4*>(Z + std::int64_t(r) * ld + c0 + 16 * ch);
+    reinterpret_cast<uint4*>(Bs + q * n)[ch] = v;
+  }
+  __syncthreads();
+  for (int j = tid; j < n; j += kStepThreads) {
+    std::uint32_t o[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+#pragma unroll
+    for (int q = 0; q < kW; ++q) o[q >> 2] |= std::uint32_t(Bs[q * n + j]) << (8 * (q & 3));
+    uint4* dst = reinterpret_cast<uint4*>(BpT + std::int64_t(j) * kW);
+    dst[0] = make_uint4(o[0], o[1], o[2], o[3]);
+    dst[1] = make_uint4(o[4], o[5], o[6], o[7]);
+  }
+}
+
+// Two-level ECH, step part 2: Z[i][c0 + j] += G[i] . Bp[:, j] for every row
+// i and j < n (n a multiple of 16), with G[i] = seg_i . NT^T (mod p) or the
+// pivot row's Gpiv.  One CTA per 32 rows: warp 0 forms the 32 rows' G
+// (lane = row, 8 x 32 dp4a against NT) into shared memory while the CTA
+// stages BpT; then the 8 warps split the 16-column chunks, lane = row:
+// 16 x 8 dp4a per chunk against BpT rows broadcast from shared memory, the
+// Barrett reduction with the old values, one 16-byte load and store per lane.
+constexpr int kStepRows = 32, kStepMaxN = 512;
+__global__ void __launch_bounds__(kStepThreads)
+ech_step_update_kernel(std::uint32_t p, std::uint32_t magic, int rows, int c0, int n,
+                       std::uint8_t* __restrict__ Z, std::int64_t ld,
+                       const std::uint8_t* __restrict__ NT, const std::uint8_t* __restrict__ Gpiv,
+                       const std::int32_t* __restrict__ rho2, const std::uint8_t* __restrict__ BpT) {
+  __shared__ __align__(16) std::uint32_t sB[kStepMaxN * 8];
+  __shared__ std::uint32_t sG[kStepRows][9];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int i0 = blockIdx.x * kStepRows;
+  for (int e = tid; e < n * 2; e += kStepThreads)
+    reinterpret_cast<uint4*>(sB)[e] = reinterpret_cast<const uint4*>(BpT)[e];
+  if (warp == 0) {
+    const int i = i0 + lane;
+    const int r = rho2[lane];
+    int myq = -1;
+#pragma unroll
+    for (int u = 0; u < kW; ++u)
+      if (__shfl_sync(0xffffffffu, r, u) == i) myq = u;
+    std::uint32_t g[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    if (i < rows && myq >= 0) {
+      const uint4* src = reinterpret_cast<const uint4*>(Gpiv + myq * kW);
+      const uint4 a = src[0], b = src[1];
+      g[0] = a.x; g[1] = a.y; g[2] = a.z; g[3] = a.w; g[4] = b.x; g[5] = b.y; g[6] = b.z; g[7] = b.w;
+    } else if (i < rows) {
+      const uint4* src = reinterpret_cast<const uint4*>(Z + std::int64_t(i) * ld + c0);
+      const uint4 a = src[0], b = src[1];
+      const std::uint32_t seg[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
+      const uint4* nt4 = reinterpret_cast<const uint4*>(NT);
+#pragma unroll 4
+      for (int t = 0; t < kW; ++t) {
+        const uint4 x = nt4[2 * t], y = nt4[2 * t + 1];
+        std::uint32_t acc = 0;
+        acc = __dp4a(seg[0], x.x, acc); acc = __dp4a(seg[1], x.y, acc);
+        acc = __dp4a(seg[2], x.z, acc); acc = __dp4a(seg[3], x.w, acc);
+        acc = __dp4a(seg[4], y.x, acc); acc = __dp4a(seg[5], y.y, acc);
+        acc = __dp4a(seg[6], y.z, acc); acc = __dp4a(seg[7], y.w, acc);
+        g[t >> 2] |= modp(acc, p, magic) << (8 * (t & 3));
+      }
+    }
+#pragma unroll
+    for (int w = 0; w < 8; ++w) sG[lane][w] = g[w];
+  }
+  __syncthreads();
+  const int i = i0 + lane;
+  if (i >= rows) return;
+  std::uint32_t g[8];
+#pragma unroll
+  for (int w = 0; w < 8; ++w) g[w] = sG[lane][w];
+  std::uint8_t* zrow = Z + std::int64_t(i) * ld + c0;
+  for (int ch = warp; ch < n / 16; ch += kStepThreads / 32) {
+    std::uint32_t out[4];
+    const uint4 old = *reinterpret_cast<const uint4*>(zrow + 16 * ch);
+    const std::uint32_t ow[4] = {old.x, old.y, old.z, old.w};
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      std::uint32_t word = 0;
+#pragma unroll
+      for (int by = 0; by < 4; ++by) {
+        const uint4* b4 = reinterpret_cast<const uint4*>(sB + (16 * ch + 4 * q + by) * 8);
+        const uint4 x = b4[0], y = b4[1];
+        std::uint32_t acc = (ow[q] >> (8 * by)) & 0xFFu;
+        acc = __dp4a(g[0], x.x, acc); acc = __dp4a(g[1], x.y, acc);
+        acc = __dp4a(g[2], x.z, acc); acc = __dp4a(g[3], x.w, acc);
+        acc = __dp4a(g[4], y.x, acc); acc = __dp4a(g[5], y.y, acc);
+        acc = __dp4a(g[6], y.z, acc); acc = __dp4a(g[7], y.w, acc);
+        word |= modp(acc, p, magic) << (8 * by);
+      }
+      out[q] = word;
+    }
+    *reinterpret_cast<uint4*>(zrow + 16 * ch) = make_uint4(out[0], out[1], out[2], out[3]);
+  }
 }
 
 // GF(2): the 32 panel columns of a row are one 32-bit word, a row
@@ -727,6 +1060,37 @@ ech_panel_gf2w_kernel(int rows, int c0, int wc, const std::uint8_t* __restrict__
   }
 }
 
+// Blocked ECH bookkeeping (see ech_panel_plant / ech_outer_finish below).
+__global__ void ech_plant_kernel(std::uint8_t* Y, std::int64_t ldy, const std::int32_t* rho2,
+                                 const std::int32_t* info, const std::int32_t* base) {
+  const int lane = threadIdx.x;
+  const int r = rho2[lane];
+  const unsigned valid = __ballot_sync(0xffffffffu, r >= 0);
+  if (r >= 0) {
+    const int slot = info[0] - __popc(valid) + lane - *base;
+    Y[std::int64_t(r) * ldy + slot] = 1;
+  }
+}
+
+__global__ void ech_outer_finish_kernel(std::uint32_t p, std::uint8_t* Y, std::int64_t ldy, int kcols,
+                                        std::int32_t* info, int cap, std::int32_t* base,
+                                        std::int32_t* rmap, int col0) {
+  const int r_now = info[0], b0 = *base;
+  for (int t = threadIdx.x; t < kcols; t += blockDim.x) {
+    const int g = b0 + t;
+    int row = -1;
+    if (g < r_now) {
+      info[1 + g] += col0;  // the steps recorded scratch-local pivot columns
+      row = info[1 + cap + g];
+      std::uint8_t* y = Y + std::int64_t(row) * ldy + t;
+      *y = std::uint8_t((*y + p - 1) % p);
+    }
+    rmap[t] = row;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) *base = r_now;
+}
+
 __global__ void scatter_rows_kernel(std::uint8_t* dst, std::int64_t ldd, std::int64_t rows,
                                     std::int64_t cols, const std::uint8_t* src,
                                     std::int64_t lds, const std::int32_t* rmap) {
@@ -795,6 +1159,52 @@ void ech_panel(std::uint32_t p, std::int64_t rows, std::int64_t c0, std::int64_t
   auto* lo_state = reinterpret_cast<std::int32_t*>(flags + ((rows + 15) / 16) * 16);
   ech_panel_win_kernel<<<1, threads, smem, s>>>(p, magic, int(rows), int(c0), int(wc), Aug, ld, flags,
                                                 info, int(cap), G, ldg, rho2, lo_state);
+  GFQ_CUDA(cudaGetLastError());
+  count_launch();
+}
+
+void ech_step(std::uint32_t p, std::int64_t rows, std::int64_t c0, std::int64_t wc, std::int64_t n,
+              std::uint8_t* Z, std::int64_t ld, std::uint8_t* flags, std::int32_t* info,
+              std::int64_t cap, std::int32_t* rho2, std::uint8_t* step_scratch, std::uint8_t* Y,
+              const std::int32_t* base, cudaStream_t s) {
+  if (wc > kW || c0 % kW || n % 16 || n > kStepMaxN || (ld & 15) ||
+      (reinterpret_cast<std::uintptr_t>(Z) & 15))
+    throw std::invalid_argument("ech_step: bad step geometry");
+  const std::size_t smem = std::max<std::size_t>(std::size_t(rows) * (kW + 1), std::size_t(kW) * n);
+  if (smem > std::size_t(kPanelSmem)) throw std::invalid_argument("ech_step: block too tall");
+  static bool attr = false;
+  if (!attr) {
+    GFQ_CUDA(cudaFuncSetAttribute(ech_step_chain_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  kPanelSmem));
+    attr = true;
+  }
+  const std::uint32_t magic = static_cast<std::uint32_t>((0x100000000ULL / p) + 1);
+  auto* lo_state = reinterpret_cast<std::int32_t*>(flags + ((rows + 15) / 16) * 16);
+  std::uint8_t* NT = step_scratch;
+  std::uint8_t* Gpiv = step_scratch + kW * kW;
+  std::uint8_t* BpT = step_scratch + 2 * kW * kW;
+  ech_step_chain_kernel<<<1, kStepThreads, smem, s>>>(p, magic, int(rows), int(c0), int(wc), int(n), Z,
+                                                      ld, flags, info, int(cap), rho2, lo_state, NT,
+                                                      Gpiv, Y, base, BpT);
+  GFQ_CUDA(cudaGetLastError());
+  ech_step_update_kernel<<<unsigned((rows + kStepRows - 1) / kStepRows), kStepThreads, 0, s>>>(
+      p, magic, int(rows), int(c0), int(n), Z, ld, NT, Gpiv, rho2, BpT);
+  GFQ_CUDA(cudaGetLastError());
+  count_launch(2);
+}
+
+void ech_panel_plant(std::uint8_t* Y, std::int64_t ldy, const std::int32_t* rho2,
+                     const std::int32_t* info, const std::int32_t* base, cudaStream_t s) {
+  ech_plant_kernel<<<1, 32, 0, s>>>(Y, ldy, rho2, info, base);
+  GFQ_CUDA(cudaGetLastError());
+  count_launch();
+}
+
+void ech_outer_finish(std::uint32_t p, std::uint8_t* Y, std::int64_t ldy, std::int64_t kcols,
+                      std::int32_t* info, std::int64_t cap, std::int32_t* base,
+                      std::int32_t* rmap, std::int64_t col0, cudaStream_t s) {
+  ech_outer_finish_kernel<<<1, 256, 0, s>>>(p, Y, ldy, int(kcols), info, int(cap), base, rmap,
+                                            int(col0));
   GFQ_CUDA(cudaGetLastError());
   count_launch();
 }

@@ -104,6 +104,34 @@ void ech_panel(std::uint32_t p, std::int64_t rows, std::int64_t c0, std::int64_t
                std::int32_t* info, std::int64_t cap, std::uint8_t* G, std::int64_t ldg,
                std::int32_t* rho2, cudaStream_t s);
 
+// Blocked (two-level) device ECH.  An outer panel of up to 256 columns is
+// eliminated in a scratch Z = [X | Y] (X = the panel's columns of Aug, Y
+// zero) by 32-wide ech_panel steps; after each step ech_panel_plant sets
+// Y[rho2[q], slot] = 1 for the step's new pivots (slot = pivot number -
+// *base), so the step's update carries Y along and Y ends as L.e_P for the
+// outer panel's row operator L = I + Gout.S_P.  ech_outer_finish turns Y
+// into Gout (subtracts the planted units), writes rmap[t] = the t-th new
+// pivot row (-1 past the last) for kcols slots and advances *base to the
+// rank (and shifts the panel's recorded pivot columns by col0, the outer
+// panel's first column: the steps record scratch-local columns); the caller gathers Bt = Aug[rmap, right of the panel] and applies
+// the trailing Aug[:, right] += Gout.Bt as ONE deep-K contraction on K1.
+// One 32-wide step of an outer panel, as two launches: the pivot chain
+// (one CTA; writes rho2 / info / flags, plants the step's Y units, and
+// leaves NT, Gpiv and the transposed pivot rows BpT in step_scratch,
+// ech_step_scratch_bytes) and the row-parallel update of Z columns
+// [c0, c0 + n) (n a multiple of 16, <= 512; Z 16-byte aligned) with dp4a.
+// Same result as ech_panel + ech_panel_plant + gather + K1 on those columns.
+constexpr std::int64_t ech_step_scratch_bytes() { return 2 * 32 * 32 + 512 * 32; }
+void ech_step(std::uint32_t p, std::int64_t rows, std::int64_t c0, std::int64_t wc, std::int64_t n,
+              std::uint8_t* Z, std::int64_t ld, std::uint8_t* flags, std::int32_t* info,
+              std::int64_t cap, std::int32_t* rho2, std::uint8_t* step_scratch, std::uint8_t* Y,
+              const std::int32_t* base, cudaStream_t s);
+void ech_panel_plant(std::uint8_t* Y, std::int64_t ldy, const std::int32_t* rho2,
+                     const std::int32_t* info, const std::int32_t* base, cudaStream_t s);
+void ech_outer_finish(std::uint32_t p, std::uint8_t* Y, std::int64_t ldy, std::int64_t kcols,
+                      std::int32_t* info, std::int64_t cap, std::int32_t* base,
+                      std::int32_t* rmap, std::int64_t col0, cudaStream_t s);
+
 // GF(2) block ECH in one launch (rows <= 1024, cols + rows <= 8192): the
 // reduced [W | T] is written to Out (rows x (cols + rows) u8) and the pivots
 // to info = [rank, cols[cap], rows[cap]].  scratch holds

@@ -878,6 +878,11 @@ def set_ech_base(n: int):
     _check(lib().gfq_set_ech_base(n))
 
 
+def set_ech_outer(width: int):
+    """Outer panel width of the two-level device ECH (-1 auto, 0 one level)."""
+    _check(lib().gfq_set_ech_outer(width))
+
+
 def set_ech_mode(mode: int):
     """0 = device panel Gauss-Jordan (default), 1 = reference split/combine recursion."""
     _check(lib().gfq_set_ech_mode(mode))

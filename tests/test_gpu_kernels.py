@@ -243,6 +243,34 @@ def test_ech_panel_window_fallbacks(G, p):
     check_ech(G, p, low, G.ech(f, low))
 
 
+@pytest.mark.parametrize("p", [2, 3, 251])
+@pytest.mark.parametrize("outer", [32, 96, 256])
+def test_ech_two_level_outer_panels(G, p, outer):
+    """The two-level device ECH (outer panels eliminated in a scratch with
+    the row operator tracked in Y, one deep-K trailing contraction per outer
+    panel) against the oracle on ragged, rank-deficient, zero-column and
+    sparse-row blocks; outputs must not depend on the outer width."""
+    G.set_ech_mode(0)
+    f = G.FieldSpec(p)
+    rng = np.random.default_rng(outer + p)
+    G.set_ech_outer(outer)
+    try:
+        for t, (m, n) in enumerate([(300, 500), (520, 300), (257, 263), (64, 700), (1100, 300)]):
+            H = rnd(p, m, n, 40 + t)
+            check_ech(G, p, H, G.ech(f, H))
+        H = rnd(p, 400, 330, 50)
+        H[:, rng.choice(330, 90, replace=False)] = 0     # free columns
+        H[rng.choice(400, 150, replace=False)] = 0       # zero rows
+        check_ech(G, p, H, G.ech(f, H))
+        H = rnd(p, 400, 300, 51)
+        H[:120, :100] = 0                               # windows fall back
+        check_ech(G, p, H, G.ech(f, H))
+        low = oracle.random_product_matrix(p, 450, 380, 150, 52)  # rank 150
+        check_ech(G, p, low, G.ech(f, low))
+    finally:
+        G.set_ech_outer(-1)
+
+
 def test_ech_reference_fixtures(G, mode, ref_runs):
     for c in ref_runs["ech"]:
         H = np.array(c["H"], np.uint8).reshape(c["m"], c["n"])
