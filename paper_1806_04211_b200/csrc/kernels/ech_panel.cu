@@ -17,6 +17,7 @@
 // returns to the host until the last panel: the ECH is a fixed launch
 // sequence.
 #include <algorithm>
+#include <cstdio>
 #include <cstdlib>
 
 #include "../common.hpp"
@@ -532,11 +533,6 @@ ech_panel_win_kernel(std::uint32_t p, std::uint32_t magic, int rows, int c0, int
            StepOut{nullptr, nullptr});
 }
 
-// word i (0..3) of a 4-word register group, dynamic index (select tree)
-__device__ __forceinline__ std::uint32_t word4(const std::uint32_t (&w)[4], int i) {
-  return sel(i & 2, sel(i & 1, w[3], w[2]), sel(i & 1, w[1], w[0]));
-}
-
 // Two-level ECH, step part 1 (one CTA of kStepThreads = 8 warps): the
 // pivot chain of the 32-wide step at scratch column c0 on the 64-row window
 // from the first open row (the pivots all lie there when the step's panel
@@ -557,7 +553,31 @@ __device__ __forceinline__ std::uint32_t word4(const std::uint32_t (&w)[4], int 
 //     pivot rows transposed so ech_step_update_kernel contracts over q with
 //     dp4a (n x 32 bytes).
 constexpr int kStepThreads = 256;
-__global__ void __launch_bounds__(kStepThreads)
+// developer timing (GFQ_STEP_DEBUG): globaltimer stamps of the chain phases
+__device__ unsigned long long g_step_stamps[16];
+__device__ __forceinline__ void stamp(int k) {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  if (threadIdx.x == 0) {
+    g_step_stamps[k] = t;
+    g_step_stamps[8 + k] = clock64();
+  }
+}
+// 2 threads per window row (W half, K half), 32 state elements each
+constexpr int kChainThreads = 128;
+__device__ __forceinline__ std::uint32_t pick32(const std::uint32_t (&x)[32], int i) {
+  std::uint32_t a[16], b[8], c[4], d[2];
+#pragma unroll
+  for (int k = 0; k < 16; ++k) a[k] = sel(i & 16, x[k + 16], x[k]);
+#pragma unroll
+  for (int k = 0; k < 8; ++k) b[k] = sel(i & 8, a[k + 8], a[k]);
+#pragma unroll
+  for (int k = 0; k < 4; ++k) c[k] = sel(i & 4, b[k + 4], b[k]);
+#pragma unroll
+  for (int k = 0; k < 2; ++k) d[k] = sel(i & 2, c[k + 2], c[k]);
+  return sel(i & 1, d[1], d[0]);
+}
+__global__ void __launch_bounds__(kChainThreads, 1)
 ech_step_chain_kernel(std::uint32_t p, std::uint32_t magic, int rows, int c0, int wc, int n,
                       std::uint8_t* __restrict__ Z, std::int64_t ld, std::uint8_t* flags,
                       std::int32_t* info, int cap, std::int32_t* rho2, std::int32_t* lo_state,
@@ -566,12 +586,15 @@ ech_step_chain_kernel(std::uint32_t p, std::uint32_t magic, int rows, int c0, in
   extern __shared__ __align__(16) std::uint8_t dsm[];
   __shared__ std::uint8_t invw[256];
   __shared__ int s_lo, s_rold, s_open;
-  __shared__ unsigned cmask[2][8];
-  __shared__ std::uint32_t Pbuf[16];
+  __shared__ __align__(16) float Pcand[2][kChainThreads / 32][64];
+  __shared__ float vcand[2][kChainThreads / 32];
+  __shared__ int cand[2][kChainThreads / 32];
+  __shared__ int colq[kW];
+  __shared__ std::uint8_t chatb[kW][kW];
   __shared__ int wpc[kW], wpr[kW], s_pr[kW];
-  __shared__ __align__(16) std::uint32_t chat[kW][8];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  for (int a = tid; a < 256; a += kStepThreads)
+  stamp(0);
+  for (int a = tid; a < 256; a += kChainThreads)
     invw[a] = (a > 0 && std::uint32_t(a) < p) ? std::uint8_t(powmod(a, p - 2, p)) : 0;
   if (warp == 0) {
     int lo = *lo_state;
@@ -594,74 +617,105 @@ ech_step_chain_kernel(std::uint32_t p, std::uint32_t magic, int rows, int c0, in
   }
   __syncthreads();
   const int lo = s_lo, r_old = s_rold;
-  const int row = tid >> 2, qd = tid & 3, gi = lo + row;
-  std::uint32_t w[4] = {0, 0, 0, 0};
+  const int row = tid >> 1, half = tid & 1, gi = lo + row;
+  // 32 state elements per thread (half 0: the panel bytes, half 1: the
+  // coefficients) as fp32 integers.  Updates are LAZY: x += f.y with f and
+  // the published pivot row y reduced (< p), so after <= 32 columns
+  // x < p + 32 (p-1)^2 < 2^24 stays exact; a value is reduced only when it
+  // is read as the column's factor, published as a pivot row, or output.
+  const float fp = float(p), invp = 1.0f / fp, roff = 0.5f * invp - 0.5f;
+  // x mod p for 0 <= x < 2^24: (x + 0.5) / p lies 0.5/p away from an integer
+  // boundary and the fp32 error of x.invp is below 0.25/p, so rounding
+  // x.invp + (0.5/p - 0.5) to nearest (the 1.5 . 2^23 trick) gives floor(x/p)
+  const auto red = [&](float v) {
+    const float q = (fmaf(v, invp, roff) + 12582912.0f) - 12582912.0f;
+    return fmaf(-fp, q, v);
+  };
+  float x[32];
+#pragma unroll
+  for (int e = 0; e < 32; ++e) x[e] = 0.0f;
   bool open = gi < rows && flags[gi] == 0;
-  if (qd < 2 && gi < rows) {
-    const std::uint8_t* src = Z + std::int64_t(gi) * ld + c0 + 16 * qd;
+  if (half == 0 && gi < rows) {
+    const std::uint8_t* src = Z + std::int64_t(gi) * ld + c0;
     if (wc == kW) {
-      const uint4 a = *reinterpret_cast<const uint4*>(src);
-      w[0] = a.x; w[1] = a.y; w[2] = a.z; w[3] = a.w;
+      const uint4 a = reinterpret_cast<const uint4*>(src)[0], b = reinterpret_cast<const uint4*>(src)[1];
+      const std::uint32_t ww[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
+#pragma unroll
+      for (int e = 0; e < 32; ++e) x[e] = float((ww[e >> 2] >> (8 * (e & 3))) & 0xFFu);
     } else {
 #pragma unroll
-      for (int c = 0; c < 16; ++c)
-        if (16 * qd + c < wc) w[c >> 2] |= std::uint32_t(src[c]) << (8 * (c & 3));
+      for (int e = 0; e < 32; ++e)
+        if (e < wc) x[e] = float(src[e]);
     }
   }
   {
-    const unsigned b = __ballot_sync(0xffffffffu, open && qd == 0);
+    const unsigned b = __ballot_sync(0xffffffffu, open && half == 0);
     if (lane == 0 && b) atomicAdd(&s_open, __popc(b));
   }
   __syncthreads();
   const bool covers_all = s_open == rows - r_old;
+  stamp(1);
   int r2 = 0, ok = 1, myq = -1;
+  // One barrier per column: every warp publishes its first candidate row's
+  // state (reduced, plus the unit at K index r2) before the barrier; after
+  // it all threads pick the first candidate s and, with sc = -1/v_s, apply
+  //   x_i += f_i.(x_s + e_r2),  f_i = v_i.sc (rows i != s),  f_s = sc - 1,
+  // i.e. w_i += f_i.w_s, k_i += f_i.(k_s + e_r2) and w_s = sc.w_s,
+  // k_s = sc.k_s + (sc - 1).e_r2 -- normalising the pivot row first and
+  // eliminating with it, without a second barrier or a branch.
 #pragma unroll 1
   for (int c = 0; c < wc; ++c) {
-    const std::uint32_t mine = (word4(w, (c >> 2) & 3) >> (8 * (c & 3))) & 0xFFu;
-    const std::uint32_t v = __shfl_sync(0xffffffffu, mine, (lane & ~3) | (c >> 4));
-    const unsigned b = __ballot_sync(0xffffffffu, qd == 0 && open && v != 0);
-    if (lane == 0) cmask[c & 1][warp] = b;
-    __syncthreads();
-    int s = -1;
+    const int par = c & 1;
+    std::uint32_t xb[32];
 #pragma unroll
-    for (int ww = 7; ww >= 0; --ww) {
-      const unsigned m = cmask[c & 1][ww];
-      if (m) s = 8 * ww + ((__ffs(m) - 1) >> 2);
+    for (int e = 0; e < 32; ++e) xb[e] = __float_as_uint(x[e]);
+    const float vf = red(__shfl_sync(0xffffffffu, __uint_as_float(pick32(xb, c)), lane & ~1));
+    const int vi = int(vf);
+    const unsigned b = __ballot_sync(0xffffffffu, half == 0 && open && vi != 0);
+    const int wrow = b ? 16 * warp + ((__ffs(b) - 1) >> 1) : 0x7FFFFFFF;
+    if (row == wrow) {
+      float* dst = Pcand[par][warp] + 32 * half;
+#pragma unroll
+      for (int e = 0; e < 8; ++e)
+        reinterpret_cast<float4*>(dst)[e] =
+            make_float4(red(x[4 * e]), red(x[4 * e + 1]), red(x[4 * e + 2]), red(x[4 * e + 3]));
+      if (half == 0) vcand[par][warp] = float(p - invw[vi]);
     }
-    if (s < 0) {
+    __syncwarp();
+    if (lane == 0) {
+      cand[par][warp] = wrow;
+      if (b) Pcand[par][warp][32 + r2] = 1.0f;  // + e_r2 (that coefficient is still 0)
+    }
+    __syncthreads();
+    int s = cand[par][0];
+#pragma unroll
+    for (int w2 = 1; w2 < kChainThreads / 32; ++w2) s = min(s, cand[par][w2]);
+    if (s == 0x7FFFFFFF) {
       if (covers_all) continue;  // a free column (uniform)
       ok = 0;
       break;
     }
-    // K byte of the new pivot's own index r2: quarter 2 + r2 / 16, word (r2 / 4) % 4
-    const int kq = 2 + (r2 >> 4), kwd = (r2 >> 2) & 3, ksh = 8 * (r2 & 3);
-    if (row == s) {
-      const std::uint32_t sc = p - invw[v];
+    const int ws = s >> 4;
+    const float sc = vcand[par][ws];
+    float y[32];
+    {
+      const float4* ps = reinterpret_cast<const float4*>(&Pcand[par][ws][32 * half]);
 #pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        std::uint32_t x = axpy4(0, sc, w[j], p, magic);
-        if (qd == kq && j == kwd) {
-          // + (s - 1) on its own pivot index
-          const std::uint32_t nv = modp(((x >> ksh) & 0xFFu) + sc + p - 1, p, magic);
-          x = (x & ~(0xFFu << ksh)) | (nv << ksh);
-        }
-        Pbuf[4 * qd + j] = x;
+      for (int e = 0; e < 8; ++e) {
+        const float4 t = ps[e];
+        y[4 * e] = t.x; y[4 * e + 1] = t.y; y[4 * e + 2] = t.z; y[4 * e + 3] = t.w;
       }
     }
-    __syncthreads();
+    float f;
     if (row == s) {
-#pragma unroll
-      for (int j = 0; j < 4; ++j) w[j] = Pbuf[4 * qd + j];
+      f = sc - 1.0f;
       open = false;
       myq = r2;
-    } else if (v) {
-#pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        // the pivot's own index bit: coefficient v on pivot r2 (the "+e_q")
-        const std::uint32_t e = (qd == kq && j == kwd) ? (1u << ksh) : 0u;
-        w[j] = axpy4(w[j], v, Pbuf[4 * qd + j] + e, p, magic);
-      }
+    } else {
+      f = red(vf * sc);
     }
+#pragma unroll
+    for (int e = 0; e < 32; ++e) x[e] = fmaf(f, y[e], x[e]);
     if (tid == 0) {
       wpc[r2] = c;
       wpr[r2] = lo + s;
@@ -669,27 +723,31 @@ ech_step_chain_kernel(std::uint32_t p, std::uint32_t magic, int rows, int c0, in
     ++r2;
   }
   __syncthreads();
+  stamp(2);
   if (!ok) {
     panel_full(p, magic, rows, c0, wc, Z, ld, flags, info, cap, nullptr, 0, rho2,
                StepOut{NT, Gpiv});
   } else {
-    if (myq >= 0 && qd >= 2) {
+    if (myq >= 0 && half == 1) {
 #pragma unroll
-      for (int j = 0; j < 4; ++j) chat[myq][4 * (qd - 2) + j] = w[j];
+      for (int e = 0; e < 32; ++e) chatb[myq][e] = std::uint8_t(int(red(x[e])));
     }
+    if (tid < kW) colq[tid] = -1;
+    __syncthreads();
+    if (tid < r2) colq[wpc[tid]] = tid;
     __syncthreads();
     // NT[t][wpc[q]] = (I + Ĉ)[q][t]; Gpiv[q] = ĉ_q
-    for (int e = tid; e < kW * kW; e += kStepThreads) {
+    for (int e = tid; e < kW * kW; e += kChainThreads) {
       const int t = e / kW, c = e % kW;
+      const int q = colq[c];
       std::uint32_t v = 0;
-      for (int q = 0; q < r2; ++q)
-        if (wpc[q] == c) {
-          v = (chat[q][t >> 2] >> (8 * (t & 3))) & 0xFFu;
-          if (t == q) v = v + 1 == p ? 0 : v + 1;
-        }
+      if (q >= 0) {
+        v = chatb[q][t];
+        if (t == q) v = v + 1 == p ? 0 : v + 1;
+      }
       NT[e] = std::uint8_t(v);
-      const int q = e / kW, tt = e % kW;
-      Gpiv[e] = q < r2 ? std::uint8_t((chat[q][tt >> 2] >> (8 * (tt & 3))) & 0xFFu) : 0;
+      const int qq = e / kW;
+      Gpiv[e] = qq < r2 ? chatb[qq][e % kW] : 0;
     }
     if (tid < kW) rho2[tid] = tid < r2 ? wpr[tid] : -1;
     if (tid < r2) {
@@ -700,6 +758,7 @@ ech_step_chain_kernel(std::uint32_t p, std::uint32_t magic, int rows, int c0, in
     if (tid == 0) info[0] = r_old + r2;
   }
   __syncthreads();
+  stamp(3);
   if (tid < kW) {
     const int r = rho2[tid];
     s_pr[tid] = r;
@@ -709,7 +768,7 @@ ech_step_chain_kernel(std::uint32_t p, std::uint32_t magic, int rows, int c0, in
   // stage the pivot rows (32 x n, 16-byte loads) in shared memory, then
   // write them transposed
   std::uint8_t* Bs = dsm;  // 32 x n
-  for (int e = tid; e < kW * (n / 16); e += kStepThreads) {
+  for (int e = tid; e < kW * (n / 16); e += kChainThreads) {
     const int q = e / (n / 16), ch = e % (n / 16);
     const int r = s_pr[q];
     uint4 v = make_uint4(0, 0, 0, 0);
@@ -717,7 +776,7 @@ ech_step_chain_kernel(std::uint32_t p, std::uint32_t magic, int rows, int c0, in
     reinterpret_cast<uint4*>(Bs + q * n)[ch] = v;
   }
   __syncthreads();
-  for (int j = tid; j < n; j += kStepThreads) {
+  for (int j = tid; j < n; j += kChainThreads) {
     std::uint32_t o[8] = {0, 0, 0, 0, 0, 0, 0, 0};
 #pragma unroll
     for (int q = 0; q < kW; ++q) o[q >> 2] |= std::uint32_t(Bs[q * n + j]) << (8 * (q & 3));
@@ -725,6 +784,8 @@ ech_step_chain_kernel(std::uint32_t p, std::uint32_t magic, int rows, int c0, in
     dst[0] = make_uint4(o[0], o[1], o[2], o[3]);
     dst[1] = make_uint4(o[4], o[5], o[6], o[7]);
   }
+  __syncthreads();
+  stamp(4);
 }
 
 // Two-level ECH, step part 2: Z[i][c0 + j] += G[i] . Bp[:, j] for every row
@@ -741,41 +802,41 @@ ech_step_update_kernel(std::uint32_t p, std::uint32_t magic, int rows, int c0, i
                        const std::uint8_t* __restrict__ NT, const std::uint8_t* __restrict__ Gpiv,
                        const std::int32_t* __restrict__ rho2, const std::uint8_t* __restrict__ BpT) {
   __shared__ __align__(16) std::uint32_t sB[kStepMaxN * 8];
+  __shared__ __align__(16) std::uint32_t sNT[kW * 8];
   __shared__ std::uint32_t sG[kStepRows][9];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int i0 = blockIdx.x * kStepRows;
   for (int e = tid; e < n * 2; e += kStepThreads)
     reinterpret_cast<uint4*>(sB)[e] = reinterpret_cast<const uint4*>(BpT)[e];
-  if (warp == 0) {
+  if (tid < kW * 2) reinterpret_cast<uint4*>(sNT)[tid] = reinterpret_cast<const uint4*>(NT)[tid];
+  __syncthreads();
+  {
+    // warp w forms G[i][4w .. 4w+3] of the CTA's 32 rows (lane = row)
     const int i = i0 + lane;
     const int r = rho2[lane];
     int myq = -1;
 #pragma unroll
     for (int u = 0; u < kW; ++u)
       if (__shfl_sync(0xffffffffu, r, u) == i) myq = u;
-    std::uint32_t g[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    std::uint32_t gw = 0;
     if (i < rows && myq >= 0) {
-      const uint4* src = reinterpret_cast<const uint4*>(Gpiv + myq * kW);
-      const uint4 a = src[0], b = src[1];
-      g[0] = a.x; g[1] = a.y; g[2] = a.z; g[3] = a.w; g[4] = b.x; g[5] = b.y; g[6] = b.z; g[7] = b.w;
+      gw = reinterpret_cast<const std::uint32_t*>(Gpiv + myq * kW)[warp];
     } else if (i < rows) {
       const uint4* src = reinterpret_cast<const uint4*>(Z + std::int64_t(i) * ld + c0);
       const uint4 a = src[0], b = src[1];
-      const std::uint32_t seg[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
-      const uint4* nt4 = reinterpret_cast<const uint4*>(NT);
-#pragma unroll 4
-      for (int t = 0; t < kW; ++t) {
-        const uint4 x = nt4[2 * t], y = nt4[2 * t + 1];
+#pragma unroll
+      for (int tt = 0; tt < 4; ++tt) {
+        const uint4* nt4 = reinterpret_cast<const uint4*>(sNT + (4 * warp + tt) * 8);
+        const uint4 x = nt4[0], y = nt4[1];
         std::uint32_t acc = 0;
-        acc = __dp4a(seg[0], x.x, acc); acc = __dp4a(seg[1], x.y, acc);
-        acc = __dp4a(seg[2], x.z, acc); acc = __dp4a(seg[3], x.w, acc);
-        acc = __dp4a(seg[4], y.x, acc); acc = __dp4a(seg[5], y.y, acc);
-        acc = __dp4a(seg[6], y.z, acc); acc = __dp4a(seg[7], y.w, acc);
-        g[t >> 2] |= modp(acc, p, magic) << (8 * (t & 3));
+        acc = __dp4a(a.x, x.x, acc); acc = __dp4a(a.y, x.y, acc);
+        acc = __dp4a(a.z, x.z, acc); acc = __dp4a(a.w, x.w, acc);
+        acc = __dp4a(b.x, y.x, acc); acc = __dp4a(b.y, y.y, acc);
+        acc = __dp4a(b.z, y.z, acc); acc = __dp4a(b.w, y.w, acc);
+        gw |= modp(acc, p, magic) << (8 * tt);
       }
     }
-#pragma unroll
-    for (int w = 0; w < 8; ++w) sG[lane][w] = g[w];
+    sG[lane][warp] = gw;
   }
   __syncthreads();
   const int i = i0 + lane;
@@ -1176,6 +1237,14 @@ void ech_step(std::uint32_t p, std::int64_t rows, std::int64_t c0, std::int64_t 
   if (!attr) {
     GFQ_CUDA(cudaFuncSetAttribute(ech_step_chain_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   kPanelSmem));
+    // both step kernels ask for the largest shared-memory carveout so the SM
+    // does not reconfigure L1 / shared memory between them
+    if (!std::getenv("GFQ_NO_CARVEOUT")) {
+      GFQ_CUDA(cudaFuncSetAttribute(ech_step_chain_kernel,
+                                    cudaFuncAttributePreferredSharedMemoryCarveout, 100));
+      GFQ_CUDA(cudaFuncSetAttribute(ech_step_update_kernel,
+                                    cudaFuncAttributePreferredSharedMemoryCarveout, 100));
+    }
     attr = true;
   }
   const std::uint32_t magic = static_cast<std::uint32_t>((0x100000000ULL / p) + 1);
@@ -1183,13 +1252,26 @@ void ech_step(std::uint32_t p, std::int64_t rows, std::int64_t c0, std::int64_t 
   std::uint8_t* NT = step_scratch;
   std::uint8_t* Gpiv = step_scratch + kW * kW;
   std::uint8_t* BpT = step_scratch + 2 * kW * kW;
-  ech_step_chain_kernel<<<1, kStepThreads, smem, s>>>(p, magic, int(rows), int(c0), int(wc), int(n), Z,
+  ech_step_chain_kernel<<<1, kChainThreads, smem, s>>>(p, magic, int(rows), int(c0), int(wc), int(n), Z,
                                                       ld, flags, info, int(cap), rho2, lo_state, NT,
                                                       Gpiv, Y, base, BpT);
   GFQ_CUDA(cudaGetLastError());
   ech_step_update_kernel<<<unsigned((rows + kStepRows - 1) / kStepRows), kStepThreads, 0, s>>>(
       p, magic, int(rows), int(c0), int(n), Z, ld, NT, Gpiv, rho2, BpT);
   GFQ_CUDA(cudaGetLastError());
+  static int dbg = std::getenv("GFQ_STEP_DEBUG") ? std::atoi(std::getenv("GFQ_STEP_DEBUG")) : 0;
+  if (dbg > 0) {
+    --dbg;
+    unsigned long long st[16];
+    GFQ_CUDA(cudaStreamSynchronize(s));
+    GFQ_CUDA(cudaMemcpyFromSymbol(st, g_step_stamps, sizeof st));
+    std::fprintf(stderr,
+                 "ech_step rows %lld c0 %lld: setup %.2f chain %.2f outputs %.2f bpt %.2f us; "
+                 "chain %llu cycles (%.2f GHz)\n",
+                 (long long)rows, (long long)c0, (st[1] - st[0]) * 1e-3, (st[2] - st[1]) * 1e-3,
+                 (st[3] - st[2]) * 1e-3, (st[4] - st[3]) * 1e-3, st[10] - st[9],
+                 double(st[10] - st[9]) / double(st[2] - st[1]));
+  }
   count_launch(2);
 }
 

@@ -1,6 +1,8 @@
-"""Run single device jobs once (for ncu launch lists): python tools/one_ech.py [n] [p] [mode]"""
+"""Run single device jobs once (for ncu launch lists): python tools/one_ech.py [n] [p] [mode]
+--reps R: run R times; --time: one untimed warm-up, then print the mean wall ms of R calls."""
 import os
 import sys
+import time
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_1806_04211_b200 import gfrref as G  # noqa: E402
@@ -13,7 +15,12 @@ G.set_ech_mode(mode)
 f = G.FieldSpec(p)
 H = G.random_matrix(f, n, n, 7)
 reps = int(sys.argv[sys.argv.index("--reps") + 1]) if "--reps" in sys.argv else 1
+if "--time" in sys.argv:
+    G.ech(f, H)
+    G.synchronize()
+t0 = time.perf_counter()
 for _ in range(reps):
     e = G.ech(f, H)
 G.synchronize()
-print("rank", e.rank())
+dt = (time.perf_counter() - t0) / reps
+print("rank", e.rank(), "ms %.3f" % (1e3 * dt) if "--time" in sys.argv else "")
