@@ -63,6 +63,7 @@ struct ClArgs {
   // for the u-th non-pivot row (QK), non-pivot columns (GC)
   std::uint32_t* P;
   std::int16_t *RS, *QK, *GC;
+  int serial;  // developer experiment (GFQ_GF2_SERIAL): leader updates after its chain
 };
 
 // leader scratch of the extraction epilogue (pivot-column flags, bytes)
@@ -97,6 +98,7 @@ __global__ void __launch_bounds__(kThreads, 1) ech_gf2_cluster_kernel(ClArgs g) 
   // the current panel's pivots (the leader's copy is authoritative)
   __shared__ int pc[32], pr[32], r2_sh, ok_sh, lo_sh, npiv_sh;
   __shared__ std::uint32_t pcoef[32], ntab[128];
+  __shared__ int colq[32], qof[kStripe];
   __shared__ std::uint32_t nomw[2][32], nomc[2][32];
   __shared__ unsigned best[3];
 
@@ -112,7 +114,7 @@ __global__ void __launch_bounds__(kThreads, 1) ech_gf2_cluster_kernel(ClArgs g) 
     return wc == 32 ? 0xFFFFFFFFu : ((1u << wc) - 1u);
   };
   auto stamp = [&](int k, int ph) {
-    if (g.dbg && cr == 0 && tid == 0 && k < 8) g.dbg[k * 16 + ph] = gtime();
+    if (g.dbg && cr == 0 && tid == 0 && k >= 0 && k < 8) g.dbg[k * 16 + ph] = gtime();
   };
 
   // ---- pack my stripe of [H | I] (warp per row, lane per word)
@@ -168,79 +170,79 @@ __global__ void __launch_bounds__(kThreads, 1) ech_gf2_cluster_kernel(ClArgs g) 
       lo += 32;
     }
     if (lo > rows) lo = rows;
+    stamp(k - 1, 9);
+    // row layout: lane l holds window rows lo + l and lo + 32 + l as their
+    // panel word w and coefficient word kk (bit q: pivot q's ORIGINAL row
+    // has been added).  Per column: two ballots pick the first open row
+    // with the bit, one shuffle pair broadcasts its (w, kk), and every other
+    // window row with the bit adds it (kk ^= kk_s ^ e_q) -- no barriers, no
+    // shared memory on the chain.
     const int i0 = lo + lane, i1 = lo + 32 + lane;
-    const std::uint32_t w0 = i0 < 1024 ? orig[i0] : 0u, w1 = i1 < 1024 ? orig[i1] : 0u;
-    const bool p0 = i0 >= rows || fl[i0] != 0, p1 = i1 >= rows || fl[i1] != 0;
-    std::uint64_t cmask = 0, kmask = 0;
-#pragma unroll
-    for (int q = 0; q < 32; ++q) {
-      const unsigned lo32 = __ballot_sync(0xffffffffu, (w0 >> q) & 1u);
-      const unsigned hi32 = __ballot_sync(0xffffffffu, (w1 >> q) & 1u);
-      if (lane == q) cmask = std::uint64_t(lo32) | (std::uint64_t(hi32) << 32);
-    }
-    std::uint64_t piv = std::uint64_t(__ballot_sync(0xffffffffu, p0)) |
-                        (std::uint64_t(__ballot_sync(0xffffffffu, p1)) << 32);
+    std::uint32_t w0 = i0 < rows ? orig[i0] : 0u, w1 = i1 < rows ? orig[i1] : 0u;
+    bool p0 = i0 >= rows || fl[i0] != 0, p1 = i1 >= rows || fl[i1] != 0;
+    std::uint32_t k0 = 0, k1 = 0;
+    const int open_in = __popc(__ballot_sync(0xffffffffu, !p0)) + __popc(__ballot_sync(0xffffffffu, !p1));
     // the window holds every non-pivotal row: a column without a candidate
     // is then a free column, not a reason to fall back
-    const bool covers_all = 64 - __popcll(piv) == rows - npiv_sh;
-    // Four columns per round: their current masks are broadcast together,
-    // every lane derives the four pivots from them in registers (each
-    // pivot's elimination applied to the later columns of the round), then
-    // applies the four eliminations to its own column and coefficient mask.
-    int r2 = 0, ok = 1;
-    for (int c0 = 0; c0 < wc && ok; c0 += 4) {
-      const int nt = wc - c0 < 4 ? wc - c0 : 4;
-      std::uint64_t bc[4], ss[4];
-      int pv[4];
-#pragma unroll
-      for (int t = 0; t < 4; ++t) bc[t] = __shfl_sync(0xffffffffu, cmask, (c0 + t) & 31);
-      int np = 0;
-#pragma unroll
-      for (int t = 0; t < 4; ++t) {
-        pv[t] = -1;
-        ss[t] = 0;
-        if (t < nt && ok) {
-          const std::uint64_t cand = bc[t] & ~piv;
-          if (!cand) {
-            if (!covers_all) ok = 0;  // a column without a window candidate: uniform
-          } else {
-            const int p = __ffsll(static_cast<long long>(cand)) - 1;
-            pv[t] = p;
-            ss[t] = bc[t] & ~(std::uint64_t(1) << p);
-            piv |= std::uint64_t(1) << p;
-#pragma unroll
-            for (int u = t + 1; u < 4; ++u)
-              if ((bc[u] >> p) & 1u) bc[u] ^= ss[t];
-            ++np;
-          }
-        }
+    const bool covers_all = open_in == rows - npiv_sh;
+    stamp(k - 1, 10);
+    const long long ck0 = clock64();
+    int r2 = 0, ok = 1, q0 = -1, q1 = -1, mpc = 0, mpr = 0;
+#pragma unroll 1
+    for (int c = 0; c < wc; ++c) {
+      const unsigned b0 = __ballot_sync(0xffffffffu, !p0 && ((w0 >> c) & 1u));
+      const unsigned b1 = __ballot_sync(0xffffffffu, !p1 && ((w1 >> c) & 1u));
+      if (!(b0 | b1)) {
+        if (covers_all) continue;
+        ok = 0;
+        break;
       }
-      int qn = r2;
-#pragma unroll
-      for (int t = 0; t < 4; ++t) {
-        if (pv[t] < 0) continue;
-        const int p = pv[t], q = qn++;
-        if ((cmask >> p) & 1u) cmask ^= ss[t];
-        if (lane < q && ((kmask >> p) & 1u)) kmask ^= ss[t];
-        if (lane == q) kmask = ss[t];
-        if (lane == 0) {
-          pc[q] = c0 + t;
-          pr[q] = lo + p;
-        }
+      const bool hi = b0 == 0;
+      const int sl = __ffs(hi ? b1 : b0) - 1;
+      const std::uint32_t pw = __shfl_sync(0xffffffffu, hi ? w1 : w0, sl);
+      const std::uint32_t pk = __shfl_sync(0xffffffffu, hi ? k1 : k0, sl) ^ (1u << r2);
+      const bool me0 = !hi && lane == sl, me1 = hi && lane == sl;
+      if (!me0 && ((w0 >> c) & 1u)) {
+        w0 ^= pw;
+        k0 ^= pk;
       }
-      r2 += np;
+      if (!me1 && ((w1 >> c) & 1u)) {
+        w1 ^= pw;
+        k1 ^= pk;
+      }
+      if (me0) {
+        p0 = true;
+        q0 = r2;
+      }
+      if (me1) {
+        p1 = true;
+        q1 = r2;
+      }
+      if (lane == r2) {  // kept in registers: no shared stores on the chain
+        mpc = c;
+        mpr = lo + (hi ? 32 : 0) + sl;
+      }
+      ++r2;
+    }
+    if (lane < r2) {
+      pc[lane] = mpc;
+      pr[lane] = mpr;
     }
     __syncwarp();
-    if (ok)
-      for (int t = 0; t < r2; ++t) {
-        const unsigned cf = __ballot_sync(0xffffffffu, (kmask >> (pr[t] - lo)) & 1u);
-        if (lane == t) pcoef[t] = cf ^ (1u << t);
-      }
+    stamp(k - 1, 11);
+    if (g.dbg && cr == 0 && tid == 0 && k >= 1 && k < 9) g.dbg[(k - 1) * 16 + 13] = clock64() - ck0;
+    // a pivot row's multiplier word: its own bit plus the pivots added to it
+    if (ok) {
+      if (q0 >= 0) pcoef[q0] = k0 ^ (1u << q0);
+      if (q1 >= 0) pcoef[q1] = k1 ^ (1u << q1);
+    }
+    __syncwarp();
     if (lane == 0) {
       ok_sh = ok;
       r2_sh = r2;
       lo_sh = lo;
     }
+    stamp(k - 1, 12);
   };
   // CTA-wide chain over all rows (warps 0..7, 4 rows per lane); leader CTA,
   // every thread calls it
@@ -363,12 +365,24 @@ __global__ void __launch_bounds__(kThreads, 1) ech_gf2_cluster_kernel(ClArgs g) 
     stamp(k, 0);
     // 1. G for my rows, pivot rows, tables
     if (r2 > 0) {
+      // column -> pivot index of the panel, my row -> pivot index (O(1)
+      // lookups below instead of loops over the r2 pivots)
+      if (tid < 32) colq[tid] = -1;
+      if (tid < kStripe) qof[tid] = -1;
+      __syncthreads();
+      if (tid < r2) {
+        colq[pc[tid]] = tid;
+        const int li = pr[tid] - row0;
+        if (li >= 0 && li < kStripe) qof[li] = tid;
+      }
+      __syncthreads();
       if (tid < 128) {
         const int kq = tid >> 4, m = tid & 15;
         std::uint32_t v = 0;
-        for (int q = 0; q < r2; ++q) {
-          const int cq = pc[q];
-          if ((cq >> 2) == kq && ((m >> (cq & 3)) & 1)) v ^= pcoef[q];
+#pragma unroll
+        for (int b2 = 0; b2 < 4; ++b2) {
+          const int q = colq[4 * kq + b2];
+          if (((m >> b2) & 1) && q >= 0) v ^= pcoef[q];
         }
         ntab[tid] = v;
       }
@@ -384,8 +398,8 @@ __global__ void __launch_bounds__(kThreads, 1) ech_gf2_cluster_kernel(ClArgs g) 
         std::uint32_t gv = 0;
 #pragma unroll
         for (int kq = 0; kq < 8; ++kq) gv ^= ntab[16 * kq + ((ow >> (4 * kq)) & 15u)];
-        for (int q = 0; q < r2; ++q)
-          if (pr[q] == row0 + li) gv = pcoef[q] ^ (1u << q);
+        const int q = qof[li];
+        if (q >= 0) gv = pcoef[q] ^ (1u << q);
         gl[li] = gv;
       }
       if (use_tab)
@@ -440,13 +454,18 @@ __global__ void __launch_bounds__(kThreads, 1) ech_gf2_cluster_kernel(ClArgs g) 
       window_chain(k + 1);
       stamp(k, 4);
     }
+    if (g.serial && cr == 0 && has_next) __syncthreads();
     // the rest of panel k's update: word wi and words wi+2.. (the leader's
     // warp 0 is busy with the chain, so its rows go to warps 1..31)
     if (r2 > 0) {
-      const int w_first = cr == 0 && has_next ? 1 : 0;
-      const int nwarps = 32 - w_first;
-      if (warp >= w_first)
-        for (int li = warp - w_first; li < nloc; li += nwarps)
+      // in the leader the chain warp (warp 0, SMSP 0) would get one issue
+      // slot in eight next to the other SMSP-0 warps, so SMSP 0's other
+      // warps sit this phase out and warps on SMSPs 1-3 share the rows
+      const bool lead = cr == 0 && has_next;
+      const int nwarps = lead ? 24 : 32;
+      const int widx = lead ? warp - (warp >> 2) - 1 : warp;
+      if (!lead || (warp & 3) != 0)
+        for (int li = widx; li < nloc; li += nwarps)
           for (int t = lane; t < nw; t += 32) {
             const int w = wi + t;
             if (has_next && w == wi + 1) continue;
@@ -612,7 +631,7 @@ bool ech_gf2_cluster(std::int64_t rows, std::int64_t cols, const std::uint8_t* H
   if (debug && !dbg) GFQ_CUDA(cudaMalloc(&dbg, 9 * 16 * sizeof(unsigned long long)));
   ClArgs g{int(rows), int(cols), int(Wd), int(cap), H, ldh, Out, ldo, info, debug ? dbg : nullptr,
             ex ? ex->P : nullptr, ex ? ex->RS : nullptr, ex ? ex->QK : nullptr,
-            ex ? ex->GC : nullptr};
+            ex ? ex->GC : nullptr, std::getenv("GFQ_GF2_SERIAL") ? 1 : 0};
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(kCl);
   cfg.blockDim = dim3(kThreads);
@@ -648,6 +667,12 @@ bool ech_gf2_cluster(std::int64_t rows, std::int64_t cols, const std::uint8_t* H
 
       std::fprintf(stderr, " | zwait %lld chain %lld", static_cast<long long>(dbg[k * 16 + 8] - dbg[k * 16 + 3]),
                    static_cast<long long>(dbg[k * 16 + 4] - dbg[k * 16 + 8]));
+      std::fprintf(stderr, " | rounds %lld cyc", static_cast<long long>(dbg[k * 16 + 13]));
+      std::fprintf(stderr, " | scan %lld masks %lld rounds %lld coef %lld",
+                   static_cast<long long>(dbg[k * 16 + 9] - dbg[k * 16 + 8]),
+                   static_cast<long long>(dbg[k * 16 + 10] - dbg[k * 16 + 9]),
+                   static_cast<long long>(dbg[k * 16 + 11] - dbg[k * 16 + 10]),
+                   static_cast<long long>(dbg[k * 16 + 12] - dbg[k * 16 + 11]));
       std::fprintf(stderr, " | total %lld ns\n",
                    static_cast<long long>(dbg[(k + 1) * 16] - dbg[k * 16]));
     }
