@@ -1,7 +1,10 @@
 // chief.cpp -- chop, plan, run, assemble (see chief.hpp).
 #include "chief.hpp"
 
+#include <algorithm>
+#include <cstdlib>
 #include <numeric>
+#include <string>
 #include <stdexcept>
 
 #include "../kernels/kernels.hpp"
@@ -251,10 +254,38 @@ PlanHandles build_plan_fused(TaskGraph& graph, const Mat& C, const FieldSpec& fi
     }
   }
 
+  // Task priorities (lower first; only the GPU schedule depends on them).
+  // The reference keys Step 1 by i + j (src/chief.cpp:116): a wavefront
+  // over anti-diagonals.  On the GPU the diagonal ClearDowns (the block
+  // ECHs) cost several times a below- or above-diagonal step, so a task's
+  // deadline is the diagonal step d = max(i, j) it feeds minus the chain of
+  // cheap steps still between it and that ECH: key = w.max(i, j) +
+  // min(i, j) (w = GFQ_PRIORITY_W, default 3; w = 1 is the reference's
+  // i + j).  UpdateRow(i, j, k) takes the key of the ClearDown(i, k) it
+  // feeds, the wide UpdateRow k = j + 2; the transform tasks (consumed only
+  // by Steps 2-3) follow the chain tasks of the same key; Steps 2-3 last.
+  static const int w_pri = [] {
+    const char* v = std::getenv("GFQ_PRIORITY_W");
+    const int w = v ? std::atoi(v) : 3;
+    return w >= 1 && w <= 16 ? w : 3;
+  }();
+  const auto key = [&](std::size_t i, std::size_t j) {
+    return std::int32_t(std::size_t(w_pri) * std::max(i, j) + std::min(i, j));
+  };
+  const auto pchain = [&](std::size_t i, std::size_t j, std::size_t kt) {
+    return w_pri == 1 ? std::int32_t(i + j) : key(i, kt) * 4;
+  };
+  const auto ptrafo = [&](std::size_t i, std::size_t j) {
+    return w_pri == 1 ? std::int32_t(i + j) : key(i, j) * 4 + 2;
+  };
+  const auto plate = [&](std::size_t v) {
+    return w_pri == 1 ? std::int32_t(v) : std::int32_t((1 << 20) + v);
+  };
   // Step 1
   for (std::size_t j = 0; j < b; ++j) {
     for (std::size_t i = 0; i < a; ++i) {
-      const std::int32_t pri = std::int32_t(i + j);
+      const std::int32_t pri = pchain(i, j, j), pri_t = ptrafo(i, j);
+      const std::int32_t pri_u = pchain(i, j, j + 1), pri_w = pchain(i, j, j + 2);
       const auto sD = [&](std::size_t v) { return e.slot(K::D, j, 0, 0, v); };
       const std::int32_t sA = e.slot(K::A, i, j, 0, 0);
       const std::int32_t sC = e.slot(K::C, i, j, 0, j);
@@ -263,29 +294,29 @@ PlanHandles build_plan_fused(TaskGraph& graph, const Mat& C, const FieldSpec& fi
       else
         e.node(T::ClearDown, std::int32_t(i), std::int32_t(j), -1, pri, {sC}, {sD(i), sA});
       if (j > 0)
-        e.node(T::Extend, std::int32_t(i), std::int32_t(j), -1, pri,
+        e.node(T::Extend, std::int32_t(i), std::int32_t(j), -1, pri_t,
                {sA, e.slot(K::E, i, 0, 0, j - 1)}, {e.slot(K::E, i, 0, 0, j)});
       else
-        e.node(T::Extend, std::int32_t(i), std::int32_t(j), -1, pri, {sA},
+        e.node(T::Extend, std::int32_t(i), std::int32_t(j), -1, pri_t, {sA},
                {e.slot(K::E, i, 0, 0, j)});
       if (j + 1 < b) {
         const std::int32_t panel = e.slot(K::CW, i, j + 1, 0, j);
         const std::int32_t cout = e.slot(K::C, i, j + 1, 0, j + 1);
         const std::int32_t bout = e.slot(K::B, j, j + 1, 0, i);
         if (i > 0)
-          e.node(T::UpdateRow, std::int32_t(i), std::int32_t(j), std::int32_t(j + 1), pri,
+          e.node(T::UpdateRow, std::int32_t(i), std::int32_t(j), std::int32_t(j + 1), pri_u,
                  {sA, panel, e.slot(K::B, j, j + 1, 0, i - 1)}, {cout, bout});
         else
-          e.node(T::UpdateRow, std::int32_t(i), std::int32_t(j), std::int32_t(j + 1), pri,
+          e.node(T::UpdateRow, std::int32_t(i), std::int32_t(j), std::int32_t(j + 1), pri_u,
                  {sA, panel}, {cout, bout});
         if (j + 2 < b) {
           const std::int32_t pout = e.slot(K::CW, i, j + 2, 0, j + 1);
           const std::int32_t bwout = e.slot(K::BW, j, j + 2, 0, i);
           if (i > 0)
-            e.node(T::UpdateRowW, std::int32_t(i), std::int32_t(j), std::int32_t(j + 2), pri,
+            e.node(T::UpdateRowW, std::int32_t(i), std::int32_t(j), std::int32_t(j + 2), pri_w,
                    {sA, panel, e.slot(K::BW, j, j + 2, 0, i - 1)}, {pout, bwout});
           else
-            e.node(T::UpdateRowW, std::int32_t(i), std::int32_t(j), std::int32_t(j + 2), pri,
+            e.node(T::UpdateRowW, std::int32_t(i), std::int32_t(j), std::int32_t(j + 2), pri_w,
                    {sA, panel}, {pout, bwout});
         }
       }
@@ -297,7 +328,7 @@ PlanHandles build_plan_fused(TaskGraph& graph, const Mat& C, const FieldSpec& fi
           tr.c0 = std::int32_t(i);
           tr.c1 = std::int32_t(j);
           tr.c2 = std::int32_t(i);
-          tr.priority = pri;
+          tr.priority = pri_t;
           tr.in[tr.n_in++] = sA;
           tr.in[tr.n_in++] = e.slot(K::E, i, 0, 0, j);
           if (j > 0) tr.in[tr.n_in++] = e.slot(K::K, i, i, 0, j - 1);
@@ -312,7 +343,7 @@ PlanHandles build_plan_fused(TaskGraph& graph, const Mat& C, const FieldSpec& fi
           if (j > 0) in.push_back(e.slot(K::KW, i, 0, 0, j - 1));
           if (i >= 2) in.push_back(e.slot(K::MT, j, 0, 0, i - 1));
           in.push_back(e.slot(K::M, j, i - 1, 0, 0));
-          e.node(T::UpdateRowTrafoW, std::int32_t(i), std::int32_t(j), -1, pri, in,
+          e.node(T::UpdateRowTrafoW, std::int32_t(i), std::int32_t(j), -1, pri_t, in,
                  {e.slot(K::KW, i, 0, 0, j), e.slot(K::MT, j, 0, 0, i)});
         }
       }
@@ -324,17 +355,17 @@ PlanHandles build_plan_fused(TaskGraph& graph, const Mat& C, const FieldSpec& fi
       for (std::size_t h = 0; h < a; ++h) {
         const bool part = h + 1 < a;
         e.node(T::RowLengthen, part ? std::int32_t(h) : -1, std::int32_t(j), std::int32_t(h),
-               std::int32_t(a + b - 1),
+               plate(a + b - 1),
                {part ? e.slot(K::MT, j, 0, 0, a - 1) : e.slot(K::M, j, a - 1, 0, 0),
                 e.slot(K::E, h, 0, 0, j), e.slot(K::E, h, 0, 0, b - 1)},
                {e.slot(K::M, j, h, 0, a - h)});
       }
   // Step 3
   for (std::size_t k = 0; k < b; ++k)
-    e.node(T::Copy, -1, std::int32_t(k), -1, std::int32_t(a + b + (b - 1 - k)),
+    e.node(T::Copy, -1, std::int32_t(k), -1, plate(a + b + (b - 1 - k)),
            {e.slot(K::D, k, 0, 0, a - 1)}, {e.slot(K::R, k, k, 0, 0)});
   for (std::size_t k = b; k-- > 1;) {
-    const std::int32_t pri = std::int32_t(a + b + (b - 1 - k));
+    const std::int32_t pri = plate(a + b + (b - 1 - k));
     for (std::size_t j = 0; j < k; ++j) {
       const std::int32_t sX = e.slot(K::X, j, k, 0, 0);
       if (k == j + 1)

@@ -188,6 +188,7 @@ __global__ void __launch_bounds__(kThreads, 1) ech_gf2_cluster_kernel(ClArgs g) 
     stamp(k - 1, 10);
     const long long ck0 = clock64();
     int r2 = 0, ok = 1, q0 = -1, q1 = -1, mpc = 0, mpr = 0;
+    const unsigned lanebit = 1u << lane;
 #pragma unroll 1
     for (int c = 0; c < wc; ++c) {
       const unsigned b0 = __ballot_sync(0xffffffffu, !p0 && ((w0 >> c) & 1u));
@@ -198,10 +199,13 @@ __global__ void __launch_bounds__(kThreads, 1) ech_gf2_cluster_kernel(ClArgs g) 
         break;
       }
       const bool hi = b0 == 0;
-      const int sl = __ffs(hi ? b1 : b0) - 1;
+      const unsigned bb = hi ? b1 : b0;
+      const int sl = __ffs(bb) - 1;
       const std::uint32_t pw = __shfl_sync(0xffffffffu, hi ? w1 : w0, sl);
       const std::uint32_t pk = __shfl_sync(0xffffffffu, hi ? k1 : k0, sl) ^ (1u << r2);
-      const bool me0 = !hi && lane == sl, me1 = hi && lane == sl;
+      // "am I the pivot lane" from the ballot's lowest bit (no lane id in the loop)
+      const bool mine = (bb & (0u - bb) & lanebit) != 0;
+      const bool me0 = !hi && mine, me1 = hi && mine;
       if (!me0 && ((w0 >> c) & 1u)) {
         w0 ^= pw;
         k0 ^= pk;
@@ -218,7 +222,7 @@ __global__ void __launch_bounds__(kThreads, 1) ech_gf2_cluster_kernel(ClArgs g) 
         p1 = true;
         q1 = r2;
       }
-      if (lane == r2) {  // kept in registers: no shared stores on the chain
+      if ((lanebit >> r2) & 1u) {  // kept in registers: no shared stores on the chain
         mpc = c;
         mpr = lo + (hi ? 32 : 0) + sl;
       }

@@ -33,21 +33,53 @@ __global__ void __launch_bounds__(NT, 1) k(long long* out, unsigned seed, int it
     ++r2;
   }
   long long t3 = clock64();
+  // exact in-kernel loop shape (row layout + register bookkeeping), 32-col panels
+  int mpc = 0, mpr = 0, q0 = -1, q1 = -1, tot = 0;
+  for (int it = 0; it < iters / 32; ++it) {
+    unsigned x0 = w0 * 2654435761u + it, x1 = w1 * 2246822519u + it, kk0 = 0, kk1 = 0;
+    bool pp0 = false, pp1 = false;
+    int rr = 0, ok = 1;
+    const bool covers_all = (it & 1);
+#pragma unroll 1
+    for (int c = 0; c < 32; ++c) {
+      const unsigned b0 = __ballot_sync(0xffffffffu, !pp0 && ((x0 >> c) & 1u));
+      const unsigned b1 = __ballot_sync(0xffffffffu, !pp1 && ((x1 >> c) & 1u));
+      if (!(b0 | b1)) {
+        if (covers_all) continue;
+        ok = 0;
+        break;
+      }
+      const bool hi = b0 == 0;
+      const int sl = __ffs(hi ? b1 : b0) - 1;
+      const unsigned pw = __shfl_sync(0xffffffffu, hi ? x1 : x0, sl);
+      const unsigned pk = __shfl_sync(0xffffffffu, hi ? kk1 : kk0, sl) ^ (1u << rr);
+      const bool me0 = !hi && lane == sl, me1 = hi && lane == sl;
+      if (!me0 && ((x0 >> c) & 1u)) { x0 ^= pw; kk0 ^= pk; }
+      if (!me1 && ((x1 >> c) & 1u)) { x1 ^= pw; kk1 ^= pk; }
+      if (me0) { pp0 = true; q0 = rr; }
+      if (me1) { pp1 = true; q1 = rr; }
+      if (lane == rr) { mpc = c; mpr = (hi ? 32 : 0) + sl; }
+      ++rr;
+    }
+    tot += rr + ok + mpc + mpr + q0 + q1 + int(kk0 ^ kk1);
+  }
+  long long t4 = clock64();
   if (lane == 0) {
-    out[0] = t1 - t0; out[1] = t2 - t1; out[2] = t3 - t2; out[3] = w0 ^ w1 ^ k0 ^ k1 ^ v ^ b;
+    out[0] = t1 - t0; out[1] = t2 - t1; out[2] = t3 - t2; out[3] = w0 ^ w1 ^ k0 ^ k1 ^ v ^ b ^ tot;
+    out[4] = t4 - t3;
   }
   __syncthreads();
 }
 int main() {
   long long* d; cudaMalloc(&d, 64);
-  long long h[4];
+  long long h[5];
   const int iters = 4096;
   for (int rep = 0; rep < 4; ++rep) {
     if (rep < 2) k<32><<<1, 32>>>(d, 12345 + rep, iters);
     else k<1024><<<1, 1024>>>(d, 12345 + rep, iters);
     cudaMemcpy(h, d, sizeof h, cudaMemcpyDeviceToHost);
-    printf("per iter cycles: shfl chain %.1f  vote chain %.1f  gf2 row step %.1f\n", double(h[0]) / iters,
-           double(h[1]) / iters, double(h[2]) / iters);
+    printf("per iter cycles: shfl chain %.1f  vote chain %.1f  gf2 row step %.1f  kernel-shape %.1f\n", double(h[0]) / iters,
+           double(h[1]) / iters, double(h[2]) / iters, double(h[4]) / iters);
   }
   return 0;
 }
