@@ -313,20 +313,21 @@ EchResult extract_ech(std::int64_t a, std::int64_t b, const Mat& aug, const std:
   return out;
 }
 
-// Outer panel width of the two-level device ECH (0 = one level).  Blocks
-// whose trailing updates are big enough for K1's tensor path take 256-wide
-// outer panels: the 32-wide steps then only sweep an L2-resident a x 512
-// scratch, and the rest of [W | T] sees one K = 256 contraction per outer
-// panel instead of eight K = 32 ones.  GFQ_ECH_OUTER overrides (0 disables).
+// Outer panel width of the two-level device ECH (0 = one level).  Every
+// block wider than one step takes 256-wide outer panels: the 32-wide steps
+// then only sweep an L2-resident rows x 512 scratch (two fused launches a
+// step), and the rest of [W | T] sees one K = 256 contraction per outer
+// panel instead of eight K = 32 ones (cfg1's 500-blocks: 11.7 -> 5.5 ms a
+// step).  GFQ_ECH_OUTER / set_ech_outer override (0 = one level).
 constexpr std::int64_t kEchOuterMax = 256;
 std::atomic<int> g_ech_outer{[] {
   const char* e = std::getenv("GFQ_ECH_OUTER");
   return e ? std::atoi(e) : -1;
 }()};
-std::int64_t ech_outer_width(std::int64_t a, std::int64_t b) {
+std::int64_t ech_outer_width(std::int64_t b) {
   const std::int64_t forced = g_ech_outer;
   if (forced >= 0) return forced == 0 ? 0 : std::min<std::int64_t>(kEchOuterMax, std::max<std::int64_t>(32, forced / 32 * 32));
-  return (b > 64 && a * (a + b) >= std::int64_t(1) << 20) ? kEchOuterMax : 0;
+  return b > 32 ? kEchOuterMax : 0;
 }
 
 // Device ECH: right-looking panel Gauss-Jordan on Aug = [W | T] (T = I), one
@@ -395,7 +396,7 @@ EchResult panel_ech(const FieldSpec& f, const Mat& h) {
   GFQ_CUDA(cudaMemsetAsync(info.ptr, 0, info.bytes, s));
   auto* inf = reinterpret_cast<std::int32_t*>(info.ptr);
   auto* r2 = reinterpret_cast<std::int32_t*>(rho2.ptr);
-  const std::int64_t ow = ech_outer_width(a, b);
+  const std::int64_t ow = ech_outer_width(b);
   if (ow == 0) {
     Mat G(a, w), Bp(w, tb + a);
     for (std::int64_t c0 = 0; c0 < b; c0 += w) {

@@ -705,16 +705,30 @@ __global__ void __launch_bounds__(32) ech_gf2_small_kernel(int rows, int cols, c
   std::uint32_t* row = sw + lane * st;
   std::uint8_t* colpiv = reinterpret_cast<std::uint8_t*>(sw + 32 * st);  // cols bytes
   __shared__ int pc[32], pr[32];
-  if (lane < rows) {
-    const std::uint8_t* h = H + std::int64_t(lane) * ldh;
-    for (int w = 0; w < Wd; ++w) {
+  // pack [H | I] warp-cooperatively: lane w builds word w of each row from
+  // 32 consecutive bytes (coalesced 16-byte loads when aligned)
+  const bool vec = (reinterpret_cast<std::uintptr_t>(H) & 15) == 0 && (ldh & 15) == 0;
+  for (int i = 0; i < rows; ++i) {
+    const std::uint8_t* h = H + std::int64_t(i) * ldh;
+    for (int w = lane; w < Wd; w += 32) {
       std::uint32_t word = 0;
-      for (int b = 0; b < 32; ++b) {
-        const int j = 32 * w + b;
-        if (j < cols) word |= std::uint32_t(h[j] & 1u) << b;
+      const int j0 = 32 * w;
+      if (vec && j0 + 32 <= cols) {
+        const uint4 a = reinterpret_cast<const uint4*>(h + j0)[0], b = reinterpret_cast<const uint4*>(h + j0)[1];
+        const std::uint32_t v[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+          const std::uint32_t x = v[q] & 0x01010101u;  // one bit per byte
+          word |= ((x & 1u) | ((x >> 7) & 2u) | ((x >> 14) & 4u) | ((x >> 21) & 8u)) << (4 * q);
+        }
+      } else {
+        for (int b = 0; b < 32; ++b) {
+          const int j = j0 + b;
+          if (j < cols) word |= std::uint32_t(h[j] & 1u) << b;
+        }
       }
-      if (32 * w <= cols + lane && cols + lane < 32 * w + 32) word |= 1u << (cols + lane - 32 * w);
-      row[w] = word;
+      if (j0 <= cols + i && cols + i < j0 + 32) word |= 1u << (cols + i - j0);
+      sw[i * st + w] = word;
     }
   }
   for (int c = lane; c < cols; c += 32) colpiv[c] = 0;
@@ -761,12 +775,19 @@ __global__ void __launch_bounds__(32) ech_gf2_small_kernel(int rows, int cols, c
       m &= m - 1;
       out[s] = std::uint8_t((row[pos >> 5] >> (pos & 31)) & 1u);
     }
-    // R rows: the non-pivot columns of pivot rows
-    if (q >= 0) {
-      std::uint8_t* rr = ex.R + std::int64_t(q) * ex.ldr;
-      int t = 0;
-      for (int c = 0; c < cols; ++c)
-        if (!colpiv[c]) rr[t++] = std::uint8_t((row[c >> 5] >> (c & 31)) & 1u);
+  }
+  // R rows (the non-pivot columns of the pivot rows), warp-cooperatively:
+  // column c goes to position c - #(pivot columns < c); pc is increasing
+  __syncwarp();
+  for (int t2 = 0; t2 < r; ++t2) {
+    const int prw = pr[t2];
+    const std::uint32_t* src = sw + prw * st;
+    std::uint8_t* rr = ex.R + std::int64_t(t2) * ex.ldr;
+    int below_c = 0;  // pivot columns < c (c increases, so it only advances)
+    for (int c = lane; c < cols; c += 32) {
+      while (below_c < r && pc[below_c] < c) ++below_c;
+      if (colpiv[c]) continue;
+      rr[c - below_c] = std::uint8_t((src[c >> 5] >> (c & 31)) & 1u);
     }
   }
 }
