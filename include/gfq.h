@@ -84,6 +84,21 @@ int gfq_mad_counters(int64_t* simt_launches, int64_t* tc_launches, int reset);
 /* K6: exact device replica of random_matrix / random_product_matrix
  * (include/gfrref/generate.hpp:33-39, src/generate.cpp:16-38). */
 int gfq_random_matrix(uint32_t p, int64_t rows, int64_t cols, uint64_t seed, gfq_mat** out);
+/* Fields.  Every entry point's `p` is a field code: a prime p <= 251 is
+ * GF(p) itself; gfq_field_register returns the code (>= 0x10000) of
+ * GF(p^k), p^k <= 256, with the given monic irreducible modulus c0..ck
+ * (n_modulus = k + 1; NULL / 0: the reference's default modulus), the
+ * reference's FieldSpec(p, k, modulus) (include/gfrref/field.hpp:24-30).
+ * Elements are encoded like the reference: sum_i c_i p^i, one byte each. */
+int gfq_field_register(uint32_t p, uint32_t k, const uint32_t* modulus, int n_modulus,
+                       uint32_t* code);
+/* p, k, q = p^k and the modulus (k + 1 coefficients; {0, 1} for k = 1). */
+int gfq_field_info(uint32_t code, uint32_t* p, uint32_t* k, uint32_t* q, uint32_t* modulus);
+/* Host field arithmetic (reference FieldSpec add / mul / neg / inv,
+ * include/gfrref/field.hpp:45-88): op 0 add, 1 mul, 2 neg(a), 3 inv(a). */
+int gfq_field_op(uint32_t code, int op, uint32_t a, uint32_t b, uint32_t* out);
+/* Reference default_modulus (include/gfrref/field.hpp:118): k + 1 coefficients. */
+int gfq_default_modulus(uint32_t p, uint32_t k, uint32_t* modulus);
 int gfq_random_product_matrix(uint32_t p, int64_t rows, int64_t cols, int64_t inner,
                               uint64_t seed, gfq_mat** out);
 /* Base-case size of the device ECH recursion (<= 128; results unaffected). */

@@ -52,6 +52,15 @@ def _load():
     lib.gfo_oracle_rref.restype = ctypes.c_int64
     lib.gfo_inv.argtypes = [ctypes.c_uint32, ctypes.c_uint32]
     lib.gfo_inv.restype = ctypes.c_uint32
+    lib.gfo_field_ext.argtypes = [ctypes.c_uint32, ctypes.c_uint32, _u32p]
+    lib.gfo_field_ext.restype = ctypes.c_uint32
+    for fn in (lib.gfo_add, lib.gfo_mul):
+        fn.argtypes = [ctypes.c_uint32, ctypes.c_uint32, ctypes.c_uint32]
+        fn.restype = ctypes.c_uint32
+    lib.gfo_neg.argtypes = [ctypes.c_uint32, ctypes.c_uint32]
+    lib.gfo_neg.restype = ctypes.c_uint32
+    lib.gfo_order.argtypes = [ctypes.c_uint32]
+    lib.gfo_order.restype = ctypes.c_uint32
     return lib
 
 
@@ -84,7 +93,18 @@ def _load_ref():
     r.ref_out_materialize.argtypes = [ctypes.c_void_p, _u8p]
     r.ref_out_assembled_R.argtypes = [ctypes.c_void_p, _u8p]
     r.ref_verify.argtypes = [ctypes.c_void_p, ctypes.c_uint32, _sz, _sz, _u8p, _sz]
+    r.ref_field_register.argtypes = [ctypes.c_uint32, ctypes.c_uint32, _u32p, _sz]
+    r.ref_field_register.restype = ctypes.c_uint32
+    r.ref_field_op.argtypes = [ctypes.c_uint32, ctypes.c_int, ctypes.c_uint32, ctypes.c_uint32]
+    r.ref_field_op.restype = ctypes.c_uint32
+    r.ref_default_modulus.argtypes = [ctypes.c_uint32, ctypes.c_uint32, _u32p]
     return r
+
+
+def _need_ref():
+    if ref is None:
+        raise RuntimeError("reference library oracle/_ref/libgfrref_ref.so not built")
+    return ref
 
 
 lib = _load()
@@ -101,6 +121,50 @@ def u8ptr(a: np.ndarray):
 def u32ptr(a: np.ndarray):
     assert a.dtype == np.uint32 and a.flags["C_CONTIGUOUS"]
     return a.ctypes.data_as(_u32p)
+
+
+def ext_code(p: int, k: int, modulus) -> int:
+    """Code of GF(p^k) with this modulus in the C restatement (q <= 256);
+    every oracle function takes it in place of p."""
+    m = np.ascontiguousarray(np.asarray(modulus, np.uint32))
+    code = lib.gfo_field_ext(p, k, u32ptr(m))
+    if code == 0:
+        raise ValueError(f"oracle: cannot build GF({p}^{k}) with modulus {list(modulus)}")
+    return int(code)
+
+
+def field_op(code: int, op: str, a: int, b: int = 0) -> int:
+    if op == "add":
+        return int(lib.gfo_add(code, a, b))
+    if op == "mul":
+        return int(lib.gfo_mul(code, a, b))
+    if op == "neg":
+        return int(lib.gfo_neg(code, a))
+    return int(lib.gfo_inv(code, a))
+
+
+def ref_ext_code(p: int, k: int, modulus=None) -> int:
+    """Code of the reference library's FieldSpec(p, k, modulus) for the ref_*
+    functions (oracle/ref_shim.cpp)."""
+    r = _need_ref()
+    if modulus is None:
+        code = r.ref_field_register(p, k, None, 0)
+    else:
+        m = np.ascontiguousarray(np.asarray(modulus, np.uint32))
+        code = r.ref_field_register(p, k, u32ptr(m), m.size)
+    if code == 0:
+        raise ValueError(r.ref_last_error().decode())
+    return int(code)
+
+
+def ref_field_op(code: int, op: str, a: int, b: int = 0) -> int:
+    return int(_need_ref().ref_field_op(code, {"add": 0, "mul": 1, "neg": 2, "inv": 3}[op], a, b))
+
+
+def ref_default_modulus(p: int, k: int):
+    out = np.zeros(k + 1, np.uint32)
+    _need_ref().ref_default_modulus(p, k, u32ptr(out))
+    return [int(x) for x in out]
 
 
 def random_matrix(p: int, rows: int, cols: int, seed: int) -> np.ndarray:
@@ -134,6 +198,25 @@ def mad(p: int, a: np.ndarray, b: np.ndarray, c: np.ndarray | None = None) -> np
         lib.gfo_mad(p, m, k, n, u8ptr(a) if a.size else u8ptr(np.zeros(1, np.uint8)), max(k, 1),
                     u8ptr(b) if b.size else u8ptr(np.zeros(1, np.uint8)), max(n, 1),
                     u8ptr(c) if c is not None else None, n, u8ptr(out), n)
+    return out
+
+
+def ref_mad(p: int, a: np.ndarray, b: np.ndarray, c: np.ndarray | None = None) -> np.ndarray:
+    """The reference's own ``mat_mul`` / ``mat_mul_add`` (src/matrix.cpp:137-144)."""
+    r = _need_ref()
+    a = np.ascontiguousarray(a, np.uint8)
+    b = np.ascontiguousarray(b, np.uint8)
+    m, k = a.shape
+    n = b.shape[1]
+    out = np.zeros((m, n), np.uint8)
+    z = np.zeros(1, np.uint8)
+    if c is not None:
+        c = np.ascontiguousarray(c, np.uint8)
+    rc = r.ref_mad(p, m, k, n, u8ptr(a) if a.size else u8ptr(z), max(k, 1), u8ptr(b) if b.size else u8ptr(z),
+                   max(n, 1), u8ptr(c) if c is not None else None, max(n, 1), u8ptr(out) if out.size else u8ptr(z),
+                   max(n, 1))
+    if rc != 0:
+        raise RuntimeError(r.ref_last_error().decode())
     return out
 
 

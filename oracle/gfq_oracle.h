@@ -65,6 +65,15 @@ int64_t gfo_oracle_rref(uint32_t p, size_t m, size_t n, const uint8_t* C,
 /* Field helpers (reference include/gfrref/field.hpp:45-78, src/field.cpp:220-237). */
 uint32_t gfo_inv(uint32_t p, uint32_t a);
 
+/* Fields: every `p` above is a field code -- p for GF(p), or the code
+ * gfo_field_ext returns for GF(p^k) (q = p^k <= 256, monic irreducible
+ * modulus c0..ck; 0 on failure).  Elements are encoded sum_i c_i p^i. */
+uint32_t gfo_field_ext(uint32_t p, uint32_t k, const uint32_t* modulus);
+uint32_t gfo_order(uint32_t code);
+uint32_t gfo_add(uint32_t code, uint32_t a, uint32_t b);
+uint32_t gfo_mul(uint32_t code, uint32_t a, uint32_t b);
+uint32_t gfo_neg(uint32_t code, uint32_t a);
+
 #ifdef __cplusplus
 }
 #endif

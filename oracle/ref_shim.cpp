@@ -43,6 +43,17 @@ void to_u8(const Matrix& m, std::uint8_t* dst, std::size_t ld) {
       dst[r * ld + c] = static_cast<std::uint8_t>(m.at(r, c));
 }
 
+// Field codes: p for GF(p); 0x10000 + i for the i-th field registered with
+// ref_field_register (the reference's FieldSpec(p, k, modulus)).
+std::vector<FieldSpec>& ext_fields() {
+  static std::vector<FieldSpec> v;
+  return v;
+}
+FieldSpec fs(std::uint32_t code) {
+  if (code >= 0x10000u) return ext_fields().at(code - 0x10000u);
+  return FieldSpec(code);
+}
+
 struct RefOut {
   EchelonOutput out;
   explicit RefOut(EchelonOutput o) : out(std::move(o)) {}
@@ -53,20 +64,52 @@ extern "C" {
 
 const char* ref_last_error() { return g_err.c_str(); }
 
+std::uint32_t ref_field_register(std::uint32_t p, std::uint32_t k, const std::uint32_t* mod,
+                                 std::size_t n) {
+  try {
+    std::vector<std::uint32_t> m;
+    if (mod) m.assign(mod, mod + n);
+    FieldSpec f(p, k, m);
+    auto& v = ext_fields();
+    for (std::size_t i = 0; i < v.size(); ++i)
+      if (v[i] == f) return std::uint32_t(0x10000u + i);
+    v.push_back(f);
+    return std::uint32_t(0x10000u + v.size() - 1);
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return 0;
+  }
+}
+
+std::uint32_t ref_field_op(std::uint32_t code, int op, std::uint32_t a, std::uint32_t b) {
+  const FieldSpec f = fs(code);
+  switch (op) {
+    case 0: return f.add(a, b);
+    case 1: return f.mul(a, b);
+    case 2: return f.neg(a);
+    default: return f.inv(a);
+  }
+}
+
+void ref_default_modulus(std::uint32_t p, std::uint32_t k, std::uint32_t* out) {
+  const auto m = default_modulus(p, k);
+  for (std::size_t i = 0; i < m.size(); ++i) out[i] = m[i];
+}
+
 int ref_hardware_concurrency() {
   return static_cast<int>(std::thread::hardware_concurrency());
 }
 
 void ref_random_matrix(std::uint32_t p, std::size_t rows, std::size_t cols,
                        std::uint64_t seed, std::uint8_t* out, std::size_t ld) {
-  to_u8(random_matrix(FieldSpec(p), rows, cols, seed), out, ld);
+  to_u8(random_matrix(fs(p), rows, cols, seed), out, ld);
 }
 
 void ref_random_product_matrix(std::uint32_t p, std::size_t rows,
                                std::size_t cols, std::size_t inner,
                                std::uint64_t seed, std::uint8_t* out,
                                std::size_t ld) {
-  to_u8(random_product_matrix(FieldSpec(p), rows, cols, inner, seed), out, ld);
+  to_u8(random_product_matrix(fs(p), rows, cols, inner, seed), out, ld);
 }
 
 int ref_mad(std::uint32_t p, std::size_t m, std::size_t k, std::size_t n,
@@ -74,7 +117,7 @@ int ref_mad(std::uint32_t p, std::size_t m, std::size_t k, std::size_t n,
             std::size_t ldb, const std::uint8_t* Cin, std::size_t ldc,
             std::uint8_t* D, std::size_t ldd) {
   try {
-    const FieldSpec f(p);
+    const FieldSpec f = fs(p);
     const Matrix a = from_u8(m, k, A, lda), b = from_u8(k, n, B, ldb);
     const Matrix out = Cin ? mat_mul_add(f, from_u8(m, n, Cin, ldc), a, b)
                            : mat_mul(f, a, b);
@@ -104,7 +147,7 @@ std::int64_t ref_ech(std::uint32_t p, std::size_t m, std::size_t n,
                      std::uint32_t* gamma, std::uint8_t* M, std::uint8_t* K,
                      std::uint8_t* R) {
   try {
-    return put_ech(ech(FieldSpec(p), from_u8(m, n, H, ld), threshold), rho,
+    return put_ech(ech(fs(p), from_u8(m, n, H, ld), threshold), rho,
                    gamma, M, K, R);
   } catch (const std::exception& e) {
     g_err = e.what();
@@ -118,7 +161,7 @@ std::int64_t ref_oracle_rref(std::uint32_t p, std::size_t m, std::size_t n,
                              std::uint8_t* M, std::uint8_t* K,
                              std::uint8_t* R) {
   try {
-    return put_ech(oracle_rref(FieldSpec(p), from_u8(m, n, C, ld)), rho, gamma,
+    return put_ech(oracle_rref(fs(p), from_u8(m, n, C, ld)), rho, gamma,
                    M, K, R);
   } catch (const std::exception& e) {
     g_err = e.what();
@@ -141,7 +184,7 @@ void* ref_echelonize(std::uint32_t p, std::size_t m, std::size_t n,
     o.ech_threshold = threshold;
     RunReport rep;
     const auto t0 = std::chrono::steady_clock::now();
-    EchelonOutput out = echelonize(c, FieldSpec(p), o, &rep);
+    EchelonOutput out = echelonize(c, fs(p), o, &rep);
     const auto t1 = std::chrono::steady_clock::now();
     if (wall_s) *wall_s = std::chrono::duration<double>(t1 - t0).count();
     if (run_s) *run_s = double(rep.wall_ns) * 1e-9;

@@ -73,6 +73,10 @@ PROTOS = {
     "gfq_random_product_matrix": (I, [U32, I64, I64, I64, U64, vpp]),
     "gfq_set_ech_base": (I, [U64]),
     "gfq_set_ech_outer": (I, [ctypes.c_int]),
+    "gfq_field_register": (I, [U32, U32, ctypes.c_void_p, I, ctypes.c_void_p]),
+    "gfq_field_info": (I, [U32, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p]),
+    "gfq_field_op": (I, [U32, I, U32, U32, ctypes.c_void_p]),
+    "gfq_default_modulus": (I, [U32, U32, ctypes.c_void_p]),
     "gfq_set_ech_mode": (I, [I]),
     "gfq_launch_count": (I, [I, c_i64p]),
     "gfq_profile": (I, [I]),

@@ -221,7 +221,7 @@ int gfq_mad_raw(uint32_t p, int64_t m, int64_t n, int64_t k, const uint8_t* A, i
                 int64_t ldd) {
   return guard([&] {
     gfq::FieldSpec f(p);
-    gfq::dev::mad(f.p(), m, n, k, A, lda, Bm, ldb, Cin, ldc, D, ldd, gfq::cur_stream());
+    gfq::field_mad(f, m, n, k, A, lda, Bm, ldb, Cin, ldc, D, ldd, gfq::cur_stream());
   });
 }
 int gfq_set_mad_policy(int policy) { return guard([&] { gfq::dev::set_mad_policy(policy); }); }
@@ -233,11 +233,53 @@ int gfq_mad_counters(int64_t* simt, int64_t* tc, int reset) {
 }
 
 namespace {
+// one below(q) draw per entry of the reference stream (src/generate.cpp:16-24);
+// `p` is a field code, q its order
 void fill_exact(uint32_t p, int64_t rows, int64_t cols, uint64_t seed, uint64_t draw0,
                 uint8_t* dst, int64_t ld) {
-  gfq::random_fill_exact(p, rows, cols, seed, draw0, cols, dst, ld);
+  gfq::random_fill_exact(gfq::FieldSpec(p).order(), rows, cols, seed, draw0, cols, dst, ld);
 }
 }  // namespace
+
+// ---------------------------------------------------------------- fields
+int gfq_field_register(uint32_t p, uint32_t k, const uint32_t* modulus, int n_modulus,
+                       uint32_t* code) {
+  return guard([&] {
+    if (!code) throw std::invalid_argument("gfq_field_register: null output");
+    std::vector<uint32_t> mod;
+    if (modulus && n_modulus > 0) mod.assign(modulus, modulus + n_modulus);
+    *code = gfq::FieldSpec(p, k, mod).code();
+  });
+}
+int gfq_field_info(uint32_t code, uint32_t* p, uint32_t* k, uint32_t* q, uint32_t* modulus) {
+  return guard([&] {
+    const gfq::FieldSpec f(code);
+    if (p) *p = f.p();
+    if (k) *k = f.k();
+    if (q) *q = f.order();
+    if (modulus)
+      for (std::size_t i = 0; i < f.modulus().size(); ++i) modulus[i] = f.modulus()[i];
+  });
+}
+int gfq_field_op(uint32_t code, int op, uint32_t a, uint32_t b, uint32_t* out) {
+  return guard([&] {
+    const gfq::FieldSpec f(code);
+    if (a >= f.order() || b >= f.order()) throw std::invalid_argument("field: element out of range");
+    switch (op) {
+      case 0: *out = f.add(a, b); break;
+      case 1: *out = f.mul(a, b); break;
+      case 2: *out = f.neg(a); break;
+      case 3: *out = f.inv(a); break;
+      default: throw std::invalid_argument("gfq_field_op: op must be 0..3");
+    }
+  });
+}
+int gfq_default_modulus(uint32_t p, uint32_t k, uint32_t* modulus) {
+  return guard([&] {
+    const auto m = gfq::default_modulus(p, k);
+    for (std::size_t i = 0; i < m.size(); ++i) modulus[i] = m[i];
+  });
+}
 
 int gfq_random_matrix(uint32_t p, int64_t rows, int64_t cols, uint64_t seed, gfq_mat** out) {
   return guard([&] {

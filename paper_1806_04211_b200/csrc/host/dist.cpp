@@ -433,7 +433,7 @@ EchelonOutput echelonize_dist(const Mat* C, std::int64_t m, std::int64_t n, std:
       colblk[k] = C->col_view(std::int64_t(cs.col_offset(k)), std::int64_t(cs.col_parts[k]));
     } else {
       colblk[k] = Mat(m, std::int64_t(cs.col_parts[k]));
-      random_fill_exact(field.p(), m, std::int64_t(cs.col_parts[k]), seed,
+      random_fill_exact(field.order(), m, std::int64_t(cs.col_parts[k]), seed,
                         std::uint64_t(cs.col_offset(k)), n, colblk[k].data(), colblk[k].ld());
     }
   }

@@ -38,7 +38,18 @@ void put_matrix(std::ostream& out, const Mat& m) {
   put_rows(out, h.data(), m.rows(), m.cols(), m.cols());
 }
 
-void put_field(std::ostream& out, std::uint32_t p) { out << "field p=" << p << " k=1\n"; }
+// reference src/io.cpp:143-153 (write_field_line); `code` is a field code
+void put_field(std::ostream& out, std::uint32_t code) {
+  const FieldSpec f(code);
+  out << "field p=" << f.p() << " k=" << f.k();
+  if (f.k() > 1) {
+    out << " modulus=";
+    const std::vector<std::uint32_t>& mod = f.modulus();
+    for (std::size_t t = 0; t < mod.size(); ++t) out << (t ? "," : "") << mod[t];
+  }
+  out << "\n";
+}
+
 
 std::ofstream open_out(const std::string& path) {
   std::ofstream out(path, std::ios::binary);
@@ -104,6 +115,22 @@ std::uint64_t key_u64(const Lines& lr, const std::vector<std::string>& t, std::s
 
 }  // namespace
 
+// reference src/io.cpp:527-543
+std::vector<std::uint32_t> parse_modulus(const std::string& text) {
+  std::vector<std::uint32_t> out;
+  std::size_t pos = 0;
+  while (true) {
+    const std::size_t comma = text.find(',', pos);
+    const std::string tok = comma == std::string::npos ? text.substr(pos) : text.substr(pos, comma - pos);
+    std::uint64_t v = 0;
+    if (!to_u64(tok, v) || v >= (1u << 16)) throw ParseError("invalid modulus coefficient: '" + tok + "'");
+    out.push_back(std::uint32_t(v));
+    if (comma == std::string::npos) break;
+    pos = comma + 1;
+  }
+  return out;
+}
+
 // reference src/io.cpp:199-213
 GfMatHost read_gfmat(std::istream& in, const std::string& name) {
   Lines lr{in, name};
@@ -112,12 +139,32 @@ GfMatHost read_gfmat(std::istream& in, const std::string& name) {
   if (ft.empty() || ft[0] != "field") lr.fail("expected a field header");
   const std::uint64_t p = key_u64(lr, ft, 1, "p");
   const std::uint64_t k = key_u64(lr, ft, 2, "k");
-  if (k != 1) lr.fail("extension fields GF(p^k) are not supported on the B200 path");
-  if (ft.size() != 3) lr.fail("prime fields take no modulus");
-  try {
-    FieldSpec f(std::uint32_t(p > 0xFFFFFFFFull ? 0 : p));
-  } catch (const std::exception& e) {
-    lr.fail(e.what());
+  // reference src/io.cpp:115-140 (parse_field_line)
+  if (p < 2 || p >= (1u << 16)) lr.fail("field characteristic out of range");
+  if (k < 1) lr.fail("field degree must be at least 1");
+  std::uint32_t code = 0, q = 0;
+  if (k == 1) {
+    if (ft.size() != 3) lr.fail("prime fields take no modulus");
+    try {
+      const FieldSpec f{std::uint32_t(p)};
+      code = f.code();
+      q = f.order();
+    } catch (const std::exception& e) {
+      lr.fail(e.what());
+    }
+  } else {
+    if (ft.size() != 4) lr.fail("extension fields need modulus=c0,...,ck");
+    const std::string& mt = ft[3];
+    if (mt.rfind("modulus=", 0) != 0) lr.fail("expected modulus=...");
+    try {
+      const FieldSpec f(std::uint32_t(p), std::uint32_t(k), parse_modulus(mt.substr(8)));
+      code = f.code();
+      q = f.order();
+    } catch (const ParseError&) {
+      throw;
+    } catch (const std::exception& e) {
+      lr.fail(e.what());
+    }
   }
   const std::vector<std::string> dt = tokens(lr.expect("rows=... cols=..."));
   const std::uint64_t rows = key_u64(lr, dt, 0, "rows");
@@ -125,7 +172,7 @@ GfMatHost read_gfmat(std::istream& in, const std::string& name) {
   if (dt.size() != 2) lr.fail("unexpected tokens after cols=...");
   if (rows > (1u << 24) || cols > (1u << 24)) lr.fail("dimensions out of range");
   GfMatHost m;
-  m.p = std::uint32_t(p);
+  m.p = code;
   m.rows = std::int64_t(rows);
   m.cols = std::int64_t(cols);
   m.data.resize(std::size_t(rows * cols));
@@ -141,7 +188,7 @@ GfMatHost read_gfmat(std::istream& in, const std::string& name) {
       const auto res = std::from_chars(s, e, v);
       if (res.ec != std::errc() || (res.ptr < e && *res.ptr != ' ' && *res.ptr != '\t'))
         lr.fail("invalid entry");
-      if (v >= p) lr.fail("entry " + std::to_string(v) + " is not below p");
+      if (v >= q) lr.fail("entry '" + std::to_string(v) + "' is not an element encoding");
       if (c >= cols) lr.fail("too many entries in row");
       m.data[std::size_t(r * cols + c)] = std::uint8_t(v);
       ++c;
@@ -210,7 +257,7 @@ void write_selects_file(const std::string& path, const EchelonOutput& res) {
 void write_transform(std::ostream& out, const EchelonOutput& res) {
   if (!res.with_transform) throw std::logic_error("transformation was not computed");
   out << "TRANSFORM v1\n";
-  put_field(out, res.field.p());
+  put_field(out, res.field.code());
   out << "block_rows=" << res.chop.a() << " block_cols=" << res.chop.b() << "\n";
   for (std::size_t j = 0; j < res.chop.b(); ++j)
     for (std::size_t h = 0; h < res.chop.a(); ++h) {

@@ -62,6 +62,21 @@ void set_ech_base(std::size_t n) {
 std::size_t ech_base() { return g_ech_base; }
 
 // ---------------------------------------------------------------- products
+// D = (Cin ? Cin : 0) + A.B over the field: K1 for GF(p), the digit-plane
+// contraction (dev::mad_ext, one K1 launch over GF(p)) for GF(p^k).
+void field_mad(const FieldSpec& f, std::int64_t m, std::int64_t n, std::int64_t k,
+               const std::uint8_t* A, std::int64_t lda, const std::uint8_t* B, std::int64_t ldb,
+               const std::uint8_t* Cin, std::int64_t ldc, std::uint8_t* D, std::int64_t ldd,
+               cudaStream_t s) {
+  if (!f.is_ext()) {
+    dev::mad(f.p(), m, n, k, A, lda, B, ldb, Cin, ldc, D, ldd, s);
+    return;
+  }
+  if (m == 0 || n == 0) return;
+  DevBuf scratch{static_cast<std::size_t>(dev::mad_ext_scratch_bytes(f.k(), m, n, k))};
+  dev::mad_ext(f.ext_dev(), m, n, k, A, lda, B, ldb, Cin, ldc, D, ldd, scratch.ptr, s);
+}
+
 static Mat mul_add_kernel(const FieldSpec& f, const Mat* addend, const Mat& b, const Mat& c) {
   // reference src/matrix.cpp:81-89 shape contract
   if (b.cols() != c.rows()) throw std::invalid_argument("mul: inner dimensions disagree");
@@ -70,9 +85,9 @@ static Mat mul_add_kernel(const FieldSpec& f, const Mat* addend, const Mat& b, c
   const std::int64_t m = b.rows(), inner = b.cols(), n = c.cols();
   Mat out(m, n);
   if (m == 0 || n == 0) return out;
-  dev::mad(f.p(), m, n, inner, b.data(), b.ld(), c.data(), c.ld(),
-           addend ? addend->data() : nullptr, addend ? addend->ld() : 0, out.data(), out.ld(),
-           cur_stream());
+  field_mad(f, m, n, inner, b.data(), b.ld(), c.data(), c.ld(),
+            addend ? addend->data() : nullptr, addend ? addend->ld() : 0, out.data(), out.ld(),
+            cur_stream());
   return out;
 }
 
@@ -93,9 +108,9 @@ void mad_into(const FieldSpec& f, const Mat& d, const Mat* addend, const Mat& b,
                                 "x" + std::to_string(addend->cols()) + " vs " +
                                 std::to_string(b.rows()) + "x" + std::to_string(c.cols()) + ")");
   if (d.empty()) return;
-  dev::mad(f.p(), d.rows(), d.cols(), b.cols(), b.data(), b.ld(), c.data(), c.ld(),
-           addend ? addend->data() : nullptr, addend ? addend->ld() : 0, d.data(), d.ld(),
-           cur_stream());
+  field_mad(f, d.rows(), d.cols(), b.cols(), b.data(), b.ld(), c.data(), c.ld(),
+            addend ? addend->data() : nullptr, addend ? addend->ld() : 0, d.data(), d.ld(),
+            cur_stream());
 }
 Mat mat_mul_add(const FieldSpec& f, const Mat& a, const Mat& b, const Mat& c) {
   return mul_add_kernel(f, &a, b, c);
@@ -260,8 +275,12 @@ EchResult direct_ech(const FieldSpec& f, const Mat& h) {
   const std::int64_t rmax = std::min(a, b);
   Mat W(a, b), Tc(a, rmax > 0 ? rmax : 1);
   auto info = std::make_shared<DevBuf>(std::size_t(4 * (2 * rmax + 1)));
-  dev::ech_base(f.p(), a, b, h.data(), h.ld(), W.data(), W.ld(), Tc.data(), Tc.ld(),
-                reinterpret_cast<std::int32_t*>(info->ptr), cur_stream());
+  if (f.is_ext())
+    dev::ech_base_ext(f.ext_dev(), a, b, h.data(), h.ld(), W.data(), W.ld(), Tc.data(), Tc.ld(),
+                      reinterpret_cast<std::int32_t*>(info->ptr), cur_stream());
+  else
+    dev::ech_base(f.p(), a, b, h.data(), h.ld(), W.data(), W.ld(), Tc.data(), Tc.ld(),
+                  reinterpret_cast<std::int32_t*>(info->ptr), cur_stream());
   std::vector<std::int32_t> hi(std::size_t(2 * rmax + 1));
   download_i32(reinterpret_cast<const std::int32_t*>(info->ptr), hi.data(), hi.size());
   const std::int64_t r = hi[0];
@@ -532,7 +551,9 @@ EchResult ech(const FieldSpec& f, const Mat& h, std::size_t threshold) {
     e.gamma = IndexSet(std::size_t(beta), {});
     return e;
   }
-  if (ech_mode() == 0) {
+  // GF(p^k): the reference's split/combine recursion (its products are
+  // digit-plane K1 contractions) over the table-driven base case
+  if (ech_mode() == 0 && !f.is_ext()) {
     // panel ECH whenever the panel fits one CTA's shared memory; taller
     // blocks split their rows (reference combine_horizontal) first
     if (alpha * (f.p() == 2 ? 5 : 33) <= dev::kPanelSmem) return panel_ech(f, h);

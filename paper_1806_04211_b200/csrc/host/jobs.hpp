@@ -13,6 +13,12 @@
 
 namespace gfq {
 
+/// D = (Cin ? Cin : 0) + A.B over the field f (K1 for GF(p), the digit-plane
+/// contraction for GF(p^k)); raw device operands, stream-ordered.
+void field_mad(const FieldSpec& f, std::int64_t m, std::int64_t n, std::int64_t k,
+               const std::uint8_t* A, std::int64_t lda, const std::uint8_t* B, std::int64_t ldb,
+               const std::uint8_t* Cin, std::int64_t ldc, std::uint8_t* D, std::int64_t ldd,
+               cudaStream_t s);
 Mat cpy(const Mat& a);                                             // jobs.hpp:37
 Mat mul(const FieldSpec& f, const Mat& b, const Mat& c);           // jobs.hpp:40
 Mat mad(const FieldSpec& f, const Mat& a, const Mat& b, const Mat& c);  // jobs.hpp:43

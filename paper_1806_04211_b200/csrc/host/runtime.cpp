@@ -11,6 +11,7 @@
 #include <stdexcept>
 
 #include "types.hpp"
+#include "../kernels/kernels.hpp"
 
 namespace gfq {
 
@@ -80,17 +81,229 @@ int sm_count() {
 }
 
 // ---------------------------------------------------------------- FieldSpec
-FieldSpec::FieldSpec(std::uint32_t p) : p_(p) {
-  bool prime = p >= 2;
-  for (std::uint32_t d = 2; prime && d * d <= p; ++d)
-    if (p % d == 0) prime = false;
-  if (!prime) throw std::invalid_argument("field: p must be prime");
+// ---------------------------------------------------------------- fields
+namespace {
+using Poly = std::vector<std::uint32_t>;
+bool is_prime(std::uint32_t p) {
+  if (p < 2) return false;
+  for (std::uint32_t d = 2; d * d <= p; ++d)
+    if (p % d == 0) return false;
+  return true;
+}
+int deg(const Poly& a) {
+  for (int i = int(a.size()) - 1; i >= 0; --i)
+    if (a[std::size_t(i)] != 0) return i;
+  return -1;
+}
+// a mod m over GF(p), m monic (reference src/field.cpp:35-46)
+Poly poly_mod(Poly a, const Poly& m, std::uint32_t p) {
+  const int dm = deg(m);
+  for (int i = deg(a); dm >= 0 && i >= dm; i = deg(a)) {
+    const std::uint64_t c = a[std::size_t(i)];
+    for (int t = 0; t <= dm; ++t) {
+      const std::uint64_t v = a[std::size_t(i - dm + t)] + (p - m[std::size_t(t)]) % p * c;
+      a[std::size_t(i - dm + t)] = std::uint32_t(v % p);
+    }
+  }
+  return a;
+}
+// no monic divisor of degree 1..k/2 (reference src/field.cpp:59-78)
+bool poly_irreducible(const Poly& m, std::uint32_t p) {
+  const int k = deg(m);
+  if (k < 1) return false;
+  for (int d = 1; 2 * d <= k; ++d) {
+    std::uint64_t count = 1;
+    for (int i = 0; i < d; ++i) count *= p;
+    for (std::uint64_t c = 0; c < count; ++c) {
+      Poly div(std::size_t(d) + 1, 0);
+      std::uint64_t t = c;
+      for (int i = 0; i < d; ++i) {
+        div[std::size_t(i)] = std::uint32_t(t % p);
+        t /= p;
+      }
+      div[std::size_t(d)] = 1;
+      if (deg(poly_mod(m, div, p)) < 0) return false;
+    }
+  }
+  return true;
+}
+}  // namespace
+
+std::vector<std::uint32_t> default_modulus(std::uint32_t p, std::uint32_t k) {
+  if (!is_prime(p)) throw std::invalid_argument("field: p must be prime");
+  if (k == 1) return {0, 1};
+  std::uint64_t count = 1;
+  for (std::uint32_t i = 0; i < k; ++i) count *= p;
+  for (std::uint64_t c = 0; c < count; ++c) {
+    Poly m(k + 1, 0);
+    std::uint64_t t = c;
+    for (std::uint32_t i = 0; i < k; ++i) {
+      m[i] = std::uint32_t(t % p);
+      t /= p;
+    }
+    m[k] = 1;
+    if (poly_irreducible(m, p)) return m;
+  }
+  throw std::logic_error("field: no irreducible modulus found");
+}
+
+/// Host + device tables of GF(p^k) (q <= 256): the arithmetic is table
+/// lookups on encoded elements (the reference uses log / antilog / Zech
+/// tables, src/field.cpp:180-212; products of polynomials mod the modulus
+/// give the same field, so the tables hold identical values).
+struct ExtTablesHost {
+  std::uint32_t p = 0, k = 1, q = 0;
+  std::vector<std::uint32_t> modulus;
+  std::vector<std::uint8_t> mul, add, neg, inv, dig, red;
+  std::uint32_t code = 0;
+  mutable std::once_flag dev_once;
+  mutable std::uint8_t* dev = nullptr;
+  mutable dev::ExtTables view{};
+};
+
+namespace {
+std::mutex g_field_mtx;
+std::vector<std::shared_ptr<const ExtTablesHost>>* g_fields =
+    new std::vector<std::shared_ptr<const ExtTablesHost>>();  // process lifetime
+constexpr std::uint32_t kFieldCode0 = 0x10000;
+
+std::shared_ptr<const ExtTablesHost> make_ext(std::uint32_t p, std::uint32_t k, Poly mod) {
+  auto t = std::make_shared<ExtTablesHost>();
+  std::uint32_t q = 1;
+  for (std::uint32_t i = 0; i < k; ++i) q *= p;
+  t->p = p;
+  t->k = k;
+  t->q = q;
+  t->modulus = mod;
+  const auto decode = [&](std::uint32_t e) {
+    Poly d(k, 0);
+    for (std::uint32_t i = 0; i < k; ++i) {
+      d[i] = e % p;
+      e /= p;
+    }
+    return d;
+  };
+  const auto encode = [&](const Poly& d) {
+    std::uint32_t v = 0;
+    for (std::uint32_t i = k; i-- > 0;) v = v * p + (i < d.size() ? d[i] : 0);
+    return v;
+  };
+  t->dig.resize(std::size_t(q) * k);
+  for (std::uint32_t e = 0; e < q; ++e) {
+    const Poly d = decode(e);
+    for (std::uint32_t i = 0; i < k; ++i) t->dig[std::size_t(e) * k + i] = std::uint8_t(d[i]);
+  }
+  t->red.resize(std::size_t(2 * k - 1) * k);
+  for (std::uint32_t sdeg = 0; sdeg < 2 * k - 1; ++sdeg) {
+    Poly x(sdeg + 1, 0);
+    x[sdeg] = 1;
+    const Poly r = poly_mod(x, mod, p);
+    for (std::uint32_t u = 0; u < k; ++u)
+      t->red[std::size_t(sdeg) * k + u] = std::uint8_t(u < r.size() ? r[u] : 0);
+  }
+  t->mul.resize(std::size_t(q) * q);
+  t->add.resize(std::size_t(q) * q);
+  for (std::uint32_t a = 0; a < q; ++a)
+    for (std::uint32_t b = 0; b < q; ++b) {
+      const Poly da = decode(a), db = decode(b);
+      Poly sum(k), prod(2 * k - 1, 0);
+      for (std::uint32_t i = 0; i < k; ++i) sum[i] = (da[i] + db[i]) % p;
+      for (std::uint32_t i = 0; i < k; ++i)
+        for (std::uint32_t j = 0; j < k; ++j) prod[i + j] = (prod[i + j] + da[i] * db[j]) % p;
+      t->add[std::size_t(a) * q + b] = std::uint8_t(encode(sum));
+      t->mul[std::size_t(a) * q + b] = std::uint8_t(encode(poly_mod(prod, mod, p)));
+    }
+  t->neg.resize(q);
+  t->inv.assign(q, 0);
+  for (std::uint32_t a = 0; a < q; ++a) {
+    const Poly d = decode(a);
+    Poly n(k);
+    for (std::uint32_t i = 0; i < k; ++i) n[i] = (p - d[i]) % p;
+    t->neg[a] = std::uint8_t(encode(n));
+    for (std::uint32_t b = 1; b < q && a; ++b)
+      if (t->mul[std::size_t(a) * q + b] == 1) {
+        t->inv[a] = std::uint8_t(b);
+        break;
+      }
+  }
+  return t;
+}
+}  // namespace
+
+FieldSpec::FieldSpec(std::uint32_t p) {
+  if (p >= kFieldCode0) {
+    std::lock_guard<std::mutex> lk(g_field_mtx);
+    const std::size_t idx = p - kFieldCode0;
+    if (idx >= g_fields->size()) throw std::invalid_argument("field: unknown field code");
+    ext_ = (*g_fields)[idx];
+    p_ = ext_->p;
+    k_ = ext_->k;
+    q_ = ext_->q;
+    return;
+  }
+  if (!is_prime(p)) throw std::invalid_argument("field: p must be prime");
   if (p > 251)
     throw std::invalid_argument("field: the B200 path stores residues as u8 (p <= 251)");
+  p_ = q_ = p;
+}
+
+FieldSpec::FieldSpec(std::uint32_t p, std::uint32_t k, std::vector<std::uint32_t> modulus) {
+  // reference src/field.cpp:143-169 validation order and messages
+  if (!is_prime(p)) throw std::invalid_argument("field: p must be prime");
+  if (p >= (1u << 16)) throw std::invalid_argument("field: p must be < 2^16");
+  if (k < 1) throw std::invalid_argument("field: k must be >= 1");
+  std::uint64_t q = 1;
+  for (std::uint32_t i = 0; i < k; ++i) {
+    q *= p;
+    if (q >= (1u << 20)) throw std::invalid_argument("field: p^k must be < 2^20");
+  }
+  if (k == 1) {
+    *this = FieldSpec(p);
+    return;
+  }
+  if (q > 256)
+    throw std::invalid_argument("field: the B200 path stores elements as u8 (p^k <= 256)");
+  if (modulus.empty()) modulus = default_modulus(p, k);
+  if (modulus.size() != std::size_t(k) + 1 || modulus[k] != 1)
+    throw std::invalid_argument("field: modulus must be monic of degree k");
+  for (std::uint32_t c : modulus)
+    if (c >= p) throw std::invalid_argument("field: modulus coefficient >= p");
+  if (!poly_irreducible(modulus, p)) throw std::invalid_argument("field: modulus is not irreducible");
+  p_ = p;
+  k_ = k;
+  q_ = std::uint32_t(q);
+  std::lock_guard<std::mutex> lk(g_field_mtx);
+  for (const auto& e : *g_fields)
+    if (e->p == p && e->k == k && e->modulus == modulus) {
+      ext_ = e;
+      return;
+    }
+  auto t = make_ext(p, k, modulus);
+  const_cast<ExtTablesHost&>(*t).code = kFieldCode0 + std::uint32_t(g_fields->size());
+  g_fields->push_back(t);
+  ext_ = t;
+}
+
+std::uint32_t FieldSpec::code() const { return ext_ ? ext_->code : p_; }
+
+const std::vector<std::uint32_t>& FieldSpec::modulus() const {
+  static const std::vector<std::uint32_t> prime_mod{0, 1};
+  return ext_ ? ext_->modulus : prime_mod;
+}
+
+Elem FieldSpec::add(Elem a, Elem b) const {
+  return ext_ ? ext_->add[std::size_t(a) * q_ + b] : (a + b) % p_;
+}
+Elem FieldSpec::neg(Elem a) const {
+  return ext_ ? ext_->neg[a] : (a == 0 ? 0 : p_ - a);
+}
+Elem FieldSpec::mul(Elem a, Elem b) const {
+  return ext_ ? ext_->mul[std::size_t(a) * q_ + b] : Elem(std::uint64_t(a) * b % p_);
 }
 
 Elem FieldSpec::inv(Elem a) const {
-  if (a % p_ == 0) throw std::domain_error("field: inverse of zero");
+  if (a % q_ == 0) throw std::domain_error("field: inverse of zero");
+  if (ext_) return ext_->inv[a];
   std::uint64_t r = 1, b = a % p_;
   std::uint32_t e = p_ - 2;
   while (e) {
@@ -99,6 +312,29 @@ Elem FieldSpec::inv(Elem a) const {
     e >>= 1;
   }
   return Elem(r);
+}
+
+const dev::ExtTables& FieldSpec::ext_dev() const {
+  if (!ext_) throw std::logic_error("FieldSpec::ext_dev on a prime field");
+  const ExtTablesHost& t = *ext_;
+  std::call_once(t.dev_once, [&] {
+    const std::size_t q = t.q, k = t.k;
+    const std::size_t n = 2 * q * q + 2 * q + q * k + (2 * k - 1) * k;
+    GFQ_CUDA(cudaMalloc(&t.dev, n));  // process lifetime, like the field registry
+    std::vector<std::uint8_t> all;
+    all.reserve(n);
+    all.insert(all.end(), t.mul.begin(), t.mul.end());
+    all.insert(all.end(), t.add.begin(), t.add.end());
+    all.insert(all.end(), t.neg.begin(), t.neg.end());
+    all.insert(all.end(), t.inv.begin(), t.inv.end());
+    all.insert(all.end(), t.dig.begin(), t.dig.end());
+    all.insert(all.end(), t.red.begin(), t.red.end());
+    GFQ_CUDA(cudaMemcpy(t.dev, all.data(), n, cudaMemcpyHostToDevice));
+    std::uint8_t* d = t.dev;
+    t.view = dev::ExtTables{t.p, t.k, t.q, d, d + q * q, d + 2 * q * q, d + 2 * q * q + q,
+                            d + 2 * q * q + 2 * q, d + 2 * q * q + 2 * q + q * k};
+  });
+  return t.view;
 }
 
 // ---------------------------------------------------------------- host profile

@@ -22,24 +22,55 @@ namespace gfq {
 
 using Elem = std::uint32_t;
 
-/// GF(p), p prime <= 251 (one residue per byte).  Mirrors the prime-field
-/// half of reference FieldSpec (include/gfrref/field.hpp:20-110); extension
-/// fields are out of scope for the B200 path.
+/// Tables of an extension field GF(p^k), q = p^k <= 256 (runtime.cpp):
+/// mul / add are q x q, neg / inv q entries, dig the k base-p digits of
+/// every element, red the digits of x^s mod the modulus for s < 2k - 1;
+/// a device copy (kernels.hpp dev::ExtTables) is uploaded on first use.
+struct ExtTablesHost;
+namespace dev {
+struct ExtTables;
+}
+
+/// GF(q), q = p^k <= 256: one element per byte, encoded like the reference
+/// (include/gfrref/field.hpp:12-14: sum_i c_i p^i).  Mirrors reference
+/// FieldSpec (include/gfrref/field.hpp:20-110, src/field.cpp:143-237):
+/// FieldSpec(p) is the prime field, FieldSpec(p, k, modulus) the extension
+/// with a monic irreducible modulus (empty: the lexicographically first one,
+/// constant coefficient varying fastest).  Prime fields need p <= 251,
+/// extension fields p^k <= 256 (u8 storage; the reference allows p < 2^16,
+/// p^k < 2^20).  code(): the integer the C ABI passes as "p" -- p itself for
+/// a prime field, a registered id >= 0x10000 for an extension field
+/// (FieldSpec(code) resolves either).
 class FieldSpec {
  public:
-  explicit FieldSpec(std::uint32_t p);
+  explicit FieldSpec(std::uint32_t p_or_code);
+  FieldSpec(std::uint32_t p, std::uint32_t k, std::vector<std::uint32_t> modulus = {});
   std::uint32_t p() const { return p_; }
-  std::uint32_t order() const { return p_; }
-  Elem add(Elem a, Elem b) const { return (a + b) % p_; }
-  Elem neg(Elem a) const { return a == 0 ? 0 : p_ - a; }
-  Elem mul(Elem a, Elem b) const { return Elem(std::uint64_t(a) * b % p_); }
+  std::uint32_t k() const { return k_; }
+  std::uint32_t order() const { return q_; }
+  bool is_ext() const { return k_ > 1; }
+  std::uint32_t code() const;
+  const std::vector<std::uint32_t>& modulus() const;
+  Elem add(Elem a, Elem b) const;
+  Elem neg(Elem a) const;
+  Elem mul(Elem a, Elem b) const;
   Elem inv(Elem a) const;
-  bool operator==(const FieldSpec& o) const { return p_ == o.p_; }
-  std::string name() const { return "GF(" + std::to_string(p_) + ")"; }
+  bool operator==(const FieldSpec& o) const {
+    return p_ == o.p_ && k_ == o.k_ && modulus() == o.modulus();
+  }
+  std::string name() const {
+    return k_ == 1 ? "GF(" + std::to_string(p_) + ")"
+                   : "GF(" + std::to_string(p_) + "^" + std::to_string(k_) + ")";
+  }
+  /// Device tables (extension fields only; uploaded on first use).
+  const dev::ExtTables& ext_dev() const;
 
  private:
-  std::uint32_t p_;
+  std::uint32_t p_ = 0, k_ = 1, q_ = 0;
+  std::shared_ptr<const ExtTablesHost> ext_;
 };
+/// Reference default_modulus (src/field.cpp:125-138).
+std::vector<std::uint32_t> default_modulus(std::uint32_t p, std::uint32_t k);
 
 /// A stream-ordered device allocation (cudaMallocAsync pool).
 struct DevBuf {

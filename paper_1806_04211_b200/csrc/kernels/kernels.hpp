@@ -55,6 +55,36 @@ int mad_policy();
 void mad_counters(std::int64_t* simt, std::int64_t* tc);
 void reset_mad_counters();
 
+// ---------------------------------------------------------------- GF(p^k)
+// Extension field GF(q), q = p^k <= 256, elements as encoded bytes
+// (sum_i c_i p^i).  Tables live in device memory (FieldSpec::ext()).
+struct ExtTables {
+  std::uint32_t p, k, q;
+  const std::uint8_t* mul;  // q x q products
+  const std::uint8_t* add;  // q x q sums
+  const std::uint8_t* neg;  // q
+  const std::uint8_t* inv;  // q (inv[0] = 0)
+  const std::uint8_t* dig;  // q x k base-p digits
+  const std::uint8_t* red;  // (2k-1) x k digits of x^s mod the modulus
+};
+// D = (Cin ? Cin : 0) + A.B over GF(p^k) as ONE K1 contraction over GF(p):
+// A (m x K) is split into its digit planes, interleaved (m x kK, column
+// k.t + i = digit i of A[., t]); B (K x n) is expanded to the k x k blocks
+// of the multiplication-by-element maps (kK x kn: row k.t + i, column
+// k.j + u = sum_j' red[i + j'][u] . digit j' of B[t][j], mod p); the
+// interleaved digits of Cin are the addend; the m x kn digit result is
+// re-encoded into D.  scratch: mad_ext_scratch_bytes() bytes, 16-aligned.
+std::int64_t mad_ext_scratch_bytes(std::uint32_t k, std::int64_t m, std::int64_t n, std::int64_t K);
+void mad_ext(const ExtTables& f, std::int64_t m, std::int64_t n, std::int64_t K,
+             const std::uint8_t* A, std::int64_t lda, const std::uint8_t* B, std::int64_t ldb,
+             const std::uint8_t* Cin, std::int64_t ldc, std::uint8_t* D, std::int64_t ldd,
+             std::uint8_t* scratch, cudaStream_t s);
+// Base-case ECH of ech_base (rows, cols <= kEchBaseMax) over GF(p^k) with
+// table arithmetic (mul / add tables staged in shared memory).
+void ech_base_ext(const ExtTables& f, std::int64_t rows, std::int64_t cols, const std::uint8_t* H,
+                  std::int64_t ldh, std::uint8_t* W, std::int64_t ldw, std::uint8_t* Tc,
+                  std::int64_t ldt, std::int32_t* info, cudaStream_t s);
+
 // ---------------------------------------------------------------- K3/K4
 // dst[i][j] = source element chosen by the row map and the column map:
 //   rmap[i] >= 0 -> row rmap[i] of A;  rmap[i] <= -2 -> row (-rmap[i]-2) of B;

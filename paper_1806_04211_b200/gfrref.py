@@ -97,24 +97,79 @@ def _vp():
 
 # ---------------------------------------------------------------- values
 class FieldSpec:
-    """GF(p), p prime <= 251 (reference include/gfrref/field.hpp:20-110)."""
+    """GF(p) or GF(p^k) (reference include/gfrref/field.hpp:20-110).
 
-    def __init__(self, p: int):
-        p = int(p)
-        if p < 2 or any(p % d == 0 for d in range(2, int(p ** 0.5) + 1)):
-            raise ValueError("field: p must be prime")
-        if p > 251:
-            raise ValueError("field: the B200 path stores residues as u8 (p <= 251)")
-        self.p = p
+    ``FieldSpec(p)`` is the prime field (p <= 251 on the B200 path);
+    ``FieldSpec(p, k, modulus=None)`` the extension field with a monic
+    irreducible modulus ``[c0, ..., ck]`` (None: the reference's default,
+    the lexicographically first one), p**k <= 256.  Elements are encoded like
+    the reference, ``sum_i c_i p**i``, one byte each.  ``code`` is the integer
+    the C ABI takes as its field argument (p for a prime field).
+    """
+
+    def __init__(self, p: int, k: int = 1, modulus=None):
+        p, k = int(p), int(k)
+        if k == 1 and modulus is None:
+            if p < 2 or any(p % d == 0 for d in range(2, int(p ** 0.5) + 1)):
+                raise ValueError("field: p must be prime")
+            if p > 251:
+                raise ValueError("field: the B200 path stores residues as u8 (p <= 251)")
+            self.p, self.k, self.q, self.code = p, 1, p, p
+            self.modulus = (0, 1)
+            return
+        code = ctypes.c_uint32()
+        mod = None if modulus is None else (ctypes.c_uint32 * len(modulus))(*[int(c) for c in modulus])
+        _check(raw_lib().gfq_field_register(p, k, mod, 0 if modulus is None else len(modulus), ctypes.byref(code)))
+        self._from_code(code.value)
+
+    def _from_code(self, code: int):
+        p, k, q = ctypes.c_uint32(), ctypes.c_uint32(), ctypes.c_uint32()
+        mod = (ctypes.c_uint32 * 32)()
+        _check(raw_lib().gfq_field_info(code, ctypes.byref(p), ctypes.byref(k), ctypes.byref(q), mod))
+        self.p, self.k, self.q, self.code = p.value, k.value, q.value, code
+        self.modulus = tuple(mod[i] for i in range(self.k + 1))
+
+    @classmethod
+    def from_code(cls, code: int) -> "FieldSpec":
+        f = cls.__new__(cls)
+        f._from_code(int(code))
+        return f
 
     def order(self):
-        return self.p
+        return self.q
+
+    def _op(self, op, a, b=0):
+        out = ctypes.c_uint32()
+        _check(raw_lib().gfq_field_op(self.code, op, int(a), int(b), ctypes.byref(out)))
+        return out.value
+
+    def add(self, a, b):
+        return self._op(0, a, b)
+
+    def mul(self, a, b):
+        return self._op(1, a, b)
+
+    def neg(self, a):
+        return self._op(2, a)
+
+    def inv(self, a):
+        return self._op(3, a)
 
     def __eq__(self, o):
-        return isinstance(o, FieldSpec) and o.p == self.p
+        return isinstance(o, FieldSpec) and (o.p, o.k, o.modulus) == (self.p, self.k, self.modulus)
+
+    def __hash__(self):
+        return hash((self.p, self.k, self.modulus))
 
     def __repr__(self):
-        return f"GF({self.p})"
+        return f"GF({self.p})" if self.k == 1 else f"GF({self.p}^{self.k})"
+
+
+def default_modulus(p: int, k: int):
+    """Reference default_modulus (include/gfrref/field.hpp:118)."""
+    out = (ctypes.c_uint32 * (int(k) + 1))()
+    _check(raw_lib().gfq_default_modulus(int(p), int(k), out))
+    return list(out)
 
 
 class Matrix:
@@ -322,7 +377,7 @@ def mul(f: FieldSpec, b, c) -> Matrix:
     """reference jobs.hpp:40 -> K1"""
     b, c = _as_matrix(b), _as_matrix(c)
     h = _vp()
-    _check(lib().gfq_mul(f.p, b.h, c.h, ctypes.byref(h)))
+    _check(lib().gfq_mul(f.code, b.h, c.h, ctypes.byref(h)))
     return _mat(h)
 
 
@@ -330,7 +385,7 @@ def mad(f: FieldSpec, a, b, c) -> Matrix:
     """reference jobs.hpp:43 -> K1 (a + b.c)"""
     a, b, c = _as_matrix(a), _as_matrix(b), _as_matrix(c)
     h = _vp()
-    _check(lib().gfq_mad(f.p, a.h, b.h, c.h, ctypes.byref(h)))
+    _check(lib().gfq_mad(f.code, a.h, b.h, c.h, ctypes.byref(h)))
     return _mat(h)
 
 
@@ -358,7 +413,7 @@ def ech(f: FieldSpec, h, threshold: int = 256) -> EchResult:
     """reference jobs.hpp:50 -> K2 base case + K1/K3/K4 combines"""
     h = _as_matrix(h)
     M, K, R, rho, gam = _vp(), _vp(), _vp(), _vp(), _vp()
-    _check(lib().gfq_ech(f.p, h.h, threshold, *(ctypes.byref(x) for x in (M, K, R, rho, gam))))
+    _check(lib().gfq_ech(f.code, h.h, threshold, *(ctypes.byref(x) for x in (M, K, R, rho, gam))))
     return EchResult(_mat(M), _mat(K), _mat(R), IndexSet._take(rho), IndexSet._take(gam))
 
 
@@ -485,7 +540,7 @@ def clear_down(f: FieldSpec, C, D: Optional[PkgD], i: int, ech_threshold: int = 
         dp = ctypes.byref(D._struct(t)) if (D is not None and i > 0) else None
         if D is not None and i == 0:
             dp = None
-        _check(lib().gfq_clear_down(f.p, C.h, dp, i, ech_threshold, ctypes.byref(dout), ctypes.byref(aout)))
+        _check(lib().gfq_clear_down(f.code, C.h, dp, i, ech_threshold, ctypes.byref(dout), ctypes.byref(aout)))
     return PkgD._take(dout), PkgA._take(aout)
 
 
@@ -496,7 +551,7 @@ def update_row(f: FieldSpec, A: PkgA, C, B: Optional[Matrix], i: int):
     co, bo = _vp(), _vp()
     with _Temps() as t:
         a = A._struct(t)
-        _check(lib().gfq_update_row(f.p, ctypes.byref(a), C.h, _opt_h(B), i, ctypes.byref(co), ctypes.byref(bo)))
+        _check(lib().gfq_update_row(f.code, ctypes.byref(a), C.h, _opt_h(B), i, ctypes.byref(co), ctypes.byref(bo)))
     return _mat(co), _mat(bo)
 
 
@@ -508,7 +563,7 @@ def update_row_trafo(f: FieldSpec, A: PkgA, K: Optional[Matrix], M: Optional[Mat
     ko, mo = _vp(), _vp()
     with _Temps() as t:
         a, e = A._struct(t), E._struct(t)
-        _check(lib().gfq_update_row_trafo(f.p, ctypes.byref(a), _opt_h(K), _opt_h(M), ctypes.byref(e), i, h, j,
+        _check(lib().gfq_update_row_trafo(f.code, ctypes.byref(a), _opt_h(K), _opt_h(M), ctypes.byref(e), i, h, j,
                                           ctypes.byref(ko), ctypes.byref(mo)))
     return _mat(ko), _mat(mo)
 
@@ -547,7 +602,7 @@ def clear_up(f: FieldSpec, R, X, M) -> Matrix:
     """reference tasks.hpp:55 (R + X.M)"""
     R, X, M = _as_matrix(R), _as_matrix(X), _as_matrix(M)
     h = _vp()
-    _check(lib().gfq_clear_up(f.p, R.h, X.h, M.h, ctypes.byref(h)))
+    _check(lib().gfq_clear_up(f.code, R.h, X.h, M.h, ctypes.byref(h)))
     return _mat(h)
 
 
@@ -740,12 +795,12 @@ def echelonize(C, f: FieldSpec, options: EchelonizeOptions = None) -> EchelonOut
     h = _vp()
     if isinstance(C, Matrix):
         m, n = C.rows, C.cols
-        _check(lib().gfq_echelonize(f.p, C.h, ctypes.byref(o), ctypes.byref(h)))
+        _check(lib().gfq_echelonize(f.code, C.h, ctypes.byref(o), ctypes.byref(h)))
     else:
         a = np.ascontiguousarray(np.asarray(C, np.uint8))
         m, n = a.shape
         src = a if a.size else np.zeros(1, np.uint8)
-        _check(lib().gfq_echelonize_host(f.p, m, n, src.ctypes.data_as(_capi.c_u8p), max(n, 1), ctypes.byref(o),
+        _check(lib().gfq_echelonize_host(f.code, m, n, src.ctypes.data_as(_capi.c_u8p), max(n, 1), ctypes.byref(o),
                                          ctypes.byref(h)))
     return EchelonOutput(h, f, chop(m, n, options.block, options.remainder_first), options.with_transform)
 
@@ -793,7 +848,7 @@ def echelonize_dist(comm: Comm, f: FieldSpec, m: int, n: int, options: Echeloniz
     options = options or EchelonizeOptions()
     o = options._struct()
     h = _vp()
-    _check(lib().gfq_echelonize_dist(comm.h, f.p, C.h if C is not None else None, m, n, seed,
+    _check(lib().gfq_echelonize_dist(comm.h, f.code, C.h if C is not None else None, m, n, seed,
                                      ctypes.byref(o), int(gather), ctypes.byref(h)))
     return EchelonOutput(h, f, chop(m, n, options.block, options.remainder_first), options.with_transform)
 
@@ -803,13 +858,13 @@ def read_gfmat_file(path: str):
     p = ctypes.c_uint32()
     h = _vp()
     _check(lib().gfq_read_gfmat_file(os.fsencode(path), ctypes.byref(p), ctypes.byref(h)))
-    return FieldSpec(p.value), _mat(h)
+    return FieldSpec.from_code(p.value), _mat(h)
 
 
 def write_gfmat_file(path: str, f: FieldSpec, m) -> None:
     """reference write_gfmat_file (src/io.cpp:228), byte-identical."""
     m = _as_matrix(m)
-    _check(lib().gfq_write_gfmat_file(os.fsencode(path), f.p, m.h))
+    _check(lib().gfq_write_gfmat_file(os.fsencode(path), f.code, m.h))
 
 
 VERIFY_METHODS = {"auto": 0, "exact": 1, "freivalds": 2}
@@ -847,14 +902,14 @@ def dist_plan(m: int, n: int, block: int, with_transform: bool, world: int):
 def random_matrix(f: FieldSpec, rows: int, cols: int, seed: int) -> Matrix:
     """reference generate.hpp:33-35, generated on the device (K6)."""
     h = _vp()
-    _check(lib().gfq_random_matrix(f.p, rows, cols, seed, ctypes.byref(h)))
+    _check(lib().gfq_random_matrix(f.code, rows, cols, seed, ctypes.byref(h)))
     return _mat(h)
 
 
 def random_product_matrix(f: FieldSpec, rows: int, cols: int, inner: int, seed: int) -> Matrix:
     """reference generate.hpp:37-39 (K6 + K1)."""
     h = _vp()
-    _check(lib().gfq_random_product_matrix(f.p, rows, cols, inner, seed, ctypes.byref(h)))
+    _check(lib().gfq_random_product_matrix(f.code, rows, cols, inner, seed, ctypes.byref(h)))
     return _mat(h)
 
 

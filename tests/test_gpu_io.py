@@ -71,7 +71,9 @@ def test_gfmat_roundtrip_and_errors(G, tmp_path):
         "header": "GFMAT v2\nfield p=7 k=1\nrows=1 cols=1\n0\n",
         "entry": "GFMAT v1\nfield p=7 k=1\nrows=1 cols=2\n0 7\n",
         "count": "GFMAT v1\nfield p=7 k=1\nrows=2 cols=2\n0 1\n1\n",
-        "extension": "GFMAT v1\nfield p=2 k=2 modulus=1,1,1\nrows=1 cols=1\n0\n",
+        # GF(p^k) files load (tests/test_gpu_ext.py); these two fields do not
+        "reducible": "GFMAT v1\nfield p=2 k=2 modulus=1,0,1\nrows=1 cols=1\n0\n",
+        "u8_storage": "GFMAT v1\nfield p=11 k=3 modulus=4,1,0,1\nrows=1 cols=1\n0\n",
         "trailing": "GFMAT v1\nfield p=3 k=1\nrows=1 cols=1\n2\nextra\n",
     }
     for what, text in bad.items():
