@@ -349,8 +349,11 @@ PlanHandles build_plan_fused(TaskGraph& graph, const Mat& C, const FieldSpec& fi
       }
     }
   }
-  // Step 2 (M(j, h, a-1-h): part h of the row-(a-1) T_M panel, or the h = a-1 block)
-  if (with_transform)
+  // Step 2: one wide RowLengthen per j (c0 = -2) widening every part h of
+  // row j's T_M panel (row block a-1's panel + the M(j, a-1) block) into
+  // the panel MW(j, b)
+  static const bool rl_narrow = std::getenv("GFQ_RL_NARROW") != nullptr;  // A/B: per-h tasks
+  if (with_transform && rl_narrow)
     for (std::size_t j = 0; j < b; ++j)
       for (std::size_t h = 0; h < a; ++h) {
         const bool part = h + 1 < a;
@@ -360,6 +363,16 @@ PlanHandles build_plan_fused(TaskGraph& graph, const Mat& C, const FieldSpec& fi
                 e.slot(K::E, h, 0, 0, j), e.slot(K::E, h, 0, 0, b - 1)},
                {e.slot(K::M, j, h, 0, a - h)});
       }
+  if (with_transform && !rl_narrow)
+    for (std::size_t j = 0; j < b; ++j) {
+      std::vector<std::int32_t> in;
+      if (a > 1) in.push_back(e.slot(K::MT, j, 0, 0, a - 1));
+      in.push_back(e.slot(K::M, j, a - 1, 0, 0));
+      for (std::size_t h = 0; h < a; ++h) in.push_back(e.slot(K::E, h, 0, 0, j));
+      for (std::size_t h = 0; h < a; ++h) in.push_back(e.slot(K::E, h, 0, 0, b - 1));
+      e.node(T::RowLengthen, -2, std::int32_t(j), -1, plate(a + b - 1), in,
+             {e.slot(K::MW, j, b, 0, 0)});
+    }
   // Step 3
   for (std::size_t k = 0; k < b; ++k)
     e.node(T::Copy, -1, std::int32_t(k), -1, plate(a + b + (b - 1 - k)),
@@ -385,9 +398,12 @@ PlanHandles build_plan_fused(TaskGraph& graph, const Mat& C, const FieldSpec& fi
              {e.slot(K::RW, j, k, 0, 0)});
       if (with_transform) {
         std::vector<std::int32_t> min{sX};
-        if (k + 1 == b) {
+        if (k + 1 == b && rl_narrow) {
           for (std::size_t h = 0; h < a; ++h) min.push_back(e.slot(K::M, j, h, 0, a - h));
           for (std::size_t h = 0; h < a; ++h) min.push_back(e.slot(K::M, k, h, 0, a - h));
+        } else if (k + 1 == b) {
+          min.push_back(e.slot(K::MW, j, b, 0, 0));
+          min.push_back(e.slot(K::MW, k, b, 0, 0));
         } else {
           min.push_back(e.slot(K::MW, j, k + 1, 0, 0));
           min.push_back(e.slot(K::MW, k, k + 1, 0, 0));
@@ -417,10 +433,10 @@ PlanHandles build_plan_fused(TaskGraph& graph, const Mat& C, const FieldSpec& fi
     hd.m_part.assign(b, std::vector<std::int32_t>(a, -1));
     for (std::size_t j = 0; j < b; ++j)
       for (std::size_t h = 0; h < a; ++h) {
-        if (j + 1 == b) {
+        if (j + 1 == b && rl_narrow) {
           hd.m_final[j][h] = e.slot(K::M, j, h, 0, a - h);
         } else {
-          hd.m_final[j][h] = e.slot(K::MW, j, j + 1, 0, 0);
+          hd.m_final[j][h] = e.slot(K::MW, j, j + 1, 0, 0);  // j = b-1: the RowLengthen panel
           hd.m_part[j][h] = std::int32_t(h);
         }
       }

@@ -23,6 +23,13 @@ Mat select(std::int64_t rows, std::int64_t cols, const Mat& A, const Mat* B,
            const std::vector<std::int32_t>* rmap, const std::vector<std::int32_t>* cmap) {
   Mat out(rows, cols);
   if (out.empty()) return out;
+  // small maps ride in the launch parameters (no upload call)
+  static const bool inline_maps = std::getenv("GFQ_NO_INLINE_MAPS") == nullptr;
+  if (inline_maps &&
+      dev::select2d_inline(out.data(), out.ld(), rows, cols, A.data(), A.ld(), B ? B->data() : nullptr,
+                           B ? B->ld() : 0, rmap ? rmap->data() : nullptr,
+                           cmap ? cmap->data() : nullptr, cur_stream()))
+    return out;
   auto rb = rmap ? upload_i32(*rmap) : nullptr;
   auto cb = cmap ? upload_i32(*cmap) : nullptr;
   dev::select2d(out.data(), out.ld(), rows, cols, A.data(), A.ld(), B ? B->data() : nullptr,
@@ -97,6 +104,9 @@ Mat mat_mul(const FieldSpec& f, const Mat& b, const Mat& c) {
 
 Mat col_gather(const Mat& m, std::int64_t out_cols, const std::vector<std::int32_t>& cmap) {
   return select(m.rows(), out_cols, m, nullptr, nullptr, &cmap);
+}
+Mat col_gather2(const Mat& a, const Mat* b, std::int64_t out_cols, const std::vector<std::int32_t>& cmap) {
+  return select(a.rows(), out_cols, a, b, nullptr, &cmap);
 }
 
 void mad_into(const FieldSpec& f, const Mat& d, const Mat* addend, const Mat& b, const Mat& c) {

@@ -29,6 +29,8 @@ Mat mat_mul_add(const FieldSpec& f, const Mat& a, const Mat& b, const Mat& c);  
 void mad_into(const FieldSpec& f, const Mat& d, const Mat* addend, const Mat& b, const Mat& c);
 /// out[:, c] = m[:, cmap[c]] (cmap[c] = -1: zero column), one K3 launch.
 Mat col_gather(const Mat& m, std::int64_t out_cols, const std::vector<std::int32_t>& cmap);
+/// out[:, c] = a[:, cmap[c]] (>= 0), b[:, -cmap[c]-2] (<= -2) or 0 (-1); one K3 launch.
+Mat col_gather2(const Mat& a, const Mat* b, std::int64_t out_cols, const std::vector<std::int32_t>& cmap);
 
 /// Negative reduced echelonisation of one block (jobs.hpp:50).  Same
 /// recursion as the reference (split the longer dimension, combine), base

@@ -460,6 +460,106 @@ __global__ void set_entries_kernel(std::uint8_t* dst, std::int64_t ldd,
 }
 }  // namespace
 
+namespace {
+// select2d with the row / column maps passed IN the launch parameters
+// (int16 entries: rows first, then columns): no upload, so no extra CUDA
+// call on the host.  A block handles up to 2048 output columns (16 a thread)
+// for a strided set of rows; the column map is staged once per block in
+// shared memory, the row map is read uniformly per row.
+template <int CAP>
+__global__ void __launch_bounds__(128)
+select_inline_kernel(std::uint8_t* dst, std::int64_t ldd, std::int64_t rows, std::int64_t cols,
+                     const std::uint8_t* A, std::int64_t lda, const std::uint8_t* B,
+                     std::int64_t ldb, const __grid_constant__ InlineMaps<CAP> maps) {
+  __shared__ std::int32_t scm[2048];
+  const std::int64_t nr = maps.nr, nc = maps.nc;
+  const std::int64_t c0 = std::int64_t(blockIdx.x) * 2048;
+  const std::int64_t cn = cols - c0 < 2048 ? cols - c0 : 2048;
+  if (nc)
+    for (int e = threadIdx.x; e < cn; e += blockDim.x) scm[e] = maps.v[nr + c0 + e];
+  __syncthreads();
+  const std::int64_t j0 = c0 + 16 * threadIdx.x;
+  if (j0 >= cols) return;
+  const bool full = j0 + 16 <= cols;
+  for (std::int64_t i = blockIdx.y; i < rows; i += gridDim.y) {
+    const std::int32_t rv = nr ? maps.v[i] : std::int32_t(i);
+    const bool rowB = nr && rv <= -2;
+    const std::int64_t r = rowB ? -rv - 2 : rv;
+    const std::uint8_t* arow = (rv == -1 || rowB) ? nullptr : A + r * lda;
+    const std::uint8_t* brow = B ? B + (rowB ? r : (nr ? r : i)) * ldb : nullptr;
+    std::uint32_t w[4] = {0, 0, 0, 0};
+    if (rv != -1) {
+      if (!nc) {
+        const std::uint8_t* src = rowB ? brow : arow;
+        if (full) {
+          const uint4 x = *reinterpret_cast<const uint4*>(src + j0);
+          w[0] = x.x; w[1] = x.y; w[2] = x.z; w[3] = x.w;
+        } else {
+          for (int q = 0; q < 16; ++q)
+            if (j0 + q < cols) w[q >> 2] |= std::uint32_t(src[j0 + q]) << (8 * (q & 3));
+        }
+      } else {
+#pragma unroll
+        for (int q = 0; q < 16; ++q) {
+          if (j0 + q >= cols) break;
+          const std::int32_t cv = scm[16 * threadIdx.x + q];
+          std::uint32_t x = 0;
+          if (cv >= 0) x = rowB ? brow[cv] : arow[cv];
+          else if (cv <= -2) x = brow[-cv - 2];
+          w[q >> 2] |= x << (8 * (q & 3));
+        }
+      }
+    }
+    std::uint8_t* drow = dst + i * ldd + j0;
+    if (full) {
+      *reinterpret_cast<uint4*>(drow) = make_uint4(w[0], w[1], w[2], w[3]);
+    } else {
+      for (std::int64_t c = 0; c < cols - j0; ++c) drow[c] = std::uint8_t((w[c >> 2] >> (8 * (c & 3))) & 0xFF);
+    }
+  }
+}
+
+template <int CAP>
+bool launch_inline(std::uint8_t* dst, std::int64_t ldd, std::int64_t rows, std::int64_t cols,
+                   const std::uint8_t* A, std::int64_t lda, const std::uint8_t* B, std::int64_t ldb,
+                   const std::int32_t* rmap, const std::int32_t* cmap, cudaStream_t s) {
+  InlineMaps<CAP> m;
+  m.nr = rmap ? std::int32_t(rows) : 0;
+  m.nc = cmap ? std::int32_t(cols) : 0;
+  for (std::int64_t i = 0; i < m.nr; ++i) m.v[i] = std::int16_t(rmap[i]);
+  for (std::int64_t j = 0; j < m.nc; ++j) m.v[m.nr + j] = std::int16_t(cmap[j]);
+  const unsigned gx = unsigned((cols + 2047) / 2048);
+  const unsigned gy = unsigned(rows < 64 ? rows : 64);
+  select_inline_kernel<CAP><<<dim3(gx, gy), 128, 0, s>>>(dst, ldd, rows, cols, A, lda, B, ldb, m);
+  GFQ_CUDA(cudaGetLastError());
+  count_launch();
+  return true;
+}
+}  // namespace
+
+bool select2d_inline(std::uint8_t* dst, std::int64_t ldd, std::int64_t rows, std::int64_t cols,
+                     const std::uint8_t* A, std::int64_t lda, const std::uint8_t* B,
+                     std::int64_t ldb, const std::int32_t* rmap, const std::int32_t* cmap,
+                     cudaStream_t s) {
+  if (rows == 0 || cols == 0) return true;
+  const std::int64_t n = (rmap ? rows : 0) + (cmap ? cols : 0);
+  const auto al = [](const void* ptr, std::int64_t ld) {
+    return ptr == nullptr || ((reinterpret_cast<std::uintptr_t>(ptr) & 15) == 0 && (ld & 15) == 0);
+  };
+  if (n > 4096 || !al(dst, ldd) || rows > 65535 * 64 || (!cmap && !(al(A, lda) && al(B, ldb))))
+    return false;
+  const auto fits = [](const std::int32_t* m, std::int64_t k) {
+    for (std::int64_t i = 0; i < k; ++i)
+      if (m[i] < -32768 || m[i] > 32767) return false;
+    return true;
+  };
+  if ((rmap && !fits(rmap, rows)) || (cmap && !fits(cmap, cols))) return false;
+  hprof::Scope hp(hprof::kSelect);
+  if (n <= 512) return launch_inline<512>(dst, ldd, rows, cols, A, lda, B, ldb, rmap, cmap, s);
+  if (n <= 1536) return launch_inline<1536>(dst, ldd, rows, cols, A, lda, B, ldb, rmap, cmap, s);
+  return launch_inline<4096>(dst, ldd, rows, cols, A, lda, B, ldb, rmap, cmap, s);
+}
+
 void select2d(std::uint8_t* dst, std::int64_t ldd, std::int64_t rows,
               std::int64_t cols, const std::uint8_t* A, std::int64_t lda,
               const std::uint8_t* B, std::int64_t ldb, const std::int32_t* rmap,

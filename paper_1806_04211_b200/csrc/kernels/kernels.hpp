@@ -97,6 +97,20 @@ void select2d(std::uint8_t* dst, std::int64_t ldd, std::int64_t rows,
               const std::uint8_t* B, std::int64_t ldb, const std::int32_t* rmap,
               const std::int32_t* cmap, cudaStream_t s);
 
+// select2d with HOST maps carried in the launch parameters (int16 entries,
+// rows + cols <= 4096; no upload).  Returns false (nothing launched) when
+// the maps do not fit or dst is not 16-byte aligned; the caller then
+// uploads the maps and calls select2d.
+template <int CAP>
+struct InlineMaps {
+  std::int32_t nr, nc;
+  std::int16_t v[CAP];
+};
+bool select2d_inline(std::uint8_t* dst, std::int64_t ldd, std::int64_t rows, std::int64_t cols,
+                     const std::uint8_t* A, std::int64_t lda, const std::uint8_t* B,
+                     std::int64_t ldb, const std::int32_t* rmap, const std::int32_t* cmap,
+                     cudaStream_t s);
+
 // dst[pos[2q]][pos[2q+1]] = value for q < n  (identity planting, adi).
 void set_entries(std::uint8_t* dst, std::int64_t ldd, const std::int32_t* pos,
                  std::int64_t n, std::uint8_t value, cudaStream_t s);

@@ -2,10 +2,28 @@
 // the GF(2) row-layout pivot step) on one SM (does not ship).
 #include <cstdio>
 #include <cstdint>
-template <int NT>
+__shared__ volatile int g_stop;
+template <int NT, int MODE>
 __global__ void __launch_bounds__(NT, 1) k(long long* out, unsigned seed, int iters) {
   const int lane = threadIdx.x & 31;
-  if (threadIdx.x >= 32) { __syncthreads(); return; }
+  __shared__ unsigned buf[4096];
+  if (threadIdx.x == 0) g_stop = 0;
+  for (int i = threadIdx.x; i < 4096; i += NT) buf[i] = i * 2654435761u;
+  __syncthreads();
+  if (threadIdx.x >= 32) {
+    if (MODE == 1) {  // smem traffic like the stripe update
+      unsigned acc = threadIdx.x;
+      while (!g_stop) {
+#pragma unroll 8
+        for (int q = 0; q < 64; ++q) acc ^= buf[(acc + q * 33) & 4095];
+      }
+      if (acc == 12345) out[7] = acc;
+    } else if (MODE == 2) {  // spin on a shared flag
+      while (!g_stop) {}
+    }
+    __syncthreads();
+    return;
+  }
   unsigned v = seed * (lane + 1);
   long long t0 = clock64();
   for (int i = 0; i < iters; ++i) v = __shfl_sync(0xffffffffu, v, (v + i) & 31) + 1;
@@ -67,6 +85,7 @@ __global__ void __launch_bounds__(NT, 1) k(long long* out, unsigned seed, int it
   if (lane == 0) {
     out[0] = t1 - t0; out[1] = t2 - t1; out[2] = t3 - t2; out[3] = w0 ^ w1 ^ k0 ^ k1 ^ v ^ b ^ tot;
     out[4] = t4 - t3;
+    g_stop = 1;
   }
   __syncthreads();
 }
@@ -75,8 +94,12 @@ int main() {
   long long h[5];
   const int iters = 4096;
   for (int rep = 0; rep < 4; ++rep) {
-    if (rep < 2) k<32><<<1, 32>>>(d, 12345 + rep, iters);
-    else k<1024><<<1, 1024>>>(d, 12345 + rep, iters);
+    const char* names[4] = {"32 thr", "1024 idle", "1024 smem-busy", "1024 spin"};
+    printf("%-16s ", names[rep]);
+    if (rep == 0) k<32, 0><<<1, 32>>>(d, 12345 + rep, iters);
+    else if (rep == 1) k<1024, 0><<<1, 1024>>>(d, 12345 + rep, iters);
+    else if (rep == 2) k<1024, 1><<<1, 1024>>>(d, 12345 + rep, iters);
+    else k<1024, 2><<<1, 1024>>>(d, 12345 + rep, iters);
     cudaMemcpy(h, d, sizeof h, cudaMemcpyDeviceToHost);
     printf("per iter cycles: shfl chain %.1f  vote chain %.1f  gf2 row step %.1f  kernel-shape %.1f\n", double(h[0]) / iters,
            double(h[1]) / iters, double(h[2]) / iters, double(h[4]) / iters);
