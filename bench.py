@@ -316,11 +316,13 @@ def main():
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             e0.record()
             if comm is None:
-                out = G.echelonize(Ch.numpy(), f, opts)  # H2D inside the call
+                # H2D inside the call; every output block streams into the
+                # pinned `dl` as soon as it is final (D2H overlaps Step 3)
+                out = G.echelonize(Ch.numpy(), f, opts, host_out=dl.numpy())
             else:
                 out = step(Cin=G.Matrix.from_numpy(Ch.numpy()), gather=True)
-            if rank == 0:
-                out.download_blocks(dl.numpy())
+                if rank == 0:
+                    out.download_blocks(dl.numpy())
             sel_bytes = 4 * out.rank * 2
             e1.record()
             e1.synchronize()
@@ -334,7 +336,7 @@ def main():
         e2e = {"value": work / (e_ms / 1e3), "unit": UNIT,
                "h2d_bytes_per_step": world * cfg["m"] * cfg["n"],
                "d2h_bytes_per_step": int(nbytes + sel_bytes), "ms_per_step": e_ms,
-               "path": "gfq_echelonize_host (pinned host C -> HBM) + gfq_output_download_blocks" if comm is None
+               "path": "gfq_echelonize_host_into (pinned host C -> HBM, every output block -> pinned host as it becomes final)" if comm is None
                else "each rank uploads pinned host C, gfq_echelonize_dist(gather), rank 0 downloads all blocks"}
 
     # ---------------- roofline of the dominant kernel (K1 tcgen05 contraction)

@@ -211,6 +211,13 @@ int gfq_echelonize(uint32_t p, const gfq_mat* C, const gfq_options* opt, gfq_out
 /* Same, input in host memory (copied to HBM inside the call). */
 int gfq_echelonize_host(uint32_t p, int64_t m, int64_t n, const uint8_t* C, int64_t ld,
                         const gfq_options* opt, gfq_output** out);
+/* Same, and every output block also lands in host_out (gfq_output_download_blocks'
+ * layout, cap bytes; pinned memory recommended): each block is copied as soon
+ * as it is final, so the download overlaps the back-substitution (Step 3).
+ * The buffer is complete when the call returns. */
+int gfq_echelonize_host_into(uint32_t p, int64_t m, int64_t n, const uint8_t* C, int64_t ld,
+                             const gfq_options* opt, uint8_t* host_out, uint64_t cap,
+                             gfq_output** out);
 
 int gfq_output_rank(const gfq_output* o, uint64_t* rank);
 int gfq_output_grid(const gfq_output* o, uint64_t* a, uint64_t* b);

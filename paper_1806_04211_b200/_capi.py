@@ -107,6 +107,7 @@ PROTOS = {
     "gfq_options_default": (None, [_P(Options)]),
     "gfq_echelonize": (I, [U32, vp, _P(Options), vpp]),
     "gfq_echelonize_host": (I, [U32, I64, I64, c_u8p, I64, _P(Options), vpp]),
+    "gfq_echelonize_host_into": (I, [U32, I64, I64, c_u8p, I64, _P(Options), c_u8p, U64, vpp]),
     "gfq_output_rank": (I, [vp, c_u64p]),
     "gfq_output_grid": (I, [vp, c_u64p, c_u64p]),
     "gfq_output_select": (I, [vp, I, U64, c_u32p, c_u64p]),

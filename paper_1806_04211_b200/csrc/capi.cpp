@@ -534,6 +534,25 @@ int gfq_echelonize_host(uint32_t p, int64_t m, int64_t n, const uint8_t* C, int6
   });
 }
 
+int gfq_echelonize_host_into(uint32_t p, int64_t m, int64_t n, const uint8_t* C, int64_t ld,
+                             const gfq_options* opt, uint8_t* host_out, uint64_t cap,
+                             gfq_output** out) {
+  return guard([&] {
+    require_device();
+    const gfq::FieldSpec f(p);
+    if (m < 0 || n < 0 || (m > 0 && n > 0 && (!C || ld < n)))
+      throw std::invalid_argument("echelonize_host: bad matrix arguments");
+    if (!host_out) throw std::invalid_argument("echelonize_host_into: null output buffer");
+    gfq::EchelonizeOptions o = to_opts(opt);
+    o.host_out = host_out;
+    o.host_out_cap = cap;
+    gfq::RunReport rep;
+    auto res = std::make_unique<gfq_output>(gfq::echelonize_host(C, m, n, ld, f, o, &rep));
+    res->report = std::move(rep);
+    *out = res.release();
+  });
+}
+
 int gfq_output_rank(const gfq_output* o, uint64_t* rank) {
   return guard([&] { *rank = O(o).out.rank; });
 }

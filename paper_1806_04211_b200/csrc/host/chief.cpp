@@ -3,6 +3,13 @@
 
 #include <algorithm>
 #include <cstdlib>
+#include <condition_variable>
+#include <deque>
+#include <memory>
+#include <mutex>
+#include <thread>
+#include <unordered_map>
+#include <unordered_set>
 #include <numeric>
 #include <string>
 #include <stdexcept>
@@ -454,6 +461,164 @@ PlanHandles build_plan_fused(TaskGraph& graph, const Mat& C, const FieldSpec& fi
 
 // ---------------------------------------------------------------- echelonize
 namespace {
+// Early output download (EchelonizeOptions::host_out): every final block is
+// copied D2H, in gfq_output_download_blocks' layout (R_blocks[j][l >= j],
+// T_M_blocks[j][h], T_K_blocks[i][h <= i]), the moment its slot is
+// published.  Block shapes follow from the final D (|gamma_j|) and E
+// (|rho_i|) packages, so copies start once the last of those is published
+// (end of Step 1) and the Step-3 blocks stream out as their rounds finish.
+class EarlyDownload {
+ public:
+  EarlyDownload(const PlanHandles& h, const ChopSpec& cs, bool with_transform, std::uint8_t* host,
+                std::uint64_t cap)
+      : h_(h), cs_(cs), host_(host), cap_(cap) {
+    const std::size_t a = cs.a(), b = cs.b();
+    for (std::size_t j = 0; j < b; ++j)
+      for (std::size_t l = j; l < b; ++l)
+        add(0, j, l, h.r_final[j][l], h.r_part.empty() ? -1 : h.r_part[j][l]);
+    if (with_transform) {
+      for (std::size_t j = 0; j < b; ++j)
+        for (std::size_t hh = 0; hh < a; ++hh)
+          add(1, j, hh, h.m_final[j][hh], h.m_part.empty() ? -1 : h.m_part[j][hh]);
+      for (std::size_t i = 0; i < a; ++i)
+        for (std::size_t hh = 0; hh <= i; ++hh)
+          add(2, i, hh, h.k_final[i][hh], h.k_part.empty() ? -1 : h.k_part[i][hh]);
+    }
+    for (auto sid : h.d_final) interest_.insert(sid);
+    for (auto sid : h.e_final) interest_.insert(sid);
+    GFQ_CUDA(cudaGetDevice(&device_));
+    GFQ_CUDA(cudaStreamCreateWithFlags(&stream_, cudaStreamNonBlocking));
+    thread_ = std::thread([this] { loop(); });
+  }
+  ~EarlyDownload() {
+    try {
+      finish();
+    } catch (...) {
+      // an error was already reported (or the run itself failed)
+    }
+    cudaStreamDestroy(stream_);
+  }
+  // RunOptions::on_publish (executor lock held): queue interesting slots
+  void publish(std::int32_t sid, const std::shared_ptr<Published>& pub) {
+    if (!interest_.count(sid)) return;
+    std::lock_guard<std::mutex> lk(mtx_);
+    q_.emplace_back(sid, pub);
+    cv_.notify_one();
+  }
+  // after run(): drain, wait for the copies, rethrow a failure
+  void finish() {
+    if (thread_.joinable()) {
+      {
+        std::lock_guard<std::mutex> lk(mtx_);
+        done_ = true;
+        cv_.notify_one();
+      }
+      thread_.join();
+      GFQ_CUDA(cudaStreamSynchronize(stream_));
+    }
+    if (!error_.empty()) throw std::runtime_error("early download: " + error_);
+  }
+
+ private:
+  struct Blk {
+    int kind;
+    std::size_t x, y;
+    std::int32_t slot, part;
+    std::uint64_t off = 0, rows = 0, cols = 0;
+  };
+  void add(int kind, std::size_t x, std::size_t y, std::int32_t slot, std::int32_t part) {
+    by_slot_[slot].push_back(blocks_.size());
+    blocks_.push_back(Blk{kind, x, y, slot, part});
+    interest_.insert(slot);
+  }
+  void loop() {
+    cudaSetDevice(device_);
+    set_cur_stream(stream_);
+    try {
+      for (;;) {
+        std::pair<std::int32_t, std::shared_ptr<Published>> item;
+        {
+          std::unique_lock<std::mutex> lk(mtx_);
+          cv_.wait(lk, [&] { return done_ || !q_.empty(); });
+          if (q_.empty()) return;
+          item = std::move(q_.front());
+          q_.pop_front();
+        }
+        pubs_[item.first] = item.second;
+        if (!layout_) {
+          bool all = true;
+          for (auto sid : h_.d_final) all = all && pubs_.count(sid);
+          for (auto sid : h_.e_final) all = all && pubs_.count(sid);
+          if (!all) continue;
+          make_layout();
+          for (const auto& kv : pubs_) issue(kv.first, *kv.second);
+        } else {
+          issue(item.first, *item.second);
+        }
+      }
+    } catch (const std::exception& e) {
+      error_ = e.what();
+    }
+  }
+  void make_layout() {
+    const auto gam = [&](std::size_t j) { return std::get<PkgD>(pubs_[h_.d_final[j]]->value).gamma.size(); };
+    const auto rho = [&](std::size_t i) { return std::get<PkgE>(pubs_[h_.e_final[i]]->value).rho.size(); };
+    std::uint64_t off = 0;
+    for (auto& bk : blocks_) {
+      if (bk.kind == 0) {
+        bk.rows = gam(bk.x);
+        bk.cols = cs_.col_parts[bk.y] - gam(bk.y);
+      } else if (bk.kind == 1) {
+        bk.rows = gam(bk.x);
+        bk.cols = rho(bk.y);
+      } else {
+        bk.rows = cs_.row_parts[bk.x] - rho(bk.x);
+        bk.cols = rho(bk.y);
+      }
+      bk.off = off;
+      off += bk.rows * bk.cols;
+    }
+    if (off > cap_) throw std::invalid_argument("host_out buffer too small");
+    layout_ = true;
+  }
+  void issue(std::int32_t sid, const Published& pub) {
+    auto it = by_slot_.find(sid);
+    if (it == by_slot_.end()) return;
+    bool waited = false;
+    for (std::size_t bi : it->second) {
+      const Blk& bk = blocks_[bi];
+      if (!bk.rows || !bk.cols) continue;
+      const Mat m = bk.part < 0 ? std::get<Mat>(pub.value)
+                                : std::get<MatParts>(pub.value).part(std::size_t(bk.part));
+      if (std::uint64_t(m.rows()) != bk.rows || std::uint64_t(m.cols()) != bk.cols)
+        throw std::logic_error("output block shape disagrees with the layout");
+      if (!waited && pub.ready) GFQ_CUDA(cudaStreamWaitEvent(stream_, pub.ready->ev, 0));
+      waited = true;
+      GFQ_CUDA(cudaMemcpy2DAsync(host_ + bk.off, std::size_t(bk.cols), m.data(), std::size_t(m.ld()),
+                                 std::size_t(bk.cols), std::size_t(bk.rows), cudaMemcpyDeviceToHost,
+                                 stream_));
+    }
+  }
+
+  const PlanHandles& h_;
+  const ChopSpec& cs_;
+  std::uint8_t* host_;
+  std::uint64_t cap_;
+  std::vector<Blk> blocks_;
+  std::unordered_map<std::int32_t, std::vector<std::size_t>> by_slot_;
+  std::unordered_set<std::int32_t> interest_;
+  std::unordered_map<std::int32_t, std::shared_ptr<Published>> pubs_;
+  bool layout_ = false;
+  int device_ = 0;
+  cudaStream_t stream_ = nullptr;
+  std::mutex mtx_;
+  std::condition_variable cv_;
+  std::deque<std::pair<std::int32_t, std::shared_ptr<Published>>> q_;
+  bool done_ = false;
+  std::string error_;
+  std::thread thread_;
+};
+
 EchelonOutput echelonize_impl(const Mat& C, const FieldSpec& field, const EchelonizeOptions& options,
                               RunReport* report,
                               const std::vector<std::shared_ptr<EventBox>>* row_ready);
@@ -553,7 +718,16 @@ EchelonOutput echelonize_impl(const Mat& C, const FieldSpec& field, const Echelo
   ro.workers = options.threads;
   ro.collect_trace = options.collect_trace;
   ro.retain_all = options.retain_all;
+  std::unique_ptr<EarlyDownload> early;
+  if (options.host_out) {
+    early = std::make_unique<EarlyDownload>(h, cs, options.with_transform, options.host_out,
+                                            options.host_out_cap);
+    ro.on_publish = [&early](std::int32_t sid, const std::shared_ptr<Published>& pub) {
+      early->publish(sid, pub);
+    };
+  }
   RunReport rep = run(graph, ro);
+  if (early) early->finish();
   if (report) *report = std::move(rep);
 
   for (std::size_t j = 0; j < b; ++j) {

@@ -72,6 +72,11 @@ struct EchelonizeOptions {
   bool collect_trace = false;
   bool retain_all = false;
   bool fuse = true;  // wide UpdateRow / ClearUp jobs (single GPU); false = the reference's task grid
+  // Optional pinned host buffer receiving every output block in
+  // gfq_output_download_blocks' layout, each block copied (on its own copy
+  // stream) as soon as it is final -- the download overlaps Step 3.
+  std::uint8_t* host_out = nullptr;
+  std::uint64_t host_out_cap = 0;
 };
 
 /// The fused single-GPU plan (same values, wide jobs per panel).  With

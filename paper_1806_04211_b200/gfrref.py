@@ -787,12 +787,24 @@ class EchelonOutput:
                      dev_start_ns=int(ds[q]), dev_end_ns=int(de[q])) for q in range(cnt)]
 
 
-def echelonize(C, f: FieldSpec, options: EchelonizeOptions = None) -> EchelonOutput:
+def echelonize(C, f: FieldSpec, options: EchelonizeOptions = None, host_out=None) -> EchelonOutput:
     """reference chief.hpp:88-90.  C: a device ``Matrix`` or a host uint8
-    array (copied to HBM inside the call)."""
+    array (copied to HBM inside the call).  host_out (host C only): a uint8
+    array of at least block_bytes() bytes receiving every output block in
+    download_blocks' layout, each copied as soon as it is final."""
     options = options or EchelonizeOptions()
     o = options._struct()
     h = _vp()
+    if host_out is not None:
+        if isinstance(C, Matrix):
+            raise ValueError("echelonize: host_out needs a host input")
+        a = np.ascontiguousarray(np.asarray(C, np.uint8))
+        m, n = a.shape
+        src = a if a.size else np.zeros(1, np.uint8)
+        _check(lib().gfq_echelonize_host_into(f.code, m, n, src.ctypes.data_as(_capi.c_u8p), max(n, 1),
+                                              ctypes.byref(o), host_out.ctypes.data_as(_capi.c_u8p),
+                                              host_out.nbytes, ctypes.byref(h)))
+        return EchelonOutput(h, f, chop(m, n, options.block, options.remainder_first), options.with_transform)
     if isinstance(C, Matrix):
         m, n = C.rows, C.cols
         _check(lib().gfq_echelonize(f.code, C.h, ctypes.byref(o), ctypes.byref(h)))

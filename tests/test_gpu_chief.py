@@ -255,3 +255,25 @@ def test_fused_plan_matches_reference_grid(G, p, m, n, block, kind, wt):
         assert "UpdateRowW" in kinds and "ClearUpRW" in kinds
     if wt and a > 1:
         assert "UpdateRowTrafoW" in kinds
+
+
+@pytest.mark.parametrize("p,m,n,block,kind,wt,fuse", [
+    (2, 300, 260, 64, "random", True, True), (7, 250, 310, 48, "product", True, True),
+    (3, 200, 200, 50, "random", False, True), (251, 130, 170, 40, "random", True, False),
+    (2, 96, 96, 96, "random", True, True)])
+def test_early_download_matches_download_blocks(G, p, m, n, block, kind, wt, fuse):
+    """echelonize(host C, host_out=buf) streams every final block into buf
+    while Step 3 runs; the bytes equal gfq_output_download_blocks'."""
+    C = oracle.random_matrix(p, m, n, 4) if kind == "random" else oracle.random_product_matrix(p, m, n, 30, 4)
+    opts = G.EchelonizeOptions(block=block, threads=3, with_transform=wt, fuse=fuse)
+    ref = G.echelonize(C, G.FieldSpec(p), opts)
+    want = np.zeros(ref.block_bytes(), np.uint8)
+    ref.download_blocks(want)
+    buf = np.full(ref.block_bytes() + 7, 0xAB, np.uint8)
+    out = G.echelonize(C, G.FieldSpec(p), opts, host_out=buf)
+    assert out.rank == ref.rank
+    np.testing.assert_array_equal(buf[: want.size], want)
+    assert (buf[want.size:] == 0xAB).all()
+    if want.size:
+        with pytest.raises(Exception, match="too small"):
+            G.echelonize(C, G.FieldSpec(p), opts, host_out=np.zeros(want.size - 1, np.uint8))
