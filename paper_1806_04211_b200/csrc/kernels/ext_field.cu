@@ -34,26 +34,47 @@ __global__ void ext_split_kernel(std::uint32_t k, const std::uint8_t* __restrict
     }
 }
 
-// Bexp[k.t + i][k.j + u] = sum_{j'} red[i + j'][u] . digit j' of B[t][j]  (mod p)
+// Bexp[k.t + i][k.j + u] = sum_{j'} red[i + j'][u] . digit j' of B[t][j]  (mod p).
+// One thread writes 16 consecutive bytes of one Bexp row (a 16-byte store);
+// the k x k x k coefficients red[i + j'][u] sit in shared memory.
 __global__ void ext_expand_kernel(std::uint32_t p, std::uint32_t k,
                                   const std::uint8_t* __restrict__ dig,
                                   const std::uint8_t* __restrict__ red, std::int64_t K,
                                   std::int64_t n, const std::uint8_t* __restrict__ B,
                                   std::int64_t ldb, std::uint8_t* __restrict__ E,
                                   std::int64_t lde) {
-  for (std::int64_t t = blockIdx.y; t < K; t += gridDim.y)
-    for (std::int64_t j = blockIdx.x * std::int64_t(blockDim.x) + threadIdx.x; j < n;
-         j += std::int64_t(gridDim.x) * blockDim.x) {
-      const std::uint8_t* bd = dig + std::uint32_t(B[t * ldb + j]) * k;
-      for (std::uint32_t i = 0; i < k; ++i) {
-        std::uint8_t* o = E + (t * k + i) * lde + j * k;
-        for (std::uint32_t u = 0; u < k; ++u) {
-          std::uint32_t acc = 0;
-          for (std::uint32_t jj = 0; jj < k; ++jj) acc += std::uint32_t(red[(i + jj) * k + u]) * bd[jj];
-          o[u] = std::uint8_t(acc % p);
+  __shared__ std::uint8_t cf[8][8][8];  // cf[i][u][j'] = red[i + j'][u]
+  for (std::uint32_t e = threadIdx.x; e < k * k * k; e += blockDim.x) {
+    const std::uint32_t i = e / (k * k), u = (e / k) % k, jj = e % k;
+    cf[i][u][jj] = red[(i + jj) * k + u];
+  }
+  __syncthreads();
+  const std::int64_t width = std::int64_t(k) * n, nch = (width + 15) / 16;
+  for (std::int64_t row = blockIdx.y; row < K * k; row += gridDim.y) {
+    const std::int64_t t = row / k;
+    const std::uint32_t i = std::uint32_t(row % k);
+    const std::uint8_t* brow = B + t * ldb;
+    for (std::int64_t ch = blockIdx.x * std::int64_t(blockDim.x) + threadIdx.x; ch < nch;
+         ch += std::int64_t(gridDim.x) * blockDim.x) {
+      std::uint32_t w[4] = {0, 0, 0, 0};
+      const std::int64_t c0 = 16 * ch;
+      std::int64_t j = c0 / k;
+      std::uint32_t u = std::uint32_t(c0 % k);
+      const std::uint8_t* bd = dig + std::uint32_t(j < n ? brow[j] : 0) * k;
+      for (int q = 0; q < 16; ++q) {
+        if (c0 + q >= width) break;
+        std::uint32_t acc = 0;
+        for (std::uint32_t jj = 0; jj < k; ++jj) acc += std::uint32_t(cf[i][u][jj]) * bd[jj];
+        w[q >> 2] |= (acc % p) << (8 * (q & 3));
+        if (++u == k) {
+          u = 0;
+          ++j;
+          bd = dig + std::uint32_t(j < n ? brow[j] : 0) * k;
         }
       }
+      *reinterpret_cast<uint4*>(E + row * lde + c0) = make_uint4(w[0], w[1], w[2], w[3]);
     }
+  }
 }
 
 // dst[i][j] = sum_d src[i][k.j + d] p^d
@@ -190,7 +211,12 @@ void mad_ext(const ExtTables& f, std::int64_t m, std::int64_t n, std::int64_t K,
   if (K > 0) {
     ext_split_kernel<<<grid2(m, K), 128, 0, s>>>(k, f.dig, m, K, A, lda, A2, lda2);
     GFQ_CUDA(cudaGetLastError());
-    ext_expand_kernel<<<grid2(K, n), 128, 0, s>>>(f.p, k, f.dig, f.red, K, n, B, ldb, E, lde);
+    {
+      const std::int64_t nch = (std::int64_t(k) * n + 15) / 16, rows = K * k;
+      const dim3 g(unsigned((nch + 127) / 128 < 64 ? (nch + 127) / 128 : 64),
+                   unsigned(rows < 65535 ? rows : 65535));
+      ext_expand_kernel<<<g, 128, 0, s>>>(f.p, k, f.dig, f.red, K, n, B, ldb, E, lde);
+    }
     GFQ_CUDA(cudaGetLastError());
     count_launch(2);
   }
