@@ -199,6 +199,40 @@ def k1_traffic():
         return None
 
 
+def k1_isolated(G, p, peak):
+    """K1 alone on a quiet device: CUDA events around 20 back-to-back
+    launches (after 3 warm-ups) through gfq_mad_raw on the current stream,
+    tcgen05 path forced; shapes: the cfg2a block product (1024^3) and the
+    cfg4 block product (4096^3)."""
+    import torch
+    out = []
+    G.set_mad_policy(2)
+    try:
+        for (m, n, k) in [(1024, 1024, 1024), (4096, 4096, 4096)]:
+            A = torch.randint(0, p, (m, k), dtype=torch.uint8, device="cuda")
+            Bm = torch.randint(0, p, (k, n), dtype=torch.uint8, device="cuda")
+            D = torch.zeros((m, n), dtype=torch.uint8, device="cuda")
+            G.set_stream(torch.cuda.current_stream().cuda_stream)
+            call = lambda: G.mad_raw(p, m, n, k, A.data_ptr(), k, Bm.data_ptr(), n, D.data_ptr(), n,
+                                     D.data_ptr(), n)
+            for _ in range(3):
+                call()
+            torch.cuda.synchronize()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            for _ in range(20):
+                call()
+            e1.record()
+            e1.synchronize()
+            us = 1e3 * e0.elapsed_time(e1) / 20
+            tops = 2.0 * m * n * k / (us * 1e-6) / 1e12
+            out.append({"shape": f"{m}x{n}x{k}", "us": us, "tflops": tops, "frac": tops / peak})
+    finally:
+        G.set_mad_policy(0)
+        G.set_stream(0)
+    return out
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -361,6 +395,11 @@ def main():
                     f"over {args.steps} profiled steps run right after the timed region "
                     f"({sum(prof_ms) / max(1, len(prof_ms)):.2f} ms/step with events); launches on "
                     "concurrent worker streams overlap, so per-launch times include SM sharing"}
+
+    # K1 timed alone (no concurrent streams), CUDA events around back-to-back
+    # launches: the step's dominant shape and the cfg4 block shape
+    if rank == 0:
+        roof["isolated"] = k1_isolated(G, cfg["p"], peak)
 
     base = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
