@@ -533,18 +533,13 @@ ech_panel_win_kernel(std::uint32_t p, std::uint32_t magic, int rows, int c0, int
            StepOut{nullptr, nullptr});
 }
 
-// Two-level ECH, step part 1 (one CTA of kStepThreads = 8 warps): the
-// pivot chain of the 32-wide step at scratch column c0 on the 64-row window
-// from the first open row (the pivots all lie there when the step's panel
-// has full rank -- the chosen row is the FIRST open row with a nonzero).
-// Thread (row = tid / 4, quarter = tid % 4) holds 4 of the row's 16 state
-// words in registers: quarters 0-1 the 32 panel bytes, quarters 2-3 the
-// coefficients of the pivot rows' ORIGINAL values added to the row
-// (Gauss-Jordan with coefficient tracking; a pivot row is scaled by
-// -1/pivot).  Per column: the factor by a 4-lane shuffle, candidates by
-// ballot, two CTA barriers (candidate masks, normalised pivot row), then
-// every row's axpy.  A column with no window candidate while open rows lie
-// outside the window sends the step to the full CTA algorithm (panel_full).
+// Two-level ECH, step part 1 (one CTA of kChainThreads): the pivot chain of
+// the 32-wide step at scratch column c0 on the 64-row window from the first
+// open row (the pivots all lie there when the step's panel has full rank --
+// the chosen row is the FIRST open row with a nonzero).  Warp 0 runs the
+// chain alone, barrier-free (see the loop below); a column with no window
+// candidate while open rows lie outside the window sends the step to the
+// full CTA algorithm (panel_full, all threads).
 // Then
 //   * NT / Gpiv (StepOut) instead of G: G[new pivot q] = ĉ_q, G[other i] =
 //     seg_i[pc] . (I + Ĉ)  (the multipliers of ech_panel_kernel),
@@ -563,20 +558,8 @@ __device__ __forceinline__ void stamp(int k) {
     g_step_stamps[8 + k] = clock64();
   }
 }
-// 2 threads per window row (W half, K half), 32 state elements each
+// warp 0 runs the chain; the other warps join the fallback and the outputs
 constexpr int kChainThreads = 128;
-__device__ __forceinline__ std::uint32_t pick32(const std::uint32_t (&x)[32], int i) {
-  std::uint32_t a[16], b[8], c[4], d[2];
-#pragma unroll
-  for (int k = 0; k < 16; ++k) a[k] = sel(i & 16, x[k + 16], x[k]);
-#pragma unroll
-  for (int k = 0; k < 8; ++k) b[k] = sel(i & 8, a[k + 8], a[k]);
-#pragma unroll
-  for (int k = 0; k < 4; ++k) c[k] = sel(i & 4, b[k + 4], b[k]);
-#pragma unroll
-  for (int k = 0; k < 2; ++k) d[k] = sel(i & 2, c[k + 2], c[k]);
-  return sel(i & 1, d[1], d[0]);
-}
 __global__ void __launch_bounds__(kChainThreads, 1)
 ech_step_chain_kernel(std::uint32_t p, std::uint32_t magic, int rows, int c0, int wc, int n,
                       std::uint8_t* __restrict__ Z, std::int64_t ld, std::uint8_t* flags,
@@ -585,10 +568,10 @@ ech_step_chain_kernel(std::uint32_t p, std::uint32_t magic, int rows, int c0, in
                       std::uint8_t* BpT) {
   extern __shared__ __align__(16) std::uint8_t dsm[];
   __shared__ std::uint8_t invw[256];
-  __shared__ int s_lo, s_rold, s_open;
-  __shared__ __align__(16) float Pcand[2][kChainThreads / 32][64];
-  __shared__ float vcand[2][kChainThreads / 32];
-  __shared__ int cand[2][kChainThreads / 32];
+  __shared__ int s_lo, s_rold;
+  __shared__ __align__(16) float wrow[64];  // the column's pivot row (raw, then reduced)
+  __shared__ float s_v;
+  __shared__ int s_ok, s_r2;
   __shared__ int colq[kW];
   __shared__ std::uint8_t chatb[kW][kW];
   __shared__ int wpc[kW], wpr[kW], s_pr[kW];
@@ -611,18 +594,23 @@ ech_step_chain_kernel(std::uint32_t p, std::uint32_t magic, int rows, int c0, in
     if (lane == 0) {
       s_lo = lo;
       s_rold = info[0];
-      s_open = 0;
       *lo_state = lo;
     }
   }
   __syncthreads();
   const int lo = s_lo, r_old = s_rold;
-  const int row = tid >> 1, half = tid & 1, gi = lo + row;
-  // 32 state elements per thread (half 0: the panel bytes, half 1: the
-  // coefficients) as fp32 integers.  Updates are LAZY: x += f.y with f and
-  // the published pivot row y reduced (< p), so after <= 32 columns
-  // x < p + 32 (p-1)^2 < 2^24 stays exact; a value is reduced only when it
-  // is read as the column's factor, published as a pivot row, or output.
+  // ---- the window chain, in warp 0 alone (no CTA barriers): lane l holds
+  // window rows lo + l and lo + 32 + l, each as 32 panel elements (kept
+  // SHIFTED so the current column is element 0: no dynamic register
+  // indexing) and 32 coefficients (of the pivot rows' ORIGINAL values),
+  // all fp32 integers.  Updates are LAZY: x += f.y with f and the
+  // published pivot row y reduced (< p), so after <= 32 columns
+  // x < p + 32 (p-1)^2 < 2^24 stays exact.  Per column: two ballots pick
+  // the first open row with a nonzero; its lane stores the raw row to
+  // shared memory, the warp reduces it (two elements a lane) and plants the
+  // unit at coefficient r2; every lane applies x_i += f_i.(x_s + e_r2) with
+  // f_i = v_i.sc (f_s = sc - 1 on the pivot row), sc = -1/v_s -- normalising
+  // the pivot row and eliminating with it in one update.
   const float fp = float(p), invp = 1.0f / fp, roff = 0.5f * invp - 0.5f;
   // x mod p for 0 <= x < 2^24: (x + 0.5) / p lies 0.5/p away from an integer
   // boundary and the fp32 error of x.invp is below 0.25/p, so rounding
@@ -631,107 +619,146 @@ ech_step_chain_kernel(std::uint32_t p, std::uint32_t magic, int rows, int c0, in
     const float q = (fmaf(v, invp, roff) + 12582912.0f) - 12582912.0f;
     return fmaf(-fp, q, v);
   };
-  float x[32];
+  if (warp == 0) {
+    float w0[32], w1[32], k0[32], k1[32];
+    const int i0 = lo + lane, i1 = lo + 32 + lane;
+    bool open0 = i0 < rows && flags[i0] == 0, open1 = i1 < rows && flags[i1] == 0;
 #pragma unroll
-  for (int e = 0; e < 32; ++e) x[e] = 0.0f;
-  bool open = gi < rows && flags[gi] == 0;
-  if (half == 0 && gi < rows) {
-    const std::uint8_t* src = Z + std::int64_t(gi) * ld + c0;
-    if (wc == kW) {
-      const uint4 a = reinterpret_cast<const uint4*>(src)[0], b = reinterpret_cast<const uint4*>(src)[1];
-      const std::uint32_t ww[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
+    for (int e = 0; e < 32; ++e) w0[e] = w1[e] = k0[e] = k1[e] = 0.0f;
+    const auto load = [&](int gi, float (&w)[32]) {
+      if (gi >= rows) return;
+      const std::uint8_t* src = Z + std::int64_t(gi) * ld + c0;
+      if (wc == kW) {
+        const uint4 a = reinterpret_cast<const uint4*>(src)[0], b = reinterpret_cast<const uint4*>(src)[1];
+        const std::uint32_t ww[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
 #pragma unroll
-      for (int e = 0; e < 32; ++e) x[e] = float((ww[e >> 2] >> (8 * (e & 3))) & 0xFFu);
-    } else {
+        for (int e = 0; e < 32; ++e) w[e] = float((ww[e >> 2] >> (8 * (e & 3))) & 0xFFu);
+      } else {
 #pragma unroll
-      for (int e = 0; e < 32; ++e)
-        if (e < wc) x[e] = float(src[e]);
-    }
-  }
-  {
-    const unsigned b = __ballot_sync(0xffffffffu, open && half == 0);
-    if (lane == 0 && b) atomicAdd(&s_open, __popc(b));
-  }
-  __syncthreads();
-  const bool covers_all = s_open == rows - r_old;
-  stamp(1);
-  int r2 = 0, ok = 1, myq = -1;
-  // One barrier per column: every warp publishes its first candidate row's
-  // state (reduced, plus the unit at K index r2) before the barrier; after
-  // it all threads pick the first candidate s and, with sc = -1/v_s, apply
-  //   x_i += f_i.(x_s + e_r2),  f_i = v_i.sc (rows i != s),  f_s = sc - 1,
-  // i.e. w_i += f_i.w_s, k_i += f_i.(k_s + e_r2) and w_s = sc.w_s,
-  // k_s = sc.k_s + (sc - 1).e_r2 -- normalising the pivot row first and
-  // eliminating with it, without a second barrier or a branch.
+        for (int e = 0; e < 32; ++e)
+          if (e < wc) w[e] = float(src[e]);
+      }
+    };
+    load(i0, w0);
+    load(i1, w1);
+    const int open_in = __popc(__ballot_sync(0xffffffffu, open0)) + __popc(__ballot_sync(0xffffffffu, open1));
+    const bool covers_all = open_in == rows - r_old;
+    stamp(1);
+    int r2 = 0, ok = 1, q0 = -1, q1 = -1, mpc = 0, mpr = 0;
+    const unsigned lanebit = 1u << lane;
 #pragma unroll 1
-  for (int c = 0; c < wc; ++c) {
-    const int par = c & 1;
-    std::uint32_t xb[32];
+    for (int c = 0; c < wc; ++c) {
+      const float v0 = red(w0[0]), v1 = red(w1[0]);
+      const unsigned b0 = __ballot_sync(0xffffffffu, open0 && v0 != 0.0f);
+      const unsigned b1 = __ballot_sync(0xffffffffu, open1 && v1 != 0.0f);
+      // the shifted panel moves on whether or not the column has a pivot
+      if (!(b0 | b1)) {
+        if (!covers_all) {
+          ok = 0;
+          break;
+        }
 #pragma unroll
-    for (int e = 0; e < 32; ++e) xb[e] = __float_as_uint(x[e]);
-    const float vf = red(__shfl_sync(0xffffffffu, __uint_as_float(pick32(xb, c)), lane & ~1));
-    const int vi = int(vf);
-    const unsigned b = __ballot_sync(0xffffffffu, half == 0 && open && vi != 0);
-    const int wrow = b ? 16 * warp + ((__ffs(b) - 1) >> 1) : 0x7FFFFFFF;
-    if (row == wrow) {
-      float* dst = Pcand[par][warp] + 32 * half;
+        for (int e = 0; e < 31; ++e) {
+          w0[e] = w0[e + 1];
+          w1[e] = w1[e + 1];
+        }
+        w0[31] = w1[31] = 0.0f;
+        continue;  // a free column
+      }
+      const bool hi = b0 == 0;
+      const unsigned bb = hi ? b1 : b0;
+      const bool mine = (bb & (0u - bb) & lanebit) != 0;
+      // the pivot lane publishes its raw row: 32 panel + 32 coefficient values
+      // (two predicated store runs, no per-element selects)
+      float4* dst = reinterpret_cast<float4*>(wrow);
+      if (mine && !hi) {
 #pragma unroll
-      for (int e = 0; e < 8; ++e)
-        reinterpret_cast<float4*>(dst)[e] =
-            make_float4(red(x[4 * e]), red(x[4 * e + 1]), red(x[4 * e + 2]), red(x[4 * e + 3]));
-      if (half == 0) vcand[par][warp] = float(p - invw[vi]);
+        for (int e = 0; e < 8; ++e) {
+          dst[e] = make_float4(w0[4 * e], w0[4 * e + 1], w0[4 * e + 2], w0[4 * e + 3]);
+          dst[8 + e] = make_float4(k0[4 * e], k0[4 * e + 1], k0[4 * e + 2], k0[4 * e + 3]);
+        }
+        s_v = v0;
+      }
+      if (mine && hi) {
+#pragma unroll
+        for (int e = 0; e < 8; ++e) {
+          dst[e] = make_float4(w1[4 * e], w1[4 * e + 1], w1[4 * e + 2], w1[4 * e + 3]);
+          dst[8 + e] = make_float4(k1[4 * e], k1[4 * e + 1], k1[4 * e + 2], k1[4 * e + 3]);
+        }
+        s_v = v1;
+      }
+      __syncwarp();
+      // reduce the published row, two elements a lane; plant e_r2 (that
+      // coefficient is still 0 in every row)
+      wrow[lane] = red(wrow[lane]);
+      wrow[32 + lane] = lane == r2 ? 1.0f : red(wrow[32 + lane]);
+      __syncwarp();
+      const float sc = float(p - invw[int(s_v)]);
+      float y[64];
+      {
+        const float4* src = reinterpret_cast<const float4*>(wrow);
+#pragma unroll
+        for (int e = 0; e < 16; ++e) {
+          const float4 t = src[e];
+          y[4 * e] = t.x; y[4 * e + 1] = t.y; y[4 * e + 2] = t.z; y[4 * e + 3] = t.w;
+        }
+      }
+      const bool me0 = !hi && mine, me1 = hi && mine;
+      const float f0 = me0 ? sc - 1.0f : red(v0 * sc);
+      const float f1 = me1 ? sc - 1.0f : red(v1 * sc);
+      // shift the panel part while updating; coefficients in place
+#pragma unroll
+      for (int e = 0; e < 31; ++e) {
+        w0[e] = fmaf(f0, y[e + 1], w0[e + 1]);
+        w1[e] = fmaf(f1, y[e + 1], w1[e + 1]);
+      }
+      w0[31] = w1[31] = 0.0f;
+#pragma unroll
+      for (int e = 0; e < 32; ++e) {
+        k0[e] = fmaf(f0, y[32 + e], k0[e]);
+        k1[e] = fmaf(f1, y[32 + e], k1[e]);
+      }
+      if (me0) {
+        open0 = false;
+        q0 = r2;
+      }
+      if (me1) {
+        open1 = false;
+        q1 = r2;
+      }
+      if ((lanebit >> r2) & 1u) {
+        mpc = c;
+        mpr = lo + (hi ? 32 : 0) + (__ffs(bb) - 1);
+      }
+      ++r2;
+      __syncwarp();  // wrow is rewritten by the next column's pivot lane
     }
-    __syncwarp();
-    if (lane == 0) {
-      cand[par][warp] = wrow;
-      if (b) Pcand[par][warp][32 + r2] = 1.0f;  // + e_r2 (that coefficient is still 0)
+    if (lane < r2) {
+      wpc[lane] = mpc;
+      wpr[lane] = mpr;
     }
-    __syncthreads();
-    int s = cand[par][0];
+    if (ok) {
+      if (q0 >= 0) {
 #pragma unroll
-    for (int w2 = 1; w2 < kChainThreads / 32; ++w2) s = min(s, cand[par][w2]);
-    if (s == 0x7FFFFFFF) {
-      if (covers_all) continue;  // a free column (uniform)
-      ok = 0;
-      break;
-    }
-    const int ws = s >> 4;
-    const float sc = vcand[par][ws];
-    float y[32];
-    {
-      const float4* ps = reinterpret_cast<const float4*>(&Pcand[par][ws][32 * half]);
+        for (int e = 0; e < 32; ++e) chatb[q0][e] = std::uint8_t(int(red(k0[e])));
+      }
+      if (q1 >= 0) {
 #pragma unroll
-      for (int e = 0; e < 8; ++e) {
-        const float4 t = ps[e];
-        y[4 * e] = t.x; y[4 * e + 1] = t.y; y[4 * e + 2] = t.z; y[4 * e + 3] = t.w;
+        for (int e = 0; e < 32; ++e) chatb[q1][e] = std::uint8_t(int(red(k1[e])));
       }
     }
-    float f;
-    if (row == s) {
-      f = sc - 1.0f;
-      open = false;
-      myq = r2;
-    } else {
-      f = red(vf * sc);
+    if (lane == 0) {
+      s_ok = ok;
+      s_r2 = r2;
     }
-#pragma unroll
-    for (int e = 0; e < 32; ++e) x[e] = fmaf(f, y[e], x[e]);
-    if (tid == 0) {
-      wpc[r2] = c;
-      wpr[r2] = lo + s;
-    }
-    ++r2;
   }
   __syncthreads();
   stamp(2);
+  const int ok = s_ok, r2 = s_r2;
   if (!ok) {
     panel_full(p, magic, rows, c0, wc, Z, ld, flags, info, cap, nullptr, 0, rho2,
                StepOut{NT, Gpiv});
   } else {
-    if (myq >= 0 && half == 1) {
-#pragma unroll
-      for (int e = 0; e < 32; ++e) chatb[myq][e] = std::uint8_t(int(red(x[e])));
-    }
     if (tid < kW) colq[tid] = -1;
     __syncthreads();
     if (tid < r2) colq[wpc[tid]] = tid;
