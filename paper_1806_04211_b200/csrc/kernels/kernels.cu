@@ -529,7 +529,7 @@ bool launch_inline(std::uint8_t* dst, std::int64_t ldd, std::int64_t rows, std::
   for (std::int64_t i = 0; i < m.nr; ++i) m.v[i] = std::int16_t(rmap[i]);
   for (std::int64_t j = 0; j < m.nc; ++j) m.v[m.nr + j] = std::int16_t(cmap[j]);
   const unsigned gx = unsigned((cols + 2047) / 2048);
-  const unsigned gy = unsigned(rows < 64 ? rows : 64);
+  const unsigned gy = unsigned(rows < 256 ? rows : 256);
   select_inline_kernel<CAP><<<dim3(gx, gy), 128, 0, s>>>(dst, ldd, rows, cols, A, lda, B, ldb, m);
   GFQ_CUDA(cudaGetLastError());
   count_launch();
@@ -546,7 +546,10 @@ bool select2d_inline(std::uint8_t* dst, std::int64_t ldd, std::int64_t rows, std
   const auto al = [](const void* ptr, std::int64_t ld) {
     return ptr == nullptr || ((reinterpret_cast<std::uintptr_t>(ptr) & 15) == 0 && (ld & 15) == 0);
   };
-  if (n > 4096 || !al(dst, ldd) || rows > 65535 * 64 || (!cmap && !(al(A, lda) && al(B, ldb))))
+  // large gathers take the upload path: the upload is cheap next to them and
+  // the regular kernels spread rows over far more blocks
+  if (n > 4096 || !al(dst, ldd) || rows * cols > (std::int64_t(1) << 20) ||
+      (!cmap && !(al(A, lda) && al(B, ldb))))
     return false;
   const auto fits = [](const std::int32_t* m, std::int64_t k) {
     for (std::int64_t i = 0; i < k; ++i)
