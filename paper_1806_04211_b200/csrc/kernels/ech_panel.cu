@@ -19,6 +19,8 @@
 #include <algorithm>
 #include <cstdio>
 #include <cstdlib>
+#include <unordered_map>
+#include <mutex>
 
 #include "../common.hpp"
 #include "kernels.hpp"
@@ -565,7 +567,7 @@ ech_step_chain_kernel(std::uint32_t p, std::uint32_t magic, int rows, int c0, in
                       std::uint8_t* __restrict__ Z, std::int64_t ld, std::uint8_t* flags,
                       std::int32_t* info, int cap, std::int32_t* rho2, std::int32_t* lo_state,
                       std::uint8_t* NT, std::uint8_t* Gpiv, std::uint8_t* Y, const std::int32_t* base,
-                      std::uint8_t* BpT) {
+                      std::uint8_t* BpT, const std::uint8_t* __restrict__ invtab) {
   extern __shared__ __align__(16) std::uint8_t dsm[];
   __shared__ std::uint8_t invw[256];
   __shared__ int s_lo, s_rold;
@@ -577,8 +579,7 @@ ech_step_chain_kernel(std::uint32_t p, std::uint32_t magic, int rows, int c0, in
   __shared__ int wpc[kW], wpr[kW], s_pr[kW];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   stamp(0);
-  for (int a = tid; a < 256; a += kChainThreads)
-    invw[a] = (a > 0 && std::uint32_t(a) < p) ? std::uint8_t(powmod(a, p - 2, p)) : 0;
+  for (int a = tid; a < 256; a += kChainThreads) invw[a] = invtab[a];  // inverses mod p (cached)
   if (warp == 0) {
     int lo = *lo_state;
     for (;;) {
@@ -599,6 +600,20 @@ ech_step_chain_kernel(std::uint32_t p, std::uint32_t magic, int rows, int c0, in
   }
   __syncthreads();
   const int lo = s_lo, r_old = s_rold;
+  // warps 1.. stage the window rows' step columns [c0, c0 + n) in shared
+  // memory while warp 0 runs the chain: the step's pivot rows are window
+  // rows, so BpT is built from here (the region doubles as panel_full's
+  // fallback storage, after which the tail reads Z instead)
+  std::uint8_t* Ws = dsm;  // 64 x n
+  if (warp > 0) {
+    const int nv = n / 16;
+    for (int e = tid - 32; e < 64 * nv; e += kChainThreads - 32) {
+      const int r = e / nv, ch = e % nv;
+      uint4 v = make_uint4(0, 0, 0, 0);
+      if (lo + r < rows) v = *reinterpret_cast<const uint4*>(Z + std::int64_t(lo + r) * ld + c0 + 16 * ch);
+      reinterpret_cast<uint4*>(Ws + r * n)[ch] = v;
+    }
+  }
   // ---- the window chain, in warp 0 alone (no CTA barriers): lane l holds
   // window rows lo + l and lo + 32 + l, each as 32 panel elements (kept
   // SHIFTED so the current column is element 0: no dynamic register
@@ -792,16 +807,22 @@ ech_step_chain_kernel(std::uint32_t p, std::uint32_t magic, int rows, int c0, in
     if (r >= 0) Y[std::int64_t(r) * ld + (r_old + tid - *base)] = 1;
   }
   __syncthreads();
-  // stage the pivot rows (32 x n, 16-byte loads) in shared memory, then
-  // write them transposed
-  std::uint8_t* Bs = dsm;  // 32 x n
+  // the pivot rows (32 x n) in shared memory -- from the window staging
+  // (plus the Y unit just planted) or, after a fallback, from Z -- then
+  // written transposed
+  std::uint8_t* Bs = dsm + 64 * n;  // 32 x n, after the staged window
+  const int y_col = int(Y - Z) - c0;  // Y's first column relative to c0
   for (int e = tid; e < kW * (n / 16); e += kChainThreads) {
     const int q = e / (n / 16), ch = e % (n / 16);
     const int r = s_pr[q];
     uint4 v = make_uint4(0, 0, 0, 0);
-    if (r >= 0) v = *reinterpret_cast<const uint4*>(Z + std::int64_t(r) * ld + c0 + 16 * ch);
+    if (r >= 0)
+      v = ok ? reinterpret_cast<const uint4*>(Ws + (r - lo) * n)[ch]
+             : *reinterpret_cast<const uint4*>(Z + std::int64_t(r) * ld + c0 + 16 * ch);
     reinterpret_cast<uint4*>(Bs + q * n)[ch] = v;
   }
+  __syncthreads();
+  if (ok && tid < kW && s_pr[tid] >= 0) Bs[tid * n + y_col + (r_old + tid - *base)] = 1;
   __syncthreads();
   for (int j = tid; j < n; j += kChainThreads) {
     std::uint32_t o[8] = {0, 0, 0, 0, 0, 0, 0, 0};
@@ -1251,6 +1272,30 @@ void ech_panel(std::uint32_t p, std::int64_t rows, std::int64_t c0, std::int64_t
   count_launch();
 }
 
+// inverses mod p (0 -> 0), one 256-byte device table per prime, built once
+const std::uint8_t* inv_table(std::uint32_t p) {
+  static std::mutex mtx;
+  static std::unordered_map<std::uint32_t, std::uint8_t*>* tabs =
+      new std::unordered_map<std::uint32_t, std::uint8_t*>();  // process lifetime
+  std::lock_guard<std::mutex> lk(mtx);
+  auto it = tabs->find(p);
+  if (it != tabs->end()) return it->second;
+  std::uint8_t host[256] = {0};
+  for (std::uint32_t a = 1; a < p && a < 256; ++a) {
+    std::uint64_t r = 1, b = a;
+    for (std::uint32_t e = p - 2; e; e >>= 1) {
+      if (e & 1) r = r * b % p;
+      b = b * b % p;
+    }
+    host[a] = std::uint8_t(r);
+  }
+  std::uint8_t* d = nullptr;
+  GFQ_CUDA(cudaMalloc(&d, 256));
+  GFQ_CUDA(cudaMemcpy(d, host, 256, cudaMemcpyHostToDevice));
+  (*tabs)[p] = d;
+  return d;
+}
+
 void ech_step(std::uint32_t p, std::int64_t rows, std::int64_t c0, std::int64_t wc, std::int64_t n,
               std::uint8_t* Z, std::int64_t ld, std::uint8_t* flags, std::int32_t* info,
               std::int64_t cap, std::int32_t* rho2, std::uint8_t* step_scratch, std::uint8_t* Y,
@@ -1258,7 +1303,7 @@ void ech_step(std::uint32_t p, std::int64_t rows, std::int64_t c0, std::int64_t 
   if (wc > kW || c0 % kW || n % 16 || n > kStepMaxN || (ld & 15) ||
       (reinterpret_cast<std::uintptr_t>(Z) & 15))
     throw std::invalid_argument("ech_step: bad step geometry");
-  const std::size_t smem = std::max<std::size_t>(std::size_t(rows) * (kW + 1), std::size_t(kW) * n);
+  const std::size_t smem = std::max<std::size_t>(std::size_t(rows) * (kW + 1), std::size_t(64 + kW) * n);
   if (smem > std::size_t(kPanelSmem)) throw std::invalid_argument("ech_step: block too tall");
   static bool attr = false;
   if (!attr) {
@@ -1281,7 +1326,7 @@ void ech_step(std::uint32_t p, std::int64_t rows, std::int64_t c0, std::int64_t 
   std::uint8_t* BpT = step_scratch + 2 * kW * kW;
   ech_step_chain_kernel<<<1, kChainThreads, smem, s>>>(p, magic, int(rows), int(c0), int(wc), int(n), Z,
                                                       ld, flags, info, int(cap), rho2, lo_state, NT,
-                                                      Gpiv, Y, base, BpT);
+                                                      Gpiv, Y, base, BpT, inv_table(p));
   GFQ_CUDA(cudaGetLastError());
   ech_step_update_kernel<<<unsigned((rows + kStepRows - 1) / kStepRows), kStepThreads, 0, s>>>(
       p, magic, int(rows), int(c0), int(n), Z, ld, NT, Gpiv, rho2, BpT);
