@@ -1,4 +1,6 @@
 cd $GRAFT_REPO_ROOT
+timeout 1500 python -m pytest tests -m gpu -x -q -p no:cacheprovider > gpurun_out/gputests.log 2>&1; echo "rc=$?" >> gpurun_out/gputests.log
+timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1; echo "rc=$?" >> gpurun_out/smoke.log
 timeout 400 python bench.py > gpurun_out/bench_final.log 2>&1
 for c in cfg1 cfg2b cfg3 cfg4 cfg5s; do timeout 900 python bench.py --config $c --steps 3 --warmup 3 --no-cpu-baseline --no-e2e > gpurun_out/bench_$c.log 2>&1; done
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/cfg2a_launches.csv python tools/one_step.py cfg2a 4 > gpurun_out/ncu_step.log 2>&1
