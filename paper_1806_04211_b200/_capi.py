@@ -10,7 +10,7 @@ import ctypes
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "lib", "libgfq.so")
+LIB_PATH = os.environ.get("GFQ_LIB_PATH") or os.path.join(HERE, "lib", "libgfq.so")  # override: A/B builds
 HEADER = os.path.join(os.path.dirname(HERE), "include", "gfq.h")
 
 c_u8p = ctypes.POINTER(ctypes.c_uint8)

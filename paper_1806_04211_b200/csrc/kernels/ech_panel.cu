@@ -572,7 +572,6 @@ ech_step_chain_kernel(std::uint32_t p, std::uint32_t magic, int rows, int c0, in
   __shared__ std::uint8_t invw[256];
   __shared__ int s_lo, s_rold;
   __shared__ __align__(16) float wrow[64];  // the column's pivot row (raw, then reduced)
-  __shared__ float s_v;
   __shared__ int s_ok, s_r2;
   __shared__ int colq[kW];
   __shared__ std::uint8_t chatb[kW][kW];
@@ -664,6 +663,9 @@ ech_step_chain_kernel(std::uint32_t p, std::uint32_t magic, int rows, int c0, in
 #pragma unroll 1
     for (int c = 0; c < wc; ++c) {
       const float v0 = red(w0[0]), v1 = red(w1[0]);
+      // every lane looks up its candidates' inverses now, overlapping the
+      // votes; the pivot lane's is shuffled out below (no smem round trip)
+      const std::uint32_t iv0 = invw[int(v0)], iv1 = invw[int(v1)];
       const unsigned b0 = __ballot_sync(0xffffffffu, open0 && v0 != 0.0f);
       const unsigned b1 = __ballot_sync(0xffffffffu, open1 && v1 != 0.0f);
       // the shifted panel moves on whether or not the column has a pivot
@@ -692,7 +694,6 @@ ech_step_chain_kernel(std::uint32_t p, std::uint32_t magic, int rows, int c0, in
           dst[e] = make_float4(w0[4 * e], w0[4 * e + 1], w0[4 * e + 2], w0[4 * e + 3]);
           dst[8 + e] = make_float4(k0[4 * e], k0[4 * e + 1], k0[4 * e + 2], k0[4 * e + 3]);
         }
-        s_v = v0;
       }
       if (mine && hi) {
 #pragma unroll
@@ -700,15 +701,15 @@ ech_step_chain_kernel(std::uint32_t p, std::uint32_t magic, int rows, int c0, in
           dst[e] = make_float4(w1[4 * e], w1[4 * e + 1], w1[4 * e + 2], w1[4 * e + 3]);
           dst[8 + e] = make_float4(k1[4 * e], k1[4 * e + 1], k1[4 * e + 2], k1[4 * e + 3]);
         }
-        s_v = v1;
       }
+      const std::uint32_t ivp = __shfl_sync(0xffffffffu, hi ? iv1 : iv0, __ffs(bb) - 1);
       __syncwarp();
       // reduce the published row, two elements a lane; plant e_r2 (that
       // coefficient is still 0 in every row)
       wrow[lane] = red(wrow[lane]);
       wrow[32 + lane] = lane == r2 ? 1.0f : red(wrow[32 + lane]);
       __syncwarp();
-      const float sc = float(p - invw[int(s_v)]);
+      const float sc = float(p - ivp);
       float y[64];
       {
         const float4* src = reinterpret_cast<const float4*>(wrow);
