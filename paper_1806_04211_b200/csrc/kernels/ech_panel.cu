@@ -855,12 +855,8 @@ ech_step_update_kernel(std::uint32_t p, std::uint32_t magic, int rows, int c0, i
   __shared__ std::uint32_t sG[kStepRows][9];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int i0 = blockIdx.x * kStepRows;
-  // blockIdx.y: this CTA's range of 16-column chunks (small blocks split
-  // their columns over more CTAs so the update is not confined to a few SMs)
-  const int nch = n / 16, cpg = (nch + gridDim.y - 1) / gridDim.y;
-  const int ch0 = blockIdx.y * cpg, ch1 = min(nch, ch0 + cpg);
-  for (int e = tid; e < (ch1 - ch0) * 32; e += kStepThreads)
-    reinterpret_cast<uint4*>(sB)[e] = reinterpret_cast<const uint4*>(BpT)[ch0 * 32 + e];
+  for (int e = tid; e < n * 2; e += kStepThreads)
+    reinterpret_cast<uint4*>(sB)[e] = reinterpret_cast<const uint4*>(BpT)[e];
   if (tid < kW * 2) reinterpret_cast<uint4*>(sNT)[tid] = reinterpret_cast<const uint4*>(NT)[tid];
   __syncthreads();
   {
@@ -898,7 +894,7 @@ ech_step_update_kernel(std::uint32_t p, std::uint32_t magic, int rows, int c0, i
 #pragma unroll
   for (int w = 0; w < 8; ++w) g[w] = sG[lane][w];
   std::uint8_t* zrow = Z + std::int64_t(i) * ld + c0;
-  for (int ch = ch0 + warp; ch < ch1; ch += kStepThreads / 32) {
+  for (int ch = warp; ch < n / 16; ch += kStepThreads / 32) {
     std::uint32_t out[4];
     const uint4 old = *reinterpret_cast<const uint4*>(zrow + 16 * ch);
     const std::uint32_t ow[4] = {old.x, old.y, old.z, old.w};
@@ -907,7 +903,7 @@ ech_step_update_kernel(std::uint32_t p, std::uint32_t magic, int rows, int c0, i
       std::uint32_t word = 0;
 #pragma unroll
       for (int by = 0; by < 4; ++by) {
-        const uint4* b4 = reinterpret_cast<const uint4*>(sB + (16 * (ch - ch0) + 4 * q + by) * 8);
+        const uint4* b4 = reinterpret_cast<const uint4*>(sB + (16 * ch + 4 * q + by) * 8);
         const uint4 x = b4[0], y = b4[1];
         std::uint32_t acc = (ow[q] >> (8 * by)) & 0xFFu;
         acc = __dp4a(g[0], x.x, acc); acc = __dp4a(g[1], x.y, acc);
@@ -1333,9 +1329,7 @@ void ech_step(std::uint32_t p, std::int64_t rows, std::int64_t c0, std::int64_t 
                                                       ld, flags, info, int(cap), rho2, lo_state, NT,
                                                       Gpiv, Y, base, BpT, inv_table(p));
   GFQ_CUDA(cudaGetLastError());
-  const int row_ctas = int((rows + kStepRows - 1) / kStepRows), nch = int(n / 16);
-  const int groups = std::max(1, std::min((nch + 7) / 8, (2 * sm_count() + row_ctas - 1) / row_ctas));
-  ech_step_update_kernel<<<dim3(unsigned(row_ctas), unsigned(groups)), kStepThreads, 0, s>>>(
+  ech_step_update_kernel<<<unsigned((rows + kStepRows - 1) / kStepRows), kStepThreads, 0, s>>>(
       p, magic, int(rows), int(c0), int(n), Z, ld, NT, Gpiv, rho2, BpT);
   GFQ_CUDA(cudaGetLastError());
   static int dbg = std::getenv("GFQ_STEP_DEBUG") ? std::atoi(std::getenv("GFQ_STEP_DEBUG")) : 0;
