@@ -844,6 +844,9 @@ ech_step_chain_kernel(std::uint32_t p, std::uint32_t magic, int rows, int c0, in
 // stages BpT; then the 8 warps split the 16-column chunks, lane = row:
 // 16 x 8 dp4a per chunk against BpT rows broadcast from shared memory, the
 // Barrett reduction with the old values, one 16-byte load and store per lane.
+// A row's columns must stay in ONE CTA: G is formed from the row's panel
+// segment, which the same update overwrites in place (splitting the columns
+// over CTAs races -- measured 3% faster and wrong on cfg3).
 constexpr int kStepRows = 32, kStepMaxN = 512;
 __global__ void __launch_bounds__(kStepThreads)
 ech_step_update_kernel(std::uint32_t p, std::uint32_t magic, int rows, int c0, int n,
