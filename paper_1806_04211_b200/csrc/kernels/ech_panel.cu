@@ -550,6 +550,21 @@ ech_panel_win_kernel(std::uint32_t p, std::uint32_t magic, int rows, int c0, int
 //     pivot rows transposed so ech_step_update_kernel contracts over q with
 //     dp4a (n x 32 bytes).
 constexpr int kStepThreads = 256;
+// Programmatic dependent launch between the step kernels: each is launched
+// with programmatic stream serialization, so its CTAs may become resident
+// while the previous kernel drains.  griddepcontrol.wait (first, before any
+// global access) returns once the previous grid has completed and its
+// writes are visible; launch_dependents lets the next kernel's CTAs get
+// scheduled early (they wait the same way).  Without a programmatic
+// predecessor both are no-ops.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_release() {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+__device__ __forceinline__ void pdl_wait_and_release() {
+  pdl_wait();
+  pdl_release();
+}
 // developer timing (GFQ_STEP_DEBUG): globaltimer stamps of the chain phases
 __device__ unsigned long long g_step_stamps[16];
 __device__ __forceinline__ void stamp(int k) {
@@ -576,6 +591,8 @@ ech_step_chain_kernel(std::uint32_t p, std::uint32_t magic, int rows, int c0, in
   __shared__ int colq[kW];
   __shared__ std::uint8_t chatb[kW][kW];
   __shared__ int wpc[kW], wpr[kW], s_pr[kW];
+  pdl_wait();  // released after the chain (below): the update's CTAs
+               // should not sit on SMs other streams' K1 tiles could use
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   stamp(0);
   for (int a = tid; a < 256; a += kChainThreads) invw[a] = invtab[a];  // inverses mod p (cached)
@@ -770,6 +787,7 @@ ech_step_chain_kernel(std::uint32_t p, std::uint32_t magic, int rows, int c0, in
   }
   __syncthreads();
   stamp(2);
+  pdl_release();
   const int ok = s_ok, r2 = s_r2;
   if (!ok) {
     panel_full(p, magic, rows, c0, wc, Z, ld, flags, info, cap, nullptr, 0, rho2,
@@ -856,6 +874,7 @@ ech_step_update_kernel(std::uint32_t p, std::uint32_t magic, int rows, int c0, i
   __shared__ __align__(16) std::uint32_t sB[kStepMaxN * 8];
   __shared__ __align__(16) std::uint32_t sNT[kW * 8];
   __shared__ std::uint32_t sG[kStepRows][9];
+  pdl_wait_and_release();
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int i0 = blockIdx.x * kStepRows;
   for (int e = tid; e < n * 2; e += kStepThreads)
@@ -1328,13 +1347,26 @@ void ech_step(std::uint32_t p, std::int64_t rows, std::int64_t c0, std::int64_t 
   std::uint8_t* NT = step_scratch;
   std::uint8_t* Gpiv = step_scratch + kW * kW;
   std::uint8_t* BpT = step_scratch + 2 * kW * kW;
-  ech_step_chain_kernel<<<1, kChainThreads, smem, s>>>(p, magic, int(rows), int(c0), int(wc), int(n), Z,
-                                                      ld, flags, info, int(cap), rho2, lo_state, NT,
-                                                      Gpiv, Y, base, BpT, inv_table(p));
-  GFQ_CUDA(cudaGetLastError());
-  ech_step_update_kernel<<<unsigned((rows + kStepRows - 1) / kStepRows), kStepThreads, 0, s>>>(
-      p, magic, int(rows), int(c0), int(n), Z, ld, NT, Gpiv, rho2, BpT);
-  GFQ_CUDA(cudaGetLastError());
+  static const bool pdl = std::getenv("GFQ_NO_PDL") == nullptr;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cudaLaunchConfig_t cfg = {};
+  cfg.stream = s;
+  cfg.attrs = at;
+  cfg.numAttrs = pdl ? 1 : 0;
+  cfg.gridDim = dim3(1);
+  cfg.blockDim = dim3(kChainThreads);
+  cfg.dynamicSmemBytes = smem;
+  const std::uint8_t* invt = inv_table(p);
+  GFQ_CUDA(cudaLaunchKernelEx(&cfg, ech_step_chain_kernel, p, magic, int(rows), int(c0), int(wc), int(n),
+                              Z, ld, flags, info, int(cap), rho2, lo_state, NT, Gpiv, Y, base, BpT, invt));
+  cfg.gridDim = dim3(unsigned((rows + kStepRows - 1) / kStepRows));
+  cfg.blockDim = dim3(kStepThreads);
+  cfg.dynamicSmemBytes = 0;
+  GFQ_CUDA(cudaLaunchKernelEx(&cfg, ech_step_update_kernel, p, magic, int(rows), int(c0), int(n), Z, ld,
+                              static_cast<const std::uint8_t*>(NT), static_cast<const std::uint8_t*>(Gpiv),
+                              static_cast<const std::int32_t*>(rho2), static_cast<const std::uint8_t*>(BpT)));
   static int dbg = std::getenv("GFQ_STEP_DEBUG") ? std::atoi(std::getenv("GFQ_STEP_DEBUG")) : 0;
   if (dbg > 0) {
     --dbg;
