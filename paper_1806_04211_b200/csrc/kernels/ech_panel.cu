@@ -550,21 +550,9 @@ ech_panel_win_kernel(std::uint32_t p, std::uint32_t magic, int rows, int c0, int
 //     pivot rows transposed so ech_step_update_kernel contracts over q with
 //     dp4a (n x 32 bytes).
 constexpr int kStepThreads = 256;
-// Programmatic dependent launch between the step kernels: each is launched
-// with programmatic stream serialization, so its CTAs may become resident
-// while the previous kernel drains.  griddepcontrol.wait (first, before any
-// global access) returns once the previous grid has completed and its
-// writes are visible; launch_dependents lets the next kernel's CTAs get
-// scheduled early (they wait the same way).  Without a programmatic
-// predecessor both are no-ops.
-__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
-__device__ __forceinline__ void pdl_release() {
-  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
-}
-__device__ __forceinline__ void pdl_wait_and_release() {
-  pdl_wait();
-  pdl_release();
-}
+// The step kernels chain with programmatic dependent launch (launch_pdl,
+// kernels.hpp): the chain releases its dependents only after the chain loop,
+// so the update's CTAs do not sit on SMs other streams' K1 tiles could use.
 // developer timing (GFQ_STEP_DEBUG): globaltimer stamps of the chain phases
 __device__ unsigned long long g_step_stamps[16];
 __device__ __forceinline__ void stamp(int k) {
@@ -1347,7 +1335,7 @@ void ech_step(std::uint32_t p, std::int64_t rows, std::int64_t c0, std::int64_t 
   std::uint8_t* NT = step_scratch;
   std::uint8_t* Gpiv = step_scratch + kW * kW;
   std::uint8_t* BpT = step_scratch + 2 * kW * kW;
-  static const bool pdl = std::getenv("GFQ_NO_PDL") == nullptr;
+  const bool pdl = pdl_enabled();
   cudaLaunchAttribute at[1];
   at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   at[0].val.programmaticStreamSerializationAllowed = 1;

@@ -163,6 +163,10 @@ gf_mad_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
                  int m, int n, int k, std::uint32_t p, std::uint32_t magic,
                  const std::uint8_t* Cin, std::int64_t ldc, std::uint8_t* D, std::int64_t ldd,
                  unsigned long long* dbg) {
+  // PDL: wait for the predecessor grid before any global access; dependents
+  // are released only at exit (a waiting 200 KB-smem K1 CTA would hold an SM
+  // other streams could use)
+  pdl_wait();
   using G = Geo<BN>;
   constexpr int STAGES = G::STAGES;
   // dbg (developer timing, GFQ_TC_DEBUG): per CTA 8 globaltimer stamps.
@@ -490,11 +494,11 @@ bool mad_tc(std::uint32_t p, std::int64_t m, std::int64_t n, std::int64_t k,
     const std::uint8_t* cin = k0 == 0 ? Cin : D;
     const std::int64_t ldcin = k0 == 0 ? ldc : ldd;
     if (narrow)
-      gf_mad_tc_kernel<128><<<grid, NUM_THREADS, Geo<128>::SMEM_BYTES, s>>>(
-          mA, mB, int(m), int(n), int(kk), p, magic, cin, ldcin, D, ldd, tc_debug_buf());
+      GFQ_CUDA(launch_pdl(gf_mad_tc_kernel<128>, dim3(grid), dim3(NUM_THREADS), Geo<128>::SMEM_BYTES, s, 
+          mA, mB, int(m), int(n), int(kk), p, magic, cin, ldcin, D, ldd, tc_debug_buf()));
     else
-      gf_mad_tc_kernel<256><<<grid, NUM_THREADS, Geo<256>::SMEM_BYTES, s>>>(
-          mA, mB, int(m), int(n), int(kk), p, magic, cin, ldcin, D, ldd, tc_debug_buf());
+      GFQ_CUDA(launch_pdl(gf_mad_tc_kernel<256>, dim3(grid), dim3(NUM_THREADS), Geo<256>::SMEM_BYTES, s, 
+          mA, mB, int(m), int(n), int(kk), p, magic, cin, ldcin, D, ldd, tc_debug_buf()));
     GFQ_CUDA(cudaGetLastError());
     count_launch();
   }

@@ -14,6 +14,11 @@
 
 namespace gfq::dev {
 
+bool pdl_enabled() {
+  static const bool on = std::getenv("GFQ_NO_PDL") == nullptr;
+  return on;
+}
+
 // ------------------------------------------------------------------ helpers
 // x mod p for any 32-bit x: q_est = floor(x * ceil(2^32/p) / 2^32) is q or q+1.
 __device__ __forceinline__ std::uint32_t modp(std::uint32_t x, std::uint32_t p,
@@ -45,6 +50,7 @@ mad_simt_kernel(std::uint32_t p, std::uint32_t magic, int m, int n, int k,
                 const std::uint8_t* __restrict__ B, std::int64_t ldb,
                 const std::uint8_t* Cin, std::int64_t ldc, std::uint8_t* D,
                 std::int64_t ldd) {
+  pdl_wait_and_release();
   __shared__ std::uint8_t As[kTm][kTk + 4];
   __shared__ std::uint8_t Bs[kTk][kTn + 4];
   const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
@@ -103,6 +109,7 @@ mad_smallk_kernel(std::uint32_t p, std::uint32_t magic, int m, int n, int k,
                   const std::uint8_t* __restrict__ A, std::int64_t lda,
                   const std::uint8_t* __restrict__ B, std::int64_t ldb,
                   const std::uint8_t* Cin, std::int64_t ldc, std::uint8_t* D, std::int64_t ldd) {
+  pdl_wait_and_release();
   const int nvec = (n + 15) >> 4;
   const std::int64_t tid = std::int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
   const std::int64_t total = std::int64_t(m) * nvec;
@@ -209,9 +216,9 @@ void mad_simt(std::uint32_t p, std::int64_t m, std::int64_t n, std::int64_t k,
     for (std::int64_t m0 = 0; m0 < m; m0 += std::int64_t(65535) * kTm) {
       const std::int64_t mm = (m - m0) < std::int64_t(65535) * kTm ? (m - m0) : std::int64_t(65535) * kTm;
       dim3 grid(unsigned((n + kTn - 1) / kTn), unsigned((mm + kTm - 1) / kTm));
-      mad_simt_kernel<<<grid, 256, 0, s>>>(
+      GFQ_CUDA(launch_pdl(mad_simt_kernel, dim3(grid), dim3(256), 0, s, 
           p, mg, int(mm), int(n), int(kk), A + m0 * lda + k0, lda, B + k0 * ldb, ldb,
-          cin ? cin + m0 * ldcin : nullptr, ldcin, D + m0 * ldd, ldd);
+          cin ? cin + m0 * ldcin : nullptr, ldcin, D + m0 * ldd, ldd));
       GFQ_CUDA(cudaGetLastError());
     count_launch();
     }
@@ -302,8 +309,8 @@ void mad(std::uint32_t p, std::int64_t m, std::int64_t n, std::int64_t k,
     const std::int64_t total = m * ((n + 15) / 16);
     const std::int64_t cap = std::int64_t(sm_count()) * 8;
     const unsigned grid = unsigned(std::min<std::int64_t>((total + 255) / 256, cap));
-    mad_smallk_kernel<<<grid, 256, 0, s>>>(p, magic_of(p), int(m), int(n), int(k), A, lda, B, ldb,
-                                           Cin, ldc, D, ldd);
+    GFQ_CUDA(launch_pdl(mad_smallk_kernel, dim3(grid), dim3(256), 0, s, p, magic_of(p), int(m), int(n), int(k), A, lda, B, ldb,
+                                           Cin, ldc, D, ldd));
     GFQ_CUDA(cudaGetLastError());
     count_launch();
     done = true;
@@ -351,6 +358,7 @@ __global__ void select_rows_v16_kernel(std::uint8_t* dst, std::int64_t ldd,
                                        const std::uint8_t* A, std::int64_t lda,
                                        const std::uint8_t* B, std::int64_t ldb,
                                        const std::int32_t* rmap) {
+  pdl_wait_and_release();
   const std::int64_t nvec = (cols + 15) / 16;
   for (std::int64_t i = blockIdx.y; i < rows; i += gridDim.y) {
     bool fromB = false;
@@ -374,6 +382,7 @@ __global__ void select2d_kernel(std::uint8_t* dst, std::int64_t ldd,
                                 const std::uint8_t* B, std::int64_t ldb,
                                 const std::int32_t* rmap,
                                 const std::int32_t* cmap) {
+  pdl_wait_and_release();
   for (std::int64_t i = blockIdx.y; i < rows; i += gridDim.y) {
     std::int32_t rv = -3;  // "no row map"
     if (rmap) rv = rmap[i];
@@ -402,6 +411,7 @@ __global__ void select2d_v16_kernel(std::uint8_t* dst, std::int64_t ldd,
                                     const std::uint8_t* B, std::int64_t ldb,
                                     const std::int32_t* rmap,
                                     const std::int32_t* cmap) {
+  pdl_wait_and_release();
   const std::int64_t nvec = (cols + 15) / 16;
   for (std::int64_t i = blockIdx.y; i < rows; i += gridDim.y) {
     std::int32_t rv = -3;  // "no row map"
@@ -454,6 +464,7 @@ __global__ void select2d_v16_kernel(std::uint8_t* dst, std::int64_t ldd,
 __global__ void set_entries_kernel(std::uint8_t* dst, std::int64_t ldd,
                                    const std::int32_t* pos, std::int64_t n,
                                    std::uint8_t value) {
+  pdl_wait_and_release();
   for (std::int64_t q = blockIdx.x * blockDim.x + threadIdx.x; q < n;
        q += std::int64_t(gridDim.x) * blockDim.x)
     dst[std::int64_t(pos[2 * q]) * ldd + pos[2 * q + 1]] = value;
@@ -471,6 +482,7 @@ __global__ void __launch_bounds__(128)
 select_inline_kernel(std::uint8_t* dst, std::int64_t ldd, std::int64_t rows, std::int64_t cols,
                      const std::uint8_t* A, std::int64_t lda, const std::uint8_t* B,
                      std::int64_t ldb, const __grid_constant__ InlineMaps<CAP> maps) {
+  pdl_wait_and_release();
   __shared__ std::int32_t scm[2048];
   const std::int64_t nr = maps.nr, nc = maps.nc;
   const std::int64_t c0 = std::int64_t(blockIdx.x) * 2048;
@@ -530,7 +542,7 @@ bool launch_inline(std::uint8_t* dst, std::int64_t ldd, std::int64_t rows, std::
   for (std::int64_t j = 0; j < m.nc; ++j) m.v[m.nr + j] = std::int16_t(cmap[j]);
   const unsigned gx = unsigned((cols + 2047) / 2048);
   const unsigned gy = unsigned(rows < 256 ? rows : 256);
-  select_inline_kernel<CAP><<<dim3(gx, gy), 128, 0, s>>>(dst, ldd, rows, cols, A, lda, B, ldb, m);
+  GFQ_CUDA(launch_pdl(select_inline_kernel<CAP>, dim3(dim3(gx, gy)), dim3(128), 0, s, dst, ldd, rows, cols, A, lda, B, ldb, m));
   GFQ_CUDA(cudaGetLastError());
   count_launch();
   return true;
@@ -577,14 +589,14 @@ void select2d(std::uint8_t* dst, std::int64_t ldd, std::int64_t rows,
   if (!cmap && al(dst, ldd) && al(A, lda) && al(B, ldb)) {
     const std::int64_t nvec = (cols + 15) / 16;
     const unsigned gx = unsigned((nvec + 127) / 128);
-    select_rows_v16_kernel<<<dim3(gx, gy), 128, 0, s>>>(dst, ldd, rows, cols, A, lda, B, ldb, rmap);
+    GFQ_CUDA(launch_pdl(select_rows_v16_kernel, dim3(dim3(gx, gy)), dim3(128), 0, s, dst, ldd, rows, cols, A, lda, B, ldb, rmap));
   } else if (cmap && al(dst, ldd)) {
     const std::int64_t nvec = (cols + 15) / 16;
     const unsigned gx = unsigned((nvec + 127) / 128);
-    select2d_v16_kernel<<<dim3(gx, gy), 128, 0, s>>>(dst, ldd, rows, cols, A, lda, B, ldb, rmap, cmap);
+    GFQ_CUDA(launch_pdl(select2d_v16_kernel, dim3(dim3(gx, gy)), dim3(128), 0, s, dst, ldd, rows, cols, A, lda, B, ldb, rmap, cmap));
   } else {
     const unsigned gx = unsigned((cols + 255) / 256);
-    select2d_kernel<<<dim3(gx, gy), 256, 0, s>>>(dst, ldd, rows, cols, A, lda, B, ldb, rmap, cmap);
+    GFQ_CUDA(launch_pdl(select2d_kernel, dim3(dim3(gx, gy)), dim3(256), 0, s, dst, ldd, rows, cols, A, lda, B, ldb, rmap, cmap));
   }
   GFQ_CUDA(cudaGetLastError());
     count_launch();
@@ -593,7 +605,7 @@ void select2d(std::uint8_t* dst, std::int64_t ldd, std::int64_t rows,
 void set_entries(std::uint8_t* dst, std::int64_t ldd, const std::int32_t* pos,
                  std::int64_t n, std::uint8_t value, cudaStream_t s) {
   if (n == 0) return;
-  set_entries_kernel<<<unsigned((n + 255) / 256), 256, 0, s>>>(dst, ldd, pos, n, value);
+  GFQ_CUDA(launch_pdl(set_entries_kernel, dim3(unsigned((n + 255) / 256)), dim3(256), 0, s, dst, ldd, pos, n, value));
   GFQ_CUDA(cudaGetLastError());
     count_launch();
 }

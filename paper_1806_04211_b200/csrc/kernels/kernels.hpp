@@ -6,9 +6,45 @@
 
 #include <cuda_runtime.h>
 
+#include <cstddef>
 #include <cstdint>
+#include <utility>
 
 namespace gfq::dev {
+
+// Programmatic dependent launch (PDL).  launch_pdl launches a kernel with
+// programmatic stream serialization, so its CTAs may become resident while
+// the previous kernel in the stream drains; every kernel launched this way
+// calls pdl_wait() before its first global-memory access (it returns once
+// the predecessor grid has completed and its writes are visible -- a no-op
+// without a programmatic predecessor) and pdl_release() once its own
+// dependents may be scheduled.  GFQ_NO_PDL=1 launches without the attribute.
+#ifdef __CUDACC__
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_release() {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+__device__ __forceinline__ void pdl_wait_and_release() {
+  pdl_wait();
+  pdl_release();
+}
+#endif
+bool pdl_enabled();
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, std::size_t smem,
+                              cudaStream_t s, Args&&... args) {
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cfg.attrs = at;
+  cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
+}
 
 // ---------------------------------------------------------------- K1
 // D = (Cin ? Cin : 0) + A.B mod p   (A: m x k, B: k x n, Cin/D: m x n).
