@@ -451,10 +451,7 @@ EchResult panel_ech(const FieldSpec& f, const Mat& h) {
   for (std::int64_t C0 = 0; C0 < b; C0 += ow) {
     const std::int64_t wd = std::min(ow, b - C0), kc = std::min(wd, a);
     // Z[:, 0:wd] = Aug[:, C0:C0+wd], Z[:, ow:] = 0
-    GFQ_CUDA(cudaMemcpy2DAsync(Z.data(), std::size_t(Z.ld()), aug.data() + C0, std::size_t(aug.ld()),
-                               std::size_t(wd), std::size_t(a), cudaMemcpyDeviceToDevice, s));
-    GFQ_CUDA(cudaMemset2DAsync(Z.data() + wd, std::size_t(Z.ld()), 0, std::size_t(2 * ow - wd),
-                               std::size_t(a), s));
+    dev::copy_cols(Z.data(), Z.ld(), aug.data() + C0, aug.ld(), a, wd, 2 * ow, s);
     std::uint8_t* Y = Z.data() + ow;
     for (std::int64_t c0 = 0; c0 < wd; c0 += w) {
       const std::int64_t wc = std::min(w, wd - c0);
@@ -475,8 +472,8 @@ EchResult panel_ech(const FieldSpec& f, const Mat& h) {
                Z.data() + c0, Z.ld(), s);
     }
     dev::ech_outer_finish(f.p(), Y, Z.ld(), kc, inf, cap, base, rmap, C0, s);
-    GFQ_CUDA(cudaMemcpy2DAsync(aug.data() + C0, std::size_t(aug.ld()), Z.data(), std::size_t(Z.ld()),
-                               std::size_t(wd), std::size_t(a), cudaMemcpyDeviceToDevice, s));
+    // (columns [wd, round16(wd)) of the last panel are the zero gap before T)
+    dev::copy_cols(aug.data() + C0, aug.ld(), Z.data(), Z.ld(), a, wd, (wd + 15) / 16 * 16, s);
     const std::int64_t r0 = C0 + wd, n = tb + a - r0;
     dev::select2d(Bt.data(), Bt.ld(), kc, n, aug.data() + r0, aug.ld(), nullptr, 0, rmap, nullptr, s);
     dev::mad(f.p(), a, n, kc, Y, Z.ld(), Bt.data(), Bt.ld(), aug.data() + r0, aug.ld(),

@@ -19,6 +19,8 @@
 #include <algorithm>
 #include <cstdio>
 #include <cstdlib>
+#include <cstring>
+#include <stdexcept>
 #include <unordered_map>
 #include <mutex>
 
@@ -1195,6 +1197,7 @@ __global__ void ech_plant_kernel(std::uint8_t* Y, std::int64_t ldy, const std::i
 __global__ void ech_outer_finish_kernel(std::uint32_t p, std::uint8_t* Y, std::int64_t ldy, int kcols,
                                         std::int32_t* info, int cap, std::int32_t* base,
                                         std::int32_t* rmap, int col0) {
+  pdl_wait_and_release();
   const int r_now = info[0], b0 = *base;
   for (int t = threadIdx.x; t < kcols; t += blockDim.x) {
     const int g = b0 + t;
@@ -1381,9 +1384,46 @@ void ech_panel_plant(std::uint8_t* Y, std::int64_t ldy, const std::int32_t* rho2
 void ech_outer_finish(std::uint32_t p, std::uint8_t* Y, std::int64_t ldy, std::int64_t kcols,
                       std::int32_t* info, std::int64_t cap, std::int32_t* base,
                       std::int32_t* rmap, std::int64_t col0, cudaStream_t s) {
-  ech_outer_finish_kernel<<<1, 256, 0, s>>>(p, Y, ldy, int(kcols), info, int(cap), base, rmap,
-                                            int(col0));
-  GFQ_CUDA(cudaGetLastError());
+  GFQ_CUDA(launch_pdl(ech_outer_finish_kernel, dim3(1), dim3(256), 0, s, p, Y, ldy, int(kcols), info,
+                      int(cap), base, rmap, int(col0)));
+  count_launch();
+}
+
+// dst[i][0:wd] = src[i][0:wd], dst[i][wd:width] = 0 (16-byte aligned rows,
+// width a multiple of 16): the two-level ECH's scratch load and write-back
+// as one kernel in the step kernels' PDL chain (a cudaMemcpy2D / memset
+// would break it)
+__global__ void copy_cols_kernel(std::uint8_t* __restrict__ dst, std::int64_t ldd,
+                                 const std::uint8_t* __restrict__ src, std::int64_t lds,
+                                 std::int64_t rows, int wd, int width) {
+  pdl_wait_and_release();
+  const int nv = width / 16;
+  for (std::int64_t e = std::int64_t(blockIdx.x) * blockDim.x + threadIdx.x; e < rows * nv;
+       e += std::int64_t(gridDim.x) * blockDim.x) {
+    const std::int64_t i = e / nv;
+    const int c = int(e % nv) * 16;
+    uint4 v = make_uint4(0, 0, 0, 0);
+    if (c + 16 <= wd) {
+      v = *reinterpret_cast<const uint4*>(src + i * lds + c);
+    } else if (c < wd) {
+      std::uint8_t b[16] = {};
+      for (int t = 0; c + t < wd; ++t) b[t] = src[i * lds + c + t];
+      std::memcpy(&v, b, 16);
+    }
+    *reinterpret_cast<uint4*>(dst + i * ldd + c) = v;
+  }
+}
+
+void copy_cols(std::uint8_t* dst, std::int64_t ldd, const std::uint8_t* src, std::int64_t lds,
+               std::int64_t rows, std::int64_t wd, std::int64_t width, cudaStream_t s) {
+  if (rows == 0 || width == 0) return;
+  if (width % 16 || (ldd & 15) || (reinterpret_cast<std::uintptr_t>(dst) & 15) ||
+      (wd >= 16 && ((lds & 15) || (reinterpret_cast<std::uintptr_t>(src) & 15))))
+    throw std::invalid_argument("copy_cols: unaligned");
+  const std::int64_t work = rows * (width / 16);
+  const unsigned grid = unsigned(std::min<std::int64_t>((work + 255) / 256, 8 * sm_count()));
+  GFQ_CUDA(launch_pdl(copy_cols_kernel, dim3(grid), dim3(256), 0, s, dst, ldd, src, lds, rows, int(wd),
+                      int(width)));
   count_launch();
 }
 

@@ -211,6 +211,10 @@ void ech_panel_plant(std::uint8_t* Y, std::int64_t ldy, const std::int32_t* rho2
 void ech_outer_finish(std::uint32_t p, std::uint8_t* Y, std::int64_t ldy, std::int64_t kcols,
                       std::int32_t* info, std::int64_t cap, std::int32_t* base,
                       std::int32_t* rmap, std::int64_t col0, cudaStream_t s);
+// dst[i][0:wd] = src[i][0:wd], dst[i][wd:width] = 0 (rows 16-byte aligned,
+// width % 16 == 0); the two-level ECH's scratch copies, PDL-launched
+void copy_cols(std::uint8_t* dst, std::int64_t ldd, const std::uint8_t* src, std::int64_t lds,
+               std::int64_t rows, std::int64_t wd, std::int64_t width, cudaStream_t s);
 
 // GF(2) block ECH in one launch (rows <= 1024, cols + rows <= 8192): the
 // reduced [W | T] is written to Out (rows x (cols + rows) u8) and the pivots
