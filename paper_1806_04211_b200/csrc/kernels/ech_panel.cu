@@ -533,6 +533,7 @@ ech_panel_win_kernel(std::uint32_t p, std::uint32_t magic, int rows, int c0, int
                      const std::uint8_t* __restrict__ Aug, std::int64_t ld, std::uint8_t* flags,
                      std::int32_t* info, int cap, std::uint8_t* G, std::int64_t ldg,
                      std::int32_t* rho2, std::int32_t* lo_state) {
+  pdl_wait_and_release();
   win_body(p, magic, rows, c0, wc, Aug, ld, flags, info, cap, G, ldg, rho2, lo_state,
            StepOut{nullptr, nullptr});
 }
@@ -938,6 +939,7 @@ __global__ void __launch_bounds__(1024)
 ech_panel_gf2_kernel(int rows, int c0, int wc, const std::uint8_t* __restrict__ Aug, std::int64_t ld,
                      std::uint8_t* flags, std::int32_t* info, int cap, std::uint8_t* G,
                      std::int64_t ldg, std::int32_t* rho2) {
+  pdl_wait_and_release();
   extern __shared__ __align__(16) std::uint8_t sm[];
   std::uint32_t* bits = reinterpret_cast<std::uint32_t*>(sm);  // rows words
   std::uint8_t* fl = sm + 4 * rows;                             // rows flags
@@ -1065,6 +1067,7 @@ __global__ void __launch_bounds__(1024)
 ech_panel_gf2w_kernel(int rows, int c0, int wc, const std::uint8_t* __restrict__ Aug,
                       std::int64_t ld, std::uint8_t* flags, std::int32_t* info, int cap,
                       std::uint8_t* G, std::int64_t ldg, std::int32_t* rho2) {
+  pdl_wait_and_release();
   __shared__ std::uint32_t orig[1024];
   __shared__ int pc[kW], pr[kW];
   __shared__ std::uint32_t n2[kW];
@@ -1185,6 +1188,7 @@ ech_panel_gf2w_kernel(int rows, int c0, int wc, const std::uint8_t* __restrict__
 // Blocked ECH bookkeeping (see ech_panel_plant / ech_outer_finish below).
 __global__ void ech_plant_kernel(std::uint8_t* Y, std::int64_t ldy, const std::int32_t* rho2,
                                  const std::int32_t* info, const std::int32_t* base) {
+  pdl_wait_and_release();
   const int lane = threadIdx.x;
   const int r = rho2[lane];
   const unsigned valid = __ballot_sync(0xffffffffu, r >= 0);
@@ -1253,8 +1257,8 @@ void ech_panel(std::uint32_t p, std::int64_t rows, std::int64_t c0, std::int64_t
   const std::int64_t r32 = (rows + 31) / 32 * 32;
   const int threads = r32 >= max_threads ? max_threads : int(r32 < 64 ? 64 : r32);
   if (p == 2 && rows <= 1024) {
-    ech_panel_gf2w_kernel<<<1, 1024, 0, s>>>(int(rows), int(c0), int(wc), Aug, ld, flags, info,
-                                             int(cap), G, ldg, rho2);
+    GFQ_CUDA(launch_pdl(ech_panel_gf2w_kernel, dim3(1), dim3(1024), 0, s, int(rows), int(c0), int(wc), Aug, ld, flags, info,
+                                             int(cap), G, ldg, rho2));
     GFQ_CUDA(cudaGetLastError());
     count_launch();
     return;
@@ -1262,8 +1266,8 @@ void ech_panel(std::uint32_t p, std::int64_t rows, std::int64_t c0, std::int64_t
   if (p == 2) {
     const std::size_t smem2 = std::size_t(rows) * 5;
     if (smem2 > std::size_t(kPanelSmem)) throw std::invalid_argument("ech_panel: block too tall");
-    ech_panel_gf2_kernel<<<1, threads, smem2, s>>>(int(rows), int(c0), int(wc), Aug, ld, flags,
-                                                   info, int(cap), G, ldg, rho2);
+    GFQ_CUDA(launch_pdl(ech_panel_gf2_kernel, dim3(1), dim3(threads), smem2, s, int(rows), int(c0), int(wc), Aug, ld, flags,
+                                                   info, int(cap), G, ldg, rho2));
     GFQ_CUDA(cudaGetLastError());
     count_launch();
     return;
@@ -1280,8 +1284,8 @@ void ech_panel(std::uint32_t p, std::int64_t rows, std::int64_t c0, std::int64_t
   // the window start persists after the flags (the caller allocates
   // ech_panel_flag_bytes(rows) and zeroes them before the first panel)
   auto* lo_state = reinterpret_cast<std::int32_t*>(flags + ((rows + 15) / 16) * 16);
-  ech_panel_win_kernel<<<1, threads, smem, s>>>(p, magic, int(rows), int(c0), int(wc), Aug, ld, flags,
-                                                info, int(cap), G, ldg, rho2, lo_state);
+  GFQ_CUDA(launch_pdl(ech_panel_win_kernel, dim3(1), dim3(threads), smem, s, p, magic, int(rows), int(c0), int(wc), Aug, ld, flags,
+                                                info, int(cap), G, ldg, rho2, lo_state));
   GFQ_CUDA(cudaGetLastError());
   count_launch();
 }
@@ -1338,26 +1342,13 @@ void ech_step(std::uint32_t p, std::int64_t rows, std::int64_t c0, std::int64_t 
   std::uint8_t* NT = step_scratch;
   std::uint8_t* Gpiv = step_scratch + kW * kW;
   std::uint8_t* BpT = step_scratch + 2 * kW * kW;
-  const bool pdl = pdl_enabled();
-  cudaLaunchAttribute at[1];
-  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  at[0].val.programmaticStreamSerializationAllowed = 1;
-  cudaLaunchConfig_t cfg = {};
-  cfg.stream = s;
-  cfg.attrs = at;
-  cfg.numAttrs = pdl ? 1 : 0;
-  cfg.gridDim = dim3(1);
-  cfg.blockDim = dim3(kChainThreads);
-  cfg.dynamicSmemBytes = smem;
   const std::uint8_t* invt = inv_table(p);
-  GFQ_CUDA(cudaLaunchKernelEx(&cfg, ech_step_chain_kernel, p, magic, int(rows), int(c0), int(wc), int(n),
-                              Z, ld, flags, info, int(cap), rho2, lo_state, NT, Gpiv, Y, base, BpT, invt));
-  cfg.gridDim = dim3(unsigned((rows + kStepRows - 1) / kStepRows));
-  cfg.blockDim = dim3(kStepThreads);
-  cfg.dynamicSmemBytes = 0;
-  GFQ_CUDA(cudaLaunchKernelEx(&cfg, ech_step_update_kernel, p, magic, int(rows), int(c0), int(n), Z, ld,
-                              static_cast<const std::uint8_t*>(NT), static_cast<const std::uint8_t*>(Gpiv),
-                              static_cast<const std::int32_t*>(rho2), static_cast<const std::uint8_t*>(BpT)));
+  GFQ_CUDA(launch_pdl(ech_step_chain_kernel, dim3(1), dim3(kChainThreads), smem, s, p, magic, int(rows),
+                      int(c0), int(wc), int(n), Z, ld, flags, info, int(cap), rho2, lo_state, NT, Gpiv,
+                      Y, base, BpT, invt));
+  GFQ_CUDA(launch_pdl(ech_step_update_kernel, dim3(unsigned((rows + kStepRows - 1) / kStepRows)),
+                      dim3(kStepThreads), 0, s, p, magic, int(rows), int(c0), int(n), Z, ld, NT, Gpiv,
+                      rho2, BpT));
   static int dbg = std::getenv("GFQ_STEP_DEBUG") ? std::atoi(std::getenv("GFQ_STEP_DEBUG")) : 0;
   if (dbg > 0) {
     --dbg;
@@ -1376,7 +1367,7 @@ void ech_step(std::uint32_t p, std::int64_t rows, std::int64_t c0, std::int64_t 
 
 void ech_panel_plant(std::uint8_t* Y, std::int64_t ldy, const std::int32_t* rho2,
                      const std::int32_t* info, const std::int32_t* base, cudaStream_t s) {
-  ech_plant_kernel<<<1, 32, 0, s>>>(Y, ldy, rho2, info, base);
+  GFQ_CUDA(launch_pdl(ech_plant_kernel, dim3(1), dim3(32), 0, s, Y, ldy, rho2, info, base));
   GFQ_CUDA(cudaGetLastError());
   count_launch();
 }
