@@ -101,10 +101,17 @@ int gfq_field_op(uint32_t code, int op, uint32_t a, uint32_t b, uint32_t* out);
 int gfq_default_modulus(uint32_t p, uint32_t k, uint32_t* modulus);
 int gfq_random_product_matrix(uint32_t p, int64_t rows, int64_t cols, int64_t inner,
                               uint64_t seed, gfq_mat** out);
+/* Developer check (no reference counterpart): bit 0 fills every device
+ * allocation with 0xA5, bit 1 every freed block with 0x5A, each on its
+ * stream, so reads of never-written or released memory change results. */
+int gfq_set_poison(int mode);
 /* Base-case size of the device ECH recursion (<= 128; results unaffected). */
 int gfq_set_ech_base(uint64_t n);
-/* ECH algorithm: 0 = panel Gauss-Jordan on [W | T] (default), 1 = the
- * reference's split/combine recursion (jobs.cpp:202-225).  Same outputs. */
+/* ECH algorithm: 0 = device ECH (default; GF(2) blocks larger than the
+ * cluster kernel's 1024 rows / 8192 packed columns split by the reference's
+ * rule down to it), 1 = the reference's split/combine recursion
+ * (src/jobs.cpp:202-225) over the small base kernel, 2 = as 0 but tall GF(2)
+ * blocks on the two-level panel path.  Same outputs. */
 int gfq_set_ech_mode(int mode);
 /* Outer panel width of the two-level device ECH: -1 = automatic (default),
  * 0 = one level (32-wide steps over all of [W | T]), else 32..256 (rounded

@@ -78,6 +78,7 @@ PROTOS = {
     "gfq_field_op": (I, [U32, I, U32, U32, ctypes.c_void_p]),
     "gfq_default_modulus": (I, [U32, U32, ctypes.c_void_p]),
     "gfq_set_ech_mode": (I, [I]),
+    "gfq_set_poison": (I, [I]),
     "gfq_launch_count": (I, [I, c_i64p]),
     "gfq_profile": (I, [I]),
     "gfq_profile_take": (I, [c_i64p, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_double)]),

@@ -303,11 +303,17 @@ int gfq_random_product_matrix(uint32_t p, int64_t rows, int64_t cols, int64_t in
   });
 }
 
+int gfq_set_poison(int mode) {
+  return guard([&] {
+    if (mode < 0 || mode > 3) throw std::invalid_argument("poison mode must be 0..3");
+    gfq::set_poison_mode(mode);
+  });
+}
 int gfq_set_ech_base(uint64_t n) { return guard([&] { gfq::set_ech_base(size_t(n)); }); }
 int gfq_set_ech_outer(int width) { return guard([&] { gfq::set_ech_outer(width); }); }
 int gfq_set_ech_mode(int mode) {
   return guard([&] {
-    if (mode != 0 && mode != 1) throw std::invalid_argument("ech mode must be 0 or 1");
+    if (mode < 0 || mode > 2) throw std::invalid_argument("ech mode must be 0, 1 or 2");
     gfq::set_ech_mode(mode);
   });
 }

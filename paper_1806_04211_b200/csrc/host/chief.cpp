@@ -699,6 +699,12 @@ EchelonOutput echelonize_impl(const Mat& C, const FieldSpec& field, const Echelo
     return out;
   }
 
+  // the run's working set (input-sized panels, the transformation, ECH
+  // scratch) in one pool growth step, not hundreds of cache misses
+  {
+    const std::size_t m = std::size_t(C.rows()), n = std::size_t(C.cols());
+    reserve_pool(2 * m * n + (options.with_transform ? 2 * m * m : 0));
+  }
   TaskGraph graph;
   graph.ech_threshold = options.ech_threshold;
   const bool fused = options.fuse && 2 * a + 1 <= std::size_t(TaskNode::kMaxIn);

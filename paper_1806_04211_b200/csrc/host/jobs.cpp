@@ -482,6 +482,22 @@ EchResult panel_ech(const FieldSpec& f, const Mat& h) {
   return extract_ech(a, b, aug, inf, cap, tb);
 }
 
+// GF(2) blocks the cluster kernel (ech_gf2_cluster) eliminates in one
+// launch: <= 1024 rows, the packed [W | T] row of <= 256 words.
+constexpr std::int64_t kGf2ClusterRows = 1024;
+bool gf2_cluster_fits(std::int64_t a, std::int64_t b) {
+  return a <= kGf2ClusterRows && (a + b + 31) / 32 <= 256;
+}
+// ech mode 2 (or GFQ_GF2_SPLIT=0) keeps tall GF(2) blocks on the
+// two-level panel path
+bool gf2_split_enabled() {
+  static const bool on = [] {
+    const char* e = std::getenv("GFQ_GF2_SPLIT");
+    return !(e && e[0] == '0');
+  }();
+  return on && ech_mode() != 2;
+}
+
 // Split point: half, rounded to a multiple of 16 so column views keep the
 // 16-byte alignment the TMA path needs (outputs do not depend on it).
 std::int64_t split_of(std::int64_t n) {
@@ -560,7 +576,22 @@ EchResult ech(const FieldSpec& f, const Mat& h, std::size_t threshold) {
   }
   // GF(p^k): the reference's split/combine recursion (its products are
   // digit-plane K1 contractions) over the table-driven base case
-  if (ech_mode() == 0 && !f.is_ext()) {
+  if (ech_mode() != 1 && !f.is_ext()) {
+    // GF(2): the 8-CTA cluster kernel takes blocks of <= 1024 rows with
+    // rows + cols <= 8192; anything larger follows the reference's own
+    // split rule (src/jobs.cpp:202-225: rows when alpha >= beta, else
+    // columns) down to it, so a tall 8192^2 ECH is eight cluster ECHs plus
+    // K1 combines instead of 256 single-CTA panel steps.
+    if (f.p() == 2 && gf2_split_enabled() && !gf2_cluster_fits(alpha, beta)) {
+      if (alpha >= beta || alpha > kGf2ClusterRows) {
+        const std::int64_t alpha1 = split_of(alpha);
+        const EchResult e1 = ech(f, h.row_view(0, alpha1), threshold);
+        return combine_horizontal(f, h.row_view(alpha1, alpha - alpha1), e1, alpha1, threshold);
+      }
+      const std::int64_t beta1 = split_of(beta);
+      const EchResult e1 = ech(f, h.col_view(0, beta1), threshold);
+      return combine_vertical(f, h.col_view(beta1, beta - beta1), e1, beta1, threshold);
+    }
     // panel ECH whenever the panel fits one CTA's shared memory; taller
     // blocks split their rows (reference combine_horizontal) first
     if (alpha * (f.p() == 2 ? 5 : 33) <= dev::kPanelSmem) return panel_ech(f, h);

@@ -402,6 +402,45 @@ void* take(std::unordered_map<std::size_t, std::vector<void*>>& lists, std::size
 }
 }  // namespace
 
+namespace {
+std::atomic<int> g_poison{[] {
+  const char* e = std::getenv("GFQ_POISON");
+  return e ? std::atoi(e) : 0;
+}()};
+}  // namespace
+int poison_mode() { return g_poison.load(std::memory_order_relaxed); }
+void set_poison_mode(int mode) { g_poison = mode; }
+
+// Grow the stream-ordered pool in ONE step to hold `bytes` more than it
+// uses now: hundreds of block-cache misses that each grow the pool by a
+// mapping cost milliseconds apiece (cfg5s: ~500 misses, first steps up to
+// 1.6x slower); one big reservation up front makes them cheap carve-outs.
+void reserve_pool(std::size_t bytes) {
+  init_pool();
+  int dev = 0;
+  GFQ_CUDA(cudaGetDevice(&dev));
+  cudaMemPool_t pool;
+  GFQ_CUDA(cudaDeviceGetDefaultMemPool(&pool, dev));
+  std::uint64_t reserved = 0, used = 0;
+  GFQ_CUDA(cudaMemPoolGetAttribute(pool, cudaMemPoolAttrReservedMemCurrent, &reserved));
+  GFQ_CUDA(cudaMemPoolGetAttribute(pool, cudaMemPoolAttrUsedMemCurrent, &used));
+  if (reserved >= used + bytes) return;
+  std::size_t free_b = 0, total_b = 0;
+  GFQ_CUDA(cudaMemGetInfo(&free_b, &total_b));
+  std::size_t want = used + bytes - reserved;
+  const std::size_t cap = free_b > (std::size_t(2) << 30) ? free_b - (std::size_t(2) << 30) : 0;
+  if (want > cap) want = cap;
+  if (want < (std::size_t(64) << 20)) return;
+  void* p = nullptr;
+  const cudaStream_t s = cur_stream_raw();
+  if (cudaMallocAsync(&p, want, s) == cudaSuccess) {
+    GFQ_CUDA(cudaFreeAsync(p, s));
+    GFQ_CUDA(cudaStreamSynchronize(s));
+  } else {
+    cudaGetLastError();
+  }
+}
+
 void release_stream(cudaStream_t s) {
   BlockCache& c = cache();
   std::lock_guard<std::mutex> lk(c.mtx);
@@ -453,6 +492,10 @@ DevBuf::DevBuf(std::size_t n) : bytes(n) {
     c.cls_of[p] = cls;
   }
   ptr = static_cast<std::uint8_t*>(p);
+  // Developer check (GFQ_POISON bit 0): fill every allocation with 0xA5 on
+  // its stream, so a read of memory the code never wrote shows up as a
+  // wrong result instead of silently seeing zeros or a recycled block.
+  if (poison_mode() & 1) GFQ_CUDA(cudaMemsetAsync(p, 0xA5, cls, s));
   const std::int64_t now = (g_live += std::int64_t(n));
   std::int64_t prev = g_peak.load();
   while (now > prev && !g_peak.compare_exchange_weak(prev, now)) {
@@ -464,6 +507,10 @@ DevBuf::~DevBuf() {
     // Stream-ordered release: every job on this value was issued on the
     // current stream (or joined into it by the executor) before release.
     hprof::Scope hp(hprof::kFree);
+    // GFQ_POISON bit 1: overwrite the block on the freeing stream, so a
+    // kernel on another stream that still reads it (a missing dependency)
+    // sees garbage.
+    if (poison_mode() & 2) cudaMemsetAsync(ptr, 0x5A, bytes, cur_stream_raw());
     BlockCache& c = cache();
     std::lock_guard<std::mutex> lk(c.mtx);
     auto it = c.cls_of.find(ptr);

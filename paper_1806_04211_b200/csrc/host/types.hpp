@@ -86,6 +86,13 @@ struct DevBuf {
 /// The stream `s` has drained (synchronised): blocks released on it become
 /// reusable from any stream.
 void release_stream(cudaStream_t s);
+/// Developer check: bit 0 fills every allocation with 0xA5, bit 1 every
+/// freed block with 0x5A (on its stream); GFQ_POISON sets the start value.
+int poison_mode();
+void set_poison_mode(int mode);
+/// Make the stream-ordered pool hold `bytes` beyond its current use (one
+/// growth step instead of many small ones).
+void reserve_pool(std::size_t bytes);
 /// One-time runtime setup (memory pool attributes, pinned staging ring).
 void warm_runtime();
 

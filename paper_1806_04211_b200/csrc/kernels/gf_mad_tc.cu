@@ -16,6 +16,7 @@
 //
 // Exactness: (p-1)^2 * k + (p-1) < 2^31 is required per launch; the host
 // splits K into chunks and chains them through the addend (mod p between).
+#include <vector>
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
@@ -484,13 +485,29 @@ bool mad_tc(std::uint32_t p, std::int64_t m, std::int64_t n, std::int64_t k,
   const bool narrow = 11 * ((t128 + sms - 1) / sms) < 18 * ((t256 + sms - 1) / sms);
   const std::int64_t tiles = narrow ? t128 : t256;
   const int grid = int(tiles < sms ? tiles : sms);
-  for (std::int64_t k0 = 0; k0 < k; k0 += kc) {
-    const std::int64_t kk = (k - k0) < kc ? (k - k0) : kc;
+  // Every chunk's tensor maps are built (and validated) before the first
+  // launch: returning false after a launch would let the caller's SIMT
+  // fallback re-add A.B onto a D that already holds part of it (in-place
+  // callers pass Cin == D).
+  struct Chunk {
+    std::int64_t k0, kk;
     CUtensorMap mA, mB;
+  };
+  std::vector<Chunk> chunks;
+  for (std::int64_t k0 = 0; k0 < k; k0 += kc) {
+    Chunk c;
+    c.k0 = k0;
+    c.kk = (k - k0) < kc ? (k - k0) : kc;
     // A sub-block starting at column k0 must stay 16B aligned.
     if ((k0 & 15) != 0) return false;
-    if (!make_map(&mA, A + k0, kk, m, lda)) return false;
-    if (!make_map(&mB, B + k0 * ldb, n, kk, ldb)) return false;
+    if (!make_map(&c.mA, A + k0, c.kk, m, lda)) return false;
+    if (!make_map(&c.mB, B + k0 * ldb, n, c.kk, ldb)) return false;
+    chunks.push_back(c);
+  }
+  for (const Chunk& c : chunks) {
+    const std::int64_t k0 = c.k0, kk = c.kk;
+    const CUtensorMap& mA = c.mA;
+    const CUtensorMap& mB = c.mB;
     const std::uint8_t* cin = k0 == 0 ? Cin : D;
     const std::int64_t ldcin = k0 == 0 ? ldc : ldd;
     if (narrow)

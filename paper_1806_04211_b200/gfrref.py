@@ -950,8 +950,15 @@ def set_ech_outer(width: int):
     _check(lib().gfq_set_ech_outer(width))
 
 
+def set_poison(mode: int):
+    """Developer check: bit 0 poisons allocations (0xA5), bit 1 freed blocks (0x5A)."""
+    _check(lib().gfq_set_poison(mode))
+
+
 def set_ech_mode(mode: int):
-    """0 = device panel Gauss-Jordan (default), 1 = reference split/combine recursion."""
+    """0 = device ECH (default: GF(2) blocks beyond the cluster kernel split by the
+    reference rule), 1 = reference split/combine recursion over the small base
+    kernel, 2 = device ECH with tall GF(2) blocks on the two-level panel path."""
     _check(lib().gfq_set_ech_mode(mode))
 
 

@@ -312,3 +312,40 @@ def test_generator_matches_reference(G, ref_runs):
                                       oracle.random_matrix(p, m, n, seed))
     np.testing.assert_array_equal(G.random_product_matrix(G.FieldSpec(7), 300, 280, 100, 4).numpy(),
                                   oracle.random_product_matrix(7, 300, 280, 100, 4))
+
+
+@pytest.mark.parametrize("case", ["square2048", "tall1536", "wide1000x7500", "low2048", "zero_rows"])
+def test_ech_gf2_split_vs_reference(G, case):
+    """GF(2) blocks beyond the cluster kernel (> 1024 rows, or rows + cols >
+    8192) split by the reference's rule (src/jobs.cpp:202-225) down to it;
+    bit-exact against the reference's own ech and the two-level panel path."""
+    p = 2
+    f = G.FieldSpec(p)
+    rng = np.random.default_rng(7)
+    if case == "square2048":
+        H = rnd(p, 2048, 2048, 61)
+    elif case == "tall1536":
+        H = rnd(p, 1536, 900, 62)
+    elif case == "wide1000x7500":
+        H = rnd(p, 1000, 7500, 63)
+    elif case == "low2048":
+        P = rng.integers(0, 2, (2048, 1500)).astype(np.float64)
+        Q = rng.integers(0, 2, (1500, 2048)).astype(np.float64)
+        H = (P @ Q).astype(np.int64).__mod__(2).astype(np.uint8)
+    else:
+        H = rnd(p, 2100, 1100, 64)
+        H[:700] = 0
+        H[1500:1800] = H[100:400] ^ H[900:1200]
+    want = oracle.ref_ech(p, H)
+    G.set_ech_mode(0)
+    got = G.ech(f, H)
+    G.set_ech_mode(2)
+    try:
+        alt = G.ech(f, H)
+    finally:
+        G.set_ech_mode(0)
+    for e in (got, alt):
+        assert e.rank() == want["rank"]
+        assert list(e.rho.members) == list(want["rho"]) and list(e.gamma.members) == list(want["gamma"])
+        for key in "MKR":
+            np.testing.assert_array_equal(getattr(e, key).numpy(), want[key])

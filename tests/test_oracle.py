@@ -286,3 +286,27 @@ def test_restatement_vs_live_reference_more_cases():
             for l in range(j, ref.b):
                 np.testing.assert_array_equal(got.R_blocks[(j, l)], ref.block(0, j, l))
         np.testing.assert_array_equal(got.materialize_transform(), ref.materialize_transform())
+
+
+@pytest.mark.skipif(oracle.ref is None, reason="oracle/_ref not built")
+@pytest.mark.parametrize("p", [2, 3, 251])
+def test_reference_tk_support_is_lex_first(p):
+    """The structural pin used for cfg5s (tests/test_gpu_configs.py): in the
+    reference's own output every T_K row (a non-selected row t) is supported
+    only on selected rows of smaller index -- varrho is the
+    lexicographically-first row basis (src/chief.cpp:436-460)."""
+    rng = np.random.default_rng(p)
+    for t, (m, n, r, block) in enumerate([(60, 50, 20, 16), (90, 40, 35, 32), (64, 64, 64, 16)]):
+        P = oracle.random_matrix(p, m, r, 300 + t)
+        Q = oracle.random_matrix(p, r, n, 400 + t)
+        C = oracle.mad(p, P, Q)
+        C[rng.choice(m, m // 5, replace=False)] = 0
+        ref = oracle.ref_echelonize(p, C, block, threads=2)
+        for i in range(ref.a):
+            sel = ref.varrho(i).astype(np.int64)
+            rows_i = min(block, m - i * block)
+            non = np.setdiff1d(np.arange(rows_i), sel)
+            tk = ref.block(2, i, i)
+            assert tk.shape == (len(non), len(sel))
+            if tk.size:
+                assert not np.any(tk[sel[None, :] > non[:, None]])
