@@ -324,6 +324,13 @@ int gfq_profile(int on) { return guard([&] { gfq::dev::set_profile(on != 0); });
 int gfq_profile_take(int64_t* launches2, double* ops2, double* ms2) {
   return guard([&] { gfq::dev::profile_take(launches2, ops2, ms2); });
 }
+int gfq_profile_take_kinds(int n, int64_t* launches, double* work, double* ms) {
+  return guard([&] {
+    if (n < 0 || (n > 0 && (!launches || !work || !ms)))
+      throw std::invalid_argument("gfq_profile_take_kinds: bad buffers");
+    gfq::dev::profile_take_kinds(n, launches, work, ms);
+  });
+}
 int gfq_tc_debug_take(uint64_t* stamps) {
   return guard([&] {
     if (!stamps) throw std::invalid_argument("gfq_tc_debug_take: null buffer");

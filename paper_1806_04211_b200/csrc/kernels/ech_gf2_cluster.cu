@@ -630,6 +630,9 @@ bool ech_gf2_cluster(std::int64_t rows, std::int64_t cols, const std::uint8_t* H
                                       kExBytes)));
     attr = true;
   }
+  // algorithmic bytes: H read, M / K / R written (rank taken as min(rows, cols))
+  const double rk = double(std::min(rows, cols));
+  ProfScope ps(kProfEchGf2, double(rows) * double(cols) + rk * (double(rows) + double(cols) - rk), s);
   static const bool debug = std::getenv("GFQ_GF2_DEBUG") != nullptr;
   static unsigned long long* dbg = nullptr;
   if (debug && !dbg) GFQ_CUDA(cudaMalloc(&dbg, 9 * 16 * sizeof(unsigned long long)));
@@ -806,6 +809,8 @@ bool ech_gf2_small(std::int64_t rows, std::int64_t cols, const std::uint8_t* H, 
                                   200 * 1024));
     attr = true;
   }
+  const double rk = double(std::min(rows, cols));
+  ProfScope ps(kProfEchGf2, double(rows) * double(cols) + rk * (double(rows) + double(cols) - rk), s);
   ech_gf2_small_kernel<<<1, 32, smem, s>>>(int(rows), int(cols), H, ldh, info, int(cap), ex);
   GFQ_CUDA(cudaGetLastError());
   count_launch();

@@ -1256,6 +1256,8 @@ void ech_panel(std::uint32_t p, std::int64_t rows, std::int64_t c0, std::int64_t
   }();
   const std::int64_t r32 = (rows + 31) / 32 * 32;
   const int threads = r32 >= max_threads ? max_threads : int(r32 < 64 ? 64 : r32);
+  // algorithmic bytes: the rows x 32 panel read, G (rows x 32) written
+  ProfScope ps(kProfEchPanel, 2.0 * double(rows) * double(kW), s);
   if (p == 2 && rows <= 1024) {
     GFQ_CUDA(launch_pdl(ech_panel_gf2w_kernel, dim3(1), dim3(1024), 0, s, int(rows), int(c0), int(wc), Aug, ld, flags, info,
                                              int(cap), G, ldg, rho2));
@@ -1338,6 +1340,8 @@ void ech_step(std::uint32_t p, std::int64_t rows, std::int64_t c0, std::int64_t 
     attr = true;
   }
   const std::uint32_t magic = static_cast<std::uint32_t>((0x100000000ULL / p) + 1);
+  // algorithmic bytes: the step's rows x n slice of Z read and written
+  ProfScope ps(kProfEchPanel, 2.0 * double(rows) * double(n), s);
   auto* lo_state = reinterpret_cast<std::int32_t*>(flags + ((rows + 15) / 16) * 16);
   std::uint8_t* NT = step_scratch;
   std::uint8_t* Gpiv = step_scratch + kW * kW;

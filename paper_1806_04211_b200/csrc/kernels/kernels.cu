@@ -4,6 +4,7 @@
 //   K2 base case (single-CTA Gauss-Jordan ECH in shared memory),
 //   K6 (counter-form SplitMix64 generator).
 // The tensor-core contraction lives in gf_mad_tc.cu.
+#include <cstdio>
 #include <algorithm>
 #include <atomic>
 #include <mutex>
@@ -244,27 +245,48 @@ std::int64_t launch_count(bool reset) {
   return reset ? g_launches.exchange(0) : g_launches.load();
 }
 void set_profile(bool on) { g_profile = on; }
-void profile_take(std::int64_t launches[2], double ops[2], double ms[2]) {
+bool profile_on() { return g_profile; }
+
+ProfScope::ProfScope(int kind, double work, cudaStream_t s) : work_(work), kind_(kind), s_(s) {
+  if (!g_profile) return;
+  GFQ_CUDA(cudaEventCreate(&e0_));
+  GFQ_CUDA(cudaEventCreate(&e1_));
+  GFQ_CUDA(cudaEventRecord(e0_, s_));
+}
+ProfScope::~ProfScope() {
+  if (!e0_) return;
+  cudaEventRecord(e1_, s_);
+  std::lock_guard<std::mutex> lk(g_prof_mtx);
+  g_prof.push_back(ProfRec{e0_, e1_, work_, kind_});
+}
+
+void profile_take_kinds(int n, std::int64_t* launches, double* work, double* ms) {
   std::vector<ProfRec> recs;
   {
     std::lock_guard<std::mutex> lk(g_prof_mtx);
     recs.swap(g_prof);
   }
-  for (int q = 0; q < 2; ++q) {
+  for (int q = 0; q < n; ++q) {
     launches[q] = 0;
-    ops[q] = 0;
+    work[q] = 0;
     ms[q] = 0;
   }
   for (auto& r : recs) {
     float t = 0;
     GFQ_CUDA(cudaEventSynchronize(r.e1));
     GFQ_CUDA(cudaEventElapsedTime(&t, r.e0, r.e1));
-    launches[r.path] += 1;
-    ops[r.path] += r.ops;
-    ms[r.path] += t;
+    if (r.path < n) {
+      launches[r.path] += 1;
+      work[r.path] += r.ops;
+      ms[r.path] += t;
+    }
     cudaEventDestroy(r.e0);
     cudaEventDestroy(r.e1);
   }
+}
+
+void profile_take(std::int64_t launches[2], double ops[2], double ms[2]) {
+  profile_take_kinds(2, launches, ops, ms);
 }
 
 void set_mad_policy(int policy) { g_policy = policy; }
@@ -331,6 +353,11 @@ void mad(std::uint32_t p, std::int64_t m, std::int64_t n, std::int64_t k,
     std::lock_guard<std::mutex> lk(g_prof_mtx);
     g_prof.push_back(rec);
   }
+  // developer log of every contraction's shape and path (GFQ_MAD_LOG)
+  static const bool log = std::getenv("GFQ_MAD_LOG") != nullptr;
+  if (log)
+    std::fprintf(stderr, "mad m=%lld n=%lld k=%lld path=%s\n", static_cast<long long>(m),
+                 static_cast<long long>(n), static_cast<long long>(k), rec.path ? "simt" : "tc");
 }
 
 // ------------------------------------------------------------------ K3/K4
@@ -570,6 +597,7 @@ bool select2d_inline(std::uint8_t* dst, std::int64_t ldd, std::int64_t rows, std
   };
   if ((rmap && !fits(rmap, rows)) || (cmap && !fits(cmap, cols))) return false;
   hprof::Scope hp(hprof::kSelect);
+  ProfScope ps(kProfSelect, 2.0 * double(rows) * double(cols) + 4.0 * double(n), s);
   if (n <= 512) return launch_inline<512>(dst, ldd, rows, cols, A, lda, B, ldb, rmap, cmap, s);
   if (n <= 1536) return launch_inline<1536>(dst, ldd, rows, cols, A, lda, B, ldb, rmap, cmap, s);
   return launch_inline<4096>(dst, ldd, rows, cols, A, lda, B, ldb, rmap, cmap, s);
@@ -581,6 +609,8 @@ void select2d(std::uint8_t* dst, std::int64_t ldd, std::int64_t rows,
               const std::int32_t* cmap, cudaStream_t s) {
   if (rows == 0 || cols == 0) return;
   hprof::Scope hp(hprof::kSelect);
+  ProfScope ps(kProfSelect,
+               2.0 * double(rows) * double(cols) + 4.0 * double((rmap ? rows : 0) + (cmap ? cols : 0)), s);
   const unsigned gy = unsigned(rows < 65535 ? rows : 65535);
   const auto al = [](const void* ptr, std::int64_t ld) {
     return ptr == nullptr ||

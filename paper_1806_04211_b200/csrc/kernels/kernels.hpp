@@ -77,7 +77,36 @@ bool mad_tc(std::uint32_t p, std::int64_t m, std::int64_t n, std::int64_t k,
 void count_launch(std::int64_t n = 1);
 std::int64_t launch_count(bool reset);
 void set_profile(bool on);
+bool profile_on();
 void profile_take(std::int64_t launches[2], double ops[2], double ms[2]);
+// Kernel families timed by the profiler (bench.py's roofline lines): the
+// work unit is int8 ops (2*m*n*k) for the contractions, algorithmic bytes
+// (u8 payload read + written, +4 B per index) for the HBM-bound families.
+enum ProfKind : int {
+  kProfTc = 0,       // K1 tcgen05 contraction            (ops)
+  kProfSimt = 1,     // K1 SIMT / small-K contraction     (ops)
+  kProfEchGf2 = 2,   // GF(2) cluster / small ECH kernels (bytes)
+  kProfEchPanel = 3, // general-p panel / step ECH kernels (bytes)
+  kProfSelect = 4,   // row / column gathers, riffles      (bytes)
+  kProfKinds = 5
+};
+// Brackets the launches issued in its scope with CUDA events on `s` when
+// profiling is on (a no-op otherwise).
+class ProfScope {
+ public:
+  ProfScope(int kind, double work, cudaStream_t s);
+  ~ProfScope();
+  void set_kind(int kind) { kind_ = kind; }
+  ProfScope(const ProfScope&) = delete;
+  ProfScope& operator=(const ProfScope&) = delete;
+
+ private:
+  cudaEvent_t e0_ = nullptr, e1_ = nullptr;
+  double work_ = 0;
+  int kind_ = 0;
+  cudaStream_t s_ = nullptr;
+};
+void profile_take_kinds(int n, std::int64_t* launches, double* work, double* ms);
 
 // Developer timing of K1 (env GFQ_TC_DEBUG): per-CTA globaltimer stamps of
 // the last launch, 148 x 8 u64 (0 start, 1 setup done, 2 first stage

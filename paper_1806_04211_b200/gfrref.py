@@ -982,6 +982,20 @@ def profile_take():
     return {"tc": (l[0], o[0], t[0]), "simt": (l[1], o[1], t[1])}
 
 
+PROFILE_KINDS = ("k1_tc", "k1_simt", "ech_gf2", "ech_panel", "select")
+
+
+def profile_take_kinds():
+    """Per kernel family since the last take: {name: (launches, work, ms)};
+    work = int8 ops for k1_*, algorithmic bytes for the others."""
+    n = len(PROFILE_KINDS)
+    l = (ctypes.c_int64 * n)()
+    w = (ctypes.c_double * n)()
+    t = (ctypes.c_double * n)()
+    _check(lib().gfq_profile_take_kinds(n, l, w, t))
+    return {name: (l[q], w[q], t[q]) for q, name in enumerate(PROFILE_KINDS)}
+
+
 def set_stream(stream_ptr: int):
     _check(lib().gfq_set_stream(stream_ptr or None))
 

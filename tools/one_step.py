@@ -23,6 +23,9 @@ if "--warm" in sys.argv:
     G.synchronize()
 reps = int(sys.argv[sys.argv.index("--reps") + 1]) if "--reps" in sys.argv else 1
 walls = []
+if "--prof" in sys.argv:
+    G.profile(True)
+    G.profile_take_kinds()
 for _ in range(reps):
     t0 = time.time()
     out = G.echelonize(C, f, G.EchelonizeOptions(block=cfg["block"], threads=threads,
@@ -30,6 +33,12 @@ for _ in range(reps):
     G.synchronize()
     walls.append(1e3 * (time.time() - t0))
 print("rank", out.rank, "wall_ms", " ".join(f"{w:.2f}" for w in walls), "min", f"{min(walls):.2f}")
+if "--prof" in sys.argv:
+    for k, (l, w, ms) in G.profile_take_kinds().items():
+        unit = "TOPS" if k.startswith("k1") else "GB/s"
+        rate = (w / (ms / 1e3) / (1e12 if unit == "TOPS" else 1e9)) if ms > 0 else 0
+        print(f"prof {k:10s} launches {l / reps:8.1f}/step  ms {ms / reps:8.2f}/step  {rate:9.1f} {unit}")
+    G.profile(False)
 if "--trace" in sys.argv:
     import csv
     with open(sys.argv[sys.argv.index("--trace") + 1], "w") as fh:
