@@ -124,6 +124,10 @@ int gfq_set_ech_outer(int width);
 int gfq_launch_count(int reset, int64_t* launches);
 int gfq_profile(int on);
 int gfq_profile_take(int64_t* launches2, double* ops2, double* ms2);
+/* HBM accounting: bytes held by live device matrices / scratch (the
+ * library's own allocations), their high-water mark since the last reset,
+ * and the stream-ordered pool's reserved high-water. */
+int gfq_device_memory(int reset_peak, int64_t* live, int64_t* peak, int64_t* pool_reserved);
 /* The same per kernel family (n <= 5): [0] K1 tcgen05, [1] K1 SIMT (work =
  * int8 ops), [2] GF(2) cluster ECH, [3] general-p panel/step ECH, [4]
  * gathers/riffles (work = algorithmic bytes read + written). */

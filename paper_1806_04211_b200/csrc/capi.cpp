@@ -324,6 +324,22 @@ int gfq_profile(int on) { return guard([&] { gfq::dev::set_profile(on != 0); });
 int gfq_profile_take(int64_t* launches2, double* ops2, double* ms2) {
   return guard([&] { gfq::dev::profile_take(launches2, ops2, ms2); });
 }
+int gfq_device_memory(int reset_peak, int64_t* live, int64_t* peak, int64_t* pool_reserved) {
+  return guard([&] {
+    if (live) *live = gfq::live_device_bytes();
+    if (peak) *peak = gfq::peak_device_bytes();
+    if (pool_reserved) {
+      int dev = 0;
+      GFQ_CUDA(cudaGetDevice(&dev));
+      cudaMemPool_t pool;
+      GFQ_CUDA(cudaDeviceGetDefaultMemPool(&pool, dev));
+      std::uint64_t v = 0;
+      GFQ_CUDA(cudaMemPoolGetAttribute(pool, cudaMemPoolAttrReservedMemHigh, &v));
+      *pool_reserved = int64_t(v);
+    }
+    if (reset_peak) gfq::reset_peak_device_bytes();
+  });
+}
 int gfq_profile_take_kinds(int n, int64_t* launches, double* work, double* ms) {
   return guard([&] {
     if (n < 0 || (n > 0 && (!launches || !work || !ms)))

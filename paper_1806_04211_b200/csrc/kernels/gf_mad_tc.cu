@@ -489,33 +489,55 @@ bool mad_tc(std::uint32_t p, std::int64_t m, std::int64_t n, std::int64_t k,
   // launch: returning false after a launch would let the caller's SIMT
   // fallback re-add A.B onto a D that already holds part of it (in-place
   // callers pass Cin == D).
+  // Row pieces: a persistent launch holds every SM until its last tile, so
+  // a long one starves the critical-path ECH on the high-priority stream;
+  // GFQ_K1_MAX_WAVES = w cuts launches to <= w tile waves each (row pieces
+  // of the output), letting the block scheduler interleave between them.
+  static const std::int64_t max_waves = [] {
+    const char* e = std::getenv("GFQ_K1_MAX_WAVES");
+    return e ? std::int64_t(std::atoll(e)) : std::int64_t(0);
+  }();
+  const std::int64_t tiles_per_rowtile = narrow ? (n + 127) / 128 : (n + 255) / 256;
+  std::int64_t mp = m;
+  if (max_waves > 0 && tiles > max_waves * sms)
+    mp = std::max<std::int64_t>(1, (max_waves * sms) / tiles_per_rowtile) * BM;
   struct Chunk {
-    std::int64_t k0, kk;
+    std::int64_t m0, mm, k0, kk;
+    int grid;
     CUtensorMap mA, mB;
   };
   std::vector<Chunk> chunks;
   for (std::int64_t k0 = 0; k0 < k; k0 += kc) {
-    Chunk c;
-    c.k0 = k0;
-    c.kk = (k - k0) < kc ? (k - k0) : kc;
-    // A sub-block starting at column k0 must stay 16B aligned.
-    if ((k0 & 15) != 0) return false;
-    if (!make_map(&c.mA, A + k0, c.kk, m, lda)) return false;
-    if (!make_map(&c.mB, B + k0 * ldb, n, c.kk, ldb)) return false;
-    chunks.push_back(c);
+    for (std::int64_t m0 = 0; m0 < m; m0 += mp) {
+      Chunk c;
+      c.m0 = m0;
+      c.mm = std::min(mp, m - m0);
+      c.k0 = k0;
+      c.kk = (k - k0) < kc ? (k - k0) : kc;
+      const std::int64_t t = (c.mm + BM - 1) / BM * tiles_per_rowtile;
+      c.grid = int(t < sms ? t : sms);
+      // A sub-block starting at column k0 must stay 16B aligned.
+      if ((k0 & 15) != 0) return false;
+      if (!make_map(&c.mA, A + m0 * lda + k0, c.kk, c.mm, lda)) return false;
+      if (!make_map(&c.mB, B + k0 * ldb, n, c.kk, ldb)) return false;
+      chunks.push_back(c);
+    }
   }
+  (void)grid;
   for (const Chunk& c : chunks) {
-    const std::int64_t k0 = c.k0, kk = c.kk;
+    const std::int64_t k0 = c.k0, kk = c.kk, m0 = c.m0;
     const CUtensorMap& mA = c.mA;
     const CUtensorMap& mB = c.mB;
     const std::uint8_t* cin = k0 == 0 ? Cin : D;
     const std::int64_t ldcin = k0 == 0 ? ldc : ldd;
+    if (cin) cin += m0 * ldcin;
+    std::uint8_t* d = D + m0 * ldd;
     if (narrow)
-      GFQ_CUDA(launch_pdl(gf_mad_tc_kernel<128>, dim3(grid), dim3(NUM_THREADS), Geo<128>::SMEM_BYTES, s, 
-          mA, mB, int(m), int(n), int(kk), p, magic, cin, ldcin, D, ldd, tc_debug_buf()));
+      GFQ_CUDA(launch_pdl(gf_mad_tc_kernel<128>, dim3(c.grid), dim3(NUM_THREADS), Geo<128>::SMEM_BYTES, s,
+          mA, mB, int(c.mm), int(n), int(kk), p, magic, cin, ldcin, d, ldd, tc_debug_buf()));
     else
-      GFQ_CUDA(launch_pdl(gf_mad_tc_kernel<256>, dim3(grid), dim3(NUM_THREADS), Geo<256>::SMEM_BYTES, s, 
-          mA, mB, int(m), int(n), int(kk), p, magic, cin, ldcin, D, ldd, tc_debug_buf()));
+      GFQ_CUDA(launch_pdl(gf_mad_tc_kernel<256>, dim3(c.grid), dim3(NUM_THREADS), Geo<256>::SMEM_BYTES, s,
+          mA, mB, int(c.mm), int(n), int(kk), p, magic, cin, ldcin, d, ldd, tc_debug_buf()));
     GFQ_CUDA(cudaGetLastError());
     count_launch();
   }

@@ -597,6 +597,10 @@ bool select2d_inline(std::uint8_t* dst, std::int64_t ldd, std::int64_t rows, std
   };
   if ((rmap && !fits(rmap, rows)) || (cmap && !fits(cmap, cols))) return false;
   hprof::Scope hp(hprof::kSelect);
+  static const bool log = std::getenv("GFQ_MAD_LOG") != nullptr;
+  if (log)
+    std::fprintf(stderr, "select rows=%lld cols=%lld rmap=%d cmap=%d inline\n", static_cast<long long>(rows),
+                 static_cast<long long>(cols), rmap ? 1 : 0, cmap ? 1 : 0);
   ProfScope ps(kProfSelect, 2.0 * double(rows) * double(cols) + 4.0 * double(n), s);
   if (n <= 512) return launch_inline<512>(dst, ldd, rows, cols, A, lda, B, ldb, rmap, cmap, s);
   if (n <= 1536) return launch_inline<1536>(dst, ldd, rows, cols, A, lda, B, ldb, rmap, cmap, s);
@@ -609,6 +613,10 @@ void select2d(std::uint8_t* dst, std::int64_t ldd, std::int64_t rows,
               const std::int32_t* cmap, cudaStream_t s) {
   if (rows == 0 || cols == 0) return;
   hprof::Scope hp(hprof::kSelect);
+  static const bool log = std::getenv("GFQ_MAD_LOG") != nullptr;
+  if (log)
+    std::fprintf(stderr, "select rows=%lld cols=%lld rmap=%d cmap=%d\n", static_cast<long long>(rows),
+                 static_cast<long long>(cols), rmap ? 1 : 0, cmap ? 1 : 0);
   ProfScope ps(kProfSelect,
                2.0 * double(rows) * double(cols) + 4.0 * double((rmap ? rows : 0) + (cmap ? cols : 0)), s);
   const unsigned gy = unsigned(rows < 65535 ? rows : 65535);

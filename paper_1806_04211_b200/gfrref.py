@@ -982,6 +982,14 @@ def profile_take():
     return {"tc": (l[0], o[0], t[0]), "simt": (l[1], o[1], t[1])}
 
 
+def device_memory(reset_peak: bool = False) -> dict:
+    """The library's device bytes: live, high-water since the last reset,
+    and the stream-ordered pool's reserved high-water."""
+    live, peak, res = ctypes.c_int64(), ctypes.c_int64(), ctypes.c_int64()
+    _check(lib().gfq_device_memory(int(reset_peak), ctypes.byref(live), ctypes.byref(peak), ctypes.byref(res)))
+    return {"live": live.value, "peak": peak.value, "pool_reserved_high": res.value}
+
+
 PROFILE_KINDS = ("k1_tc", "k1_simt", "ech_gf2", "ech_panel", "select")
 
 

@@ -39,6 +39,7 @@ if "--prof" in sys.argv:
         rate = (w / (ms / 1e3) / (1e12 if unit == "TOPS" else 1e9)) if ms > 0 else 0
         print(f"prof {k:10s} launches {l / reps:8.1f}/step  ms {ms / reps:8.2f}/step  {rate:9.1f} {unit}")
     G.profile(False)
+print("device_memory", G.device_memory())
 if "--trace" in sys.argv:
     import csv
     with open(sys.argv[sys.argv.index("--trace") + 1], "w") as fh:
