@@ -60,6 +60,8 @@ struct Scope {
     if (on) add(slot, now() - t0);
   }
 };
+// Name of the task the calling thread executes (developer shape logs).
+extern thread_local const char* t_task_name;
 }  // namespace hprof
 
 inline std::int64_t round_up(std::int64_t v, std::int64_t m) {

@@ -238,6 +238,10 @@ Mat rrf(const BitString& u, const Mat& b, const Mat& c) {
   if (b.cols() != c.cols() && b.rows() != 0 && c.rows() != 0)
     throw std::invalid_argument("rrf: column counts disagree");
   const std::int64_t cols = (b.rows() != 0 || c.rows() == 0) ? b.cols() : c.cols();
+  // one side empty: the riffle is the other input (values are immutable,
+  // so the result may share its storage -- no copy)
+  if (b.rows() == 0 && c.cols() == cols) return c;
+  if (c.rows() == 0 && b.cols() == cols) return b;
   std::vector<std::int32_t> map(u.size());
   std::int32_t bi = 0, ci = 0;
   for (std::size_t l = 0; l < u.size(); ++l) map[l] = u.bits[l] ? -(ci++) - 2 : bi++;
@@ -248,6 +252,7 @@ Mat crz(const Mat& m, const BitString& lambda, std::size_t out_cols) {
   if (lambda.size() != out_cols) throw std::invalid_argument("crz: lambda length must equal out_cols");
   if (std::int64_t(lambda.count_ones()) != m.cols())
     throw std::invalid_argument("crz: ones count must equal input columns");
+  if (std::int64_t(out_cols) == m.cols()) return m;  // no zero column to insert
   std::vector<std::int32_t> map(out_cols);
   std::int32_t src = 0;
   for (std::size_t l = 0; l < out_cols; ++l) map[l] = lambda.bits[l] ? src++ : -1;
@@ -483,10 +488,12 @@ EchResult panel_ech(const FieldSpec& f, const Mat& h) {
 }
 
 // GF(2) blocks the cluster kernel (ech_gf2_cluster) eliminates in one
-// launch: <= 1024 rows, the packed [W | T] row of <= 256 words.
+// launch on its fast path: <= 1024 rows and a packed [W | T] row of <= 96
+// words (its nibble-table update; wider rows take a bit-serial update
+// several times slower than splitting).
 constexpr std::int64_t kGf2ClusterRows = 1024;
 bool gf2_cluster_fits(std::int64_t a, std::int64_t b) {
-  return a <= kGf2ClusterRows && (a + b + 31) / 32 <= 256;
+  return a <= kGf2ClusterRows && (a + b + 31) / 32 <= 96;
 }
 // ech mode 2 (or GFQ_GF2_SPLIT=0) keeps tall GF(2) blocks on the
 // two-level panel path
@@ -583,7 +590,7 @@ EchResult ech(const FieldSpec& f, const Mat& h, std::size_t threshold) {
     // columns) down to it, so a tall 8192^2 ECH is eight cluster ECHs plus
     // K1 combines instead of 256 single-CTA panel steps.
     if (f.p() == 2 && gf2_split_enabled() && !gf2_cluster_fits(alpha, beta)) {
-      if (alpha >= beta || alpha > kGf2ClusterRows) {
+      if (alpha >= beta) {
         const std::int64_t alpha1 = split_of(alpha);
         const EchResult e1 = ech(f, h.row_view(0, alpha1), threshold);
         return combine_horizontal(f, h.row_view(alpha1, alpha - alpha1), e1, alpha1, threshold);

@@ -340,6 +340,7 @@ const dev::ExtTables& FieldSpec::ext_dev() const {
 // ---------------------------------------------------------------- host profile
 namespace hprof {
 const bool on = std::getenv("GFQ_HOSTPROF") != nullptr;
+thread_local const char* t_task_name = "-";
 namespace {
 std::atomic<std::int64_t> g_ns[kSlots];
 std::atomic<std::int64_t> g_cnt[kSlots];

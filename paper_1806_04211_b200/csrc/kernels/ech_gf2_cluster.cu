@@ -486,6 +486,9 @@ __global__ void __launch_bounds__(kThreads, 1) ech_gf2_cluster_kernel(ClArgs g) 
     cluster.sync();  // X: panel k done everywhere, panel k+1's pivots published
     stamp(k, 6);
     rtot += r2;
+    // every row pivotal: the remaining panels can hold no pivot and their
+    // updates are empty (rtot is the same in every CTA)
+    if (rtot >= rows) break;
   }
 
   if (g.dbg && cr == 0 && tid == 0) g.dbg[8 * 16 + 0] = gtime();
