@@ -2,9 +2,10 @@
 """Benchmark: RREF + transformation over GF(q) (arXiv 1806.04211 Chief) on B200.
 
 One step = one full ``echelonize`` (ChopMatrix -> Steps 1-3 -> EchelonOutput,
-with transformation) of the BASELINE.json configs[1] workload:
-GF(2) dense 8192 x 8192, iid uniform entries (reference random_matrix,
-seed 1, generated on the device by K6), block 1024.
+with transformation) of the largest BASELINE.json configuration that fits one
+GPU: configs[4]'s 1-GPU case, GF(2) 65536 x 65536, iid uniform entries
+(reference random_matrix, seed 1, generated on the device by K6), block 8192
+(an 8 x 8 block grid).  ``--config`` selects the other configs.
 Metric: effective GF(q) mult-adds/s = m*n*r / step time.
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
@@ -30,7 +31,7 @@ sys.path.insert(0, ROOT)
 
 from paper_1806_04211_b200.workloads import CONFIGS  # noqa: E402
 
-DEFAULT = "cfg2a"
+DEFAULT = "cfg5s"
 METRIC = "RREF+transform effective GF(q) mult-adds/s (m*n*r / wall)"
 UNIT = "mult-adds/s"
 
@@ -107,48 +108,54 @@ def setup_dist():
     return world, rank, local, dist
 
 
-def cpu_baseline(cfg, C_host, rank_r, budget_s=25.0):
+def ref_sample(cfg):
+    """The reference's CPU sample of a workload: the leading s x s submatrix
+    with the config's block GRID kept (block = s / grid), so the reference
+    runs the same Chief task DAG as the full job, scaled.  s = the full size
+    when it is at most 8192 (cfg1 / cfg2a: the exact config), else 8192:
+    at cfg5s's own block (8192) any sample that bounded is ONE block, which
+    the reference would eliminate in a single task on one thread."""
+    grid = max(1, cfg["m"] // cfg["block"])
+    side = min(cfg["m"], cfg["n"])
+    if side <= 8192:
+        s = side
+        blk = cfg["block"]
+    else:
+        s = 8192 // grid * grid
+        blk = s // grid
+    same = s == cfg["m"] and s == cfg["n"] and blk == cfg["block"]
+    label = (f"full {cfg['m']}x{cfg['n']} input, block {blk}" if same else
+             f"leading {s}x{s} of the {cfg['m']}x{cfg['n']} input, block {blk} (the config's "
+             f"{grid}x{grid} block grid, scaled: the full job does not fit host RAM / minutes)")
+    return s, blk, same, label
+
+
+def cpu_baseline(cfg, C):
     """The reference library (oracle/_ref, compiled from /root/reference) on
-    the host cores, on a bounded sample of the workload: the leading
-    s x s submatrix (s a multiple of the block) sized so one call takes about
-    `budget_s` seconds with all host threads."""
+    the host cores, all threads, once, on ref_sample's bounded sample."""
     import oracle
     if oracle.ref is None:
         return None
     threads = max(1, oracle.ref.ref_hardware_concurrency())
-    blk = cfg["block"]
-    # calibrate on one block-grid 2x2 leading sample
-    s0 = min(2 * blk, cfg["m"], cfg["n"])
-    t0 = time.time()
-    o = oracle.ref_echelonize(cfg["p"], C_host[:s0, :s0].copy(), blk, threads=threads)
-    dt = max(time.time() - t0, 1e-3)
-    rate = s0 * s0 * o.rank / dt
-    # grid-level parallelism grows with the sample; be conservative (rate x2)
-    s = s0
-    while True:
-        nxt = s + blk
-        if nxt > min(cfg["m"], cfg["n"]):
-            break
-        if nxt ** 3 / (2 * rate) > budget_s:
-            break
-        s = nxt
-    sample = C_host[:s, :s].copy()
+    s, blk, same, label = ref_sample(cfg)
+    if cfg["kind"] == "random":   # the leading rows of the same row-major draw stream
+        sample = oracle.random_matrix(cfg["p"], s, cfg["n"], cfg["seed"])[:, :s].copy()
+    else:
+        sample = C.numpy()[:s, :s].copy()
     t0 = time.time()
     o = oracle.ref_echelonize(cfg["p"], sample, blk, threads=threads)
     wall = time.time() - t0
     work = s * s * o.rank
     return {"value": work / wall, "unit": UNIT, "cores": threads, "kind": "reference",
-            "sample": f"leading {s}x{s} of the {cfg['m']}x{cfg['n']} input, block {blk}, "
-                      f"gfrref::echelonize with_transform, {threads} threads, 1 call, {wall:.2f} s",
-            "wall_s": wall}
+            "sample": f"{label}; gfrref::echelonize with_transform, {threads} threads, 1 call, {wall:.2f} s",
+            "same_config": same, "wall_s": wall}
 
 
 def run_reference(args, cfg, world, rank):
     """--impl reference: the reference's own CPU implementation (oracle/_ref)
-    with all host threads; each step a bounded sample of the workload."""
+    with all host threads; each step one call on ref_sample's sample."""
     if rank != 0:
         return
-    import numpy as np  # noqa: F401
     import oracle
     if oracle.ref is None:
         print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/libgfrref_ref.so not built"}))
@@ -157,16 +164,11 @@ def run_reference(args, cfg, world, rank):
     if cfg["kind"] != "random":
         print(json.dumps({"impl": "reference", "unavailable": "reference arm wired for the random workloads only"}))
         return
-    C = oracle.random_matrix(cfg["p"], cfg["m"], cfg["n"], cfg["seed"])
-    blk = cfg["block"]
-    budget = 150.0 / max(1, args.steps + args.warmup)
-    s0 = min(2 * blk, cfg["m"], cfg["n"])
-    t0 = time.time()
-    o = oracle.ref_echelonize(cfg["p"], C[:s0, :s0].copy(), blk, threads=threads)
-    rate = s0 * s0 * o.rank / max(time.time() - t0, 1e-3)
-    s = s0
-    while s + blk <= min(cfg["m"], cfg["n"]) and (s + blk) ** 3 / (2 * rate) <= budget:
-        s += blk
+    s, blk, same, label = ref_sample(cfg)
+    # the leading s x s of random_matrix(m, n) (row-major draws): rows of the
+    # full stream, generated by the reference itself only where they fit
+    C = oracle.random_matrix(cfg["p"], s, cfg["n"], cfg["seed"]) if s < cfg["m"] else \
+        oracle.random_matrix(cfg["p"], cfg["m"], cfg["n"], cfg["seed"])
     sample = C[:s, :s].copy()
     for _ in range(args.warmup):
         oracle.ref_echelonize(cfg["p"], sample, blk, threads=threads)
@@ -182,33 +184,44 @@ def run_reference(args, cfg, world, rank):
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * tot / args.steps,
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "u32 (reference Elem)",
             "data": "synthetic: reference random_matrix seed 1 (host)",
-            "config": {"workload": cfg["desc"], "p": cfg["p"], "m": cfg["m"], "n": cfg["n"], "block": blk,
-                       "sample": f"leading {s}x{s}"},
+            "config": {"workload": cfg["desc"], "p": cfg["p"], "m": cfg["m"], "n": cfg["n"], "block": cfg["block"],
+                       "sample": label, "sample_block": blk, "same_config": same},
             "cpu_baseline": {"value": val, "unit": UNIT, "cores": threads, "kind": "reference",
-                             "sample": f"leading {s}x{s} of the {cfg['m']}x{cfg['n']} input per step, block {blk}"},
+                             "sample": f"{label}, per step"},
             "e2e": {"value": val, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line))
 
 
-def k1_traffic():
-    """Per-launch DRAM bytes of K1 from the committed ncu --set full summary."""
+def load_traffic(config):
+    """Per-family DRAM traffic of one launch of the config's dominant shape
+    (ncu --set full, dram__bytes_read.sum + dram__bytes_write.sum), from
+    profiles/r02_traffic.json; {} when not captured."""
     try:
-        with open(os.path.join(ROOT, "profiles", "k1_ncu_summary.json")) as f:
-            return json.load(f).get("dram_bytes_per_launch")
+        with open(os.path.join(ROOT, "profiles", "r02_traffic.json")) as f:
+            return json.load(f).get(config, {})
     except Exception:
-        return None
+        return {}
 
 
-def k1_isolated(G, p, peak):
-    """K1 alone on a quiet device: CUDA events around 20 back-to-back
-    launches (after 3 warm-ups) through gfq_mad_raw on the current stream,
-    tcgen05 path forced; shapes: the cfg2a block product (1024^3) and the
-    cfg4 block product (4096^3)."""
+def dominant_shape(config):
+    """The K1 shape with the most work in one step of the config (GFQ_MAD_LOG)."""
+    return {"cfg5s": (8192, 65536, 8192), "cfg4": (4096, 32768, 4096), "cfg3": (2048, 12288, 2048),
+            "cfg2a": (1024, 8192, 1024), "cfg2b": (1024, 8192, 1024), "cfg1": (500, 2000, 500)}.get(config)
+
+
+def k1_isolated(G, p, peak, dominant=None):
+    """K1 alone on a quiet device: CUDA events around back-to-back launches
+    (after 3 warm-ups) through gfq_mad_raw on the current stream, tcgen05
+    path forced; shapes: the 1024^3 block product and the step's dominant
+    shape."""
     import torch
     out = []
+    shapes = [(1024, 1024, 1024)]
+    if dominant and dominant not in shapes:
+        shapes.append(dominant)
     G.set_mad_policy(2)
     try:
-        for (m, n, k) in [(1024, 1024, 1024), (4096, 4096, 4096)]:
+        for (m, n, k) in shapes:
             A = torch.randint(0, p, (m, k), dtype=torch.uint8, device="cuda")
             Bm = torch.randint(0, p, (k, n), dtype=torch.uint8, device="cuda")
             D = torch.zeros((m, n), dtype=torch.uint8, device="cuda")
@@ -218,15 +231,17 @@ def k1_isolated(G, p, peak):
             for _ in range(3):
                 call()
             torch.cuda.synchronize()
+            reps = 20 if m * n * k < 1 << 34 else 5
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             e0.record()
-            for _ in range(20):
+            for _ in range(reps):
                 call()
             e1.record()
             e1.synchronize()
-            us = 1e3 * e0.elapsed_time(e1) / 20
+            us = 1e3 * e0.elapsed_time(e1) / reps
             tops = 2.0 * m * n * k / (us * 1e-6) / 1e12
             out.append({"shape": f"{m}x{n}x{k}", "us": us, "tflops": tops, "frac": tops / peak})
+            del A, Bm, D
     finally:
         G.set_mad_policy(0)
         G.set_stream(0)
@@ -291,6 +306,7 @@ def main():
 
     # ---------------- timed region (device-resident input)
     G.launch_count(reset=True)
+    G.device_memory(reset_peak=True)
     clocks = ClockSampler(local)
     barrier()
     clocks.start()
@@ -309,11 +325,17 @@ def main():
     barrier()
     clk = clocks.stop()
     launches = G.launch_count(reset=True)
+    dm = G.device_memory()
+    hbm = {"high_water_bytes": dm["peak"], "input_bytes": cfg["m"] * cfg["n"],
+           "high_water_over_input": dm["peak"] / (cfg["m"] * cfg["n"]),
+           "pool_reserved_high_bytes": dm["pool_reserved_high"],
+           "note": "the library's device allocations (matrices, panels, scratch) during the timed steps; "
+                   "the input and one step's outputs included"}
     # K1 per-launch device timing: the same steps again with CUDA events
     # around every K1 launch on its worker stream (kept out of the timed
     # region above: the events add host work per launch).
     G.profile(True)
-    G.profile_take()
+    G.profile_take_kinds()
     prof_ms = []
     for _ in range(args.steps):
         flush.fill_(3)
@@ -324,14 +346,14 @@ def main():
         e1.synchronize()
         prof_ms.append(e0.elapsed_time(e1))
         del out
-    prof = G.profile_take()
+    prof = G.profile_take_kinds()
     G.profile(False)
     tot_ms = sum(times)
     if dist:
         t = torch.tensor([tot_ms], device="cuda", dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         tot_ms = float(t.item())
-    # strong scaling: the same cfg2a job sharded over the N GPUs
+    # strong scaling: the same job sharded over the N GPUs
     value = work * args.steps / (tot_ms / 1e3)
 
     # ---------------- e2e: public API with host buffers (H2D + D2H inside)
@@ -373,37 +395,64 @@ def main():
                "path": "gfq_echelonize_host_into (pinned host C -> HBM, every output block -> pinned host as it becomes final)" if comm is None
                else "each rank uploads pinned host C, gfq_echelonize_dist(gather), rank 0 downloads all blocks"}
 
-    # ---------------- roofline of the dominant kernel (K1 tcgen05 contraction)
+    # ---------------- rooflines of the two kernel families with the most device time
     peaks = measured_peaks()
-    tc_l, tc_ops, tc_ms = prof["tc"]
-    si_l, si_ops, si_ms = prof["simt"]
     if peaks and peaks.get("bf16_tflops"):
-        peak = 2.0 * peaks["bf16_tflops"]
-        peak_src = "2 x measured cuBLAS bf16 burst (MEASURED_PEAKS.json); B200 dense int8 = 2 x dense bf16"
+        tpeak = 2.0 * peaks["bf16_tflops"]
+        tpeak_src = "2 x measured cuBLAS bf16 burst (MEASURED_PEAKS.json); B200 dense int8 = 2 x dense bf16"
     else:
-        peak = 2.0 * 1590.0
-        peak_src = "fallback 2 x 1.59 PF bf16 (B200_PROFILING.md)"
-    achieved = (tc_ops / (tc_ms / 1e3) / 1e12) if tc_ms > 0 else 0.0
-    roof = {"kernel": "gf_mad_tc_kernel (K1, tcgen05.mma kind::i8)", "bound": "tensor",
-            "achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak if peak else None,
-            "traffic": k1_traffic(), "peak_source": peak_src,
-            "ops_per_launch": tc_ops / tc_l if tc_l else 0, "launches": tc_l,
-            "avg_launch_us": 1e3 * tc_ms / tc_l if tc_l else 0,
-            "share_of_step": (tc_ms / sum(prof_ms)) if prof_ms else None,
-            "simt_k1": {"launches": si_l, "ops": si_ops, "ms": si_ms},
-            "note": "int8 ops = 2 x MACs; CUDA events around every K1 launch on its worker stream, "
-                    f"over {args.steps} profiled steps run right after the timed region "
-                    f"({sum(prof_ms) / max(1, len(prof_ms)):.2f} ms/step with events); launches on "
-                    "concurrent worker streams overlap, so per-launch times include SM sharing"}
+        tpeak = 2.0 * 1590.0
+        tpeak_src = "fallback 2 x 1.59 PF bf16 (B200_PROFILING.md)"
+    if peaks and peaks.get("hbm_gbs"):
+        hpeak, hpeak_src = peaks["hbm_gbs"], "measured copy bandwidth (MEASURED_PEAKS.json)"
+    else:
+        hpeak, hpeak_src = 7672.0, "fallback (B200_PROFILING.md)"
+    names = {"k1_tc": "gf_mad_tc_kernel (K1, tcgen05.mma kind::i8)",
+             "k1_simt": "mad_smallk / mad_simt (K1 SIMT, K < 32)",
+             "ech_gf2": "ech_gf2_cluster_kernel (K2, GF(2) 8-CTA cluster ECH)",
+             "ech_panel": "ech_step_chain / ech_step_update / ech_panel (K2, general p)",
+             "select": "select2d_v16 / select_rows_v16 / select_inline (K3/K4 gathers, riffles)"}
+    traffic = load_traffic(args.config)
+    step_ms = sum(prof_ms) / max(1, len(prof_ms))
+    roofs = []
+    for fam, (nl, wk, ms) in sorted(prof.items(), key=lambda kv: -kv[1][2]):
+        if nl == 0 or ms <= 0:
+            continue
+        tensor = fam.startswith("k1")
+        ach = wk / (ms / 1e3) / (1e12 if tensor else 1e9)
+        peak = tpeak if tensor else hpeak
+        tr = traffic.get(fam)
+        roofs.append({"kernel": names.get(fam, fam), "family": fam, "bound": "tensor" if tensor else "hbm",
+                      "achieved": ach, "peak": peak, "unit": "TFLOP/s" if tensor else "GB/s",
+                      "frac": ach / peak, "traffic": tr["dram_bytes"] if tr else None,
+                      "traffic_shape": tr["shape"] if tr else None,
+                      "traffic_algorithmic": tr["algorithmic_bytes"] if tr else None,
+                      "peak_source": tpeak_src if tensor else hpeak_src,
+                      "work_per_launch": wk / nl, "work_unit": "int8 ops (2 x MACs)" if tensor else
+                      "algorithmic bytes (u8 payload read + written, +4 B per index)",
+                      "launches_per_step": nl / max(1, args.steps), "avg_launch_us": 1e3 * ms / nl,
+                      "event_ms_per_step": ms / max(1, args.steps),
+                      "share_of_step": ms / max(1, args.steps) / step_ms if step_ms else None})
+        if len(roofs) == 2:
+            break
+    note = ("CUDA events around every launch of the family on its worker stream, over "
+            f"{args.steps} profiled steps run right after the timed region ({step_ms:.2f} ms/step with "
+            "events); launches on concurrent worker streams overlap, so per-launch times include SM "
+            "sharing (share_of_step can exceed 1); traffic = ncu dram__bytes_read+write of one launch "
+            "of the step's dominant shape run alone (profiles/r02_traffic.json)")
+    roof = dict(roofs[0]) if roofs else {}
+    roof["note"] = note
+    roof["second"] = roofs[1] if len(roofs) > 1 else None
+    roof["families"] = {k: {"launches": v[0], "work": v[1], "ms": v[2]} for k, v in prof.items()}
 
     # K1 timed alone (no concurrent streams), CUDA events around back-to-back
-    # launches: the step's dominant shape and the cfg4 block shape
+    # launches: the block product and the step's dominant shape
     if rank == 0:
-        roof["isolated"] = k1_isolated(G, cfg["p"], peak)
+        roof["isolated"] = k1_isolated(G, cfg["p"], tpeak, dominant_shape(args.config))
 
     base = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        base = cpu_baseline(cfg, C.numpy(), rank_r)
+        base = cpu_baseline(cfg, C)
 
     if rank == 0:
         line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
@@ -419,6 +468,7 @@ def main():
                            if world > 1 else "1 GPU"},
                 "wall_ms_per_step": 1e3 * sum(walls) / len(walls),
                 "roofline": roof, "cpu_baseline": base, "e2e": e2e, "clocks": clk,
+                "hbm": hbm,
                 "gpu_launches": launches}
         print(json.dumps(line))
     if dist:

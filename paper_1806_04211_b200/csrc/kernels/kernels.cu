@@ -356,8 +356,8 @@ void mad(std::uint32_t p, std::int64_t m, std::int64_t n, std::int64_t k,
   // developer log of every contraction's shape and path (GFQ_MAD_LOG)
   static const bool log = std::getenv("GFQ_MAD_LOG") != nullptr;
   if (log)
-    std::fprintf(stderr, "mad m=%lld n=%lld k=%lld path=%s\n", static_cast<long long>(m),
-                 static_cast<long long>(n), static_cast<long long>(k), rec.path ? "simt" : "tc");
+    std::fprintf(stderr, "mad m=%lld n=%lld k=%lld path=%s task=%s\n", static_cast<long long>(m),
+                 static_cast<long long>(n), static_cast<long long>(k), rec.path ? "simt" : "tc", hprof::t_task_name);
 }
 
 // ------------------------------------------------------------------ K3/K4
@@ -466,16 +466,49 @@ __global__ void select2d_v16_kernel(std::uint8_t* dst, std::int64_t ldd,
 #pragma unroll
           for (int q = 0; q < 16; ++q) cm[q] = j0 + q < cols ? cmap[j0 + q] : -1;
         }
+        // fast path: the 16 columns are one contiguous run of one source row
+        // (the common case: crz / RowLengthen insert a few zero columns
+        // into long runs) -- two aligned 16-byte loads and funnel shifts
+        // instead of 16 byte loads
+        bool run = true;
+        const std::int32_t c0 = cm[0];
 #pragma unroll
-        for (int q = 0; q < 16; ++q) {
-          const std::int32_t cv = cm[q];
-          std::uint32_t x = 0;
-          if (cv >= 0) {
-            x = rowB ? brow[cv] : arow[cv];
-          } else if (cv <= -2) {
-            x = brow[-cv - 2];
+        for (int q = 1; q < 16; ++q) run = run && (c0 >= 0 ? cm[q] == c0 + q : (c0 <= -2 && cm[q] == c0 - q));
+        const std::uint8_t* srow = c0 >= 0 ? (rowB ? brow : arow) : brow;
+        const std::int64_t sc = c0 >= 0 ? c0 : std::int64_t(-c0 - 2);
+        const std::int64_t sld = (c0 >= 0 && !rowB) ? lda : ldb;
+        if (run && srow && ((reinterpret_cast<std::uintptr_t>(srow) | std::uintptr_t(sld)) & 15) == 0 &&
+            (sc & ~std::int64_t(15)) + 32 <= sld) {
+          const uint4* p16 = reinterpret_cast<const uint4*>(srow + (sc & ~std::int64_t(15)));
+          const uint4 lo = p16[0];
+          const int sh = int(sc & 15);
+          if (sh == 0) {
+            w[0] = lo.x; w[1] = lo.y; w[2] = lo.z; w[3] = lo.w;
+          } else {
+            const uint4 hi = p16[1];
+            std::uint32_t u[8] = {lo.x, lo.y, lo.z, lo.w, hi.x, hi.y, hi.z, hi.w};
+            const int wq = sh >> 2, bs = 8 * (sh & 3);
+            // word shift by wq in two register-resident stages (no dynamic
+            // indexing, which would spill the array to local memory)
+#pragma unroll
+            for (int q = 0; q < 6; ++q) u[q] = (wq & 2) ? u[q + 2] : u[q];
+#pragma unroll
+            for (int q = 0; q < 5; ++q) u[q] = (wq & 1) ? u[q + 1] : u[q];
+#pragma unroll
+            for (int q = 0; q < 4; ++q) w[q] = bs ? __funnelshift_r(u[q], u[q + 1], bs) : u[q];
           }
-          w[q >> 2] |= x << (8 * (q & 3));
+        } else {
+#pragma unroll
+          for (int q = 0; q < 16; ++q) {
+            const std::int32_t cv = cm[q];
+            std::uint32_t x = 0;
+            if (cv >= 0) {
+              x = rowB ? brow[cv] : arow[cv];
+            } else if (cv <= -2) {
+              x = brow[-cv - 2];
+            }
+            w[q >> 2] |= x << (8 * (q & 3));
+          }
         }
       }
       if (j0 + 16 <= cols) {
@@ -599,8 +632,8 @@ bool select2d_inline(std::uint8_t* dst, std::int64_t ldd, std::int64_t rows, std
   hprof::Scope hp(hprof::kSelect);
   static const bool log = std::getenv("GFQ_MAD_LOG") != nullptr;
   if (log)
-    std::fprintf(stderr, "select rows=%lld cols=%lld rmap=%d cmap=%d inline\n", static_cast<long long>(rows),
-                 static_cast<long long>(cols), rmap ? 1 : 0, cmap ? 1 : 0);
+    std::fprintf(stderr, "select rows=%lld cols=%lld rmap=%d cmap=%d task=%s inline\n", static_cast<long long>(rows),
+                 static_cast<long long>(cols), rmap ? 1 : 0, cmap ? 1 : 0, hprof::t_task_name);
   ProfScope ps(kProfSelect, 2.0 * double(rows) * double(cols) + 4.0 * double(n), s);
   if (n <= 512) return launch_inline<512>(dst, ldd, rows, cols, A, lda, B, ldb, rmap, cmap, s);
   if (n <= 1536) return launch_inline<1536>(dst, ldd, rows, cols, A, lda, B, ldb, rmap, cmap, s);
@@ -615,8 +648,8 @@ void select2d(std::uint8_t* dst, std::int64_t ldd, std::int64_t rows,
   hprof::Scope hp(hprof::kSelect);
   static const bool log = std::getenv("GFQ_MAD_LOG") != nullptr;
   if (log)
-    std::fprintf(stderr, "select rows=%lld cols=%lld rmap=%d cmap=%d\n", static_cast<long long>(rows),
-                 static_cast<long long>(cols), rmap ? 1 : 0, cmap ? 1 : 0);
+    std::fprintf(stderr, "select rows=%lld cols=%lld rmap=%d cmap=%d task=%s\n", static_cast<long long>(rows),
+                 static_cast<long long>(cols), rmap ? 1 : 0, cmap ? 1 : 0, hprof::t_task_name);
   ProfScope ps(kProfSelect,
                2.0 * double(rows) * double(cols) + 4.0 * double((rmap ? rows : 0) + (cmap ? cols : 0)), s);
   const unsigned gy = unsigned(rows < 65535 ? rows : 65535);

@@ -162,6 +162,26 @@ def test_index_jobs_pinned(G, pinned):
     assert rho == G.IndexSet(3, (0, 2)) and list(u) == [1, 1]
 
 
+@pytest.mark.parametrize("zeros", [0, 1, 7, 300])
+def test_crz_long_runs(G, zeros):
+    """Column riffles whose map is long contiguous runs (the 16-byte run fast
+    path of the gather, at every source alignment) against the restatement,
+    including the pass-through when nothing is inserted."""
+    rng = np.random.default_rng(zeros)
+    m = rnd(251, 70, 3000, 9)
+    lam = np.ones(3000 + zeros, np.uint8)
+    lam[rng.choice(3000 + zeros, zeros, replace=False)] = 0
+    lam = tuple(int(x) for x in lam)
+    for view in (m, m[:, 5:]):   # the second: source rows not 16B-aligned at column 0
+        view = np.ascontiguousarray(view)
+        k = view.shape[1]
+        lam2 = lam[: k + zeros]
+        if sum(lam2) != k:
+            lam2 = tuple([1] * k + [0] * zeros)
+        got = G.crz(view, lam2, len(lam2))
+        np.testing.assert_array_equal(got.numpy(), R.crz(view, lam2, len(lam2)))
+
+
 # ------------------------------------------------------------------ K2 + recursion (ech)
 @pytest.fixture(params=[0, 1], ids=["panel", "recursive"])
 def mode(G, request):
