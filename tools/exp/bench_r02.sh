@@ -3,7 +3,7 @@
 # ncu --set full of the dominant shapes, launch list of one cfg5s step
 cd $GRAFT_REPO_ROOT
 mkdir -p gpurun_out/r02
-timeout 1200 python -m pytest tests/test_gpu_kernels.py tests/test_gpu_configs.py -q -x -p no:cacheprovider -k "crz or cfg5s or poison or cfg4_vs" 2>&1 | tail -3
+timeout 1200 python -m pytest tests/test_gpu_kernels.py tests/test_gpu_configs.py tests/test_gpu_dropin.py -q -x -p no:cacheprovider -k "crz or cfg5s or poison or cfg4_vs or dropin" 2>&1 | tail -3
 timeout 900 python bench.py > gpurun_out/r02/bench_cfg5s.json 2> gpurun_out/r02/bench_cfg5s.err; echo "bench rc=$?"
 tail -c 3000 gpurun_out/r02/bench_cfg5s.json
 timeout 600 python bench.py --config cfg2a --no-cpu-baseline > gpurun_out/r02/bench_cfg2a.json 2>&1; echo "cfg2a rc=$?"
