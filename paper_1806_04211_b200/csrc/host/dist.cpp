@@ -204,10 +204,18 @@ std::vector<BcastItem> bcast_schedule(const ChopSpec& cs, const PlanHandles&, Ta
                                       const Sharding& sh) {
   std::vector<BcastItem> out;
   const std::size_t a = cs.a(), b = cs.b();
-  for (std::size_t j = 0; j < b; ++j)
-    for (std::size_t i = 0; i < a; ++i)
+  // Step 1 in wavefront order: anti-diagonal i + j (the plan's priority,
+  // src/chief.cpp:116), then column.  PkgA(i, j) depends through broadcasts
+  // only on PkgA(i', j') with i' <= i, j' < j, all on earlier anti-diagonals,
+  // so this is a topological order every rank can issue without deadlock --
+  // and PkgA(0, j+1) no longer waits behind PkgA(a-1, j), which kept the
+  // j-outer order one column pair at a time.
+  for (std::size_t d = 0; d + 1 < a + b; ++d)
+    for (std::size_t j = (d >= a ? d - a + 1 : 0); j <= d && j < b; ++j) {
+      const std::size_t i = d - j;
       out.push_back({g.find_slot({PkgKind::A, std::uint16_t(i), std::uint16_t(j), 0, 0}),
                      sh.owner_col(j), true, i, j, 0});
+    }
   for (std::size_t k = b; k-- > 1;)
     for (std::size_t j = 0; j < k; ++j)
       out.push_back({g.find_slot({PkgKind::X, std::uint16_t(j), std::uint16_t(k), 0, 0}),

@@ -10,10 +10,11 @@
 //   Extend(i,j)                          -> every rank (host-only index merge)
 // The only packages that cross ranks are PkgA(i,j) (root: owner of column
 // j) and X(j,k) (root: owner of column k).  They are broadcast in one fixed
-// global order -- A in Step-1 plan order, then X in Step-3 order -- which is
-// a topological order of the plan (A(i,j) depends only on earlier A's; X
-// only on Step-1 outputs), so every rank can issue the collectives in the
-// same sequence without deadlock.
+// global order -- A by anti-diagonal i + j then column (the Step-1
+// wavefront), then X in Step-3 order -- which is a topological order of the
+// plan (A(i,j) depends only on A(i',j') with i' <= i, j' < j; X only on
+// Step-1 outputs), so every rank can issue the collectives in the same
+// sequence without deadlock.
 #pragma once
 
 #include <cstdint>

@@ -62,22 +62,25 @@ def sharded_run(p, C, block, with_transform, world, rank, owner, sched):
         o = owner[(kind, c0, c1, c2)]
         return o == -1 or o == rank
 
-    for j in range(b):
-        for i in range(a):
-            if mine("ClearDown", i, j, -1):
-                D[(j, i)], A[(i, j)] = R.clear_down(p, Cs[(i, j, j)], D[(j, i - 1)] if i > 0 else R.PkgD(), i)
-            need("A", i, j)
-            E[(i, j)] = R.extend(A[(i, j)], E[(i, j - 1)] if j > 0 else None, j)
-            for k in range(j + 1, b):
-                if mine("UpdateRow", i, j, k):
-                    Cs[(i, k, j + 1)], B[(j, k, i)] = R.update_row(
-                        p, A[(i, j)], Cs[(i, k, j)], B[(j, k, i - 1)] if i > 0 else None, i)
-            if with_transform:
-                for h in range(i + 1):
-                    if mine("UpdateRowTrafo", i, j, h):
-                        K[(i, h, j)], M[(j, h, i - h)] = R.update_row_trafo(
-                            p, A[(i, j)], K[(i, h, j - 1)] if j > 0 else None,
-                            M[(j, h, i - 1 - h)] if h < i else None, E[(h, j)], i, h, j)
+    # Step 1 in the schedule's PkgA order (the wavefront: i + j, then j) --
+    # a valid sequential order of the plan, and the order the broadcasts need
+    a_order = [(it[1], it[2]) for it in sched if it[0]]
+    assert sorted(a_order) == [(i, j) for i in range(a) for j in range(b)]
+    for (i, j) in a_order:
+        if mine("ClearDown", i, j, -1):
+            D[(j, i)], A[(i, j)] = R.clear_down(p, Cs[(i, j, j)], D[(j, i - 1)] if i > 0 else R.PkgD(), i)
+        need("A", i, j)
+        E[(i, j)] = R.extend(A[(i, j)], E[(i, j - 1)] if j > 0 else None, j)
+        for k in range(j + 1, b):
+            if mine("UpdateRow", i, j, k):
+                Cs[(i, k, j + 1)], B[(j, k, i)] = R.update_row(
+                    p, A[(i, j)], Cs[(i, k, j)], B[(j, k, i - 1)] if i > 0 else None, i)
+        if with_transform:
+            for h in range(i + 1):
+                if mine("UpdateRowTrafo", i, j, h):
+                    K[(i, h, j)], M[(j, h, i - h)] = R.update_row_trafo(
+                        p, A[(i, j)], K[(i, h, j - 1)] if j > 0 else None,
+                        M[(j, h, i - 1 - h)] if h < i else None, E[(h, j)], i, h, j)
     if with_transform:
         for j in range(b):
             for h in range(a):
@@ -108,6 +111,21 @@ def sharded_run(p, C, block, with_transform, world, rank, owner, sched):
         out["TM"] = {(j, h): M[(j, h, a - h + (b - 1 - j))] for j in range(b) for h in range(a) if h % world == rank}
         out["TK"] = {(i, h): K[(i, h, b - 1)] for i in range(a) for h in range(i + 1) if h % world == rank}
     return out
+
+
+def test_broadcast_order_is_wavefront():
+    """PkgA broadcasts follow the Step-1 wavefront (anti-diagonal i + j, then
+    j) and precede every X broadcast; X in Step-3 order (k descending)."""
+    import sys
+    sys.path.insert(0, ROOT)
+    from paper_1806_04211_b200 import gfrref as G
+    _, sched = G.dist_plan(40, 48, 8, True, 4)
+    a_items = [(it[1], it[2]) for it in sched if it[0]]
+    assert a_items == sorted(a_items, key=lambda ij: (ij[0] + ij[1], ij[1]))
+    first_x = next(q for q, it in enumerate(sched) if not it[0])
+    assert all(it[0] for it in sched[:first_x]) and not any(it[0] for it in sched[first_x:])
+    ks = [it[3] for it in sched[first_x:]]
+    assert ks == sorted(ks, reverse=True)
 
 
 def _worker(rank, world, port, case, q):
@@ -158,6 +176,8 @@ def _worker(rank, world, port, case, q):
     ((5, 18, 21, 4, True, "product"), 2),
     ((7, 15, 15, 4, False, "random"), 2),
     ((3, 16, 16, 3, True, "product"), 3),
+    ((2, 24, 20, 4, True, "random"), 4),
+    ((3, 22, 26, 5, True, "product"), 4),
 ])
 def test_sharded_chief_gloo(case, world):
     ctx = mp.get_context("spawn")
