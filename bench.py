@@ -346,7 +346,7 @@ def main():
         e1.synchronize()
         prof_ms.append(e0.elapsed_time(e1))
         del out
-    prof = G.profile_take_kinds()
+    prof = G.profile_take_kinds(with_union=True)
     G.profile(False)
     tot_ms = sum(times)
     if dist:
@@ -415,13 +415,14 @@ def main():
     traffic = load_traffic(args.config)
     step_ms = sum(prof_ms) / max(1, len(prof_ms))
     roofs = []
-    for fam, (nl, wk, ms) in sorted(prof.items(), key=lambda kv: -kv[1][2]):
-        if nl == 0 or ms <= 0:
+    for fam, (nl, wk, ms, ums) in sorted(prof.items(), key=lambda kv: -kv[1][3]):
+        if nl == 0 or ums <= 0:
             continue
         tensor = fam.startswith("k1")
-        ach = wk / (ms / 1e3) / (1e12 if tensor else 1e9)
+        ach = wk / (ums / 1e3) / (1e12 if tensor else 1e9)
         peak = tpeak if tensor else hpeak
         tr = traffic.get(fam)
+        nsteps = max(1, args.steps)
         roofs.append({"kernel": names.get(fam, fam), "family": fam, "bound": "tensor" if tensor else "hbm",
                       "achieved": ach, "peak": peak, "unit": "TFLOP/s" if tensor else "GB/s",
                       "frac": ach / peak, "traffic": tr["dram_bytes"] if tr else None,
@@ -430,20 +431,22 @@ def main():
                       "peak_source": tpeak_src if tensor else hpeak_src,
                       "work_per_launch": wk / nl, "work_unit": "int8 ops (2 x MACs)" if tensor else
                       "algorithmic bytes (u8 payload read + written, +4 B per index)",
-                      "launches_per_step": nl / max(1, args.steps), "avg_launch_us": 1e3 * ms / nl,
-                      "event_ms_per_step": ms / max(1, args.steps),
-                      "share_of_step": ms / max(1, args.steps) / step_ms if step_ms else None})
+                      "launches_per_step": nl / nsteps, "avg_launch_us": 1e3 * ms / nl,
+                      "busy_ms_per_step": ums / nsteps, "event_ms_per_step": ms / nsteps,
+                      "share_of_step": ums / nsteps / step_ms if step_ms else None})
         if len(roofs) == 2:
             break
-    note = ("CUDA events around every launch of the family on its worker stream, over "
-            f"{args.steps} profiled steps run right after the timed region ({step_ms:.2f} ms/step with "
-            "events); launches on concurrent worker streams overlap, so per-launch times include SM "
-            "sharing (share_of_step can exceed 1); traffic = ncu dram__bytes_read+write of one launch "
-            "of the step's dominant shape run alone (profiles/r02_traffic.json)")
+    note = ("achieved = the family's algorithmic work / its busy time: CUDA events around every launch "
+            f"on its worker stream over {args.steps} profiled steps run right after the timed region "
+            f"({step_ms:.2f} ms/step with events), the launch windows merged on one device clock so "
+            "concurrent launches on several streams count once (they still share SMs with the other "
+            "families); event_ms_per_step = the unmerged sum; traffic = ncu dram__bytes_read+write of one "
+            "launch of the step's dominant shape run alone (profiles/r02_traffic.json)")
     roof = dict(roofs[0]) if roofs else {}
     roof["note"] = note
     roof["second"] = roofs[1] if len(roofs) > 1 else None
-    roof["families"] = {k: {"launches": v[0], "work": v[1], "ms": v[2]} for k, v in prof.items()}
+    roof["families"] = {k: {"launches": v[0], "work": v[1], "event_ms": v[2], "busy_ms": v[3]}
+                        for k, v in prof.items()}
 
     # K1 timed alone (no concurrent streams), CUDA events around back-to-back
     # launches: the block product and the step's dominant shape

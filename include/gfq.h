@@ -130,8 +130,10 @@ int gfq_profile_take(int64_t* launches2, double* ops2, double* ms2);
 int gfq_device_memory(int reset_peak, int64_t* live, int64_t* peak, int64_t* pool_reserved);
 /* The same per kernel family (n <= 5): [0] K1 tcgen05, [1] K1 SIMT (work =
  * int8 ops), [2] GF(2) cluster ECH, [3] general-p panel/step ECH, [4]
- * gathers/riffles (work = algorithmic bytes read + written). */
-int gfq_profile_take_kinds(int n, int64_t* launches, double* work, double* ms);
+ * gathers/riffles (work = algorithmic bytes read + written); ms = summed
+ * per-launch event time, union_ms (may be NULL) = the time any launch of
+ * the family was running (concurrent launches counted once). */
+int gfq_profile_take_kinds(int n, int64_t* launches, double* work, double* ms, double* union_ms);
 /* Developer timing of the last K1 tcgen05 launch when the process runs with
  * GFQ_TC_DEBUG set: 148 x 8 globaltimer stamps per CTA (0 start, 1 setup,
  * 2 first stage landed, 3 MMAs issued, 4 accumulator ready, 5 epilogue

@@ -82,7 +82,8 @@ PROTOS = {
     "gfq_launch_count": (I, [I, c_i64p]),
     "gfq_profile": (I, [I]),
     "gfq_device_memory": (I, [I, c_i64p, c_i64p, c_i64p]),
-    "gfq_profile_take_kinds": (I, [I, c_i64p, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_double)]),
+    "gfq_profile_take_kinds": (I, [I, c_i64p, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_double),
+                                   ctypes.POINTER(ctypes.c_double)]),
     "gfq_profile_take": (I, [c_i64p, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_double)]),
     "gfq_mul": (I, [U32, vp, vp, vpp]),
     "gfq_mad": (I, [U32, vp, vp, vp, vpp]),

@@ -340,11 +340,11 @@ int gfq_device_memory(int reset_peak, int64_t* live, int64_t* peak, int64_t* poo
     if (reset_peak) gfq::reset_peak_device_bytes();
   });
 }
-int gfq_profile_take_kinds(int n, int64_t* launches, double* work, double* ms) {
+int gfq_profile_take_kinds(int n, int64_t* launches, double* work, double* ms, double* union_ms) {
   return guard([&] {
     if (n < 0 || (n > 0 && (!launches || !work || !ms)))
       throw std::invalid_argument("gfq_profile_take_kinds: bad buffers");
-    gfq::dev::profile_take_kinds(n, launches, work, ms);
+    gfq::dev::profile_take_kinds(n, launches, work, ms, union_ms);
   });
 }
 int gfq_tc_debug_take(uint64_t* stamps) {

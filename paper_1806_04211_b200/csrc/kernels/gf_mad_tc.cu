@@ -158,12 +158,29 @@ __device__ __forceinline__ std::uint32_t pack_low_bytes(std::uint32_t v0, std::u
   return __byte_perm(lo, hi, 0x5410);
 }
 
+// Tile raster: groups of `gm` M-tiles, M fastest inside a group, then N,
+// then the next group.  The 148 tiles in flight span gm A row-panels and
+// ~148/gm B column-panels, so the group's A slice (gm x 128 x K bytes, kept
+// <= ~32 MB by the host) stays L2-resident while B streams through once per
+// group; a plain M-fastest order over all M re-reads the whole of A every
+// wave once A outgrows L2 (8192 x 65536 x 8192: 7.96 GB of DRAM reads for
+// 1.14 GB of operands, profiles/r02_traffic.json).
+__device__ __forceinline__ void tile_coords(int tile, int num_m, int num_n, int gm, int& mb, int& nb) {
+  const int per_group = gm * num_n;
+  const int g = tile / per_group;
+  const int r = tile - g * per_group;
+  const int m0 = g * gm;
+  const int rows = num_m - m0 < gm ? num_m - m0 : gm;
+  mb = m0 + r % rows;
+  nb = r / rows;
+}
+
 template <int BN>
 __global__ void __launch_bounds__(NUM_THREADS, 1)
 gf_mad_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                  int m, int n, int k, std::uint32_t p, std::uint32_t magic,
                  const std::uint8_t* Cin, std::int64_t ldc, std::uint8_t* D, std::int64_t ldd,
-                 unsigned long long* dbg) {
+                 int gm, unsigned long long* dbg) {
   // PDL: wait for the predecessor grid before any global access; dependents
   // are released only at exit (a waiting 200 KB-smem K1 CTA would hold an SM
   // other streams could use)
@@ -228,7 +245,8 @@ gf_mad_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
       int stage = 0;
       std::uint32_t phase = 0;
       for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
-        const int mb = tile % num_m, nb = tile / num_m;
+        int mb, nb;
+        tile_coords(tile, num_m, num_n, gm, mb, nb);
         for (int kb = 0; kb < num_kb; ++kb) {
           mbar_wait(&empty[stage], phase ^ 1);
           mbar_arrive_expect_tx(&full[stage], G::STAGE_BYTES);
@@ -291,7 +309,8 @@ gf_mad_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
     const bool p2 = p == 2;
     int it = 0;
     for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++it) {
-      const int mb = tile % num_m, nb = tile / num_m;
+      int mb, nb;
+        tile_coords(tile, num_m, num_n, gm, mb, nb);
       const int acc = it & 1;
       const std::uint32_t acc_phase = (it >> 1) & 1;
       const int row = mb * BM + row_in_tile;
@@ -524,6 +543,11 @@ bool mad_tc(std::uint32_t p, std::int64_t m, std::int64_t n, std::int64_t k,
     }
   }
   (void)grid;
+  static const std::int64_t group_mb = [] {
+    const char* e = std::getenv("GFQ_K1_GROUP_MB");
+    const std::int64_t v = e ? std::int64_t(std::atoll(e)) : 32;
+    return v > 0 ? v : std::int64_t(1) << 20;  // <= 0: one group (plain M-fastest raster)
+  }();
   for (const Chunk& c : chunks) {
     const std::int64_t k0 = c.k0, kk = c.kk, m0 = c.m0;
     const CUtensorMap& mA = c.mA;
@@ -532,12 +556,16 @@ bool mad_tc(std::uint32_t p, std::int64_t m, std::int64_t n, std::int64_t k,
     const std::int64_t ldcin = k0 == 0 ? ldc : ldd;
     if (cin) cin += m0 * ldcin;
     std::uint8_t* d = D + m0 * ldd;
+    // raster group: the A slice of gm M-tiles within ~32 MB (GFQ_K1_GROUP_MB)
+    const std::int64_t num_m = (c.mm + BM - 1) / BM;
+    const std::int64_t gm = std::max<std::int64_t>(
+        1, std::min<std::int64_t>(num_m, (group_mb << 20) / (std::int64_t(BM) * std::max<std::int64_t>(kk, 1))));
     if (narrow)
       GFQ_CUDA(launch_pdl(gf_mad_tc_kernel<128>, dim3(c.grid), dim3(NUM_THREADS), Geo<128>::SMEM_BYTES, s,
-          mA, mB, int(c.mm), int(n), int(kk), p, magic, cin, ldcin, d, ldd, tc_debug_buf()));
+          mA, mB, int(c.mm), int(n), int(kk), p, magic, cin, ldcin, d, ldd, int(gm), tc_debug_buf()));
     else
       GFQ_CUDA(launch_pdl(gf_mad_tc_kernel<256>, dim3(c.grid), dim3(NUM_THREADS), Geo<256>::SMEM_BYTES, s,
-          mA, mB, int(c.mm), int(n), int(kk), p, magic, cin, ldcin, d, ldd, tc_debug_buf()));
+          mA, mB, int(c.mm), int(n), int(kk), p, magic, cin, ldcin, d, ldd, int(gm), tc_debug_buf()));
     GFQ_CUDA(cudaGetLastError());
     count_launch();
   }

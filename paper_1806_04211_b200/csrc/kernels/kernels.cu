@@ -260,7 +260,7 @@ ProfScope::~ProfScope() {
   g_prof.push_back(ProfRec{e0_, e1_, work_, kind_});
 }
 
-void profile_take_kinds(int n, std::int64_t* launches, double* work, double* ms) {
+void profile_take_kinds(int n, std::int64_t* launches, double* work, double* ms, double* union_ms) {
   std::vector<ProfRec> recs;
   {
     std::lock_guard<std::mutex> lk(g_prof_mtx);
@@ -270,23 +270,50 @@ void profile_take_kinds(int n, std::int64_t* launches, double* work, double* ms)
     launches[q] = 0;
     work[q] = 0;
     ms[q] = 0;
+    if (union_ms) union_ms[q] = 0;
   }
+  // per family: the launches' [start, end) on a common device clock (the
+  // first record's start), merged -- the time the family was running at
+  // all, so concurrent launches on several streams are not double counted
+  std::vector<std::vector<std::pair<double, double>>> iv(std::size_t(n > 0 ? n : 0));
   for (auto& r : recs) {
-    float t = 0;
+    float t = 0, t0 = 0;
     GFQ_CUDA(cudaEventSynchronize(r.e1));
     GFQ_CUDA(cudaEventElapsedTime(&t, r.e0, r.e1));
     if (r.path < n) {
       launches[r.path] += 1;
       work[r.path] += r.ops;
       ms[r.path] += t;
+      if (union_ms && cudaEventElapsedTime(&t0, recs.front().e0, r.e0) == cudaSuccess)
+        iv[std::size_t(r.path)].emplace_back(double(t0), double(t0) + double(t));
     }
+  }
+  for (auto& r : recs) {
     cudaEventDestroy(r.e0);
     cudaEventDestroy(r.e1);
   }
+  cudaGetLastError();
+  if (union_ms)
+    for (int q = 0; q < n; ++q) {
+      auto& v = iv[std::size_t(q)];
+      std::sort(v.begin(), v.end());
+      double tot = 0, lo = 0, hi = -1e300;
+      for (const auto& [a, b] : v) {
+        if (a > hi) {
+          if (hi > lo) tot += hi - lo;
+          lo = a;
+          hi = b;
+        } else if (b > hi) {
+          hi = b;
+        }
+      }
+      if (hi > lo) tot += hi - lo;
+      union_ms[q] = tot;
+    }
 }
 
 void profile_take(std::int64_t launches[2], double ops[2], double ms[2]) {
-  profile_take_kinds(2, launches, ops, ms);
+  profile_take_kinds(2, launches, ops, ms, nullptr);
 }
 
 void set_mad_policy(int policy) { g_policy = policy; }

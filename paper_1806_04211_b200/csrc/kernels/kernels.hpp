@@ -106,7 +106,7 @@ class ProfScope {
   int kind_ = 0;
   cudaStream_t s_ = nullptr;
 };
-void profile_take_kinds(int n, std::int64_t* launches, double* work, double* ms);
+void profile_take_kinds(int n, std::int64_t* launches, double* work, double* ms, double* union_ms);
 
 // Developer timing of K1 (env GFQ_TC_DEBUG): per-CTA globaltimer stamps of
 // the last launch, 148 x 8 u64 (0 start, 1 setup done, 2 first stage

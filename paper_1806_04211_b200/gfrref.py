@@ -993,14 +993,18 @@ def device_memory(reset_peak: bool = False) -> dict:
 PROFILE_KINDS = ("k1_tc", "k1_simt", "ech_gf2", "ech_panel", "select")
 
 
-def profile_take_kinds():
-    """Per kernel family since the last take: {name: (launches, work, ms)};
+def profile_take_kinds(with_union: bool = False):
+    """Per kernel family since the last take: {name: (launches, work, ms)}
+    (+ union_ms, the time any launch of the family ran, with_union);
     work = int8 ops for k1_*, algorithmic bytes for the others."""
     n = len(PROFILE_KINDS)
     l = (ctypes.c_int64 * n)()
     w = (ctypes.c_double * n)()
     t = (ctypes.c_double * n)()
-    _check(lib().gfq_profile_take_kinds(n, l, w, t))
+    u = (ctypes.c_double * n)()
+    _check(lib().gfq_profile_take_kinds(n, l, w, t, u))
+    if with_union:
+        return {name: (l[q], w[q], t[q], u[q]) for q, name in enumerate(PROFILE_KINDS)}
     return {name: (l[q], w[q], t[q]) for q, name in enumerate(PROFILE_KINDS)}
 
 

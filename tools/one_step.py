@@ -34,10 +34,11 @@ for _ in range(reps):
     walls.append(1e3 * (time.time() - t0))
 print("rank", out.rank, "wall_ms", " ".join(f"{w:.2f}" for w in walls), "min", f"{min(walls):.2f}")
 if "--prof" in sys.argv:
-    for k, (l, w, ms) in G.profile_take_kinds().items():
+    for k, (l, w, ms, ums) in G.profile_take_kinds(with_union=True).items():
         unit = "TOPS" if k.startswith("k1") else "GB/s"
-        rate = (w / (ms / 1e3) / (1e12 if unit == "TOPS" else 1e9)) if ms > 0 else 0
-        print(f"prof {k:10s} launches {l / reps:8.1f}/step  ms {ms / reps:8.2f}/step  {rate:9.1f} {unit}")
+        rate = (w / (ums / 1e3) / (1e12 if unit == "TOPS" else 1e9)) if ums > 0 else 0
+        print(f"prof {k:10s} launches {l / reps:8.1f}/step  event ms {ms / reps:8.2f}/step  busy ms "
+              f"{ums / reps:8.2f}/step  {rate:9.1f} {unit} (work / busy)")
     G.profile(False)
 print("device_memory", G.device_memory())
 if "--trace" in sys.argv:
