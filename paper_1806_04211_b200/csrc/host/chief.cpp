@@ -703,7 +703,9 @@ EchelonOutput echelonize_impl(const Mat& C, const FieldSpec& field, const Echelo
   // scratch) in one pool growth step, not hundreds of cache misses
   {
     const std::size_t m = std::size_t(C.rows()), n = std::size_t(C.cols());
-    reserve_pool(2 * m * n + (options.with_transform ? 2 * m * m : 0));
+    // measured high-water: ~6.8x the input at cfg5s (input, T, panels in
+    // flight, ECH scratch)
+    reserve_pool(4 * m * n + (options.with_transform ? 4 * m * m : 0));
   }
   TaskGraph graph;
   graph.ech_threshold = options.ech_threshold;

@@ -18,11 +18,75 @@ const std::int32_t* dptr(const std::shared_ptr<DevBuf>& b) {
   return b ? reinterpret_cast<const std::int32_t*>(b->ptr) : nullptr;
 }
 
+// A select whose one map is a handful of runs (consecutive source rows or
+// columns of one operand, or zeros) is a few strided copies: they go to the
+// copy engines (cudaMemcpy2DAsync / cudaMemset2DAsync), which move the bytes
+// without taking SM time from the contractions running beside them.  The
+// large gathers of the plan are of this kind: a riffle inserting one row
+// (3 runs), a row split with one row missing (2 runs), a widening by a new
+// zero part (a few runs).  GFQ_NO_DMA_SELECT=1 keeps them on the kernels.
+struct Run {
+  std::int64_t t, len, src;  // output start, length, source start
+  int from;                  // 0: A, 1: B, -1: zeros
+};
+bool runs_of(const std::vector<std::int32_t>& map, std::vector<Run>& out, std::size_t cap) {
+  out.clear();
+  for (std::size_t t = 0; t < map.size();) {
+    const std::int32_t v = map[t];
+    const int from = v >= 0 ? 0 : (v == -1 ? -1 : 1);
+    const std::int64_t src = v >= 0 ? v : (v == -1 ? 0 : -std::int64_t(v) - 2);
+    std::size_t e = t + 1;
+    while (e < map.size()) {
+      const std::int32_t w = map[e];
+      const std::int64_t d = std::int64_t(e - t);
+      const bool cont = from == 0 ? w == v + d : (from == -1 ? w == -1 : w == v - d);
+      if (!cont) break;
+      ++e;
+    }
+    out.push_back(Run{std::int64_t(t), std::int64_t(e - t), src, from});
+    if (out.size() > cap) return false;
+    t = e;
+  }
+  return true;
+}
+bool select_dma(const Mat& out, const Mat& A, const Mat* B, const std::vector<std::int32_t>* rmap,
+                const std::vector<std::int32_t>* cmap) {
+  static const bool off = std::getenv("GFQ_NO_DMA_SELECT") != nullptr;
+  constexpr std::size_t kMaxRuns = 8;
+  const std::int64_t rows = out.rows(), cols = out.cols();
+  if (off || (rmap && cmap) || rows * cols < (std::int64_t(8) << 20)) return false;
+  std::vector<Run> runs;
+  if (!rmap && !cmap) runs.push_back(Run{0, cols, 0, 0});
+  else if (!runs_of(rmap ? *rmap : *cmap, runs, kMaxRuns)) return false;
+  const cudaStream_t s = cur_stream();
+  dev::ProfScope ps(dev::kProfSelect, 2.0 * double(rows) * double(cols), s);
+  for (const Run& r : runs) {
+    const Mat* S = r.from == 1 ? B : &A;
+    if (rmap) {
+      std::uint8_t* d = out.data() + r.t * out.ld();
+      if (r.from < 0)
+        GFQ_CUDA(cudaMemset2DAsync(d, std::size_t(out.ld()), 0, std::size_t(cols), std::size_t(r.len), s));
+      else
+        GFQ_CUDA(cudaMemcpy2DAsync(d, std::size_t(out.ld()), S->data() + r.src * S->ld(), std::size_t(S->ld()),
+                                   std::size_t(cols), std::size_t(r.len), cudaMemcpyDeviceToDevice, s));
+    } else {
+      std::uint8_t* d = out.data() + r.t;
+      if (r.from < 0)
+        GFQ_CUDA(cudaMemset2DAsync(d, std::size_t(out.ld()), 0, std::size_t(r.len), std::size_t(rows), s));
+      else
+        GFQ_CUDA(cudaMemcpy2DAsync(d, std::size_t(out.ld()), S->data() + r.src, std::size_t(S->ld()),
+                                   std::size_t(r.len), std::size_t(rows), cudaMemcpyDeviceToDevice, s));
+    }
+  }
+  return true;
+}
+
 // out = select(A | B) by optional row/column maps (kernels.hpp select2d).
 Mat select(std::int64_t rows, std::int64_t cols, const Mat& A, const Mat* B,
            const std::vector<std::int32_t>* rmap, const std::vector<std::int32_t>* cmap) {
   Mat out(rows, cols);
   if (out.empty()) return out;
+  if (select_dma(out, A, B, rmap, cmap)) return out;
   // small maps ride in the launch parameters (no upload call)
   static const bool inline_maps = std::getenv("GFQ_NO_INLINE_MAPS") == nullptr;
   if (inline_maps &&

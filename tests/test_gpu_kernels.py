@@ -182,6 +182,30 @@ def test_crz_long_runs(G, zeros):
         np.testing.assert_array_equal(got.numpy(), R.crz(view, lam2, len(lam2)))
 
 
+def test_dma_selects_few_runs(G):
+    """Large selects whose map is a few runs go to the copy engines
+    (cudaMemcpy2DAsync / cudaMemset2DAsync): riffle inserting rows, a row
+    split with rows missing, a widening by a zero part, two-operand column
+    riffles -- all against the restatement."""
+    rng = np.random.default_rng(3)
+    b = rnd(7, 2300, 4000, 1)     # >= 8 MB outputs take the DMA path
+    c = rnd(7, 2, 4000, 2)
+    u = [0] * 2302
+    u[5] = u[1900] = 1
+    np.testing.assert_array_equal(G.rrf(tuple(u), b, c).numpy(), R.rrf(tuple(u), b, c))
+    rho = G.IndexSet(2300, tuple(x for x in range(2300) if x not in (17, 2299)))
+    sel, rest = G.rex(b, rho)
+    want_sel, want_rest = R.rex(b, R.IndexSet(2300, [x for x in range(2300) if x not in (17, 2299)]))
+    np.testing.assert_array_equal(sel.numpy(), want_sel)
+    np.testing.assert_array_equal(rest.numpy(), want_rest)
+    lam = tuple([1] * 1500 + [0] * 700 + [1] * 2500)
+    np.testing.assert_array_equal(G.crz(b, lam, len(lam)).numpy(), R.crz(b, lam, len(lam)))
+    gam = G.IndexSet(4000, tuple(range(0, 3000)))
+    s2, r2 = G.cex(b, gam)
+    np.testing.assert_array_equal(s2.numpy(), b[:, :3000])
+    np.testing.assert_array_equal(r2.numpy(), b[:, 3000:])
+
+
 # ------------------------------------------------------------------ K2 + recursion (ech)
 @pytest.fixture(params=[0, 1], ids=["panel", "recursive"])
 def mode(G, request):
