@@ -24,7 +24,7 @@ const std::int32_t* dptr(const std::shared_ptr<DevBuf>& b) {
 // without taking SM time from the contractions running beside them.  The
 // large gathers of the plan are of this kind: a riffle inserting one row
 // (3 runs), a row split with one row missing (2 runs), a widening by a new
-// zero part (a few runs).  GFQ_NO_DMA_SELECT=1 keeps them on the kernels.
+// zero part (a few runs).
 struct Run {
   std::int64_t t, len, src;  // output start, length, source start
   int from;                  // 0: A, 1: B, -1: zeros
@@ -51,7 +51,9 @@ bool runs_of(const std::vector<std::int32_t>& map, std::vector<Run>& out, std::s
 }
 bool select_dma(const Mat& out, const Mat& A, const Mat* B, const std::vector<std::int32_t>* rmap,
                 const std::vector<std::int32_t>* cmap) {
-  static const bool off = std::getenv("GFQ_NO_DMA_SELECT") != nullptr;
+  // measured neutral on cfg5s (the copy engines are no faster than the
+  // gather kernels beside K1): opt-in with GFQ_DMA_SELECT=1
+  static const bool off = std::getenv("GFQ_DMA_SELECT") == nullptr;
   constexpr std::size_t kMaxRuns = 8;
   const std::int64_t rows = out.rows(), cols = out.cols();
   if (off || (rmap && cmap) || rows * cols < (std::int64_t(8) << 20)) return false;

@@ -288,6 +288,15 @@ void profile_take_kinds(int n, std::int64_t* launches, double* work, double* ms,
         iv[std::size_t(r.path)].emplace_back(double(t0), double(t0) + double(t));
     }
   }
+  // developer dump of every launch window (GFQ_PROF_DUMP=path): family,
+  // start ms, end ms on the common clock
+  if (const char* path = std::getenv("GFQ_PROF_DUMP")) {
+    if (FILE* fh = std::fopen(path, "a")) {
+      for (int q = 0; q < n; ++q)
+        for (const auto& [a, b] : iv[std::size_t(q)]) std::fprintf(fh, "%d %.4f %.4f\n", q, a, b);
+      std::fclose(fh);
+    }
+  }
   for (auto& r : recs) {
     cudaEventDestroy(r.e0);
     cudaEventDestroy(r.e1);
