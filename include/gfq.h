@@ -101,6 +101,10 @@ int gfq_field_op(uint32_t code, int op, uint32_t a, uint32_t b, uint32_t* out);
 int gfq_default_modulus(uint32_t p, uint32_t k, uint32_t* modulus);
 int gfq_random_product_matrix(uint32_t p, int64_t rows, int64_t cols, int64_t inner,
                               uint64_t seed, gfq_mat** out);
+/* Reserve the stream-ordered device pool for an m x n echelonize (every
+ * echelonize does this itself; calling it once up front keeps the one-time
+ * mapping of physical memory out of the first call). */
+int gfq_reserve_for(int64_t m, int64_t n, int with_transform);
 /* Developer check (no reference counterpart): bit 0 fills every device
  * allocation with 0xA5, bit 1 every freed block with 0x5A, each on its
  * stream, so reads of never-written or released memory change results. */

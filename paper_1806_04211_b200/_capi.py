@@ -79,6 +79,7 @@ PROTOS = {
     "gfq_default_modulus": (I, [U32, U32, ctypes.c_void_p]),
     "gfq_set_ech_mode": (I, [I]),
     "gfq_set_poison": (I, [I]),
+    "gfq_reserve_for": (I, [I64, I64, I]),
     "gfq_launch_count": (I, [I, c_i64p]),
     "gfq_profile": (I, [I]),
     "gfq_device_memory": (I, [I, c_i64p, c_i64p, c_i64p]),

@@ -303,6 +303,12 @@ int gfq_random_product_matrix(uint32_t p, int64_t rows, int64_t cols, int64_t in
   });
 }
 
+int gfq_reserve_for(int64_t m, int64_t n, int with_transform) {
+  return guard([&] {
+    if (m < 0 || n < 0) throw std::invalid_argument("gfq_reserve_for: negative shape");
+    gfq::reserve_for(std::size_t(m), std::size_t(n), with_transform != 0);
+  });
+}
 int gfq_set_poison(int mode) {
   return guard([&] {
     if (mode < 0 || mode > 3) throw std::invalid_argument("poison mode must be 0..3");

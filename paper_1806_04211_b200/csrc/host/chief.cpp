@@ -624,6 +624,15 @@ EchelonOutput echelonize_impl(const Mat& C, const FieldSpec& field, const Echelo
                               const std::vector<std::shared_ptr<EventBox>>* row_ready);
 }  // namespace
 
+void reserve_for(std::size_t m, std::size_t n, bool with_transform) {
+  // live high-water ~6.8x the input at cfg5s (input, T, panels in flight,
+  // ECH scratch); the block cache's size-class lists hold about 2.5x that
+  // in the pool (cfg5s: ~90 GB reserved for a 33 GB live peak): with less
+  // reserved, each new size class maps memory (~0.3-1 ms a miss).  Mapping
+  // is a one-time cost (cfg5s: ~3.5 s), so callers may pay it up front.
+  reserve_pool(10 * m * n + (with_transform ? 10 * m * m : 0));
+}
+
 EchelonOutput echelonize(const Mat& C, const FieldSpec& field, const EchelonizeOptions& options,
                          RunReport* report) {
   return echelonize_impl(C, field, options, report, nullptr);
@@ -701,12 +710,7 @@ EchelonOutput echelonize_impl(const Mat& C, const FieldSpec& field, const Echelo
 
   // the run's working set (input-sized panels, the transformation, ECH
   // scratch) in one pool growth step, not hundreds of cache misses
-  {
-    const std::size_t m = std::size_t(C.rows()), n = std::size_t(C.cols());
-    // measured high-water: ~6.8x the input at cfg5s (input, T, panels in
-    // flight, ECH scratch)
-    reserve_pool(4 * m * n + (options.with_transform ? 4 * m * m : 0));
-  }
+  reserve_for(std::size_t(C.rows()), std::size_t(C.cols()), options.with_transform);
   TaskGraph graph;
   graph.ech_threshold = options.ech_threshold;
   const bool fused = options.fuse && 2 * a + 1 <= std::size_t(TaskNode::kMaxIn);

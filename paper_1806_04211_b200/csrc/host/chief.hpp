@@ -95,6 +95,10 @@ EchelonOutput echelonize_host(const std::uint8_t* host, std::int64_t m, std::int
 /// reference include/gfrref/chief.hpp:88-90.  C is device-resident.
 EchelonOutput echelonize(const Mat& C, const FieldSpec& field, const EchelonizeOptions& options,
                          RunReport* report = nullptr);
+/// Reserve the device pool for an m x n echelonize up front (every call
+/// does it too; doing it once before timing keeps the one-time mapping of
+/// physical memory out of the first step).
+void reserve_for(std::size_t m, std::size_t n, bool with_transform);
 
 /// reference include/gfrref/chief.hpp:100: the m x m transformation,
 /// materialised on the device.

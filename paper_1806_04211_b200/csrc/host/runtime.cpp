@@ -24,6 +24,7 @@ namespace gfq {
 namespace {
 thread_local cudaStream_t t_stream = nullptr;
 std::atomic<std::int64_t> g_live{0}, g_peak{0};
+std::atomic<std::int64_t> g_cached{0};  // bytes parked in the block cache's lists
 std::once_flag g_pool_once;
 
 void init_pool() {
@@ -399,6 +400,7 @@ void* take(std::unordered_map<std::size_t, std::vector<void*>>& lists, std::size
   if (it == lists.end() || it->second.empty()) return nullptr;
   void* p = it->second.back();
   it->second.pop_back();
+  g_cached -= std::int64_t(cls);
   return p;
 }
 }  // namespace
@@ -425,6 +427,9 @@ void reserve_pool(std::size_t bytes) {
   std::uint64_t reserved = 0, used = 0;
   GFQ_CUDA(cudaMemPoolGetAttribute(pool, cudaMemPoolAttrReservedMemCurrent, &reserved));
   GFQ_CUDA(cudaMemPoolGetAttribute(pool, cudaMemPoolAttrUsedMemCurrent, &used));
+  // blocks parked in the cache are "used" to the pool but free to us
+  const std::int64_t parked = g_cached.load();
+  if (parked > 0) used = used > std::uint64_t(parked) ? used - std::uint64_t(parked) : 0;
   if (reserved >= used + bytes) return;
   std::size_t free_b = 0, total_b = 0;
   GFQ_CUDA(cudaMemGetInfo(&free_b, &total_b));
@@ -459,11 +464,20 @@ DevBuf::DevBuf(std::size_t n) : bytes(n) {
   init_pool();
   hprof::Scope hp(hprof::kMalloc);
   const cudaStream_t s = cur_stream_raw();
-  const std::size_t cls = size_class(n);
+  // GFQ_CACHE_MAX_MB = x: blocks of >= x MB bypass the cache and go to the
+  // stream-ordered pool directly.  Measured worse (cfg5s: 2849 pool misses
+  // at ~450 us, cfg4 steps 66 -> 116-228 ms), so off by default: the cache
+  // keeps every size and echelonize reserves the pool up front instead.
+  static const std::size_t large = [] {
+    const char* e = std::getenv("GFQ_CACHE_MAX_MB");
+    return e ? std::size_t(std::atoll(e)) << 20 : ~std::size_t(0);
+  }();
+  const bool big = n >= large;
+  const std::size_t cls = big ? (n + 511) / 512 * 512 : size_class(n);
   BlockCache& c = cache();
   void* p = nullptr;
   static const bool nocache = std::getenv("GFQ_NO_BLOCK_CACHE") != nullptr;
-  if (!nocache) {
+  if (!nocache && !big) {
     std::lock_guard<std::mutex> lk(c.mtx);
     auto it = c.by_stream.find(s);
     if (it != c.by_stream.end()) p = take(it->second, cls);
@@ -482,6 +496,7 @@ DevBuf::DevBuf(std::size_t n) : bytes(n) {
           for (void* q : v) {
             drop.push_back(q);
             c.cls_of.erase(q);
+            g_cached -= std::int64_t(k);
           }
         c.idle.clear();
       }
@@ -489,8 +504,10 @@ DevBuf::DevBuf(std::size_t n) : bytes(n) {
       e = cudaMallocAsync(&p, cls, s);
     }
     GFQ_CUDA(e);
-    std::lock_guard<std::mutex> lk(c.mtx);
-    c.cls_of[p] = cls;
+    if (!big) {
+      std::lock_guard<std::mutex> lk(c.mtx);
+      c.cls_of[p] = cls;
+    }
   }
   ptr = static_cast<std::uint8_t*>(p);
   // Developer check (GFQ_POISON bit 0): fill every allocation with 0xA5 on
@@ -516,7 +533,10 @@ DevBuf::~DevBuf() {
     std::lock_guard<std::mutex> lk(c.mtx);
     auto it = c.cls_of.find(ptr);
     static const bool nocache = std::getenv("GFQ_NO_BLOCK_CACHE") != nullptr;
-    if (it != c.cls_of.end() && !nocache) c.by_stream[cur_stream_raw()][it->second].push_back(ptr);
+    if (it != c.cls_of.end() && !nocache) {
+      c.by_stream[cur_stream_raw()][it->second].push_back(ptr);
+      g_cached += std::int64_t(it->second);
+    }
     else {
       if (it != c.cls_of.end()) c.cls_of.erase(it);
       cudaFreeAsync(ptr, cur_stream_raw());

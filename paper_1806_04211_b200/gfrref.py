@@ -950,6 +950,11 @@ def set_ech_outer(width: int):
     _check(lib().gfq_set_ech_outer(width))
 
 
+def reserve_for(m: int, n: int, with_transform: bool = True):
+    """Reserve the device pool for an m x n echelonize up front (gfq_reserve_for)."""
+    _check(lib().gfq_reserve_for(m, n, int(with_transform)))
+
+
 def set_poison(mode: int):
     """Developer check: bit 0 poisons allocations (0xA5), bit 1 freed blocks (0x5A)."""
     _check(lib().gfq_set_poison(mode))

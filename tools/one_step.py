@@ -17,6 +17,8 @@ cfg = CONFIGS[name]
 G.lib()
 f = G.FieldSpec(cfg["p"])
 C = workloads.build(G, name)
+if "--reserve" in sys.argv:
+    G.reserve_for(cfg["m"], cfg["n"], True)
 G.synchronize()
 if "--warm" in sys.argv:
     G.echelonize(C, f, G.EchelonizeOptions(block=cfg["block"], threads=threads))
