@@ -11,24 +11,6 @@
 
 namespace gfq {
 
-namespace {
-std::atomic<std::size_t> g_ech_base{64};
-
-const std::int32_t* dptr(const std::shared_ptr<DevBuf>& b) {
-  return b ? reinterpret_cast<const std::int32_t*>(b->ptr) : nullptr;
-}
-
-// A select whose one map is a handful of runs (consecutive source rows or
-// columns of one operand, or zeros) is a few strided copies: they go to the
-// copy engines (cudaMemcpy2DAsync / cudaMemset2DAsync), which move the bytes
-// without taking SM time from the contractions running beside them.  The
-// large gathers of the plan are of this kind: a riffle inserting one row
-// (3 runs), a row split with one row missing (2 runs), a widening by a new
-// zero part (a few runs).
-struct Run {
-  std::int64_t t, len, src;  // output start, length, source start
-  int from;                  // 0: A, 1: B, -1: zeros
-};
 bool runs_of(const std::vector<std::int32_t>& map, std::vector<Run>& out, std::size_t cap) {
   out.clear();
   for (std::size_t t = 0; t < map.size();) {
@@ -49,6 +31,20 @@ bool runs_of(const std::vector<std::int32_t>& map, std::vector<Run>& out, std::s
   }
   return true;
 }
+namespace {
+std::atomic<std::size_t> g_ech_base{64};
+
+const std::int32_t* dptr(const std::shared_ptr<DevBuf>& b) {
+  return b ? reinterpret_cast<const std::int32_t*>(b->ptr) : nullptr;
+}
+
+// A select whose one map is a handful of runs (consecutive source rows or
+// columns of one operand, or zeros) is a few strided copies: they go to the
+// copy engines (cudaMemcpy2DAsync / cudaMemset2DAsync), which move the bytes
+// without taking SM time from the contractions running beside them.  The
+// large gathers of the plan are of this kind: a riffle inserting one row
+// (3 runs), a row split with one row missing (2 runs), a widening by a new
+// zero part (a few runs).
 bool select_dma(const Mat& out, const Mat& A, const Mat* B, const std::vector<std::int32_t>* rmap,
                 const std::vector<std::int32_t>* cmap) {
   // measured neutral on cfg5s (the copy engines are no faster than the

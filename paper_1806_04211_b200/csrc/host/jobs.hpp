@@ -66,6 +66,15 @@ std::size_t ech_base();
 /// ECH algorithm: 0 = device panel Gauss-Jordan (default), 1 = the
 /// reference's split/combine recursion down to the K2 base case.  Both give
 /// the same (canonical) outputs.
+/// A gather map as runs: output [t, t+len) from consecutive source indices
+/// src.. of operand `from` (0: A, 1: B; codes v >= 0 / v <= -2 of the
+/// select maps) or zeros (from = -1, code -1).  False when more than `cap`.
+struct Run {
+  std::int64_t t, len, src;
+  int from;
+};
+bool runs_of(const std::vector<std::int32_t>& map, std::vector<Run>& out, std::size_t cap);
+
 void set_ech_mode(int mode);
 /// Outer panel width of the two-level device ECH: -1 = automatic, 0 = one
 /// level, else 32..256 (multiple of 32).  Outputs do not depend on it.

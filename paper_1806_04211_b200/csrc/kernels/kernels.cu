@@ -465,9 +465,14 @@ __global__ void select2d_kernel(std::uint8_t* dst, std::int64_t ldd,
   }
 }
 
-// General select (column map present), 16 output columns per thread: the
-// column map is read as int4 vectors and the 16 gathered bytes leave as one
-// 16-byte store (dst 16B-aligned rows).
+// General select (column map present), 16 output columns per thread and
+// kSelRows rows per block: the 16 column-map entries are read (as int4
+// vectors) and classified once, then reused for every row of the block's
+// row group -- the map costs 64 B of loads per 16 B of payload otherwise.
+// A contiguous run of one source row (crz / RowLengthen: long runs with a
+// few inserted zero columns) takes two aligned 16-byte loads and funnel
+// shifts; anything else 16 byte loads.  16-byte stores (dst rows 16B-aligned).
+constexpr int kSelRows = 8;
 __global__ void select2d_v16_kernel(std::uint8_t* dst, std::int64_t ldd,
                                     std::int64_t rows, std::int64_t cols,
                                     const std::uint8_t* A, std::int64_t lda,
@@ -476,82 +481,86 @@ __global__ void select2d_v16_kernel(std::uint8_t* dst, std::int64_t ldd,
                                     const std::int32_t* cmap) {
   pdl_wait_and_release();
   const std::int64_t nvec = (cols + 15) / 16;
-  for (std::int64_t i = blockIdx.y; i < rows; i += gridDim.y) {
-    std::int32_t rv = -3;  // "no row map"
-    if (rmap) rv = rmap[i];
-    const bool rowB = rmap && rv <= -2;
-    const std::int64_t r = rmap ? (rowB ? -rv - 2 : rv) : i;
-    const std::uint8_t* arow = (rv == -1 || rowB) ? nullptr : A + r * lda;
-    const std::uint8_t* brow = B ? B + (rowB ? r : (rmap ? r : i)) * ldb : nullptr;
-    for (std::int64_t v = blockIdx.x * blockDim.x + threadIdx.x; v < nvec;
-         v += std::int64_t(gridDim.x) * blockDim.x) {
-      const std::int64_t j0 = v * 16;
-      std::uint32_t w[4] = {0, 0, 0, 0};
-      if (rv != -1) {
-        std::int32_t cm[16];
-        if (j0 + 16 <= cols && (reinterpret_cast<std::uintptr_t>(cmap + j0) & 15) == 0) {
+  for (std::int64_t v = blockIdx.x * blockDim.x + threadIdx.x; v < nvec;
+       v += std::int64_t(gridDim.x) * blockDim.x) {
+    const std::int64_t j0 = v * 16;
+    std::int32_t cm[16];
+    if (j0 + 16 <= cols && (reinterpret_cast<std::uintptr_t>(cmap + j0) & 15) == 0) {
 #pragma unroll
-          for (int q = 0; q < 4; ++q) {
-            const int4 c4 = reinterpret_cast<const int4*>(cmap + j0)[q];
-            cm[4 * q] = c4.x;
-            cm[4 * q + 1] = c4.y;
-            cm[4 * q + 2] = c4.z;
-            cm[4 * q + 3] = c4.w;
-          }
-        } else {
-#pragma unroll
-          for (int q = 0; q < 16; ++q) cm[q] = j0 + q < cols ? cmap[j0 + q] : -1;
-        }
-        // fast path: the 16 columns are one contiguous run of one source row
-        // (the common case: crz / RowLengthen insert a few zero columns
-        // into long runs) -- two aligned 16-byte loads and funnel shifts
-        // instead of 16 byte loads
-        bool run = true;
-        const std::int32_t c0 = cm[0];
-#pragma unroll
-        for (int q = 1; q < 16; ++q) run = run && (c0 >= 0 ? cm[q] == c0 + q : (c0 <= -2 && cm[q] == c0 - q));
-        const std::uint8_t* srow = c0 >= 0 ? (rowB ? brow : arow) : brow;
-        const std::int64_t sc = c0 >= 0 ? c0 : std::int64_t(-c0 - 2);
-        const std::int64_t sld = (c0 >= 0 && !rowB) ? lda : ldb;
-        if (run && srow && ((reinterpret_cast<std::uintptr_t>(srow) | std::uintptr_t(sld)) & 15) == 0 &&
-            (sc & ~std::int64_t(15)) + 32 <= sld) {
-          const uint4* p16 = reinterpret_cast<const uint4*>(srow + (sc & ~std::int64_t(15)));
-          const uint4 lo = p16[0];
-          const int sh = int(sc & 15);
-          if (sh == 0) {
-            w[0] = lo.x; w[1] = lo.y; w[2] = lo.z; w[3] = lo.w;
-          } else {
-            const uint4 hi = p16[1];
-            std::uint32_t u[8] = {lo.x, lo.y, lo.z, lo.w, hi.x, hi.y, hi.z, hi.w};
-            const int wq = sh >> 2, bs = 8 * (sh & 3);
-            // word shift by wq in two register-resident stages (no dynamic
-            // indexing, which would spill the array to local memory)
-#pragma unroll
-            for (int q = 0; q < 6; ++q) u[q] = (wq & 2) ? u[q + 2] : u[q];
-#pragma unroll
-            for (int q = 0; q < 5; ++q) u[q] = (wq & 1) ? u[q + 1] : u[q];
-#pragma unroll
-            for (int q = 0; q < 4; ++q) w[q] = bs ? __funnelshift_r(u[q], u[q + 1], bs) : u[q];
-          }
-        } else {
-#pragma unroll
-          for (int q = 0; q < 16; ++q) {
-            const std::int32_t cv = cm[q];
-            std::uint32_t x = 0;
-            if (cv >= 0) {
-              x = rowB ? brow[cv] : arow[cv];
-            } else if (cv <= -2) {
-              x = brow[-cv - 2];
-            }
-            w[q >> 2] |= x << (8 * (q & 3));
-          }
-        }
+      for (int q = 0; q < 4; ++q) {
+        const int4 c4 = reinterpret_cast<const int4*>(cmap + j0)[q];
+        cm[4 * q] = c4.x;
+        cm[4 * q + 1] = c4.y;
+        cm[4 * q + 2] = c4.z;
+        cm[4 * q + 3] = c4.w;
       }
-      if (j0 + 16 <= cols) {
-        *reinterpret_cast<uint4*>(dst + i * ldd + j0) = make_uint4(w[0], w[1], w[2], w[3]);
-      } else {
-        for (std::int64_t c = j0; c < cols; ++c)
-          dst[i * ldd + c] = std::uint8_t((w[(c - j0) >> 2] >> (8 * ((c - j0) & 3))) & 0xFF);
+    } else {
+#pragma unroll
+      for (int q = 0; q < 16; ++q) cm[q] = j0 + q < cols ? cmap[j0 + q] : -1;
+    }
+    const std::int32_t c0 = cm[0];
+    bool run = c0 != -1;
+#pragma unroll
+    for (int q = 1; q < 16; ++q) run = run && (c0 >= 0 ? cm[q] == c0 + q : cm[q] == c0 - q);
+    bool zero = true;
+#pragma unroll
+    for (int q = 0; q < 16; ++q) zero = zero && cm[q] == -1;
+    const bool colB = c0 <= -2;                       // the run's source operand
+    const std::int64_t sc = c0 >= 0 ? c0 : std::int64_t(-c0 - 2);
+    for (std::int64_t i0 = std::int64_t(blockIdx.y) * kSelRows; i0 < rows;
+         i0 += std::int64_t(gridDim.y) * kSelRows) {
+      const std::int64_t i1 = i0 + kSelRows < rows ? i0 + kSelRows : rows;
+      for (std::int64_t i = i0; i < i1; ++i) {
+        std::int32_t rv = -3;  // "no row map"
+        if (rmap) rv = rmap[i];
+        const bool rowB = rmap && rv <= -2;
+        const std::int64_t r = rmap ? (rowB ? -rv - 2 : rv) : i;
+        const std::uint8_t* arow = (rv == -1 || rowB) ? nullptr : A + r * lda;
+        const std::uint8_t* brow = B ? B + (rowB ? r : (rmap ? r : i)) * ldb : nullptr;
+        std::uint32_t w[4] = {0, 0, 0, 0};
+        if (rv != -1 && !zero) {
+          const std::uint8_t* srow = colB ? brow : (rowB ? brow : arow);
+          const std::int64_t sld = (colB || rowB) ? ldb : lda;
+          if (run && srow && ((reinterpret_cast<std::uintptr_t>(srow) | std::uintptr_t(sld)) & 15) == 0 &&
+              (sc & ~std::int64_t(15)) + 32 <= sld) {
+            const uint4* p16 = reinterpret_cast<const uint4*>(srow + (sc & ~std::int64_t(15)));
+            const uint4 lo = p16[0];
+            const int sh = int(sc & 15);
+            if (sh == 0) {
+              w[0] = lo.x; w[1] = lo.y; w[2] = lo.z; w[3] = lo.w;
+            } else {
+              const uint4 hi = p16[1];
+              std::uint32_t u[8] = {lo.x, lo.y, lo.z, lo.w, hi.x, hi.y, hi.z, hi.w};
+              const int wq = sh >> 2, bs = 8 * (sh & 3);
+              // word shift by wq in two register-resident stages (no dynamic
+              // indexing, which would spill the array to local memory)
+#pragma unroll
+              for (int q = 0; q < 6; ++q) u[q] = (wq & 2) ? u[q + 2] : u[q];
+#pragma unroll
+              for (int q = 0; q < 5; ++q) u[q] = (wq & 1) ? u[q + 1] : u[q];
+#pragma unroll
+              for (int q = 0; q < 4; ++q) w[q] = bs ? __funnelshift_r(u[q], u[q + 1], bs) : u[q];
+            }
+          } else {
+#pragma unroll
+            for (int q = 0; q < 16; ++q) {
+              const std::int32_t cv = cm[q];
+              std::uint32_t x = 0;
+              if (cv >= 0) {
+                x = rowB ? brow[cv] : arow[cv];
+              } else if (cv <= -2) {
+                x = brow[-cv - 2];
+              }
+              w[q >> 2] |= x << (8 * (q & 3));
+            }
+          }
+        }
+        if (j0 + 16 <= cols) {
+          *reinterpret_cast<uint4*>(dst + i * ldd + j0) = make_uint4(w[0], w[1], w[2], w[3]);
+        } else {
+          for (std::int64_t c = j0; c < cols; ++c)
+            dst[i * ldd + c] = std::uint8_t((w[(c - j0) >> 2] >> (8 * ((c - j0) & 3))) & 0xFF);
+        }
       }
     }
   }
@@ -700,7 +709,9 @@ void select2d(std::uint8_t* dst, std::int64_t ldd, std::int64_t rows,
   } else if (cmap && al(dst, ldd)) {
     const std::int64_t nvec = (cols + 15) / 16;
     const unsigned gx = unsigned((nvec + 127) / 128);
-    GFQ_CUDA(launch_pdl(select2d_v16_kernel, dim3(dim3(gx, gy)), dim3(128), 0, s, dst, ldd, rows, cols, A, lda, B, ldb, rmap, cmap));
+    const std::int64_t ry = (rows + kSelRows - 1) / kSelRows;
+    const unsigned gyr = unsigned(ry < 65535 ? ry : 65535);
+    GFQ_CUDA(launch_pdl(select2d_v16_kernel, dim3(dim3(gx, gyr)), dim3(128), 0, s, dst, ldd, rows, cols, A, lda, B, ldb, rmap, cmap));
   } else {
     const unsigned gx = unsigned((cols + 255) / 256);
     GFQ_CUDA(launch_pdl(select2d_kernel, dim3(dim3(gx, gy)), dim3(256), 0, s, dst, ldd, rows, cols, A, lda, B, ldb, rmap, cmap));
