@@ -105,11 +105,21 @@ mad_simt_kernel(std::uint32_t p, std::uint32_t magic, int m, int n, int k,
 // one row (one uint4 of D and of Cin), the K coefficients of its A row and
 // the K x 16-byte slab of B (both L1/L2 resident across threads).
 constexpr int kSmallK = 32;
+// MAPS: the row maps of the fused gather / riffle forms (mad_smallk_maps):
+// B row t = Bsrc[brm[t]], the addend of output row i = Cin[crm[i]] (-1:
+// none), output row i lands at D[drm[i]].
+struct SmallkMaps {
+  const std::int32_t* brm;
+  const std::int32_t* crm;
+  const std::int32_t* drm;
+};
+template <bool MAPS>
 __global__ void __launch_bounds__(256)
 mad_smallk_kernel(std::uint32_t p, std::uint32_t magic, int m, int n, int k,
                   const std::uint8_t* __restrict__ A, std::int64_t lda,
                   const std::uint8_t* __restrict__ B, std::int64_t ldb,
-                  const std::uint8_t* Cin, std::int64_t ldc, std::uint8_t* D, std::int64_t ldd) {
+                  const std::uint8_t* Cin, std::int64_t ldc, std::uint8_t* D, std::int64_t ldd,
+                  SmallkMaps mp) {
   pdl_wait_and_release();
   const int nvec = (n + 15) >> 4;
   const std::int64_t tid = std::int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
@@ -124,7 +134,7 @@ mad_smallk_kernel(std::uint32_t p, std::uint32_t magic, int m, int n, int k,
       uint4 x = make_uint4(0, 0, 0, 0);
       for (int t = 0; t < k; ++t) {
         if (!arow[t]) continue;
-        const std::uint8_t* brow = B + std::int64_t(t) * ldb + j0;
+        const std::uint8_t* brow = B + std::int64_t(MAPS && mp.brm ? mp.brm[t] : t) * ldb + j0;
         uint4 b;
         if (full) {
           b = *reinterpret_cast<const uint4*>(brow);
@@ -147,7 +157,7 @@ mad_smallk_kernel(std::uint32_t p, std::uint32_t magic, int m, int n, int k,
       for (int t = 0; t < k; ++t) {
         const std::uint32_t a = arow[t];
         if (!a) continue;
-        const std::uint8_t* brow = B + std::int64_t(t) * ldb + j0;
+        const std::uint8_t* brow = B + std::int64_t(MAPS && mp.brm ? mp.brm[t] : t) * ldb + j0;
         if (full) {
           const uint4 b = *reinterpret_cast<const uint4*>(brow);
           const std::uint32_t bw[4] = {b.x, b.y, b.z, b.w};
@@ -158,8 +168,10 @@ mad_smallk_kernel(std::uint32_t p, std::uint32_t magic, int m, int n, int k,
         }
       }
     }
-    const std::uint8_t* crow = Cin ? Cin + std::int64_t(i) * ldc + j0 : nullptr;
-    std::uint8_t* drow = D + std::int64_t(i) * ldd + j0;
+    const std::int64_t ci = MAPS && mp.crm ? std::int64_t(mp.crm[i]) : std::int64_t(i);
+    const std::int64_t di = MAPS && mp.drm ? std::int64_t(mp.drm[i]) : std::int64_t(i);
+    const std::uint8_t* crow = (Cin && ci >= 0) ? Cin + ci * ldc + j0 : nullptr;
+    std::uint8_t* drow = D + di * ldd + j0;
     if (full) {
       std::uint32_t cw[4] = {0, 0, 0, 0};
       if (crow) {
@@ -367,8 +379,8 @@ void mad(std::uint32_t p, std::int64_t m, std::int64_t n, std::int64_t k,
     const std::int64_t total = m * ((n + 15) / 16);
     const std::int64_t cap = std::int64_t(sm_count()) * 8;
     const unsigned grid = unsigned(std::min<std::int64_t>((total + 255) / 256, cap));
-    GFQ_CUDA(launch_pdl(mad_smallk_kernel, dim3(grid), dim3(256), 0, s, p, magic_of(p), int(m), int(n), int(k), A, lda, B, ldb,
-                                           Cin, ldc, D, ldd));
+    GFQ_CUDA(launch_pdl(mad_smallk_kernel<false>, dim3(grid), dim3(256), 0, s, p, magic_of(p), int(m), int(n), int(k), A, lda, B, ldb,
+                                           Cin, ldc, D, ldd, SmallkMaps{nullptr, nullptr, nullptr}));
     GFQ_CUDA(cudaGetLastError());
     count_launch();
     done = true;
@@ -394,6 +406,28 @@ void mad(std::uint32_t p, std::int64_t m, std::int64_t n, std::int64_t k,
   if (log)
     std::fprintf(stderr, "mad m=%lld n=%lld k=%lld path=%s task=%s\n", static_cast<long long>(m),
                  static_cast<long long>(n), static_cast<long long>(k), rec.path ? "simt" : "tc", hprof::t_task_name);
+}
+
+void mad_smallk_maps(std::uint32_t p, std::int64_t m, std::int64_t n, std::int64_t k,
+                     const std::uint8_t* A, std::int64_t lda, const std::uint8_t* B, std::int64_t ldb,
+                     const std::int32_t* brm, const std::uint8_t* Cin, std::int64_t ldc,
+                     const std::int32_t* crm, std::uint8_t* D, std::int64_t ldd, const std::int32_t* drm,
+                     cudaStream_t s) {
+  if (m == 0 || n == 0) return;
+  if (k < 1 || k > kSmallK) throw std::invalid_argument("mad_smallk_maps: k must be 1..32");
+  const auto al = [](const void* q, std::int64_t ld) {
+    return q == nullptr || ((reinterpret_cast<std::uintptr_t>(q) & 15) == 0 && (ld & 15) == 0);
+  };
+  if (!al(B, ldb) || !al(Cin, ldc) || !al(D, ldd))
+    throw std::invalid_argument("mad_smallk_maps: operands must be 16-byte aligned");
+  hprof::Scope hp(hprof::kMad);
+  ProfScope ps(kProfSimt, 2.0 * double(m) * double(n) * double(k), s);
+  const std::int64_t total = m * ((n + 15) / 16);
+  const std::int64_t cap = std::int64_t(sm_count()) * 8;
+  const unsigned grid = unsigned(std::min<std::int64_t>((total + 255) / 256, cap));
+  GFQ_CUDA(launch_pdl(mad_smallk_kernel<true>, dim3(grid), dim3(256), 0, s, p, magic_of(p), int(m), int(n),
+                      int(k), A, lda, B, ldb, Cin, ldc, D, ldd, SmallkMaps{brm, crm, drm}));
+  count_launch();
 }
 
 // ------------------------------------------------------------------ K3/K4

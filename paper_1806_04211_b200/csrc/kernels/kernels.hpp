@@ -57,6 +57,17 @@ void mad(std::uint32_t p, std::int64_t m, std::int64_t n, std::int64_t k,
          std::int64_t ldb, const std::uint8_t* Cin, std::int64_t ldc,
          std::uint8_t* D, std::int64_t ldd, cudaStream_t s);
 
+// The small-K contraction (k <= 32, 16-byte aligned B / Cin / D) with row
+// maps, for the rank-r' updates fused with their gathers / riffles:
+// D[drm[i]] = Cin[crm[i]] + sum_t A[i][t] * B[brm[t]] (each map may be
+// null = identity; crm[i] = -1: no addend).  Maps are device arrays.
+void mad_smallk_maps(std::uint32_t p, std::int64_t m, std::int64_t n, std::int64_t k,
+                     const std::uint8_t* A, std::int64_t lda, const std::uint8_t* B, std::int64_t ldb,
+                     const std::int32_t* brm, const std::uint8_t* Cin, std::int64_t ldc,
+                     const std::int32_t* crm, std::uint8_t* D, std::int64_t ldd, const std::int32_t* drm,
+                     cudaStream_t s);
+constexpr int kSmallKMax = 32;
+
 // Force a specific K1 implementation (tests / profiling).
 void mad_simt(std::uint32_t p, std::int64_t m, std::int64_t n, std::int64_t k,
               const std::uint8_t* A, std::int64_t lda, const std::uint8_t* B,
