@@ -275,10 +275,20 @@ def main():
     G.lib()
     f = G.FieldSpec(cfg["p"])
     from paper_1806_04211_b200 import workloads
-    C = workloads.build(G, args.config)
+    if cfg.get("sharded_only") and world < 4:
+        if rank == 0:
+            print(json.dumps({"metric": METRIC, "unavailable": f"{args.config} ({cfg['m']}x{cfg['n']} u8 = "
+                              f"{cfg['m'] * cfg['n'] / 2**30:.0f} GiB input) runs sharded over >= 4 GPUs only"}))
+        if dist:
+            dist.destroy_process_group()
+        return
+    # the full-size cfg5 never exists on one GPU: every rank generates only
+    # its own block columns of the seeded stream (K6) inside the call
+    C = None if cfg.get("sharded_only") else workloads.build(G, args.config)
     opts = G.EchelonizeOptions(block=cfg["block"], threads=args.threads, with_transform=True)
     # the one-time mapping of the device pool (cfg5s: ~3.5 s) before any step
-    G.reserve_for(cfg["m"], cfg["n"], True)
+    # (sharded: this rank's share of the block columns)
+    G.reserve_for(cfg["m"], max(1, cfg["n"] // world), True)
     flush = torch.empty(512 << 20, dtype=torch.uint8, device="cuda")
 
     def barrier():
@@ -297,7 +307,7 @@ def main():
     def step(Cin=None, gather=False):
         Cin = C if Cin is None else Cin
         if comm is not None:
-            return G.echelonize_dist(comm, f, cfg["m"], cfg["n"], opts, C=Cin, gather=gather)
+            return G.echelonize_dist(comm, f, cfg["m"], cfg["n"], opts, C=Cin, seed=cfg["seed"], gather=gather)
         return G.echelonize(Cin, f, opts)
 
     rank_r = step(gather=True).rank
@@ -328,11 +338,15 @@ def main():
     clk = clocks.stop()
     launches = G.launch_count(reset=True)
     dm = G.device_memory()
+    if dist:
+        t = torch.tensor([float(dm["peak"])], device="cuda", dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        dm["peak"] = int(t.item())
     hbm = {"high_water_bytes": dm["peak"], "input_bytes": cfg["m"] * cfg["n"],
            "high_water_over_input": dm["peak"] / (cfg["m"] * cfg["n"]),
            "pool_reserved_high_bytes": dm["pool_reserved_high"],
-           "note": "the library's device allocations (matrices, panels, scratch) during the timed steps; "
-                   "the input and one step's outputs included"}
+           "note": "the library's device allocations (matrices, panels, scratch) during the timed steps, "
+                   "max over ranks; the input and one step's outputs included"}
     # K1 per-launch device timing: the same steps again with CUDA events
     # around every K1 launch on its worker stream (kept out of the timed
     # region above: the events add host work per launch).
@@ -360,7 +374,11 @@ def main():
 
     # ---------------- e2e: public API with host buffers (H2D + D2H inside)
     e2e = None
-    if not args.no_e2e:
+    if cfg.get("sharded_only") and not args.no_e2e:
+        e2e = {"value": None, "unit": UNIT, "h2d_bytes_per_step": None, "d2h_bytes_per_step": None,
+               "note": f"{args.config}'s {cfg['m'] * cfg['n'] / 2**30:.0f} GiB input has no host copy: each rank "
+                       "generates its own block columns on the device"}
+    elif not args.no_e2e:
         Ch = torch.empty((cfg["m"], cfg["n"]), dtype=torch.uint8, pin_memory=True)
         Ch.numpy()[:] = C.numpy()
         probe = step(gather=True)

@@ -8,7 +8,9 @@
 #include <algorithm>
 #include <condition_variable>
 #include <cstring>
+#include <deque>
 #include <map>
+#include <thread>
 #include <mutex>
 #include <stdexcept>
 
@@ -61,6 +63,7 @@ struct NcclApi {
                             cudaStream_t) = nullptr;
   ncclResult_t (*commDestroy)(ncclComm_t) = nullptr;
   const char* (*getErrorString)(ncclResult_t) = nullptr;
+  ncclResult_t (*commSplit)(ncclComm_t, int, int, ncclComm_t*, ncclConfig_t*) = nullptr;
 };
 
 NcclApi& nccl() {
@@ -74,6 +77,7 @@ NcclApi& nccl() {
     a.broadcast = reinterpret_cast<decltype(a.broadcast)>(dlsym(a.h, "ncclBroadcast"));
     a.commDestroy = reinterpret_cast<decltype(a.commDestroy)>(dlsym(a.h, "ncclCommDestroy"));
     a.getErrorString = reinterpret_cast<decltype(a.getErrorString)>(dlsym(a.h, "ncclGetErrorString"));
+    a.commSplit = reinterpret_cast<decltype(a.commSplit)>(dlsym(a.h, "ncclCommSplit"));
     if (!a.getUniqueId || !a.commInitRank || !a.broadcast || !a.commDestroy)
       throw std::runtime_error("libnccl.so.2 lacks the required symbols");
     return a;
@@ -93,6 +97,14 @@ class NcclComm : public Comm {
     ncclUniqueId id;
     std::memcpy(&id, id128, sizeof id);
     nccl_check(nccl().commInitRank(&comm_, world, id, rank), "ncclCommInitRank");
+  }
+  NcclComm(int world, int rank, ncclComm_t c) : world_(world), rank_(rank), comm_(c) {}
+  std::shared_ptr<Comm> split_channel() override {
+    // an independent communicator over the same ranks (collective)
+    if (!nccl().commSplit) throw std::runtime_error("libnccl.so.2 lacks ncclCommSplit");
+    ncclComm_t c = nullptr;
+    nccl_check(nccl().commSplit(comm_, 0, rank_, &c, nullptr), "ncclCommSplit");
+    return std::make_shared<NcclComm>(world_, rank_, c);
   }
   ~NcclComm() override {
     if (comm_) nccl().commDestroy(comm_);
@@ -133,6 +145,7 @@ struct LoopbackHub {
   };
   std::map<long, Entry> entries;
   int world = 1;
+  std::vector<std::shared_ptr<LoopbackHub>> children;  // split channels, by index
 };
 
 class LoopbackComm : public Comm {
@@ -140,6 +153,20 @@ class LoopbackComm : public Comm {
   LoopbackComm(std::shared_ptr<LoopbackHub> hub, int rank) : hub_(std::move(hub)), rank_(rank) {}
   int rank() const override { return rank_; }
   int world() const override { return hub_->world; }
+  std::shared_ptr<Comm> split_channel() override {
+    // the n-th split of every rank shares one child hub
+    std::shared_ptr<LoopbackHub> child;
+    {
+      std::lock_guard<std::mutex> lk(hub_->m);
+      const std::size_t idx = splits_++;
+      while (hub_->children.size() <= idx) {
+        hub_->children.push_back(std::make_shared<LoopbackHub>());
+        hub_->children.back()->world = hub_->world;
+      }
+      child = hub_->children[idx];
+    }
+    return std::make_shared<LoopbackComm>(child, rank_);
+  }
   void bcast(void* buf, std::size_t bytes, int root, cudaStream_t s) override {
     const long id = seq_++;
     LoopbackHub& h = *hub_;
@@ -188,6 +215,7 @@ class LoopbackComm : public Comm {
   std::shared_ptr<LoopbackHub> hub_;
   int rank_;
   long seq_ = 0;
+  std::size_t splits_ = 0;
 };
 }  // namespace
 
@@ -261,64 +289,168 @@ struct CommState {
   std::size_t hdr_cap;
 };
 
+// A PkgA header: the host-side fields a receiver needs before it can size
+// and post the payload broadcast.
+struct PkgAHeader {
+  std::int32_t rp = 0, r = 0, live = 0;
+  bool hasA = false, hasE = false, hasL = false;
+  std::vector<std::uint32_t> rho;
+  std::vector<std::uint8_t> lam;
+};
+
+// Headers travel on their own channel (Comm::split_channel) and stream,
+// driven by a header thread that runs ahead of the payload loop: a
+// receiver's host round trip for header q (D2H + stream sync) then never
+// waits behind the large payload broadcasts queued before it, and payload
+// q is posted the moment its header is known.  Both channels issue their
+// collectives in the one schedule order, so neither can deadlock: the
+// header thread blocks only on packages being produced, the payload loop
+// only on headers.
+class HeaderChannel {
+ public:
+  HeaderChannel(CommState& st, CommApi& api) : st_(st), api_(api) {
+    comm_ = st.comm->split_channel();
+    int least = 0, greatest = 0;
+    GFQ_CUDA(cudaDeviceGetStreamPriorityRange(&least, &greatest));
+    GFQ_CUDA(cudaStreamCreateWithPriority(&stream_, cudaStreamNonBlocking, greatest));
+    GFQ_CUDA(cudaGetDevice(&device_));
+    thread_ = std::thread([this] { run(); });
+  }
+  ~HeaderChannel() {
+    {
+      std::lock_guard<std::mutex> lk(m_);
+      quit_ = true;
+    }
+    cv_.notify_all();
+    if (thread_.joinable()) thread_.join();
+    cudaStreamDestroy(stream_);
+  }
+  // the next PkgA header in schedule order (blocks until it arrived)
+  PkgAHeader next() {
+    std::unique_lock<std::mutex> lk(m_);
+    cv_.wait(lk, [&] { return !q_.empty() || !error_.empty(); });
+    if (!error_.empty()) throw std::runtime_error(error_);
+    PkgAHeader h = std::move(q_.front());
+    q_.pop_front();
+    return h;
+  }
+
+ private:
+  void run() {
+    cudaSetDevice(device_);
+    set_cur_stream(stream_);
+    try {
+      const int me = comm_->rank();
+      DevBuf dhdr{st_.hdr_cap * 4};
+      std::vector<std::int32_t> hhdr(st_.hdr_cap);
+      std::int32_t* pinned = nullptr;
+      GFQ_CUDA(cudaMallocHost(reinterpret_cast<void**>(&pinned), st_.hdr_cap * 4));
+      struct PinnedFree {
+        std::int32_t* p;
+        ~PinnedFree() { cudaFreeHost(p); }
+      } pf{pinned};
+      for (const BcastItem& it : *st_.sched) {
+        if (!it.is_a) continue;
+        {
+          std::lock_guard<std::mutex> lk(m_);
+          if (quit_) return;
+        }
+        PkgAHeader h;
+        if (it.root == me) {
+          // host fields only: no wait on the package's device data
+          const auto pub = api_.wait_local(it.slot);
+          const PkgA& A = std::get<PkgA>(pub->value);
+          h.rp = std::int32_t(A.rho_prime.size());
+          h.live = std::int32_t(A.rho_prime.universe);
+          h.r = A.A ? std::int32_t(A.A->cols()) : 0;
+          h.hasA = bool(A.A);
+          h.hasE = bool(A.E);
+          h.hasL = bool(A.lambda);
+          h.rho = A.rho_prime.members;
+          if (A.lambda) h.lam = A.lambda->bits;
+          std::fill(hhdr.begin(), hhdr.end(), 0);
+          hhdr[0] = h.rp;
+          hhdr[1] = h.r;
+          hhdr[2] = h.live;
+          hhdr[3] = h.hasA;
+          hhdr[4] = h.hasE;
+          hhdr[5] = h.hasL;
+          hhdr[6] = std::int32_t(h.lam.size());
+          for (std::int32_t q = 0; q < h.rp; ++q) hhdr[kHdr + q] = std::int32_t(h.rho[std::size_t(q)]);
+          for (std::int32_t q = 0; q < hhdr[6]; ++q) hhdr[kHdr + h.rp + q] = h.lam[std::size_t(q)];
+          std::memcpy(pinned, hhdr.data(), st_.hdr_cap * 4);
+          GFQ_CUDA(cudaMemcpyAsync(dhdr.ptr, pinned, st_.hdr_cap * 4, cudaMemcpyHostToDevice, stream_));
+          comm_->bcast(dhdr.ptr, st_.hdr_cap * 4, it.root, stream_);
+          // the pinned buffer is rewritten by the next header: drain the copy
+          GFQ_CUDA(cudaStreamSynchronize(stream_));
+        } else {
+          comm_->bcast(dhdr.ptr, st_.hdr_cap * 4, it.root, stream_);
+          GFQ_CUDA(cudaMemcpyAsync(pinned, dhdr.ptr, st_.hdr_cap * 4, cudaMemcpyDeviceToHost, stream_));
+          GFQ_CUDA(cudaStreamSynchronize(stream_));
+          std::memcpy(hhdr.data(), pinned, st_.hdr_cap * 4);
+          h.rp = hhdr[0];
+          h.r = hhdr[1];
+          h.live = hhdr[2];
+          h.hasA = hhdr[3];
+          h.hasE = hhdr[4];
+          h.hasL = hhdr[5];
+          h.rho.assign(hhdr.begin() + kHdr, hhdr.begin() + kHdr + h.rp);
+          h.lam.assign(hhdr.begin() + kHdr + h.rp, hhdr.begin() + kHdr + h.rp + hhdr[6]);
+        }
+        std::lock_guard<std::mutex> lk(m_);
+        q_.push_back(std::move(h));
+        cv_.notify_all();
+      }
+    } catch (const std::exception& e) {
+      std::lock_guard<std::mutex> lk(m_);
+      error_ = std::string("header channel: ") + e.what();
+      cv_.notify_all();
+    }
+    set_cur_stream(nullptr);
+  }
+
+  CommState& st_;
+  CommApi& api_;
+  std::shared_ptr<Comm> comm_;
+  cudaStream_t stream_ = nullptr;
+  int device_ = 0;
+  std::thread thread_;
+  std::mutex m_;
+  std::condition_variable cv_;
+  std::deque<PkgAHeader> q_;
+  std::string error_;
+  bool quit_ = false;
+};
+
+void comm_loop_body(CommState& st, CommApi& api, HeaderChannel& headers);
+
 void comm_loop(CommState& st, CommApi& api) {
+  HeaderChannel headers(st, api);
+  try {
+    comm_loop_body(st, api, headers);
+  } catch (const std::exception& e) {
+    // release the header thread if it waits on a package (its destructor joins)
+    if (api.abort) api.abort(e.what());
+    throw;
+  }
+}
+
+void comm_loop_body(CommState& st, CommApi& api, HeaderChannel& headers) {
   Comm& comm = *st.comm;
   const int me = comm.rank();
   const cudaStream_t s = api.stream;
-  DevBuf dhdr{st.hdr_cap * 4};
-  std::vector<std::int32_t> hhdr(st.hdr_cap);
-  std::int32_t* pinned = nullptr;
-  GFQ_CUDA(cudaMallocHost(reinterpret_cast<void**>(&pinned), st.hdr_cap * 4));
-  struct PinnedFree {
-    std::int32_t* p;
-    ~PinnedFree() { cudaFreeHost(p); }
-  } pf{pinned};
 
   for (const BcastItem& it : *st.sched) {
     const bool root = it.root == me;
     if (it.is_a) {
-      // ---- PkgA(i, j): header (shapes, rho', lambda) then one payload
+      // ---- PkgA(i, j): the header from the header channel, then one payload
       std::shared_ptr<Published> pub;
-      std::int32_t rp = 0, r = 0, live = 0;
-      bool hasA = false, hasE = false, hasL = false;
-      std::vector<std::uint32_t> rho;
-      std::vector<std::uint8_t> lam;
+      PkgAHeader hd = headers.next();
+      const std::int32_t rp = hd.rp, r = hd.r, live = hd.live;
+      const bool hasA = hd.hasA, hasE = hd.hasE, hasL = hd.hasL;
       if (root) {
         pub = api.wait_local(it.slot);
         if (pub->ready) GFQ_CUDA(cudaStreamWaitEvent(s, pub->ready->ev, 0));
-        const PkgA& A = std::get<PkgA>(pub->value);
-        rp = std::int32_t(A.rho_prime.size());
-        live = std::int32_t(A.rho_prime.universe);
-        r = A.A ? std::int32_t(A.A->cols()) : 0;
-        hasA = bool(A.A);
-        hasE = bool(A.E);
-        hasL = bool(A.lambda);
-        std::fill(hhdr.begin(), hhdr.end(), 0);
-        hhdr[0] = rp;
-        hhdr[1] = r;
-        hhdr[2] = live;
-        hhdr[3] = hasA;
-        hhdr[4] = hasE;
-        hhdr[5] = hasL;
-        hhdr[6] = hasL ? std::int32_t(A.lambda->size()) : 0;
-        for (std::int32_t q = 0; q < rp; ++q) hhdr[kHdr + q] = std::int32_t(A.rho_prime.members[q]);
-        for (std::int32_t q = 0; q < hhdr[6]; ++q) hhdr[kHdr + rp + q] = A.lambda->bits[q];
-        std::memcpy(pinned, hhdr.data(), st.hdr_cap * 4);
-        GFQ_CUDA(cudaMemcpyAsync(dhdr.ptr, pinned, st.hdr_cap * 4, cudaMemcpyHostToDevice, s));
-      }
-      comm.bcast(dhdr.ptr, st.hdr_cap * 4, it.root, s);
-      if (!root) {
-        GFQ_CUDA(cudaMemcpyAsync(pinned, dhdr.ptr, st.hdr_cap * 4, cudaMemcpyDeviceToHost, s));
-        GFQ_CUDA(cudaStreamSynchronize(s));
-        std::memcpy(hhdr.data(), pinned, st.hdr_cap * 4);
-        rp = hhdr[0];
-        r = hhdr[1];
-        live = hhdr[2];
-        hasA = hhdr[3];
-        hasE = hhdr[4];
-        hasL = hhdr[5];
-        rho.assign(hhdr.begin() + kHdr, hhdr.begin() + kHdr + rp);
-        lam.assign(hhdr.begin() + kHdr + rp, hhdr.begin() + kHdr + rp + hhdr[6]);
       }
       Layout L;
       L.add(hasA ? live : 0, hasA ? r : 0);  // A.A
@@ -343,8 +475,8 @@ void comm_loop(CommState& st, CommApi& api) {
         A.M = Mat::view_of(payload, P[1].off, P[1].rows, P[1].cols, P[1].ld);
         A.K = Mat::view_of(payload, P[2].off, P[2].rows, P[2].cols, P[2].ld);
         if (hasE) A.E = Mat::view_of(payload, P[3].off, P[3].rows, P[3].cols, P[3].ld);
-        A.rho_prime = IndexSet(std::size_t(live), rho);
-        if (hasL) A.lambda = BitString(lam);
+        A.rho_prime = IndexSet(std::size_t(live), std::move(hd.rho));
+        if (hasL) A.lambda = BitString(std::move(hd.lam));
         auto np = std::make_shared<Published>();
         np->value = std::move(A);
         np->ready = std::make_shared<EventBox>();

@@ -43,6 +43,9 @@ class Comm {
   /// Broadcast `bytes` from `root`'s `buf` into every rank's `buf`, ordered
   /// on `s`.  May block the calling (communication) thread.
   virtual void bcast(void* buf, std::size_t bytes, int root, cudaStream_t s) = 0;
+  /// A second, independent channel over the same ranks (every rank calls it
+  /// at the same point): its broadcasts order only against each other.
+  virtual std::shared_ptr<Comm> split_channel() = 0;
 };
 
 /// NCCL communicator (libnccl.so.2 opened at run time).

@@ -25,6 +25,11 @@ CONFIGS = {
                  desc="cfg4 GF(251) 32768x32768 block 4096"),
     "cfg5s": dict(p=2, m=65536, n=65536, block=8192, seed=1, kind="random",
                   desc="cfg5 1-GPU: GF(2) 65536x65536 leading case, block 8192"),
+    # configs[4] at full size: 68.7 GB of u8 input, a 32 x 32 block grid;
+    # only the block-column sharded run (N >= 4, each rank generating its
+    # own columns of the seeded stream) holds it -- see bench.py
+    "cfg5": dict(p=2, m=262144, n=262144, block=8192, seed=1, kind="random", sharded_only=True,
+                 desc="cfg5 GF(2) 262144x262144 block 8192 (BASELINE configs[4], sharded)"),
 }
 
 
