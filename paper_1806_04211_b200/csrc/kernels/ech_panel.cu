@@ -668,14 +668,18 @@ ech_step_chain_kernel(std::uint32_t p, std::uint32_t magic, int rows, int c0, in
     stamp(1);
     int r2 = 0, ok = 1, q0 = -1, q1 = -1, mpc = 0, mpr = 0;
     const unsigned lanebit = 1u << lane;
+    // Rotated loop: the next column's head (its elements after this
+    // column's update, their residues, inverse lookups and the two votes)
+    // is computed right after f0 / f1 are known and BEFORE the bulk of the
+    // update, so the bulk's independent FMAs fill the latency of the head's
+    // shared-memory lookups and votes instead of sitting in front of them
+    // (in-order issue in one warp).
+    float v0 = red(w0[0]), v1 = red(w1[0]);
+    std::uint32_t iv0 = invw[int(v0)], iv1 = invw[int(v1)];
+    unsigned b0 = __ballot_sync(0xffffffffu, open0 && v0 != 0.0f);
+    unsigned b1 = __ballot_sync(0xffffffffu, open1 && v1 != 0.0f);
 #pragma unroll 1
     for (int c = 0; c < wc; ++c) {
-      const float v0 = red(w0[0]), v1 = red(w1[0]);
-      // every lane looks up its candidates' inverses now, overlapping the
-      // votes; the pivot lane's is shuffled out below (no smem round trip)
-      const std::uint32_t iv0 = invw[int(v0)], iv1 = invw[int(v1)];
-      const unsigned b0 = __ballot_sync(0xffffffffu, open0 && v0 != 0.0f);
-      const unsigned b1 = __ballot_sync(0xffffffffu, open1 && v1 != 0.0f);
       // the shifted panel moves on whether or not the column has a pivot
       if (!(b0 | b1)) {
         if (!covers_all) {
@@ -688,6 +692,12 @@ ech_step_chain_kernel(std::uint32_t p, std::uint32_t magic, int rows, int c0, in
           w1[e] = w1[e + 1];
         }
         w0[31] = w1[31] = 0.0f;
+        v0 = red(w0[0]);
+        v1 = red(w1[0]);
+        iv0 = invw[int(v0)];
+        iv1 = invw[int(v1)];
+        b0 = __ballot_sync(0xffffffffu, open0 && v0 != 0.0f);
+        b1 = __ballot_sync(0xffffffffu, open1 && v1 != 0.0f);
         continue;  // a free column
       }
       const bool hi = b0 == 0;
@@ -730,18 +740,6 @@ ech_step_chain_kernel(std::uint32_t p, std::uint32_t magic, int rows, int c0, in
       const bool me0 = !hi && mine, me1 = hi && mine;
       const float f0 = me0 ? sc - 1.0f : red(v0 * sc);
       const float f1 = me1 ? sc - 1.0f : red(v1 * sc);
-      // shift the panel part while updating; coefficients in place
-#pragma unroll
-      for (int e = 0; e < 31; ++e) {
-        w0[e] = fmaf(f0, y[e + 1], w0[e + 1]);
-        w1[e] = fmaf(f1, y[e + 1], w1[e + 1]);
-      }
-      w0[31] = w1[31] = 0.0f;
-#pragma unroll
-      for (int e = 0; e < 32; ++e) {
-        k0[e] = fmaf(f0, y[32 + e], k0[e]);
-        k1[e] = fmaf(f1, y[32 + e], k1[e]);
-      }
       if (me0) {
         open0 = false;
         q0 = r2;
@@ -755,6 +753,28 @@ ech_step_chain_kernel(std::uint32_t p, std::uint32_t magic, int rows, int c0, in
         mpr = lo + (hi ? 32 : 0) + (__ffs(bb) - 1);
       }
       ++r2;
+      // the next column's head first
+      const float h0 = fmaf(f0, y[1], w0[1]), h1 = fmaf(f1, y[1], w1[1]);
+      v0 = red(h0);
+      v1 = red(h1);
+      iv0 = invw[int(v0)];
+      iv1 = invw[int(v1)];
+      // then the bulk: shift the panel part while updating; coefficients in place
+#pragma unroll
+      for (int e = 1; e < 31; ++e) {
+        w0[e] = fmaf(f0, y[e + 1], w0[e + 1]);
+        w1[e] = fmaf(f1, y[e + 1], w1[e + 1]);
+      }
+      w0[0] = h0;
+      w1[0] = h1;
+      w0[31] = w1[31] = 0.0f;
+#pragma unroll
+      for (int e = 0; e < 32; ++e) {
+        k0[e] = fmaf(f0, y[32 + e], k0[e]);
+        k1[e] = fmaf(f1, y[32 + e], k1[e]);
+      }
+      b0 = __ballot_sync(0xffffffffu, open0 && v0 != 0.0f);
+      b1 = __ballot_sync(0xffffffffu, open1 && v1 != 0.0f);
       __syncwarp();  // wrow is rewritten by the next column's pivot lane
     }
     if (lane < r2) {
