@@ -568,6 +568,10 @@ __device__ __forceinline__ void stamp(int k) {
 }
 // warp 0 runs the chain; the other warps join the fallback and the outputs
 constexpr int kChainThreads = 128;
+// TW: the chain in two warps (warp w holds window rows lo + 32w + lane),
+// exchanging votes and the pivot row through shared memory at named
+// barriers: half the per-lane update work on each of two SMSPs.
+template <bool TW>
 __global__ void __launch_bounds__(kChainThreads, 1)
 ech_step_chain_kernel(std::uint32_t p, std::uint32_t magic, int rows, int c0, int wc, int n,
                       std::uint8_t* __restrict__ Z, std::int64_t ld, std::uint8_t* flags,
@@ -612,9 +616,10 @@ ech_step_chain_kernel(std::uint32_t p, std::uint32_t magic, int rows, int c0, in
   // rows, so BpT is built from here (the region doubles as panel_full's
   // fallback storage, after which the tail reads Z instead)
   std::uint8_t* Ws = dsm;  // 64 x n
-  if (warp > 0) {
+  constexpr int kChainW = TW ? 2 : 1;  // warps running the chain
+  if (warp >= kChainW) {
     const int nv = n / 16;
-    for (int e = tid - 32; e < 64 * nv; e += kChainThreads - 32) {
+    for (int e = tid - 32 * kChainW; e < 64 * nv; e += kChainThreads - 32 * kChainW) {
       const int r = e / nv, ch = e % nv;
       uint4 v = make_uint4(0, 0, 0, 0);
       if (lo + r < rows) v = *reinterpret_cast<const uint4*>(Z + std::int64_t(lo + r) * ld + c0 + 16 * ch);
@@ -641,7 +646,124 @@ ech_step_chain_kernel(std::uint32_t p, std::uint32_t magic, int rows, int c0, in
     const float q = (fmaf(v, invp, roff) + 12582912.0f) - 12582912.0f;
     return fmaf(-fp, q, v);
   };
-  if (warp == 0) {
+  if (TW && warp < 2) {
+    __shared__ unsigned s_ball[2][2];
+    __shared__ int s_cnt[2];
+    __shared__ std::uint32_t s_iv;
+    const auto bar = [] { asm volatile("bar.sync 1, 64;" ::: "memory"); };
+    float w[32], k[32];
+    const int row = lo + 32 * warp + lane;
+    bool open = row < rows && flags[row] == 0;
+#pragma unroll
+    for (int e = 0; e < 32; ++e) w[e] = k[e] = 0.0f;
+    if (row < rows) {
+      const std::uint8_t* src = Z + std::int64_t(row) * ld + c0;
+      if (wc == kW) {
+        const uint4 a = reinterpret_cast<const uint4*>(src)[0], b = reinterpret_cast<const uint4*>(src)[1];
+        const std::uint32_t ww[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
+#pragma unroll
+        for (int e = 0; e < 32; ++e) w[e] = float((ww[e >> 2] >> (8 * (e & 3))) & 0xFFu);
+      } else {
+#pragma unroll
+        for (int e = 0; e < 32; ++e)
+          if (e < wc) w[e] = float(src[e]);
+      }
+    }
+    {
+      const unsigned ob = __ballot_sync(0xffffffffu, open);
+      if (lane == 0) s_cnt[warp] = __popc(ob);
+    }
+    bar();
+    const bool covers_all = s_cnt[0] + s_cnt[1] == rows - r_old;
+    stamp(1);
+    int r2 = 0, ok = 1, q = -1, mpc = 0, mpr = 0;
+    float v = red(w[0]);
+    std::uint32_t iv = invw[int(v)];
+    unsigned b = __ballot_sync(0xffffffffu, open && v != 0.0f);
+#pragma unroll 1
+    for (int c = 0; c < wc; ++c) {
+      if (lane == 0) s_ball[c & 1][warp] = b;
+      bar();
+      const unsigned ball0 = s_ball[c & 1][0], ball1 = s_ball[c & 1][1];
+      if (!(ball0 | ball1)) {
+        if (!covers_all) {
+          ok = 0;
+          break;
+        }
+#pragma unroll
+        for (int e = 0; e < 31; ++e) w[e] = w[e + 1];
+        w[31] = 0.0f;
+        v = red(w[0]);
+        iv = invw[int(v)];
+        b = __ballot_sync(0xffffffffu, open && v != 0.0f);
+        continue;  // a free column
+      }
+      const int pw = ball0 ? 0 : 1;
+      const unsigned bb = pw ? ball1 : ball0;
+      const int pl = __ffs(bb) - 1;
+      const bool mine = warp == pw && lane == pl;
+      if (mine) {
+        float4* dst = reinterpret_cast<float4*>(wrow);
+#pragma unroll
+        for (int e = 0; e < 8; ++e) {
+          dst[e] = make_float4(w[4 * e], w[4 * e + 1], w[4 * e + 2], w[4 * e + 3]);
+          dst[8 + e] = make_float4(k[4 * e], k[4 * e + 1], k[4 * e + 2], k[4 * e + 3]);
+        }
+        s_iv = iv;
+      }
+      bar();
+      // reduce the published row, one element a thread; plant e_r2 (that
+      // coefficient is still 0 in every row)
+      {
+        const int t = 32 * warp + lane;
+        wrow[t] = t == 32 + r2 ? 1.0f : red(wrow[t]);
+      }
+      bar();
+      const float sc = float(p - s_iv);
+      float y[64];
+      {
+        const float4* src = reinterpret_cast<const float4*>(wrow);
+#pragma unroll
+        for (int e = 0; e < 16; ++e) {
+          const float4 t = src[e];
+          y[4 * e] = t.x; y[4 * e + 1] = t.y; y[4 * e + 2] = t.z; y[4 * e + 3] = t.w;
+        }
+      }
+      const float f = mine ? sc - 1.0f : red(v * sc);
+      if (mine) {
+        open = false;
+        q = r2;
+      }
+      if (warp == 0 && lane == r2) {
+        mpc = c;
+        mpr = lo + 32 * pw + pl;
+      }
+      ++r2;
+      const float h = fmaf(f, y[1], w[1]);
+      v = red(h);
+      iv = invw[int(v)];
+#pragma unroll
+      for (int e = 1; e < 31; ++e) w[e] = fmaf(f, y[e + 1], w[e + 1]);
+      w[0] = h;
+      w[31] = 0.0f;
+#pragma unroll
+      for (int e = 0; e < 32; ++e) k[e] = fmaf(f, y[32 + e], k[e]);
+      b = __ballot_sync(0xffffffffu, open && v != 0.0f);
+    }
+    if (warp == 0 && lane < r2) {
+      wpc[lane] = mpc;
+      wpr[lane] = mpr;
+    }
+    if (ok && q >= 0) {
+#pragma unroll
+      for (int e = 0; e < 32; ++e) chatb[q][e] = std::uint8_t(int(red(k[e])));
+    }
+    if (warp == 0 && lane == 0) {
+      s_ok = ok;
+      s_r2 = r2;
+    }
+  }
+  if (!TW && warp == 0) {
     float w0[32], w1[32], k0[32], k1[32];
     const int i0 = lo + lane, i1 = lo + 32 + lane;
     bool open0 = i0 < rows && flags[i0] == 0, open1 = i1 < rows && flags[i1] == 0;
@@ -1347,13 +1469,13 @@ void ech_step(std::uint32_t p, std::int64_t rows, std::int64_t c0, std::int64_t 
   if (smem > std::size_t(kPanelSmem)) throw std::invalid_argument("ech_step: block too tall");
   static bool attr = false;
   if (!attr) {
-    GFQ_CUDA(cudaFuncSetAttribute(ech_step_chain_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  kPanelSmem));
+    for (auto fn : {ech_step_chain_kernel<false>, ech_step_chain_kernel<true>})
+      GFQ_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, kPanelSmem));
     // both step kernels ask for the largest shared-memory carveout so the SM
     // does not reconfigure L1 / shared memory between them
     if (!std::getenv("GFQ_NO_CARVEOUT")) {
-      GFQ_CUDA(cudaFuncSetAttribute(ech_step_chain_kernel,
-                                    cudaFuncAttributePreferredSharedMemoryCarveout, 100));
+      for (auto fn : {ech_step_chain_kernel<false>, ech_step_chain_kernel<true>})
+        GFQ_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
       GFQ_CUDA(cudaFuncSetAttribute(ech_step_update_kernel,
                                     cudaFuncAttributePreferredSharedMemoryCarveout, 100));
     }
@@ -1367,7 +1489,9 @@ void ech_step(std::uint32_t p, std::int64_t rows, std::int64_t c0, std::int64_t 
   std::uint8_t* Gpiv = step_scratch + kW * kW;
   std::uint8_t* BpT = step_scratch + 2 * kW * kW;
   const std::uint8_t* invt = inv_table(p);
-  GFQ_CUDA(launch_pdl(ech_step_chain_kernel, dim3(1), dim3(kChainThreads), smem, s, p, magic, int(rows),
+  static const bool one_warp = std::getenv("GFQ_CHAIN1") != nullptr;  // A/B: the one-warp chain
+  GFQ_CUDA(launch_pdl(one_warp ? ech_step_chain_kernel<false> : ech_step_chain_kernel<true>, dim3(1),
+                      dim3(kChainThreads), smem, s, p, magic, int(rows),
                       int(c0), int(wc), int(n), Z, ld, flags, info, int(cap), rho2, lo_state, NT, Gpiv,
                       Y, base, BpT, invt));
   GFQ_CUDA(launch_pdl(ech_step_update_kernel, dim3(unsigned((rows + kStepRows - 1) / kStepRows)),
