@@ -38,53 +38,11 @@ const std::int32_t* dptr(const std::shared_ptr<DevBuf>& b) {
   return b ? reinterpret_cast<const std::int32_t*>(b->ptr) : nullptr;
 }
 
-// A select whose one map is a handful of runs (consecutive source rows or
-// columns of one operand, or zeros) is a few strided copies: they go to the
-// copy engines (cudaMemcpy2DAsync / cudaMemset2DAsync), which move the bytes
-// without taking SM time from the contractions running beside them.  The
-// large gathers of the plan are of this kind: a riffle inserting one row
-// (3 runs), a row split with one row missing (2 runs), a widening by a new
-// zero part (a few runs).
-bool select_dma(const Mat& out, const Mat& A, const Mat* B, const std::vector<std::int32_t>* rmap,
-                const std::vector<std::int32_t>* cmap) {
-  // measured neutral on cfg5s (the copy engines are no faster than the
-  // gather kernels beside K1): opt-in with GFQ_DMA_SELECT=1
-  static const bool off = std::getenv("GFQ_DMA_SELECT") == nullptr;
-  constexpr std::size_t kMaxRuns = 8;
-  const std::int64_t rows = out.rows(), cols = out.cols();
-  if (off || (rmap && cmap) || rows * cols < (std::int64_t(8) << 20)) return false;
-  std::vector<Run> runs;
-  if (!rmap && !cmap) runs.push_back(Run{0, cols, 0, 0});
-  else if (!runs_of(rmap ? *rmap : *cmap, runs, kMaxRuns)) return false;
-  const cudaStream_t s = cur_stream();
-  dev::ProfScope ps(dev::kProfSelect, 2.0 * double(rows) * double(cols), s);
-  for (const Run& r : runs) {
-    const Mat* S = r.from == 1 ? B : &A;
-    if (rmap) {
-      std::uint8_t* d = out.data() + r.t * out.ld();
-      if (r.from < 0)
-        GFQ_CUDA(cudaMemset2DAsync(d, std::size_t(out.ld()), 0, std::size_t(cols), std::size_t(r.len), s));
-      else
-        GFQ_CUDA(cudaMemcpy2DAsync(d, std::size_t(out.ld()), S->data() + r.src * S->ld(), std::size_t(S->ld()),
-                                   std::size_t(cols), std::size_t(r.len), cudaMemcpyDeviceToDevice, s));
-    } else {
-      std::uint8_t* d = out.data() + r.t;
-      if (r.from < 0)
-        GFQ_CUDA(cudaMemset2DAsync(d, std::size_t(out.ld()), 0, std::size_t(r.len), std::size_t(rows), s));
-      else
-        GFQ_CUDA(cudaMemcpy2DAsync(d, std::size_t(out.ld()), S->data() + r.src, std::size_t(S->ld()),
-                                   std::size_t(r.len), std::size_t(rows), cudaMemcpyDeviceToDevice, s));
-    }
-  }
-  return true;
-}
-
 // out = select(A | B) by optional row/column maps (kernels.hpp select2d).
 Mat select(std::int64_t rows, std::int64_t cols, const Mat& A, const Mat* B,
            const std::vector<std::int32_t>* rmap, const std::vector<std::int32_t>* cmap) {
   Mat out(rows, cols);
   if (out.empty()) return out;
-  if (select_dma(out, A, B, rmap, cmap)) return out;
   // small maps ride in the launch parameters (no upload call)
   static const bool inline_maps = std::getenv("GFQ_NO_INLINE_MAPS") == nullptr;
   if (inline_maps &&

@@ -464,20 +464,11 @@ DevBuf::DevBuf(std::size_t n) : bytes(n) {
   init_pool();
   hprof::Scope hp(hprof::kMalloc);
   const cudaStream_t s = cur_stream_raw();
-  // GFQ_CACHE_MAX_MB = x: blocks of >= x MB bypass the cache and go to the
-  // stream-ordered pool directly.  Measured worse (cfg5s: 2849 pool misses
-  // at ~450 us, cfg4 steps 66 -> 116-228 ms), so off by default: the cache
-  // keeps every size and echelonize reserves the pool up front instead.
-  static const std::size_t large = [] {
-    const char* e = std::getenv("GFQ_CACHE_MAX_MB");
-    return e ? std::size_t(std::atoll(e)) << 20 : ~std::size_t(0);
-  }();
-  const bool big = n >= large;
-  const std::size_t cls = big ? (n + 511) / 512 * 512 : size_class(n);
+  const std::size_t cls = size_class(n);
   BlockCache& c = cache();
   void* p = nullptr;
   static const bool nocache = std::getenv("GFQ_NO_BLOCK_CACHE") != nullptr;
-  if (!nocache && !big) {
+  if (!nocache) {
     std::lock_guard<std::mutex> lk(c.mtx);
     auto it = c.by_stream.find(s);
     if (it != c.by_stream.end()) p = take(it->second, cls);
@@ -504,10 +495,8 @@ DevBuf::DevBuf(std::size_t n) : bytes(n) {
       e = cudaMallocAsync(&p, cls, s);
     }
     GFQ_CUDA(e);
-    if (!big) {
-      std::lock_guard<std::mutex> lk(c.mtx);
-      c.cls_of[p] = cls;
-    }
+    std::lock_guard<std::mutex> lk(c.mtx);
+    c.cls_of[p] = cls;
   }
   ptr = static_cast<std::uint8_t*>(p);
   // Developer check (GFQ_POISON bit 0): fill every allocation with 0xA5 on
