@@ -277,3 +277,38 @@ def test_early_download_matches_download_blocks(G, p, m, n, block, kind, wt, fus
     if want.size:
         with pytest.raises(Exception, match="too small"):
             G.echelonize(C, G.FieldSpec(p), opts, host_out=np.zeros(want.size - 1, np.uint8))
+
+
+def test_concurrent_runs_share_the_executor_pools(G):
+    """Several host threads echelonize at once: the process-wide worker-thread
+    and stream pools (csrc/host/scheduler.cpp run_on_workers / acquire_stream)
+    hand each run its own workers and streams; every result must equal the
+    same run made alone, over several rounds (pooled streams are reused)."""
+    import threading
+    cases = [(3, 700, 650, 128), (2, 1500, 1400, 256), (7, 600, 900, 100), (251, 512, 512, 128)]
+    inputs = [(p, oracle.random_matrix(p, m, n, 40 + q), block) for q, (p, m, n, block) in enumerate(cases)]
+    alone = []
+    for p, C, block in inputs:
+        out = G.echelonize(C, G.FieldSpec(p), G.EchelonizeOptions(block=block, threads=3))
+        alone.append((out.rank, out.assembled_R().numpy(), out.materialize_transform().numpy()))
+    for _ in range(3):
+        got, errs = [None] * len(inputs), []
+
+        def body(q):
+            try:
+                p, C, block = inputs[q]
+                out = G.echelonize(C, G.FieldSpec(p), G.EchelonizeOptions(block=block, threads=3))
+                got[q] = (out.rank, out.assembled_R().numpy(), out.materialize_transform().numpy())
+            except Exception as e:  # noqa: BLE001
+                errs.append(e)
+
+        th = [threading.Thread(target=body, args=(q,)) for q in range(len(inputs))]
+        for t in th:
+            t.start()
+        for t in th:
+            t.join(timeout=300)
+        assert not errs, errs
+        for q in range(len(inputs)):
+            assert got[q][0] == alone[q][0]
+            np.testing.assert_array_equal(got[q][1], alone[q][1])
+            np.testing.assert_array_equal(got[q][2], alone[q][2])
