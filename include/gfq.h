@@ -267,6 +267,9 @@ int gfq_output_trace(const gfq_output* o, uint64_t* n, int32_t* kind, int32_t* i
  * first kernel, and to its last kernel completing; -1 when unavailable. */
 int gfq_output_trace_device(const gfq_output* o, uint64_t* n, int64_t* dev_start_ns,
                             int64_t* dev_end_ns);
+/* Live package bytes right after each trace record's task (TraceRecord::
+ * live_bytes, include/gfrref/scheduler.hpp:90), same order. */
+int gfq_output_trace_live(const gfq_output* o, uint64_t* n, int64_t* live_bytes);
 void gfq_output_free(gfq_output* o);
 
 /* ------------------------------------------------------------ text I/O */

@@ -83,6 +83,7 @@ PROTOS = {
     "gfq_launch_count": (I, [I, c_i64p]),
     "gfq_profile": (I, [I]),
     "gfq_device_memory": (I, [I, c_i64p, c_i64p, c_i64p]),
+    "gfq_output_trace_live": (I, [vp, c_u64p, c_i64p]),
     "gfq_profile_take_kinds": (I, [I, c_i64p, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_double),
                                    ctypes.POINTER(ctypes.c_double)]),
     "gfq_profile_take": (I, [c_i64p, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_double)]),

@@ -696,6 +696,14 @@ int gfq_output_trace_device(const gfq_output* o, uint64_t* n, int64_t* dev_start
     }
   });
 }
+int gfq_output_trace_live(const gfq_output* o, uint64_t* n, int64_t* live_bytes) {
+  return guard([&] {
+    const auto& tr = O(o).report.trace;
+    if (n) *n = tr.size();
+    if (live_bytes)
+      for (size_t q = 0; q < tr.size(); ++q) live_bytes[q] = tr[q].live_bytes;
+  });
+}
 void gfq_output_free(gfq_output* o) { delete o; }
 
 int gfq_read_gfmat_file(const char* path, uint32_t* p, gfq_mat** out) {

@@ -782,9 +782,12 @@ class EchelonOutput:
         ds, de = np.zeros(max(cnt, 1), np.int64), np.zeros(max(cnt, 1), np.int64)
         _check(lib().gfq_output_trace_device(self.h, None, ds.ctypes.data_as(_capi.c_i64p),
                                              de.ctypes.data_as(_capi.c_i64p)))
+        live = np.zeros(max(cnt, 1), np.int64)
+        _check(lib().gfq_output_trace_live(self.h, None, live.ctypes.data_as(_capi.c_i64p)))
         return [dict(kind=TASK_KINDS[kind[q]], i=int(i[q]), j=int(j[q]), k=int(k[q]), worker=int(w[q]),
                      start_ns=int(s[q]), end_ns=int(e[q]), detail=int(det[q]),
-                     dev_start_ns=int(ds[q]), dev_end_ns=int(de[q])) for q in range(cnt)]
+                     dev_start_ns=int(ds[q]), dev_end_ns=int(de[q]), live_bytes=int(live[q]))
+                for q in range(cnt)]
 
 
 def echelonize(C, f: FieldSpec, options: EchelonizeOptions = None, host_out=None) -> EchelonOutput:

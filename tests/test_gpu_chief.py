@@ -312,3 +312,26 @@ def test_concurrent_runs_share_the_executor_pools(G):
             assert got[q][0] == alone[q][0]
             np.testing.assert_array_equal(got[q][1], alone[q][1])
             np.testing.assert_array_equal(got[q][2], alone[q][2])
+
+
+STEP1 = {"ClearDown", "UpdateRow", "UpdateRowTrafo", "Extend", "UpdateRowW", "UpdateRowTrafoW"}
+STEP3 = {"Copy", "PreClearUp", "ClearUp", "ClearUpRW", "ClearUpMW"}
+
+
+@pytest.mark.parametrize("threads,fuse", [(1, False), (1, True), (4, True)])
+def test_memory_stability_acceptance_criterion6(G, threads, fuse):
+    """The reference's acceptance criterion 6 (tests/acceptance.cpp:480-520)
+    on the same input: 2048^2 GF(3), seed 0x6eed, block 256, with trace --
+    peak live package bytes <= 4x the input, and the Step-3 peak <= 1.6x the
+    Step-1 peak (the refcounted release keeps Step 3 from growing)."""
+    p, n = 3, 2048
+    C = G.random_matrix(G.FieldSpec(p), n, n, 0x6EED)
+    out = G.echelonize(C, G.FieldSpec(p), G.EchelonizeOptions(block=256, threads=threads, collect_trace=True,
+                                                              fuse=fuse))
+    rep = out.report()
+    input_bytes = n * n
+    step1 = max((t["live_bytes"] for t in out.trace() if t["kind"] in STEP1), default=0)
+    step3 = max((t["live_bytes"] for t in out.trace() if t["kind"] in STEP3), default=0)
+    assert step1 > 0
+    assert rep["peak_live_bytes"] <= 4.0 * input_bytes, (rep["peak_live_bytes"], input_bytes)
+    assert step3 <= 1.6 * step1, (step3, step1)
