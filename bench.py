@@ -209,17 +209,18 @@ def dominant_shape(config):
             "cfg2a": (1024, 8192, 1024), "cfg2b": (1024, 8192, 1024), "cfg1": (500, 2000, 500)}.get(config)
 
 
-def k1_isolated(G, p, peak, dominant=None):
+def k1_isolated(G, p, peak, dominant=None, policy=2):
     """K1 alone on a quiet device: CUDA events around back-to-back launches
     (after 3 warm-ups) through gfq_mad_raw on the current stream, tcgen05
-    path forced; shapes: the 1024^3 block product and the step's dominant
-    shape."""
+    path forced (policy 2: kind::i8; 3: the FP4 path, its two operand
+    packing passes included); shapes: the 1024^3 block product and the
+    step's dominant shape."""
     import torch
     out = []
     shapes = [(1024, 1024, 1024)]
     if dominant and dominant not in shapes:
         shapes.append(dominant)
-    G.set_mad_policy(2)
+    G.set_mad_policy(policy)
     try:
         for (m, n, k) in shapes:
             A = torch.randint(0, p, (m, k), dtype=torch.uint8, device="cuda")
@@ -427,11 +428,17 @@ def main():
         hpeak, hpeak_src = peaks["hbm_gbs"], "measured copy bandwidth (MEASURED_PEAKS.json)"
     else:
         hpeak, hpeak_src = 7672.0, "fallback (B200_PROFILING.md)"
+    # the FP4 path (kind::mxf4) peaks at 4 x dense bf16 (B200: 9 vs 2.25 PF nominal)
+    f4peak = 2.0 * tpeak
+    f4peak_src = tpeak_src.replace("2 x measured", "4 x measured").replace(
+        "B200 dense int8 = 2 x dense bf16", "B200 dense fp4 = 4 x dense bf16")
     names = {"k1_tc": "gf_mad_tc_kernel (K1, tcgen05.mma kind::i8)",
+             "k1_f4": "gf_mad_f4_kernel (K1f, tcgen05.mma kind::mxf4, E2M1 residues, fp32 sums)",
              "k1_simt": "mad_smallk / mad_simt (K1 SIMT, K < 32)",
              "ech_gf2": "ech_gf2_cluster_kernel (K2, GF(2) 8-CTA cluster ECH)",
              "ech_panel": "ech_step_chain / ech_step_update / ech_panel (K2, general p)",
-             "select": "select2d_v16 / select_rows_v16 / select_inline (K3/K4 gathers, riffles)"}
+             "select": "select2d_v16 / select_rows_v16 / select_inline (K3/K4 gathers, riffles) + "
+                       "pack_rows_f4 / pack_cols_f4 (K1f operand packing)"}
     traffic = load_traffic(args.config)
     step_ms = sum(prof_ms) / max(1, len(prof_ms))
     roofs = []
@@ -440,7 +447,7 @@ def main():
             continue
         tensor = fam.startswith("k1")
         ach = wk / (ums / 1e3) / (1e12 if tensor else 1e9)
-        peak = tpeak if tensor else hpeak
+        peak = (f4peak if fam == "k1_f4" else tpeak) if tensor else hpeak
         tr = traffic.get(fam)
         nsteps = max(1, args.steps)
         roofs.append({"kernel": names.get(fam, fam), "family": fam, "bound": "tensor" if tensor else "hbm",
@@ -448,7 +455,7 @@ def main():
                       "frac": ach / peak, "traffic": tr["dram_bytes"] if tr else None,
                       "traffic_shape": tr["shape"] if tr else None,
                       "traffic_algorithmic": tr["algorithmic_bytes"] if tr else None,
-                      "peak_source": tpeak_src if tensor else hpeak_src,
+                      "peak_source": (f4peak_src if fam == "k1_f4" else tpeak_src) if tensor else hpeak_src,
                       "work_per_launch": wk / nl, "work_unit": "int8 ops (2 x MACs)" if tensor else
                       "algorithmic bytes (u8 payload read + written, +4 B per index)",
                       "launches_per_step": nl / nsteps, "avg_launch_us": 1e3 * ms / nl,
@@ -472,6 +479,8 @@ def main():
     # launches: the block product and the step's dominant shape
     if rank == 0:
         roof["isolated"] = k1_isolated(G, cfg["p"], tpeak, dominant_shape(args.config))
+        if cfg["p"] in (2, 3, 5, 7):
+            roof["isolated_f4"] = k1_isolated(G, cfg["p"], f4peak, dominant_shape(args.config), policy=3)
 
     base = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:

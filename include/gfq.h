@@ -78,7 +78,8 @@ void gfq_bits_free(gfq_bits* b);
 int gfq_mad_raw(uint32_t p, int64_t m, int64_t n, int64_t k, const uint8_t* A, int64_t lda,
                 const uint8_t* B, int64_t ldb, const uint8_t* Cin, int64_t ldc, uint8_t* D,
                 int64_t ldd);
-/* K1 path policy: 0 auto, 1 SIMT only, 2 tcgen05 whenever TMA-legal. */
+/* K1 path policy: 0 auto, 1 SIMT only, 2 tcgen05 kind::i8 whenever TMA-legal,
+ * 3 the FP4 tcgen05 path (kind::mxf4, p in {2,3,5,7}) whenever legal. */
 int gfq_set_mad_policy(int policy);
 int gfq_mad_counters(int64_t* simt_launches, int64_t* tc_launches, int reset);
 /* K6: exact device replica of random_matrix / random_product_matrix

@@ -96,6 +96,12 @@ void field_mad(const FieldSpec& f, std::int64_t m, std::int64_t n, std::int64_t 
                const std::uint8_t* Cin, std::int64_t ldc, std::uint8_t* D, std::int64_t ldd,
                cudaStream_t s) {
   if (!f.is_ext()) {
+    // K1f (FP4 tensor cores) for the small fields: its packed operands live
+    // in a stream-ordered scratch block on this (the current) stream
+    if (s == cur_stream_raw() && dev::use_f4(f.p(), m, n, k)) {
+      DevBuf scratch{static_cast<std::size_t>(dev::mad_f4_scratch_bytes(m, n, k))};
+      if (dev::mad_f4(f.p(), m, n, k, A, lda, B, ldb, Cin, ldc, D, ldd, scratch.ptr, s)) return;
+    }
     dev::mad(f.p(), m, n, k, A, lda, B, ldb, Cin, ldc, D, ldd, s);
     return;
   }

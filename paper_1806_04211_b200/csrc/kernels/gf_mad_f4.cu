@@ -1,0 +1,449 @@
+// gf_mad_f4.cu -- K1f: the block multiply-accumulate D = Cin + A.B mod p for
+// the small primes p in {2, 3, 5, 7} on the FP4 tensor-core path
+// (tcgen05.mma kind::mxf4, block-scaled E2M1 operands, fp32 accumulators in
+// TMEM), which issues twice the multiply-adds per instruction of kind::i8
+// for the same 32 operand bytes.  Same contract as K1 (gf_mad_tc.cu), which
+// replaces the reference's scalar mul_add_kernel (src/matrix.cpp:81-133).
+//
+// Exactness.  Every residue is encoded as the E2M1 value of its symmetric
+// representative s in [-(p-1)/2, (p-1)/2] (p = 2: 0 / 1), which is exact for
+// |s| <= 3 (E2M1 holds 0, 0.5, 1, 1.5, 2, 3, 4, 6).  The block scales are all
+// 2^0 (UE8M0 127), so each product s_a.s_b is an integer with |.| <= 9 and the
+// fp32 accumulator holds the exact integer sum while |sum| <= 9.k < 2^24; the
+// host keeps k below that per launch (k <= 1.8M, never reached by the
+// Chief).  The epilogue rounds the accumulator to an int32 (exact), adds a
+// multiple of p that makes it non-negative, the addend, and reduces mod p.
+//
+// Operand layout.  kind::mxf4 reads both operands K-major with two E2M1
+// values per byte, so each contraction first packs A (m x k -> m x kp/2
+// bytes) and transposes + packs B (k x n -> n x kp/2 bytes), kp = k rounded
+// up to 64, zero padded; pack kernels below (HBM-bound, 1.5 B moved per
+// element).  The MMA kernel then mirrors K1: 128 x 192 tiles, K-block 128
+// bytes (256 elements) per stage, 5-stage TMA ring (SWIZZLE_128B, both
+// operands K-major), one MMA-issuing thread, fp32 accumulators
+// double-buffered in TMEM (2 x 192 columns) and released once in registers,
+// the scale factors (all 0x7F) planted once per CTA in 32 further TMEM
+// columns, 8 epilogue warps.  192 rather than 256 columns because 2 x 256
+// accumulator columns would leave no TMEM for the scale factors.
+#include <cuda.h>
+
+#include <algorithm>
+#include <atomic>
+#include <cstdlib>
+#include <mutex>
+#include <vector>
+
+#include "../common.hpp"
+#include "kernels.hpp"
+#include "tc_ptx.cuh"
+
+namespace gfq::dev {
+namespace f4 {
+using namespace tc;
+
+constexpr int BM = 128, BN = 192, BKB = 128;  // BKB: packed bytes of K per stage (256 elements)
+constexpr int A_STAGE = BM * BKB;             // 16 KB
+constexpr int B_STAGE = BN * BKB;             // 24 KB
+constexpr int STAGE_BYTES = A_STAGE + B_STAGE;
+constexpr int STAGES = 5;
+constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 + 256;
+constexpr int EPI_WARPS = 8;
+constexpr int NUM_THREADS = 64 + 32 * EPI_WARPS;
+constexpr int TMEM_COLS = 512;
+constexpr int SF_COL = 2 * BN;       // 384: scale factors of A (16 columns), then of B (16)
+// kind::mxf4 instruction descriptor: A = B = E2M1 (MXF4 format 1, bits 7-9
+// and 10-12), both K-major, N >> 3 at bit 17, scale format UE8M0 (bit 23),
+// M >> 4 at bit 24, scale-factor ids 0, dense K = 64.
+constexpr std::uint32_t IDESC = (1u << 7) | (1u << 10) | ((std::uint32_t(BN) >> 3) << 17) | (1u << 23) |
+                                ((std::uint32_t(BM) >> 4) << 24);
+
+__device__ __forceinline__ void mma_f4(std::uint32_t d_tmem, std::uint64_t adesc, std::uint64_t bdesc,
+                                       std::uint32_t idesc, std::uint32_t accumulate, std::uint32_t sfa,
+                                       std::uint32_t sfb) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::mxf4.block_scale.block32 [%0], %1, %2, %3, [%5], [%6], p;\n\t}" ::"r"(
+          d_tmem),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate), "r"(sfa), "r"(sfb));
+}
+
+__device__ __forceinline__ void tmem_st32_const(std::uint32_t taddr, std::uint32_t x) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], "
+      "{%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,"
+      "%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1};" ::"r"(taddr),
+      "r"(x));
+  asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+}
+
+__global__ void __launch_bounds__(NUM_THREADS, 1)
+gf_mad_f4_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, int m,
+                 int n, int kpb, std::uint32_t p, std::uint32_t magic, std::uint32_t bias,
+                 const std::uint8_t* Cin, std::int64_t ldc, std::uint8_t* D, std::int64_t ldd, int gm) {
+  pdl_wait();
+  extern __shared__ __align__(1024) std::uint8_t smem_raw[];
+  std::uint8_t* smem = reinterpret_cast<std::uint8_t*>(
+      (reinterpret_cast<std::uintptr_t>(smem_raw) + 1023) & ~std::uintptr_t(1023));
+  std::uint8_t* sA = smem;
+  std::uint8_t* sB = smem + STAGES * A_STAGE;
+  std::uint64_t* bars = reinterpret_cast<std::uint64_t*>(smem + STAGES * STAGE_BYTES);
+  std::uint64_t* full = bars;
+  std::uint64_t* empty = bars + STAGES;
+  std::uint64_t* tfull = bars + 2 * STAGES;
+  std::uint64_t* tempty = bars + 2 * STAGES + 2;
+  std::uint32_t* tmem_slot = reinterpret_cast<std::uint32_t*>(bars + 2 * STAGES + 4);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int num_m = (m + BM - 1) / BM, num_n = (n + BN - 1) / BN;
+  const int num_tiles = num_m * num_n;
+  const int num_kb = (kpb + BKB - 1) / BKB;
+
+  if (warp == 0 && lane == 0) {
+    prefetch_tmap(&tmA);
+    prefetch_tmap(&tmB);
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(&tfull[a], 1);
+      mbar_init(&tempty[a], EPI_WARPS);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                 "r"(TMEM_COLS));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  fence_before();
+  __syncthreads();
+  fence_after();
+  const std::uint32_t tmem_base = *tmem_slot;
+  // plant the scale factors: every byte of TMEM columns [SF_COL, SF_COL+32)
+  // = UE8M0 127 (2^0), whatever lanes / bytes the MMA reads them from
+  if (warp >= 2 && warp < 6) {
+    const int quarter = warp & 3;
+    tmem_st32_const(tmem_base + (std::uint32_t(quarter * 32) << 16) + std::uint32_t(SF_COL), 0x7F7F7F7Fu);
+  }
+  fence_before();
+  __syncthreads();
+  fence_after();
+  const std::uint32_t sfa = tmem_base + std::uint32_t(SF_COL);
+  const std::uint32_t sfb = tmem_base + std::uint32_t(SF_COL + 16);
+
+  if (warp == 0) {
+    if (lane == 0) {
+      int stage = 0;
+      std::uint32_t phase = 0;
+      for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
+        int mb, nb;
+        tile_coords(tile, num_m, num_n, gm, mb, nb);
+        for (int kb = 0; kb < num_kb; ++kb) {
+          mbar_wait(&empty[stage], phase ^ 1);
+          mbar_arrive_expect_tx(&full[stage], STAGE_BYTES);
+          tma_load_2d(&tmA, &full[stage], sA + stage * A_STAGE, kb * BKB, mb * BM);
+          tma_load_2d(&tmB, &full[stage], sB + stage * B_STAGE, kb * BKB, nb * BN);
+          if (++stage == STAGES) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      int stage = 0;
+      std::uint32_t phase = 0;
+      int it = 0;
+      for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++it) {
+        const int acc = it & 1;
+        const std::uint32_t acc_phase = (it >> 1) & 1;
+        mbar_wait(&tempty[acc], acc_phase ^ 1);
+        fence_after();
+        const std::uint32_t d_tmem = tmem_base + std::uint32_t(acc * BN);
+        for (int kb = 0; kb < num_kb; ++kb) {
+          mbar_wait(&full[stage], phase);
+          fence_after();
+          const std::uint32_t a0 = smem_u32(sA + stage * A_STAGE);
+          const std::uint32_t b0 = smem_u32(sB + stage * B_STAGE);
+#pragma unroll
+          for (int kk = 0; kk < BKB / 32; ++kk) {
+            // both operands K-major SW128: 32 bytes (64 E2M1 values) per MMA
+            const std::uint64_t ad = umma_desc(a0 + kk * 32, 16, 1024);
+            const std::uint64_t bd = umma_desc(b0 + kk * 32, 16, 1024);
+            mma_f4(d_tmem, ad, bd, IDESC, (kb | kk) != 0, sfa, sfb);
+          }
+          mma_commit(&empty[stage]);
+          if (++stage == STAGES) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+        mma_commit(&tfull[acc]);
+      }
+    }
+  } else {
+    // epilogue: warp w reads TMEM lane quarter w % 4 and one half (96
+    // columns) of the tile
+    constexpr int HALF = BN / 2, CHUNKS = HALF / 32;
+    const int quarter = warp & 3;
+    const int half = (warp - 2) >> 2;
+    const int row_in_tile = quarter * 32 + lane;
+    const bool p2 = p == 2;
+    int it = 0;
+    for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++it) {
+      int mb, nb;
+      tile_coords(tile, num_m, num_n, gm, mb, nb);
+      const int acc = it & 1;
+      const std::uint32_t acc_phase = (it >> 1) & 1;
+      const int row = mb * BM + row_in_tile;
+      const bool row_ok = row < m;
+      const int cbase = nb * BN + half * HALF;
+      const std::uint8_t* crow = (Cin && row_ok) ? Cin + std::int64_t(row) * ldc : nullptr;
+      std::uint8_t* drow = row_ok ? D + std::int64_t(row) * ldd : nullptr;
+      const bool vec = row_ok && cbase + HALF <= n &&
+                       (reinterpret_cast<std::uintptr_t>(drow + cbase) & 15) == 0 &&
+                       (!crow || (reinterpret_cast<std::uintptr_t>(crow + cbase) & 15) == 0);
+      uint4 cpre[HALF / 16];
+#pragma unroll
+      for (int q = 0; q < HALF / 16; ++q) cpre[q] = make_uint4(0, 0, 0, 0);
+      if (vec && crow) {
+#pragma unroll
+        for (int q = 0; q < HALF / 16; ++q) cpre[q] = reinterpret_cast<const uint4*>(crow + cbase)[q];
+      }
+      mbar_wait(&tfull[acc], acc_phase);
+      fence_after();
+#pragma unroll
+      for (int ch = 0; ch < CHUNKS; ++ch) {
+        std::uint32_t v[32];
+        const std::uint32_t taddr =
+            tmem_base + (std::uint32_t(quarter * 32) << 16) + std::uint32_t(acc * BN + half * HALF + ch * 32);
+        tmem_ld32(taddr, v);
+        if (ch == CHUNKS - 1) {
+          fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&tempty[acc]);
+        }
+        // the exact integer sums (fp32 -> int32 is exact below 2^24), made
+        // non-negative by `bias` (a multiple of p; 0 for p = 2)
+#pragma unroll
+        for (int c = 0; c < 32; ++c) v[c] = std::uint32_t(__float2int_rn(__uint_as_float(v[c]))) + bias;
+        const int col0 = cbase + ch * 32;
+        if (vec) {
+          const std::uint32_t cw[8] = {cpre[2 * ch].x,     cpre[2 * ch].y,     cpre[2 * ch].z,
+                                       cpre[2 * ch].w,     cpre[2 * ch + 1].x, cpre[2 * ch + 1].y,
+                                       cpre[2 * ch + 1].z, cpre[2 * ch + 1].w};
+          std::uint32_t ow[8];
+          if (p2) {
+#pragma unroll
+            for (int w = 0; w < 8; ++w)
+              ow[w] = (pack_low_bytes(v[4 * w], v[4 * w + 1], v[4 * w + 2], v[4 * w + 3]) ^ cw[w]) & 0x01010101u;
+          } else {
+#pragma unroll
+            for (int w = 0; w < 8; ++w) {
+              std::uint32_t r[4];
+#pragma unroll
+              for (int b = 0; b < 4; ++b) r[b] = modp(v[4 * w + b] + __byte_perm(cw[w], 0, 0x4440 + b), p, magic);
+              ow[w] = pack_low_bytes(r[0], r[1], r[2], r[3]);
+            }
+          }
+          reinterpret_cast<uint4*>(drow + col0)[0] = make_uint4(ow[0], ow[1], ow[2], ow[3]);
+          reinterpret_cast<uint4*>(drow + col0)[1] = make_uint4(ow[4], ow[5], ow[6], ow[7]);
+        } else if (row_ok) {
+#pragma unroll
+          for (int c = 0; c < 32; ++c) {
+            if (col0 + c < n) {
+              std::uint32_t x = v[c];
+              if (crow) x += crow[col0 + c];
+              drow[col0 + c] = static_cast<std::uint8_t>(modp(x, p, magic));
+            }
+          }
+        }
+      }
+    }
+  }
+
+  fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(TMEM_COLS));
+  }
+}
+
+// E2M1 codes of the residues 0..7 as nibbles of one word: residue v maps to
+// its symmetric representative s (v <= (p-1)/2 ? v : v - p), encoded as
+// sign bit 3 | magnitude code (0 -> 0, 1 -> 2, 2 -> 4, 3 -> 5).
+__host__ __device__ constexpr std::uint32_t e2m1_of_mag(std::uint32_t a) {
+  return a == 0 ? 0u : a == 1 ? 2u : a == 2 ? 4u : 5u;
+}
+std::uint32_t code_word(std::uint32_t p) {
+  std::uint32_t w = 0;
+  for (std::uint32_t v = 0; v < p && v < 8; ++v) {
+    const bool neg = p > 2 && v > (p - 1) / 2;
+    const std::uint32_t mag = neg ? p - v : v;
+    w |= ((neg ? 8u : 0u) | e2m1_of_mag(mag)) << (4 * v);
+  }
+  return w;
+}
+
+// two residue bytes -> one byte of two E2M1 codes (element 2j low nibble)
+__device__ __forceinline__ std::uint32_t pack4(std::uint32_t x, std::uint32_t codes) {
+  // x holds 4 residues (bytes); returns 2 packed bytes in the low 16 bits
+  const std::uint32_t c0 = (codes >> (4 * (x & 0xFF))) & 0xF;
+  const std::uint32_t c1 = (codes >> (4 * ((x >> 8) & 0xFF))) & 0xF;
+  const std::uint32_t c2 = (codes >> (4 * ((x >> 16) & 0xFF))) & 0xF;
+  const std::uint32_t c3 = (codes >> (4 * (x >> 24))) & 0xF;
+  return c0 | (c1 << 4) | (c2 << 8) | (c3 << 12);
+}
+
+// A (m x k residues, row-major) -> Ap (m x kpb bytes): one thread per 32
+// elements (16 output bytes), columns >= k zero.
+__global__ void __launch_bounds__(256) pack_rows_f4_kernel(const std::uint8_t* A, std::int64_t lda, int m, int k,
+                                                           std::uint8_t* out, int kpb, std::uint32_t codes) {
+  pdl_wait_and_release();
+  const int per_row = kpb / 16;
+  const std::int64_t total = std::int64_t(m) * per_row;
+  const bool al = ((reinterpret_cast<std::uintptr_t>(A) | std::uintptr_t(lda)) & 15) == 0;
+  for (std::int64_t t = std::int64_t(blockIdx.x) * blockDim.x + threadIdx.x; t < total;
+       t += std::int64_t(gridDim.x) * blockDim.x) {
+    const int r = int(t / per_row), q = int(t - std::int64_t(r) * per_row);
+    const int c0 = q * 32;
+    const std::uint8_t* src = A + std::int64_t(r) * lda;
+    std::uint32_t w[8];
+    if (al && c0 + 32 <= k) {
+      const uint4 lo = reinterpret_cast<const uint4*>(src + c0)[0];
+      const uint4 hi = reinterpret_cast<const uint4*>(src + c0)[1];
+      w[0] = lo.x; w[1] = lo.y; w[2] = lo.z; w[3] = lo.w;
+      w[4] = hi.x; w[5] = hi.y; w[6] = hi.z; w[7] = hi.w;
+    } else {
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        std::uint32_t x = 0;
+#pragma unroll
+        for (int b = 0; b < 4; ++b) {
+          const int c = c0 + 4 * u + b;
+          if (c < k) x |= std::uint32_t(src[c]) << (8 * b);
+        }
+        w[u] = x;
+      }
+    }
+    // residue 0 codes to 0, so the zero padding packs to zero bytes
+    uint4 o;
+    o.x = pack4(w[0], codes) | (pack4(w[1], codes) << 16);
+    o.y = pack4(w[2], codes) | (pack4(w[3], codes) << 16);
+    o.z = pack4(w[4], codes) | (pack4(w[5], codes) << 16);
+    o.w = pack4(w[6], codes) | (pack4(w[7], codes) << 16);
+    reinterpret_cast<uint4*>(out + std::int64_t(r) * kpb)[q] = o;
+  }
+}
+
+// B (k x n residues, row-major) -> Bt (n x kpb bytes, K-major): a CTA packs a
+// 64 (k) x 256 (n) tile through shared memory; thread j writes the 32 bytes
+// of column j's 64 codes.
+__global__ void __launch_bounds__(256) pack_cols_f4_kernel(const std::uint8_t* B, std::int64_t ldb, int k, int n,
+                                                           std::uint8_t* out, int kpb, std::uint32_t codes) {
+  pdl_wait_and_release();
+  __shared__ __align__(16) std::uint8_t tile[64][256 + 16];
+  const int n0 = blockIdx.x * 256, k0 = blockIdx.y * 64;
+  const bool al = ((reinterpret_cast<std::uintptr_t>(B) | std::uintptr_t(ldb)) & 15) == 0;
+  // load: 64 rows x 16 uint4 = 1024 vectors, 4 per thread
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    const int v = threadIdx.x + 256 * q;
+    const int r = v >> 4, c = (v & 15) * 16;
+    const int kr = k0 + r, nc = n0 + c;
+    uint4 x = make_uint4(0, 0, 0, 0);
+    if (kr < k) {
+      const std::uint8_t* src = B + std::int64_t(kr) * ldb + nc;
+      if (al && nc + 16 <= n) {
+        x = *reinterpret_cast<const uint4*>(src);
+      } else {
+        std::uint32_t w[4] = {0, 0, 0, 0};
+        for (int b = 0; b < 16; ++b)
+          if (nc + b < n) w[b >> 2] |= std::uint32_t(src[b]) << (8 * (b & 3));
+        x = make_uint4(w[0], w[1], w[2], w[3]);
+      }
+    }
+    *reinterpret_cast<uint4*>(&tile[r][c]) = x;
+  }
+  __syncthreads();
+  const int j = n0 + threadIdx.x;
+  if (j >= n) return;
+  std::uint32_t o[8];
+#pragma unroll
+  for (int u = 0; u < 8; ++u) {
+    std::uint32_t x = 0;
+#pragma unroll
+    for (int b = 0; b < 8; ++b) x |= ((codes >> (4 * tile[8 * u + b][threadIdx.x])) & 0xF) << (4 * b);
+    o[u] = x;
+  }
+  uint4* dst = reinterpret_cast<uint4*>(out + std::int64_t(j) * kpb + k0 / 2);
+  dst[0] = make_uint4(o[0], o[1], o[2], o[3]);
+  dst[1] = make_uint4(o[4], o[5], o[6], o[7]);
+}
+
+}  // namespace f4
+
+bool f4_field(std::uint32_t p) { return p == 2 || p == 3 || p == 5 || p == 7; }
+
+std::int64_t mad_f4_scratch_bytes(std::int64_t m, std::int64_t n, std::int64_t k) {
+  const std::int64_t kpb = (k + 63) / 64 * 32;
+  return (m + n) * kpb + 256;
+}
+
+bool mad_f4(std::uint32_t p, std::int64_t m, std::int64_t n, std::int64_t k, const std::uint8_t* A,
+            std::int64_t lda, const std::uint8_t* B, std::int64_t ldb, const std::uint8_t* Cin, std::int64_t ldc,
+            std::uint8_t* D, std::int64_t ldd, std::uint8_t* scratch, cudaStream_t s) {
+  using namespace f4;
+  if (!f4_field(p) || m <= 0 || n <= 0 || k <= 0) return false;
+  // |sum| <= h^2 k must stay below 2^24 (h = (p-1)/2, 1 for p = 2)
+  const std::int64_t h = p == 2 ? 1 : (p - 1) / 2;
+  if (h * h * k >= (std::int64_t(1) << 24) || m >= (1LL << 31) || n >= (1LL << 31)) return false;
+  if ((reinterpret_cast<std::uintptr_t>(scratch) & 15) != 0) return false;
+  static std::once_flag attr_once;
+  std::call_once(attr_once, [] {
+    GFQ_CUDA(cudaFuncSetAttribute(gf_mad_f4_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES));
+  });
+  const std::int64_t kpb = (k + 63) / 64 * 32;
+  std::uint8_t* Ap = scratch;
+  std::uint8_t* Bt = scratch + (m * kpb + 127) / 128 * 128;
+  CUtensorMap mA, mB;
+  if (!make_map_box(&mA, Ap, kpb, m, kpb, BKB, BM)) return false;
+  if (!make_map_box(&mB, Bt, kpb, n, kpb, BKB, BN)) return false;
+  const std::uint32_t codes = code_word(p);
+  {
+    ProfScope ps(kProfSelect, double(m) * double(k) * 1.5, s);
+    const std::int64_t total = m * (kpb / 16);
+    const std::int64_t cap = std::int64_t(sm_count()) * 8;
+    const unsigned grid = unsigned(std::min<std::int64_t>((total + 255) / 256, cap));
+    GFQ_CUDA(launch_pdl(pack_rows_f4_kernel, dim3(grid), dim3(256), 0, s, A, lda, int(m), int(k), Ap, int(kpb),
+                        codes));
+    count_launch();
+  }
+  {
+    ProfScope ps(kProfSelect, double(n) * double(k) * 1.5, s);
+    GFQ_CUDA(launch_pdl(pack_cols_f4_kernel, dim3(unsigned((n + 255) / 256), unsigned(kpb / 32)), dim3(256), 0, s,
+                      B, ldb, int(k), int(n), Bt, int(kpb), codes));
+    count_launch();
+  }
+  const std::int64_t sms = sm_count();
+  const std::int64_t num_m = (m + BM - 1) / BM, tiles = num_m * ((n + BN - 1) / BN);
+  const int grid = int(tiles < sms ? tiles : sms);
+  // raster group: the A slice of gm M-tiles within ~32 MB
+  const std::int64_t gm = std::max<std::int64_t>(
+      1, std::min<std::int64_t>(num_m, (std::int64_t(32) << 20) / (std::int64_t(BM) * kpb)));
+  const std::uint32_t magic = static_cast<std::uint32_t>((0x100000000ULL / p) + 1);
+  const std::uint32_t bias = p == 2 ? 0u : std::uint32_t((h * h * k + p - 1) / p * p);
+  ProfScope ps(kProfF4, 2.0 * double(m) * double(n) * double(k), s);
+  GFQ_CUDA(launch_pdl(gf_mad_f4_kernel, dim3(grid), dim3(NUM_THREADS), SMEM_BYTES, s, mA, mB, int(m), int(n),
+                      int(kpb), p, magic, bias, Cin, ldc, D, ldd, int(gm)));
+  GFQ_CUDA(cudaGetLastError());
+  count_launch();
+  return true;
+}
+
+}  // namespace gfq::dev

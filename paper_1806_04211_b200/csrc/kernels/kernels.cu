@@ -338,6 +338,21 @@ void profile_take(std::int64_t launches[2], double ops[2], double ms[2]) {
 }
 
 void set_mad_policy(int policy) { g_policy = policy; }
+// K1f dispatch: small fields, tiles that fill the 128 x 192 grid, and
+// enough work that the two packing passes (1.5 B per operand element) stay
+// small next to the contraction; GFQ_NO_F4 keeps every product on kind::i8.
+bool use_f4(std::uint32_t p, std::int64_t m, std::int64_t n, std::int64_t k) {
+  static const bool off = std::getenv("GFQ_NO_F4") != nullptr;
+  static const double min_work = [] {
+    const char* e = std::getenv("GFQ_F4_MIN_MACS");
+    return e ? std::atof(e) : 1.0e11;
+  }();
+  const int pol = g_policy;
+  if (!f4_field(p) || pol == 1 || pol == 2 || m <= 0 || n <= 0 || k <= 0) return false;
+  if (pol == 3) return true;
+  if (off) return false;
+  return m >= 128 && n >= 192 && k >= 128 && double(m) * double(n) * double(k) >= min_work;
+}
 int mad_policy() { return g_policy; }
 void mad_counters(std::int64_t* simt, std::int64_t* tc) {
   *simt = g_simt;

@@ -79,6 +79,19 @@ bool mad_tc(std::uint32_t p, std::int64_t m, std::int64_t n, std::int64_t k,
             std::int64_t ldb, const std::uint8_t* Cin, std::int64_t ldc,
             std::uint8_t* D, std::int64_t ldd, cudaStream_t s);
 
+// K1f: the same contraction on the FP4 tensor cores (tcgen05.mma kind::mxf4,
+// gf_mad_f4.cu) for p in {2, 3, 5, 7}: the residues as E2M1 values of their
+// symmetric representatives, exact fp32 sums.  `scratch` holds the packed
+// operands (mad_f4_scratch_bytes, 16-byte aligned, stream-ordered on s).
+// Returns false (launching nothing) for other p or a k beyond the exact
+// range.  use_f4 is the dispatch rule (policy, field, size).
+bool f4_field(std::uint32_t p);
+bool use_f4(std::uint32_t p, std::int64_t m, std::int64_t n, std::int64_t k);
+std::int64_t mad_f4_scratch_bytes(std::int64_t m, std::int64_t n, std::int64_t k);
+bool mad_f4(std::uint32_t p, std::int64_t m, std::int64_t n, std::int64_t k, const std::uint8_t* A,
+            std::int64_t lda, const std::uint8_t* B, std::int64_t ldb, const std::uint8_t* Cin, std::int64_t ldc,
+            std::uint8_t* D, std::int64_t ldd, std::uint8_t* scratch, cudaStream_t s);
+
 // ---------------------------------------------------------------- accounting
 // Every kernel launch of this library bumps a counter (bench.py's
 // gpu_launches).  With profiling on, each K1 launch is bracketed by CUDA
@@ -99,7 +112,8 @@ enum ProfKind : int {
   kProfEchGf2 = 2,   // GF(2) cluster / small ECH kernels (bytes)
   kProfEchPanel = 3, // general-p panel / step ECH kernels (bytes)
   kProfSelect = 4,   // row / column gathers, riffles      (bytes)
-  kProfKinds = 5
+  kProfF4 = 5,       // K1f FP4 tcgen05 contraction        (ops)
+  kProfKinds = 6
 };
 // Brackets the launches issued in its scope with CUDA events on `s` when
 // profiling is on (a no-op otherwise).
@@ -124,7 +138,8 @@ void profile_take_kinds(int n, std::int64_t* launches, double* work, double* ms,
 // landed, 3 MMAs issued, 4 first accumulator ready, 5 epilogue done, 6 exit).
 void tc_debug_take(unsigned long long* host);
 
-// Selects which path `mad` uses: 0 = auto, 1 = SIMT only, 2 = tcgen05 whenever legal.
+// Selects which path `mad` uses: 0 = auto, 1 = SIMT only, 2 = tcgen05 kind::i8
+// whenever legal, 3 = the FP4 path (K1f) whenever legal (else as 2).
 void set_mad_policy(int policy);
 int mad_policy();
 // Counters of K1 launches by path since the last reset (host-side).

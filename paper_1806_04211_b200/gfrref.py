@@ -998,7 +998,7 @@ def device_memory(reset_peak: bool = False) -> dict:
     return {"live": live.value, "peak": peak.value, "pool_reserved_high": res.value}
 
 
-PROFILE_KINDS = ("k1_tc", "k1_simt", "ech_gf2", "ech_panel", "select")
+PROFILE_KINDS = ("k1_tc", "k1_simt", "ech_gf2", "ech_panel", "select", "k1_f4")
 
 
 def profile_take_kinds(with_union: bool = False):

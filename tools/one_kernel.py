@@ -2,6 +2,7 @@
 bench's dominant shapes (profiles/r02_traffic.json):
 
   python tools/one_kernel.py mad P M N K [reps]     K1: D = D + A.B (in place, like the step)
+  python tools/one_kernel.py mad4 P M N K [reps]    the same on K1f (FP4 path, p in {2,3,5,7})
   python tools/one_kernel.py crz ROWS COLS ZEROS    column riffle with zero columns (K4 gather)
   python tools/one_kernel.py ech2 N                 GF(2) cluster ECH of an N x N block
 
@@ -16,14 +17,14 @@ from paper_1806_04211_b200 import gfrref as G  # noqa: E402
 
 mode = sys.argv[1]
 G.lib()
-if mode == "mad":
+if mode in ("mad", "mad4"):
     import torch
     p, m, n, k = (int(x) for x in sys.argv[2:6])
     reps = int(sys.argv[6]) if len(sys.argv) > 6 else 4
     A = torch.randint(0, p, (m, k), dtype=torch.uint8, device="cuda")
     B = torch.randint(0, p, (k, n), dtype=torch.uint8, device="cuda")
     D = torch.randint(0, p, (m, n), dtype=torch.uint8, device="cuda")
-    G.set_mad_policy(2)
+    G.set_mad_policy(2 if mode == "mad" else 3)
     G.set_stream(torch.cuda.current_stream().cuda_stream)
     for _ in range(reps):
         G.mad_raw(p, m, n, k, A.data_ptr(), k, B.data_ptr(), n, D.data_ptr(), n, D.data_ptr(), n)

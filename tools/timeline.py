@@ -5,7 +5,7 @@ which kernel families ran; K1-idle stretches and what ran during them.
 import sys
 from collections import defaultdict
 
-NAMES = ["k1_tc", "k1_simt", "ech_gf2", "ech_panel", "select"]
+NAMES = ["k1_tc", "k1_simt", "ech_gf2", "ech_panel", "select", "k1_f4"]
 rows = [l.split() for l in open(sys.argv[1]) if l.strip()]
 iv = defaultdict(list)
 for f, a, b in rows:
