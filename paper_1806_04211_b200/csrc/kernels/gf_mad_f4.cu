@@ -31,6 +31,7 @@
 #include <atomic>
 #include <cstdlib>
 #include <mutex>
+#include <stdexcept>
 #include <vector>
 
 #include "../common.hpp"
@@ -341,49 +342,74 @@ __global__ void __launch_bounds__(256) pack_rows_f4_kernel(const std::uint8_t* A
   }
 }
 
-// B (k x n residues, row-major) -> Bt (n x kpb bytes, K-major): a CTA packs a
-// 64 (k) x 256 (n) tile through shared memory; thread j writes the 32 bytes
-// of column j's 64 codes.
+// B (k x n residues, row-major) -> Bt (n x kpb bytes, K-major): a CTA packs
+// a 128 (k) x 512 (n) tile staged in shared memory (16 coalesced 16-byte
+// loads a thread, all in flight together); thread t then reads 4 adjacent
+// columns (one 32-bit word a row: a warp covers 128 consecutive bytes, no
+// bank conflicts) over 64 rows and writes each column's 64 codes as one
+// 32-byte sector.
+constexpr int PC_K = 128, PC_N = 512, PC_LD = PC_N + 16;
+constexpr int PC_SMEM = PC_K * PC_LD;
 __global__ void __launch_bounds__(256) pack_cols_f4_kernel(const std::uint8_t* B, std::int64_t ldb, int k, int n,
                                                            std::uint8_t* out, int kpb, std::uint32_t codes) {
   pdl_wait_and_release();
-  __shared__ __align__(16) std::uint8_t tile[64][256 + 16];
-  const int n0 = blockIdx.x * 256, k0 = blockIdx.y * 64;
+  extern __shared__ __align__(16) std::uint8_t tile[];
+  const int n0 = blockIdx.x * PC_N, k0 = blockIdx.y * PC_K;
   const bool al = ((reinterpret_cast<std::uintptr_t>(B) | std::uintptr_t(ldb)) & 15) == 0;
-  // load: 64 rows x 16 uint4 = 1024 vectors, 4 per thread
+  uint4 x[16];
 #pragma unroll
-  for (int q = 0; q < 4; ++q) {
-    const int v = threadIdx.x + 256 * q;
-    const int r = v >> 4, c = (v & 15) * 16;
+  for (int q = 0; q < 16; ++q) {
+    const int v = threadIdx.x + 256 * q;  // 128 rows x 32 vectors
+    const int r = v >> 5, c = (v & 31) * 16;
     const int kr = k0 + r, nc = n0 + c;
-    uint4 x = make_uint4(0, 0, 0, 0);
+    x[q] = make_uint4(0, 0, 0, 0);
     if (kr < k) {
       const std::uint8_t* src = B + std::int64_t(kr) * ldb + nc;
       if (al && nc + 16 <= n) {
-        x = *reinterpret_cast<const uint4*>(src);
+        x[q] = *reinterpret_cast<const uint4*>(src);
       } else {
         std::uint32_t w[4] = {0, 0, 0, 0};
         for (int b = 0; b < 16; ++b)
           if (nc + b < n) w[b >> 2] |= std::uint32_t(src[b]) << (8 * (b & 3));
-        x = make_uint4(w[0], w[1], w[2], w[3]);
+        x[q] = make_uint4(w[0], w[1], w[2], w[3]);
       }
     }
-    *reinterpret_cast<uint4*>(&tile[r][c]) = x;
+  }
+#pragma unroll
+  for (int q = 0; q < 16; ++q) {
+    const int v = threadIdx.x + 256 * q;
+    *reinterpret_cast<uint4*>(tile + (v >> 5) * PC_LD + (v & 31) * 16) = x[q];
   }
   __syncthreads();
-  const int j = n0 + threadIdx.x;
-  if (j >= n) return;
-  std::uint32_t o[8];
+  const int cg = threadIdx.x & 127, rh = threadIdx.x >> 7;  // 4 columns, 64 rows
+  const int j0 = n0 + 4 * cg;
+  if (j0 >= n) return;
+  std::uint32_t o[4][8];
 #pragma unroll
   for (int u = 0; u < 8; ++u) {
-    std::uint32_t x = 0;
+    std::uint32_t a0 = 0, a1 = 0, a2 = 0, a3 = 0;
 #pragma unroll
-    for (int b = 0; b < 8; ++b) x |= ((codes >> (4 * tile[8 * u + b][threadIdx.x])) & 0xF) << (4 * b);
-    o[u] = x;
+    for (int b = 0; b < 8; ++b) {
+      const std::uint32_t w = *reinterpret_cast<const std::uint32_t*>(tile + (64 * rh + 8 * u + b) * PC_LD + 4 * cg);
+      a0 |= ((codes >> (4 * (w & 0xFF))) & 0xF) << (4 * b);
+      a1 |= ((codes >> (4 * ((w >> 8) & 0xFF))) & 0xF) << (4 * b);
+      a2 |= ((codes >> (4 * ((w >> 16) & 0xFF))) & 0xF) << (4 * b);
+      a3 |= ((codes >> (4 * (w >> 24))) & 0xF) << (4 * b);
+    }
+    o[0][u] = a0;
+    o[1][u] = a1;
+    o[2][u] = a2;
+    o[3][u] = a3;
   }
-  uint4* dst = reinterpret_cast<uint4*>(out + std::int64_t(j) * kpb + k0 / 2);
-  dst[0] = make_uint4(o[0], o[1], o[2], o[3]);
-  dst[1] = make_uint4(o[4], o[5], o[6], o[7]);
+  const int kb = (k0 + 64 * rh) / 2;  // byte offset of these 64 codes
+  if (kb >= kpb) return;
+#pragma unroll
+  for (int c = 0; c < 4; ++c) {
+    if (j0 + c >= n) break;
+    uint4* dst = reinterpret_cast<uint4*>(out + std::int64_t(j0 + c) * kpb + kb);
+    dst[0] = make_uint4(o[c][0], o[c][1], o[c][2], o[c][3]);
+    dst[1] = make_uint4(o[c][4], o[c][5], o[c][6], o[c][7]);
+  }
 }
 
 }  // namespace f4
@@ -407,6 +433,7 @@ bool mad_f4(std::uint32_t p, std::int64_t m, std::int64_t n, std::int64_t k, con
   static std::once_flag attr_once;
   std::call_once(attr_once, [] {
     GFQ_CUDA(cudaFuncSetAttribute(gf_mad_f4_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES));
+    GFQ_CUDA(cudaFuncSetAttribute(pack_cols_f4_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, PC_SMEM));
   });
   const std::int64_t kpb = (k + 63) / 64 * 32;
   std::uint8_t* Ap = scratch;
@@ -426,23 +453,39 @@ bool mad_f4(std::uint32_t p, std::int64_t m, std::int64_t n, std::int64_t k, con
   }
   {
     ProfScope ps(kProfSelect, double(n) * double(k) * 1.5, s);
-    GFQ_CUDA(launch_pdl(pack_cols_f4_kernel, dim3(unsigned((n + 255) / 256), unsigned(kpb / 32)), dim3(256), 0, s,
+    GFQ_CUDA(launch_pdl(pack_cols_f4_kernel, dim3(unsigned((n + PC_N - 1) / PC_N), unsigned((kpb + 63) / 64)),
+                        dim3(256), std::size_t(PC_SMEM), s,
                       B, ldb, int(k), int(n), Bt, int(kpb), codes));
     count_launch();
   }
-  const std::int64_t sms = sm_count();
-  const std::int64_t num_m = (m + BM - 1) / BM, tiles = num_m * ((n + BN - 1) / BN);
-  const int grid = int(tiles < sms ? tiles : sms);
-  // raster group: the A slice of gm M-tiles within ~32 MB
-  const std::int64_t gm = std::max<std::int64_t>(
-      1, std::min<std::int64_t>(num_m, (std::int64_t(32) << 20) / (std::int64_t(BM) * kpb)));
+  const std::int64_t sms = k1_sms(s);
+  const std::int64_t tiles_per_rowtile = (n + BN - 1) / BN;
+  // row pieces of <= GFQ_K1_MAX_WAVES tile waves each (see mad_tc)
+  static const std::int64_t max_waves = [] {
+    const char* e = std::getenv("GFQ_K1_MAX_WAVES");
+    return e ? std::int64_t(std::atoll(e)) : std::int64_t(0);
+  }();
+  std::int64_t mp = m;
+  if (max_waves > 0 && (m + BM - 1) / BM * tiles_per_rowtile > max_waves * sms)
+    mp = std::max<std::int64_t>(1, (max_waves * sms) / tiles_per_rowtile) * BM;
   const std::uint32_t magic = static_cast<std::uint32_t>((0x100000000ULL / p) + 1);
   const std::uint32_t bias = p == 2 ? 0u : std::uint32_t((h * h * k + p - 1) / p * p);
   ProfScope ps(kProfF4, 2.0 * double(m) * double(n) * double(k), s);
-  GFQ_CUDA(launch_pdl(gf_mad_f4_kernel, dim3(grid), dim3(NUM_THREADS), SMEM_BYTES, s, mA, mB, int(m), int(n),
-                      int(kpb), p, magic, bias, Cin, ldc, D, ldd, int(gm)));
-  GFQ_CUDA(cudaGetLastError());
-  count_launch();
+  K1Lane lane(s);
+  for (std::int64_t m0 = 0; m0 < m; m0 += mp) {
+    const std::int64_t mm = std::min(mp, m - m0);
+    CUtensorMap mA;
+    if (!make_map_box(&mA, Ap + m0 * kpb, kpb, mm, kpb, BKB, BM)) throw std::runtime_error("mad_f4: tensor map");
+    const std::int64_t num_m = (mm + BM - 1) / BM, tiles = num_m * tiles_per_rowtile;
+    const int grid = int(tiles < sms ? tiles : sms);
+    // raster group: the A slice of gm M-tiles within ~32 MB
+    const std::int64_t gm = std::max<std::int64_t>(
+        1, std::min<std::int64_t>(num_m, (std::int64_t(32) << 20) / (std::int64_t(BM) * kpb)));
+    GFQ_CUDA(launch_pdl(gf_mad_f4_kernel, dim3(grid), dim3(NUM_THREADS), SMEM_BYTES, s, mA, mB, int(mm), int(n),
+                        int(kpb), p, magic, bias, Cin ? Cin + m0 * ldc : nullptr, ldc, D + m0 * ldd, ldd, int(gm)));
+    GFQ_CUDA(cudaGetLastError());
+    count_launch();
+  }
   return true;
 }
 

@@ -384,7 +384,7 @@ bool mad_tc(std::uint32_t p, std::int64_t m, std::int64_t n, std::int64_t k,
   const std::uint32_t magic = static_cast<std::uint32_t>((0x100000000ULL / p) + 1);
   // N tile: 128 wide when that cuts the tile-waves enough (a 128-wide tile
   // costs ~0.55 of a 256-wide one: A is re-read and the MMA is narrower).
-  const std::int64_t sms = sm_count();
+  const std::int64_t sms = k1_sms(s);
   const std::int64_t mt = (m + BM - 1) / BM;
   const std::int64_t t256 = mt * ((n + 255) / 256), t128 = mt * ((n + 127) / 128);
   const bool narrow = 11 * ((t128 + sms - 1) / sms) < 18 * ((t256 + sms - 1) / sms);
@@ -434,6 +434,7 @@ bool mad_tc(std::uint32_t p, std::int64_t m, std::int64_t n, std::int64_t k,
     const std::int64_t v = e ? std::int64_t(std::atoll(e)) : 32;
     return v > 0 ? v : std::int64_t(1) << 20;  // <= 0: one group (plain M-fastest raster)
   }();
+  K1Lane lane(s);
   for (const Chunk& c : chunks) {
     const std::int64_t k0 = c.k0, kk = c.kk, m0 = c.m0;
     const CUtensorMap& mA = c.mA;

@@ -5,6 +5,7 @@
 //   K6 (counter-form SplitMix64 generator).
 // The tensor-core contraction lives in gf_mad_tc.cu.
 #include <cstdio>
+#include <cstring>
 #include <algorithm>
 #include <atomic>
 #include <mutex>
@@ -247,6 +248,7 @@ struct ProfRec {
   cudaEvent_t e0, e1;
   double ops;
   int path;
+  const char* task = nullptr;  // issuing task (developer dump)
 };
 std::mutex g_prof_mtx;
 std::vector<ProfRec> g_prof;
@@ -269,7 +271,7 @@ ProfScope::~ProfScope() {
   if (!e0_) return;
   cudaEventRecord(e1_, s_);
   std::lock_guard<std::mutex> lk(g_prof_mtx);
-  g_prof.push_back(ProfRec{e0_, e1_, work_, kind_});
+  g_prof.push_back(ProfRec{e0_, e1_, work_, kind_, hprof::t_task_name});
 }
 
 void profile_take_kinds(int n, std::int64_t* launches, double* work, double* ms, double* union_ms) {
@@ -306,6 +308,15 @@ void profile_take_kinds(int n, std::int64_t* launches, double* work, double* ms,
     if (FILE* fh = std::fopen(path, "a")) {
       for (int q = 0; q < n; ++q)
         for (const auto& [a, b] : iv[std::size_t(q)]) std::fprintf(fh, "%d %.4f %.4f\n", q, a, b);
+      // (GFQ_PROF_DUMP_TASKS: one line per launch with its issuing task)
+      if (std::getenv("GFQ_PROF_DUMP_TASKS"))
+        for (auto& r : recs) {
+          float t = 0, t0 = 0;
+          if (cudaEventElapsedTime(&t, r.e0, r.e1) == cudaSuccess &&
+              cudaEventElapsedTime(&t0, recs.front().e0, r.e0) == cudaSuccess)
+            std::fprintf(fh, "T %d %.4f %.4f %.1f %s\n", r.path, double(t0), double(t0) + double(t), r.ops,
+                         r.task ? r.task : "-");
+        }
       std::fclose(fh);
     }
   }
@@ -341,6 +352,66 @@ void set_mad_policy(int policy) { g_policy = policy; }
 // K1f dispatch: small fields, tiles that fill the 128 x 192 grid, and
 // enough work that the two packing passes (1.5 B per operand element) stay
 // small next to the contraction; GFQ_NO_F4 keeps every product on kind::i8.
+// Streams at the device's greatest priority carry the Step-1 critical path
+// (the executor's ClearDown / UpdateRow(i, j, j+1) stream).
+bool stream_is_critical(cudaStream_t s) {
+  static const int greatest = [] {
+    int lo = 0, hi = 0;
+    GFQ_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+    return hi;
+  }();
+  if (s == nullptr) return false;
+  int pr = 0;
+  if (cudaStreamGetPriority(s, &pr) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return pr == greatest && greatest != 0;
+}
+int k1_sms(cudaStream_t s) {
+  static const int reserve = [] {
+    const char* e = std::getenv("GFQ_K1_SM_RESERVE");
+    return e ? std::atoi(e) : 0;
+  }();
+  static const int crit = [] {
+    const char* e = std::getenv("GFQ_CRIT_GRID");
+    return e ? std::atoi(e) : 0;
+  }();
+  if (stream_is_critical(s))
+    return crit > 0 && std::strcmp(hprof::t_task_name, "ClearDown") == 0 ? std::min(crit, sm_count()) : sm_count();
+  if (reserve <= 0) return sm_count();
+  return std::max(1, sm_count() - reserve);
+}
+// The K1 lane (GFQ_K1_LANE=1): persistent contractions issued from
+// non-critical streams run one at a time (each waits for the previous one
+// on any stream), so together with GFQ_K1_SM_RESERVE they never occupy the
+// reserved SMs the critical path's kernels need.
+namespace {
+std::mutex g_lane_mtx;
+cudaEvent_t g_lane_ev[64];
+int g_lane_n = 0;
+bool g_lane_has = false;
+}  // namespace
+K1Lane::K1Lane(cudaStream_t s) : s_(s) {
+  static const bool on = std::getenv("GFQ_K1_LANE") != nullptr;
+  if (!on || stream_is_critical(s)) return;
+  g_lane_mtx.lock();
+  held_ = true;
+  if (!g_lane_n) {
+    for (auto& e : g_lane_ev) GFQ_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    g_lane_n = 64;
+  }
+  static int cur = 0;
+  if (g_lane_has) GFQ_CUDA(cudaStreamWaitEvent(s, g_lane_ev[cur], 0));
+  cur_ = &cur;
+}
+K1Lane::~K1Lane() {
+  if (!held_) return;
+  *cur_ = (*cur_ + 1) % g_lane_n;
+  cudaEventRecord(g_lane_ev[*cur_], s_);
+  g_lane_has = true;
+  g_lane_mtx.unlock();
+}
 bool use_f4(std::uint32_t p, std::int64_t m, std::int64_t n, std::int64_t k) {
   static const bool off = std::getenv("GFQ_NO_F4") != nullptr;
   static const double min_work = [] {
@@ -378,7 +449,7 @@ void mad(std::uint32_t p, std::int64_t m, std::int64_t n, std::int64_t k,
   // would stream K through 64-wide tiles with a tiny grid.
   const bool big = k >= 32 && (double(m) * double(n) * double(k) >= 4.0 * 1024 * 1024 || k >= 128);
   const bool prof = g_profile;
-  ProfRec rec{nullptr, nullptr, 2.0 * double(m) * double(n) * double(k), 0};
+  ProfRec rec{nullptr, nullptr, 2.0 * double(m) * double(n) * double(k), 0, hprof::t_task_name};
   if (prof) {
     GFQ_CUDA(cudaEventCreate(&rec.e0));
     GFQ_CUDA(cudaEventCreate(&rec.e1));

@@ -86,6 +86,25 @@ bool mad_tc(std::uint32_t p, std::int64_t m, std::int64_t n, std::int64_t k,
 // Returns false (launching nothing) for other p or a k beyond the exact
 // range.  use_f4 is the dispatch rule (policy, field, size).
 bool f4_field(std::uint32_t p);
+// SMs a persistent K1 / K1f launch on `s` may occupy: all of them, minus
+// GFQ_K1_SM_RESERVE (default 0) on non-critical streams -- kept free for
+// the critical path's kernels.  stream_is_critical: s has the device's
+// greatest priority (the executor's Step-1 critical-path stream).
+bool stream_is_critical(cudaStream_t s);
+int k1_sms(cudaStream_t s);
+// Scope around a persistent contraction's launches (see kernels.cu).
+class K1Lane {
+ public:
+  explicit K1Lane(cudaStream_t s);
+  ~K1Lane();
+  K1Lane(const K1Lane&) = delete;
+  K1Lane& operator=(const K1Lane&) = delete;
+
+ private:
+  cudaStream_t s_;
+  bool held_ = false;
+  int* cur_ = nullptr;
+};
 bool use_f4(std::uint32_t p, std::int64_t m, std::int64_t n, std::int64_t k);
 std::int64_t mad_f4_scratch_bytes(std::int64_t m, std::int64_t n, std::int64_t k);
 bool mad_f4(std::uint32_t p, std::int64_t m, std::int64_t n, std::int64_t k, const std::uint8_t* A,

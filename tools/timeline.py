@@ -6,7 +6,7 @@ import sys
 from collections import defaultdict
 
 NAMES = ["k1_tc", "k1_simt", "ech_gf2", "ech_panel", "select", "k1_f4"]
-rows = [l.split() for l in open(sys.argv[1]) if l.strip()]
+rows = [l.split() for l in open(sys.argv[1]) if l.strip() and not l.startswith("T ")]
 iv = defaultdict(list)
 for f, a, b in rows:
     iv[int(f)].append((float(a), float(b)))
