@@ -18,12 +18,12 @@
 // values per byte, so each contraction first packs A (m x k -> m x kp/2
 // bytes) and transposes + packs B (k x n -> n x kp/2 bytes), kp = k rounded
 // up to 64, zero padded; pack kernels below (HBM-bound, 1.5 B moved per
-// element).  The MMA kernel then mirrors K1: 128 x 192 tiles, K-block 128
+// element).  The MMA kernel then mirrors K1: 128 x 224 tiles, K-block 128
 // bytes (256 elements) per stage, 5-stage TMA ring (SWIZZLE_128B, both
 // operands K-major), one MMA-issuing thread, fp32 accumulators
-// double-buffered in TMEM (2 x 192 columns) and released once in registers,
+// double-buffered in TMEM (2 x 224 columns) and released once in registers,
 // the scale factors (all 0x7F) planted once per CTA in 32 further TMEM
-// columns, 8 epilogue warps.  192 rather than 256 columns because 2 x 256
+// columns, 8 epilogue warps.  224 rather than 256 columns because 2 x 256
 // accumulator columns would leave no TMEM for the scale factors.
 #include <cuda.h>
 
@@ -32,6 +32,7 @@
 #include <cstdlib>
 #include <mutex>
 #include <stdexcept>
+#include <type_traits>
 #include <vector>
 
 #include "../common.hpp"
@@ -42,21 +43,34 @@ namespace gfq::dev {
 namespace f4 {
 using namespace tc;
 
-constexpr int BM = 128, BN = 192, BKB = 128;  // BKB: packed bytes of K per stage (256 elements)
-constexpr int A_STAGE = BM * BKB;             // 16 KB
-constexpr int B_STAGE = BN * BKB;             // 24 KB
-constexpr int STAGE_BYTES = A_STAGE + B_STAGE;
-constexpr int STAGES = 5;
-constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 + 256;
+constexpr int BM = 128, BKB = 128;  // BKB: packed bytes of K per stage (256 elements)
+constexpr int A_STAGE = BM * BKB;   // 16 KB
 constexpr int EPI_WARPS = 8;
 constexpr int NUM_THREADS = 64 + 32 * EPI_WARPS;
 constexpr int TMEM_COLS = 512;
-constexpr int SF_COL = 2 * BN;       // 384: scale factors of A (16 columns), then of B (16)
-// kind::mxf4 instruction descriptor: A = B = E2M1 (MXF4 format 1, bits 7-9
-// and 10-12), both K-major, N >> 3 at bit 17, scale format UE8M0 (bit 23),
-// M >> 4 at bit 24, scale-factor ids 0, dense K = 64.
-constexpr std::uint32_t IDESC = (1u << 7) | (1u << 10) | ((std::uint32_t(BN) >> 3) << 17) | (1u << 23) |
-                                ((std::uint32_t(BM) >> 4) << 24);
+// Tile variants: BN output columns, STAGES ring depth, ACCS accumulators in
+// TMEM (2 = the epilogue of tile i overlaps the MMAs of tile i+1); the
+// scale factors take 32 TMEM columns after the accumulators.
+template <int BN_, int STAGES_, int ACCS_>
+struct Cfg {
+  static constexpr int BN = BN_, STAGES = STAGES_, ACCS = ACCS_;
+  static constexpr int B_STAGE = BN * BKB;
+  static constexpr int STAGE_BYTES = A_STAGE + B_STAGE;
+  static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 + 256;
+  static constexpr int SF_COL = ACCS * BN;  // scale factors of A (16 columns), then of B (16)
+  static_assert(SF_COL + 32 <= TMEM_COLS, "TMEM: accumulators + scale factors");
+  static_assert(SMEM_BYTES <= 227 * 1024, "shared memory");
+  // kind::mxf4 instruction descriptor: A = B = E2M1 (MXF4 format 1, bits 7-9
+  // and 10-12), both K-major, N >> 3 at bit 17, scale format UE8M0 (bit 23),
+  // M >> 4 at bit 24, scale-factor ids 0, dense K = 64.
+  static constexpr std::uint32_t IDESC = (1u << 7) | (1u << 10) | ((std::uint32_t(BN) >> 3) << 17) |
+                                         (1u << 23) | ((std::uint32_t(BM) >> 4) << 24);
+};
+// measured on 8192 x 8192 x 65536 GF(2) (tools/f4_bench.py, kernel only):
+// 192 x 2: 6.33 POPS, 224 x 2: 6.64, 256 x 1: 6.59
+using CfgA = Cfg<224, 5, 2>;  // default
+using CfgB = Cfg<192, 5, 2>;
+using CfgC = Cfg<256, 4, 1>;
 
 __device__ __forceinline__ void mma_f4(std::uint32_t d_tmem, std::uint64_t adesc, std::uint64_t bdesc,
                                        std::uint32_t idesc, std::uint32_t accumulate, std::uint32_t sfa,
@@ -69,6 +83,16 @@ __device__ __forceinline__ void mma_f4(std::uint32_t d_tmem, std::uint64_t adesc
       "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate), "r"(sfa), "r"(sfb));
 }
 
+__device__ __forceinline__ void tmem_ld16(std::uint32_t taddr, std::uint32_t (&v)[16]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 "
+      "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+      : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
+        "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+
 __device__ __forceinline__ void tmem_st32_const(std::uint32_t taddr, std::uint32_t x) {
   asm volatile(
       "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], "
@@ -78,11 +102,14 @@ __device__ __forceinline__ void tmem_st32_const(std::uint32_t taddr, std::uint32
   asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
 }
 
+template <class C>
 __global__ void __launch_bounds__(NUM_THREADS, 1)
 gf_mad_f4_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, int m,
                  int n, int kpb, std::uint32_t p, std::uint32_t magic, std::uint32_t bias,
                  const std::uint8_t* Cin, std::int64_t ldc, std::uint8_t* D, std::int64_t ldd, int gm) {
   pdl_wait();
+  constexpr int BN = C::BN, STAGES = C::STAGES, ACCS = C::ACCS, B_STAGE = C::B_STAGE,
+                STAGE_BYTES = C::STAGE_BYTES, SF_COL = C::SF_COL;
   extern __shared__ __align__(1024) std::uint8_t smem_raw[];
   std::uint8_t* smem = reinterpret_cast<std::uint8_t*>(
       (reinterpret_cast<std::uintptr_t>(smem_raw) + 1023) & ~std::uintptr_t(1023));
@@ -160,8 +187,8 @@ gf_mad_f4_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
       std::uint32_t phase = 0;
       int it = 0;
       for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++it) {
-        const int acc = it & 1;
-        const std::uint32_t acc_phase = (it >> 1) & 1;
+        const int acc = ACCS == 2 ? (it & 1) : 0;
+        const std::uint32_t acc_phase = ACCS == 2 ? ((it >> 1) & 1) : (it & 1);
         mbar_wait(&tempty[acc], acc_phase ^ 1);
         fence_after();
         const std::uint32_t d_tmem = tmem_base + std::uint32_t(acc * BN);
@@ -175,7 +202,7 @@ gf_mad_f4_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
             // both operands K-major SW128: 32 bytes (64 E2M1 values) per MMA
             const std::uint64_t ad = umma_desc(a0 + kk * 32, 16, 1024);
             const std::uint64_t bd = umma_desc(b0 + kk * 32, 16, 1024);
-            mma_f4(d_tmem, ad, bd, IDESC, (kb | kk) != 0, sfa, sfb);
+            mma_f4(d_tmem, ad, bd, C::IDESC, (kb | kk) != 0, sfa, sfb);
           }
           mma_commit(&empty[stage]);
           if (++stage == STAGES) {
@@ -187,9 +214,11 @@ gf_mad_f4_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
       }
     }
   } else {
-    // epilogue: warp w reads TMEM lane quarter w % 4 and one half (96
-    // columns) of the tile
-    constexpr int HALF = BN / 2, CHUNKS = HALF / 32;
+    // epilogue: warp w reads TMEM lane quarter w % 4 and one half of the
+    // tile's columns, in chunks of 32 columns (+ one of 16)
+    constexpr int HALF = BN / 2, C32 = HALF / 32, TAIL = HALF % 32;
+    static_assert(TAIL == 0 || TAIL == 16, "epilogue chunks");
+    constexpr int NCH = C32 + (TAIL ? 1 : 0);
     const int quarter = warp & 3;
     const int half = (warp - 2) >> 2;
     const int row_in_tile = quarter * 32 + lane;
@@ -198,8 +227,8 @@ gf_mad_f4_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
     for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++it) {
       int mb, nb;
       tile_coords(tile, num_m, num_n, gm, mb, nb);
-      const int acc = it & 1;
-      const std::uint32_t acc_phase = (it >> 1) & 1;
+      const int acc = ACCS == 2 ? (it & 1) : 0;
+      const std::uint32_t acc_phase = ACCS == 2 ? ((it >> 1) & 1) : (it & 1);
       const int row = mb * BM + row_in_tile;
       const bool row_ok = row < m;
       const int cbase = nb * BN + half * HALF;
@@ -217,13 +246,10 @@ gf_mad_f4_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
       }
       mbar_wait(&tfull[acc], acc_phase);
       fence_after();
-#pragma unroll
-      for (int ch = 0; ch < CHUNKS; ++ch) {
-        std::uint32_t v[32];
-        const std::uint32_t taddr =
-            tmem_base + (std::uint32_t(quarter * 32) << 16) + std::uint32_t(acc * BN + half * HALF + ch * 32);
-        tmem_ld32(taddr, v);
-        if (ch == CHUNKS - 1) {
+      // W columns (16 or 32) of accumulators at column offset c0 of the half
+      auto process = [&](std::uint32_t* v, auto wtag, int c0, bool last) {
+        constexpr int W = decltype(wtag)::value;
+        if (last) {
           fence_before();
           __syncwarp();
           if (lane == 0) mbar_arrive(&tempty[acc]);
@@ -231,31 +257,34 @@ gf_mad_f4_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
         // the exact integer sums (fp32 -> int32 is exact below 2^24), made
         // non-negative by `bias` (a multiple of p; 0 for p = 2)
 #pragma unroll
-        for (int c = 0; c < 32; ++c) v[c] = std::uint32_t(__float2int_rn(__uint_as_float(v[c]))) + bias;
-        const int col0 = cbase + ch * 32;
+        for (int c = 0; c < W; ++c) v[c] = std::uint32_t(__float2int_rn(__uint_as_float(v[c]))) + bias;
+        const int col0 = cbase + c0;
         if (vec) {
-          const std::uint32_t cw[8] = {cpre[2 * ch].x,     cpre[2 * ch].y,     cpre[2 * ch].z,
-                                       cpre[2 * ch].w,     cpre[2 * ch + 1].x, cpre[2 * ch + 1].y,
-                                       cpre[2 * ch + 1].z, cpre[2 * ch + 1].w};
-          std::uint32_t ow[8];
-          if (p2) {
 #pragma unroll
-            for (int w = 0; w < 8; ++w)
-              ow[w] = (pack_low_bytes(v[4 * w], v[4 * w + 1], v[4 * w + 2], v[4 * w + 3]) ^ cw[w]) & 0x01010101u;
-          } else {
+          for (int h = 0; h < W / 16; ++h) {
+            const uint4 cq = cpre[c0 / 16 + h];
+            const std::uint32_t cw[4] = {cq.x, cq.y, cq.z, cq.w};
+            std::uint32_t ow[4];
+            if (p2) {
 #pragma unroll
-            for (int w = 0; w < 8; ++w) {
-              std::uint32_t r[4];
+              for (int w = 0; w < 4; ++w)
+                ow[w] = (pack_low_bytes(v[16 * h + 4 * w], v[16 * h + 4 * w + 1], v[16 * h + 4 * w + 2],
+                                        v[16 * h + 4 * w + 3]) ^ cw[w]) & 0x01010101u;
+            } else {
 #pragma unroll
-              for (int b = 0; b < 4; ++b) r[b] = modp(v[4 * w + b] + __byte_perm(cw[w], 0, 0x4440 + b), p, magic);
-              ow[w] = pack_low_bytes(r[0], r[1], r[2], r[3]);
+              for (int w = 0; w < 4; ++w) {
+                std::uint32_t r[4];
+#pragma unroll
+                for (int b = 0; b < 4; ++b)
+                  r[b] = modp(v[16 * h + 4 * w + b] + __byte_perm(cw[w], 0, 0x4440 + b), p, magic);
+                ow[w] = pack_low_bytes(r[0], r[1], r[2], r[3]);
+              }
             }
+            reinterpret_cast<uint4*>(drow + col0)[h] = make_uint4(ow[0], ow[1], ow[2], ow[3]);
           }
-          reinterpret_cast<uint4*>(drow + col0)[0] = make_uint4(ow[0], ow[1], ow[2], ow[3]);
-          reinterpret_cast<uint4*>(drow + col0)[1] = make_uint4(ow[4], ow[5], ow[6], ow[7]);
         } else if (row_ok) {
 #pragma unroll
-          for (int c = 0; c < 32; ++c) {
+          for (int c = 0; c < W; ++c) {
             if (col0 + c < n) {
               std::uint32_t x = v[c];
               if (crow) x += crow[col0 + c];
@@ -263,6 +292,19 @@ gf_mad_f4_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
             }
           }
         }
+      };
+      const std::uint32_t tbase =
+          tmem_base + (std::uint32_t(quarter * 32) << 16) + std::uint32_t(acc * BN + half * HALF);
+#pragma unroll
+      for (int ch = 0; ch < C32; ++ch) {
+        std::uint32_t v[32];
+        tmem_ld32(tbase + std::uint32_t(ch * 32), v);
+        process(v, std::integral_constant<int, 32>{}, ch * 32, ch == NCH - 1);
+      }
+      if constexpr (TAIL != 0) {
+        std::uint32_t v[16];
+        tmem_ld16(tbase + std::uint32_t(C32 * 32), v);
+        process(v, std::integral_constant<int, 16>{}, C32 * 32, true);
       }
     }
   }
@@ -432,9 +474,19 @@ bool mad_f4(std::uint32_t p, std::int64_t m, std::int64_t n, std::int64_t k, con
   if ((reinterpret_cast<std::uintptr_t>(scratch) & 15) != 0) return false;
   static std::once_flag attr_once;
   std::call_once(attr_once, [] {
-    GFQ_CUDA(cudaFuncSetAttribute(gf_mad_f4_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES));
+    GFQ_CUDA(cudaFuncSetAttribute(gf_mad_f4_kernel<CfgA>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  CfgA::SMEM_BYTES));
+    GFQ_CUDA(cudaFuncSetAttribute(gf_mad_f4_kernel<CfgB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  CfgB::SMEM_BYTES));
+    GFQ_CUDA(cudaFuncSetAttribute(gf_mad_f4_kernel<CfgC>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  CfgC::SMEM_BYTES));
     GFQ_CUDA(cudaFuncSetAttribute(pack_cols_f4_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, PC_SMEM));
   });
+  static const int variant = [] {
+    const char* e = std::getenv("GFQ_F4_VARIANT");
+    return e ? std::atoi(e) : 0;
+  }();
+  const int BN = variant == 1 ? CfgB::BN : variant == 2 ? CfgC::BN : CfgA::BN;
   const std::int64_t kpb = (k + 63) / 64 * 32;
   std::uint8_t* Ap = scratch;
   std::uint8_t* Bt = scratch + (m * kpb + 127) / 128 * 128;
@@ -481,8 +533,17 @@ bool mad_f4(std::uint32_t p, std::int64_t m, std::int64_t n, std::int64_t k, con
     // raster group: the A slice of gm M-tiles within ~32 MB
     const std::int64_t gm = std::max<std::int64_t>(
         1, std::min<std::int64_t>(num_m, (std::int64_t(32) << 20) / (std::int64_t(BM) * kpb)));
-    GFQ_CUDA(launch_pdl(gf_mad_f4_kernel, dim3(grid), dim3(NUM_THREADS), SMEM_BYTES, s, mA, mB, int(mm), int(n),
-                        int(kpb), p, magic, bias, Cin ? Cin + m0 * ldc : nullptr, ldc, D + m0 * ldd, ldd, int(gm)));
+    const std::uint8_t* cin = Cin ? Cin + m0 * ldc : nullptr;
+    std::uint8_t* d = D + m0 * ldd;
+    if (variant == 1)
+      GFQ_CUDA(launch_pdl(gf_mad_f4_kernel<CfgB>, dim3(grid), dim3(NUM_THREADS), CfgB::SMEM_BYTES, s, mA, mB,
+                          int(mm), int(n), int(kpb), p, magic, bias, cin, ldc, d, ldd, int(gm)));
+    else if (variant == 2)
+      GFQ_CUDA(launch_pdl(gf_mad_f4_kernel<CfgC>, dim3(grid), dim3(NUM_THREADS), CfgC::SMEM_BYTES, s, mA, mB,
+                          int(mm), int(n), int(kpb), p, magic, bias, cin, ldc, d, ldd, int(gm)));
+    else
+      GFQ_CUDA(launch_pdl(gf_mad_f4_kernel<CfgA>, dim3(grid), dim3(NUM_THREADS), CfgA::SMEM_BYTES, s, mA, mB,
+                          int(mm), int(n), int(kpb), p, magic, bias, cin, ldc, d, ldd, int(gm)));
     GFQ_CUDA(cudaGetLastError());
     count_launch();
   }
