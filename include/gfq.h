@@ -112,11 +112,13 @@ int gfq_reserve_for(int64_t m, int64_t n, int with_transform);
 int gfq_set_poison(int mode);
 /* Base-case size of the device ECH recursion (<= 128; results unaffected). */
 int gfq_set_ech_base(uint64_t n);
-/* ECH algorithm: 0 = device ECH (default; GF(2) blocks larger than the
- * cluster kernel's 1024 rows / 8192 packed columns split by the reference's
- * rule down to it), 1 = the reference's split/combine recursion
- * (src/jobs.cpp:202-225) over the small base kernel, 2 = as 0 but tall GF(2)
- * blocks on the two-level panel path.  Same outputs. */
+/* ECH algorithm: 0 = device ECH (default; GF(2) blocks beyond the whole-block
+ * cluster kernel split by the reference's rule down to it), 1 = the
+ * reference's split/combine recursion (src/jobs.cpp:202-225) over the small
+ * base kernel, 2 = as 0 but tall GF(2) blocks on the two-level path with
+ * single-CTA panel steps, 3 = as 0, 4 = as 0 but GF(2) blocks beyond the
+ * whole-block cluster kernel (up to 8192 rows) on the two-level path with
+ * one cluster launch per outer panel.  Same outputs. */
 int gfq_set_ech_mode(int mode);
 /* Outer panel width of the two-level device ECH: -1 = automatic (default),
  * 0 = one level (32-wide steps over all of [W | T]), else 32..256 (rounded

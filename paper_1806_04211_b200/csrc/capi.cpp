@@ -319,7 +319,7 @@ int gfq_set_ech_base(uint64_t n) { return guard([&] { gfq::set_ech_base(size_t(n
 int gfq_set_ech_outer(int width) { return guard([&] { gfq::set_ech_outer(width); }); }
 int gfq_set_ech_mode(int mode) {
   return guard([&] {
-    if (mode < 0 || mode > 2) throw std::invalid_argument("ech mode must be 0, 1 or 2");
+    if (mode < 0 || mode > 4) throw std::invalid_argument("ech mode must be 0..4");
     gfq::set_ech_mode(mode);
   });
 }

@@ -394,11 +394,34 @@ std::int64_t ech_outer_width(std::int64_t b) {
 // K2 panel launch + a row gather + two K1 launches per 32-column panel, no
 // host round trip until the pivots are read back at the end.  Outputs in the
 // reference's conventions (same extraction as direct_ech, T uncompacted).
-EchResult panel_ech(const FieldSpec& f, const Mat& h) {
+// GF(2) blocks beyond the whole-block cluster kernel's fast path may take
+// the two-level path with each outer panel factorized by ONE cluster launch
+// (dev::ech_gf2_outer, rows <= 8192; ech mode 4 or GFQ_GF2_OUTER=1): no host
+// round trip until the end, but on 8192^2 blocks it measured slower than the
+// split (10.4 vs 8.7 ms alone, cfg5s 197 vs 174 ms), so the split stays the
+// default.
+bool gf2_outer_enabled() {
+  static const bool env = [] {
+    const char* e = std::getenv("GFQ_GF2_OUTER");
+    return e && e[0] == '1';
+  }();
+  return ech_mode() == 4 || (env && ech_mode() == 0);
+}
+constexpr std::int64_t kGf2OuterRows = 8192;
+std::int64_t gf2_outer_width() {
+  static const std::int64_t w = [] {
+    const char* e = std::getenv("GFQ_GF2_OUTER_W");
+    const std::int64_t v = e ? std::atoll(e) : 256;
+    return v == 512 ? std::int64_t(512) : std::int64_t(256);
+  }();
+  return w;
+}
+
+EchResult panel_ech(const FieldSpec& f, const Mat& h, bool block_cluster = true) {
   const std::int64_t a = h.rows(), b = h.cols(), w = 32;
   const std::int64_t cap = std::min(a, b);
   const cudaStream_t s = cur_stream();
-  if (f.p() == 2 && a <= 1024 && (a + b + 31) / 32 <= 256) {
+  if (block_cluster && f.p() == 2 && a <= 1024 && (a + b + 31) / 32 <= 256) {
     DevBuf info{static_cast<std::size_t>(4 * (1 + 2 * cap))};
     auto* inf = reinterpret_cast<std::int32_t*>(info.ptr);
     {
@@ -450,13 +473,15 @@ EchResult panel_ech(const FieldSpec& f, const Mat& h) {
     dev::set_entries(aug.data(), aug.ld(), dptr(db), a, 1, s);
   }
   DevBuf flags{static_cast<std::size_t>(dev::ech_panel_flag_bytes(a))};
-  DevBuf info{static_cast<std::size_t>(4 * (1 + 2 * cap) + 4 * (2 + kEchOuterMax))};
+  DevBuf info{static_cast<std::size_t>(4 * (1 + 2 * cap) + 4 * (2 + 512))};  // + base, rmap (<= 512 slots)
   DevBuf rho2{static_cast<std::size_t>(4 * w)};
   GFQ_CUDA(cudaMemsetAsync(flags.ptr, 0, flags.bytes, s));
   GFQ_CUDA(cudaMemsetAsync(info.ptr, 0, info.bytes, s));
   auto* inf = reinterpret_cast<std::int32_t*>(info.ptr);
   auto* r2 = reinterpret_cast<std::int32_t*>(rho2.ptr);
-  const std::int64_t ow = ech_outer_width(b);
+  const std::int64_t ow = (f.p() == 2 && !block_cluster && a <= kGf2OuterRows && b > 256)
+                             ? gf2_outer_width()
+                             : ech_outer_width(b);
   if (ow == 0) {
     Mat G(a, w), Bp(w, tb + a);
     for (std::int64_t c0 = 0; c0 < b; c0 += w) {
@@ -475,6 +500,7 @@ EchResult panel_ech(const FieldSpec& f, const Mat& h) {
   // panel's row operator to everything right of it (W and T) on K1.
   auto* base = inf + 1 + 2 * cap;  // rank at the start of the outer panel
   auto* rmap = base + 1;           // the outer panel's pivot rows (ow slots)
+  const bool gf2o = f.p() == 2 && !block_cluster && a <= kGf2OuterRows;
   Mat Z(a, 2 * ow), Bt(ow, tb + a);
   DevBuf step{static_cast<std::size_t>(dev::ech_step_scratch_bytes())};
   const bool fused = a * 33 <= dev::kPanelSmem;
@@ -484,7 +510,8 @@ EchResult panel_ech(const FieldSpec& f, const Mat& h) {
     // Z[:, 0:wd] = Aug[:, C0:C0+wd], Z[:, ow:] = 0
     dev::copy_cols(Z.data(), Z.ld(), aug.data() + C0, aug.ld(), a, wd, 2 * ow, s);
     std::uint8_t* Y = Z.data() + ow;
-    for (std::int64_t c0 = 0; c0 < wd; c0 += w) {
+    const bool done_outer = gf2o && dev::ech_gf2_outer(a, wd, ow, Z.data(), Z.ld(), flags.ptr, inf, cap, s);
+    for (std::int64_t c0 = done_outer ? wd : 0; c0 < wd; c0 += w) {
       const std::int64_t wc = std::min(w, wd - c0);
       // the step updates Z columns from c0 through Y's used slots
       const std::int64_t n = (ow + std::min(kc, c0 + w) - c0 + 15) / 16 * 16;
@@ -615,6 +642,9 @@ EchResult ech(const FieldSpec& f, const Mat& h, std::size_t threshold) {
     // split rule (src/jobs.cpp:202-225: rows when alpha >= beta, else
     // columns) down to it, so a tall 8192^2 ECH is eight cluster ECHs plus
     // K1 combines instead of 256 single-CTA panel steps.
+    if (f.p() == 2 && !gf2_cluster_fits(alpha, beta) && alpha > 32 && alpha <= kGf2OuterRows &&
+        gf2_outer_enabled())
+      return panel_ech(f, h, false);
     if (f.p() == 2 && gf2_split_enabled() && !gf2_cluster_fits(alpha, beta)) {
       if (alpha >= beta) {
         const std::int64_t alpha1 = split_of(alpha);

@@ -322,6 +322,15 @@ bool ech_gf2_cluster(std::int64_t rows, std::int64_t cols, const std::uint8_t* H
 bool ech_gf2_small(std::int64_t rows, std::int64_t cols, const std::uint8_t* H, std::int64_t ldh,
                    std::int32_t* info, std::int64_t cap, cudaStream_t s, const EchExtract& ex);
 
+// One outer panel of the two-level GF(2) ECH in one 8-CTA cluster launch
+// (ech_gf2_outer.cu): Z = [X | Y] (rows x 2 ow u8, X = Z[:, 0:wd], Y =
+// Z[:, ow:2 ow] zero on entry), rows <= 8192, ow in {256, 512}; leaves Z,
+// flags and info exactly as the 32-wide ech_step launches over the panel
+// would (then ech_outer_finish).  Returns false (nothing launched) outside
+// those limits or with GFQ_NO_GF2_OUTER set.
+bool ech_gf2_outer(std::int64_t rows, std::int64_t wd, std::int64_t ow, std::uint8_t* Z, std::int64_t ldz,
+                   std::uint8_t* flags, std::int32_t* info, std::int64_t cap, cudaStream_t s);
+
 // dst[rmap[i]] = src[i] for rmap[i] >= 0 (row scatter).
 void scatter_rows(std::uint8_t* dst, std::int64_t ldd, std::int64_t rows, std::int64_t cols,
                   const std::uint8_t* src, std::int64_t lds, const std::int32_t* rmap,

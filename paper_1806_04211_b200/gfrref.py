@@ -966,7 +966,10 @@ def set_poison(mode: int):
 def set_ech_mode(mode: int):
     """0 = device ECH (default: GF(2) blocks beyond the cluster kernel split by the
     reference rule), 1 = reference split/combine recursion over the small base
-    kernel, 2 = device ECH with tall GF(2) blocks on the two-level panel path."""
+    kernel, 2 = device ECH with tall GF(2) blocks on the two-level path with
+    single-CTA panel steps, 3 = as 0, 4 = device ECH with GF(2) blocks beyond the
+    whole-block cluster kernel on the two-level path, one cluster launch per
+    outer panel (ech_gf2_outer)."""
     _check(lib().gfq_set_ech_mode(mode))
 
 

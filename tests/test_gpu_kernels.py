@@ -360,9 +360,12 @@ def test_generator_matches_reference(G, ref_runs):
 
 @pytest.mark.parametrize("case", ["square2048", "tall1536", "wide1000x7500", "low2048", "zero_rows"])
 def test_ech_gf2_split_vs_reference(G, case):
-    """GF(2) blocks beyond the cluster kernel (> 1024 rows, or rows + cols >
-    8192) split by the reference's rule (src/jobs.cpp:202-225) down to it;
-    bit-exact against the reference's own ech and the two-level panel path."""
+    """GF(2) blocks beyond the whole-block cluster kernel (> 1024 rows, or a
+    packed [W | T] row beyond its nibble tables): the two-level path with one
+    cluster launch per outer panel (mode 4), the same path with single-CTA
+    panel steps (mode 2) and the reference's split rule (src/jobs.cpp:202-225)
+    down to the cluster kernel (mode 0, the default), each bit-exact against
+    the reference's own ech."""
     p = 2
     f = G.FieldSpec(p)
     rng = np.random.default_rng(7)
@@ -381,14 +384,14 @@ def test_ech_gf2_split_vs_reference(G, case):
         H[:700] = 0
         H[1500:1800] = H[100:400] ^ H[900:1200]
     want = oracle.ref_ech(p, H)
-    G.set_ech_mode(0)
-    got = G.ech(f, H)
-    G.set_ech_mode(2)
+    outs = []
     try:
-        alt = G.ech(f, H)
+        for mode in (4, 2, 0):  # outer-panel cluster, single-CTA panel steps, split
+            G.set_ech_mode(mode)
+            outs.append(G.ech(f, H))
     finally:
         G.set_ech_mode(0)
-    for e in (got, alt):
+    for e in outs:
         assert e.rank() == want["rank"]
         assert list(e.rho.members) == list(want["rho"]) and list(e.gamma.members) == list(want["gamma"])
         for key in "MKR":
