@@ -192,122 +192,44 @@ __global__ void __launch_bounds__(kThreads, 1) ech_gf2_cluster_kernel(ClArgs g) 
     const long long ck0 = clock64();
     int r2 = 0, ok = 1, q0 = -1, q1 = -1, mpc = 0, mpr = 0;
     const unsigned lanebit = 1u << lane;
-    // fast path, column layout: lane c holds column c of the window as a
-    // 64-bit row mask (cm), lane q the rows whose coefficient word has pivot
-    // q (km); a pivot step is one 64-bit shuffle (column c's mask), the first
-    // open row p, and every lane flipping its masks by the column's other
-    // rows iff row p has its bit (~290 against ~550 cycles a column in row
-    // layout, measured in ech_gf2_outer)
-    std::uint64_t cm = 0, km = 0;
-    for (int i = 0; i < 32; ++i) {
-      const unsigned blo = __ballot_sync(0xffffffffu, (w0 >> i) & 1u);
-      const unsigned bhi = __ballot_sync(0xffffffffu, (w1 >> i) & 1u);
-      if (lane == i) cm = std::uint64_t(blo) | (std::uint64_t(bhi) << 32);
-    }
-    std::uint64_t openm = std::uint64_t(__ballot_sync(0xffffffffu, !p0)) |
-                          (std::uint64_t(__ballot_sync(0xffffffffu, !p1)) << 32);
-    int myslot = -1;
-    int c = 0;
 #pragma unroll 1
-    for (; c < wc; ++c) {
-      const std::uint64_t M = __shfl_sync(0xffffffffu, cm, c);
-      const std::uint64_t cand = M & openm;
-      if (cand == 0) {
+    for (int c = 0; c < wc; ++c) {
+      const unsigned b0 = __ballot_sync(0xffffffffu, !p0 && ((w0 >> c) & 1u));
+      const unsigned b1 = __ballot_sync(0xffffffffu, !p1 && ((w1 >> c) & 1u));
+      if (!(b0 | b1)) {
         if (covers_all) continue;
+        ok = 0;
         break;
       }
-      const int pidx = __ffsll(static_cast<long long>(cand)) - 1;
-      const std::uint64_t pbit = std::uint64_t(1) << pidx;
-      const std::uint64_t R = M & ~pbit;
-      if (cm & pbit) cm ^= R;
-      if (km & pbit) km ^= R;
-      if (lane == r2) {
-        km ^= R;
-        myslot = pidx;
+      const bool hi = b0 == 0;
+      const unsigned bb = hi ? b1 : b0;
+      const int sl = __ffs(bb) - 1;
+      const std::uint32_t pw = __shfl_sync(0xffffffffu, hi ? w1 : w0, sl);
+      const std::uint32_t pk = __shfl_sync(0xffffffffu, hi ? k1 : k0, sl) ^ (1u << r2);
+      // "am I the pivot lane" from the ballot's lowest bit (no lane id in the loop)
+      const bool mine = (bb & (0u - bb) & lanebit) != 0;
+      const bool me0 = !hi && mine, me1 = hi && mine;
+      if (!me0 && ((w0 >> c) & 1u)) {
+        w0 ^= pw;
+        k0 ^= pk;
+      }
+      if (!me1 && ((w1 >> c) & 1u)) {
+        w1 ^= pw;
+        k1 ^= pk;
+      }
+      if (me0) {
+        p0 = true;
+        q0 = r2;
+      }
+      if (me1) {
+        p1 = true;
+        q1 = r2;
+      }
+      if ((lanebit >> r2) & 1u) {  // kept in registers: no shared stores on the chain
         mpc = c;
-        mpr = lo + pidx;
+        mpr = lo + (hi ? 32 : 0) + sl;
       }
-      openm &= ~pbit;
       ++r2;
-    }
-    if (c == wc) {
-      // the pivot rows' multiplier words: bit q' of row p's coefficient is
-      // bit p of lane q''s km
-      for (int q = 0; q < r2; ++q) {
-        const int sl = __shfl_sync(0xffffffffu, myslot, q);
-        const unsigned b = __ballot_sync(0xffffffffu, (km >> sl) & 1u);
-        if (lane == 0) pcoef[q] = b ^ (1u << q);
-      }
-    } else {
-      // a column without a window candidate: back to row layout (row i's
-      // word / coefficient = bit i of every lane's cm / km) and the row
-      // layout chain from column c (which falls back to the CTA chain)
-      for (int i = 0; i < 64; ++i) {
-        const unsigned bw = __ballot_sync(0xffffffffu, (cm >> i) & 1u);
-        const unsigned bk = __ballot_sync(0xffffffffu, (km >> i) & 1u);
-        if (i == lane) {
-          w0 = bw;
-          k0 = bk;
-        }
-        if (i == lane + 32) {
-          w1 = bw;
-          k1 = bk;
-        }
-      }
-      for (int q = 0; q < r2; ++q) {
-        const int sl = __shfl_sync(0xffffffffu, myslot, q);
-        if (sl == lane) {
-          p0 = true;
-          q0 = q;
-        }
-        if (sl == lane + 32) {
-          p1 = true;
-          q1 = q;
-        }
-      }
-#pragma unroll 1
-        for (; c < wc; ++c) {
-        const unsigned b0 = __ballot_sync(0xffffffffu, !p0 && ((w0 >> c) & 1u));
-        const unsigned b1 = __ballot_sync(0xffffffffu, !p1 && ((w1 >> c) & 1u));
-        if (!(b0 | b1)) {
-          if (covers_all) continue;
-          ok = 0;
-          break;
-        }
-        const bool hi = b0 == 0;
-        const unsigned bb = hi ? b1 : b0;
-        const int sl = __ffs(bb) - 1;
-        const std::uint32_t pw = __shfl_sync(0xffffffffu, hi ? w1 : w0, sl);
-        const std::uint32_t pk = __shfl_sync(0xffffffffu, hi ? k1 : k0, sl) ^ (1u << r2);
-        // "am I the pivot lane" from the ballot's lowest bit (no lane id in the loop)
-        const bool mine = (bb & (0u - bb) & lanebit) != 0;
-        const bool me0 = !hi && mine, me1 = hi && mine;
-        if (!me0 && ((w0 >> c) & 1u)) {
-          w0 ^= pw;
-          k0 ^= pk;
-        }
-        if (!me1 && ((w1 >> c) & 1u)) {
-          w1 ^= pw;
-          k1 ^= pk;
-        }
-        if (me0) {
-          p0 = true;
-          q0 = r2;
-        }
-        if (me1) {
-          p1 = true;
-          q1 = r2;
-        }
-        if ((lanebit >> r2) & 1u) {  // kept in registers: no shared stores on the chain
-          mpc = c;
-          mpr = lo + (hi ? 32 : 0) + sl;
-        }
-        ++r2;
-      }
-      if (ok) {
-        if (q0 >= 0) pcoef[q0] = k0 ^ (1u << q0);
-        if (q1 >= 0) pcoef[q1] = k1 ^ (1u << q1);
-      }
     }
     if (lane < r2) {
       pc[lane] = mpc;
@@ -316,6 +238,11 @@ __global__ void __launch_bounds__(kThreads, 1) ech_gf2_cluster_kernel(ClArgs g) 
     __syncwarp();
     stamp(k - 1, 11);
     if (g.dbg && cr == 0 && tid == 0 && k >= 1 && k < 9) g.dbg[(k - 1) * 16 + 13] = clock64() - ck0;
+    // a pivot row's multiplier word: its own bit plus the pivots added to it
+    if (ok) {
+      if (q0 >= 0) pcoef[q0] = k0 ^ (1u << q0);
+      if (q1 >= 0) pcoef[q1] = k1 ^ (1u << q1);
+    }
     __syncwarp();
     if (lane == 0) {
       ok_sh = ok;
