@@ -2,6 +2,8 @@
 #include "chief.hpp"
 
 #include <algorithm>
+#include <chrono>
+#include <cstdio>
 #include <cstdlib>
 #include <condition_variable>
 #include <deque>
@@ -247,7 +249,7 @@ PlanHandles build_plan_fused(TaskGraph& graph, const Mat& C, const FieldSpec& fi
     return row_ready ? (*row_ready)[i] : std::shared_ptr<EventBox>();
   };
   for (std::size_t i = 0; i < a; ++i) {
-    graph.add_input({K::C, std::uint16_t(i), 0, 0, 0}, blk(i, 0), ready(i));
+    graph.add_input({K::C, std::uint16_t(i), 0, 0, 0}, blk(i, 0), ready(i), true);
     if (b > 1) {
       MatParts panel;
       const std::int64_t o1 = std::int64_t(cs.col_offset(1));
@@ -257,7 +259,7 @@ PlanHandles build_plan_fused(TaskGraph& graph, const Mat& C, const FieldSpec& fi
         panel.off.push_back(std::int64_t(cs.col_offset(k)) - o1);
         panel.w.push_back(std::int64_t(cs.col_parts[k]));
       }
-      graph.add_input({K::CW, std::uint16_t(i), 1, 0, 0}, std::move(panel), ready(i));
+      graph.add_input({K::CW, std::uint16_t(i), 1, 0, 0}, std::move(panel), ready(i), true);
     }
   }
 
@@ -467,6 +469,15 @@ namespace {
 // published.  Block shapes follow from the final D (|gamma_j|) and E
 // (|rho_i|) packages, so copies start once the last of those is published
 // (end of Step 1) and the Step-3 blocks stream out as their rounds finish.
+// Developer timeline of the host-buffer path (GFQ_E2E_DEBUG): device times
+// of each input row's arrival and each output block's download, from the
+// start of the upload.
+bool e2e_debug() {
+  static const bool on = std::getenv("GFQ_E2E_DEBUG") != nullptr;
+  return on;
+}
+cudaEvent_t g_e2e_t0 = nullptr;
+
 class EarlyDownload {
  public:
   EarlyDownload(const PlanHandles& h, const ChopSpec& cs, bool with_transform, std::uint8_t* host,
@@ -495,6 +506,15 @@ class EarlyDownload {
       finish();
     } catch (...) {
       // an error was already reported (or the run itself failed)
+    }
+    if (e2e_debug() && g_e2e_t0) {
+      for (const auto& [label, ev] : dbg_) {
+        float ms = 0;
+        if (cudaEventElapsedTime(&ms, g_e2e_t0, ev) == cudaSuccess)
+          std::fprintf(stderr, "e2e download %s done at %.2f ms\n", label.c_str(), double(ms));
+        cudaEventDestroy(ev);
+      }
+      cudaGetLastError();
     }
     cudaStreamDestroy(stream_);
   }
@@ -593,10 +613,29 @@ class EarlyDownload {
       if (std::uint64_t(m.rows()) != bk.rows || std::uint64_t(m.cols()) != bk.cols)
         throw std::logic_error("output block shape disagrees with the layout");
       if (!waited && pub.ready) GFQ_CUDA(cudaStreamWaitEvent(stream_, pub.ready->ev, 0));
+      if (!waited && e2e_debug()) {
+        // when the block's data was final (a timing event behind the publish event)
+        if (!dbg_stream_) GFQ_CUDA(cudaStreamCreateWithFlags(&dbg_stream_, cudaStreamNonBlocking));
+        if (pub.ready) GFQ_CUDA(cudaStreamWaitEvent(dbg_stream_, pub.ready->ev, 0));
+        cudaEvent_t ev;
+        GFQ_CUDA(cudaEventCreate(&ev));
+        GFQ_CUDA(cudaEventRecord(ev, dbg_stream_));
+        dbg_.emplace_back(std::string("  READY slot ") + std::to_string(sid) + " kind" + std::to_string(bk.kind) +
+                              " [" + std::to_string(bk.x) + "][" + std::to_string(bk.y) + "]",
+                          ev);
+      }
       waited = true;
       GFQ_CUDA(cudaMemcpy2DAsync(host_ + bk.off, std::size_t(bk.cols), m.data(), std::size_t(m.ld()),
                                  std::size_t(bk.cols), std::size_t(bk.rows), cudaMemcpyDeviceToHost,
                                  stream_));
+      if (e2e_debug()) {
+        cudaEvent_t ev;
+        GFQ_CUDA(cudaEventCreate(&ev));
+        GFQ_CUDA(cudaEventRecord(ev, stream_));
+        dbg_.emplace_back(std::string("kind") + std::to_string(bk.kind) + " [" + std::to_string(bk.x) + "][" +
+                              std::to_string(bk.y) + "] " + std::to_string(bk.rows) + "x" + std::to_string(bk.cols),
+                          ev);
+      }
     }
   }
 
@@ -617,6 +656,8 @@ class EarlyDownload {
   bool done_ = false;
   std::string error_;
   std::thread thread_;
+  std::vector<std::pair<std::string, cudaEvent_t>> dbg_;
+  cudaStream_t dbg_stream_ = nullptr;
 };
 
 EchelonOutput echelonize_impl(const Mat& C, const FieldSpec& field, const EchelonizeOptions& options,
@@ -641,7 +682,12 @@ EchelonOutput echelonize(const Mat& C, const FieldSpec& field, const EchelonizeO
 EchelonOutput echelonize_host(const std::uint8_t* host, std::int64_t m, std::int64_t n,
                               std::int64_t ld, const FieldSpec& field,
                               const EchelonizeOptions& options, RunReport* report) {
+  const auto h0 = std::chrono::steady_clock::now();
+  const auto hms = [&h0] {
+    return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - h0).count();
+  };
   Mat C(m, n);
+  if (e2e_debug()) std::fprintf(stderr, "e2e host: input allocated at %.2f ms\n", hms());
   const ChopSpec cs = chop(std::size_t(m), std::size_t(n), options.block, options.remainder_first);
   const bool streamed = options.fuse && !C.empty() && cs.a() > 0 && cs.b() > 0 &&
                         2 * cs.a() + 1 <= std::size_t(TaskNode::kMaxIn);
@@ -660,6 +706,11 @@ EchelonOutput echelonize_host(const std::uint8_t* host, std::int64_t m, std::int
     auto alloc_done = std::make_shared<EventBox>();
     GFQ_CUDA(cudaEventRecord(alloc_done->ev, cur_stream()));
     GFQ_CUDA(cudaStreamWaitEvent(cs_stream, alloc_done->ev, 0));
+    std::vector<cudaEvent_t> dbg_rows;
+    if (e2e_debug()) {
+      if (!g_e2e_t0) GFQ_CUDA(cudaEventCreate(&g_e2e_t0));
+      GFQ_CUDA(cudaEventRecord(g_e2e_t0, cs_stream));
+    }
     for (std::size_t i = 0; i < cs.a(); ++i) {
       const std::int64_t r0 = std::int64_t(cs.row_offset(i)), nr = std::int64_t(cs.row_parts[i]);
       GFQ_CUDA(cudaMemcpy2DAsync(C.data() + r0 * C.ld(), std::size_t(C.ld()), host + r0 * ld,
@@ -668,10 +719,26 @@ EchelonOutput echelonize_host(const std::uint8_t* host, std::int64_t m, std::int
       auto ev = std::make_shared<EventBox>();
       GFQ_CUDA(cudaEventRecord(ev->ev, cs_stream));
       row_ready.push_back(std::move(ev));
+      if (e2e_debug()) {
+        cudaEvent_t t;
+        GFQ_CUDA(cudaEventCreate(&t));
+        GFQ_CUDA(cudaEventRecord(t, cs_stream));
+        dbg_rows.push_back(t);
+      }
     }
+    if (e2e_debug()) std::fprintf(stderr, "e2e host: uploads enqueued at %.2f ms\n", hms());
     EchelonOutput out = echelonize_impl(C, field, options, report, &row_ready);
+    if (e2e_debug()) std::fprintf(stderr, "e2e host: run + downloads done at %.2f ms\n", hms());
     GFQ_CUDA(cudaStreamSynchronize(cs_stream));  // the host buffer may be reused on return
+    if (e2e_debug()) std::fprintf(stderr, "e2e host: upload stream synchronized at %.2f ms\n", hms());
+    for (std::size_t i = 0; i < dbg_rows.size(); ++i) {
+      float ms = 0;
+      GFQ_CUDA(cudaEventElapsedTime(&ms, g_e2e_t0, dbg_rows[i]));
+      std::fprintf(stderr, "e2e upload row %zu landed at %.2f ms\n", i, double(ms));
+      cudaEventDestroy(dbg_rows[i]);
+    }
     cudaStreamDestroy(cs_stream);
+    if (e2e_debug()) std::fprintf(stderr, "e2e host: return at %.2f ms\n", hms());
     return out;
   } catch (...) {
     cudaStreamSynchronize(cs_stream);

@@ -73,7 +73,7 @@ void random_fill_exact(std::uint32_t p, std::int64_t rows, std::int64_t cols, st
                        std::int64_t ld) {
   if (rows == 0 || cols == 0) return;
   DevBuf rej{4};
-  GFQ_CUDA(cudaMemsetAsync(rej.ptr, 0, 4, cur_stream()));
+  dev::fill2d(rej.ptr, 4, 1, 4, 0, cur_stream());
   dev::random_fill(p, rows, cols, seed, draw0, draw_ld, dst, ld,
                    reinterpret_cast<std::uint32_t*>(rej.ptr), cur_stream());
   std::int32_t nrej = 0;
@@ -475,8 +475,8 @@ EchResult panel_ech(const FieldSpec& f, const Mat& h, bool block_cluster = true)
   DevBuf flags{static_cast<std::size_t>(dev::ech_panel_flag_bytes(a))};
   DevBuf info{static_cast<std::size_t>(4 * (1 + 2 * cap) + 4 * (2 + 512))};  // + base, rmap (<= 512 slots)
   DevBuf rho2{static_cast<std::size_t>(4 * w)};
-  GFQ_CUDA(cudaMemsetAsync(flags.ptr, 0, flags.bytes, s));
-  GFQ_CUDA(cudaMemsetAsync(info.ptr, 0, info.bytes, s));
+  dev::fill2d(flags.ptr, std::int64_t(flags.bytes), 1, std::int64_t(flags.bytes), 0, s);
+  dev::fill2d(info.ptr, std::int64_t(info.bytes), 1, std::int64_t(info.bytes), 0, s);
   auto* inf = reinterpret_cast<std::int32_t*>(info.ptr);
   auto* r2 = reinterpret_cast<std::int32_t*>(rho2.ptr);
   const std::int64_t ow = (f.p() == 2 && !block_cluster && a <= kGf2OuterRows && b > 256)

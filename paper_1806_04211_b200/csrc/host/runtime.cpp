@@ -551,7 +551,7 @@ Mat Mat::zeros(std::int64_t rows, std::int64_t cols) {
   Mat m(rows, cols);
   if (!m.empty()) {
     hprof::Scope hp(hprof::kMemset);
-    GFQ_CUDA(cudaMemsetAsync(m.data_, 0, std::size_t(rows) * std::size_t(m.ld_), cur_stream()));
+    dev::fill2d(m.data_, m.ld_, rows, m.ld_, 0, cur_stream());
   }
   return m;
 }
@@ -660,12 +660,43 @@ std::size_t PkgA::byte_size() const {
 
 // ---------------------------------------------------------------- staging
 namespace {
-// One process-wide pinned staging ring for small index uploads (pinning is
-// expensive: it is done once, not per executor thread or per call).
+// One process-wide pinned, device-mapped staging ring for small index
+// uploads (pinning is expensive: it is done once, not per executor thread or
+// per call).  An upload is a memcpy into the ring and a tiny kernel that
+// reads the ring over the bus into the device buffer -- not a copy-engine
+// transfer, so it never queues behind a bulk host-to-device copy (the
+// streamed input of gfq_echelonize_host: 4.3 GB at cfg5s held every index
+// upload of the first ECH for ~70 ms).  Reuse of a ring region waits for
+// the copy kernels that read it (events recorded after each one).
 struct Staging {
   std::mutex mtx;
   std::uint8_t* host = nullptr;
+  std::uint8_t* dev = nullptr;  // the ring's device-side address (mapped)
   std::size_t cap = 0, off = 0;
+  std::vector<cudaEvent_t> inflight, spare;  // copy kernels since the last wrap
+  void ensure() {
+    if (host) return;
+    cap = std::size_t(64) << 20;
+    GFQ_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&host), cap, cudaHostAllocMapped | cudaHostAllocPortable));
+    GFQ_CUDA(cudaHostGetDevicePointer(reinterpret_cast<void**>(&dev), host, 0));
+  }
+  cudaEvent_t event() {
+    if (spare.empty()) {
+      cudaEvent_t e;
+      GFQ_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+      return e;
+    }
+    cudaEvent_t e = spare.back();
+    spare.pop_back();
+    return e;
+  }
+  void drain() {
+    for (cudaEvent_t e : inflight) {
+      GFQ_CUDA(cudaEventSynchronize(e));
+      spare.push_back(e);
+    }
+    inflight.clear();
+  }
 };
 Staging& staging() {
   static Staging* st = new Staging();  // intentionally leaked (process lifetime)
@@ -693,10 +724,7 @@ void warm_runtime() {
   });
   Staging& st = staging();
   std::lock_guard<std::mutex> lk(st.mtx);
-  if (!st.host) {
-    st.cap = std::size_t(64) << 20;
-    GFQ_CUDA(cudaMallocHost(reinterpret_cast<void**>(&st.host), st.cap));
-  }
+  st.ensure();
 }
 
 std::shared_ptr<DevBuf> upload_i32(const std::vector<std::int32_t>& v) {
@@ -707,10 +735,7 @@ std::shared_ptr<DevBuf> upload_i32(const std::vector<std::int32_t>& v) {
   Staging& st = staging();
   const std::size_t need = (bytes + 255) / 256 * 256;
   std::lock_guard<std::mutex> lk(st.mtx);
-  if (!st.host) {
-    st.cap = std::size_t(64) << 20;
-    GFQ_CUDA(cudaMallocHost(reinterpret_cast<void**>(&st.host), st.cap));
-  }
+  st.ensure();
   if (need > st.cap) {
     // oversized: synchronous copy through pageable memory
     GFQ_CUDA(cudaMemcpyAsync(buf->ptr, v.data(), bytes, cudaMemcpyHostToDevice, cur_stream()));
@@ -718,13 +743,16 @@ std::shared_ptr<DevBuf> upload_i32(const std::vector<std::int32_t>& v) {
     return buf;
   }
   if (st.off + need > st.cap) {
-    // wrap: earlier copies out of the ring (on any stream) must have landed
-    GFQ_CUDA(cudaDeviceSynchronize());
+    // wrap: the copy kernels that read the ring since the last wrap must be done
+    st.drain();
     st.off = 0;
   }
   std::memcpy(st.host + st.off, v.data(), bytes);
-  GFQ_CUDA(cudaMemcpyAsync(buf->ptr, st.host + st.off, bytes, cudaMemcpyHostToDevice,
-                           cur_stream()));
+  const cudaStream_t s = cur_stream();
+  dev::copy_from_mapped(buf->ptr, st.dev + st.off, bytes, s);
+  cudaEvent_t e = st.event();
+  GFQ_CUDA(cudaEventRecord(e, s));
+  st.inflight.push_back(e);
   st.off += need;
   return buf;
 }
@@ -732,9 +760,29 @@ std::shared_ptr<DevBuf> upload_i32(const std::vector<std::int32_t>& v) {
 void download_i32(const std::int32_t* dev, std::int32_t* host, std::size_t n) {
   if (n == 0) return;
   hprof::Scope hp(hprof::kSync);
-  GFQ_CUDA(cudaMemcpyAsync(host, dev, n * sizeof(std::int32_t), cudaMemcpyDeviceToHost,
-                           cur_stream()));
-  GFQ_CUDA(cudaStreamSynchronize(cur_stream()));
+  // through a per-thread pinned, device-mapped buffer written by a kernel:
+  // no copy-engine transfer, so a readback never queues behind a bulk
+  // host copy (the streamed input of gfq_echelonize_host)
+  struct Mapped {
+    std::uint8_t* host = nullptr;
+    std::uint8_t* dev = nullptr;
+    std::size_t cap = 0;
+    ~Mapped() {
+      if (host) cudaFreeHost(host);
+    }
+  };
+  thread_local Mapped mb;
+  const std::size_t bytes = n * sizeof(std::int32_t);
+  if (bytes > mb.cap) {
+    if (mb.host) GFQ_CUDA(cudaFreeHost(mb.host));
+    mb.cap = std::max<std::size_t>(bytes, std::size_t(1) << 16);
+    GFQ_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&mb.host), mb.cap, cudaHostAllocMapped | cudaHostAllocPortable));
+    GFQ_CUDA(cudaHostGetDevicePointer(reinterpret_cast<void**>(&mb.dev), mb.host, 0));
+  }
+  const cudaStream_t s = cur_stream();
+  dev::copy_to_mapped(mb.dev, reinterpret_cast<const std::uint8_t*>(dev), bytes, s);
+  GFQ_CUDA(cudaStreamSynchronize(s));
+  std::memcpy(host, mb.host, bytes);
 }
 
 }  // namespace gfq

@@ -383,7 +383,7 @@ bool ech_gf2_block(std::int64_t rows, std::int64_t cols, const std::uint8_t* H, 
   static unsigned long long* dbg = nullptr;
   if (debug && !dbg) GFQ_CUDA(cudaMallocManaged(&dbg, 64 * sizeof(unsigned long long)));
   g.dbg = debug ? dbg : nullptr;
-  GFQ_CUDA(cudaMemsetAsync(g.bar, 0, 4 * sizeof(unsigned), s));
+  fill2d(reinterpret_cast<std::uint8_t*>(g.bar), 16, 1, 4 * sizeof(unsigned), 0, s);
   void* args[] = {&g};
   GFQ_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(ech_gf2_coop_kernel),
                                        dim3(unsigned(blocks)), dim3(1024), args, 0, s));

@@ -212,13 +212,13 @@ void mad_simt(std::uint32_t p, std::int64_t m, std::int64_t n, std::int64_t k,
               std::uint8_t* D, std::int64_t ldd, cudaStream_t s) {
   if (m == 0 || n == 0) return;
   if (k == 0) {
-    // D = Cin or 0: a strided copy / memset (no kernel of ours)
+    // D = Cin or 0: a strided copy / fill, as kernels (a copy-engine
+    // transfer would queue behind a bulk host copy on the same engine)
     if (Cin == D && ldc == ldd) return;
     if (Cin)
-      GFQ_CUDA(cudaMemcpy2DAsync(D, std::size_t(ldd), Cin, std::size_t(ldc), std::size_t(n),
-                                 std::size_t(m), cudaMemcpyDeviceToDevice, s));
+      select2d(D, ldd, m, n, Cin, ldc, nullptr, 0, nullptr, nullptr, s);
     else
-      GFQ_CUDA(cudaMemset2DAsync(D, std::size_t(ldd), 0, std::size_t(n), std::size_t(m), s));
+      fill2d(D, ldd, m, n, 0, s);
     return;
   }
   const std::int64_t kc = k_chunk_limit(p);
@@ -838,6 +838,72 @@ void select2d(std::uint8_t* dst, std::int64_t ldd, std::int64_t rows,
   }
   GFQ_CUDA(cudaGetLastError());
     count_launch();
+}
+
+namespace {
+// dst rows [0, rows) x bytes [0, width) = value (16-byte stores where aligned)
+__global__ void fill2d_kernel(std::uint8_t* dst, std::int64_t ldd, std::int64_t rows, std::int64_t width,
+                              std::uint8_t value) {
+  pdl_wait_and_release();
+  const std::uint32_t v4 = 0x01010101u * value;
+  const bool al = ((reinterpret_cast<std::uintptr_t>(dst) | std::uintptr_t(ldd)) & 15) == 0;
+  const std::int64_t nv = al ? width / 16 : 0;
+  for (std::int64_t i = blockIdx.y; i < rows; i += gridDim.y) {
+    std::uint8_t* row = dst + i * ldd;
+    for (std::int64_t v = std::int64_t(blockIdx.x) * blockDim.x + threadIdx.x; v < nv;
+         v += std::int64_t(gridDim.x) * blockDim.x)
+      reinterpret_cast<uint4*>(row)[v] = make_uint4(v4, v4, v4, v4);
+    for (std::int64_t b = nv * 16 + std::int64_t(blockIdx.x) * blockDim.x + threadIdx.x; b < width;
+         b += std::int64_t(gridDim.x) * blockDim.x)
+      row[b] = value;
+  }
+}
+__global__ void copy_from_mapped_kernel(std::uint8_t* dst, const std::uint8_t* src, std::size_t bytes) {
+  pdl_wait_and_release();
+  const std::size_t nv = bytes / 16;
+  for (std::size_t v = std::size_t(blockIdx.x) * blockDim.x + threadIdx.x; v < nv;
+       v += std::size_t(gridDim.x) * blockDim.x)
+    // .cv loads: a ring slot is rewritten by the host between uploads, so no
+    // cached copy of an earlier content may be used
+    reinterpret_cast<uint4*>(dst)[v] = __ldcv(reinterpret_cast<const uint4*>(src) + v);
+  for (std::size_t b = nv * 16 + 4 * (std::size_t(blockIdx.x) * blockDim.x + threadIdx.x); b < bytes;
+       b += 4 * std::size_t(gridDim.x) * blockDim.x)
+    *reinterpret_cast<std::uint32_t*>(dst + b) = __ldcv(reinterpret_cast<const unsigned int*>(src + b));
+}
+}  // namespace
+
+void fill2d(std::uint8_t* dst, std::int64_t ldd, std::int64_t rows, std::int64_t width, std::uint8_t value,
+            cudaStream_t s) {
+  if (rows <= 0 || width <= 0) return;
+  const std::int64_t per_row = (width + 15) / 16;
+  const unsigned gx = unsigned(std::min<std::int64_t>((per_row + 255) / 256, 64));
+  const unsigned gy = unsigned(std::min<std::int64_t>(rows, 65535));
+  GFQ_CUDA(launch_pdl(fill2d_kernel, dim3(gx, gy), dim3(256), 0, s, dst, ldd, rows, width, value));
+  count_launch();
+}
+
+namespace {
+__global__ void copy_to_mapped_kernel(std::uint8_t* dst, const std::uint8_t* src, std::size_t bytes) {
+  pdl_wait_and_release();
+  for (std::size_t b = 4 * (std::size_t(blockIdx.x) * blockDim.x + threadIdx.x); b < bytes;
+       b += 4 * std::size_t(gridDim.x) * blockDim.x)
+    __stcs(reinterpret_cast<unsigned int*>(dst + b), *reinterpret_cast<const unsigned int*>(src + b));
+}
+}  // namespace
+
+void copy_to_mapped(std::uint8_t* dst, const std::uint8_t* src, std::size_t bytes, cudaStream_t s) {
+  if (bytes == 0) return;
+  const unsigned grid = unsigned(std::min<std::size_t>((bytes / 4 + 255) / 256, 32));
+  GFQ_CUDA(launch_pdl(copy_to_mapped_kernel, dim3(grid), dim3(256), 0, s, dst, src, bytes));
+  count_launch();
+}
+
+void copy_from_mapped(std::uint8_t* dst, const std::uint8_t* src, std::size_t bytes, cudaStream_t s) {
+  if (bytes == 0) return;
+  const std::size_t nv = (bytes + 15) / 16;
+  const unsigned grid = unsigned(std::min<std::size_t>((nv + 255) / 256, 64));
+  GFQ_CUDA(launch_pdl(copy_from_mapped_kernel, dim3(grid), dim3(256), 0, s, dst, src, bytes));
+  count_launch();
 }
 
 void set_entries(std::uint8_t* dst, std::int64_t ldd, const std::int32_t* pos,

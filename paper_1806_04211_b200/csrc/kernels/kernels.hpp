@@ -331,6 +331,18 @@ bool ech_gf2_small(std::int64_t rows, std::int64_t cols, const std::uint8_t* H, 
 bool ech_gf2_outer(std::int64_t rows, std::int64_t wd, std::int64_t ow, std::uint8_t* Z, std::int64_t ldz,
                    std::uint8_t* flags, std::int32_t* info, std::int64_t cap, cudaStream_t s);
 
+// dst[0:bytes] = src[0:bytes] by a kernel reading `src` (device address of
+// pinned, mapped host memory) over the bus: a host-to-device upload that
+// does not go through a copy engine (so it never waits behind a bulk copy).
+// 16-byte aligned pointers, bytes a multiple of 4.
+void copy_from_mapped(std::uint8_t* dst, const std::uint8_t* src, std::size_t bytes, cudaStream_t s);
+// dst (device address of pinned, mapped host memory)[0:bytes] = src[0:bytes]
+// by a kernel (a readback without a copy engine); bytes a multiple of 4.
+void copy_to_mapped(std::uint8_t* dst, const std::uint8_t* src, std::size_t bytes, cudaStream_t s);
+// dst[i][0:width] = value for i < rows, as a kernel (not a copy-engine memset).
+void fill2d(std::uint8_t* dst, std::int64_t ldd, std::int64_t rows, std::int64_t width, std::uint8_t value,
+            cudaStream_t s);
+
 // dst[rmap[i]] = src[i] for rmap[i] >= 0 (row scatter).
 void scatter_rows(std::uint8_t* dst, std::int64_t ldd, std::int64_t rows, std::int64_t cols,
                   const std::uint8_t* src, std::int64_t lds, const std::int32_t* rmap,

@@ -1,5 +1,6 @@
 """Run single device jobs once (for ncu launch lists): python tools/one_ech.py [n] [p] [mode]
---reps R: run R times; --time: one untimed warm-up, then print the mean wall ms of R calls."""
+--reps R: run R times; --time: one untimed warm-up, then print the mean wall ms of R calls;
+--prof: launch windows per kernel family (with GFQ_PROF_DUMP=path)."""
 import os
 import sys
 import time
@@ -18,9 +19,15 @@ reps = int(sys.argv[sys.argv.index("--reps") + 1]) if "--reps" in sys.argv else 
 if "--time" in sys.argv:
     G.ech(f, H)
     G.synchronize()
+if "--prof" in sys.argv:
+    G.profile(True)
+    G.profile_take_kinds()
 t0 = time.perf_counter()
 for _ in range(reps):
     e = G.ech(f, H)
 G.synchronize()
+if "--prof" in sys.argv:
+    G.profile_take_kinds()  # GFQ_PROF_DUMP=path writes the launch windows
+    G.profile(False)
 dt = (time.perf_counter() - t0) / reps
 print("rank", e.rank(), "ms %.3f" % (1e3 * dt) if "--time" in sys.argv else "")
