@@ -58,6 +58,12 @@ int gfq_synchronize(void);
 /* ------------------------------------------------------------ values */
 /* Matrix (reference include/gfrref/matrix.hpp:15-43), device-resident. */
 int gfq_mat_upload(int64_t rows, int64_t cols, const uint8_t* host, int64_t ld, gfq_mat** out);
+/* Wide fields (GF(p), p > 251; GF(p^k), p^k > 256) store u32 elements:
+ * gfq_mat_upload32 takes a host u32 array with row stride ld ELEMENTS (NULL:
+ * zeros); gfq_mat_esize reports 1 (u8) or 4 (u32); gfq_mat_download and
+ * gfq_mat_device_ptr strides are in bytes. */
+int gfq_mat_upload32(int64_t rows, int64_t cols, const uint32_t* host, int64_t ld, gfq_mat** out);
+int gfq_mat_esize(const gfq_mat* m, int* esize);
 int gfq_mat_copy_device(int64_t rows, int64_t cols, const uint8_t* dev, int64_t ld,
                         gfq_mat** out);
 int gfq_mat_shape(const gfq_mat* m, int64_t* rows, int64_t* cols);
@@ -85,12 +91,14 @@ int gfq_mad_counters(int64_t* simt_launches, int64_t* tc_launches, int reset);
 /* K6: exact device replica of random_matrix / random_product_matrix
  * (include/gfrref/generate.hpp:33-39, src/generate.cpp:16-38). */
 int gfq_random_matrix(uint32_t p, int64_t rows, int64_t cols, uint64_t seed, gfq_mat** out);
-/* Fields.  Every entry point's `p` is a field code: a prime p <= 251 is
+/* Fields.  Every entry point's `p` is a field code: a prime p < 2^16 is
  * GF(p) itself; gfq_field_register returns the code (>= 0x10000) of
- * GF(p^k), p^k <= 256, with the given monic irreducible modulus c0..ck
+ * GF(p^k), p^k < 2^20, with the given monic irreducible modulus c0..ck
  * (n_modulus = k + 1; NULL / 0: the reference's default modulus), the
- * reference's FieldSpec(p, k, modulus) (include/gfrref/field.hpp:24-30).
- * Elements are encoded like the reference: sum_i c_i p^i, one byte each. */
+ * reference's FieldSpec(p, k, modulus) (include/gfrref/field.hpp:24-30,
+ * src/field.cpp:143-149).  Elements are encoded like the reference,
+ * sum_i c_i p^i: one byte each for p <= 251 / p^k <= 256 (the tensor-core
+ * path), u32 for the wider fields (gfq_mat_upload32 / gfq_mat_esize). */
 int gfq_field_register(uint32_t p, uint32_t k, const uint32_t* modulus, int n_modulus,
                        uint32_t* code);
 /* p, k, q = p^k and the modulus (k + 1 coefficients; {0, 1} for k = 1). */

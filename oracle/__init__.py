@@ -98,6 +98,7 @@ def _load_ref():
     r.ref_field_op.argtypes = [ctypes.c_uint32, ctypes.c_int, ctypes.c_uint32, ctypes.c_uint32]
     r.ref_field_op.restype = ctypes.c_uint32
     r.ref_default_modulus.argtypes = [ctypes.c_uint32, ctypes.c_uint32, _u32p]
+    r.ref_set_elem_bytes.argtypes = [ctypes.c_int]
     return r
 
 
@@ -373,3 +374,115 @@ def ref_random_product_matrix(p: int, rows: int, cols: int, inner: int, seed: in
     if out.size:
         ref.ref_random_product_matrix(p, rows, cols, inner, seed, u8ptr(out), cols)
     return out
+
+
+# ---------------------------------------------------------------- wide fields (u32 buffers)
+# Fields whose elements do not fit a byte (GF(p), p > 251; GF(p^k),
+# p^k > 256) cross the shim as u32 buffers: ref_set_elem_bytes(4) around
+# each call (oracle/ref_shim.cpp).  TEST INFRASTRUCTURE ONLY.
+class _Wide:
+    def __enter__(self):
+        _need_ref().ref_set_elem_bytes(4)
+
+    def __exit__(self, *exc):
+        ref.ref_set_elem_bytes(1)
+
+
+def _raw(a: np.ndarray):
+    assert a.flags["C_CONTIGUOUS"]
+    return a.ctypes.data_as(_u8p)
+
+
+def ref32_random_matrix(code: int, rows: int, cols: int, seed: int) -> np.ndarray:
+    """The reference's random_matrix (src/generate.cpp:16-24) as u32."""
+    out = np.zeros((rows, cols), np.uint32)
+    if out.size:
+        with _Wide():
+            ref.ref_random_matrix(code, rows, cols, seed, _raw(out), cols)
+    return out
+
+
+def ref32_mad(code: int, a: np.ndarray, b: np.ndarray, c: np.ndarray | None = None) -> np.ndarray:
+    """The reference's mat_mul / mat_mul_add (src/matrix.cpp:137-144) on u32 matrices."""
+    a = np.ascontiguousarray(a, np.uint32)
+    b = np.ascontiguousarray(b, np.uint32)
+    m, k = a.shape
+    n = b.shape[1]
+    out = np.zeros((m, n), np.uint32)
+    z = np.zeros(1, np.uint32)
+    if c is not None:
+        c = np.ascontiguousarray(c, np.uint32)
+    with _Wide():
+        rc = ref.ref_mad(code, m, k, n, _raw(a) if a.size else _raw(z), max(k, 1), _raw(b) if b.size else _raw(z),
+                         max(n, 1), _raw(c) if c is not None else None, max(n, 1), _raw(out) if out.size else _raw(z),
+                         max(n, 1))
+    if rc != 0:
+        raise RuntimeError(ref.ref_last_error().decode())
+    return out
+
+
+def ref32_ech(code: int, H: np.ndarray, threshold: int = 256):
+    """The reference's single-block ech (src/jobs.cpp:202-225) on a u32 matrix."""
+    H = np.ascontiguousarray(H, np.uint32)
+    m, n = H.shape
+    rho = np.zeros(max(m, 1), np.uint32)
+    gamma = np.zeros(max(n, 1), np.uint32)
+    M = np.zeros(max(m * m, 1), np.uint32)
+    K = np.zeros(max(m * m, 1), np.uint32)
+    R = np.zeros(max(m * n, 1), np.uint32)
+    src = H if H.size else np.zeros((1, 1), np.uint32)
+    with _Wide():
+        r = ref.ref_ech(code, m, n, _raw(src), max(n, 1), threshold, u32ptr(rho), u32ptr(gamma), _raw(M), _raw(K),
+                        _raw(R))
+    if r < 0:
+        raise RuntimeError(ref.ref_last_error().decode())
+    return dict(rank=int(r), rho=rho[:r].copy(), gamma=gamma[:r].copy(),
+                M=M[: r * r].reshape(r, r).copy(), K=K[: (m - r) * r].reshape(m - r, r).copy(),
+                R=R[: r * (n - r)].reshape(r, n - r).copy())
+
+
+class RefOutput32(RefOutput):
+    """RefOutput whose blocks are u32 (wide fields)."""
+
+    def block(self, kind: int, x: int, y: int) -> np.ndarray:
+        rows, cols = ctypes.c_int64(), ctypes.c_int64()
+        if ref.ref_out_block(self.h, kind, x, y, ctypes.byref(rows), ctypes.byref(cols), None):
+            raise IndexError(ref.ref_last_error().decode())
+        buf = np.zeros((rows.value, cols.value), np.uint32)
+        if buf.size:
+            with _Wide():
+                ref.ref_out_block(self.h, kind, x, y, ctypes.byref(rows), ctypes.byref(cols), _raw(buf))
+        return buf
+
+    def materialize_transform(self) -> np.ndarray:
+        t = np.zeros((self.m, self.m), np.uint32)
+        if t.size:
+            with _Wide():
+                bad = ref.ref_out_materialize(self.h, _raw(t))
+            if bad:
+                raise RuntimeError(ref.ref_last_error().decode())
+        return t
+
+    def assembled_R(self) -> np.ndarray:
+        r = self.rank
+        out = np.zeros((r, self.n - r), np.uint32)
+        if out.size:
+            with _Wide():
+                ref.ref_out_assembled_R(self.h, _raw(out))
+        return out
+
+
+def ref32_echelonize(code: int, C: np.ndarray, block: int, threads: int = 1, with_transform: bool = True,
+                     threshold: int = 256) -> RefOutput32:
+    """The reference's own gfrref::echelonize (src/chief.cpp:322-386) on a u32 matrix."""
+    r = _need_ref()
+    C = np.ascontiguousarray(C, np.uint32)
+    m, n = C.shape
+    wall, run = ctypes.c_double(), ctypes.c_double()
+    src = C if C.size else np.zeros((1, 1), np.uint32)
+    with _Wide():
+        h = r.ref_echelonize(code, m, n, _raw(src), max(n, 1), block, threads, int(with_transform), threshold,
+                             ctypes.byref(wall), ctypes.byref(run))
+    if not h:
+        raise RuntimeError(r.ref_last_error().decode())
+    return RefOutput32(h, m, n, wall.value, run.value)

@@ -28,19 +28,28 @@ using namespace gfrref;
 
 namespace {
 thread_local std::string g_err;
+// element width of every buffer crossing the shim: 1 (u8) or 4 (u32, the
+// wide fields); leading dimensions stay in elements
+int g_elem_bytes = 1;
 
 Matrix from_u8(std::size_t rows, std::size_t cols, const std::uint8_t* src,
                std::size_t ld) {
   Matrix m(rows, cols);
   for (std::size_t r = 0; r < rows; ++r)
-    for (std::size_t c = 0; c < cols; ++c) m.at(r, c) = src[r * ld + c];
+    for (std::size_t c = 0; c < cols; ++c)
+      m.at(r, c) = g_elem_bytes == 4 ? reinterpret_cast<const std::uint32_t*>(src)[r * ld + c]
+                                     : src[r * ld + c];
   return m;
 }
 
 void to_u8(const Matrix& m, std::uint8_t* dst, std::size_t ld) {
   for (std::size_t r = 0; r < m.rows(); ++r)
-    for (std::size_t c = 0; c < m.cols(); ++c)
-      dst[r * ld + c] = static_cast<std::uint8_t>(m.at(r, c));
+    for (std::size_t c = 0; c < m.cols(); ++c) {
+      if (g_elem_bytes == 4)
+        reinterpret_cast<std::uint32_t*>(dst)[r * ld + c] = static_cast<std::uint32_t>(m.at(r, c));
+      else
+        dst[r * ld + c] = static_cast<std::uint8_t>(m.at(r, c));
+    }
 }
 
 // Field codes: p for GF(p); 0x10000 + i for the i-th field registered with
@@ -63,6 +72,9 @@ struct RefOut {
 extern "C" {
 
 const char* ref_last_error() { return g_err.c_str(); }
+
+// 1: u8 matrix buffers (default), 4: u32 (fields beyond u8 elements)
+void ref_set_elem_bytes(int bytes) { g_elem_bytes = bytes == 4 ? 4 : 1; }
 
 std::uint32_t ref_field_register(std::uint32_t p, std::uint32_t k, const std::uint32_t* mod,
                                  std::size_t n) {

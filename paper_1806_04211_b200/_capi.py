@@ -55,6 +55,8 @@ PROTOS = {
     "gfq_set_stream": (I, [vp]),
     "gfq_synchronize": (I, []),
     "gfq_mat_upload": (I, [I64, I64, c_u8p, I64, vpp]),
+    "gfq_mat_upload32": (I, [I64, I64, c_u32p, I64, vpp]),
+    "gfq_mat_esize": (I, [vp, ctypes.POINTER(ctypes.c_int)]),
     "gfq_mat_copy_device": (I, [I64, I64, vp, I64, vpp]),
     "gfq_mat_shape": (I, [vp, c_i64p, c_i64p]),
     "gfq_mat_download": (I, [vp, c_u8p, I64]),

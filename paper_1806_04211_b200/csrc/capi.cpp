@@ -161,6 +161,16 @@ int gfq_mat_upload(int64_t rows, int64_t cols, const uint8_t* host, int64_t ld, 
     *out = wrap(host ? gfq::Mat::from_host(rows, cols, host, ld) : gfq::Mat::zeros(rows, cols));
   });
 }
+int gfq_mat_upload32(int64_t rows, int64_t cols, const uint32_t* host, int64_t ld, gfq_mat** out) {
+  return guard([&] {
+    require_device();
+    *out = wrap(host ? gfq::Mat::from_host(rows, cols, reinterpret_cast<const uint8_t*>(host), ld * 4, 4)
+                     : gfq::Mat::zeros(rows, cols, 4));
+  });
+}
+int gfq_mat_esize(const gfq_mat* m, int* esize) {
+  return guard([&] { *esize = M(m).esize(); });
+}
 int gfq_mat_copy_device(int64_t rows, int64_t cols, const uint8_t* dev, int64_t ld, gfq_mat** out) {
   return guard([&] {
     gfq::Mat m(rows, cols);
@@ -237,7 +247,8 @@ namespace {
 // `p` is a field code, q its order
 void fill_exact(uint32_t p, int64_t rows, int64_t cols, uint64_t seed, uint64_t draw0,
                 uint8_t* dst, int64_t ld) {
-  gfq::random_fill_exact(gfq::FieldSpec(p).order(), rows, cols, seed, draw0, cols, dst, ld);
+  const gfq::FieldSpec f(p);
+  gfq::random_fill_exact(f.order(), rows, cols, seed, draw0, cols, dst, ld, f.esize());
 }
 }  // namespace
 
@@ -284,7 +295,7 @@ int gfq_default_modulus(uint32_t p, uint32_t k, uint32_t* modulus) {
 int gfq_random_matrix(uint32_t p, int64_t rows, int64_t cols, uint64_t seed, gfq_mat** out) {
   return guard([&] {
     require_device();
-    gfq::Mat m(rows, cols);
+    gfq::Mat m(rows, cols, gfq::FieldSpec(p).esize());
     if (!m.empty()) fill_exact(p, rows, cols, seed, 0, m.data(), m.ld());
     *out = wrap(std::move(m));
   });
@@ -295,7 +306,7 @@ int gfq_random_product_matrix(uint32_t p, int64_t rows, int64_t cols, int64_t in
   return guard([&] {
     require_device();
     gfq::FieldSpec f(p);
-    gfq::Mat P(rows, inner), Q(inner, cols);
+    gfq::Mat P(rows, inner, f.esize()), Q(inner, cols, f.esize());
     if (!P.empty()) fill_exact(p, rows, inner, seed, 0, P.data(), P.ld());
     if (!Q.empty())
       fill_exact(p, inner, cols, seed, uint64_t(rows) * uint64_t(inner), Q.data(), Q.ld());
@@ -638,7 +649,7 @@ extern "C" {
 int gfq_output_block_bytes(const gfq_output* o, uint64_t* bytes) {
   return guard([&] {
     uint64_t n = 0;
-    for_each_block(O(o).out, [&](const gfq::Mat& m) { n += uint64_t(m.rows()) * uint64_t(m.cols()); });
+    for_each_block(O(o).out, [&](const gfq::Mat& m) { n += uint64_t(m.rows()) * uint64_t(m.row_bytes()); });
     *bytes = n;
   });
 }
@@ -646,11 +657,11 @@ int gfq_output_download_blocks(const gfq_output* o, uint8_t* host, uint64_t cap)
   return guard([&] {
     uint64_t off = 0;
     for_each_block(O(o).out, [&](const gfq::Mat& m) {
-      const uint64_t sz = uint64_t(m.rows()) * uint64_t(m.cols());
+      const uint64_t sz = uint64_t(m.rows()) * uint64_t(m.row_bytes());
       if (off + sz > cap) throw std::invalid_argument("download_blocks: buffer too small");
       if (sz)
-        GFQ_CUDA(cudaMemcpy2DAsync(host + off, size_t(m.cols()), m.data(), size_t(m.ld()),
-                                   size_t(m.cols()), size_t(m.rows()), cudaMemcpyDeviceToHost,
+        GFQ_CUDA(cudaMemcpy2DAsync(host + off, size_t(m.row_bytes()), m.data(), size_t(m.ld()),
+                                   size_t(m.row_bytes()), size_t(m.rows()), cudaMemcpyDeviceToHost,
                                    gfq::cur_stream()));
       off += sz;
     });
@@ -711,7 +722,7 @@ int gfq_read_gfmat_file(const char* path, uint32_t* p, gfq_mat** out) {
     if (!path || !p || !out) throw std::invalid_argument("gfq_read_gfmat_file: null argument");
     const gfq::GfMatHost h = gfq::read_gfmat_file(path);
     *p = h.p;
-    *out = wrap(gfq::Mat::from_host(h.rows, h.cols, h.data.data(), h.cols > 0 ? h.cols : 1));
+    *out = wrap(gfq::Mat::from_host(h.rows, h.cols, h.data.data(), h.cols > 0 ? h.cols * h.esize : 1, h.esize));
   });
 }
 int gfq_write_gfmat_file(const char* path, uint32_t p, const gfq_mat* m) {

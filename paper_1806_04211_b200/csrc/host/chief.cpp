@@ -689,6 +689,8 @@ EchelonOutput echelonize_host(const std::uint8_t* host, std::int64_t m, std::int
   Mat C(m, n);
   if (e2e_debug()) std::fprintf(stderr, "e2e host: input allocated at %.2f ms\n", hms());
   const ChopSpec cs = chop(std::size_t(m), std::size_t(n), options.block, options.remainder_first);
+  if (field.wide())
+    throw std::invalid_argument("echelonize_host: wide fields (u32 elements) take a device matrix");
   const bool streamed = options.fuse && !C.empty() && cs.a() > 0 && cs.b() > 0 &&
                         2 * cs.a() + 1 <= std::size_t(TaskNode::kMaxIn);
   if (!streamed) {
@@ -764,13 +766,13 @@ EchelonOutput echelonize_impl(const Mat& C, const FieldSpec& field, const Echelo
     for (std::size_t i = 0; i < a; ++i) out.varrho.emplace_back(cs.row_parts[i], std::vector<std::uint32_t>{});
     out.R_blocks.assign(b, std::vector<Mat>(b));
     for (std::size_t j = 0; j < b; ++j)
-      for (std::size_t l = j; l < b; ++l) out.R_blocks[j][l] = Mat(0, std::int64_t(cs.col_parts[l]));
+      for (std::size_t l = j; l < b; ++l) out.R_blocks[j][l] = Mat(0, std::int64_t(cs.col_parts[l]), field.esize());
     if (options.with_transform) {
       out.T_M_blocks.assign(b, std::vector<Mat>(a));
       out.T_K_blocks.resize(a);
       for (std::size_t i = 0; i < a; ++i)
         for (std::size_t h = 0; h <= i; ++h)
-          out.T_K_blocks[i].push_back(Mat(std::int64_t(cs.row_parts[i]), 0));
+          out.T_K_blocks[i].push_back(Mat(std::int64_t(cs.row_parts[i]), 0, field.esize()));
     }
     return out;
   }
@@ -780,7 +782,8 @@ EchelonOutput echelonize_impl(const Mat& C, const FieldSpec& field, const Echelo
   reserve_for(std::size_t(C.rows()), std::size_t(C.cols()), options.with_transform);
   TaskGraph graph;
   graph.ech_threshold = options.ech_threshold;
-  const bool fused = options.fuse && 2 * a + 1 <= std::size_t(TaskNode::kMaxIn);
+  // wide fields (u32 storage) run the reference's per-block task grid
+  const bool fused = options.fuse && !field.wide() && 2 * a + 1 <= std::size_t(TaskNode::kMaxIn);
   const PlanHandles h = fused ? build_plan_fused(graph, C, field, cs, options.with_transform, row_ready)
                               : build_plan(graph, C, field, cs, options.with_transform);
   for (auto id : h.d_final) graph.retain(id);
@@ -857,7 +860,8 @@ std::vector<std::uint32_t> EchelonOutput::global_varrho() const {
 // reference src/chief.cpp:408-425, as device-to-device block copies.
 Mat EchelonOutput::assembled_R() const {
   const std::int64_t n = std::int64_t(chop.cols());
-  Mat out = Mat::zeros(std::int64_t(rank), n - std::int64_t(rank));
+  const int es = field.esize();
+  Mat out = Mat::zeros(std::int64_t(rank), n - std::int64_t(rank), es);
   if (out.empty()) return out;
   std::int64_t row = 0;
   for (std::size_t j = 0; j < upsilon.size(); ++j) {
@@ -866,8 +870,8 @@ Mat EchelonOutput::assembled_R() const {
       const std::int64_t width = std::int64_t(chop.col_parts[l] - upsilon[l].size());
       if (l >= j && width > 0 && upsilon[j].size() > 0) {
         const Mat& blk = R_blocks[j][l];
-        GFQ_CUDA(cudaMemcpy2DAsync(out.data() + row * out.ld() + col, std::size_t(out.ld()),
-                                   blk.data(), std::size_t(blk.ld()), std::size_t(width),
+        GFQ_CUDA(cudaMemcpy2DAsync(out.data() + row * out.ld() + col * es, std::size_t(out.ld()),
+                                   blk.data(), std::size_t(blk.ld()), std::size_t(width * es),
                                    std::size_t(blk.rows()), cudaMemcpyDeviceToDevice,
                                    cur_stream()));
       }
@@ -885,14 +889,18 @@ Mat materialize_transform(const EchelonOutput& out) {
   if (!out.with_transform) throw std::logic_error("transformation was not computed");
   const std::int64_t m = std::int64_t(out.chop.rows());
   const std::size_t a = out.chop.a(), b = out.chop.b();
-  Mat t = Mat::zeros(m, m);
+  const int es = out.field.esize();
+  Mat t = Mat::zeros(m, m, es);
   if (t.empty()) return t;
-  // per block row h: column map of its stripe (selected row -> position)
+  // per block row h: column map of its stripe (selected row -> position),
+  // byte-level for wide elements
   std::vector<std::shared_ptr<DevBuf>> cmaps(a);
   for (std::size_t h = 0; h < a; ++h) {
-    std::vector<std::int32_t> map(out.chop.row_parts[h], -1);
+    std::vector<std::int32_t> map(out.chop.row_parts[h] * std::size_t(es), -1);
     for (std::size_t s = 0; s < out.varrho[h].size(); ++s)
-      map[out.varrho[h].members[s]] = std::int32_t(s);
+      for (int q = 0; q < es; ++q)
+        map[std::size_t(out.varrho[h].members[s]) * std::size_t(es) + std::size_t(q)] =
+            std::int32_t(s) * es + q;
     cmaps[h] = upload_i32(map);
   }
   std::int64_t row = 0;
@@ -901,8 +909,8 @@ Mat materialize_transform(const EchelonOutput& out) {
     for (std::size_t h = 0; h < a && nr > 0; ++h) {
       const Mat& mjh = out.T_M_blocks[j][h];
       if (out.varrho[h].size() == 0) continue;
-      dev::select2d(t.data() + row * t.ld() + std::int64_t(out.chop.row_offset(h)), t.ld(), nr,
-                    std::int64_t(out.chop.row_parts[h]), mjh.data(), mjh.ld(), nullptr, 0,
+      dev::select2d(t.data() + row * t.ld() + std::int64_t(out.chop.row_offset(h)) * es, t.ld(), nr,
+                    std::int64_t(out.chop.row_parts[h]) * es, mjh.data(), mjh.ld(), nullptr, 0,
                     nullptr, reinterpret_cast<const std::int32_t*>(cmaps[h]->ptr), cur_stream());
     }
     row += nr;
@@ -914,8 +922,8 @@ Mat materialize_transform(const EchelonOutput& out) {
     for (std::size_t h = 0; h <= i && nr > 0; ++h) {
       const Mat& kih = out.T_K_blocks[i][h];
       if (out.varrho[h].size() == 0) continue;
-      dev::select2d(t.data() + row * t.ld() + std::int64_t(out.chop.row_offset(h)), t.ld(), nr,
-                    std::int64_t(out.chop.row_parts[h]), kih.data(), kih.ld(), nullptr, 0,
+      dev::select2d(t.data() + row * t.ld() + std::int64_t(out.chop.row_offset(h)) * es, t.ld(), nr,
+                    std::int64_t(out.chop.row_parts[h]) * es, kih.data(), kih.ld(), nullptr, 0,
                     nullptr, reinterpret_cast<const std::int32_t*>(cmaps[h]->ptr), cur_stream());
     }
     // identity at the row's own column (written after the stripe scatter,
@@ -928,8 +936,12 @@ Mat materialize_transform(const EchelonOutput& out) {
   }
   if (!ones.empty()) {
     auto pb = upload_i32(ones);
-    dev::set_entries(t.data(), t.ld(), reinterpret_cast<const std::int32_t*>(pb->ptr),
-                     std::int64_t(ones.size() / 2), 1, cur_stream());
+    if (es == 4)
+      dev::set_entries_u32(t.data(), t.ld(), reinterpret_cast<const std::int32_t*>(pb->ptr),
+                           std::int64_t(ones.size() / 2), 1, cur_stream());
+    else
+      dev::set_entries(t.data(), t.ld(), reinterpret_cast<const std::int32_t*>(pb->ptr),
+                       std::int64_t(ones.size() / 2), 1, cur_stream());
   }
   return t;
 }

@@ -3,6 +3,7 @@
 #include "io.hpp"
 
 #include <charconv>
+#include <cstring>
 #include <fstream>
 #include <istream>
 #include <ostream>
@@ -12,15 +13,17 @@ namespace {
 
 // One matrix row as "v v v\n": a matrix body line (reference :175-186).
 void put_rows(std::ostream& out, const std::uint8_t* data, std::int64_t rows, std::int64_t cols,
-              std::int64_t ld) {
+              std::int64_t ld, int esize) {
   std::string line;
-  char buf[4];
+  char buf[12];
   for (std::int64_t r = 0; r < rows; ++r) {
     line.clear();
     const std::uint8_t* row = data + r * ld;
     for (std::int64_t c = 0; c < cols; ++c) {
       if (c) line.push_back(' ');
-      const auto res = std::to_chars(buf, buf + sizeof buf, unsigned(row[c]));
+      unsigned v = row[c];
+      if (esize == 4) std::memcpy(&v, row + 4 * c, 4);
+      const auto res = std::to_chars(buf, buf + sizeof buf, v);
       line.append(buf, res.ptr);
     }
     line.push_back('\n');
@@ -35,7 +38,7 @@ void put_matrix(std::ostream& out, const Mat& m) {
     return;
   }
   const std::vector<std::uint8_t> h = m.to_host();
-  put_rows(out, h.data(), m.rows(), m.cols(), m.cols());
+  put_rows(out, h.data(), m.rows(), m.cols(), m.row_bytes(), m.esize());
 }
 
 // reference src/io.cpp:143-153 (write_field_line); `code` is a field code
@@ -175,7 +178,8 @@ GfMatHost read_gfmat(std::istream& in, const std::string& name) {
   m.p = code;
   m.rows = std::int64_t(rows);
   m.cols = std::int64_t(cols);
-  m.data.resize(std::size_t(rows * cols));
+  m.esize = FieldSpec(code).esize();
+  m.data.resize(std::size_t(rows * cols) * std::size_t(m.esize));
   for (std::uint64_t r = 0; r < rows; ++r) {
     const std::string line = lr.expect("a matrix row");
     const char* s = line.data();
@@ -190,7 +194,10 @@ GfMatHost read_gfmat(std::istream& in, const std::string& name) {
         lr.fail("invalid entry");
       if (v >= q) lr.fail("entry '" + std::to_string(v) + "' is not an element encoding");
       if (c >= cols) lr.fail("too many entries in row");
-      m.data[std::size_t(r * cols + c)] = std::uint8_t(v);
+      if (m.esize == 4)
+        std::memcpy(&m.data[std::size_t(r * cols + c) * 4], &v, 4);
+      else
+        m.data[std::size_t(r * cols + c)] = std::uint8_t(v);
       ++c;
       s = res.ptr;
     }

@@ -1,8 +1,8 @@
 // io.hpp -- the reference's text formats for the cmd_ech drop-in (SURVEY
 // §8f item 3): GFMAT v1 matrices, SELECTS v1 and TRANSFORM v1 files
 // (reference include/gfrref/io.hpp:17-45, src/io.cpp:143-286), written
-// byte-identically from device-resident outputs.  Prime fields only (the
-// B200 path stores residues as one byte, p <= 251).
+// byte-identically from device-resident outputs.  Every field of the
+// reference (u32 elements for p > 251 / p^k > 256).
 #pragma once
 
 #include <cstdint>
@@ -24,7 +24,8 @@ struct ParseError : std::invalid_argument {
 struct GfMatHost {
   std::uint32_t p = 2;
   std::int64_t rows = 0, cols = 0;
-  std::vector<std::uint8_t> data;  // row-major, ld = cols
+  int esize = 1;                   // bytes per element (4: wide field)
+  std::vector<std::uint8_t> data;  // row-major, ld = cols * esize
 };
 
 GfMatHost read_gfmat(std::istream& in, const std::string& name);

@@ -41,18 +41,40 @@ const std::int32_t* dptr(const std::shared_ptr<DevBuf>& b) {
 // out = select(A | B) by optional row/column maps (kernels.hpp select2d).
 Mat select(std::int64_t rows, std::int64_t cols, const Mat& A, const Mat* B,
            const std::vector<std::int32_t>* rmap, const std::vector<std::int32_t>* cmap) {
-  Mat out(rows, cols);
+  // element size of the result: the sources' (an empty source carries no
+  // storage and may have been made without one)
+  int es = A.esize();
+  if (B && B->esize() != es) {
+    if (A.empty())
+      es = B->esize();
+    else if (!B->empty())
+      throw std::invalid_argument("select: element sizes of the sources disagree");
+  }
+  Mat out(rows, cols, es);
   if (out.empty()) return out;
+  // wide elements: the byte-level kernels get byte columns and a byte map
+  std::vector<std::int32_t> bmap;
+  if (es != 1 && cmap) {
+    bmap.resize(cmap->size() * std::size_t(es));
+    for (std::size_t j = 0; j < cmap->size(); ++j) {
+      const std::int32_t v = (*cmap)[j];
+      for (int b = 0; b < es; ++b)
+        bmap[j * std::size_t(es) + std::size_t(b)] =
+            v >= 0 ? v * es + b : (v == -1 ? -1 : -((-v - 2) * es + b) - 2);
+    }
+    cmap = &bmap;
+  }
+  const std::int64_t bcols = cols * es;
   // small maps ride in the launch parameters (no upload call)
   static const bool inline_maps = std::getenv("GFQ_NO_INLINE_MAPS") == nullptr;
   if (inline_maps &&
-      dev::select2d_inline(out.data(), out.ld(), rows, cols, A.data(), A.ld(), B ? B->data() : nullptr,
+      dev::select2d_inline(out.data(), out.ld(), rows, bcols, A.data(), A.ld(), B ? B->data() : nullptr,
                            B ? B->ld() : 0, rmap ? rmap->data() : nullptr,
                            cmap ? cmap->data() : nullptr, cur_stream()))
     return out;
   auto rb = rmap ? upload_i32(*rmap) : nullptr;
   auto cb = cmap ? upload_i32(*cmap) : nullptr;
-  dev::select2d(out.data(), out.ld(), rows, cols, A.data(), A.ld(), B ? B->data() : nullptr,
+  dev::select2d(out.data(), out.ld(), rows, bcols, A.data(), A.ld(), B ? B->data() : nullptr,
                 B ? B->ld() : 0, dptr(rb), dptr(cb), cur_stream());
   return out;
 }
@@ -70,12 +92,16 @@ int ech_mode() { return g_ech_mode; }
 
 void random_fill_exact(std::uint32_t p, std::int64_t rows, std::int64_t cols, std::uint64_t seed,
                        std::uint64_t draw0, std::int64_t draw_ld, std::uint8_t* dst,
-                       std::int64_t ld) {
+                       std::int64_t ld, int esize) {
   if (rows == 0 || cols == 0) return;
   DevBuf rej{4};
   dev::fill2d(rej.ptr, 4, 1, 4, 0, cur_stream());
-  dev::random_fill(p, rows, cols, seed, draw0, draw_ld, dst, ld,
-                   reinterpret_cast<std::uint32_t*>(rej.ptr), cur_stream());
+  if (esize == 4)
+    dev::random_fill_wide(p, rows, cols, seed, draw0, draw_ld, dst, ld,
+                          reinterpret_cast<std::uint32_t*>(rej.ptr), cur_stream());
+  else
+    dev::random_fill(p, rows, cols, seed, draw0, draw_ld, dst, ld,
+                     reinterpret_cast<std::uint32_t*>(rej.ptr), cur_stream());
   std::int32_t nrej = 0;
   download_i32(reinterpret_cast<const std::int32_t*>(rej.ptr), &nrej, 1);
   if (nrej != 0)
@@ -95,6 +121,10 @@ void field_mad(const FieldSpec& f, std::int64_t m, std::int64_t n, std::int64_t 
                const std::uint8_t* A, std::int64_t lda, const std::uint8_t* B, std::int64_t ldb,
                const std::uint8_t* Cin, std::int64_t ldc, std::uint8_t* D, std::int64_t ldd,
                cudaStream_t s) {
+  if (f.wide()) {
+    dev::mad_wide(f.wide_dev(), m, n, k, A, lda, B, ldb, Cin, ldc, D, ldd, s);
+    return;
+  }
   if (!f.is_ext()) {
     // K1f (FP4 tensor cores) for the small fields: its packed operands live
     // in a stream-ordered scratch block on this (the current) stream
@@ -116,7 +146,7 @@ static Mat mul_add_kernel(const FieldSpec& f, const Mat* addend, const Mat& b, c
   if (addend && (addend->rows() != b.rows() || addend->cols() != c.cols()))
     throw std::invalid_argument("mad: addend shape mismatch");
   const std::int64_t m = b.rows(), inner = b.cols(), n = c.cols();
-  Mat out(m, n);
+  Mat out(m, n, f.esize());
   if (m == 0 || n == 0) return out;
   field_mad(f, m, n, inner, b.data(), b.ld(), c.data(), c.ld(),
             addend ? addend->data() : nullptr, addend ? addend->ld() : 0, out.data(), out.ld(),
@@ -300,7 +330,10 @@ Mat adi(const Mat& k, const BitString& delta) {
     }
   if (!pos.empty()) {
     auto pb = upload_i32(pos);
-    dev::set_entries(out.data(), out.ld(), dptr(pb), std::int64_t(pos.size() / 2), 1, cur_stream());
+    if (out.esize() == 4)
+      dev::set_entries_u32(out.data(), out.ld(), dptr(pb), std::int64_t(pos.size() / 2), 1, cur_stream());
+    else
+      dev::set_entries(out.data(), out.ld(), dptr(pb), std::int64_t(pos.size() / 2), 1, cur_stream());
   }
   return out;
 }
@@ -314,9 +347,12 @@ namespace {
 EchResult direct_ech(const FieldSpec& f, const Mat& h) {
   const std::int64_t a = h.rows(), b = h.cols();
   const std::int64_t rmax = std::min(a, b);
-  Mat W(a, b), Tc(a, rmax > 0 ? rmax : 1);
+  Mat W(a, b, f.esize()), Tc(a, rmax > 0 ? rmax : 1, f.esize());
   auto info = std::make_shared<DevBuf>(std::size_t(4 * (2 * rmax + 1)));
-  if (f.is_ext())
+  if (f.wide())
+    dev::ech_base_wide(f.wide_dev(), a, b, h.data(), h.ld(), W.data(), W.ld(), Tc.data(), Tc.ld(),
+                       reinterpret_cast<std::int32_t*>(info->ptr), cur_stream());
+  else if (f.is_ext())
     dev::ech_base_ext(f.ext_dev(), a, b, h.data(), h.ld(), W.data(), W.ld(), Tc.data(), Tc.ld(),
                       reinterpret_cast<std::int32_t*>(info->ptr), cur_stream());
   else
@@ -588,7 +624,7 @@ EchResult combine_horizontal(const FieldSpec& f, const Mat& h2, const EchResult&
   out.M = rrf(lam, hcat(ma, mb), hcat(mc, e2.M));
   out.R = rrf(lam, mad(f, r1_rest, e_mid, e2.R), e2.R);
   const Mat k_bottom_left = mul(f, mad(f, a_rest, e2.K, a_sel), e1.M);
-  out.K = vcat(hcat(e1.K, Mat::zeros(e1.K.rows(), std::int64_t(e2.rho.size()))),
+  out.K = vcat(hcat(e1.K, Mat::zeros(e1.K.rows(), std::int64_t(e2.rho.size()), f.esize())),
                hcat(k_bottom_left, e2.K));
   out.rho = shifted_union(e1.rho, e2.rho, std::size_t(alpha1), std::size_t(alpha1 + h2.rows()));
   return out;
@@ -610,7 +646,7 @@ EchResult combine_vertical(const FieldSpec& f, const Mat& h2, const EchResult& e
   out.gamma = shifted_union(e1.gamma, e2.gamma, std::size_t(beta1), std::size_t(beta1 + h2.cols()));
   out.M = col_riffle(u, vcat(mad(f, e1.M, x_piv, g), g), vcat(mul(f, x_piv, e2.M), e2.M));
   out.R = vcat(hcat(e1.R, mad(f, x_rest, x_piv, e2.R)),
-               hcat(Mat::zeros(std::int64_t(e2.rho.size()), e1.R.cols()), e2.R));
+               hcat(Mat::zeros(std::int64_t(e2.rho.size()), e1.R.cols(), f.esize()), e2.R));
   out.K = col_riffle(u, mad(f, k1_rest, e2.K, k1_sel), e2.K);
   return out;
 }
@@ -627,16 +663,16 @@ EchResult ech(const FieldSpec& f, const Mat& h, std::size_t threshold) {
   const std::int64_t alpha = h.rows(), beta = h.cols();
   if (alpha == 0 || beta == 0) {
     EchResult e;
-    e.M = Mat(0, 0);
-    e.K = Mat(alpha, 0);
-    e.R = Mat(0, beta);
+    e.M = Mat(0, 0, f.esize());
+    e.K = Mat(alpha, 0, f.esize());
+    e.R = Mat(0, beta, f.esize());
     e.rho = IndexSet(std::size_t(alpha), {});
     e.gamma = IndexSet(std::size_t(beta), {});
     return e;
   }
   // GF(p^k): the reference's split/combine recursion (its products are
   // digit-plane K1 contractions) over the table-driven base case
-  if (ech_mode() != 1 && !f.is_ext()) {
+  if (ech_mode() != 1 && !f.is_ext() && !f.wide()) {
     // GF(2): the 8-CTA cluster kernel takes blocks of <= 1024 rows with
     // rows + cols <= 8192; anything larger follows the reference's own
     // split rule (src/jobs.cpp:202-225: rows when alpha >= beta, else
@@ -662,7 +698,8 @@ EchResult ech(const FieldSpec& f, const Mat& h, std::size_t threshold) {
     const EchResult e1 = ech(f, h.row_view(0, alpha1), threshold);
     return combine_horizontal(f, h.row_view(alpha1, alpha - alpha1), e1, alpha1, threshold);
   }
-  const std::int64_t base = std::int64_t(std::min(threshold, ech_base()));
+  std::int64_t base = std::int64_t(std::min(threshold, ech_base()));
+  if (f.wide()) base = std::min<std::int64_t>(base, dev::kEchBaseWideMax);
   if (alpha <= base && beta <= base) return direct_ech(f, h);
   if (alpha >= beta) {
     const std::int64_t alpha1 = split_of(alpha);

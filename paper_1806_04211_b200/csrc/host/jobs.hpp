@@ -56,9 +56,10 @@ Mat hcat(const Mat& a, const Mat& b);                                 // matrix.
 /// entry (r, c) takes draw draw0 + r * draw_ld + c.  A draw in the
 /// rejection band (probability < 2^-56 per draw) would shift the reference's
 /// stream; that case is reported (std::runtime_error), never silently wrong.
+/// esize 4: u32 elements (wide fields; p is then the field order).
 void random_fill_exact(std::uint32_t p, std::int64_t rows, std::int64_t cols, std::uint64_t seed,
                        std::uint64_t draw0, std::int64_t draw_ld, std::uint8_t* dst,
-                       std::int64_t ld);
+                       std::int64_t ld, int esize = 1);
 
 /// Tunable: largest block the K2 base-case kernel takes (<= kEchBaseMax).
 void set_ech_base(std::size_t n);

@@ -160,6 +160,13 @@ struct ExtTablesHost {
   mutable std::once_flag dev_once;
   mutable std::uint8_t* dev = nullptr;
   mutable dev::ExtTables view{};
+  // wide extension fields (q > 256): log / antilog / Zech tables of a
+  // generator g of GF(q)* (the reference's own representation,
+  // src/field.cpp:180-212); zech[n] = log(1 + g^n), -1 where 1 + g^n = 0
+  bool wide = false;
+  std::vector<std::uint32_t> wexp, wlog;
+  std::vector<std::int32_t> wzech;
+  mutable std::uint32_t* wdev = nullptr;
 };
 
 namespace {
@@ -229,6 +236,89 @@ std::shared_ptr<const ExtTablesHost> make_ext(std::uint32_t p, std::uint32_t k, 
   }
   return t;
 }
+
+// Wide GF(p^k) (256 < q < 2^20): the tables above would be q x q, so the
+// field is held as log / antilog / Zech tables built from polynomial
+// products mod the modulus.
+std::shared_ptr<const ExtTablesHost> make_ext_wide(std::uint32_t p, std::uint32_t k, Poly mod) {
+  auto t = std::make_shared<ExtTablesHost>();
+  std::uint32_t q = 1;
+  for (std::uint32_t i = 0; i < k; ++i) q *= p;
+  t->p = p;
+  t->k = k;
+  t->q = q;
+  t->modulus = mod;
+  t->wide = true;
+  const auto decode = [&](std::uint32_t e) {
+    Poly d(k, 0);
+    for (std::uint32_t i = 0; i < k; ++i) {
+      d[i] = e % p;
+      e /= p;
+    }
+    return d;
+  };
+  const auto encode = [&](const Poly& d) {
+    std::uint32_t v = 0;
+    for (std::uint32_t i = k; i-- > 0;) v = v * p + (i < d.size() ? d[i] : 0);
+    return v;
+  };
+  const auto mulenc = [&](std::uint32_t a, std::uint32_t b) {
+    const Poly da = decode(a), db = decode(b);
+    Poly prod(2 * k - 1, 0);
+    for (std::uint32_t i = 0; i < k; ++i)
+      for (std::uint32_t j = 0; j < k; ++j)
+        prod[i + j] = std::uint32_t((prod[i + j] + std::uint64_t(da[i]) * db[j]) % p);
+    return encode(poly_mod(prod, mod, p));
+  };
+  const auto powenc = [&](std::uint32_t a, std::uint64_t e) {
+    std::uint32_t r = 1;
+    while (e) {
+      if (e & 1) r = mulenc(r, a);
+      a = mulenc(a, a);
+      e >>= 1;
+    }
+    return r;
+  };
+  // the prime factors of q - 1 and the smallest generator
+  std::vector<std::uint32_t> fac;
+  {
+    std::uint32_t n = q - 1;
+    for (std::uint32_t d = 2; d * d <= n; ++d)
+      if (n % d == 0) {
+        fac.push_back(d);
+        while (n % d == 0) n /= d;
+      }
+    if (n > 1) fac.push_back(n);
+  }
+  std::uint32_t g = 0;
+  for (std::uint32_t c = 2; c < q && !g; ++c) {
+    bool ok = true;
+    for (std::uint32_t r : fac)
+      if (powenc(c, (q - 1) / r) == 1) {
+        ok = false;
+        break;
+      }
+    if (ok) g = c;
+  }
+  if (!g) throw std::logic_error("field: no generator found");
+  t->wexp.resize(q - 1);
+  t->wlog.assign(q, 0);
+  std::uint32_t x = 1;
+  for (std::uint32_t i = 0; i + 1 < q; ++i) {
+    t->wexp[i] = x;
+    t->wlog[x] = i;
+    x = mulenc(x, g);
+  }
+  t->wzech.resize(q - 1);
+  for (std::uint32_t n = 0; n + 1 < q; ++n) {
+    const Poly d = decode(t->wexp[n]);
+    Poly e = d;
+    e[0] = (e[0] + 1) % p;  // 1 + g^n
+    const std::uint32_t v = encode(e);
+    t->wzech[n] = v == 0 ? -1 : std::int32_t(t->wlog[v]);
+  }
+  return t;
+}
 }  // namespace
 
 FieldSpec::FieldSpec(std::uint32_t p) {
@@ -243,8 +333,7 @@ FieldSpec::FieldSpec(std::uint32_t p) {
     return;
   }
   if (!is_prime(p)) throw std::invalid_argument("field: p must be prime");
-  if (p > 251)
-    throw std::invalid_argument("field: the B200 path stores residues as u8 (p <= 251)");
+  if (p >= (1u << 16)) throw std::invalid_argument("field: p must be < 2^16");
   p_ = q_ = p;
 }
 
@@ -262,8 +351,6 @@ FieldSpec::FieldSpec(std::uint32_t p, std::uint32_t k, std::vector<std::uint32_t
     *this = FieldSpec(p);
     return;
   }
-  if (q > 256)
-    throw std::invalid_argument("field: the B200 path stores elements as u8 (p^k <= 256)");
   if (modulus.empty()) modulus = default_modulus(p, k);
   if (modulus.size() != std::size_t(k) + 1 || modulus[k] != 1)
     throw std::invalid_argument("field: modulus must be monic of degree k");
@@ -279,7 +366,7 @@ FieldSpec::FieldSpec(std::uint32_t p, std::uint32_t k, std::vector<std::uint32_t
       ext_ = e;
       return;
     }
-  auto t = make_ext(p, k, modulus);
+  auto t = q > 256 ? make_ext_wide(p, k, modulus) : make_ext(p, k, modulus);
   const_cast<ExtTablesHost&>(*t).code = kFieldCode0 + std::uint32_t(g_fields->size());
   g_fields->push_back(t);
   ext_ = t;
@@ -292,18 +379,37 @@ const std::vector<std::uint32_t>& FieldSpec::modulus() const {
   return ext_ ? ext_->modulus : prime_mod;
 }
 
+namespace {
+// base-p digit-wise a + s.b of two encoded GF(p^k) elements (s = 1 or p-1)
+Elem digit_axpy(Elem a, Elem b, std::uint32_t s, std::uint32_t p, std::uint32_t k) {
+  Elem r = 0, m = 1;
+  for (std::uint32_t i = 0; i < k; ++i) {
+    r += Elem((a % p + std::uint64_t(s) * (b % p)) % p) * m;
+    a /= p;
+    b /= p;
+    m *= p;
+  }
+  return r;
+}
+}  // namespace
+
 Elem FieldSpec::add(Elem a, Elem b) const {
+  if (ext_ && ext_->wide) return digit_axpy(a, b, 1, p_, k_);
   return ext_ ? ext_->add[std::size_t(a) * q_ + b] : (a + b) % p_;
 }
 Elem FieldSpec::neg(Elem a) const {
+  if (ext_ && ext_->wide) return digit_axpy(0, a, p_ - 1, p_, k_);
   return ext_ ? ext_->neg[a] : (a == 0 ? 0 : p_ - a);
 }
 Elem FieldSpec::mul(Elem a, Elem b) const {
+  if (ext_ && ext_->wide)
+    return (a == 0 || b == 0) ? 0 : ext_->wexp[(std::uint64_t(ext_->wlog[a]) + ext_->wlog[b]) % (q_ - 1)];
   return ext_ ? ext_->mul[std::size_t(a) * q_ + b] : Elem(std::uint64_t(a) * b % p_);
 }
 
 Elem FieldSpec::inv(Elem a) const {
   if (a % q_ == 0) throw std::domain_error("field: inverse of zero");
+  if (ext_ && ext_->wide) return ext_->wexp[(q_ - 1 - ext_->wlog[a] % (q_ - 1)) % (q_ - 1)];
   if (ext_) return ext_->inv[a];
   std::uint64_t r = 1, b = a % p_;
   std::uint32_t e = p_ - 2;
@@ -315,8 +421,30 @@ Elem FieldSpec::inv(Elem a) const {
   return Elem(r);
 }
 
+dev::WideField FieldSpec::wide_dev() const {
+  dev::WideField w{p_, k_, q_, nullptr, nullptr, nullptr};
+  if (!ext_) return w;
+  const ExtTablesHost& t = *ext_;
+  if (!t.wide) throw std::logic_error("FieldSpec::wide_dev on a u8 extension field");
+  std::call_once(t.dev_once, [&] {
+    const std::size_t n = (t.q - 1) + t.q + (t.q - 1);
+    GFQ_CUDA(cudaMalloc(&t.wdev, n * 4));  // process lifetime, like the field registry
+    std::vector<std::uint32_t> all;
+    all.reserve(n);
+    all.insert(all.end(), t.wexp.begin(), t.wexp.end());
+    all.insert(all.end(), t.wlog.begin(), t.wlog.end());
+    for (std::int32_t z : t.wzech) all.push_back(std::uint32_t(z));
+    GFQ_CUDA(cudaMemcpy(t.wdev, all.data(), n * 4, cudaMemcpyHostToDevice));
+  });
+  w.exp = t.wdev;
+  w.log = t.wdev + (t.q - 1);
+  w.zech = reinterpret_cast<const std::int32_t*>(t.wdev + (t.q - 1) + t.q);
+  return w;
+}
+
 const dev::ExtTables& FieldSpec::ext_dev() const {
   if (!ext_) throw std::logic_error("FieldSpec::ext_dev on a prime field");
+  if (ext_->wide) throw std::logic_error("FieldSpec::ext_dev on a wide extension field");
   const ExtTablesHost& t = *ext_;
   std::call_once(t.dev_once, [&] {
     const std::size_t q = t.q, k = t.k;
@@ -538,17 +666,18 @@ std::int64_t live_device_bytes() { return g_live; }
 std::int64_t peak_device_bytes() { return g_peak; }
 void reset_peak_device_bytes() { g_peak = g_live.load(); }
 
-Mat::Mat(std::int64_t rows, std::int64_t cols) : rows_(rows), cols_(cols) {
+Mat::Mat(std::int64_t rows, std::int64_t cols, int esize) : rows_(rows), cols_(cols), esize_(esize) {
   if (rows < 0 || cols < 0) throw std::invalid_argument("matrix: negative shape");
-  ld_ = round_up(cols > 0 ? cols : 1, 16);
+  if (esize != 1 && esize != 4) throw std::invalid_argument("matrix: element size must be 1 or 4");
+  ld_ = round_up(cols > 0 ? cols * esize : 1, 16);
   if (rows > 0 && cols > 0) {
     buf_ = std::make_shared<DevBuf>(std::size_t(rows) * std::size_t(ld_));
     data_ = buf_->ptr;
   }
 }
 
-Mat Mat::zeros(std::int64_t rows, std::int64_t cols) {
-  Mat m(rows, cols);
+Mat Mat::zeros(std::int64_t rows, std::int64_t cols, int esize) {
+  Mat m(rows, cols, esize);
   if (!m.empty()) {
     hprof::Scope hp(hprof::kMemset);
     dev::fill2d(m.data_, m.ld_, rows, m.ld_, 0, cur_stream());
@@ -557,11 +686,11 @@ Mat Mat::zeros(std::int64_t rows, std::int64_t cols) {
 }
 
 Mat Mat::from_host(std::int64_t rows, std::int64_t cols, const std::uint8_t* src,
-                   std::int64_t ld) {
-  Mat m(rows, cols);
+                   std::int64_t ld, int esize) {
+  Mat m(rows, cols, esize);
   if (!m.empty()) {
     GFQ_CUDA(cudaMemcpy2DAsync(m.data_, std::size_t(m.ld_), src, std::size_t(ld),
-                               std::size_t(cols), std::size_t(rows), cudaMemcpyHostToDevice,
+                               std::size_t(cols * esize), std::size_t(rows), cudaMemcpyHostToDevice,
                                cur_stream()));
     // pageable source: make the copy complete before the caller may reuse it
     GFQ_CUDA(cudaStreamSynchronize(cur_stream()));
@@ -570,13 +699,14 @@ Mat Mat::from_host(std::int64_t rows, std::int64_t cols, const std::uint8_t* src
 }
 
 Mat Mat::view_of(std::shared_ptr<DevBuf> buf, std::size_t offset, std::int64_t rows,
-                 std::int64_t cols, std::int64_t ld) {
+                 std::int64_t cols, std::int64_t ld, int esize) {
   Mat v;
   v.rows_ = rows;
   v.cols_ = cols;
   v.ld_ = ld;
+  v.esize_ = esize;
   if (rows > 0 && cols > 0) {
-    if (!buf || offset + std::size_t((rows - 1) * ld + cols) > buf->bytes)
+    if (!buf || offset + std::size_t((rows - 1) * ld + cols * esize) > buf->bytes)
       throw std::invalid_argument("matrix: view outside its allocation");
     v.data_ = buf->ptr + offset;
   }
@@ -591,6 +721,7 @@ Mat Mat::row_view(std::int64_t r0, std::int64_t n) const {
   v.rows_ = n;
   v.cols_ = cols_;
   v.ld_ = ld_;
+  v.esize_ = esize_;
   v.data_ = (data_ && n > 0 && cols_ > 0) ? data_ + r0 * ld_ : nullptr;
   return v;
 }
@@ -602,20 +733,21 @@ Mat Mat::col_view(std::int64_t c0, std::int64_t n) const {
   v.rows_ = rows_;
   v.cols_ = n;
   v.ld_ = ld_;
-  v.data_ = (data_ && n > 0 && rows_ > 0) ? data_ + c0 : nullptr;
+  v.esize_ = esize_;
+  v.data_ = (data_ && n > 0 && rows_ > 0) ? data_ + c0 * esize_ : nullptr;
   return v;
 }
 
 void Mat::to_host(std::uint8_t* dst, std::int64_t ld) const {
   if (empty()) return;
-  GFQ_CUDA(cudaMemcpy2DAsync(dst, std::size_t(ld), data_, std::size_t(ld_), std::size_t(cols_),
+  GFQ_CUDA(cudaMemcpy2DAsync(dst, std::size_t(ld), data_, std::size_t(ld_), std::size_t(cols_ * esize_),
                              std::size_t(rows_), cudaMemcpyDeviceToHost, cur_stream()));
   GFQ_CUDA(cudaStreamSynchronize(cur_stream()));
 }
 
 std::vector<std::uint8_t> Mat::to_host() const {
-  std::vector<std::uint8_t> out(std::size_t(rows_) * std::size_t(cols_));
-  to_host(out.data(), cols_ > 0 ? cols_ : 1);
+  std::vector<std::uint8_t> out(std::size_t(rows_) * std::size_t(cols_) * std::size_t(esize_));
+  to_host(out.data(), cols_ > 0 ? cols_ * esize_ : 1);
   return out;
 }
 

@@ -29,18 +29,21 @@ using Elem = std::uint32_t;
 struct ExtTablesHost;
 namespace dev {
 struct ExtTables;
+struct WideField;
 }
 
-/// GF(q), q = p^k <= 256: one element per byte, encoded like the reference
+/// GF(q), q = p^k, elements encoded like the reference
 /// (include/gfrref/field.hpp:12-14: sum_i c_i p^i).  Mirrors reference
 /// FieldSpec (include/gfrref/field.hpp:20-110, src/field.cpp:143-237):
-/// FieldSpec(p) is the prime field, FieldSpec(p, k, modulus) the extension
-/// with a monic irreducible modulus (empty: the lexicographically first one,
-/// constant coefficient varying fastest).  Prime fields need p <= 251,
-/// extension fields p^k <= 256 (u8 storage; the reference allows p < 2^16,
-/// p^k < 2^20).  code(): the integer the C ABI passes as "p" -- p itself for
-/// a prime field, a registered id >= 0x10000 for an extension field
-/// (FieldSpec(code) resolves either).
+/// FieldSpec(p) is the prime field (p < 2^16), FieldSpec(p, k, modulus) the
+/// extension with a monic irreducible modulus (empty: the lexicographically
+/// first one, constant coefficient varying fastest), p^k < 2^20.  Storage:
+/// one byte per element when p <= 251 (prime) or q <= 256 (extension), the
+/// tensor-core path; four bytes (u32) otherwise ("wide" fields: SIMT
+/// contraction, the reference's split/combine ECH over a one-CTA base case).
+/// code(): the integer the C ABI passes as "p" -- p itself for a prime
+/// field, a registered id >= 0x10000 for an extension field (FieldSpec(code)
+/// resolves either).
 class FieldSpec {
  public:
   explicit FieldSpec(std::uint32_t p_or_code);
@@ -49,6 +52,10 @@ class FieldSpec {
   std::uint32_t k() const { return k_; }
   std::uint32_t order() const { return q_; }
   bool is_ext() const { return k_ > 1; }
+  /// u32 storage (p > 251 or q > 256)
+  bool wide() const { return k_ > 1 ? q_ > 256 : p_ > 251; }
+  /// bytes per stored element
+  int esize() const { return wide() ? 4 : 1; }
   std::uint32_t code() const;
   const std::vector<std::uint32_t>& modulus() const;
   Elem add(Elem a, Elem b) const;
@@ -64,6 +71,9 @@ class FieldSpec {
   }
   /// Device tables (extension fields only; uploaded on first use).
   const dev::ExtTables& ext_dev() const;
+  /// Device view of a wide field (log / antilog / Zech tables for wide
+  /// extension fields, uploaded on first use).
+  dev::WideField wide_dev() const;
 
  private:
   std::uint32_t p_ = 0, k_ = 1, q_ = 0;
@@ -101,27 +111,31 @@ std::int64_t live_device_bytes();
 std::int64_t peak_device_bytes();
 void reset_peak_device_bytes();
 
-/// Device-resident dense u8 matrix.  Zero-dimensional shapes carry no
-/// storage.  Values are immutable once published (jobs return fresh
-/// matrices); row/column views share the parent's storage.
+/// Device-resident dense matrix of u8 (esize 1) or u32 (esize 4, wide
+/// fields) elements.  Zero-dimensional shapes carry no storage.  Values are
+/// immutable once published (jobs return fresh matrices); row/column views
+/// share the parent's storage.  cols() counts elements, ld() bytes.
 class Mat {
  public:
   Mat() = default;
-  Mat(std::int64_t rows, std::int64_t cols);  // uninitialised storage
-  static Mat zeros(std::int64_t rows, std::int64_t cols);
+  Mat(std::int64_t rows, std::int64_t cols, int esize = 1);  // uninitialised storage
+  static Mat zeros(std::int64_t rows, std::int64_t cols, int esize = 1);
   static Mat from_host(std::int64_t rows, std::int64_t cols, const std::uint8_t* src,
-                       std::int64_t ld);
+                       std::int64_t ld, int esize = 1);
 
   std::int64_t rows() const { return rows_; }
   std::int64_t cols() const { return cols_; }
   std::int64_t ld() const { return ld_; }
+  int esize() const { return esize_; }
+  /// bytes of one row's elements
+  std::int64_t row_bytes() const { return cols_ * esize_; }
   std::uint8_t* data() const { return data_; }
   bool empty() const { return rows_ == 0 || cols_ == 0; }
 
   /// A matrix living inside an existing allocation (e.g. a received
   /// broadcast payload): rows x cols at byte `offset`, row stride ld.
   static Mat view_of(std::shared_ptr<DevBuf> buf, std::size_t offset, std::int64_t rows,
-                     std::int64_t cols, std::int64_t ld);
+                     std::int64_t cols, std::int64_t ld, int esize = 1);
   /// Rows [r0, r0+n) as a view (no copy).
   Mat row_view(std::int64_t r0, std::int64_t n) const;
   /// Columns [c0, c0+n) as a view (no copy; may lose 16-byte alignment).
@@ -131,12 +145,13 @@ class Mat {
   std::vector<std::uint8_t> to_host() const;
 
   /// Bytes accounted to this value (reference Matrix::byte_size analogue).
-  std::size_t byte_size() const { return std::size_t(rows_) * std::size_t(cols_) + 48; }
+  std::size_t byte_size() const { return std::size_t(rows_) * std::size_t(cols_) * std::size_t(esize_) + 48; }
 
  private:
   std::shared_ptr<DevBuf> buf_;
   std::uint8_t* data_ = nullptr;
   std::int64_t rows_ = 0, cols_ = 0, ld_ = 0;
+  int esize_ = 1;
 };
 
 /// A sorted subset of {0, ..., universe-1} (reference include/gfrref/matrix.hpp:53-70).

@@ -15,6 +15,7 @@ namespace {
 
 struct Mismatch {
   DevBuf buf{16};
+  int es = 1;  // element bytes of the compared matrices (positions come back in bytes)
   Mismatch() {
     const unsigned long long init[2] = {0ull, ~0ull};
     GFQ_CUDA(cudaMemcpyAsync(buf.ptr, init, sizeof init, cudaMemcpyHostToDevice, cur_stream()));
@@ -26,13 +27,47 @@ struct Mismatch {
     unsigned long long h[2];
     GFQ_CUDA(cudaMemcpyAsync(h, buf.ptr, sizeof h, cudaMemcpyDeviceToHost, cur_stream()));
     GFQ_CUDA(cudaStreamSynchronize(cur_stream()));
-    return {h[0], h[1]};
+    // (the count is of bytes for wide elements: a differing element counts
+    // once per differing byte; the first position is returned in elements)
+    return {h[0], es == 1 || h[0] == 0 ? h[1] : h[1] / std::uint64_t(es)};
   }
 };
 
-void cmp(const Mat& a, const Mat* b, int mode, std::uint8_t value, Mismatch& mm) {
-  dev::compare(a.rows(), a.cols(), a.data(), a.ld(), b ? b->data() : nullptr, b ? b->ld() : 0,
-               mode, value, mm.dev(), cur_stream());
+// a == b (mode 0), a == 0 (mode 1), a == value.I (mode 2), on u8 or u32
+// elements (wide fields: byte-level compares; value.I as an explicit matrix)
+void cmp(const Mat& a, const Mat* b, int mode, std::uint32_t value, Mismatch& mm) {
+  if (a.esize() == 1) {
+    dev::compare(a.rows(), a.cols(), a.data(), a.ld(), b ? b->data() : nullptr, b ? b->ld() : 0, mode,
+                 std::uint8_t(value), mm.dev(), cur_stream());
+    return;
+  }
+  mm.es = a.esize();
+  Mat vi;
+  if (mode == 2) {
+    vi = Mat::zeros(a.rows(), a.cols(), a.esize());
+    std::vector<std::int32_t> pos;
+    for (std::int64_t i = 0; i < std::min(a.rows(), a.cols()); ++i) {
+      pos.push_back(std::int32_t(i));
+      pos.push_back(std::int32_t(i));
+    }
+    if (!pos.empty()) {
+      auto pb = upload_i32(pos);
+      dev::set_entries_u32(vi.data(), vi.ld(), reinterpret_cast<const std::int32_t*>(pb->ptr),
+                           std::int64_t(pos.size() / 2), value, cur_stream());
+    }
+    b = &vi;
+    mode = 0;
+  }
+  dev::compare(a.rows(), a.row_bytes(), a.data(), a.ld(), b ? b->data() : nullptr, b ? b->ld() : 0, mode, 0,
+               mm.dev(), cur_stream());
+  if (mode == 0 && b == &vi) GFQ_CUDA(cudaStreamSynchronize(cur_stream()));  // vi dies on return
+}
+
+// u8 mask (1 where the u32 element is nonzero) of a wide matrix
+Mat nonzero_mask(const Mat& a) {
+  Mat out(a.rows(), a.cols(), 1);
+  if (!out.empty()) dev::nonzero_mask_u32(a.rows(), a.cols(), a.data(), a.ld(), out.data(), out.ld(), cur_stream());
+  return out;
 }
 
 std::vector<std::uint32_t> complement(std::size_t universe, const std::vector<std::uint32_t>& s) {
@@ -102,7 +137,7 @@ std::string check_exact(const Mat& C, const EchelonOutput& out, const Mat& Rasm,
   Mismatch top_piv, top_rest, bottom;
   if (r > 0) {
     const Mat top = P.row_view(0, r);
-    cmp(take_cols(top, gups), nullptr, 2, std::uint8_t(f.p() - 1), top_piv);
+    cmp(take_cols(top, gups), nullptr, 2, f.neg(1), top_piv);
     if (!grest.empty()) {
       const Mat tr = take_cols(top, grest);
       cmp(tr, &Rasm, 0, 0, top_rest);
@@ -128,8 +163,11 @@ std::string check_freivalds(const Mat& C, const EchelonOutput& out, std::uint64_
   const ChopSpec& ch = out.chop;
   const std::size_t a = ch.a(), b = ch.b();
   const std::int64_t n = C.cols();
-  Mat X(n, s);
-  dev::random_fill(f.p(), n, s, seed, 0, s, X.data(), X.ld(), nullptr, cur_stream());
+  Mat X(n, s, f.esize());
+  if (f.wide())
+    dev::random_fill_wide(f.order(), n, s, seed, 0, s, X.data(), X.ld(), nullptr, cur_stream());
+  else
+    dev::random_fill(f.p(), n, s, seed, 0, s, X.data(), X.ld(), nullptr, cur_stream());
   const Mat Y = mat_mul(f, C, X);  // m x s
   // Y restricted to the pivot rows of each block row (the columns of T_M / T_K).
   std::vector<Mat> Yv(a);
@@ -145,7 +183,7 @@ std::string check_freivalds(const Mat& C, const EchelonOutput& out, std::uint64_
     for (std::size_t h = 0; h < a; ++h)
       if (!Yv[h].empty()) lhs = mat_mul_add(f, lhs, out.T_M_blocks[j][h], Yv[h]);
     // rhs = sum_{l >= j} R(j,l) . X[non-pivot cols of l]   ( = E.X + X_piv)
-    Mat rhs = Mat::zeros(rj, s);
+    Mat rhs = Mat::zeros(rj, s, f.esize());
     for (std::size_t l = j; l < b; ++l) {
       const std::size_t w = ch.col_parts[l] - out.upsilon[l].size();
       if (w == 0) continue;
@@ -223,7 +261,9 @@ VerifyResult verify(const Mat& C, const EchelonOutput& out, VerifyMethod method,
     std::vector<std::int32_t> pc(gups.begin(), gups.end()), rcv(grest.begin(), grest.end());
     auto dpc = upload_i32(pc), drc = upload_i32(rcv);
     Mismatch mm;
-    dev::echelon_check(Rasm.rows(), Rasm.cols(), Rasm.data(), Rasm.ld(),
+    // wide elements: the check reads a nonzero mask (one byte per element)
+    const Mat Rchk = Rasm.esize() == 1 ? Rasm : nonzero_mask(Rasm);
+    dev::echelon_check(Rchk.rows(), Rchk.cols(), Rchk.data(), Rchk.ld(),
                        reinterpret_cast<const std::int32_t*>(dpc->ptr),
                        reinterpret_cast<const std::int32_t*>(drc->ptr), mm.dev(), cur_stream());
     if (auto [c, first] = mm.take(); c)

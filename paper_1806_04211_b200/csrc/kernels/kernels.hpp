@@ -195,6 +195,36 @@ void ech_base_ext(const ExtTables& f, std::int64_t rows, std::int64_t cols, cons
                   std::int64_t ldh, std::uint8_t* W, std::int64_t ldw, std::uint8_t* Tc,
                   std::int64_t ldt, std::int32_t* info, cudaStream_t s);
 
+// ---------------------------------------------------------------- wide fields
+// GF(p), 251 < p < 2^16, and GF(p^k), 256 < p^k < 2^20: u32 elements
+// (wide.cu).  k == 1: prime-field arithmetic; else the log / antilog / Zech
+// tables of FieldSpec::wide_dev (exp: q-1, log: q, zech: q-1 entries).
+struct WideField {
+  std::uint32_t p, k, q;
+  const std::uint32_t* exp;
+  const std::uint32_t* log;
+  const std::int32_t* zech;
+};
+// D = (Cin ? Cin : 0) + A.B over a wide field (byte strides).
+void mad_wide(const WideField& f, std::int64_t m, std::int64_t n, std::int64_t k, const std::uint8_t* A,
+              std::int64_t lda, const std::uint8_t* B, std::int64_t ldb, const std::uint8_t* Cin, std::int64_t ldc,
+              std::uint8_t* D, std::int64_t ldd, cudaStream_t s);
+// ech_base over a wide field (rows, cols <= kEchBaseWideMax).
+constexpr int kEchBaseWideMax = 64;
+void ech_base_wide(const WideField& f, std::int64_t rows, std::int64_t cols, const std::uint8_t* H, std::int64_t ldh,
+                   std::uint8_t* W, std::int64_t ldw, std::uint8_t* Tc, std::int64_t ldt, std::int32_t* info,
+                   cudaStream_t s);
+// dst (u32 elements)[pos[2q]][pos[2q+1]] = value for q < n.
+void set_entries_u32(std::uint8_t* dst, std::int64_t ldd, const std::int32_t* pos, std::int64_t n,
+                     std::uint32_t value, cudaStream_t s);
+// dst[i][j] = (src[i][j] != 0) (u32 source, u8 mask).
+void nonzero_mask_u32(std::int64_t rows, std::int64_t cols, const std::uint8_t* src, std::int64_t lds,
+                      std::uint8_t* dst, std::int64_t ldd, cudaStream_t s);
+// random_fill for a field of order q stored as u32.
+void random_fill_wide(std::uint32_t q, std::int64_t rows, std::int64_t cols, std::uint64_t seed, std::uint64_t draw0,
+                      std::int64_t draw_ld, std::uint8_t* dst, std::int64_t ldd, std::uint32_t* rejects,
+                      cudaStream_t s);
+
 // ---------------------------------------------------------------- K3/K4
 // dst[i][j] = source element chosen by the row map and the column map:
 //   rmap[i] >= 0 -> row rmap[i] of A;  rmap[i] <= -2 -> row (-rmap[i]-2) of B;

@@ -99,12 +99,13 @@ def _vp():
 class FieldSpec:
     """GF(p) or GF(p^k) (reference include/gfrref/field.hpp:20-110).
 
-    ``FieldSpec(p)`` is the prime field (p <= 251 on the B200 path);
+    ``FieldSpec(p)`` is the prime field (p < 2**16);
     ``FieldSpec(p, k, modulus=None)`` the extension field with a monic
     irreducible modulus ``[c0, ..., ck]`` (None: the reference's default,
-    the lexicographically first one), p**k <= 256.  Elements are encoded like
-    the reference, ``sum_i c_i p**i``, one byte each.  ``code`` is the integer
-    the C ABI takes as its field argument (p for a prime field).
+    the lexicographically first one), p**k < 2**20.  Elements are encoded
+    like the reference, ``sum_i c_i p**i``: one byte each for p <= 251 /
+    p**k <= 256 (the tensor-core path), u32 for the "wide" rest.  ``code`` is
+    the integer the C ABI takes as its field argument (p for a prime field).
     """
 
     def __init__(self, p: int, k: int = 1, modulus=None):
@@ -112,8 +113,8 @@ class FieldSpec:
         if k == 1 and modulus is None:
             if p < 2 or any(p % d == 0 for d in range(2, int(p ** 0.5) + 1)):
                 raise ValueError("field: p must be prime")
-            if p > 251:
-                raise ValueError("field: the B200 path stores residues as u8 (p <= 251)")
+            if p >= 1 << 16:
+                raise ValueError("field: p must be < 2^16")
             self.p, self.k, self.q, self.code = p, 1, p, p
             self.modulus = (0, 1)
             return
@@ -137,6 +138,15 @@ class FieldSpec:
 
     def order(self):
         return self.q
+
+    @property
+    def wide(self) -> bool:
+        """u32 element storage (p > 251, or p**k > 256)"""
+        return self.q > 256 if self.k > 1 else self.p > 251
+
+    @property
+    def esize(self) -> int:
+        return 4 if self.wide else 1
 
     def _op(self, op, a, b=0):
         out = ctypes.c_uint32()
@@ -175,15 +185,20 @@ def default_modulus(p: int, k: int):
 class Matrix:
     """Device-resident dense u8 matrix (reference Matrix, include/gfrref/matrix.hpp:15-43)."""
 
-    __slots__ = ("h", "rows", "cols")
+    __slots__ = ("h", "rows", "cols", "esize")
 
-    def __init__(self, handle, rows=None, cols=None):
+    def __init__(self, handle, rows=None, cols=None, esize=None):
         self.h = handle
         if rows is None:
             r, c = ctypes.c_int64(), ctypes.c_int64()
             _check(lib().gfq_mat_shape(handle, ctypes.byref(r), ctypes.byref(c)))
             rows, cols = r.value, c.value
         self.rows, self.cols = int(rows), int(cols)
+        if esize is None:
+            e = ctypes.c_int()
+            _check(lib().gfq_mat_esize(handle, ctypes.byref(e)))
+            esize = e.value
+        self.esize = int(esize)
 
     def __del__(self):
         if self.h and _lib is not None:
@@ -191,21 +206,34 @@ class Matrix:
             self.h = None
 
     @staticmethod
-    def from_numpy(a) -> "Matrix":
-        a = np.ascontiguousarray(np.asarray(a, dtype=np.uint8))
+    def from_numpy(a, esize=None) -> "Matrix":
+        """u8 storage for uint8 arrays, u32 (wide fields) for wider dtypes or
+        esize=4."""
+        a = np.asarray(a)
+        if esize is None:
+            esize = 1 if a.dtype.itemsize == 1 else 4
         if a.ndim != 2:
             raise ValueError("matrix: expected a 2-D array")
         r, c = a.shape
         h = _vp()
+        if esize == 4:
+            a = np.ascontiguousarray(a.astype(np.uint32))
+            src = a if a.size else np.zeros(1, np.uint32)
+            _check(lib().gfq_mat_upload32(r, c, src.ctypes.data_as(_capi.c_u32p), max(c, 1), ctypes.byref(h)))
+            return Matrix(h, r, c, 4)
+        a = np.ascontiguousarray(a.astype(np.uint8))
         src = a if a.size else np.zeros(1, np.uint8)
         _check(lib().gfq_mat_upload(r, c, src.ctypes.data_as(_capi.c_u8p), max(c, 1), ctypes.byref(h)))
-        return Matrix(h, r, c)
+        return Matrix(h, r, c, 1)
 
     @staticmethod
-    def zeros(rows: int, cols: int) -> "Matrix":
+    def zeros(rows: int, cols: int, esize: int = 1) -> "Matrix":
         h = _vp()
-        _check(lib().gfq_mat_upload(rows, cols, None, max(cols, 1), ctypes.byref(h)))
-        return Matrix(h, rows, cols)
+        if esize == 4:
+            _check(lib().gfq_mat_upload32(rows, cols, None, max(cols, 1), ctypes.byref(h)))
+        else:
+            _check(lib().gfq_mat_upload(rows, cols, None, max(cols, 1), ctypes.byref(h)))
+        return Matrix(h, rows, cols, esize)
 
     @staticmethod
     def from_device(ptr: int, rows: int, cols: int, ld: int) -> "Matrix":
@@ -214,9 +242,9 @@ class Matrix:
         return Matrix(h, rows, cols)
 
     def numpy(self) -> np.ndarray:
-        out = np.zeros((self.rows, self.cols), np.uint8)
+        out = np.zeros((self.rows, self.cols), np.uint32 if self.esize == 4 else np.uint8)
         if out.size:
-            _check(lib().gfq_mat_download(self.h, out.ctypes.data_as(_capi.c_u8p), self.cols))
+            _check(lib().gfq_mat_download(self.h, out.ctypes.data_as(_capi.c_u8p), self.cols * self.esize))
         return out
 
     def device_ptr(self):
@@ -367,17 +395,20 @@ def _opt_h(m: Optional[Matrix]):
 
 
 # ---------------------------------------------------------------- jobs
-def _as_matrix(x) -> Matrix:
-    return x if isinstance(x, Matrix) else Matrix.from_numpy(x)
+def _as_matrix(x, f: "FieldSpec" = None) -> Matrix:
+    """A device Matrix as is; a host array uploaded (u32 for a wide field f)."""
+    if isinstance(x, Matrix):
+        return x
+    return Matrix.from_numpy(x, f.esize if f is not None else None)
 
 
 def cpy(a: Matrix) -> Matrix:
-    return rrf(BitString([0] * a.rows), a, Matrix.zeros(0, a.cols))
+    return rrf(BitString([0] * a.rows), a, Matrix.zeros(0, a.cols, a.esize))
 
 
 def mul(f: FieldSpec, b, c) -> Matrix:
     """reference jobs.hpp:40 -> K1"""
-    b, c = _as_matrix(b), _as_matrix(c)
+    b, c = _as_matrix(b, f), _as_matrix(c, f)
     h = _vp()
     _check(lib().gfq_mul(f.code, b.h, c.h, ctypes.byref(h)))
     return _mat(h)
@@ -385,7 +416,7 @@ def mul(f: FieldSpec, b, c) -> Matrix:
 
 def mad(f: FieldSpec, a, b, c) -> Matrix:
     """reference jobs.hpp:43 -> K1 (a + b.c)"""
-    a, b, c = _as_matrix(a), _as_matrix(b), _as_matrix(c)
+    a, b, c = _as_matrix(a, f), _as_matrix(b, f), _as_matrix(c, f)
     h = _vp()
     _check(lib().gfq_mad(f.code, a.h, b.h, c.h, ctypes.byref(h)))
     return _mat(h)
@@ -413,7 +444,7 @@ class EchResult:
 
 def ech(f: FieldSpec, h, threshold: int = 256) -> EchResult:
     """reference jobs.hpp:50 -> K2 base case + K1/K3/K4 combines"""
-    h = _as_matrix(h)
+    h = _as_matrix(h, f)
     M, K, R, rho, gam = _vp(), _vp(), _vp(), _vp(), _vp()
     _check(lib().gfq_ech(f.code, h.h, threshold, *(ctypes.byref(x) for x in (M, K, R, rho, gam))))
     return EchResult(_mat(M), _mat(K), _mat(R), IndexSet._take(rho), IndexSet._take(gam))
@@ -536,7 +567,7 @@ class PkgE:
 
 def clear_down(f: FieldSpec, C, D: Optional[PkgD], i: int, ech_threshold: int = 256):
     """reference tasks.hpp:19 -> (PkgD, PkgA)"""
-    C = _as_matrix(C)
+    C = _as_matrix(C, f)
     dout, aout = _capi.PkgD(), _capi.PkgA()
     with _Temps() as t:
         dp = ctypes.byref(D._struct(t)) if (D is not None and i > 0) else None
@@ -548,8 +579,8 @@ def clear_down(f: FieldSpec, C, D: Optional[PkgD], i: int, ech_threshold: int = 
 
 def update_row(f: FieldSpec, A: PkgA, C, B: Optional[Matrix], i: int):
     """reference tasks.hpp:26 -> (C', B')"""
-    C = _as_matrix(C)
-    B = _as_matrix(B) if B is not None else None
+    C = _as_matrix(C, f)
+    B = _as_matrix(B, f) if B is not None else None
     co, bo = _vp(), _vp()
     with _Temps() as t:
         a = A._struct(t)
@@ -560,8 +591,8 @@ def update_row(f: FieldSpec, A: PkgA, C, B: Optional[Matrix], i: int):
 def update_row_trafo(f: FieldSpec, A: PkgA, K: Optional[Matrix], M: Optional[Matrix], E: PkgE, i: int,
                      h: int, j: int):
     """reference tasks.hpp:36 -> (K', M')"""
-    K = _as_matrix(K) if K is not None else None
-    M = _as_matrix(M) if M is not None else None
+    K = _as_matrix(K, f) if K is not None else None
+    M = _as_matrix(M, f) if M is not None else None
     ko, mo = _vp(), _vp()
     with _Temps() as t:
         a, e = A._struct(t), E._struct(t)
@@ -602,7 +633,7 @@ def pre_clear_up(B, D: PkgD):
 
 def clear_up(f: FieldSpec, R, X, M) -> Matrix:
     """reference tasks.hpp:55 (R + X.M)"""
-    R, X, M = _as_matrix(R), _as_matrix(X), _as_matrix(M)
+    R, X, M = _as_matrix(R, f), _as_matrix(X, f), _as_matrix(M, f)
     h = _vp()
     _check(lib().gfq_clear_up(f.code, R.h, X.h, M.h, ctypes.byref(h)))
     return _mat(h)
@@ -800,6 +831,10 @@ def echelonize(C, f: FieldSpec, options: EchelonizeOptions = None, host_out=None
     options = options or EchelonizeOptions()
     o = options._struct()
     h = _vp()
+    if f.wide and not isinstance(C, Matrix):
+        if host_out is not None:
+            raise ValueError("echelonize: host_out needs a u8 field")
+        C = Matrix.from_numpy(C, 4)  # wide fields: u32 elements on the device
     if host_out is not None:
         if isinstance(C, Matrix):
             raise ValueError("echelonize: host_out needs a host input")
@@ -880,7 +915,7 @@ def read_gfmat_file(path: str):
 
 def write_gfmat_file(path: str, f: FieldSpec, m) -> None:
     """reference write_gfmat_file (src/io.cpp:228), byte-identical."""
-    m = _as_matrix(m)
+    m = _as_matrix(m, f)
     _check(lib().gfq_write_gfmat_file(os.fsencode(path), f.code, m.h))
 
 
@@ -892,7 +927,7 @@ def verify(C, out: EchelonOutput, method: str = "auto", seed: int = 1):
     without the oracle argument (gfq_verify).  Returns (ok, diag, checked):
     `checked` is "exact" (T materialised, T.C compared), "freivalds"
     (T.(C.X) vs E.X, X random n x 64) or "row-space" (no transform)."""
-    C = _as_matrix(C)
+    C = _as_matrix(C, out.field)
     ok = ctypes.c_int32()
     diag = ctypes.create_string_buffer(512)
     chk = ctypes.create_string_buffer(32)

@@ -64,9 +64,30 @@ def test_field_errors(G):
         G.FieldSpec(4, 2)
     with pytest.raises(ValueError, match="p\\^k must be < 2\\^20"):
         G.FieldSpec(2, 21)
-    # GF(11^3) exists in the reference (q = 1331) but not in u8 storage
-    with pytest.raises(ValueError, match="p\\^k <= 256"):
-        G.FieldSpec(11, 3)
+    # reference tests/test_field.cpp:140: characteristic too large
+    with pytest.raises(ValueError, match="p must be < 2\\^16"):
+        G.FieldSpec(65537)
+    # GF(11^3) (q = 1331, u32 storage): the reference's default modulus
+    # (tests/test_field.cpp:89)
+    assert list(G.FieldSpec(11, 3).modulus) == [4, 1, 0, 1]
+
+
+@pytest.mark.parametrize("p,k", [(257, 1), (65521, 1), (11, 3), (2, 10), (3, 7), (2, 12)])
+def test_wide_field_ops_match_reference(G, p, k):
+    """host arithmetic of the wide fields (u32 storage: log / antilog / Zech
+    tables for p^k > 256) equals the reference's FieldSpec ops"""
+    F = G.FieldSpec(p) if k == 1 else G.FieldSpec(p, k)
+    assert F.wide and F.order() == p ** k
+    rc = p if k == 1 else oracle.ref_ext_code(p, k)
+    rng = np.random.default_rng(p * 31 + k)
+    q = p ** k
+    for a, b in rng.integers(0, q, (300, 2)):
+        a, b = int(a), int(b)
+        assert F.add(a, b) == oracle.ref_field_op(rc, "add", a, b)
+        assert F.mul(a, b) == oracle.ref_field_op(rc, "mul", a, b)
+        assert F.neg(a) == oracle.ref_field_op(rc, "neg", a)
+        if a:
+            assert F.inv(a) == oracle.ref_field_op(rc, "inv", a)
 
 
 def test_tables_match_reference(ext, G):

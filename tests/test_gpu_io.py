@@ -71,9 +71,9 @@ def test_gfmat_roundtrip_and_errors(G, tmp_path):
         "header": "GFMAT v2\nfield p=7 k=1\nrows=1 cols=1\n0\n",
         "entry": "GFMAT v1\nfield p=7 k=1\nrows=1 cols=2\n0 7\n",
         "count": "GFMAT v1\nfield p=7 k=1\nrows=2 cols=2\n0 1\n1\n",
-        # GF(p^k) files load (tests/test_gpu_ext.py); these two fields do not
+        # GF(p^k) files load (tests/test_gpu_ext.py, test_gpu_wide.py); these do not
         "reducible": "GFMAT v1\nfield p=2 k=2 modulus=1,0,1\nrows=1 cols=1\n0\n",
-        "u8_storage": "GFMAT v1\nfield p=11 k=3 modulus=4,1,0,1\nrows=1 cols=1\n0\n",
+        "range": "GFMAT v1\nfield p=11 k=3 modulus=4,1,0,1\nrows=1 cols=1\n1331\n",
         "trailing": "GFMAT v1\nfield p=3 k=1\nrows=1 cols=1\n2\nextra\n",
     }
     for what, text in bad.items():
@@ -83,6 +83,12 @@ def test_gfmat_roundtrip_and_errors(G, tmp_path):
         with pytest.raises(ValueError) as ei:
             G.read_gfmat_file(fp)
         assert fp in str(ei.value), what
+    # GF(11^3) (the reference's own test field, q = 1331) loads, u32 elements
+    fp = str(tmp_path / "w.gfmat")
+    with open(fp, "w") as fh:
+        fh.write("GFMAT v1\nfield p=11 k=3 modulus=4,1,0,1\nrows=1 cols=2\n0 1330\n")
+    f, M = G.read_gfmat_file(fp)
+    assert (f.p, f.k, f.q) == (11, 3, 1331) and M.esize == 4 and M.numpy().tolist() == [[0, 1330]]
 
 
 def test_cli_exit_codes(G, tmp_path, capsys):
