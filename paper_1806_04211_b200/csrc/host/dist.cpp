@@ -553,6 +553,8 @@ IndexSet bcast_iset(Comm& comm, const IndexSet* mine, std::size_t universe, int 
 EchelonOutput echelonize_dist(const Mat* C, std::int64_t m, std::int64_t n, std::uint64_t seed,
                               const FieldSpec& field, const EchelonizeOptions& options, Comm& comm,
                               RunReport* report, bool gather) {
+  if (field.wide())
+    throw std::invalid_argument("echelonize_dist: the sharded Chief takes u8 fields (p <= 251, p^k <= 256)");
   const ChopSpec cs = chop(std::size_t(m), std::size_t(n), options.block, options.remainder_first);
   const std::size_t a = cs.a(), b = cs.b();
   EchelonOutput out{field};
