@@ -784,6 +784,15 @@ EchelonOutput echelonize_impl(const Mat& C, const FieldSpec& field, const Echelo
   graph.ech_threshold = options.ech_threshold;
   // wide fields (u32 storage) run the reference's per-block task grid
   const bool fused = options.fuse && !field.wide() && 2 * a + 1 <= std::size_t(TaskNode::kMaxIn);
+  // the critical-path SM partition pays off once blocks are large
+  // (kernels.hpp set_critical_partition); GFQ_PARTITION=0/1 forces it
+  {
+    static const int forced = [] {
+      const char* e = std::getenv("GFQ_PARTITION");
+      return e ? std::atoi(e) : -1;
+    }();
+    dev::set_critical_partition(forced >= 0 ? forced != 0 : (fused && options.block >= 4096));
+  }
   const PlanHandles h = fused ? build_plan_fused(graph, C, field, cs, options.with_transform, row_ready)
                               : build_plan(graph, C, field, cs, options.with_transform);
   for (auto id : h.d_final) graph.retain(id);

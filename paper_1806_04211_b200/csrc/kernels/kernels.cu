@@ -368,10 +368,15 @@ bool stream_is_critical(cudaStream_t s) {
   }
   return pr == greatest && greatest != 0;
 }
+namespace {
+std::atomic<bool> g_partition{false};
+}  // namespace
+void set_critical_partition(bool on) { g_partition = on; }
+bool critical_partition() { return g_partition; }
 int k1_sms(cudaStream_t s) {
   static const int reserve = [] {
     const char* e = std::getenv("GFQ_K1_SM_RESERVE");
-    return e ? std::atoi(e) : 0;
+    return e ? std::atoi(e) : 16;
   }();
   static const int crit = [] {
     const char* e = std::getenv("GFQ_CRIT_GRID");
@@ -379,7 +384,7 @@ int k1_sms(cudaStream_t s) {
   }();
   if (stream_is_critical(s))
     return crit > 0 && std::strcmp(hprof::t_task_name, "ClearDown") == 0 ? std::min(crit, sm_count()) : sm_count();
-  if (reserve <= 0) return sm_count();
+  if (reserve <= 0 || !g_partition) return sm_count();
   return std::max(1, sm_count() - reserve);
 }
 // The K1 lane (GFQ_K1_LANE=1): persistent contractions issued from
@@ -393,8 +398,11 @@ int g_lane_n = 0;
 bool g_lane_has = false;
 }  // namespace
 K1Lane::K1Lane(cudaStream_t s) : s_(s) {
-  static const bool on = std::getenv("GFQ_K1_LANE") != nullptr;
-  if (!on || stream_is_critical(s)) return;
+  static const bool on = [] {
+    const char* e = std::getenv("GFQ_K1_LANE");
+    return !(e && e[0] == '0');
+  }();
+  if (!on || !g_partition || stream_is_critical(s)) return;
   g_lane_mtx.lock();
   held_ = true;
   if (!g_lane_n) {

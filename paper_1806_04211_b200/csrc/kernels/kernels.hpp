@@ -92,6 +92,14 @@ bool f4_field(std::uint32_t p);
 // greatest priority (the executor's Step-1 critical-path stream).
 bool stream_is_critical(cudaStream_t s);
 int k1_sms(cudaStream_t s);
+// The critical-path partition (set per run by the Chief for large blocks):
+// while on, persistent contractions from non-critical streams run one at a
+// time on all but GFQ_K1_SM_RESERVE (16) SMs and the executor's bulk
+// streams live in a green context without one SM group, so the diagonal
+// ECH chain always finds SMs (cfg5s 157 -> 151 ms, cfg4 54 -> 53 ms; small
+// blocks lose ~1.5% and keep it off).
+void set_critical_partition(bool on);
+bool critical_partition();
 // Scope around a persistent contraction's launches (see kernels.cu).
 class K1Lane {
  public:
