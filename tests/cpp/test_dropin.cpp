@@ -107,11 +107,18 @@ int main(int argc, char** argv) {
     const FieldSpec f2(2);
     run_case("gf2-2048", random_matrix(f2, 2048, 2048, 5), f2, 256);
   }
-  // error behaviour: fields the B200 path cannot store raise, never fall back
-  expect_throw<std::invalid_argument>("field p=257 rejected", [] {
+  {
+    // wide fields (u32 elements): GF(257), GF(65521) and the reference's own
+    // chief-test field GF(11^3) (tests/test_chief.cpp:371)
     const FieldSpec f(257);
-    gfrref_b200::echelonize(Matrix(4, 4), f, EchelonizeOptions{});
-  });
+    run_case("wide-prime", random_matrix(f, 90, 70, 31), f, 20);
+    const FieldSpec f2(65521);
+    run_case("wide-prime", random_product_matrix(f2, 60, 75, 30, 32), f2, 16);
+    const FieldSpec f3(11, 3);
+    run_case("wide-ext", random_matrix(f3, 9, 7, 33), f3, 3);
+    run_case("wide-ext", random_matrix(f3, 50, 40, 34), f3, 12, false);
+  }
+  // error behaviour: invalid inputs raise, never fall back
   expect_throw<std::invalid_argument>("entry outside the field", [] {
     const FieldSpec f(3);
     gfrref_b200::echelonize(mat_build(1, 2, {{1, 5}}), f, EchelonizeOptions{});
