@@ -102,7 +102,14 @@ __device__ __forceinline__ void tmem_st32_const(std::uint32_t taddr, std::uint32
   asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
 }
 
-template <class C>
+// Clusters of CM x CN CTAs on a CM x CN block of tiles: the CM CTAs of one
+// N-tile share its B tile and the CN CTAs of one M-tile share its A tile, so
+// each CTA loads 1/CM of the B tile and 1/CN of the A tile and multicasts
+// each part into the rings of the CTAs sharing it -- L2 -> SM operand traffic
+// per tile drops from A + B to A/CN + B/CM.  A stage may be refilled only
+// once every CTA of the cluster has drained it, so each CTA's MMA commit
+// arrives on the `empty` barrier of all of them (count CM.CN).
+template <class C, int CM, int CN>
 __global__ void __launch_bounds__(NUM_THREADS, 1)
 gf_mad_f4_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, int m,
                  int n, int kpb, std::uint32_t p, std::uint32_t magic, std::uint32_t bias,
@@ -124,15 +131,28 @@ gf_mad_f4_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int num_m = (m + BM - 1) / BM, num_n = (n + BN - 1) / BN;
-  const int num_tiles = num_m * num_n;
+  // work units: CM x CN blocks of tiles; this CTA takes tile
+  // (CM.um + rm, CN.un + rn) of unit (um, un) -- a phantom past num_m or
+  // num_n at a ragged edge (its loads fill zeros, its outputs are all out of
+  // range)
+  constexpr int CL = CM * CN;
+  const int num_um = (num_m + CM - 1) / CM, num_un = (num_n + CN - 1) / CN;
+  const int num_tiles = num_um * num_un;
   const int num_kb = (kpb + BKB - 1) / BKB;
+  const int rank = CL > 1 ? int(cluster_ctarank()) : 0;
+  const int rm = rank % CM, rn = rank / CM;
+  std::uint16_t a_mask = 0, b_mask = 0;  // the CTAs sharing this CTA's A / B tile
+  for (int j = 0; j < CN; ++j) a_mask |= std::uint16_t(1u << (rm + CM * j));
+  for (int j = 0; j < CM; ++j) b_mask |= std::uint16_t(1u << (j + CM * rn));
+  const int first = int(blockIdx.x) / CL, stride = int(gridDim.x) / CL;
+  const int gu = gm / CM > 0 ? gm / CM : 1;
 
   if (warp == 0 && lane == 0) {
     prefetch_tmap(&tmA);
     prefetch_tmap(&tmB);
     for (int s = 0; s < STAGES; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&empty[s], 1);
+      mbar_init(&empty[s], CL);
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(&tfull[a], 1);
@@ -158,6 +178,8 @@ gf_mad_f4_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
   }
   fence_before();
   __syncthreads();
+  // the peer's barriers must be initialised before its first multicast
+  if constexpr (CL > 1) cluster_sync_all();
   fence_after();
   const std::uint32_t sfa = tmem_base + std::uint32_t(SF_COL);
   const std::uint32_t sfb = tmem_base + std::uint32_t(SF_COL + 16);
@@ -166,14 +188,23 @@ gf_mad_f4_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
     if (lane == 0) {
       int stage = 0;
       std::uint32_t phase = 0;
-      for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
-        int mb, nb;
-        tile_coords(tile, num_m, num_n, gm, mb, nb);
+      for (int tile = first; tile < num_tiles; tile += stride) {
+        int um, un;
+        tile_coords(tile, num_um, num_un, gu, um, un);
+        const int mb = um * CM + rm, nb = un * CN + rn;
         for (int kb = 0; kb < num_kb; ++kb) {
           mbar_wait(&empty[stage], phase ^ 1);
           mbar_arrive_expect_tx(&full[stage], STAGE_BYTES);
-          tma_load_2d(&tmA, &full[stage], sA + stage * A_STAGE, kb * BKB, mb * BM);
-          tma_load_2d(&tmB, &full[stage], sB + stage * B_STAGE, kb * BKB, nb * BN);
+          if constexpr (CN > 1)
+            tma_load_2d_mc(&tmA, &full[stage], sA + stage * A_STAGE + rn * (A_STAGE / CN), kb * BKB,
+                           mb * BM + rn * (BM / CN), a_mask);
+          else
+            tma_load_2d(&tmA, &full[stage], sA + stage * A_STAGE, kb * BKB, mb * BM);
+          if constexpr (CM > 1)
+            tma_load_2d_mc(&tmB, &full[stage], sB + stage * B_STAGE + rm * (B_STAGE / CM), kb * BKB,
+                           nb * BN + rm * (BN / CM), b_mask);
+          else
+            tma_load_2d(&tmB, &full[stage], sB + stage * B_STAGE, kb * BKB, nb * BN);
           if (++stage == STAGES) {
             stage = 0;
             phase ^= 1;
@@ -186,7 +217,7 @@ gf_mad_f4_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
       int stage = 0;
       std::uint32_t phase = 0;
       int it = 0;
-      for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++it) {
+      for (int tile = first; tile < num_tiles; tile += stride, ++it) {
         const int acc = ACCS == 2 ? (it & 1) : 0;
         const std::uint32_t acc_phase = ACCS == 2 ? ((it >> 1) & 1) : (it & 1);
         mbar_wait(&tempty[acc], acc_phase ^ 1);
@@ -204,7 +235,10 @@ gf_mad_f4_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
             const std::uint64_t bd = umma_desc(b0 + kk * 32, 16, 1024);
             mma_f4(d_tmem, ad, bd, C::IDESC, (kb | kk) != 0, sfa, sfb);
           }
-          mma_commit(&empty[stage]);
+          if constexpr (CL > 1)
+            mma_commit_mc(&empty[stage], std::uint16_t((1u << CL) - 1));
+          else
+            mma_commit(&empty[stage]);
           if (++stage == STAGES) {
             stage = 0;
             phase ^= 1;
@@ -224,9 +258,10 @@ gf_mad_f4_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
     const int row_in_tile = quarter * 32 + lane;
     const bool p2 = p == 2;
     int it = 0;
-    for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++it) {
-      int mb, nb;
-      tile_coords(tile, num_m, num_n, gm, mb, nb);
+    for (int tile = first; tile < num_tiles; tile += stride, ++it) {
+      int um, un;
+      tile_coords(tile, num_um, num_un, gu, um, un);
+      const int mb = um * CM + rm, nb = un * CN + rn;
       const int acc = ACCS == 2 ? (it & 1) : 0;
       const std::uint32_t acc_phase = ACCS == 2 ? ((it >> 1) & 1) : (it & 1);
       const int row = mb * BM + row_in_tile;
@@ -311,6 +346,8 @@ gf_mad_f4_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant_
 
   fence_before();
   __syncthreads();
+  // the peer's last commits arrive on this CTA's barriers
+  if constexpr (CL > 1) cluster_sync_all();
   if (warp == 1) {
     fence_after();
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(TMEM_COLS));
@@ -472,27 +509,64 @@ bool mad_f4(std::uint32_t p, std::int64_t m, std::int64_t n, std::int64_t k, con
   const std::int64_t h = p == 2 ? 1 : (p - 1) / 2;
   if (h * h * k >= (std::int64_t(1) << 24) || m >= (1LL << 31) || n >= (1LL << 31)) return false;
   if ((reinterpret_cast<std::uintptr_t>(scratch) & 15) != 0) return false;
-  static std::once_flag attr_once;
-  std::call_once(attr_once, [] {
-    GFQ_CUDA(cudaFuncSetAttribute(gf_mad_f4_kernel<CfgA>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  CfgA::SMEM_BYTES));
-    GFQ_CUDA(cudaFuncSetAttribute(gf_mad_f4_kernel<CfgB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  CfgB::SMEM_BYTES));
-    GFQ_CUDA(cudaFuncSetAttribute(gf_mad_f4_kernel<CfgC>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  CfgC::SMEM_BYTES));
-    GFQ_CUDA(cudaFuncSetAttribute(pack_cols_f4_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, PC_SMEM));
-  });
   static const int variant = [] {
     const char* e = std::getenv("GFQ_F4_VARIANT");
     return e ? std::atoi(e) : 0;
   }();
+  // operand-sharing clusters (see the kernel): GFQ_F4_CLUSTER = 1 (none),
+  // 2 (CTA pairs sharing B), 4 (2 x 2), 12 (pairs sharing A); tile 224 only
+  static const int clv = [] {
+    const char* e = std::getenv("GFQ_F4_CLUSTER");
+    const int v = e ? std::atoi(e) : 2;
+    return v == 1 || v == 4 || v == 12 ? v : 2;
+  }();
+  const int cm = variant != 0 ? 1 : clv == 2 || clv == 4 ? 2 : 1;
+  const int cn = variant != 0 ? 1 : clv == 4 || clv == 12 ? 2 : 1;
+  using KernT = void (*)(CUtensorMap, CUtensorMap, int, int, int, std::uint32_t, std::uint32_t, std::uint32_t,
+                         const std::uint8_t*, std::int64_t, std::uint8_t*, std::int64_t, int);
+  KernT kern = variant == 1   ? gf_mad_f4_kernel<CfgB, 1, 1>
+               : variant == 2 ? gf_mad_f4_kernel<CfgC, 1, 1>
+               : cm == 2 && cn == 2 ? gf_mad_f4_kernel<CfgA, 2, 2>
+               : cm == 2            ? gf_mad_f4_kernel<CfgA, 2, 1>
+               : cn == 2            ? gf_mad_f4_kernel<CfgA, 1, 2>
+                                    : gf_mad_f4_kernel<CfgA, 1, 1>;
+  const int smem = variant == 1 ? CfgB::SMEM_BYTES : variant == 2 ? CfgC::SMEM_BYTES : CfgA::SMEM_BYTES;
+  const int cl = cm * cn;
   const int BN = variant == 1 ? CfgB::BN : variant == 2 ? CfgC::BN : CfgA::BN;
+  // co-resident clusters of this shape (a persistent grid must not exceed it)
+  static const int max_clusters = [&] {
+    auto big = [](auto k, int bytes) {
+      GFQ_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+    };
+    big(gf_mad_f4_kernel<CfgA, 1, 1>, CfgA::SMEM_BYTES);
+    big(gf_mad_f4_kernel<CfgB, 1, 1>, CfgB::SMEM_BYTES);
+    big(gf_mad_f4_kernel<CfgC, 1, 1>, CfgC::SMEM_BYTES);
+    big(gf_mad_f4_kernel<CfgA, 2, 1>, CfgA::SMEM_BYTES);
+    big(gf_mad_f4_kernel<CfgA, 1, 2>, CfgA::SMEM_BYTES);
+    big(gf_mad_f4_kernel<CfgA, 2, 2>, CfgA::SMEM_BYTES);
+    big(pack_cols_f4_kernel, PC_SMEM);
+    if (cl == 1) return 1 << 30;
+    cudaLaunchAttribute at;
+    at.id = cudaLaunchAttributeClusterDimension;
+    at.val.clusterDim.x = unsigned(cl);
+    at.val.clusterDim.y = 1;
+    at.val.clusterDim.z = 1;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(unsigned(cl * 256));
+    cfg.blockDim = dim3(NUM_THREADS);
+    cfg.dynamicSmemBytes = std::size_t(smem);
+    cfg.attrs = &at;
+    cfg.numAttrs = 1;
+    int n = 0;
+    GFQ_CUDA(cudaOccupancyMaxActiveClusters(&n, kern, &cfg));
+    return n > 0 ? n : 1;
+  }();
   const std::int64_t kpb = (k + 63) / 64 * 32;
   std::uint8_t* Ap = scratch;
   std::uint8_t* Bt = scratch + (m * kpb + 127) / 128 * 128;
   CUtensorMap mA, mB;
-  if (!make_map_box(&mA, Ap, kpb, m, kpb, BKB, BM)) return false;
-  if (!make_map_box(&mB, Bt, kpb, n, kpb, BKB, BN)) return false;
+  if (!make_map_box(&mA, Ap, kpb, m, kpb, BKB, std::uint32_t(BM / cn))) return false;
+  if (!make_map_box(&mB, Bt, kpb, n, kpb, BKB, std::uint32_t(BN / cm))) return false;
   const std::uint32_t codes = code_word(p);
   {
     ProfScope ps(kProfSelect, double(m) * double(k) * 1.5, s);
@@ -527,23 +601,32 @@ bool mad_f4(std::uint32_t p, std::int64_t m, std::int64_t n, std::int64_t k, con
   for (std::int64_t m0 = 0; m0 < m; m0 += mp) {
     const std::int64_t mm = std::min(mp, m - m0);
     CUtensorMap mA;
-    if (!make_map_box(&mA, Ap + m0 * kpb, kpb, mm, kpb, BKB, BM)) throw std::runtime_error("mad_f4: tensor map");
-    const std::int64_t num_m = (mm + BM - 1) / BM, tiles = num_m * tiles_per_rowtile;
-    const int grid = int(tiles < sms ? tiles : sms);
+    if (!make_map_box(&mA, Ap + m0 * kpb, kpb, mm, kpb, BKB, std::uint32_t(BM / cn))) throw std::runtime_error("mad_f4: tensor map");
+    const std::int64_t num_m = (mm + BM - 1) / BM;
+    const std::int64_t units_all = (num_m + cm - 1) / cm * ((tiles_per_rowtile + cn - 1) / cn);
+    const std::int64_t cap = std::min<std::int64_t>(sms / cl, max_clusters);
+    const int units = int(units_all < cap ? units_all : cap);
     // raster group: the A slice of gm M-tiles within ~32 MB
     const std::int64_t gm = std::max<std::int64_t>(
         1, std::min<std::int64_t>(num_m, (std::int64_t(32) << 20) / (std::int64_t(BM) * kpb)));
     const std::uint8_t* cin = Cin ? Cin + m0 * ldc : nullptr;
     std::uint8_t* d = D + m0 * ldd;
-    if (variant == 1)
-      GFQ_CUDA(launch_pdl(gf_mad_f4_kernel<CfgB>, dim3(grid), dim3(NUM_THREADS), CfgB::SMEM_BYTES, s, mA, mB,
-                          int(mm), int(n), int(kpb), p, magic, bias, cin, ldc, d, ldd, int(gm)));
-    else if (variant == 2)
-      GFQ_CUDA(launch_pdl(gf_mad_f4_kernel<CfgC>, dim3(grid), dim3(NUM_THREADS), CfgC::SMEM_BYTES, s, mA, mB,
-                          int(mm), int(n), int(kpb), p, magic, bias, cin, ldc, d, ldd, int(gm)));
-    else
-      GFQ_CUDA(launch_pdl(gf_mad_f4_kernel<CfgA>, dim3(grid), dim3(NUM_THREADS), CfgA::SMEM_BYTES, s, mA, mB,
-                          int(mm), int(n), int(kpb), p, magic, bias, cin, ldc, d, ldd, int(gm)));
+    cudaLaunchAttribute at[2];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    at[1].id = cudaLaunchAttributeClusterDimension;
+    at[1].val.clusterDim.x = unsigned(cl);
+    at[1].val.clusterDim.y = 1;
+    at[1].val.clusterDim.z = 1;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(unsigned(units * cl));
+    cfg.blockDim = dim3(NUM_THREADS);
+    cfg.stream = s;
+    cfg.attrs = pdl_enabled() ? at : at + 1;
+    cfg.numAttrs = pdl_enabled() ? 2 : 1;
+    cfg.dynamicSmemBytes = std::size_t(smem);
+    GFQ_CUDA(cudaLaunchKernelEx(&cfg, kern, mA, mB, int(mm), int(n), int(kpb), p, magic, bias, cin, ldc, d, ldd,
+                                int(gm)));
     GFQ_CUDA(cudaGetLastError());
     count_launch();
   }

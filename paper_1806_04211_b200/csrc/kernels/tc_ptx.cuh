@@ -48,6 +48,28 @@ __device__ __forceinline__ void tma_load_2d(const CUtensorMap* map, std::uint64_
       : "memory");
 }
 
+// The same tile written at the same shared-memory offset of every CTA in
+// `mask` (cluster ranks); each destination CTA's mbarrier at `bar`'s offset
+// receives the bytes it got.
+__device__ __forceinline__ void tma_load_2d_mc(const CUtensorMap* map, std::uint64_t* bar, void* dst, int c0,
+                                               int c1, std::uint16_t mask) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster"
+      " [%0], [%1, {%3, %4}], [%2], %5;" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<std::uint64_t>(map)), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "h"(mask)
+      : "memory");
+}
+
+__device__ __forceinline__ std::uint32_t cluster_ctarank() {
+  std::uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+
 __device__ __forceinline__ void prefetch_tmap(const CUtensorMap* map) {
   asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<std::uint64_t>(map))
                : "memory");
@@ -75,6 +97,16 @@ __device__ __forceinline__ void mma_commit(std::uint64_t* bar) {
   asm volatile(
       "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
           smem_u32(bar))
+      : "memory");
+}
+
+// arrive on the mbarrier at `bar`'s offset in every CTA of `mask` once the
+// MMAs issued so far have completed
+__device__ __forceinline__ void mma_commit_mc(std::uint64_t* bar, std::uint16_t mask) {
+  asm volatile(
+      "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+          smem_u32(bar)),
+      "h"(mask)
       : "memory");
 }
 

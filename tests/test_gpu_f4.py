@@ -100,3 +100,19 @@ def test_f4_not_for_other_fields(G):
     finally:
         G.profile(False)
         G.set_mad_policy(0)
+
+
+@pytest.mark.parametrize("shape", ["1", "4", "12"])
+def test_f4_cluster_shapes(shape):
+    """The non-default operand-sharing cluster shapes (GFQ_F4_CLUSTER, read
+    once per process; the default pairs are covered above) on the ragged
+    cases, in a child process."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, GFQ_F4_CLUSTER=shape)
+    r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", "-p", "no:cacheprovider",
+                        os.path.join(root, "tests", "test_gpu_f4.py"), "-k", "random_and_ragged or extreme"],
+                       env=env, cwd=root, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
