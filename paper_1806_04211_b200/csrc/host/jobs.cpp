@@ -539,6 +539,8 @@ EchResult panel_ech(const FieldSpec& f, const Mat& h, bool block_cluster = true)
   const bool gf2o = f.p() == 2 && !block_cluster && a <= kGf2OuterRows;
   Mat Z(a, 2 * ow), Bt(ow, tb + a);
   DevBuf step{static_cast<std::size_t>(dev::ech_step_scratch_bytes())};
+  dev::fill2d(step.ptr, std::int64_t(step.bytes), 1, std::int64_t(step.bytes), 0, s);
+  std::int64_t step_seq = 0, signalled = 0;
   const bool fused = a * 33 <= dev::kPanelSmem;
   Mat G(fused ? 0 : a, w), Bp(fused ? 0 : w, 2 * ow);
   for (std::int64_t C0 = 0; C0 < b; C0 += ow) {
@@ -553,7 +555,8 @@ EchResult panel_ech(const FieldSpec& f, const Mat& h, bool block_cluster = true)
       const std::int64_t n = (ow + std::min(kc, c0 + w) - c0 + 15) / 16 * 16;
       if (fused) {
         dev::ech_step(f.p(), a, c0, wc, n, Z.data(), Z.ld(), flags.ptr, inf, cap, r2, step.ptr, Y,
-                      base, s);
+                      base, c0 > 0, c0 + w < wd, int(++step_seq), int(signalled), s);
+        if (c0 + w < wd) ++signalled;
         continue;
       }
       // GF(2) blocks too tall for the fused step's fallback: the panel

@@ -52,15 +52,17 @@ constexpr int kW = 32;  // max panel width (bytes per panel row in smem)
 
 // Load the 32-byte panel segment of row i (bytes >= wc zeroed).
 __device__ __forceinline__ void load_seg(const std::uint8_t* src, int wc, uint4& a, uint4& b) {
+  // (L2 loads: the overlapped step chain reads rows another grid is still
+  // updating -- see ech_step)
   if (wc == kW && (reinterpret_cast<std::uintptr_t>(src) & 15) == 0) {
-    a = reinterpret_cast<const uint4*>(src)[0];
-    b = reinterpret_cast<const uint4*>(src)[1];
+    a = __ldcg(reinterpret_cast<const uint4*>(src));
+    b = __ldcg(reinterpret_cast<const uint4*>(src) + 1);
     return;
   }
   std::uint32_t w[8] = {0, 0, 0, 0, 0, 0, 0, 0};
 #pragma unroll
   for (int c = 0; c < kW; ++c)
-    if (c < wc) w[c >> 2] |= std::uint32_t(src[c]) << (8 * (c & 3));
+    if (c < wc) w[c >> 2] |= std::uint32_t(__ldcg(src + c)) << (8 * (c & 3));
   a = make_uint4(w[0], w[1], w[2], w[3]);
   b = make_uint4(w[4], w[5], w[6], w[7]);
 }
@@ -111,7 +113,7 @@ __device__ __forceinline__ void panel_full(std::uint32_t p, std::uint32_t magic,
   for (int a = tid; a < 256; a += nt)
     invt[a] = (a > 0 && std::uint32_t(a) < p) ? std::uint8_t(powmod(a, p - 2, p)) : 0;
   for (int i = tid; i < rows; i += nt) {
-    const std::uint8_t f = flags[i];
+    const std::uint8_t f = __ldcg(flags + i);
     fl[i] = f;
     if (!f) {
       uint4 a, b;
@@ -120,7 +122,7 @@ __device__ __forceinline__ void panel_full(std::uint32_t p, std::uint32_t magic,
       reinterpret_cast<uint4*>(P + i * kW)[1] = b;
     }
   }
-  if (tid == 0) r_old = info[0];
+  if (tid == 0) r_old = __ldcg(info);
   __syncthreads();
 
   // ---- column-wise Gauss-Jordan on the non-pivotal rows of the panel
@@ -178,7 +180,7 @@ __device__ __forceinline__ void panel_full(std::uint32_t p, std::uint32_t magic,
   for (int e = tid; e < kW * 2 * kW; e += nt) {
     const int q = e / (2 * kW), t = e % (2 * kW);
     std::uint8_t v = 0;
-    if (q < r2 && t < r2) v = Aug[std::int64_t(pr[q]) * ld + c0 + pc[t]];
+    if (q < r2 && t < r2) v = __ldcg(Aug + std::int64_t(pr[q]) * ld + c0 + pc[t]);
     else if (q < r2 && t >= kW && t - kW == q) v = 1;
     X[q][t] = v;
   }
@@ -245,7 +247,7 @@ __device__ __forceinline__ void panel_full(std::uint32_t p, std::uint32_t magic,
       if (q < r2) {
         const std::uint8_t* src = Aug + std::int64_t(pr[q]) * ld + c0;
         acc = N2[q][t];
-        for (int u = 0; u < r2; ++u) acc += std::uint32_t(src[pc[u]]) * N2[u][t];
+        for (int u = 0; u < r2; ++u) acc += std::uint32_t(__ldcg(src + pc[u])) * N2[u][t];
       }
       so.Gpiv[e] = std::uint8_t(modp(acc, p, magic));
     }
@@ -558,6 +560,16 @@ constexpr int kStepThreads = 256;
 // so the update's CTAs do not sit on SMs other streams' K1 tiles could use.
 // developer timing (GFQ_STEP_DEBUG): globaltimer stamps of the chain phases
 __device__ unsigned long long g_step_stamps[16];
+// developer timeline (GFQ_STEP_TL=N): per step, globaltimer at the chain's
+// entry / counter wait / loop end / exit and the update's CTA-0 entry /
+// first-pass signal / exit and the last update CTA's exit
+constexpr int kTlSteps = 512;
+__device__ unsigned long long g_tl[kTlSteps][8];
+__device__ __forceinline__ unsigned long long gtime() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
 __device__ __forceinline__ void stamp(int k) {
   unsigned long long t;
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
@@ -568,16 +580,41 @@ __device__ __forceinline__ void stamp(int k) {
 }
 // warp 0 runs the chain; the other warps join the fallback and the outputs
 constexpr int kChainThreads = 128;
-// TW: the chain in two warps (warp w holds window rows lo + 32w + lane),
-// exchanging votes and the pivot row through shared memory at named
+constexpr int kStepRows = 32, kStepMaxN = 512;
+// Overlapped steps (ech_step, `chained`): the chain of step s+1 runs while
+// the update of step s is still writing, synchronised through two counters
+// instead of the grid boundary: every update CTA bumps ctr[0] once its
+// rows' first 128 columns (the next step's panel columns among them) are
+// final and ctr[1] once all its columns are; the chain waits for ctr[0] to
+// read the panel and for ctr[1] before it reads whole rows or writes
+// anything the update reads (rho2 / NT / Gpiv / BpT, the Y units).  The
+// counters only grow (a reset would race: the chain of step s+1 may start
+// while that of step s is still writing its outputs).
+__device__ __forceinline__ void spin_until(const std::int32_t* p, int target) {
+  for (;;) {
+    int v;
+    asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    if (v >= target) break;
+    __nanosleep(20);
+  }
+}
+// MODE 1 (TW): the chain in two warps (warp w holds window rows lo + 32w +
+// lane), exchanging votes and the pivot row through shared memory at named
 // barriers: half the per-lane update work on each of two SMSPs.
-template <bool TW>
+// MODE 0: one warp does both (GFQ_CHAIN_MODE=0; A/B).  (A split variant --
+// warp 0 the panel part and the pivot choice, warp 1 replaying the
+// coefficient updates from a shared-memory queue -- measured slower: the
+// per-column cost is latency, not FMA issue.)
+template <int MODE>
 __global__ void __launch_bounds__(kChainThreads, 1)
 ech_step_chain_kernel(std::uint32_t p, std::uint32_t magic, int rows, int c0, int wc, int n,
                       std::uint8_t* __restrict__ Z, std::int64_t ld, std::uint8_t* flags,
                       std::int32_t* info, int cap, std::int32_t* rho2, std::int32_t* lo_state,
                       std::uint8_t* NT, std::uint8_t* Gpiv, std::uint8_t* Y, const std::int32_t* base,
-                      std::uint8_t* BpT, const std::uint8_t* __restrict__ invtab) {
+                      std::uint8_t* BpT, const std::uint8_t* __restrict__ invtab, std::int32_t* ctr,
+                      int wait_prev, int seq, int tl) {
+  // wait_prev > 0: ctr[0] / ctr[1] must reach wait_prev (they only grow:
+  // the previous chain may still be running when this one starts)
   extern __shared__ __align__(16) std::uint8_t dsm[];
   __shared__ std::uint8_t invw[256];
   __shared__ int s_lo, s_rold;
@@ -586,16 +623,22 @@ ech_step_chain_kernel(std::uint32_t p, std::uint32_t magic, int rows, int c0, in
   __shared__ int colq[kW];
   __shared__ std::uint8_t chatb[kW][kW];
   __shared__ int wpc[kW], wpr[kW], s_pr[kW];
-  pdl_wait();  // released after the chain (below): the update's CTAs
-               // should not sit on SMs other streams' K1 tiles could use
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  if (tl >= 0 && tid == 0) g_tl[tl][0] = gtime();
+  if (wait_prev) {
+    if (tid == 0) spin_until(ctr, wait_prev);
+    __syncthreads();
+  } else {
+    pdl_wait();  // released after the chain (below): the update's CTAs
+                 // should not sit on SMs other streams' K1 tiles could use
+  }
   stamp(0);
   for (int a = tid; a < 256; a += kChainThreads) invw[a] = invtab[a];  // inverses mod p (cached)
   if (warp == 0) {
-    int lo = *lo_state;
+    int lo = __ldcg(lo_state);
     for (;;) {
       const int idx = lo + lane;
-      const unsigned b = __ballot_sync(0xffffffffu, idx < rows && flags[idx] == 0);
+      const unsigned b = __ballot_sync(0xffffffffu, idx < rows && __ldcg(flags + idx) == 0);
       if (b || lo >= rows) {
         if (b) lo += __ffs(b) - 1;
         break;
@@ -605,24 +648,29 @@ ech_step_chain_kernel(std::uint32_t p, std::uint32_t magic, int rows, int c0, in
     if (lo > rows) lo = rows;
     if (lane == 0) {
       s_lo = lo;
-      s_rold = info[0];
+      s_rold = __ldcg(info);
       *lo_state = lo;
     }
   }
   __syncthreads();
   const int lo = s_lo, r_old = s_rold;
+  if (tl >= 0 && tid == 0) g_tl[tl][1] = gtime();
   // warps 1.. stage the window rows' step columns [c0, c0 + n) in shared
   // memory while warp 0 runs the chain: the step's pivot rows are window
   // rows, so BpT is built from here (the region doubles as panel_full's
   // fallback storage, after which the tail reads Z instead)
   std::uint8_t* Ws = dsm;  // 64 x n
-  constexpr int kChainW = TW ? 2 : 1;  // warps running the chain
+  constexpr int kChainW = MODE == 0 ? 1 : 2;  // warps running the chain
   if (warp >= kChainW) {
+    if (wait_prev) {
+      if (lane == 0) spin_until(ctr + 1, wait_prev);
+      __syncwarp();
+    }
     const int nv = n / 16;
     for (int e = tid - 32 * kChainW; e < 64 * nv; e += kChainThreads - 32 * kChainW) {
       const int r = e / nv, ch = e % nv;
       uint4 v = make_uint4(0, 0, 0, 0);
-      if (lo + r < rows) v = *reinterpret_cast<const uint4*>(Z + std::int64_t(lo + r) * ld + c0 + 16 * ch);
+      if (lo + r < rows) v = __ldcg(reinterpret_cast<const uint4*>(Z + std::int64_t(lo + r) * ld + c0 + 16 * ch));
       reinterpret_cast<uint4*>(Ws + r * n)[ch] = v;
     }
   }
@@ -646,27 +694,27 @@ ech_step_chain_kernel(std::uint32_t p, std::uint32_t magic, int rows, int c0, in
     const float q = (fmaf(v, invp, roff) + 12582912.0f) - 12582912.0f;
     return fmaf(-fp, q, v);
   };
-  if (TW && warp < 2) {
+  if (MODE == 1 && warp < 2) {
     __shared__ unsigned s_ball[2][2];
     __shared__ int s_cnt[2];
     __shared__ std::uint32_t s_iv;
     const auto bar = [] { asm volatile("bar.sync 1, 64;" ::: "memory"); };
     float w[32], k[32];
     const int row = lo + 32 * warp + lane;
-    bool open = row < rows && flags[row] == 0;
+    bool open = row < rows && __ldcg(flags + row) == 0;
 #pragma unroll
     for (int e = 0; e < 32; ++e) w[e] = k[e] = 0.0f;
     if (row < rows) {
       const std::uint8_t* src = Z + std::int64_t(row) * ld + c0;
       if (wc == kW) {
-        const uint4 a = reinterpret_cast<const uint4*>(src)[0], b = reinterpret_cast<const uint4*>(src)[1];
+        const uint4 a = __ldcg(reinterpret_cast<const uint4*>(src)), b = __ldcg(reinterpret_cast<const uint4*>(src) + 1);
         const std::uint32_t ww[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
 #pragma unroll
         for (int e = 0; e < 32; ++e) w[e] = float((ww[e >> 2] >> (8 * (e & 3))) & 0xFFu);
       } else {
 #pragma unroll
         for (int e = 0; e < 32; ++e)
-          if (e < wc) w[e] = float(src[e]);
+          if (e < wc) w[e] = float(__ldcg(src + e));
       }
     }
     {
@@ -763,24 +811,24 @@ ech_step_chain_kernel(std::uint32_t p, std::uint32_t magic, int rows, int c0, in
       s_r2 = r2;
     }
   }
-  if (!TW && warp == 0) {
+  if (MODE == 0 && warp == 0) {
     float w0[32], w1[32], k0[32], k1[32];
     const int i0 = lo + lane, i1 = lo + 32 + lane;
-    bool open0 = i0 < rows && flags[i0] == 0, open1 = i1 < rows && flags[i1] == 0;
+    bool open0 = i0 < rows && __ldcg(flags + i0) == 0, open1 = i1 < rows && __ldcg(flags + i1) == 0;
 #pragma unroll
     for (int e = 0; e < 32; ++e) w0[e] = w1[e] = k0[e] = k1[e] = 0.0f;
     const auto load = [&](int gi, float (&w)[32]) {
       if (gi >= rows) return;
       const std::uint8_t* src = Z + std::int64_t(gi) * ld + c0;
       if (wc == kW) {
-        const uint4 a = reinterpret_cast<const uint4*>(src)[0], b = reinterpret_cast<const uint4*>(src)[1];
+        const uint4 a = __ldcg(reinterpret_cast<const uint4*>(src)), b = __ldcg(reinterpret_cast<const uint4*>(src) + 1);
         const std::uint32_t ww[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
 #pragma unroll
         for (int e = 0; e < 32; ++e) w[e] = float((ww[e >> 2] >> (8 * (e & 3))) & 0xFFu);
       } else {
 #pragma unroll
         for (int e = 0; e < 32; ++e)
-          if (e < wc) w[e] = float(src[e]);
+          if (e < wc) w[e] = float(__ldcg(src + e));
       }
     };
     load(i0, w0);
@@ -920,6 +968,7 @@ ech_step_chain_kernel(std::uint32_t p, std::uint32_t magic, int rows, int c0, in
   }
   __syncthreads();
   stamp(2);
+  if (tl >= 0 && tid == 0) g_tl[tl][2] = gtime();
   pdl_release();
   const int ok = s_ok, r2 = s_r2;
   if (!ok) {
@@ -970,7 +1019,7 @@ ech_step_chain_kernel(std::uint32_t p, std::uint32_t magic, int rows, int c0, in
     uint4 v = make_uint4(0, 0, 0, 0);
     if (r >= 0)
       v = ok ? reinterpret_cast<const uint4*>(Ws + (r - lo) * n)[ch]
-             : *reinterpret_cast<const uint4*>(Z + std::int64_t(r) * ld + c0 + 16 * ch);
+             : __ldcg(reinterpret_cast<const uint4*>(Z + std::int64_t(r) * ld + c0 + 16 * ch));
     reinterpret_cast<uint4*>(Bs + q * n)[ch] = v;
   }
   __syncthreads();
@@ -986,6 +1035,13 @@ ech_step_chain_kernel(std::uint32_t p, std::uint32_t magic, int rows, int c0, in
   }
   __syncthreads();
   stamp(4);
+  if (tid == 0) {
+    // the update of this step may start (its CTAs wait for ctr[2] >= seq
+    // instead of the grid boundary)
+    __threadfence();
+    asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(ctr + 2), "r"(seq) : "memory");
+    if (tl >= 0) g_tl[tl][3] = gtime();
+  }
 }
 
 // Two-level ECH, step part 2: Z[i][c0 + j] += G[i] . Bp[:, j] for every row
@@ -998,36 +1054,41 @@ ech_step_chain_kernel(std::uint32_t p, std::uint32_t magic, int rows, int c0, in
 // A row's columns must stay in ONE CTA: G is formed from the row's panel
 // segment, which the same update overwrites in place (splitting the columns
 // over CTAs races -- measured 3% faster and wrong on cfg3).
-constexpr int kStepRows = 32, kStepMaxN = 512;
 __global__ void __launch_bounds__(kStepThreads)
 ech_step_update_kernel(std::uint32_t p, std::uint32_t magic, int rows, int c0, int n,
-                       std::uint8_t* __restrict__ Z, std::int64_t ld,
-                       const std::uint8_t* __restrict__ NT, const std::uint8_t* __restrict__ Gpiv,
-                       const std::int32_t* __restrict__ rho2, const std::uint8_t* __restrict__ BpT) {
+                       std::uint8_t* Z, std::int64_t ld, const std::uint8_t* NT, const std::uint8_t* Gpiv,
+                       const std::int32_t* rho2, const std::uint8_t* BpT, std::int32_t* ctr, int signal,
+                       int seq, int tl) {
   __shared__ __align__(16) std::uint32_t sB[kStepMaxN * 8];
   __shared__ __align__(16) std::uint32_t sNT[kW * 8];
   __shared__ std::uint32_t sG[kStepRows][9];
-  pdl_wait_and_release();
+  // The chain's outputs are published by its ready flag (ctr[2] = seq), so
+  // the CTAs wait for that rather than for the chain grid to retire; all
+  // reads of data another grid writes go to L2 (__ldcg: an SM's L1 may
+  // still hold the previous step's lines).
+  pdl_release();
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  if (tid == 0) spin_until(ctr + 2, seq);
+  __syncthreads();
   const int i0 = blockIdx.x * kStepRows;
   for (int e = tid; e < n * 2; e += kStepThreads)
-    reinterpret_cast<uint4*>(sB)[e] = reinterpret_cast<const uint4*>(BpT)[e];
-  if (tid < kW * 2) reinterpret_cast<uint4*>(sNT)[tid] = reinterpret_cast<const uint4*>(NT)[tid];
+    reinterpret_cast<uint4*>(sB)[e] = __ldcg(reinterpret_cast<const uint4*>(BpT) + e);
+  if (tid < kW * 2) reinterpret_cast<uint4*>(sNT)[tid] = __ldcg(reinterpret_cast<const uint4*>(NT) + tid);
   __syncthreads();
   {
     // warp w forms G[i][4w .. 4w+3] of the CTA's 32 rows (lane = row)
     const int i = i0 + lane;
-    const int r = rho2[lane];
+    const int r = __ldcg(rho2 + lane);
     int myq = -1;
 #pragma unroll
     for (int u = 0; u < kW; ++u)
       if (__shfl_sync(0xffffffffu, r, u) == i) myq = u;
     std::uint32_t gw = 0;
     if (i < rows && myq >= 0) {
-      gw = reinterpret_cast<const std::uint32_t*>(Gpiv + myq * kW)[warp];
+      gw = __ldcg(reinterpret_cast<const std::uint32_t*>(Gpiv + myq * kW) + warp);
     } else if (i < rows) {
       const uint4* src = reinterpret_cast<const uint4*>(Z + std::int64_t(i) * ld + c0);
-      const uint4 a = src[0], b = src[1];
+      const uint4 a = __ldcg(src), b = __ldcg(src + 1);
 #pragma unroll
       for (int tt = 0; tt < 4; ++tt) {
         const uint4* nt4 = reinterpret_cast<const uint4*>(sNT + (4 * warp + tt) * 8);
@@ -1044,14 +1105,14 @@ ech_step_update_kernel(std::uint32_t p, std::uint32_t magic, int rows, int c0, i
   }
   __syncthreads();
   const int i = i0 + lane;
-  if (i >= rows) return;
+  const bool live = i < rows;
   std::uint32_t g[8];
 #pragma unroll
   for (int w = 0; w < 8; ++w) g[w] = sG[lane][w];
   std::uint8_t* zrow = Z + std::int64_t(i) * ld + c0;
-  for (int ch = warp; ch < n / 16; ch += kStepThreads / 32) {
+  const auto chunk = [&](int ch) {
     std::uint32_t out[4];
-    const uint4 old = *reinterpret_cast<const uint4*>(zrow + 16 * ch);
+    const uint4 old = __ldcg(reinterpret_cast<const uint4*>(zrow + 16 * ch));
     const std::uint32_t ow[4] = {old.x, old.y, old.z, old.w};
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
@@ -1070,6 +1131,28 @@ ech_step_update_kernel(std::uint32_t p, std::uint32_t magic, int rows, int c0, i
       out[q] = word;
     }
     *reinterpret_cast<uint4*>(zrow + 16 * ch) = make_uint4(out[0], out[1], out[2], out[3]);
+  };
+  constexpr int kWarps = kStepThreads / 32;
+  // the first chunk a warp: columns [c0, c0 + 128), the next step's panel
+  // among them (the overlapped chain waits for these, see spin_until)
+  if (tl >= 0 && tid == 0 && blockIdx.x == 0) g_tl[tl][4] = gtime();
+  if (live && warp < n / 16) chunk(warp);
+  if (signal) {
+    __threadfence();
+    __syncthreads();
+    if (tid == 0) atomicAdd(ctr, 1);
+  }
+  if (tl >= 0 && tid == 0 && blockIdx.x == 0) g_tl[tl][5] = gtime();
+  if (live)
+    for (int ch = warp + kWarps; ch < n / 16; ch += kWarps) chunk(ch);
+  if (signal) {
+    __threadfence();
+    __syncthreads();
+    if (tid == 0) atomicAdd(ctr + 1, 1);
+  }
+  if (tl >= 0 && tid == 0) {
+    if (blockIdx.x == 0) g_tl[tl][6] = gtime();
+    atomicMax(&g_tl[tl][7], gtime());
   }
 }
 
@@ -1092,7 +1175,7 @@ ech_panel_gf2_kernel(int rows, int c0, int wc, const std::uint8_t* __restrict__ 
   const int tid = threadIdx.x, nt = blockDim.x, lane = tid & 31;
 
   for (int i = tid; i < rows; i += nt) {
-    const std::uint8_t f = flags[i];
+    const std::uint8_t f = __ldcg(flags + i);
     fl[i] = f;
     std::uint32_t word = 0;
     if (!f) {
@@ -1461,7 +1544,8 @@ const std::uint8_t* inv_table(std::uint32_t p) {
 void ech_step(std::uint32_t p, std::int64_t rows, std::int64_t c0, std::int64_t wc, std::int64_t n,
               std::uint8_t* Z, std::int64_t ld, std::uint8_t* flags, std::int32_t* info,
               std::int64_t cap, std::int32_t* rho2, std::uint8_t* step_scratch, std::uint8_t* Y,
-              const std::int32_t* base, cudaStream_t s) {
+              const std::int32_t* base, bool chained_prev, bool chained_next, int seq, int signalled,
+              cudaStream_t s) {
   if (wc > kW || c0 % kW || n % 16 || n > kStepMaxN || (ld & 15) ||
       (reinterpret_cast<std::uintptr_t>(Z) & 15))
     throw std::invalid_argument("ech_step: bad step geometry");
@@ -1469,12 +1553,12 @@ void ech_step(std::uint32_t p, std::int64_t rows, std::int64_t c0, std::int64_t 
   if (smem > std::size_t(kPanelSmem)) throw std::invalid_argument("ech_step: block too tall");
   static bool attr = false;
   if (!attr) {
-    for (auto fn : {ech_step_chain_kernel<false>, ech_step_chain_kernel<true>})
+    for (auto fn : {ech_step_chain_kernel<0>, ech_step_chain_kernel<1>})
       GFQ_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, kPanelSmem));
     // both step kernels ask for the largest shared-memory carveout so the SM
     // does not reconfigure L1 / shared memory between them
     if (!std::getenv("GFQ_NO_CARVEOUT")) {
-      for (auto fn : {ech_step_chain_kernel<false>, ech_step_chain_kernel<true>})
+      for (auto fn : {ech_step_chain_kernel<0>, ech_step_chain_kernel<1>})
         GFQ_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
       GFQ_CUDA(cudaFuncSetAttribute(ech_step_update_kernel,
                                     cudaFuncAttributePreferredSharedMemoryCarveout, 100));
@@ -1488,15 +1572,47 @@ void ech_step(std::uint32_t p, std::int64_t rows, std::int64_t c0, std::int64_t 
   std::uint8_t* NT = step_scratch;
   std::uint8_t* Gpiv = step_scratch + kW * kW;
   std::uint8_t* BpT = step_scratch + 2 * kW * kW;
+  auto* ctr = reinterpret_cast<std::int32_t*>(step_scratch + 2 * kW * kW + kStepMaxN * kW);
+  static const bool overlap = [] {
+    const char* e = std::getenv("GFQ_STEP_OVERLAP");
+    return !(e && e[0] == '0');
+  }();
+  // the chain waits until every CTA of the updates signalled so far
+  // (`signalled`, the previous one included) has bumped the counters
+  const int n_upd = int((rows + kStepRows - 1) / kStepRows);
+  const int wait_prev = overlap && chained_prev && pdl_enabled() ? n_upd * signalled : 0;
+  const int signal = overlap && chained_next && pdl_enabled() ? 1 : 0;
   const std::uint8_t* invt = inv_table(p);
-  static const bool one_warp = std::getenv("GFQ_CHAIN1") != nullptr;  // A/B: the one-warp chain
-  GFQ_CUDA(launch_pdl(one_warp ? ech_step_chain_kernel<false> : ech_step_chain_kernel<true>, dim3(1),
+  static int tl_n = std::getenv("GFQ_STEP_TL") ? std::atoi(std::getenv("GFQ_STEP_TL")) : 0;
+  static int tl_i = 0;
+  const int tl = tl_i < std::min(tl_n, kTlSteps) ? tl_i : -1;
+  if (tl == 0) {
+    static const unsigned long long zero[kTlSteps][8] = {};
+    GFQ_CUDA(cudaMemcpyToSymbol(g_tl, zero, sizeof zero));
+  }
+  static const int mode = [] {  // A/B: GFQ_CHAIN_MODE = 0 one warp, 1 two row halves (default)
+    const char* e = std::getenv("GFQ_CHAIN_MODE");
+    return e && std::atoi(e) == 0 ? 0 : 1;
+  }();
+  GFQ_CUDA(launch_pdl(mode == 0 ? ech_step_chain_kernel<0> : ech_step_chain_kernel<1>, dim3(1),
                       dim3(kChainThreads), smem, s, p, magic, int(rows),
                       int(c0), int(wc), int(n), Z, ld, flags, info, int(cap), rho2, lo_state, NT, Gpiv,
-                      Y, base, BpT, invt));
+                      Y, base, BpT, invt, ctr, wait_prev, seq, tl));
   GFQ_CUDA(launch_pdl(ech_step_update_kernel, dim3(unsigned((rows + kStepRows - 1) / kStepRows)),
                       dim3(kStepThreads), 0, s, p, magic, int(rows), int(c0), int(n), Z, ld, NT, Gpiv,
-                      rho2, BpT));
+                      rho2, BpT, ctr, signal, seq, tl));
+  if (tl >= 0 && ++tl_i == std::min(tl_n, kTlSteps)) {
+    GFQ_CUDA(cudaStreamSynchronize(s));
+    static unsigned long long h[kTlSteps][8];
+    GFQ_CUDA(cudaMemcpyFromSymbol(h, g_tl, sizeof h));
+    const unsigned long long t0 = h[0][0];
+
+    for (int k = 0; k < tl_i; ++k) {
+      std::fprintf(stderr, "TL %d", k);
+      for (int j = 0; j < 8; ++j) std::fprintf(stderr, " %.2f", h[k][j] ? (double(h[k][j]) - double(t0)) * 1e-3 : -1.0);
+      std::fprintf(stderr, "\n");
+    }
+  }
   static int dbg = std::getenv("GFQ_STEP_DEBUG") ? std::atoi(std::getenv("GFQ_STEP_DEBUG")) : 0;
   if (dbg > 0) {
     --dbg;

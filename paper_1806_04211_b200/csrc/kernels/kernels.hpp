@@ -313,11 +313,19 @@ void ech_panel(std::uint32_t p, std::int64_t rows, std::int64_t c0, std::int64_t
 // ech_step_scratch_bytes) and the row-parallel update of Z columns
 // [c0, c0 + n) (n a multiple of 16, <= 512; Z 16-byte aligned) with dp4a.
 // Same result as ech_panel + ech_panel_plant + gather + K1 on those columns.
-constexpr std::int64_t ech_step_scratch_bytes() { return 2 * 32 * 32 + 512 * 32; }
+// chained_prev: the previous launch on s was the step before in the same
+// outer panel; chained_next: the next one will be the step after.  Chained
+// steps overlap the update of one with the chain of the next (two counters
+// at the end of step_scratch, which must start zeroed; GFQ_STEP_OVERLAP=0
+// serialises them at the grid boundary instead).  seq: 1, 2, ... over the
+// steps that use one step_scratch (the chain's ready flag for its update);
+// signalled: how many earlier steps on it had chained_next.
+constexpr std::int64_t ech_step_scratch_bytes() { return 2 * 32 * 32 + 512 * 32 + 16; }
 void ech_step(std::uint32_t p, std::int64_t rows, std::int64_t c0, std::int64_t wc, std::int64_t n,
               std::uint8_t* Z, std::int64_t ld, std::uint8_t* flags, std::int32_t* info,
               std::int64_t cap, std::int32_t* rho2, std::uint8_t* step_scratch, std::uint8_t* Y,
-              const std::int32_t* base, cudaStream_t s);
+              const std::int32_t* base, bool chained_prev, bool chained_next, int seq, int signalled,
+              cudaStream_t s);
 void ech_panel_plant(std::uint8_t* Y, std::int64_t ldy, const std::int32_t* rho2,
                      const std::int32_t* info, const std::int32_t* base, cudaStream_t s);
 void ech_outer_finish(std::uint32_t p, std::uint8_t* Y, std::int64_t ldy, std::int64_t kcols,
