@@ -676,6 +676,9 @@ EchResult ech(const FieldSpec& f, const Mat& h, std::size_t threshold) {
   // GF(p^k): the reference's split/combine recursion (its products are
   // digit-plane K1 contractions) over the table-driven base case
   if (ech_mode() != 1 && !f.is_ext() && !f.wide()) {
+    // thin blocks (rank <= 32: the Chief's one-column / one-row ClearDowns)
+    // in one base-case launch
+    if (std::min(alpha, beta) <= dev::kEchThinMax && dev::ech_base_fits(alpha, beta)) return direct_ech(f, h);
     // GF(2): the 8-CTA cluster kernel takes blocks of <= 1024 rows with
     // rows + cols <= 8192; anything larger follows the reference's own
     // split rule (src/jobs.cpp:202-225: rows when alpha >= beta, else

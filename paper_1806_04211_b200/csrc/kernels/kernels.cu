@@ -965,7 +965,23 @@ ech_base_kernel(std::uint32_t p, std::uint32_t magic, int rows, int cols,
   __syncthreads();
 
   int r = 0;
+  __shared__ int sel_c;
   for (int col = 0; col < cols && r < rmax; ++col) {
+    if (cols > rows) {
+      // short-wide blocks: jump to the next column holding a nonzero in a
+      // non-pivotal row (O(rows x cols) a pivot instead of a barrier round
+      // per column)
+      if (tid == 0) sel_c = cols;
+      __syncthreads();
+      const int span = cols - col;
+      for (int e = tid; e < rows * span; e += nt) {
+        const int i = e / span, c = col + e % span;
+        if (!piv[i] && w[i * cols + c]) atomicMin(&sel_c, c);
+      }
+      __syncthreads();
+      col = sel_c;
+      if (col == cols) break;  // block-uniform
+    }
     if (tid == 0) sel_s = rows;
     __syncthreads();
     for (int i = tid; i < rows; i += nt)
@@ -1025,21 +1041,30 @@ ech_base_kernel(std::uint32_t p, std::uint32_t magic, int rows, int cols,
 }
 }  // namespace
 
+std::size_t ech_base_smem(std::int64_t rows, std::int64_t cols) {
+  const std::int64_t rmax = rows < cols ? rows : cols;
+  return std::size_t(rows * cols + rows * (rmax > 0 ? rmax : 1) + 2 * rows + 256);
+}
+bool ech_base_fits(std::int64_t rows, std::int64_t cols) {
+  const std::int64_t rmax = rows < cols ? rows : cols;
+  return rmax <= kEchBaseMax && ech_base_smem(rows, cols) <= kEchBaseSmem &&
+         (rmax <= kEchThinMax || (rows <= kEchBaseMax && cols <= kEchBaseMax));
+}
+
 void ech_base(std::uint32_t p, std::int64_t rows, std::int64_t cols,
               const std::uint8_t* H, std::int64_t ldh, std::uint8_t* W,
               std::int64_t ldw, std::uint8_t* Tc, std::int64_t ldt,
               std::int32_t* info, cudaStream_t s) {
-  if (rows > kEchBaseMax || cols > kEchBaseMax)
-    throw std::invalid_argument("ech_base: block exceeds the base-case size");
-  const std::int64_t rmax = rows < cols ? rows : cols;
-  const std::size_t smem = std::size_t(rows * cols + rows * (rmax > 0 ? rmax : 1) + 2 * rows + 256);
+  if (!ech_base_fits(rows, cols)) throw std::invalid_argument("ech_base: block exceeds the base-case size");
+  const std::size_t smem = ech_base_smem(rows, cols);
   static bool attr_set = false;
   if (!attr_set) {
     GFQ_CUDA(cudaFuncSetAttribute(ech_base_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  64 * 1024));
+                                  int(kEchBaseSmem)));
     attr_set = true;
   }
   int threads = int(rows * 32);
+  if (rows * cols > 4096) threads = 1024;
   threads = threads < 64 ? 64 : (threads > 1024 ? 1024 : threads);
   ech_base_kernel<<<1, threads, smem, s>>>(p, magic_of(p), int(rows), int(cols), H, ldh, W, ldw,
                                            Tc, ldt, info);

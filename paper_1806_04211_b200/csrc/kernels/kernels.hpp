@@ -271,6 +271,13 @@ void set_entries(std::uint8_t* dst, std::int64_t ldd, const std::int32_t* pos,
 // coefficient on the q-th pivot row in discovery order) and
 // info = [rank, pivcol_0.., pivrow_0..] (2*min(rows,cols)+1 ints).
 constexpr int kEchBaseMax = 128;
+// ...and thin blocks (min(rows, cols) <= kEchThinMax, any length) whose
+// rows x (cols + min) bytes fit kEchBaseSmem: the Chief's one-column /
+// one-row ClearDowns, which the split recursion would cut into ~100 launches
+constexpr int kEchThinMax = 32;
+constexpr std::size_t kEchBaseSmem = 200 * 1024;
+std::size_t ech_base_smem(std::int64_t rows, std::int64_t cols);
+bool ech_base_fits(std::int64_t rows, std::int64_t cols);
 void ech_base(std::uint32_t p, std::int64_t rows, std::int64_t cols,
               const std::uint8_t* H, std::int64_t ldh, std::uint8_t* W,
               std::int64_t ldw, std::uint8_t* Tc, std::int64_t ldt,

@@ -396,3 +396,22 @@ def test_ech_gf2_split_vs_reference(G, case):
         assert list(e.rho.members) == list(want["rho"]) and list(e.gamma.members) == list(want["gamma"])
         for key in "MKR":
             np.testing.assert_array_equal(getattr(e, key).numpy(), want[key])
+
+
+@pytest.mark.parametrize("p", [2, 3, 251])
+def test_ech_thin_blocks(G, mode, p):
+    """Thin blocks (min(rows, cols) <= 32, the Chief's one-column / one-row
+    ClearDowns) go to the one-launch base case: tall-thin and short-wide,
+    random, sparse (mostly zero) and all-zero."""
+    f = G.FieldSpec(p)
+    for t, (m, n) in enumerate([(5000, 1), (3000, 4), (2000, 32), (1, 5000), (4, 3000), (32, 2000),
+                                (8192, 1), (1, 8192)]):
+        H = rnd(p, m, n, 500 + t)
+        check_ech(G, p, H, G.ech(f, H))
+        S = H.copy()
+        S[np.random.default_rng(t).random(S.shape) < 0.995] = 0
+        check_ech(G, p, S, G.ech(f, S))
+        Z = np.zeros((m, n), np.uint8)
+        Z[m // 2, n // 2] = 1
+        check_ech(G, p, Z, G.ech(f, Z))
+        check_ech(G, p, np.zeros((m, n), np.uint8), G.ech(f, np.zeros((m, n), np.uint8)))
