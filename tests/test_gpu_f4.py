@@ -102,17 +102,19 @@ def test_f4_not_for_other_fields(G):
         G.set_mad_policy(0)
 
 
-@pytest.mark.parametrize("shape", ["1", "4", "12"])
-def test_f4_cluster_shapes(shape):
-    """The non-default operand-sharing cluster shapes (GFQ_F4_CLUSTER, read
-    once per process; the default pairs are covered above) on the ragged
-    cases, in a child process."""
+@pytest.mark.parametrize("env", ["GFQ_F4_CLUSTER=1", "GFQ_F4_CLUSTER=4", "GFQ_F4_CLUSTER=12",
+                                 "GFQ_K1_MAX_WAVES=1"])
+def test_f4_launch_variants(env):
+    """The non-default operand-sharing cluster shapes and row-piece launches
+    (GFQ_K1_MAX_WAVES; env settings are read once per process) on the
+    ragged, extreme and large cases, in a child process."""
     import os
     import subprocess
     import sys
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-    env = dict(os.environ, GFQ_F4_CLUSTER=shape)
+    k, v = env.split("=")
     r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", "-p", "no:cacheprovider",
-                        os.path.join(root, "tests", "test_gpu_f4.py"), "-k", "random_and_ragged or extreme"],
-                       env=env, cwd=root, capture_output=True, text=True, timeout=600)
+                        os.path.join(root, "tests", "test_gpu_f4.py"), "-k",
+                        "random_and_ragged or extreme or large"],
+                       env=dict(os.environ, **{k: v}), cwd=root, capture_output=True, text=True, timeout=600)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
