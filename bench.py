@@ -401,6 +401,8 @@ def main():
                 if rank == 0:
                     out.download_blocks(dl.numpy())
             sel_bytes = 4 * out.rank * 2
+            if comm is None:
+                xfer = G.last_transfer_bytes()  # what crossed PCIe inside the call
             e1.record()
             e1.synchronize()
             et.append(e0.elapsed_time(e1))
@@ -411,8 +413,8 @@ def main():
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             e_ms = float(t.item())
         e2e = {"value": work / (e_ms / 1e3), "unit": UNIT,
-               "h2d_bytes_per_step": world * cfg["m"] * cfg["n"],
-               "d2h_bytes_per_step": int(nbytes + sel_bytes), "ms_per_step": e_ms,
+               "h2d_bytes_per_step": xfer[0] if comm is None else world * cfg["m"] * cfg["n"],
+               "d2h_bytes_per_step": int((xfer[1] if comm is None else nbytes) + sel_bytes), "ms_per_step": e_ms,
                "path": "gfq_echelonize_host_into (pinned host C -> HBM, every output block -> pinned host as it becomes final)" if comm is None
                else "each rank uploads pinned host C, gfq_echelonize_dist(gather), rank 0 downloads all blocks"}
 

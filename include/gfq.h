@@ -250,6 +250,13 @@ int gfq_echelonize_host(uint32_t p, int64_t m, int64_t n, const uint8_t* C, int6
 int gfq_echelonize_host_into(uint32_t p, int64_t m, int64_t n, const uint8_t* C, int64_t ld,
                              const gfq_options* opt, uint8_t* host_out, uint64_t cap,
                              gfq_output** out);
+/* Optional (off by default; GFQ_HOST_PACK=1 or gfq_set_host_pack(1)): GF(2)
+ * host buffers cross PCIe packed 8:1 -- host threads pack C before its
+ * upload and unpack the downloaded blocks into host_out.  Pays where host
+ * memory bandwidth well exceeds PCIe's.  The bytes that crossed PCIe in the
+ * calling thread's last gfq_echelonize_host / _host_into call: */
+int gfq_set_host_pack(int on);
+int gfq_last_transfer_bytes(int64_t* h2d, int64_t* d2h);
 
 int gfq_output_rank(const gfq_output* o, uint64_t* rank);
 int gfq_output_grid(const gfq_output* o, uint64_t* a, uint64_t* b);

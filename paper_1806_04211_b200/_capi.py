@@ -57,6 +57,8 @@ PROTOS = {
     "gfq_mat_upload": (I, [I64, I64, c_u8p, I64, vpp]),
     "gfq_mat_upload32": (I, [I64, I64, c_u32p, I64, vpp]),
     "gfq_mat_esize": (I, [vp, ctypes.POINTER(ctypes.c_int)]),
+    "gfq_last_transfer_bytes": (I, [ctypes.POINTER(ctypes.c_int64), ctypes.POINTER(ctypes.c_int64)]),
+    "gfq_set_host_pack": (I, [ctypes.c_int]),
     "gfq_mat_copy_device": (I, [I64, I64, vp, I64, vpp]),
     "gfq_mat_shape": (I, [vp, c_i64p, c_i64p]),
     "gfq_mat_download": (I, [vp, c_u8p, I64]),

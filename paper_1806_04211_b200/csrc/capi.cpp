@@ -6,6 +6,7 @@
 
 #include "../../include/gfq.h"
 #include "host/chief.hpp"
+#include "host/hostpack.hpp"
 #include "host/dist.hpp"
 #include "host/io.hpp"
 #include "host/jobs.hpp"
@@ -166,6 +167,15 @@ int gfq_mat_upload32(int64_t rows, int64_t cols, const uint32_t* host, int64_t l
     require_device();
     *out = wrap(host ? gfq::Mat::from_host(rows, cols, reinterpret_cast<const uint8_t*>(host), ld * 4, 4)
                      : gfq::Mat::zeros(rows, cols, 4));
+  });
+}
+int gfq_set_host_pack(int on) {
+  return guard([&] { gfq::hostpack::set_enabled(on != 0); });
+}
+int gfq_last_transfer_bytes(int64_t* h2d, int64_t* d2h) {
+  return guard([&] {
+    *h2d = gfq::hostpack::last_transfer().h2d;
+    *d2h = gfq::hostpack::last_transfer().d2h;
   });
 }
 int gfq_mat_esize(const gfq_mat* m, int* esize) {

@@ -17,6 +17,7 @@
 #include <stdexcept>
 
 #include "../kernels/kernels.hpp"
+#include "hostpack.hpp"
 #include "jobs.hpp"
 
 namespace gfq {
@@ -480,9 +481,12 @@ cudaEvent_t g_e2e_t0 = nullptr;
 
 class EarlyDownload {
  public:
+  // packed: GF(2) blocks leave HBM as bit rows (dev::pack_bits), cross PCIe
+  // into a pinned staging buffer and are unpacked into `host` by the host
+  // pool (hostpack) -- an eighth of the PCIe bytes
   EarlyDownload(const PlanHandles& h, const ChopSpec& cs, bool with_transform, std::uint8_t* host,
-                std::uint64_t cap)
-      : h_(h), cs_(cs), host_(host), cap_(cap) {
+                std::uint64_t cap, bool packed)
+      : h_(h), cs_(cs), host_(host), cap_(cap), packed_(packed) {
     const std::size_t a = cs.a(), b = cs.b();
     for (std::size_t j = 0; j < b; ++j)
       for (std::size_t l = j; l < b; ++l)
@@ -535,17 +539,41 @@ class EarlyDownload {
       }
       thread_.join();
       GFQ_CUDA(cudaStreamSynchronize(stream_));
+      unpacked_.wait();  // the host unpacks of the last blocks
     }
     if (!error_.empty()) throw std::runtime_error("early download: " + error_);
   }
+  std::int64_t d2h_bytes() const { return d2h_; }
 
  private:
   struct Blk {
     int kind;
     std::size_t x, y;
     std::int32_t slot, part;
-    std::uint64_t off = 0, rows = 0, cols = 0;
+    std::uint64_t off = 0, rows = 0, cols = 0, poff = 0;
   };
+  struct Unpack {
+    EarlyDownload* self;
+    const std::uint8_t* src;
+    std::int64_t ldb, rows, cols;
+    std::uint8_t* dst;
+  };
+  // stream callback once a packed block landed in the staging buffer: the
+  // unpack goes to the host pool in row chunks (no CUDA calls here)
+  static void CUDART_CB on_landed(void* p) {
+    auto* u = static_cast<Unpack*>(p);
+    const std::int64_t chunk = 512;
+    const std::int64_t n = (u->rows + chunk - 1) / chunk;
+    u->self->unpacked_.add(n);
+    for (std::int64_t r = 0; r < u->rows; r += chunk) {
+      const std::int64_t nr = std::min(chunk, u->rows - r);
+      hostpack::submit([u, r, nr] {
+        hostpack::unpack_rows(u->src + r * u->ldb, u->ldb, nr, u->cols, u->dst + r * u->cols, u->cols);
+        u->self->unpacked_.done();
+      });
+    }
+    u->self->unpacked_.done();  // the block's own count (issue)
+  }
   void add(int kind, std::size_t x, std::size_t y, std::int32_t slot, std::int32_t part) {
     by_slot_[slot].push_back(blocks_.size());
     blocks_.push_back(Blk{kind, x, y, slot, part});
@@ -583,7 +611,7 @@ class EarlyDownload {
   void make_layout() {
     const auto gam = [&](std::size_t j) { return std::get<PkgD>(pubs_[h_.d_final[j]]->value).gamma.size(); };
     const auto rho = [&](std::size_t i) { return std::get<PkgE>(pubs_[h_.e_final[i]]->value).rho.size(); };
-    std::uint64_t off = 0;
+    std::uint64_t off = 0, poff = 0;
     for (auto& bk : blocks_) {
       if (bk.kind == 0) {
         bk.rows = gam(bk.x);
@@ -597,8 +625,14 @@ class EarlyDownload {
       }
       bk.off = off;
       off += bk.rows * bk.cols;
+      bk.poff = poff;
+      poff += bk.rows * ((bk.cols + 63) / 64 * 8);  // 8-byte aligned packed rows
     }
     if (off > cap_) throw std::invalid_argument("host_out buffer too small");
+    if (packed_) {
+      dstage_ = std::make_unique<DevBuf>(std::size_t(poff));
+      hstage_ = std::make_unique<hostpack::PinnedLease>(std::size_t(poff));
+    }
     layout_ = true;
   }
   void issue(std::int32_t sid, const Published& pub) {
@@ -625,9 +659,23 @@ class EarlyDownload {
                           ev);
       }
       waited = true;
-      GFQ_CUDA(cudaMemcpy2DAsync(host_ + bk.off, std::size_t(bk.cols), m.data(), std::size_t(m.ld()),
-                                 std::size_t(bk.cols), std::size_t(bk.rows), cudaMemcpyDeviceToHost,
-                                 stream_));
+      if (packed_) {
+        const std::int64_t ldb = std::int64_t((bk.cols + 63) / 64 * 8);
+        const std::int64_t rows = std::int64_t(bk.rows), cols = std::int64_t(bk.cols);
+        dev::pack_bits(m.data(), m.ld(), rows, cols, dstage_->ptr + bk.poff, ldb, stream_);
+        GFQ_CUDA(cudaMemcpyAsync(hstage_->data() + bk.poff, dstage_->ptr + bk.poff, std::size_t(rows * ldb),
+                                 cudaMemcpyDeviceToHost, stream_));
+        d2h_ += rows * ldb;
+        jobs_.push_back(std::make_unique<Unpack>(Unpack{this, hstage_->data() + bk.poff, ldb, rows, cols,
+                                                        host_ + bk.off}));
+        unpacked_.add(1);
+        GFQ_CUDA(cudaLaunchHostFunc(stream_, &EarlyDownload::on_landed, jobs_.back().get()));
+      } else {
+        GFQ_CUDA(cudaMemcpy2DAsync(host_ + bk.off, std::size_t(bk.cols), m.data(), std::size_t(m.ld()),
+                                   std::size_t(bk.cols), std::size_t(bk.rows), cudaMemcpyDeviceToHost,
+                                   stream_));
+        d2h_ += std::int64_t(bk.rows * bk.cols);
+      }
       if (e2e_debug()) {
         cudaEvent_t ev;
         GFQ_CUDA(cudaEventCreate(&ev));
@@ -643,6 +691,12 @@ class EarlyDownload {
   const ChopSpec& cs_;
   std::uint8_t* host_;
   std::uint64_t cap_;
+  bool packed_;
+  std::unique_ptr<DevBuf> dstage_;
+  std::unique_ptr<hostpack::PinnedLease> hstage_;
+  std::vector<std::unique_ptr<Unpack>> jobs_;
+  hostpack::Latch unpacked_;
+  std::int64_t d2h_ = 0;
   std::vector<Blk> blocks_;
   std::unordered_map<std::int32_t, std::vector<std::size_t>> by_slot_;
   std::unordered_set<std::int32_t> interest_;
@@ -704,6 +758,13 @@ EchelonOutput echelonize_host(const std::uint8_t* host, std::int64_t m, std::int
   cudaStream_t cs_stream;
   GFQ_CUDA(cudaStreamCreateWithFlags(&cs_stream, cudaStreamNonBlocking));
   std::vector<std::shared_ptr<EventBox>> row_ready;
+  // (outside the try: the copy stream and the pool may still use them when
+  // an exception unwinds)
+  const bool packed = field.p() == 2 && !field.is_ext() && hostpack::enabled();
+  const std::int64_t ldb = (n + 63) / 64 * 8;
+  std::unique_ptr<hostpack::PinnedLease> stage;
+  std::unique_ptr<DevBuf> dpk;
+  std::vector<std::unique_ptr<hostpack::Latch>> packed_rows;
   try {
     auto alloc_done = std::make_shared<EventBox>();
     GFQ_CUDA(cudaEventRecord(alloc_done->ev, cur_stream()));
@@ -713,11 +774,47 @@ EchelonOutput echelonize_host(const std::uint8_t* host, std::int64_t m, std::int
       if (!g_e2e_t0) GFQ_CUDA(cudaEventCreate(&g_e2e_t0));
       GFQ_CUDA(cudaEventRecord(g_e2e_t0, cs_stream));
     }
+    // GF(2): the pool packs each block row to bits in a pinned staging
+    // buffer (row order, so block row 0 is ready first); the copy stream
+    // waits for a block row's packing (a host function blocking the stream),
+    // copies an eighth of the bytes and unpacks them in HBM
+    if (packed) {
+      stage = std::make_unique<hostpack::PinnedLease>(std::size_t(m * ldb));
+      dpk = std::make_unique<DevBuf>(std::size_t(m * ldb));
+      const std::int64_t chunk = 256;
+      for (std::size_t i = 0; i < cs.a(); ++i) {
+        const std::int64_t nr = std::int64_t(cs.row_parts[i]);
+        packed_rows.push_back(std::make_unique<hostpack::Latch>((nr + chunk - 1) / chunk));
+      }
+      for (std::size_t i = 0; i < cs.a(); ++i) {
+        const std::int64_t r0 = std::int64_t(cs.row_offset(i)), nr = std::int64_t(cs.row_parts[i]);
+        hostpack::Latch* l = packed_rows[i].get();
+        std::uint8_t* st = stage->data();
+        for (std::int64_t r = 0; r < nr; r += chunk) {
+          const std::int64_t k = std::min(chunk, nr - r);
+          hostpack::submit([=] {
+            hostpack::pack_rows(host + (r0 + r) * ld, ld, k, n, st + (r0 + r) * ldb, ldb);
+            l->done();
+          });
+        }
+      }
+      hostpack::last_transfer().h2d = m * ldb;
+    } else {
+      hostpack::last_transfer().h2d = m * n;
+    }
     for (std::size_t i = 0; i < cs.a(); ++i) {
       const std::int64_t r0 = std::int64_t(cs.row_offset(i)), nr = std::int64_t(cs.row_parts[i]);
-      GFQ_CUDA(cudaMemcpy2DAsync(C.data() + r0 * C.ld(), std::size_t(C.ld()), host + r0 * ld,
-                                 std::size_t(ld), std::size_t(n), std::size_t(nr),
+      if (packed) {
+        GFQ_CUDA(cudaLaunchHostFunc(
+            cs_stream, [](void* p) { static_cast<hostpack::Latch*>(p)->wait(); }, packed_rows[i].get()));
+        GFQ_CUDA(cudaMemcpyAsync(dpk->ptr + r0 * ldb, stage->data() + r0 * ldb, std::size_t(nr * ldb),
                                  cudaMemcpyHostToDevice, cs_stream));
+        dev::unpack_bits(dpk->ptr + r0 * ldb, ldb, nr, n, C.data() + r0 * C.ld(), C.ld(), cs_stream);
+      } else {
+        GFQ_CUDA(cudaMemcpy2DAsync(C.data() + r0 * C.ld(), std::size_t(C.ld()), host + r0 * ld,
+                                   std::size_t(ld), std::size_t(n), std::size_t(nr),
+                                   cudaMemcpyHostToDevice, cs_stream));
+      }
       auto ev = std::make_shared<EventBox>();
       GFQ_CUDA(cudaEventRecord(ev->ev, cs_stream));
       row_ready.push_back(std::move(ev));
@@ -743,6 +840,7 @@ EchelonOutput echelonize_host(const std::uint8_t* host, std::int64_t m, std::int
     if (e2e_debug()) std::fprintf(stderr, "e2e host: return at %.2f ms\n", hms());
     return out;
   } catch (...) {
+    for (auto& l : packed_rows) l->wait();
     cudaStreamSynchronize(cs_stream);
     cudaStreamDestroy(cs_stream);
     throw;
@@ -812,13 +910,17 @@ EchelonOutput echelonize_impl(const Mat& C, const FieldSpec& field, const Echelo
   std::unique_ptr<EarlyDownload> early;
   if (options.host_out) {
     early = std::make_unique<EarlyDownload>(h, cs, options.with_transform, options.host_out,
-                                            options.host_out_cap);
+                                            options.host_out_cap,
+                                            field.p() == 2 && !field.is_ext() && hostpack::enabled());
     ro.on_publish = [&early](std::int32_t sid, const std::shared_ptr<Published>& pub) {
       early->publish(sid, pub);
     };
   }
   RunReport rep = run(graph, ro);
-  if (early) early->finish();
+  if (early) {
+    early->finish();
+    hostpack::last_transfer().d2h = early->d2h_bytes();
+  }
   if (report) *report = std::move(rep);
 
   for (std::size_t j = 0; j < b; ++j) {

@@ -263,6 +263,14 @@ bool select2d_inline(std::uint8_t* dst, std::int64_t ldd, std::int64_t rows, std
 void set_entries(std::uint8_t* dst, std::int64_t ldd, const std::int32_t* pos,
                  std::int64_t n, std::uint8_t value, cudaStream_t s);
 
+// ---------------------------------------------------------------- bits
+// GF(2) transfers (bits.cu): rows x cols byte matrix <-> packed bit rows of
+// ceil(cols / 8) bytes (element c at bit c % 8 of byte c / 8).
+void pack_bits(const std::uint8_t* src, std::int64_t ld, std::int64_t rows, std::int64_t cols, std::uint8_t* dst,
+               std::int64_t ldb, cudaStream_t s);
+void unpack_bits(const std::uint8_t* src, std::int64_t ldb, std::int64_t rows, std::int64_t cols, std::uint8_t* dst,
+                 std::int64_t ld, cudaStream_t s);
+
 // ---------------------------------------------------------------- K2
 // Base-case ECH of a small block (rows, cols <= kEchBaseMax) in one CTA:
 // column-wise Gauss-Jordan with the reference's pivot rule (first

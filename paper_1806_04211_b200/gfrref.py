@@ -1056,6 +1056,19 @@ def profile_take_kinds(with_union: bool = False):
     return {name: (l[q], w[q], t[q]) for q, name in enumerate(PROFILE_KINDS)}
 
 
+def set_host_pack(on: bool):
+    """GF(2) host buffers cross PCIe packed 8:1 (off by default)."""
+    _check(lib().gfq_set_host_pack(1 if on else 0))
+
+
+def last_transfer_bytes():
+    """(h2d, d2h): bytes that crossed PCIe in this thread's last host-buffer
+    echelonize (GF(2) buffers travel packed 8:1)."""
+    h, d = ctypes.c_int64(0), ctypes.c_int64(0)
+    _check(lib().gfq_last_transfer_bytes(ctypes.byref(h), ctypes.byref(d)))
+    return h.value, d.value
+
+
 def set_stream(stream_ptr: int):
     _check(lib().gfq_set_stream(stream_ptr or None))
 

@@ -335,3 +335,38 @@ def test_memory_stability_acceptance_criterion6(G, threads, fuse):
     assert step1 > 0
     assert rep["peak_live_bytes"] <= 4.0 * input_bytes, (rep["peak_live_bytes"], input_bytes)
     assert step3 <= 1.6 * step1, (step3, step1)
+
+
+@pytest.fixture
+def host_pack(G):
+    G.set_host_pack(True)
+    yield
+    G.set_host_pack(False)
+
+
+@pytest.mark.parametrize("m,n,block", [(333, 517, 100), (1000, 70, 64), (64, 1000, 200), (517, 333, 517)])
+def test_gf2_host_buffers_cross_pcie_packed(G, host_pack, m, n, block):
+    """GF(2) host buffers travel packed 8:1 when asked (csrc/host/hostpack.cpp
+    + kernels/bits.cu): the host-input run equals the device-input run, the
+    streamed host_out equals gfq_output_download_blocks, and the PCIe byte
+    counts are the packed sizes (rows padded to 8-byte words)."""
+    f = G.FieldSpec(2)
+    C = oracle.random_matrix(2, m, n, 11)
+    opts = G.EchelonizeOptions(block=block, threads=3, with_transform=True)
+    dev = G.echelonize(G.Matrix.from_numpy(C), f, opts)
+    want = np.zeros(dev.block_bytes(), np.uint8)
+    dev.download_blocks(want)
+    buf = np.full(dev.block_bytes() + 5, 0xCD, np.uint8)
+    out = G.echelonize(C, f, opts, host_out=buf)
+    assert out.rank == dev.rank
+    np.testing.assert_array_equal(buf[: want.size], want)
+    assert (buf[want.size:] == 0xCD).all()
+    h2d, d2h = G.last_transfer_bytes()
+    assert h2d == m * ((n + 63) // 64 * 8)
+    assert 0 < d2h <= want.size // 8 + 8 * 64 * 64 and d2h < want.size
+
+
+def test_host_buffers_cross_pcie_as_bytes_by_default(G):
+    C = oracle.random_matrix(2, 200, 300, 12)
+    G.echelonize(C, G.FieldSpec(2), G.EchelonizeOptions(block=64))
+    assert G.last_transfer_bytes()[0] == 200 * 300
