@@ -246,11 +246,13 @@ PlanHandles build_plan_fused(TaskGraph& graph, const Mat& C, const FieldSpec& fi
     return C.row_view(std::int64_t(cs.row_offset(i)), std::int64_t(cs.row_parts[i]))
         .col_view(std::int64_t(cs.col_offset(k)), std::int64_t(cs.col_parts[k]));
   };
-  const auto ready = [&](std::size_t i) {
-    return row_ready ? (*row_ready)[i] : std::shared_ptr<EventBox>();
+  // row_ready holds two events a block row: [2i] block column 0 landed
+  // (all ClearDown(i, 0) needs), [2i + 1] the rest of the row
+  const auto ready = [&](std::size_t i, std::size_t part = 1) {
+    return row_ready ? (*row_ready)[2 * i + part] : std::shared_ptr<EventBox>();
   };
   for (std::size_t i = 0; i < a; ++i) {
-    graph.add_input({K::C, std::uint16_t(i), 0, 0, 0}, blk(i, 0), ready(i), true);
+    graph.add_input({K::C, std::uint16_t(i), 0, 0, 0}, blk(i, 0), ready(i, 0), true);
     if (b > 1) {
       MatParts panel;
       const std::int64_t o1 = std::int64_t(cs.col_offset(1));
@@ -387,9 +389,22 @@ PlanHandles build_plan_fused(TaskGraph& graph, const Mat& C, const FieldSpec& fi
   for (std::size_t k = 0; k < b; ++k)
     e.node(T::Copy, -1, std::int32_t(k), -1, plate(a + b + (b - 1 - k)),
            {e.slot(K::D, k, 0, 0, a - 1)}, {e.slot(K::R, k, k, 0, 0)});
+  // Step-3 order.  ClearUp(k, j) needs row k final and row j's ClearUp(k+1, j):
+  // the reference walks k outermost (every row finishes in the last few
+  // steps).  Row-major order (default; GFQ_STEP3_ORDER=0 restores k
+  // outermost) is another topological order of the same DAG: row j gets all
+  // its updates k = b-1 .. j+1 before row j-1 does, so rows become final
+  // one by one from the bottom and the host-buffer path downloads row j
+  // while rows < j are still being cleared.
+  static const bool row_major = [] {
+    const char* v = std::getenv("GFQ_STEP3_ORDER");
+    return !v || std::atoi(v) != 0;
+  }();
   for (std::size_t k = b; k-- > 1;) {
-    const std::int32_t pri = plate(a + b + (b - 1 - k));
     for (std::size_t j = 0; j < k; ++j) {
+      const std::int32_t pri = row_major && w_pri != 1
+                                   ? plate(a + b + b + (b - 1 - j) * b + (b - 1 - k))
+                                   : plate(a + b + (b - 1 - k));
       const std::int32_t sX = e.slot(K::X, j, k, 0, 0);
       if (k == j + 1)
         e.node(T::PreClearUp, -1, std::int32_t(j), std::int32_t(k), pri,
@@ -810,10 +825,23 @@ EchelonOutput echelonize_host(const std::uint8_t* host, std::int64_t m, std::int
         GFQ_CUDA(cudaMemcpyAsync(dpk->ptr + r0 * ldb, stage->data() + r0 * ldb, std::size_t(nr * ldb),
                                  cudaMemcpyHostToDevice, cs_stream));
         dev::unpack_bits(dpk->ptr + r0 * ldb, ldb, nr, n, C.data() + r0 * C.ld(), C.ld(), cs_stream);
+        auto ev0 = std::make_shared<EventBox>();
+        GFQ_CUDA(cudaEventRecord(ev0->ev, cs_stream));
+        row_ready.push_back(ev0);
       } else {
+        // block column 0 first: the row's ClearDown(i, 0) -- for i = 0 the
+        // first diagonal ECH -- starts while the rest of the row is in flight
+        const std::int64_t c0 = cs.b() > 1 ? std::int64_t(cs.col_parts[0]) : n;
         GFQ_CUDA(cudaMemcpy2DAsync(C.data() + r0 * C.ld(), std::size_t(C.ld()), host + r0 * ld,
-                                   std::size_t(ld), std::size_t(n), std::size_t(nr),
+                                   std::size_t(ld), std::size_t(c0), std::size_t(nr),
                                    cudaMemcpyHostToDevice, cs_stream));
+        auto ev0 = std::make_shared<EventBox>();
+        GFQ_CUDA(cudaEventRecord(ev0->ev, cs_stream));
+        row_ready.push_back(std::move(ev0));
+        if (c0 < n)
+          GFQ_CUDA(cudaMemcpy2DAsync(C.data() + r0 * C.ld() + c0, std::size_t(C.ld()),
+                                     host + r0 * ld + c0, std::size_t(ld), std::size_t(n - c0),
+                                     std::size_t(nr), cudaMemcpyHostToDevice, cs_stream));
       }
       auto ev = std::make_shared<EventBox>();
       GFQ_CUDA(cudaEventRecord(ev->ev, cs_stream));

@@ -80,7 +80,8 @@ struct EchelonizeOptions {
 };
 
 /// The fused single-GPU plan (same values, wide jobs per panel).  With
-/// row_ready, block row i of C is valid once row_ready[i] fires.
+/// row_ready, block row i of C is valid once row_ready[2i] (its block
+/// column 0) and row_ready[2i + 1] (the rest of the row) have fired.
 PlanHandles build_plan_fused(TaskGraph& graph, const Mat& C, const FieldSpec& field,
                              const ChopSpec& chop, bool with_transform,
                              const std::vector<std::shared_ptr<EventBox>>* row_ready = nullptr);

@@ -5,6 +5,9 @@
 #include <cstdlib>
 #include <string>
 #include <atomic>
+#include <memory>
+#include <mutex>
+#include <vector>
 #include <stdexcept>
 
 #include "../kernels/kernels.hpp"
@@ -114,6 +117,58 @@ void set_ech_base(std::size_t n) {
 }
 std::size_t ech_base() { return g_ech_base; }
 
+// ---------------------------------------------------------------- packed B cache
+namespace {
+thread_local DevBuf* t_b_owner = nullptr;
+struct PackedB {
+  const std::uint8_t* src;
+  std::int64_t n, k, ldb;
+  std::uint32_t p;
+  cudaStream_t stream;
+  cudaEvent_t ev = nullptr;
+  std::unique_ptr<DevBuf> buf;
+};
+struct PackedBCache {
+  std::mutex mtx;
+  std::vector<PackedB> items;
+  ~PackedBCache() {
+    for (auto& it : items)
+      if (it.ev) cudaEventDestroy(it.ev);
+  }
+};
+std::mutex g_packed_create_mtx;
+// The packing of B (k x n at ldb) held with its storage, made on `s` if this
+// is the first contraction to need it; nullptr when B is not inside the
+// thread's ImmutableB scope.  The returned block is ordered before s.
+const std::uint8_t* packed_b_for(std::uint32_t p, std::int64_t n, std::int64_t k, const std::uint8_t* B,
+                                 std::int64_t ldb, cudaStream_t s) {
+  static const bool off = std::getenv("GFQ_NO_BPACK_CACHE") != nullptr;
+  DevBuf* owner = t_b_owner;
+  if (off || !owner || !owner->ptr || B < owner->ptr || B >= owner->ptr + owner->bytes) return nullptr;
+  PackedBCache* cache;
+  {
+    std::lock_guard<std::mutex> lk(g_packed_create_mtx);
+    if (!owner->packed_b) owner->packed_b = std::make_shared<PackedBCache>();
+    cache = static_cast<PackedBCache*>(owner->packed_b.get());
+  }
+  std::lock_guard<std::mutex> lk(cache->mtx);
+  for (const PackedB& it : cache->items)
+    if (it.src == B && it.n == n && it.k == k && it.ldb == ldb && it.p == p) {
+      if (it.stream != s) GFQ_CUDA(cudaStreamWaitEvent(s, it.ev, 0));
+      return it.buf->ptr;
+    }
+  PackedB it{B, n, k, ldb, p, s, nullptr, nullptr};
+  it.buf = std::make_unique<DevBuf>(static_cast<std::size_t>(dev::mad_f4_bt_bytes(n, k)));
+  GFQ_CUDA(cudaEventCreateWithFlags(&it.ev, cudaEventDisableTiming));
+  dev::pack_b_f4(p, n, k, B, ldb, it.buf->ptr, s);
+  GFQ_CUDA(cudaEventRecord(it.ev, s));
+  cache->items.push_back(std::move(it));
+  return cache->items.back().buf->ptr;
+}
+}  // namespace
+ImmutableB::ImmutableB(const Mat& b) : prev_(t_b_owner) { t_b_owner = b.buf().get(); }
+ImmutableB::~ImmutableB() { t_b_owner = prev_; }
+
 // ---------------------------------------------------------------- products
 // D = (Cin ? Cin : 0) + A.B over the field: K1 for GF(p), the digit-plane
 // contraction (dev::mad_ext, one K1 launch over GF(p)) for GF(p^k).
@@ -129,8 +184,13 @@ void field_mad(const FieldSpec& f, std::int64_t m, std::int64_t n, std::int64_t 
     // K1f (FP4 tensor cores) for the small fields: its packed operands live
     // in a stream-ordered scratch block on this (the current) stream
     if (s == cur_stream_raw() && dev::use_f4(f.p(), m, n, k)) {
-      DevBuf scratch{static_cast<std::size_t>(dev::mad_f4_scratch_bytes(m, n, k))};
-      if (dev::mad_f4(f.p(), m, n, k, A, lda, B, ldb, Cin, ldc, D, ldd, scratch.ptr, s)) return;
+      if (const std::uint8_t* bt = packed_b_for(f.p(), n, k, B, ldb, s)) {
+        DevBuf scratch{static_cast<std::size_t>(dev::mad_f4_scratch_bytes(m, 0, k))};
+        if (dev::mad_f4(f.p(), m, n, k, A, lda, B, ldb, Cin, ldc, D, ldd, scratch.ptr, s, bt)) return;
+      } else {
+        DevBuf scratch{static_cast<std::size_t>(dev::mad_f4_scratch_bytes(m, n, k))};
+        if (dev::mad_f4(f.p(), m, n, k, A, lda, B, ldb, Cin, ldc, D, ldd, scratch.ptr, s)) return;
+      }
     }
     dev::mad(f.p(), m, n, k, A, lda, B, ldb, Cin, ldc, D, ldd, s);
     return;

@@ -27,6 +27,23 @@ Mat mat_mul_add(const FieldSpec& f, const Mat& a, const Mat& b, const Mat& c);  
 /// d = (addend ? addend : 0) + b.c written into an existing matrix or view
 /// (the fused plan's wide outputs); addend may alias d.
 void mad_into(const FieldSpec& f, const Mat& d, const Mat* addend, const Mat& b, const Mat& c);
+/// While alive on this thread, contractions whose B operand lies inside
+/// `b`'s storage may keep (and reuse) its K1f packing with that storage.
+/// For published, immutable packages only: the pivot rows B(j, k) / the
+/// T_M(j, .) panels that every block row below multiplies by, and Step 3's
+/// final rows -- the packing (a transpose to K-major E2M1 codes) is then
+/// done once per package instead of once per product.  GFQ_NO_BPACK_CACHE=1
+/// turns it off.
+class ImmutableB {
+ public:
+  explicit ImmutableB(const Mat& b);
+  ~ImmutableB();
+  ImmutableB(const ImmutableB&) = delete;
+  ImmutableB& operator=(const ImmutableB&) = delete;
+
+ private:
+  DevBuf* prev_;
+};
 /// out[:, c] = m[:, cmap[c]] (cmap[c] = -1: zero column), one K3 launch.
 Mat col_gather(const Mat& m, std::int64_t out_cols, const std::vector<std::int32_t>& cmap);
 /// out[:, c] = a[:, cmap[c]] (>= 0), b[:, -cmap[c]-2] (<= -2) or 0 (-1); one K3 launch.

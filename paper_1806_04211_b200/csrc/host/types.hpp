@@ -91,6 +91,10 @@ struct DevBuf {
   ~DevBuf();
   DevBuf(const DevBuf&) = delete;
   DevBuf& operator=(const DevBuf&) = delete;
+  /// K1f packings of B operands that live in this block (jobs.cpp,
+  /// ImmutableB): created by the first contraction that needs one, shared
+  /// by the later ones, released with the block.
+  std::shared_ptr<void> packed_b;
 };
 
 /// The stream `s` has drained (synchronised): blocks released on it become
@@ -130,6 +134,7 @@ class Mat {
   /// bytes of one row's elements
   std::int64_t row_bytes() const { return cols_ * esize_; }
   std::uint8_t* data() const { return data_; }
+  const std::shared_ptr<DevBuf>& buf() const { return buf_; }
   bool empty() const { return rows_ == 0 || cols_ == 0; }
 
   /// A matrix living inside an existing allocation (e.g. a received

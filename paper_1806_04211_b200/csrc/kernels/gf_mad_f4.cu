@@ -500,11 +500,33 @@ std::int64_t mad_f4_scratch_bytes(std::int64_t m, std::int64_t n, std::int64_t k
   return (m + n) * kpb + 256;
 }
 
+std::int64_t mad_f4_bt_bytes(std::int64_t n, std::int64_t k) {
+  const std::int64_t kpb = (k + 63) / 64 * 32;
+  return n * kpb + 256;
+}
+
+void pack_b_f4(std::uint32_t p, std::int64_t n, std::int64_t k, const std::uint8_t* B, std::int64_t ldb,
+               std::uint8_t* bt, cudaStream_t s) {
+  using namespace f4;
+  static const bool once = [] {
+    GFQ_CUDA(cudaFuncSetAttribute(pack_cols_f4_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, PC_SMEM));
+    return true;
+  }();
+  (void)once;
+  const std::int64_t kpb = (k + 63) / 64 * 32;
+  ProfScope ps(kProfSelect, double(n) * double(k) * 1.5, s);
+  GFQ_CUDA(launch_pdl(pack_cols_f4_kernel, dim3(unsigned((n + PC_N - 1) / PC_N), unsigned((kpb + 63) / 64)),
+                      dim3(256), std::size_t(PC_SMEM), s, B, ldb, int(k), int(n), bt, int(kpb), code_word(p)));
+  count_launch();
+}
+
 bool mad_f4(std::uint32_t p, std::int64_t m, std::int64_t n, std::int64_t k, const std::uint8_t* A,
             std::int64_t lda, const std::uint8_t* B, std::int64_t ldb, const std::uint8_t* Cin, std::int64_t ldc,
-            std::uint8_t* D, std::int64_t ldd, std::uint8_t* scratch, cudaStream_t s) {
+            std::uint8_t* D, std::int64_t ldd, std::uint8_t* scratch, cudaStream_t s,
+            const std::uint8_t* bt_packed) {
   using namespace f4;
   if (!f4_field(p) || m <= 0 || n <= 0 || k <= 0) return false;
+  if ((reinterpret_cast<std::uintptr_t>(bt_packed) & 15) != 0) return false;
   // |sum| <= h^2 k must stay below 2^24 (h = (p-1)/2, 1 for p = 2)
   const std::int64_t h = p == 2 ? 1 : (p - 1) / 2;
   if (h * h * k >= (std::int64_t(1) << 24) || m >= (1LL << 31) || n >= (1LL << 31)) return false;
@@ -563,7 +585,9 @@ bool mad_f4(std::uint32_t p, std::int64_t m, std::int64_t n, std::int64_t k, con
   }();
   const std::int64_t kpb = (k + 63) / 64 * 32;
   std::uint8_t* Ap = scratch;
-  std::uint8_t* Bt = scratch + (m * kpb + 127) / 128 * 128;
+  // B already packed (pack_b_f4 into a mad_f4_bt_bytes block, ordered before
+  // this call on s): the scratch then only holds A
+  const std::uint8_t* Bt = bt_packed ? bt_packed : scratch + (m * kpb + 127) / 128 * 128;
   CUtensorMap mA, mB;
   if (!make_map_box(&mA, Ap, kpb, m, kpb, BKB, std::uint32_t(BM / cn))) return false;
   if (!make_map_box(&mB, Bt, kpb, n, kpb, BKB, std::uint32_t(BN / cm))) return false;
@@ -577,13 +601,7 @@ bool mad_f4(std::uint32_t p, std::int64_t m, std::int64_t n, std::int64_t k, con
                         codes));
     count_launch();
   }
-  {
-    ProfScope ps(kProfSelect, double(n) * double(k) * 1.5, s);
-    GFQ_CUDA(launch_pdl(pack_cols_f4_kernel, dim3(unsigned((n + PC_N - 1) / PC_N), unsigned((kpb + 63) / 64)),
-                        dim3(256), std::size_t(PC_SMEM), s,
-                      B, ldb, int(k), int(n), Bt, int(kpb), codes));
-    count_launch();
-  }
+  if (!bt_packed) pack_b_f4(p, n, k, B, ldb, scratch + (m * kpb + 127) / 128 * 128, s);
   const std::int64_t sms = k1_sms(s);
   const std::int64_t tiles_per_rowtile = (n + BN - 1) / BN;
   // row pieces of <= GFQ_K1_MAX_WAVES tile waves each (see mad_tc)

@@ -369,7 +369,11 @@ bool stream_is_critical(cudaStream_t s) {
   return pr == greatest && greatest != 0;
 }
 namespace {
-std::atomic<bool> g_partition{false};
+// GFQ_PARTITION=1 also turns it on outside the Chief (job-level experiments)
+std::atomic<bool> g_partition{[] {
+  const char* e = std::getenv("GFQ_PARTITION");
+  return e && e[0] == '1';
+}()};
 }  // namespace
 void set_critical_partition(bool on) { g_partition = on; }
 bool critical_partition() { return g_partition; }

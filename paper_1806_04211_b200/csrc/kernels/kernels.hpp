@@ -117,7 +117,14 @@ bool use_f4(std::uint32_t p, std::int64_t m, std::int64_t n, std::int64_t k);
 std::int64_t mad_f4_scratch_bytes(std::int64_t m, std::int64_t n, std::int64_t k);
 bool mad_f4(std::uint32_t p, std::int64_t m, std::int64_t n, std::int64_t k, const std::uint8_t* A,
             std::int64_t lda, const std::uint8_t* B, std::int64_t ldb, const std::uint8_t* Cin, std::int64_t ldc,
-            std::uint8_t* D, std::int64_t ldd, std::uint8_t* scratch, cudaStream_t s);
+            std::uint8_t* D, std::int64_t ldd, std::uint8_t* scratch, cudaStream_t s,
+            const std::uint8_t* bt_packed = nullptr);
+// The B operand's packing on its own (transposed E2M1 codes, mad_f4_bt_bytes
+// bytes, 16-byte aligned): a B that several contractions share is packed
+// once and handed to mad_f4 as bt_packed (jobs.cpp, ImmutableB).
+std::int64_t mad_f4_bt_bytes(std::int64_t n, std::int64_t k);
+void pack_b_f4(std::uint32_t p, std::int64_t n, std::int64_t k, const std::uint8_t* B, std::int64_t ldb,
+               std::uint8_t* bt, cudaStream_t s);
 
 // ---------------------------------------------------------------- accounting
 // Every kernel launch of this library bumps a counter (bench.py's
