@@ -10,6 +10,35 @@ import re
 import sys
 
 
+def short_name(full):
+    """`void ns::kern<ns::Cfg<1, 2>, 3>(args)` -> `kern<ns::Cfg<1, 2>, 3>`: cut the
+    argument list at the first '(' outside template brackets (not the one in
+    `(anonymous namespace)` / `<unnamed>`), then the leading namespaces."""
+    # ncu prints names from an anonymous namespace as `unnamed>::kern(...)`
+    full = full.replace("(anonymous namespace)::", "").replace("<unnamed>::", "").replace("unnamed>::", "")
+    depth = 0
+    end = len(full)
+    for i, ch in enumerate(full):
+        if ch == "<":
+            depth += 1
+        elif ch == ">":
+            depth -= 1
+        elif ch == "(" and depth == 0:
+            end = i
+            break
+    name = re.sub(r"^void\s+", "", full[:end].strip())
+    depth = 0
+    start = 0
+    for i, ch in enumerate(name):
+        if ch == "<":
+            depth += 1
+        elif ch == ">":
+            depth -= 1
+        elif ch == ":" and depth == 0:
+            start = i + 1
+    return name[start:]
+
+
 def load(path):
     lines = open(path).read().splitlines()
     start = next(i for i, l in enumerate(lines) if l.startswith('"ID"'))
@@ -18,8 +47,7 @@ def load(path):
     for r in rows:
         if r.get("Metric Name") != "gpu__time_duration.sum":
             continue
-        name = r["Kernel Name"]
-        name = re.sub(r"\(.*", "", name.split("::")[-1])
+        name = short_name(r["Kernel Name"])
         v = float(r["Metric Value"].replace(",", ""))
         unit = r["Metric Unit"]
         v = v / 1e3 if unit in ("ns", "nsecond") else v * 1e3 if unit in ("ms", "msecond") else v
