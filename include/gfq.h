@@ -253,8 +253,11 @@ int gfq_echelonize_host_into(uint32_t p, int64_t m, int64_t n, const uint8_t* C,
 /* Optional (off by default; GFQ_HOST_PACK=1 or gfq_set_host_pack(1)): GF(2)
  * host buffers cross PCIe packed 8:1 -- host threads pack C before its
  * upload and unpack the downloaded blocks into host_out.  Pays where host
- * memory bandwidth well exceeds PCIe's.  The bytes that crossed PCIe in the
- * calling thread's last gfq_echelonize_host / _host_into call: */
+ * memory bandwidth well exceeds PCIe's.  on = N >= 2 (GFQ_HOST_PACK=N) is the
+ * hybrid: every N-th input block row and output block goes packed, the
+ * others as byte copies, so the host's packing runs beside the PCIe copies
+ * of the neighbours.  The bytes that crossed PCIe in the calling thread's
+ * last gfq_echelonize_host / _host_into call: */
 int gfq_set_host_pack(int on);
 int gfq_last_transfer_bytes(int64_t* h2d, int64_t* d2h);
 

@@ -170,7 +170,7 @@ int gfq_mat_upload32(int64_t rows, int64_t cols, const uint32_t* host, int64_t l
   });
 }
 int gfq_set_host_pack(int on) {
-  return guard([&] { gfq::hostpack::set_enabled(on != 0); });
+  return guard([&] { gfq::hostpack::set_stride(on); });
 }
 int gfq_last_transfer_bytes(int64_t* h2d, int64_t* d2h) {
   return guard([&] {

@@ -674,7 +674,7 @@ class EarlyDownload {
                           ev);
       }
       waited = true;
-      if (packed_) {
+      if (packed_ && hostpack::packs(n_issued_++)) {
         const std::int64_t ldb = std::int64_t((bk.cols + 63) / 64 * 8);
         const std::int64_t rows = std::int64_t(bk.rows), cols = std::int64_t(bk.cols);
         dev::pack_bits(m.data(), m.ld(), rows, cols, dstage_->ptr + bk.poff, ldb, stream_);
@@ -707,6 +707,7 @@ class EarlyDownload {
   std::uint8_t* host_;
   std::uint64_t cap_;
   bool packed_;
+  std::size_t n_issued_ = 0;  // blocks issued so far (hybrid: every N-th goes packed)
   std::unique_ptr<DevBuf> dstage_;
   std::unique_ptr<hostpack::PinnedLease> hstage_;
   std::vector<std::unique_ptr<Unpack>> jobs_;
@@ -802,6 +803,7 @@ EchelonOutput echelonize_host(const std::uint8_t* host, std::int64_t m, std::int
         packed_rows.push_back(std::make_unique<hostpack::Latch>((nr + chunk - 1) / chunk));
       }
       for (std::size_t i = 0; i < cs.a(); ++i) {
+        if (!hostpack::packs(i)) continue;
         const std::int64_t r0 = std::int64_t(cs.row_offset(i)), nr = std::int64_t(cs.row_parts[i]);
         hostpack::Latch* l = packed_rows[i].get();
         std::uint8_t* st = stage->data();
@@ -813,13 +815,16 @@ EchelonOutput echelonize_host(const std::uint8_t* host, std::int64_t m, std::int
           });
         }
       }
-      hostpack::last_transfer().h2d = m * ldb;
+      std::int64_t bytes = 0;
+      for (std::size_t i = 0; i < cs.a(); ++i)
+        bytes += std::int64_t(cs.row_parts[i]) * (hostpack::packs(i) ? ldb : n);
+      hostpack::last_transfer().h2d = bytes;
     } else {
       hostpack::last_transfer().h2d = m * n;
     }
     for (std::size_t i = 0; i < cs.a(); ++i) {
       const std::int64_t r0 = std::int64_t(cs.row_offset(i)), nr = std::int64_t(cs.row_parts[i]);
-      if (packed) {
+      if (packed && hostpack::packs(i)) {
         GFQ_CUDA(cudaLaunchHostFunc(
             cs_stream, [](void* p) { static_cast<hostpack::Latch*>(p)->wait(); }, packed_rows[i].get()));
         GFQ_CUDA(cudaMemcpyAsync(dpk->ptr + r0 * ldb, stage->data() + r0 * ldb, std::size_t(nr * ldb),
@@ -868,7 +873,8 @@ EchelonOutput echelonize_host(const std::uint8_t* host, std::int64_t m, std::int
     if (e2e_debug()) std::fprintf(stderr, "e2e host: return at %.2f ms\n", hms());
     return out;
   } catch (...) {
-    for (auto& l : packed_rows) l->wait();
+    for (std::size_t i = 0; i < packed_rows.size(); ++i)
+      if (hostpack::packs(i)) packed_rows[i]->wait();
     cudaStreamSynchronize(cs_stream);
     cudaStreamDestroy(cs_stream);
     throw;

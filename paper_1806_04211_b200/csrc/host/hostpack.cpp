@@ -19,11 +19,18 @@ namespace gfq::hostpack {
 namespace {
 std::atomic<int> g_enabled{[] {
   const char* e = std::getenv("GFQ_HOST_PACK");
-  return e && e[0] == '1' ? 1 : 0;
+  const int v = e ? std::atoi(e) : 0;
+  return v >= 0 && v <= 64 ? v : 0;
 }()};
 }  // namespace
 bool enabled() { return g_enabled.load() != 0; }
 void set_enabled(bool on) { g_enabled.store(on ? 1 : 0); }
+int stride() { return g_enabled.load(); }
+void set_stride(int n) { g_enabled.store(n >= 0 && n <= 64 ? n : 0); }
+bool packs(std::size_t index) {
+  const int n = g_enabled.load();
+  return n > 0 && index % std::size_t(n) == std::size_t(n - 1);
+}
 
 namespace {
 

@@ -22,6 +22,15 @@ namespace gfq::hostpack {
 // 245 ms).
 bool enabled();
 void set_enabled(bool on);
+// Hybrid transfers (GFQ_HOST_PACK=N / gfq_set_host_pack(N), N >= 2): only
+// every N-th input block row and every N-th output block goes packed, the
+// others as plain byte copies -- the pool's packing / unpacking of one piece
+// then runs while the copy engine moves its neighbours, so the host's memory
+// bandwidth and PCIe add up instead of replacing one another.  N = 1 packs
+// everything; packs(i) says whether piece i is a packed one.
+int stride();
+void set_stride(int n);
+bool packs(std::size_t index);
 
 void pack_rows(const std::uint8_t* src, std::int64_t ld, std::int64_t rows, std::int64_t cols, std::uint8_t* dst,
                std::int64_t ldb);

@@ -1056,9 +1056,11 @@ def profile_take_kinds(with_union: bool = False):
     return {name: (l[q], w[q], t[q]) for q, name in enumerate(PROFILE_KINDS)}
 
 
-def set_host_pack(on: bool):
-    """GF(2) host buffers cross PCIe packed 8:1 (off by default)."""
-    _check(lib().gfq_set_host_pack(1 if on else 0))
+def set_host_pack(on):
+    """GF(2) host buffers cross PCIe packed 8:1 (off by default).  An int
+    N >= 2 selects the hybrid: every N-th block row / output block packed,
+    the rest as byte copies (host packing and PCIe run side by side)."""
+    _check(lib().gfq_set_host_pack(int(on)))
 
 
 def last_transfer_bytes():

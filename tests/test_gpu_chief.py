@@ -366,6 +366,32 @@ def test_gf2_host_buffers_cross_pcie_packed(G, host_pack, m, n, block):
     assert 0 < d2h <= want.size // 8 + 8 * 64 * 64 and d2h < want.size
 
 
+@pytest.mark.parametrize("stride", [2, 3])
+@pytest.mark.parametrize("m,n,block", [(333, 517, 100), (517, 333, 64)])
+def test_gf2_host_buffers_hybrid_packing(G, stride, m, n, block):
+    """Hybrid transfers (gfq_set_host_pack(N >= 2)): every N-th block row and
+    output block packed, the rest as bytes -- same outputs, PCIe bytes between
+    the all-packed and the all-bytes counts."""
+    f = G.FieldSpec(2)
+    C = oracle.random_matrix(2, m, n, 13)
+    opts = G.EchelonizeOptions(block=block, threads=3, with_transform=True)
+    dev = G.echelonize(G.Matrix.from_numpy(C), f, opts)
+    want = np.zeros(dev.block_bytes(), np.uint8)
+    dev.download_blocks(want)
+    buf = np.full(dev.block_bytes() + 5, 0xCD, np.uint8)
+    G.set_host_pack(stride)
+    try:
+        out = G.echelonize(C, f, opts, host_out=buf)
+        h2d, d2h = G.last_transfer_bytes()
+    finally:
+        G.set_host_pack(False)
+    assert out.rank == dev.rank
+    np.testing.assert_array_equal(buf[: want.size], want)
+    assert (buf[want.size:] == 0xCD).all()
+    assert m * ((n + 63) // 64 * 8) < h2d < m * n
+    assert d2h < want.size
+
+
 def test_host_buffers_cross_pcie_as_bytes_by_default(G):
     C = oracle.random_matrix(2, 200, 300, 12)
     G.echelonize(C, G.FieldSpec(2), G.EchelonizeOptions(block=64))
