@@ -239,6 +239,12 @@ PlanHandles build_plan_fused(TaskGraph& graph, const Mat& C, const FieldSpec& fi
   if (std::int64_t(cs.rows()) != C.rows() || std::int64_t(cs.cols()) != C.cols())
     throw std::invalid_argument("build_plan: partition does not match matrix");
   graph.set_field(field);
+  {
+    // the widest a T_M(j, .) panel gets: every row block's part, 16-aligned
+    std::int64_t cap = 0;
+    for (std::size_t h = 0; h < a; ++h) cap += (std::int64_t(cs.row_parts[h]) + 15) / 16 * 16;
+    graph.set_trafo_capacity(cap);
+  }
   Emitter e{graph};
   using K = PkgKind;
   using T = TaskKind;

@@ -714,6 +714,22 @@ Mat Mat::view_of(std::shared_ptr<DevBuf> buf, std::size_t offset, std::int64_t r
   return v;
 }
 
+Mat Mat::with_capacity(std::int64_t rows, std::int64_t cols, std::int64_t cap_cols, int esize) {
+  if (cap_cols <= cols || rows <= 0 || cols <= 0) return Mat(rows, cols, esize);
+  Mat full(rows, cap_cols, esize);
+  return full.col_view(0, cols);
+}
+
+Mat Mat::widened(std::int64_t cols) const {
+  if (cols < cols_ || !buf_ || !data_ || rows_ <= 0) return Mat();
+  const std::int64_t in_row = std::int64_t(data_ - buf_->ptr) % ld_;
+  if (in_row + cols * esize_ > ld_) return Mat();
+  if (std::size_t(data_ - buf_->ptr) + std::size_t((rows_ - 1) * ld_ + cols * esize_) > buf_->bytes) return Mat();
+  Mat v = *this;
+  v.cols_ = cols;
+  return v;
+}
+
 Mat Mat::row_view(std::int64_t r0, std::int64_t n) const {
   if (r0 < 0 || n < 0 || r0 + n > rows_) throw std::invalid_argument("matrix: row view out of range");
   Mat v;

@@ -19,12 +19,15 @@ std::pair<Mat, Mat> update_row(const FieldSpec& f, const PkgA& A, const Mat& C,
 /// K(i, h, j-1) panel (j > 0); Mw: M(j, h, i-1-h) for h < i-1 as a panel
 /// (i >= 2), Md: M(j, i-1, 0); deltas[h] = E(h, j).delta.  Returns the
 /// K(i, h, j) and M(j, h, i-h) panels in the padded layout of the widths
-/// |delta_h|.
+/// |delta_h|.  m_capacity > 0: new M panels get a row stride of that many
+/// columns, and a block row that adds no pivot appends Md to Mw's storage in
+/// place (the returned panel is then a wider view of Mw's).
 std::pair<MatParts, MatParts> update_row_trafo_off(const FieldSpec& f, const PkgA& A,
                                                    const MatParts* Kw, const MatParts* Mw,
                                                    const Mat& Md,
                                                    const std::vector<const BitString*>& deltas,
-                                                   std::size_t i, std::size_t j);
+                                                   std::size_t i, std::size_t j,
+                                                   std::int64_t m_capacity = 0);
 
 std::pair<Mat, Mat> update_row_trafo(const FieldSpec& f, const PkgA& A,
                                      const std::optional<Mat>& K,

@@ -141,6 +141,13 @@ class Mat {
   /// broadcast payload): rows x cols at byte `offset`, row stride ld.
   static Mat view_of(std::shared_ptr<DevBuf> buf, std::size_t offset, std::int64_t rows,
                      std::int64_t cols, std::int64_t ld, int esize = 1);
+  /// Uninitialised rows x cols whose row stride has room for cap_cols
+  /// columns: `widened` can later append columns in place.
+  static Mat with_capacity(std::int64_t rows, std::int64_t cols, std::int64_t cap_cols, int esize = 1);
+  /// The same rows with `cols` >= cols() columns, the new ones being the
+  /// storage to the right of this view -- an empty Mat when the row stride
+  /// has no room for them.  The new columns are uninitialised.
+  Mat widened(std::int64_t cols) const;
   /// Rows [r0, r0+n) as a view (no copy).
   Mat row_view(std::int64_t r0, std::int64_t n) const;
   /// Columns [c0, c0+n) as a view (no copy; may lose 16-byte alignment).
