@@ -381,8 +381,29 @@ PlanHandles build_plan_fused(TaskGraph& graph, const Mat& C, const FieldSpec& fi
                 e.slot(K::E, h, 0, 0, j), e.slot(K::E, h, 0, 0, b - 1)},
                {e.slot(K::M, j, h, 0, a - h)});
       }
+  // GFQ_RL_SPLIT=0: one RowLengthen per row after the last ClearDown (A/B)
+  static const bool rl_split = [] {
+    const char* v = std::getenv("GFQ_RL_SPLIT");
+    return !(v && v[0] == '0');
+  }();
   if (with_transform && !rl_narrow)
     for (std::size_t j = 0; j < b; ++j) {
+      if (rl_split && a > 1) {
+        // two halves (scheduler.cpp RowLengthen c0 = -3 / -4): parts h < a-1
+        // need nothing from block row a-1, so for j < b-1 they are widened
+        // while the last diagonal ClearDown still runs; part a-1 is appended
+        // in place once E(a-1, b-1) exists
+        std::vector<std::int32_t> in1{e.slot(K::MT, j, 0, 0, a - 1)};
+        for (std::size_t h = 0; h + 1 < a; ++h) in1.push_back(e.slot(K::E, h, 0, 0, j));
+        for (std::size_t h = 0; h + 1 < a; ++h) in1.push_back(e.slot(K::E, h, 0, 0, b - 1));
+        const std::int32_t half = e.slot(K::MW, j, b + 1, 0, 0);
+        e.node(T::RowLengthen, -3, std::int32_t(j), -1, plate(a + b - 1), in1, {half});
+        e.node(T::RowLengthen, -4, std::int32_t(j), -1, plate(a + b - 1),
+               {half, e.slot(K::M, j, a - 1, 0, 0), e.slot(K::E, a - 1, 0, 0, j),
+                e.slot(K::E, a - 1, 0, 0, b - 1)},
+               {e.slot(K::MW, j, b, 0, 0)});
+        continue;
+      }
       std::vector<std::int32_t> in;
       if (a > 1) in.push_back(e.slot(K::MT, j, 0, 0, a - 1));
       in.push_back(e.slot(K::M, j, a - 1, 0, 0));

@@ -218,6 +218,18 @@ Mat mat_mul(const FieldSpec& f, const Mat& b, const Mat& c) {
   return mul_add_kernel(f, nullptr, b, c);
 }
 
+void col_gather_into(const Mat& dst, const Mat& a, const Mat* b, const std::vector<std::int32_t>* cmap) {
+  if (dst.empty()) return;
+  if (dst.esize() != 1 || a.esize() != 1 || (b && b->esize() != 1))
+    throw std::invalid_argument("col_gather_into: byte elements only");
+  if (a.rows() != dst.rows() || (b && b->rows() != dst.rows()) ||
+      (cmap ? std::int64_t(cmap->size()) != dst.cols() : a.cols() != dst.cols()))
+    throw std::invalid_argument("col_gather_into: shape mismatch");
+  auto cb = cmap ? upload_i32(*cmap) : nullptr;
+  dev::select2d(dst.data(), dst.ld(), dst.rows(), dst.cols(), a.data(), a.ld(), b ? b->data() : nullptr,
+                b ? b->ld() : 0, nullptr, dptr(cb), cur_stream());
+}
+
 Mat col_gather(const Mat& m, std::int64_t out_cols, const std::vector<std::int32_t>& cmap) {
   return select(m.rows(), out_cols, m, nullptr, nullptr, &cmap);
 }

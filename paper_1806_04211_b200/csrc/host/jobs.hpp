@@ -48,6 +48,9 @@ class ImmutableB {
 Mat col_gather(const Mat& m, std::int64_t out_cols, const std::vector<std::int32_t>& cmap);
 /// out[:, c] = a[:, cmap[c]] (>= 0), b[:, -cmap[c]-2] (<= -2) or 0 (-1); one K3 launch.
 Mat col_gather2(const Mat& a, const Mat* b, std::int64_t out_cols, const std::vector<std::int32_t>& cmap);
+/// The same gather (cmap null: a plain copy of a) into an existing matrix or
+/// view; u8 elements.
+void col_gather_into(const Mat& dst, const Mat& a, const Mat* b, const std::vector<std::int32_t>* cmap);
 
 /// Negative reduced echelonisation of one block (jobs.hpp:50).  Same
 /// recursion as the reference (split the longer dimension, combine), base

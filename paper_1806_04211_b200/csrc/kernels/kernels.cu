@@ -377,6 +377,14 @@ std::atomic<bool> g_partition{[] {
 }  // namespace
 void set_critical_partition(bool on) { g_partition = on; }
 bool critical_partition() { return g_partition; }
+namespace {
+// Steps 2-3 (the back substitution) run after the last ClearDown: no
+// critical path is left to keep SMs free for
+bool late_task() {
+  const char* t = hprof::t_task_name;
+  return std::strncmp(t, "ClearUp", 7) == 0 || std::strncmp(t, "PreClearUp", 10) == 0;
+}
+}  // namespace
 int k1_sms(cudaStream_t s) {
   static const int reserve = [] {
     const char* e = std::getenv("GFQ_K1_SM_RESERVE");
@@ -388,7 +396,8 @@ int k1_sms(cudaStream_t s) {
   }();
   if (stream_is_critical(s))
     return crit > 0 && std::strcmp(hprof::t_task_name, "ClearDown") == 0 ? std::min(crit, sm_count()) : sm_count();
-  if (reserve <= 0 || !g_partition) return sm_count();
+  static const bool late_reserve = std::getenv("GFQ_LATE_RESERVE") != nullptr;  // A/B
+  if (reserve <= 0 || !g_partition || (late_task() && !late_reserve)) return sm_count();
   return std::max(1, sm_count() - reserve);
 }
 // The K1 lane (GFQ_K1_LANE=1): persistent contractions issued from
@@ -406,7 +415,8 @@ K1Lane::K1Lane(cudaStream_t s) : s_(s) {
     const char* e = std::getenv("GFQ_K1_LANE");
     return !(e && e[0] == '0');
   }();
-  if (!on || !g_partition || stream_is_critical(s)) return;
+  static const bool late_lane = std::getenv("GFQ_LATE_LANE") != nullptr;  // A/B
+  if (!on || !g_partition || stream_is_critical(s) || (late_task() && !late_lane)) return;
   g_lane_mtx.lock();
   held_ = true;
   if (!g_lane_n) {
