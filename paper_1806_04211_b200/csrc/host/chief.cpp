@@ -381,10 +381,13 @@ PlanHandles build_plan_fused(TaskGraph& graph, const Mat& C, const FieldSpec& fi
                 e.slot(K::E, h, 0, 0, j), e.slot(K::E, h, 0, 0, b - 1)},
                {e.slot(K::M, j, h, 0, a - h)});
       }
-  // GFQ_RL_SPLIT=0: one RowLengthen per row after the last ClearDown (A/B)
-  static const bool rl_split = [] {
+  // GFQ_RL_SPLIT=1 (read per plan): RowLengthen in two halves, below.  Off by
+  // default: it lowers the HBM high-water (cfg5s 33.6 -> 29.9 GB) but not
+  // the step time -- the one-piece copy already hides behind
+  // UpdateRowTrafoW(a-1, b-1)
+  const bool rl_split = [] {
     const char* v = std::getenv("GFQ_RL_SPLIT");
-    return !(v && v[0] == '0');
+    return v && v[0] == '1';
   }();
   if (with_transform && !rl_narrow)
     for (std::size_t j = 0; j < b; ++j) {

@@ -392,6 +392,29 @@ def test_gf2_host_buffers_hybrid_packing(G, stride, m, n, block):
     assert d2h < want.size
 
 
+@pytest.mark.parametrize("p,m,n,block,rank", [(2, 700, 650, 128, 300), (7, 520, 600, 96, 0), (2, 512, 512, 64, 0)])
+def test_row_lengthen_in_two_halves(G, monkeypatch, p, m, n, block, rank):
+    """GFQ_RL_SPLIT=1 (chief.cpp / scheduler.cpp RowLengthen c0 = -3 / -4: parts
+    h < a-1 widened early into a full-stride panel, part a-1 appended in
+    place) gives byte-identical outputs to the one-piece RowLengthen."""
+    f = G.FieldSpec(p)
+    rng = np.random.default_rng(5)
+    if rank:
+        C = (rng.integers(0, p, (m, rank)) @ rng.integers(0, p, (rank, n)) % p).astype(np.uint8)
+    else:
+        C = oracle.random_matrix(p, m, n, 21)
+    opts = G.EchelonizeOptions(block=block, threads=3, with_transform=True)
+    outs = []
+    for split in ("0", "1"):
+        monkeypatch.setenv("GFQ_RL_SPLIT", split)
+        o = G.echelonize(G.Matrix.from_numpy(C), f, opts)
+        buf = np.zeros(o.block_bytes(), np.uint8)
+        o.download_blocks(buf)
+        outs.append((o.rank, buf))
+    assert outs[0][0] == outs[1][0]
+    np.testing.assert_array_equal(outs[0][1], outs[1][1])
+
+
 def test_host_buffers_cross_pcie_as_bytes_by_default(G):
     C = oracle.random_matrix(2, 200, 300, 12)
     G.echelonize(C, G.FieldSpec(2), G.EchelonizeOptions(block=64))
